@@ -1,0 +1,233 @@
+/*
+ * pump_gpu.h — C ABI of libpump_gpu.so, the B200 (sm_100a) data-parallel core
+ * of PUMP (arXiv 1607.06886).
+ *
+ * The reference library is header-only C++ (namespace pump) with no FFI of
+ * its own; its hot-path entry points are the C++ functions cited next to each
+ * declaration below.  This header is the thin C layer those C++ entry points
+ * sit on in this build: POD structs, caller-owned buffers, int status codes
+ * mapped 1:1 onto the reference's exception types (see pump_last_error()).
+ * include/pump/ headers re-expose the reference's C++ signatures on top of it;
+ * INTEGRATION.md shows the ctypes / C++ bindings.
+ *
+ * Conventions
+ *  - Matrices are dense, row-major, binary64.
+ *  - Every call is synchronous from the caller's view (stream-ordered inside).
+ *  - One pump_ctx per host thread; a ctx owns one CUDA device + stream and the
+ *    device-resident particle bank / graph buffers.
+ *  - No CPU fallback: if the CUDA runtime or an sm_100a device is missing the
+ *    call fails with PUMP_E_CUDA.
+ */
+#ifndef PUMP_GPU_H
+#define PUMP_GPU_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Status codes <-> reference exception types. */
+enum {
+  PUMP_OK = 0,
+  PUMP_E_INVALID_ARGUMENT = 1, /* std::invalid_argument   (lti.hpp:51, cp.hpp:217, graph.hpp:53, geom.hpp:191) */
+  PUMP_E_OUT_OF_RANGE = 2,     /* std::out_of_range       (cp.hpp:186-187) */
+  PUMP_E_RUNTIME = 3,          /* std::runtime_error      (geom.hpp:220, lti.hpp:130-171, sample.hpp:84) */
+  PUMP_E_SCENARIO = 4,         /* pump::ScenarioError     (scenario.hpp:18-20) */
+  PUMP_E_CUDA = 5,             /* device / driver failure (no reference analogue) */
+  PUMP_E_CAPACITY = 6,         /* caller buffer or device arena too small */
+  PUMP_E_LOGIC = 7             /* std::logic_error        (planner.hpp:303) */
+};
+
+/* Message of the last failing call on this thread ("" if none). */
+const char* pump_last_error(void);
+int pump_abi_version(void);
+
+/* ------------------------------------------------------------------ types */
+
+/* ClosedLoopDynamics (lti.hpp:181-190): z_{t+1} = F z + Gv (Sv nv) + Gw (Sw nw). */
+typedef struct pump_closed_loop {
+  int32_t d, dw;     /* state dim d = 2 dw for the double integrator */
+  const double* F;   /* 2d x 2d */
+  const double* Gv;  /* 2d x d  */
+  const double* Gw;  /* 2d x dw */
+  const double* Sv;  /* d x d   */
+  const double* Sw;  /* dw x dw */
+  const double* S0;  /* d x d   */
+  const double* C;   /* dw x d  */
+} pump_closed_loop;
+
+/* Workspace (geom.hpp:41-52): bounds minus a union of closed AABBs. */
+typedef struct pump_workspace {
+  int32_t dw, n_obs;
+  const double* bounds_lo; /* dw */
+  const double* bounds_hi; /* dw */
+  const double* obs_lo;    /* n_obs x dw */
+  const double* obs_hi;    /* n_obs x dw */
+} pump_workspace;
+
+/* GoalRegion (sample.hpp:22-29). */
+typedef struct pump_goal {
+  const double* lo; /* dw */
+  const double* hi; /* dw */
+  double max_speed;
+} pump_goal;
+
+/* Flat SampleGraph (graph.hpp:18-37): CSR rows in ascending neighbour order,
+ * per-edge Motion (tau, cost, acc0, jerk), per-waypoint ConvexRegion
+ * (waypoints 1..n_steps of each edge, graph.hpp:80-87) as half-space lists. */
+typedef struct pump_graph_view {
+  int32_t n_nodes, dw;
+  int64_t n_edges, n_waypoints, n_halfspaces;
+  int32_t n_goal;
+  double r_n, dt;
+  double* node_pos;      /* n_nodes x dw */
+  double* node_vel;      /* n_nodes x dw */
+  int64_t* row_ptr;      /* n_nodes + 1 */
+  int32_t* edge_to;      /* n_edges */
+  double* edge_cost;     /* n_edges */
+  double* edge_tau;      /* n_edges */
+  double* edge_acc0;     /* n_edges x dw */
+  double* edge_jerk;     /* n_edges x dw */
+  int32_t* edge_nsteps;  /* n_edges */
+  int64_t* edge_wp_off;  /* n_edges + 1  (edge e owns waypoints [off[e], off[e+1])) */
+  int64_t* wp_hs_off;    /* n_waypoints + 1 */
+  double* hs_a;          /* n_halfspaces x dw */
+  double* hs_b;          /* n_halfspaces */
+  uint8_t* hs_fallback;  /* n_halfspaces */
+  int32_t* goal_nodes;   /* n_goal, ascending */
+} pump_graph_view;
+
+/* ExploreParams (planner.hpp:26-32). */
+typedef struct pump_explore_params {
+  double alpha_min, alpha_max, lambda, r_n;
+} pump_explore_params;
+
+/* ExploreResult (planner.hpp:17-48) flattened. termination: 0 =
+ * "goal_below_alpha_min", 1 = "frontier_exhausted". */
+typedef struct pump_explore_view {
+  int64_t n_plans;
+  int32_t n_words, n_nodes;
+  int64_t n_pareto, n_goal_plans;
+  int64_t partial_plans, discarded_cp, removed_dominated, discarded_horizon;
+  int32_t rounds, termination;
+  int32_t* head;        /* n_plans */
+  int32_t* parent;      /* n_plans */
+  double* cost;         /* n_plans */
+  double* cp_hat;       /* n_plans */
+  int32_t* t_end;       /* n_plans */
+  uint64_t* masks;      /* n_plans x n_words (may be NULL on export) */
+  int64_t* pareto_ptr;  /* n_nodes + 1 */
+  int32_t* pareto_ids;  /* n_pareto (ascending ids per node) */
+  int32_t* goal_plans;  /* n_goal_plans */
+} pump_explore_view;
+
+/* PumpResult (pump.hpp:148-165) scalar part. */
+typedef struct pump_result_summary {
+  int32_t success, termination;
+  int32_t path_len, n_pareto, n_mc_evals, n_traj_points, dw;
+  int64_t partial_plans;
+  double cost, certified_cp, cp_hat, pre_smoothing_cost, smoothing_s;
+  double build_graph_seconds, explore_seconds, selection_seconds;
+  /* device-side breakdown (CUDA events), not in the reference report */
+  double bank_ms, explore_kernel_ms, mc_ms;
+  int64_t n_edges, n_plans, mc_rollouts;
+} pump_result_summary;
+
+typedef struct pump_ctx pump_ctx;
+typedef struct pump_graph pump_graph;
+typedef struct pump_explore pump_explore;
+typedef struct pump_result pump_result;
+typedef struct pump_scenario pump_scenario;
+
+/* ---------------------------------------------------------------- context */
+int pump_ctx_create(int device, pump_ctx** out);
+int pump_ctx_destroy(pump_ctx* ctx);
+/* CUDA-event time of the last kernel family launched by the ctx, ms. */
+double pump_ctx_last_kernel_ms(pump_ctx* ctx);
+/* Number of kernel launches issued by this ctx since creation. */
+int64_t pump_ctx_launch_count(pump_ctx* ctx);
+
+/* ------------------------------------------------------------- scenario */
+/* load_scenario / parse_scenario / build_models (scenario.hpp:144-301). */
+int pump_scenario_parse(const char* json_text, pump_scenario** out);
+int pump_scenario_load(const char* path, pump_scenario** out);
+int pump_scenario_free(pump_scenario* s);
+/* Closed-loop matrices of build_models(s).cl; buffers sized by d, dw
+ * (pass NULL buffers to query d, dw only). */
+int pump_scenario_closed_loop(const pump_scenario* s, int32_t* d, int32_t* dw, double* F, double* Gv, double* Gw,
+                              double* Sv, double* Sw, double* S0, double* C);
+/* JSON-scenario scalars: eps_cc, r_n, tau_max, alpha, eta, lambda, dt. */
+int pump_scenario_params(const pump_scenario* s, double out[8], int64_t iout[8]);
+
+/* ---------------------------------------------------- particle bank (K_bank) */
+/* presample_bank (lti.hpp:257-292).  The bank stays resident in the ctx;
+ * dy_out (nullable) receives (t_max+1) x n x dw doubles. */
+int pump_presample_bank(pump_ctx* ctx, const pump_closed_loop* cl, int32_t t_max, int32_t n, uint64_t seed,
+                        double* dy_out);
+/* Replace the ctx bank by a caller-provided one (hand-built banks). */
+int pump_bank_upload(pump_ctx* ctx, int32_t n, int32_t horizon, int32_t dw, const double* dy);
+
+/* ------------------------------------------------------ HSMC (K_hsmc) */
+/* Batched hsmc_extend (cp.hpp:180-208) against the ctx bank.  Task i extends
+ * masks_in[i*n_words..] along steps [step_off[i], step_off[i+1]); step s
+ * checks bank row step_t[s] against half-spaces [step_hs_off[s],
+ * step_hs_off[s+1]) of (hs_a, hs_b).  A step with an empty list is the
+ * reference's null/empty region.  Out: masks_out, popcounts; cp = 1 -
+ * popcount/n.  Returns PUMP_E_OUT_OF_RANGE if any step_t is outside
+ * [0, horizon] (checked before the empty-region skip, as cp.hpp:186-188). */
+int pump_hsmc_extend_batch(pump_ctx* ctx, int64_t n_tasks, int32_t n_words, const uint64_t* masks_in,
+                           const int64_t* step_off, const int32_t* step_t, const int64_t* step_hs_off,
+                           const double* hs_a, const double* hs_b, uint64_t* masks_out, int32_t* popcount_out);
+
+/* ----------------------------------------------- MC certification (K_mc) */
+/* Batched mc_certify (cp.hpp:214-268): trajectory j = y_nom rows
+ * [traj_off[j], traj_off[j+1]) (dw doubles each).  Rollouts
+ * [rollout_lo, rollout_hi) of n_mc are simulated for every trajectory (the
+ * multi-GPU shard); hits_out[j] = number of colliding rollouts in the range.
+ * value = hits / n_mc once summed over shards (bit-identical for any split). */
+int pump_mc_certify_batch(pump_ctx* ctx, const pump_closed_loop* cl, const pump_workspace* ws, int32_t n_traj,
+                          const int64_t* traj_off, const double* y_nom, int64_t rollout_lo, int64_t rollout_hi,
+                          uint64_t seed, double eps_cc, int64_t* hits_out);
+/* Single-trajectory convenience with the reference's signature semantics;
+ * value_out = n_hit / n_mc. */
+int pump_mc_certify(pump_ctx* ctx, const pump_closed_loop* cl, const pump_workspace* ws, int32_t n_points,
+                    const double* y_nom, int32_t n_mc, uint64_t seed, double eps_cc, double* value_out);
+
+/* ------------------------------------------------ graph build (K_graph) */
+/* build_graph (graph.hpp:50-95) for nodes (pos, vel: n x dw). tau_ratio is
+ * pow(tau_max / (tau_max*1e-7), 1/63), pass <= 0 to let the library compute
+ * it with the host libm exactly as steer.hpp:133 does. */
+int pump_build_graph(pump_ctx* ctx, int32_t n_nodes, int32_t dw, const double* pos, const double* vel,
+                     const pump_workspace* ws, const pump_goal* goal, double r_n, double dt, double eps_cc,
+                     double tau_max, pump_graph** out);
+/* Upload a prebuilt graph (pump.hpp:170 "prebuilt"). Reads every field. */
+int pump_graph_upload(pump_ctx* ctx, const pump_graph_view* view, pump_graph** out);
+/* Sizes into view (pointers untouched); then export into caller buffers
+ * (any NULL pointer is skipped). */
+int pump_graph_counts(const pump_graph* g, pump_graph_view* view);
+int pump_graph_export(const pump_graph* g, pump_graph_view* view);
+int pump_graph_free(pump_graph* g);
+
+/* ----------------------------------------------------- explore (K_hsmc..) */
+/* explore (planner.hpp:74-267) on the ctx bank; wavefront on one GPU. */
+int pump_explore_run(pump_ctx* ctx, const pump_graph* g, const pump_explore_params* p, pump_explore** out);
+int pump_explore_counts(const pump_explore* e, pump_explore_view* view);
+int pump_explore_export(const pump_explore* e, pump_explore_view* view);
+int pump_explore_free(pump_explore* e);
+
+/* ------------------------------------------------------ full pipeline */
+/* run_pump (pump.hpp:170-263). prebuilt may be NULL. */
+int pump_run(pump_ctx* ctx, const pump_scenario* s, const pump_graph* prebuilt, pump_result** out);
+int pump_result_summary_get(const pump_result* r, pump_result_summary* out);
+/* Caller buffers sized from the summary counts (NULL to skip). */
+int pump_result_arrays(const pump_result* r, int32_t* path, double* pareto_cost, double* pareto_cp,
+                       int32_t* mc_eval_ids, double* mc_eval_values, double* traj_t, double* traj_pos,
+                       double* traj_vel, double* traj_ctrl);
+int pump_result_free(pump_result* r);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* PUMP_GPU_H */

@@ -1,0 +1,318 @@
+"""Python mirror of the reference ``pump`` API over ``libpump_gpu.so``.
+
+Names and argument meanings follow the reference headers
+(/root/reference/proj/include/pump/*.hpp): ``presample_bank`` (lti.hpp:257),
+``hsmc_extend`` (cp.hpp:180), ``mc_certify`` (cp.hpp:214), ``build_graph``
+(graph.hpp:50), ``explore`` (planner.hpp:74), ``run_pump`` (pump.hpp:170),
+``load_scenario`` / ``parse_scenario`` (scenario.hpp:144-269).  Errors map to
+the reference's exception types: ``ValueError`` <- std::invalid_argument,
+``IndexError`` <- std::out_of_range, ``ScenarioError`` <- pump::ScenarioError,
+``RuntimeError`` <- std::runtime_error.
+
+Every call runs on the GPU through the C ABI; there is no CPU fallback: if
+the library or a B200 is missing, calls raise ``PumpCudaError``.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import json as _json
+import os
+
+import numpy as np
+
+from . import _abi as A
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libpump_gpu.so")
+
+_lib = None
+
+
+class PumpError(RuntimeError):
+    pass
+
+
+class ScenarioError(PumpError):
+    pass
+
+
+class PumpCudaError(PumpError):
+    pass
+
+
+class CapacityError(PumpError):
+    pass
+
+
+class LibraryMissing(ImportError):
+    pass
+
+
+_EXC = {A.PUMP_E_INVALID_ARGUMENT: ValueError, A.PUMP_E_OUT_OF_RANGE: IndexError,
+        A.PUMP_E_RUNTIME: RuntimeError, A.PUMP_E_SCENARIO: ScenarioError, A.PUMP_E_CUDA: PumpCudaError,
+        A.PUMP_E_CAPACITY: CapacityError, A.PUMP_E_LOGIC: RuntimeError}
+
+# every symbol include/pump_gpu.h declares (checked by tests/test_abi.py)
+EXPORTS = [
+    "pump_last_error", "pump_abi_version", "pump_ctx_create", "pump_ctx_destroy", "pump_ctx_last_kernel_ms",
+    "pump_ctx_launch_count", "pump_scenario_parse", "pump_scenario_load", "pump_scenario_free",
+    "pump_scenario_closed_loop", "pump_scenario_params", "pump_presample_bank", "pump_bank_upload",
+    "pump_hsmc_extend_batch", "pump_mc_certify_batch", "pump_mc_certify", "pump_build_graph", "pump_graph_upload",
+    "pump_graph_counts", "pump_graph_export", "pump_graph_free", "pump_explore_run", "pump_explore_counts",
+    "pump_explore_export", "pump_explore_free", "pump_run", "pump_result_summary_get", "pump_result_arrays",
+    "pump_result_free",
+]
+
+
+def lib():
+    """Load libpump_gpu.so (raises LibraryMissing loudly if it was not built)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise LibraryMissing(f"{LIB_PATH} not built: run `python -c 'import __graft_entry__ as g; g.build()'` "
+                                 "(there is no CPU fallback)")
+        L = C.CDLL(LIB_PATH)
+        vp = C.c_void_p
+        L.pump_last_error.restype = C.c_char_p
+        L.pump_ctx_last_kernel_ms.restype = C.c_double
+        L.pump_ctx_last_kernel_ms.argtypes = [vp]
+        L.pump_ctx_launch_count.restype = C.c_int64
+        L.pump_ctx_launch_count.argtypes = [vp]
+        L.pump_ctx_create.argtypes = [C.c_int, vp]
+        L.pump_ctx_destroy.argtypes = [vp]
+        L.pump_scenario_parse.argtypes = [C.c_char_p, vp]
+        L.pump_scenario_load.argtypes = [C.c_char_p, vp]
+        L.pump_scenario_free.argtypes = [vp]
+        L.pump_scenario_closed_loop.argtypes = [vp] * 10
+        L.pump_scenario_params.argtypes = [vp, vp, vp]
+        L.pump_presample_bank.argtypes = [vp, vp, C.c_int32, C.c_int32, C.c_uint64, vp]
+        L.pump_bank_upload.argtypes = [vp, C.c_int32, C.c_int32, C.c_int32, vp]
+        L.pump_hsmc_extend_batch.argtypes = [vp, C.c_int64, C.c_int32, vp, vp, vp, vp, vp, vp, vp, vp]
+        L.pump_mc_certify_batch.argtypes = [vp, vp, vp, C.c_int32, vp, vp, C.c_int64, C.c_int64, C.c_uint64,
+                                            C.c_double, vp]
+        L.pump_mc_certify.argtypes = [vp, vp, vp, C.c_int32, vp, C.c_int32, C.c_uint64, C.c_double, vp]
+        if hasattr(L, "pump_build_graph"):
+            L.pump_build_graph.argtypes = [vp, C.c_int32, C.c_int32, vp, vp, vp, vp, C.c_double, C.c_double,
+                                           C.c_double, C.c_double, vp]
+            L.pump_graph_upload.argtypes = [vp, vp, vp]
+            L.pump_graph_counts.argtypes = [vp, vp]
+            L.pump_graph_export.argtypes = [vp, vp]
+            L.pump_graph_free.argtypes = [vp]
+            L.pump_explore_run.argtypes = [vp, vp, vp, vp]
+            L.pump_explore_counts.argtypes = [vp, vp]
+            L.pump_explore_export.argtypes = [vp, vp]
+            L.pump_explore_free.argtypes = [vp]
+            L.pump_run.argtypes = [vp, vp, vp, vp]
+            L.pump_result_summary_get.argtypes = [vp, vp]
+            L.pump_result_arrays.argtypes = [vp] * 10
+            L.pump_result_free.argtypes = [vp]
+        _lib = L
+    return _lib
+
+
+def _check(rc):
+    if rc != 0:
+        msg = lib().pump_last_error().decode()
+        exc = _EXC.get(rc, PumpError)
+        e = exc(msg)
+        e.code = rc
+        raise e
+
+
+def _p(a):
+    return a.ctypes.data_as(C.c_void_p) if a is not None else None
+
+
+# ------------------------------------------------------------------ context
+class Context:
+    """One CUDA device + stream + resident bank (``pump_ctx``)."""
+
+    def __init__(self, device: int = 0):
+        h = C.c_void_p()
+        _check(lib().pump_ctx_create(device, C.byref(h)))
+        self.h = h
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib().pump_ctx_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @property
+    def last_kernel_ms(self) -> float:
+        return lib().pump_ctx_last_kernel_ms(self.h)
+
+    @property
+    def launches(self) -> int:
+        return lib().pump_ctx_launch_count(self.h)
+
+
+_default_ctx = None
+
+
+def default_context() -> Context:
+    global _default_ctx
+    if _default_ctx is None:
+        _default_ctx = Context(int(os.environ.get("LOCAL_RANK", "0")))
+    return _default_ctx
+
+
+# ----------------------------------------------------------------- scenario
+class Scenario:
+    """Parsed scenario (scenario.hpp:34-77) held by the library."""
+
+    def __init__(self, handle, text: str | None):
+        self.h = handle
+        self.text = text
+
+    @staticmethod
+    def parse(text: str) -> "Scenario":
+        h = C.c_void_p()
+        _check(lib().pump_scenario_parse(text.encode(), C.byref(h)))
+        return Scenario(h, text)
+
+    @staticmethod
+    def load(path: str) -> "Scenario":
+        h = C.c_void_p()
+        _check(lib().pump_scenario_load(path.encode(), C.byref(h)))
+        with open(path) as f:
+            text = f.read()
+        return Scenario(h, text)
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            lib().pump_scenario_free(self.h)
+            self.h = None
+
+    def closed_loop(self) -> dict:
+        d, dw = C.c_int32(), C.c_int32()
+        _check(lib().pump_scenario_closed_loop(self.h, C.byref(d), C.byref(dw), *([None] * 7)))
+        d, dw = d.value, dw.value
+        m = {"F": np.zeros((2 * d, 2 * d)), "Gv": np.zeros((2 * d, d)), "Gw": np.zeros((2 * d, dw)),
+             "Sv": np.zeros((d, d)), "Sw": np.zeros((dw, dw)), "S0": np.zeros((d, d)), "C": np.zeros((dw, d))}
+        _check(lib().pump_scenario_closed_loop(self.h, C.byref(C.c_int32()), C.byref(C.c_int32()),
+                                               *[_p(m[k]) for k in ("F", "Gv", "Gw", "Sv", "Sw", "S0", "C")]))
+        m["d"], m["dw"] = d, dw
+        return m
+
+    def params(self) -> dict:
+        f = np.zeros(8)
+        i = np.zeros(8, dtype=np.int64)
+        _check(lib().pump_scenario_params(self.h, _p(f), _p(i)))
+        keys_f = ["eps_cc", "r_n", "tau_max", "alpha", "eta", "lambda", "dt", "max_speed"]
+        keys_i = ["samples", "particles", "mc_samples", "bank_horizon", "seed_bank", "seed_mc", "seed_rrt", "dw"]
+        out = dict(zip(keys_f, f.tolist()))
+        out.update(dict(zip(keys_i, [int(x) for x in i])))
+        return out
+
+    def workspace(self) -> dict:
+        j = _json.loads(self.text)
+        ws = j["workspace"]
+        obs = ws.get("obstacles", [])
+        dw = len(ws["bounds"]["lo"])
+        return {"bounds_lo": np.array(ws["bounds"]["lo"], float), "bounds_hi": np.array(ws["bounds"]["hi"], float),
+                "obs_lo": np.array([o["lo"] for o in obs], float).reshape(-1, dw),
+                "obs_hi": np.array([o["hi"] for o in obs], float).reshape(-1, dw)}
+
+
+def parse_scenario(text: str) -> Scenario:
+    return Scenario.parse(text)
+
+
+def load_scenario(path: str) -> Scenario:
+    return Scenario.load(path)
+
+
+# --------------------------------------------------------------------- bank
+def presample_bank(cl: dict, t_max: int, n: int, seed: int, ctx: Context | None = None,
+                   copy_out: bool = True):
+    """presample_bank (lti.hpp:257-292) on the GPU; returns dy[(t_max+1), n, dw]
+    (the bank also stays resident in ``ctx`` for hsmc_extend / explore)."""
+    ctx = ctx or default_context()
+    keep = A.Keep()
+    s = A.closed_loop_struct(cl, keep)
+    out = np.zeros((t_max + 1, n, cl["dw"])) if copy_out else None
+    _check(lib().pump_presample_bank(ctx.h, C.byref(s), t_max, n, C.c_uint64(seed), _p(out)))
+    return out
+
+
+def bank_upload(dy: np.ndarray, ctx: Context | None = None):
+    ctx = ctx or default_context()
+    dy = np.ascontiguousarray(dy, dtype=np.float64)
+    _check(lib().pump_bank_upload(ctx.h, dy.shape[1], dy.shape[0] - 1, dy.shape[2], _p(dy)))
+
+
+# --------------------------------------------------------------------- hsmc
+def hsmc_extend_batch(masks_in, step_off, step_t, step_hs_off, hs_a, hs_b, ctx: Context | None = None):
+    """Batched hsmc_extend (cp.hpp:180-208) against the context's bank."""
+    ctx = ctx or default_context()
+    masks_in = np.ascontiguousarray(masks_in, dtype=np.uint64)
+    n_tasks, n_words = masks_in.shape
+    arrs = [np.ascontiguousarray(step_off, dtype=np.int64), np.ascontiguousarray(step_t, dtype=np.int32),
+            np.ascontiguousarray(step_hs_off, dtype=np.int64),
+            np.ascontiguousarray(hs_a, dtype=np.float64).reshape(-1), np.ascontiguousarray(hs_b, dtype=np.float64)]
+    arrs = [a if a.size else np.zeros(1, a.dtype) for a in arrs]
+    out = np.zeros_like(masks_in)
+    pop = np.zeros(n_tasks, dtype=np.int32)
+    _check(lib().pump_hsmc_extend_batch(ctx.h, n_tasks, n_words, _p(masks_in), *[_p(a) for a in arrs], _p(out),
+                                        _p(pop)))
+    return out, pop
+
+
+def full_mask(n: int) -> np.ndarray:
+    """ParticleMask::full (cp.hpp:24-31)."""
+    w = np.full((n + 63) // 64, np.uint64(0xFFFFFFFFFFFFFFFF), dtype=np.uint64)
+    if n % 64:
+        w[-1] = np.uint64((1 << (n % 64)) - 1)
+    return w
+
+
+def hsmc_extend(mask: np.ndarray, steps, n_particles: int, ctx: Context | None = None):
+    """Single hsmc_extend with the reference's signature semantics.  steps is a
+    list of (t, region) with region a list of (a, b) half-spaces or None.
+    Returns (mask', cp)."""
+    step_t, hs_off, a_rows, b_rows = [], [0], [], []
+    for t, region in steps:
+        step_t.append(t)
+        for a, b in (region or []):
+            a_rows.append(np.asarray(a, float))
+            b_rows.append(float(b))
+        hs_off.append(len(b_rows))
+    dw = a_rows[0].size if a_rows else 1
+    out, pop = hsmc_extend_batch(np.asarray(mask, np.uint64)[None, :], [0, len(steps)], step_t, hs_off,
+                                 np.array(a_rows).reshape(-1, dw) if a_rows else np.zeros((0, dw)),
+                                 np.array(b_rows), ctx)
+    return out[0], 1.0 - float(pop[0]) / n_particles
+
+
+# ----------------------------------------------------------------------- mc
+def mc_certify_batch(cl: dict, ws: dict, trajectories, rollout_lo: int, rollout_hi: int, seed: int,
+                     eps_cc: float, ctx: Context | None = None) -> np.ndarray:
+    """Colliding-rollout counts of rollouts [lo, hi) for every trajectory."""
+    ctx = ctx or default_context()
+    keep = A.Keep()
+    cls = A.closed_loop_struct(cl, keep)
+    wss = A.workspace_struct(ws, keep)
+    dw = cl["dw"]
+    ys = [np.asarray(t, float).reshape(-1, dw) for t in trajectories]
+    off = np.zeros(len(ys) + 1, dtype=np.int64)
+    off[1:] = np.cumsum([y.shape[0] for y in ys])
+    y = np.ascontiguousarray(np.concatenate(ys, axis=0) if ys else np.zeros((1, dw)))
+    hits = np.zeros(len(ys), dtype=np.int64)
+    _check(lib().pump_mc_certify_batch(ctx.h, C.byref(cls), C.byref(wss), len(ys), _p(off), _p(y), rollout_lo,
+                                       rollout_hi, C.c_uint64(seed), eps_cc, _p(hits)))
+    return hits
+
+
+def mc_certify(y_nom, cl: dict, ws: dict, n_mc: int, seed: int, eps_cc: float, ctx: Context | None = None) -> float:
+    """mc_certify (cp.hpp:214-268): fraction of colliding rollouts."""
+    if n_mc < 1:
+        raise ValueError("mc_certify: need at least one rollout")
+    if len(y_nom) == 0:
+        raise ValueError("mc_certify: empty trajectory")
+    return float(mc_certify_batch(cl, ws, [y_nom], 0, n_mc, seed, eps_cc, ctx)[0]) / n_mc

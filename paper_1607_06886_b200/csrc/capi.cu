@@ -1,0 +1,297 @@
+// C ABI of libpump_gpu.so (include/pump_gpu.h): context, scenario, bank,
+// batched HSMC and batched MC certification.  Graph / explore / pipeline
+// entry points live in capi_plan.cu.
+#include <cstring>
+#include <string>
+
+#include "ctx.h"
+#include "guard.h"
+
+using namespace pumpg;
+
+namespace pumpg {
+
+HostLoop host_loop(const pump_closed_loop* cl) {
+  if (!cl) throw std::invalid_argument("closed loop: null");
+  HostLoop L;
+  L.d = cl->d;
+  L.dw = cl->dw;
+  const int d = cl->d, dw = cl->dw;
+  if (d < 1 || dw < 1 || d > 12 || dw > 6) throw std::invalid_argument("closed loop: bad dimensions");
+  L.F.assign(cl->F, cl->F + 4 * d * d);
+  L.Gv.assign(cl->Gv, cl->Gv + 2 * d * d);
+  L.Gw.assign(cl->Gw, cl->Gw + 2 * d * dw);
+  L.Sv.assign(cl->Sv, cl->Sv + d * d);
+  L.Sw.assign(cl->Sw, cl->Sw + dw * dw);
+  L.S0.assign(cl->S0, cl->S0 + d * d);
+  L.C.assign(cl->C, cl->C + dw * d);
+  return L;
+}
+
+DevWorld upload_world(Ctx& c, const pump_workspace* ws, const std::string& prefix) {
+  if (!ws) throw std::invalid_argument("workspace: null");
+  if (ws->dw < 1 || ws->dw > 6 || ws->n_obs < 0) throw std::invalid_argument("workspace: bad dimensions");
+  DevWorld w;
+  w.dw = ws->dw;
+  w.n_obs = ws->n_obs;
+  for (int k = 0; k < ws->dw; ++k) {
+    w.blo[k] = ws->bounds_lo[k];
+    w.bhi[k] = ws->bounds_hi[k];
+  }
+  const size_t bytes = static_cast<size_t>(ws->n_obs) * ws->dw * sizeof(double);
+  DBuf& lo = c.buf(prefix + "lo", bytes);
+  DBuf& hi = c.buf(prefix + "hi", bytes);
+  c.h2d(lo.p, ws->obs_lo, bytes);
+  c.h2d(hi.p, ws->obs_hi, bytes);
+  w.d_lo = lo.as<double>();
+  w.d_hi = hi.as<double>();
+  return w;
+}
+
+}  // namespace pumpg
+
+extern "C" {
+
+const char* pump_last_error(void) { return pumpg::last_error().c_str(); }
+int pump_abi_version(void) { return 1; }
+
+int pump_ctx_create(int device, pump_ctx** out) {
+  return guard([&] {
+    int n = 0;
+    PUMP_CUDA(cudaGetDeviceCount(&n));
+    if (device < 0 || device >= n) throw CudaError("pump_ctx_create: no such CUDA device");
+    cudaDeviceProp prop;
+    PUMP_CUDA(cudaGetDeviceProperties(&prop, device));
+    if (prop.major != 10) throw CudaError("pump_ctx_create: libpump_gpu.so is built for sm_100a (B200) only");
+    PUMP_CUDA(cudaSetDevice(device));
+    auto* x = new pump_ctx;
+    x->c.device = device;
+    PUMP_CUDA(cudaStreamCreateWithFlags(&x->c.stream, cudaStreamNonBlocking));
+    PUMP_CUDA(cudaEventCreate(&x->c.ev0));
+    PUMP_CUDA(cudaEventCreate(&x->c.ev1));
+    *out = x;
+  });
+}
+
+int pump_ctx_destroy(pump_ctx* ctx) {
+  return guard([&] {
+    if (!ctx) return;
+    cudaSetDevice(ctx->c.device);
+    cudaStreamSynchronize(ctx->c.stream);
+    ctx->c.scratch.clear();
+    ctx->c.bank.release();
+    cudaEventDestroy(ctx->c.ev0);
+    cudaEventDestroy(ctx->c.ev1);
+    cudaStreamDestroy(ctx->c.stream);
+    delete ctx;
+  });
+}
+
+double pump_ctx_last_kernel_ms(pump_ctx* ctx) { return ctx ? ctx->c.last_ms : 0.0; }
+int64_t pump_ctx_launch_count(pump_ctx* ctx) { return ctx ? ctx->c.launches : 0; }
+
+// ------------------------------------------------------------- scenario
+int pump_scenario_parse(const char* json_text, pump_scenario** out) {
+  return guard([&] {
+    auto* s = new pump_scenario;
+    try {
+      s->s = pumpb::parse_scenario_text(json_text ? json_text : "");
+    } catch (...) {
+      delete s;
+      throw;
+    }
+    *out = s;
+  });
+}
+
+int pump_scenario_load(const char* path, pump_scenario** out) {
+  return guard([&] {
+    auto* s = new pump_scenario;
+    try {
+      s->s = pumpb::load_scenario(path ? path : "");
+    } catch (...) {
+      delete s;
+      throw;
+    }
+    *out = s;
+  });
+}
+
+int pump_scenario_free(pump_scenario* s) {
+  delete s;
+  return PUMP_OK;
+}
+
+int pump_scenario_closed_loop(const pump_scenario* s, int32_t* d, int32_t* dw, double* F, double* Gv, double* Gw,
+                              double* Sv, double* Sw, double* S0, double* Cm) {
+  return guard([&] {
+    *dw = s->s.workspace_dim();
+    *d = 2 * *dw;
+    if (!F) return;
+    pumpb::ClosedLoop cl = s->s.models().cl;
+    std::memcpy(F, cl.F.a.data(), cl.F.a.size() * 8);
+    std::memcpy(Gv, cl.Gv.a.data(), cl.Gv.a.size() * 8);
+    std::memcpy(Gw, cl.Gw.a.data(), cl.Gw.a.size() * 8);
+    std::memcpy(Sv, cl.Sv.a.data(), cl.Sv.a.size() * 8);
+    std::memcpy(Sw, cl.Sw.a.data(), cl.Sw.a.size() * 8);
+    std::memcpy(S0, cl.S0.a.data(), cl.S0.a.size() * 8);
+    std::memcpy(Cm, cl.C.a.data(), cl.C.a.size() * 8);
+  });
+}
+
+int pump_scenario_params(const pump_scenario* s, double out[8], int64_t iout[8]) {
+  return guard([&] {
+    const auto& x = s->s;
+    out[0] = x.effective_eps_cc();
+    out[1] = x.effective_r_n();
+    out[2] = x.effective_tau_max();
+    out[3] = x.alpha;
+    out[4] = x.effective_eta();
+    out[5] = x.lambda;
+    out[6] = x.dt;
+    out[7] = x.max_speed;
+    iout[0] = x.samples;
+    iout[1] = x.particles;
+    iout[2] = x.mc_samples;
+    iout[3] = x.bank_horizon;
+    iout[4] = static_cast<int64_t>(x.seeds.bank);
+    iout[5] = static_cast<int64_t>(x.seeds.mc);
+    iout[6] = static_cast<int64_t>(x.seeds.rrt);
+    iout[7] = x.workspace_dim();
+  });
+}
+
+// ------------------------------------------------------------------ bank
+int pump_presample_bank(pump_ctx* ctx, const pump_closed_loop* cl, int32_t t_max, int32_t n, uint64_t seed,
+                        double* dy_out) {
+  return guard([&] {
+    Ctx& c = ctx->c;
+    HostLoop L = host_loop(cl);
+    if (n < 1) throw std::invalid_argument("presample_bank: need at least one particle");
+    if (t_max < 1) throw std::invalid_argument("presample_bank: horizon must be at least 1");
+    const size_t bytes = static_cast<size_t>(t_max + 1) * n * L.dw * sizeof(double);
+    c.bank.ensure(bytes);
+    DBuf& scr = c.buf("bank_scratch", bank_scratch_bytes(L, n, t_max));
+    c.tic();
+    launch_bank(L, n, t_max, seed, c.bank.as<double>(), scr.p, c.stream, &c.launches);
+    c.toc();
+    c.bank_n = n;
+    c.bank_horizon = t_max;
+    c.bank_dw = L.dw;
+    if (dy_out) {
+      c.d2h(dy_out, c.bank.p, bytes);
+      c.sync();
+    }
+  });
+}
+
+int pump_bank_upload(pump_ctx* ctx, int32_t n, int32_t horizon, int32_t dw, const double* dy) {
+  return guard([&] {
+    Ctx& c = ctx->c;
+    if (n < 1 || horizon < 0 || dw < 1) throw std::invalid_argument("bank_upload: bad dimensions");
+    const size_t bytes = static_cast<size_t>(horizon + 1) * n * dw * sizeof(double);
+    c.bank.ensure(bytes);
+    c.h2d(c.bank.p, dy, bytes);
+    c.sync();
+    c.bank_n = n;
+    c.bank_horizon = horizon;
+    c.bank_dw = dw;
+  });
+}
+
+// ------------------------------------------------------------------ hsmc
+int pump_hsmc_extend_batch(pump_ctx* ctx, int64_t n_tasks, int32_t n_words, const uint64_t* masks_in,
+                           const int64_t* step_off, const int32_t* step_t, const int64_t* step_hs_off,
+                           const double* hs_a, const double* hs_b, uint64_t* masks_out, int32_t* popcount_out) {
+  return guard([&] {
+    Ctx& c = ctx->c;
+    if (!c.bank.p) throw std::invalid_argument("hsmc_extend: no particle bank in this context");
+    if (n_tasks <= 0) return;
+    const int64_t n_steps = step_off[n_tasks];
+    const int64_t n_hs = n_steps > 0 ? step_hs_off[n_steps] : 0;
+    const int dw = c.bank_dw;
+    char* base;
+    const size_t b_in = n_tasks * n_words * 8, b_off = (n_tasks + 1) * 8, b_t = n_steps * 4,
+                 b_hoff = (n_steps + 1) * 8, b_a = n_hs * dw * 8, b_b = n_hs * 8, b_pop = n_tasks * 4;
+    auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
+    const size_t total = al(b_in) * 2 + al(b_off) + al(b_t) + al(b_hoff) + al(b_a) + al(b_b) + al(b_pop) + 256;
+    DBuf& B = c.buf("hsmc_batch", total);
+    base = B.as<char>();
+    auto take = [&](size_t bytes) {
+      char* p = base;
+      base += al(bytes);
+      return p;
+    };
+    uint64_t* d_in = reinterpret_cast<uint64_t*>(take(b_in));
+    uint64_t* d_out = reinterpret_cast<uint64_t*>(take(b_in));
+    int64_t* d_off = reinterpret_cast<int64_t*>(take(b_off));
+    int32_t* d_t = reinterpret_cast<int32_t*>(take(b_t));
+    int64_t* d_hoff = reinterpret_cast<int64_t*>(take(b_hoff));
+    double* d_a = reinterpret_cast<double*>(take(b_a));
+    double* d_b = reinterpret_cast<double*>(take(b_b));
+    int32_t* d_pop = reinterpret_cast<int32_t*>(take(b_pop));
+    int* d_err = reinterpret_cast<int*>(take(4));
+    c.h2d(d_in, masks_in, b_in);
+    c.h2d(d_off, step_off, b_off);
+    c.h2d(d_t, step_t, b_t);
+    c.h2d(d_hoff, step_hs_off, b_hoff);
+    c.h2d(d_a, hs_a, b_a);
+    c.h2d(d_b, hs_b, b_b);
+    PUMP_CUDA(cudaMemsetAsync(d_err, 0, 4, c.stream));
+    c.tic();
+    launch_hsmc_batch(dw, c.bank_n, c.bank_horizon, c.bank.as<double>(), n_tasks, n_words, d_in, d_off, d_t, d_hoff,
+                      d_a, d_b, d_out, d_pop, d_err, c.stream, &c.launches);
+    c.toc();
+    int err = 0;
+    c.d2h(&err, d_err, 4);
+    c.d2h(masks_out, d_out, b_in);
+    c.d2h(popcount_out, d_pop, b_pop);
+    c.sync();
+    if (err) throw std::out_of_range("hsmc_extend: plan exceeds bank horizon");
+  });
+}
+
+// -------------------------------------------------------------------- mc
+int pump_mc_certify_batch(pump_ctx* ctx, const pump_closed_loop* cl, const pump_workspace* ws, int32_t n_traj,
+                          const int64_t* traj_off, const double* y_nom, int64_t rollout_lo, int64_t rollout_hi,
+                          uint64_t seed, double eps_cc, int64_t* hits_out) {
+  return guard([&] {
+    Ctx& c = ctx->c;
+    HostLoop L = host_loop(cl);
+    if (n_traj < 0) throw std::invalid_argument("mc_certify: negative trajectory count");
+    int max_pts = 0;
+    for (int j = 0; j < n_traj; ++j) {
+      const int64_t np = traj_off[j + 1] - traj_off[j];
+      if (np < 1) throw std::invalid_argument("mc_certify: empty trajectory");
+      max_pts = std::max<int>(max_pts, static_cast<int>(np));
+    }
+    if (n_traj == 0) return;
+    DevWorld w = upload_world(c, ws, "mc_ws_");
+    const int64_t n_pts = traj_off[n_traj];
+    DBuf& off = c.buf("mc_off", (n_traj + 1) * 8);
+    DBuf& yn = c.buf("mc_ynom", n_pts * L.dw * 8);
+    DBuf& hits = c.buf("mc_hits", n_traj * 8);
+    c.h2d(off.p, traj_off, (n_traj + 1) * 8);
+    c.h2d(yn.p, y_nom, n_pts * L.dw * 8);
+    PUMP_CUDA(cudaMemsetAsync(hits.p, 0, n_traj * 8, c.stream));
+    c.tic();
+    launch_mc(L, w, n_traj, off.as<int64_t>(), yn.as<double>(), max_pts, rollout_lo, rollout_hi, seed, eps_cc,
+              hits.as<unsigned long long>(), c.stream, &c.launches);
+    c.toc();
+    c.d2h(hits_out, hits.p, n_traj * 8);
+    c.sync();
+  });
+}
+
+int pump_mc_certify(pump_ctx* ctx, const pump_closed_loop* cl, const pump_workspace* ws, int32_t n_points,
+                    const double* y_nom, int32_t n_mc, uint64_t seed, double eps_cc, double* value_out) {
+  if (n_mc < 1) return fail(PUMP_E_INVALID_ARGUMENT, "mc_certify: need at least one rollout");
+  if (n_points < 1) return fail(PUMP_E_INVALID_ARGUMENT, "mc_certify: empty trajectory");
+  int64_t off[2] = {0, n_points};
+  int64_t hits = 0;
+  int rc = pump_mc_certify_batch(ctx, cl, ws, 1, off, y_nom, 0, n_mc, seed, eps_cc, &hits);
+  if (rc == PUMP_OK) *value_out = static_cast<double>(hits) / n_mc;
+  return rc;
+}
+
+}  // extern "C"

@@ -1,0 +1,118 @@
+// K_bank: presample_bank (lti.hpp:257-292) on sm_100a.
+//
+// The recursion z_{t+1} = F z_t + Gv(Sv nv_t) + Gw(Sw nw_{t+1}) is sequential
+// in t per particle, but its noise terms are not: they are pure functions of
+// the (seed, particle, timestep, channel) key.  So the bank is built in time
+// chunks of kChunk steps:
+//   k_bank_noise  — one thread per (t, i): 9 normals (3-D), u = Gv(Sv nv),
+//                   w = Gw(Sw nw); massively parallel, issue-bound on the
+//                   u64 hash + log/cos.
+//   k_bank_rec    — one thread per particle: y_t = C z_t stored, then
+//                   z <- ((F z) + u) + w, exactly the reference's rounding.
+// Noise is laid out component-major [t][r][i] so the recurrence's loads are
+// coalesced across particles.
+#include "dispatch.cuh"
+
+namespace pumpg {
+
+constexpr int kChunk = 256;
+
+template <int D, int DW>
+__global__ void __launch_bounds__(128) k_bank_noise(const LoopP<D, DW> L, int n, int t0, int tc, uint64_t seed,
+                                                    double* __restrict__ uw) {
+  const int64_t idx = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (idx >= static_cast<int64_t>(tc) * n) return;
+  const int tl = static_cast<int>(idx / n);
+  const int i = static_cast<int>(idx - static_cast<int64_t>(tl) * n);
+  const int t = t0 + tl;
+  const uint64_t sa = hash_seed_a(seed, static_cast<uint64_t>(i));
+  const uint64_t pt = mix64(sa + static_cast<uint64_t>(t));
+  const uint64_t pt1 = mix64(sa + static_cast<uint64_t>(t + 1));
+  double nv[D], nw[DW], t1[D], t2[DW];
+#pragma unroll
+  for (int k = 0; k < D; ++k) nv[k] = normal_from_prefix(pt, kProcess + k);
+#pragma unroll
+  for (int k = 0; k < DW; ++k) nw[k] = normal_from_prefix(pt1, kMeasurement + k);
+#pragma unroll
+  for (int r = 0; r < D; ++r) t1[r] = row_dot<D>(L.Sv + r * D, nv);
+#pragma unroll
+  for (int r = 0; r < DW; ++r) t2[r] = row_dot<DW>(L.Sw + r * DW, nw);
+  double* base = uw + static_cast<int64_t>(tl) * (4 * D) * n + i;
+#pragma unroll
+  for (int r = 0; r < 2 * D; ++r) {
+    base[static_cast<int64_t>(r) * n] = row_dot<D>(L.Gv + r * D, t1);
+    base[static_cast<int64_t>(2 * D + r) * n] = row_dot<DW>(L.Gw + r * DW, t2);
+  }
+}
+
+template <int D, int DW>
+__global__ void __launch_bounds__(32) k_bank_rec(const LoopP<D, DW> L, int n, int T, int t0, int tc, uint64_t seed,
+                                                 const double* __restrict__ uw, double* __restrict__ zstate,
+                                                 double* __restrict__ dy) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double z[2 * D];
+  if (t0 == 0) {
+    const uint64_t p0 = mix64(hash_seed_a(seed, static_cast<uint64_t>(i)) + 0ull);
+    double nv[D];
+#pragma unroll
+    for (int k = 0; k < D; ++k) nv[k] = normal_from_prefix(p0, static_cast<uint64_t>(k));  // kInitial + k
+#pragma unroll
+    for (int r = 0; r < D; ++r) z[r] = row_dot<D>(L.S0 + r * D, nv);
+#pragma unroll
+    for (int r = D; r < 2 * D; ++r) z[r] = 0.0;
+  } else {
+#pragma unroll
+    for (int r = 0; r < 2 * D; ++r) z[r] = zstate[static_cast<int64_t>(r) * n + i];
+  }
+  for (int tl = 0; tl <= tc; ++tl) {
+    const int t = t0 + tl;
+    if (tl == tc && t != T) break;  // next chunk stores y_t
+    double* slot = dy + (static_cast<int64_t>(t) * n + i) * DW;
+#pragma unroll
+    for (int k = 0; k < DW; ++k) slot[k] = row_dot<D>(L.C + k * D, z);
+    if (t == T) break;
+    const double* u = uw + static_cast<int64_t>(tl) * (4 * D) * n + i;
+    double zn[2 * D];
+#pragma unroll
+    for (int r = 0; r < 2 * D; ++r) {
+      double a = row_dot<2 * D>(L.F + r * 2 * D, z);
+      zn[r] = (a + u[static_cast<int64_t>(r) * n]) + u[static_cast<int64_t>(2 * D + r) * n];
+    }
+#pragma unroll
+    for (int r = 0; r < 2 * D; ++r) z[r] = zn[r];
+  }
+#pragma unroll
+  for (int r = 0; r < 2 * D; ++r) zstate[static_cast<int64_t>(r) * n + i] = z[r];
+}
+
+size_t bank_scratch_bytes(const HostLoop& L, int n, int T) {
+  (void)T;
+  const int D = L.d;
+  return (static_cast<size_t>(kChunk) * 4 * D * n + static_cast<size_t>(2 * D) * n) * sizeof(double);
+}
+
+void launch_bank(const HostLoop& HL, int n, int T, uint64_t seed, double* d_dy, void* d_scratch, cudaStream_t st,
+                 int64_t* launches) {
+  if (n < 1) throw std::invalid_argument("presample_bank: need at least one particle");
+  if (T < 1) throw std::invalid_argument("presample_bank: horizon must be at least 1");
+  dispatch_dims(HL.d, HL.dw, [&]<int D, int DW>() {
+    const LoopP<D, DW> L = make_loop<D, DW>(HL);
+    double* uw = static_cast<double*>(d_scratch);
+    double* zs = uw + static_cast<size_t>(kChunk) * 4 * D * n;
+    for (int t0 = 0; t0 <= T; t0 += kChunk) {
+      const int tc = std::min(kChunk, T - t0);  // steps advanced in this chunk
+      if (tc > 0) {
+        const int64_t items = static_cast<int64_t>(tc) * n;
+        k_bank_noise<D, DW><<<grid_for(items, 128), 128, 0, st>>>(L, n, t0, tc, seed, uw);
+        ++*launches;
+      }
+      k_bank_rec<D, DW><<<grid_for(n, 32), 32, 0, st>>>(L, n, T, t0, tc, seed, uw, zs, d_dy);
+      ++*launches;
+      if (tc < kChunk) break;
+    }
+    PUMP_CUDA(cudaGetLastError());
+  });
+}
+
+}  // namespace pumpg

@@ -1,0 +1,221 @@
+// Device building blocks shared by the sm_100a kernels.
+//
+// Bit-exactness contract: this translation unit is
+// compiled with --fmad=false, every reduction is sequential from +0.0 in the
+// reference's order, divisions and square roots are IEEE (correctly rounded),
+// and log/cos come from csrc/common/pmath.h (shared with the CPU oracle).
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "../common/pmath.h"
+
+namespace pumpg {
+
+constexpr uint64_t kPhi = 0x9e3779b97f4a7c15ULL;
+constexpr uint64_t kProcess = 1ull << 20;      // rng.hpp:52-56
+constexpr uint64_t kMeasurement = 2ull << 20;
+constexpr double kTwoPi = 2.0 * 3.14159265358979323846;
+
+// splitmix64 finalizer (rng.hpp:8-15)
+__device__ __forceinline__ uint64_t mix64(uint64_t x) {
+  x ^= x >> 30;
+  x *= 0xbf58476d1ce4e5b9ULL;
+  x ^= x >> 27;
+  x *= 0x94d049bb133111ebULL;
+  x ^= x >> 31;
+  return x;
+}
+
+// counter_hash(seed, a, b, c) = mix(prefix(seed, a, b) + c) with
+// prefix = mix(mix(mix(seed + phi) + a) + b)  (rng.hpp:20-29).  Splitting
+// out the prefix lets one (particle, timestep) key serve all its channels.
+__device__ __forceinline__ uint64_t hash_prefix2(uint64_t seed_a /* mix(mix(seed+phi)+a) */, uint64_t b) {
+  return mix64(seed_a + b);
+}
+__device__ __forceinline__ uint64_t hash_seed_a(uint64_t seed, uint64_t a) {
+  return mix64(mix64(seed + kPhi) + a);
+}
+__device__ __forceinline__ double to_unit(uint64_t x) {  // rng.hpp:32-34
+  return (static_cast<double>(x >> 11) + 1.0) * 0x1p-53;
+}
+// normal(seed, a, b, ch) given prefix = mix(mix(mix(seed+phi)+a)+b)  (rng.hpp:43-49)
+__device__ __forceinline__ double normal_from_prefix(uint64_t prefix, uint64_t ch) {
+  double u1 = to_unit(mix64(prefix + 2 * ch));
+  double u2 = to_unit(mix64(prefix + 2 * ch + 1));
+  return sqrt(-2.0 * pump_pm::plog(u1)) * pump_pm::pcos(kTwoPi * u2);
+}
+
+// Closed-loop matrices as a kernel parameter (constant bank), compile-time
+// dims so every gemv is fully unrolled with constant-bank operands.
+template <int D, int DW>
+struct LoopP {
+  double F[4 * D * D];
+  double Gv[2 * D * D];
+  double Gw[2 * D * DW];
+  double Sv[D * D];
+  double Sw[DW * DW];
+  double S0[D * D];
+  double C[DW * D];
+};
+
+// Eigen gemv row: c = 0; c = c + M_ij x_j (j ascending)
+template <int N>
+__device__ __forceinline__ double row_dot(const double* row, const double* x) {
+  double c = 0.0;
+#pragma unroll
+  for (int j = 0; j < N; ++j) c = c + row[j] * x[j];
+  return c;
+}
+
+// z <- ((F z) + Gv (Sv nv)) + Gw (Sw nw)   (lti.hpp:287, cp.hpp:254)
+template <int D, int DW>
+__device__ __forceinline__ void cl_step(const LoopP<D, DW>& L, double (&z)[2 * D], const double (&nv)[D],
+                                        const double (&nw)[DW]) {
+  double t1[D], t2[DW], zn[2 * D];
+#pragma unroll
+  for (int r = 0; r < D; ++r) t1[r] = row_dot<D>(L.Sv + r * D, nv);
+#pragma unroll
+  for (int r = 0; r < DW; ++r) t2[r] = row_dot<DW>(L.Sw + r * DW, nw);
+#pragma unroll
+  for (int r = 0; r < 2 * D; ++r) {
+    double a = row_dot<2 * D>(L.F + r * 2 * D, z);
+    double b = row_dot<D>(L.Gv + r * D, t1);
+    double c = row_dot<DW>(L.Gw + r * DW, t2);
+    zn[r] = (a + b) + c;
+  }
+#pragma unroll
+  for (int r = 0; r < 2 * D; ++r) z[r] = zn[r];
+}
+
+// ----------------------------------------------------------- geometry
+// closed AABB containment (geom.hpp:19-23)
+template <int DW>
+__device__ __forceinline__ bool box_contains(const double* lo, const double* hi, const double* p) {
+  bool in = true;
+#pragma unroll
+  for (int k = 0; k < DW; ++k) in = in && !(p[k] < lo[k] || p[k] > hi[k]);
+  return in;
+}
+
+// Workspace with obstacles stored SoA-by-box: lo[o*DW+k], hi[o*DW+k].
+struct WorldD {
+  int n_obs;
+  const double* lo;  // obstacles
+  const double* hi;
+  double blo[6], bhi[6];  // bounds
+};
+
+template <int DW>
+__device__ __forceinline__ bool point_free(const WorldD& w, const double* y) {  // geom.hpp:56-61
+  if (!box_contains<DW>(w.blo, w.bhi, y)) return false;
+  for (int o = 0; o < w.n_obs; ++o)
+    if (box_contains<DW>(w.lo + o * DW, w.hi + o * DW, y)) return false;
+  return true;
+}
+
+// slab test, closed box (geom.hpp:64-80)
+template <int DW>
+__device__ __forceinline__ bool segment_hits(const double* p0, const double* p1, const double* lo, const double* hi) {
+  double tmin = 0.0, tmax = 1.0;
+#pragma unroll
+  for (int k = 0; k < DW; ++k) {
+    double d = p1[k] - p0[k];
+    if (fabs(d) < 1e-300) {
+      if (p0[k] < lo[k] || p0[k] > hi[k]) return false;
+      continue;
+    }
+    double t0 = (lo[k] - p0[k]) / d;
+    double t1 = (hi[k] - p0[k]) / d;
+    if (t0 > t1) {
+      double s = t0;
+      t0 = t1;
+      t1 = s;
+    }
+    tmin = (tmin < t0) ? t0 : tmin;  // std::max(tmin, t0)
+    tmax = (t1 < tmax) ? t1 : tmax;  // std::min(tmax, t1)
+    if (tmin > tmax) return false;
+  }
+  return true;
+}
+
+template <int DW>
+__device__ __forceinline__ bool segment_collides(const WorldD& w, const double* p0, const double* p1) {
+  for (int o = 0; o < w.n_obs; ++o)
+    if (segment_hits<DW>(p0, p1, w.lo + o * DW, w.hi + o * DW)) return true;
+  return false;
+}
+
+template <int N>
+__device__ __forceinline__ double sqnorm(const double* x) {
+  double s = 0.0;
+#pragma unroll
+  for (int k = 0; k < N; ++k) s = s + x[k] * x[k];
+  return s;
+}
+
+// ---------------------------------------------------------------- steer
+// Motion polynomial per axis (steer.hpp:37-51)
+template <int DW>
+struct MotionD {
+  double p0[DW], v0[DW], p1[DW], v1[DW], a[DW], j[DW];
+  double tau;
+};
+
+template <int DW>
+__device__ __forceinline__ void motion_pos(const MotionD<DW>& m, double s, double* out) {
+  if (s <= 0) {
+#pragma unroll
+    for (int k = 0; k < DW; ++k) out[k] = m.p0[k];
+    return;
+  }
+  if (s >= m.tau) {
+#pragma unroll
+    for (int k = 0; k < DW; ++k) out[k] = m.p1[k];
+    return;
+  }
+#pragma unroll
+  for (int k = 0; k < DW; ++k) out[k] = m.p0[k] + m.v0[k] * s + m.a[k] * s * s / 2 + m.j[k] * s * s * s / 6;
+}
+
+template <int DW>
+__device__ __forceinline__ void motion_state(const MotionD<DW>& m, double s, double* pos, double* vel) {
+  if (s <= 0) {
+#pragma unroll
+    for (int k = 0; k < DW; ++k) {
+      pos[k] = m.p0[k];
+      vel[k] = m.v0[k];
+    }
+    return;
+  }
+  if (s >= m.tau) {
+#pragma unroll
+    for (int k = 0; k < DW; ++k) {
+      pos[k] = m.p1[k];
+      vel[k] = m.v1[k];
+    }
+    return;
+  }
+#pragma unroll
+  for (int k = 0; k < DW; ++k) {
+    pos[k] = m.p0[k] + m.v0[k] * s + m.a[k] * s * s / 2 + m.j[k] * s * s * s / 6;
+    vel[k] = m.v0[k] + m.a[k] * s + m.j[k] * s * s / 2;
+  }
+}
+
+// c(tau) (steer.hpp:84-94)
+template <int DW>
+__device__ __forceinline__ double steer_cost(const double* ap, const double* av, const double* bp, const double* bv,
+                                             double tau) {
+  double c = tau;
+#pragma unroll
+  for (int k = 0; k < DW; ++k) {
+    double dp = bp[k] - ap[k] - av[k] * tau;
+    double dv = bv[k] - av[k];
+    c += 12 * dp * dp / (tau * tau * tau) - 12 * dp * dv / (tau * tau) + 4 * dv * dv / tau;
+  }
+  return c;
+}
+
+}  // namespace pumpg

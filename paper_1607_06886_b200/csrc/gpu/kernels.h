@@ -1,0 +1,62 @@
+// Host-callable launchers of the sm_100a kernels (implemented in *.cu).
+// All launchers are stream-ordered; none synchronizes.
+#pragma once
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include <cuda_runtime.h>
+
+#include "../../../include/pump_gpu.h"
+
+namespace pumpg {
+
+struct CudaError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+inline void cuda_check(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) throw CudaError(std::string(what) + ": " + cudaGetErrorString(e));
+}
+#define PUMP_CUDA(x) ::pumpg::cuda_check((x), #x)
+
+// Host copy of a ClosedLoop (row-major), dims checked.
+struct HostLoop {
+  int d = 0, dw = 0;
+  std::vector<double> F, Gv, Gw, Sv, Sw, S0, C;
+};
+HostLoop host_loop(const pump_closed_loop* cl);
+
+// Workspace on the device: obstacles packed lo[o*dw+k], hi[o*dw+k].
+struct DevWorld {
+  int dw = 0, n_obs = 0;
+  double blo[6] = {0}, bhi[6] = {0};
+  double* d_lo = nullptr;
+  double* d_hi = nullptr;
+};
+
+// ------------------------------------------------------------------ bank
+// presample_bank (lti.hpp:257-292) into d_dy [(T+1) x n x dw].
+// scratch must hold bank_scratch_bytes(...) bytes.
+size_t bank_scratch_bytes(const HostLoop& L, int n, int T);
+void launch_bank(const HostLoop& L, int n, int T, uint64_t seed, double* d_dy, void* d_scratch, cudaStream_t st,
+                 int64_t* launches);
+
+// ------------------------------------------------------------------ hsmc
+// Batched hsmc_extend (cp.hpp:180-208); d_err set to 1 on a step outside
+// [0, horizon].
+void launch_hsmc_batch(int dw, int n, int horizon, const double* d_dy, int64_t n_tasks, int n_words,
+                       const uint64_t* d_in, const int64_t* d_step_off, const int32_t* d_step_t,
+                       const int64_t* d_step_hs_off, const double* d_hs_a, const double* d_hs_b, uint64_t* d_out,
+                       int32_t* d_pop, int* d_err, cudaStream_t st, int64_t* launches);
+
+// --------------------------------------------------------------------- mc
+// Batched mc_certify (cp.hpp:214-268) over trajectories and the rollout
+// range [r0, r1); d_hits[j] += colliding rollouts of trajectory j.
+void launch_mc(const HostLoop& L, const DevWorld& w, int n_traj, const int64_t* d_traj_off, const double* d_ynom,
+               int max_points, int64_t r0, int64_t r1, uint64_t seed, double eps_cc, unsigned long long* d_hits,
+               cudaStream_t st, int64_t* launches);
+
+}  // namespace pumpg

@@ -1,0 +1,239 @@
+// Ordered device primitives (see scan.cuh).
+#include <stdexcept>
+
+#include "kernels.h"
+#include "scan.cuh"
+
+namespace pumpg {
+
+template <class InT>
+__global__ void __launch_bounds__(kScanBlock) k_tile_sum(const InT* __restrict__ in, int64_t n,
+                                                         int64_t* __restrict__ partial) {
+  __shared__ int64_t wsum[kScanBlock / 32];
+  const int64_t base = static_cast<int64_t>(blockIdx.x) * kScanTile;
+  int64_t s = 0;
+#pragma unroll
+  for (int k = 0; k < kScanItems; ++k) {
+    const int64_t i = base + k * kScanBlock + threadIdx.x;
+    if (i < n) s += static_cast<int64_t>(in[i]);
+  }
+  s = warp_sum(s);
+  if ((threadIdx.x & 31) == 0) wsum[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    int64_t x = threadIdx.x < kScanBlock / 32 ? wsum[threadIdx.x] : 0;
+    x = warp_sum(x);
+    if (threadIdx.x == 0) partial[blockIdx.x] = x;
+  }
+}
+
+// exclusive scan of partial[0..m) in place (single block); total -> *total
+__global__ void __launch_bounds__(1024) k_scan_partials(int64_t* __restrict__ partial, int64_t m,
+                                                        int64_t* __restrict__ total) {
+  __shared__ int64_t wsum[32];
+  __shared__ int64_t carry;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  for (int64_t c0 = 0; c0 < m; c0 += 1024) {
+    const int64_t i = c0 + threadIdx.x;
+    int64_t x = i < m ? partial[i] : 0;
+    int64_t inc = warp_incl_scan(x);
+    if ((threadIdx.x & 31) == 31) wsum[threadIdx.x >> 5] = inc;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+      int64_t w = wsum[threadIdx.x];
+      int64_t wi = warp_incl_scan(w);
+      wsum[threadIdx.x] = wi - w;
+    }
+    __syncthreads();
+    const int64_t excl = carry + wsum[threadIdx.x >> 5] + inc - x;
+    if (i < m) partial[i] = excl;
+    __syncthreads();
+    if (threadIdx.x == 1023) carry = excl + x;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *total = carry;
+}
+
+template <class InT>
+__global__ void __launch_bounds__(kScanBlock) k_tile_scan(const InT* __restrict__ in, int64_t n,
+                                                          const int64_t* __restrict__ partial,
+                                                          int64_t* __restrict__ out) {
+  __shared__ int64_t tile[kScanTile];
+  __shared__ int64_t wsum[kScanBlock / 32];
+  const int64_t base = static_cast<int64_t>(blockIdx.x) * kScanTile;
+#pragma unroll
+  for (int k = 0; k < kScanItems; ++k) {
+    const int64_t i = base + k * kScanBlock + threadIdx.x;
+    tile[k * kScanBlock + threadIdx.x] = i < n ? static_cast<int64_t>(in[i]) : 0;
+  }
+  __syncthreads();
+  int64_t v[kScanItems];
+  int64_t s = 0;
+#pragma unroll
+  for (int k = 0; k < kScanItems; ++k) {
+    v[k] = tile[threadIdx.x * kScanItems + k];
+    s += v[k];
+  }
+  const int64_t inc = warp_incl_scan(s);
+  if ((threadIdx.x & 31) == 31) wsum[threadIdx.x >> 5] = inc;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    int64_t w = threadIdx.x < kScanBlock / 32 ? wsum[threadIdx.x] : 0;
+    int64_t wi = warp_incl_scan(w);
+    if (threadIdx.x < kScanBlock / 32) wsum[threadIdx.x] = wi - w;
+  }
+  __syncthreads();
+  int64_t run = partial[blockIdx.x] + wsum[threadIdx.x >> 5] + inc - s;
+#pragma unroll
+  for (int k = 0; k < kScanItems; ++k) {
+    tile[threadIdx.x * kScanItems + k] = run;
+    run += v[k];
+  }
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < kScanItems; ++k) {
+    const int64_t i = base + k * kScanBlock + threadIdx.x;
+    if (i < n) out[i] = tile[k * kScanBlock + threadIdx.x];
+  }
+}
+
+size_t scan_temp_bytes(int64_t n) { return static_cast<size_t>((n + kScanTile - 1) / kScanTile + 1) * 8 + 256; }
+
+template <class InT>
+void exclusive_scan(const InT* d_in, int64_t* d_out, int64_t n, void* d_temp, cudaStream_t st, int64_t* launches) {
+  if (n <= 0) {
+    PUMP_CUDA(cudaMemsetAsync(d_out, 0, sizeof(int64_t), st));
+    return;
+  }
+  const int64_t tiles = (n + kScanTile - 1) / kScanTile;
+  int64_t* partial = static_cast<int64_t*>(d_temp);
+  k_tile_sum<InT><<<static_cast<unsigned>(tiles), kScanBlock, 0, st>>>(d_in, n, partial);
+  k_scan_partials<<<1, 1024, 0, st>>>(partial, tiles, d_out + n);
+  k_tile_scan<InT><<<static_cast<unsigned>(tiles), kScanBlock, 0, st>>>(d_in, n, partial, d_out);
+  *launches += 3;
+  PUMP_CUDA(cudaGetLastError());
+}
+
+template void exclusive_scan<int32_t>(const int32_t*, int64_t*, int64_t, void*, cudaStream_t, int64_t*);
+template void exclusive_scan<int64_t>(const int64_t*, int64_t*, int64_t, void*, cudaStream_t, int64_t*);
+template void exclusive_scan<uint8_t>(const uint8_t*, int64_t*, int64_t, void*, cudaStream_t, int64_t*);
+
+// ------------------------------------------------------------ multisplit
+constexpr int kMsBlock = 512;
+constexpr int kMsItems = 8;
+constexpr int kMsTile = kMsBlock * kMsItems;
+constexpr int kMsKeys = 512;  // keys per pass
+constexpr int kMsWarps = kMsBlock / 32;
+
+__device__ __forceinline__ int ms_digit(int key, int shift) { return key < 0 ? -1 : ((key >> shift) & (kMsKeys - 1)); }
+
+__global__ void __launch_bounds__(kMsBlock) k_ms_hist(const int32_t* __restrict__ keys, int64_t n, int shift,
+                                                      int n_tiles, int32_t* __restrict__ counts) {
+  __shared__ int hist[kMsKeys];
+  for (int k = threadIdx.x; k < kMsKeys; k += kMsBlock) hist[k] = 0;
+  __syncthreads();
+  const int64_t base = static_cast<int64_t>(blockIdx.x) * kMsTile;
+  for (int s = 0; s < kMsItems; ++s) {
+    const int64_t i = base + s * kMsBlock + threadIdx.x;
+    if (i < n) {
+      const int d = ms_digit(keys[i], shift);
+      if (d >= 0) atomicAdd(&hist[d], 1);
+    }
+  }
+  __syncthreads();
+  for (int k = threadIdx.x; k < kMsKeys; k += kMsBlock) counts[static_cast<int64_t>(k) * n_tiles + blockIdx.x] = hist[k];
+}
+
+__global__ void __launch_bounds__(kMsBlock) k_ms_scatter(const int32_t* __restrict__ keys,
+                                                         const int32_t* __restrict__ vals, int64_t n, int shift,
+                                                         int n_tiles, const int64_t* __restrict__ offs,
+                                                         int32_t* __restrict__ okeys, int32_t* __restrict__ ovals) {
+  __shared__ int wcnt[kMsWarps][kMsKeys];
+  __shared__ int64_t run[kMsKeys];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int k = threadIdx.x; k < kMsKeys; k += kMsBlock) {
+    run[k] = offs[static_cast<int64_t>(k) * n_tiles + blockIdx.x];
+    for (int w = 0; w < kMsWarps; ++w) wcnt[w][k] = 0;
+  }
+  __syncthreads();
+  const int64_t base = static_cast<int64_t>(blockIdx.x) * kMsTile;
+  const unsigned lt = (1u << lane) - 1u;
+  for (int s = 0; s < kMsItems; ++s) {
+    const int64_t i = base + s * kMsBlock + threadIdx.x;
+    const int key = i < n ? keys[i] : -1;
+    const int d = ms_digit(key, shift);
+    const unsigned peers = __match_any_sync(0xffffffffu, d);
+    const int rank = __popc(peers & lt);
+    if (d >= 0 && rank == 0) wcnt[warp][d] = __popc(peers);
+    __syncthreads();
+    if (d >= 0) {
+      int64_t pos = run[d] + rank;
+      for (int w = 0; w < warp; ++w) pos += wcnt[w][d];
+      okeys[pos] = key;
+      ovals[pos] = vals[i];
+    }
+    __syncthreads();
+    for (int k = threadIdx.x; k < kMsKeys; k += kMsBlock) {
+      int t = 0;
+      for (int w = 0; w < kMsWarps; ++w) {
+        t += wcnt[w][k];
+        wcnt[w][k] = 0;
+      }
+      run[k] += t;
+    }
+    __syncthreads();
+  }
+}
+
+static inline size_t al256(size_t x) { return (x + 255) & ~size_t(255); }
+
+size_t multisplit_temp_bytes(int64_t n, int n_keys) {
+  const int64_t tiles = (n + kMsTile - 1) / kMsTile;
+  const int64_t cn = static_cast<int64_t>(kMsKeys) * (tiles > 0 ? tiles : 1);
+  (void)n_keys;
+  return al256(cn * 4) + al256((cn + 1) * 8) + al256(scan_temp_bytes(cn)) + 2 * al256((n + 1) * 4) + 256;
+}
+
+void stable_multisplit(const int32_t* d_keys, const int32_t* d_vals, int64_t n, int n_keys, int32_t* d_out,
+                       int64_t* d_count, void* d_temp, cudaStream_t st, int64_t* launches) {
+  if (n <= 0) {
+    PUMP_CUDA(cudaMemsetAsync(d_count, 0, 8, st));
+    return;
+  }
+  if (n_keys > kMsKeys * kMsKeys) throw std::invalid_argument("multisplit: key range too large");
+  const int64_t tiles = (n + kMsTile - 1) / kMsTile;
+  const int64_t cn = static_cast<int64_t>(kMsKeys) * tiles;
+  char* p = static_cast<char*>(d_temp);
+  int32_t* counts = reinterpret_cast<int32_t*>(p);
+  p += al256(cn * 4);
+  int64_t* offs = reinterpret_cast<int64_t*>(p);
+  p += al256((cn + 1) * 8);
+  void* stmp = p;
+  p += al256(scan_temp_bytes(cn));
+  int32_t* k2 = reinterpret_cast<int32_t*>(p);
+  p += al256((n + 1) * 4);
+  int32_t* v2 = reinterpret_cast<int32_t*>(p);
+  const int passes = n_keys <= kMsKeys ? 1 : 2;
+  // LSD passes: pass 0 on the low 9 bits, pass 1 (if any) on the next 9.
+  const int32_t* ck = d_keys;
+  const int32_t* cv = d_vals;
+  for (int pass = 0; pass < passes; ++pass) {
+    const int shift = 9 * pass;
+    const bool last = pass == passes - 1;
+    int32_t* ok = last ? k2 : k2;  // keys always go to scratch
+    int32_t* ov = last ? d_out : v2;
+    if (!last) ov = v2;
+    k_ms_hist<<<static_cast<unsigned>(tiles), kMsBlock, 0, st>>>(ck, n, shift, static_cast<int>(tiles), counts);
+    exclusive_scan<int32_t>(counts, offs, cn, stmp, st, launches);
+    if (last) PUMP_CUDA(cudaMemcpyAsync(d_count, offs + cn, 8, cudaMemcpyDeviceToDevice, st));
+    k_ms_scatter<<<static_cast<unsigned>(tiles), kMsBlock, 0, st>>>(ck, cv, n, shift, static_cast<int>(tiles), offs,
+                                                                     ok, ov);
+    *launches += 2;
+    ck = k2;
+    cv = v2;
+  }
+  PUMP_CUDA(cudaGetLastError());
+}
+
+}  // namespace pumpg
