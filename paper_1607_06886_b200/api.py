@@ -316,3 +316,106 @@ def mc_certify(y_nom, cl: dict, ws: dict, n_mc: int, seed: int, eps_cc: float, c
     if len(y_nom) == 0:
         raise ValueError("mc_certify: empty trajectory")
     return float(mc_certify_batch(cl, ws, [y_nom], 0, n_mc, seed, eps_cc, ctx)[0]) / n_mc
+
+
+# -------------------------------------------------------------------- graph
+class Graph:
+    """Device-resident SampleGraph (graph.hpp:25-37)."""
+
+    def __init__(self, handle, ctx):
+        self.h = handle
+        self.ctx = ctx
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            lib().pump_graph_free(self.h)
+            self.h = None
+
+    def counts(self) -> dict:
+        v = A.GraphViewC()
+        _check(lib().pump_graph_counts(self.h, C.byref(v)))
+        return {f: getattr(v, f) for f, _ in v._fields_ if f not in A.GRAPH_ARRAYS}
+
+    def export(self) -> dict:
+        v = A.GraphViewC()
+        _check(lib().pump_graph_counts(self.h, C.byref(v)))
+        return A.export_view(v, A.GRAPH_ARRAYS, lambda h, pv: lib().pump_graph_export(h, pv), self.h)
+
+    @property
+    def edge_count(self) -> int:
+        return int(self.counts()["n_edges"])
+
+
+def build_graph(pos, vel, ws: dict, goal: dict, r_n: float, dt: float, eps_cc: float, tau_max: float,
+                ctx: Context | None = None) -> Graph:
+    """build_graph (graph.hpp:50-95) on the GPU for nodes (pos, vel: n x dw)."""
+    ctx = ctx or default_context()
+    keep = A.Keep()
+    pos = keep.f64(pos)
+    vel = keep.f64(vel)
+    n, dw = pos.shape
+    wss = A.workspace_struct(ws, keep)
+    gs = A.goal_struct(goal, keep)
+    h = C.c_void_p()
+    _check(lib().pump_build_graph(ctx.h, n, dw, _p(pos), _p(vel), C.byref(wss), C.byref(gs), r_n, dt, eps_cc,
+                                  tau_max, C.byref(h)))
+    return Graph(h, ctx)
+
+
+def graph_upload(g: dict, ctx: Context | None = None) -> Graph:
+    """Upload a prebuilt graph (flat arrays as returned by Graph.export)."""
+    ctx = ctx or default_context()
+    keep = A.Keep()
+    v = A.view_from_arrays(A.GraphViewC, g, A.GRAPH_ARRAYS, keep,
+                           {k: g[k] for k in ("n_nodes", "dw", "n_edges", "n_waypoints", "n_halfspaces", "n_goal",
+                                              "r_n", "dt")})
+    h = C.c_void_p()
+    _check(lib().pump_graph_upload(ctx.h, C.byref(v), C.byref(h)))
+    return Graph(h, ctx)
+
+
+# ------------------------------------------------------------------ explore
+def explore(graph: Graph, alpha_min: float, alpha_max: float, lam: float, r_n: float,
+            ctx: Context | None = None, masks: bool = True) -> dict:
+    """explore (planner.hpp:74-267) on the context's resident bank."""
+    ctx = ctx or graph.ctx
+    p = A.ExploreParamsC()
+    p.alpha_min, p.alpha_max, p.lambda_, p.r_n = alpha_min, alpha_max, lam, r_n
+    h = C.c_void_p()
+    _check(lib().pump_explore_run(ctx.h, graph.h, C.byref(p), C.byref(h)))
+    try:
+        v = A.ExploreViewC()
+        _check(lib().pump_explore_counts(h, C.byref(v)))
+        out = A.export_view(v, A.EXPLORE_ARRAYS, lambda hh, pv: lib().pump_explore_export(hh, pv), h,
+                            skip=() if masks else ("masks",))
+    finally:
+        lib().pump_explore_free(h)
+    out["termination"] = A.TERMINATION[out["termination"]]
+    return out
+
+
+# ----------------------------------------------------------------- pipeline
+def run_pump(scenario: Scenario, prebuilt: Graph | None = None, ctx: Context | None = None) -> dict:
+    """run_pump (pump.hpp:170-263): graph build, bank + explore, bisection
+    selection with MC certification, smoothing — all hot loops on the GPU."""
+    ctx = ctx or default_context()
+    h = C.c_void_p()
+    _check(lib().pump_run(ctx.h, scenario.h, prebuilt.h if prebuilt else None, C.byref(h)))
+    try:
+        s = A.ResultSummaryC()
+        _check(lib().pump_result_summary_get(h, C.byref(s)))
+        dw = s.dw
+        path = np.zeros(s.path_len, dtype=np.int32)
+        pc, pcp = np.zeros(s.n_pareto), np.zeros(s.n_pareto)
+        ids, mcs = np.zeros(s.n_mc_evals, dtype=np.int32), np.zeros(s.n_mc_evals)
+        n = s.n_traj_points
+        tt, tp, tv, tu = np.zeros(n), np.zeros((n, dw)), np.zeros((n, dw)), np.zeros((n, dw))
+        _check(lib().pump_result_arrays(h, *[_p(x) if x.size else None
+                                             for x in (path, pc, pcp, ids, mcs, tt, tp, tv, tu)]))
+    finally:
+        lib().pump_result_free(h)
+    out = {f: getattr(s, f) for f, _ in s._fields_}
+    out.update(path=path, pareto_cost=pc, pareto_cp=pcp, mc_eval_ids=ids, mc_eval_values=mcs, traj_t=tt,
+               traj_pos=tp, traj_vel=tv, traj_ctrl=tu)
+    out["termination"] = A.TERMINATION[out["termination"]]
+    return out

@@ -1,0 +1,954 @@
+// C ABI: build_graph / explore / run_pump (include/pump_gpu.h) and the host
+// orchestration of the full solve (pump.hpp:170-263).  Host glue that the
+// reference runs on the CPU after exploration (path walk, waypoint
+// concatenation, front reduction, Alg. 4 bisection replay, smoothing
+// bisection) runs here in C++ with the same __host__ __device__ geometry the
+// kernels use; every Monte-Carlo certification runs on the GPU (K_mc).
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <limits>
+#include <numeric>
+
+#include "ctx.h"
+#include "gpu/dispatch.cuh"
+#include "gpu/explore.h"
+#include "gpu/graph.h"
+#include "guard.h"
+
+using namespace pumpg;
+
+namespace pumpg {
+
+// ---------------------------------------------------------------- host glue
+struct HWp {  // Waypoint (steer.hpp:184-188)
+  double t;
+  double p[6], v[6], u[6];
+};
+
+struct HMotion {
+  double p0[6], v0[6], p1[6], v1[6], a[6], j[6];
+  double tau;
+};
+
+template <int DW>
+static MotionD<DW> as_motion(const HMotion& h) {
+  MotionD<DW> m;
+  for (int k = 0; k < DW; ++k) {
+    m.p0[k] = h.p0[k];
+    m.v0[k] = h.v0[k];
+    m.p1[k] = h.p1[k];
+    m.v1[k] = h.v1[k];
+    m.a[k] = h.a[k];
+    m.j[k] = h.j[k];
+  }
+  m.tau = h.tau;
+  return m;
+}
+
+// fixed_time_coeffs (steer.hpp:63-79) + cost
+static double fixed_time(HMotion& m, int dw) {
+  const double tau = m.tau;
+  double effort = 0;
+  for (int k = 0; k < dw; ++k) {
+    double dp = m.p1[k] - m.p0[k] - m.v0[k] * tau;
+    double dv = m.v1[k] - m.v0[k];
+    m.a[k] = 6 * dp / (tau * tau) - 2 * dv / tau;
+    m.j[k] = -12 * dp / (tau * tau * tau) + 6 * dv / (tau * tau);
+    effort += 12 * dp * dp / (tau * tau * tau) - 12 * dp * dv / (tau * tau) + 4 * dv * dv / tau;
+  }
+  return tau + effort;
+}
+
+static void state_at(const HMotion& m, int dw, double s, double* p, double* v) {
+  dispatch_dw(dw, [&]<int DW>() { motion_state<DW>(as_motion<DW>(m), s, p, v); });
+}
+
+static void control_at(const HMotion& m, int dw, double s, double* u) {  // steer.hpp:53-57
+  if (m.tau <= 0) {
+    for (int k = 0; k < dw; ++k) u[k] = 0;
+    return;
+  }
+  s = std::clamp(s, 0.0, m.tau);
+  for (int k = 0; k < dw; ++k) u[k] = m.a[k] + m.j[k] * s;
+}
+
+static std::vector<HWp> motion_waypoints(const HMotion& m, int dw, double dt) {  // steer.hpp:192-212
+  std::vector<HWp> out;
+  HWp w{};
+  if (m.tau <= 0) {
+    w.t = 0;
+    std::memcpy(w.p, m.p0, sizeof(w.p));
+    std::memcpy(w.v, m.v0, sizeof(w.v));
+    out.push_back(w);
+    return out;
+  }
+  const int k = static_cast<int>(std::floor(m.tau / dt + 1e-9));
+  const double rem = m.tau - k * dt;
+  for (int i = 0; i <= k; ++i) {
+    const double t = i * dt;
+    w.t = t;
+    state_at(m, dw, t, w.p, w.v);
+    control_at(m, dw, t, w.u);
+    out.push_back(w);
+  }
+  if (rem > 1e-9) {
+    w.t = m.tau;
+    std::memcpy(w.p, m.p1, sizeof(w.p));
+    std::memcpy(w.v, m.v1, sizeof(w.v));
+    control_at(m, dw, m.tau, w.u);
+    out.push_back(w);
+  } else {
+    out.back().t = m.tau;
+    std::memcpy(out.back().p, m.p1, sizeof(w.p));
+    std::memcpy(out.back().v, m.v1, sizeof(w.v));
+  }
+  return out;
+}
+
+static double seq_sqn(const double* x, int n) {
+  double s = 0.0;
+  for (int k = 0; k < n; ++k) s = s + x[k] * x[k];
+  return s;
+}
+
+static double trajectory_cost(const std::vector<HWp>& t, int dw) {  // planner.hpp:319-330
+  double c = t.empty() ? 0 : t.back().t;
+  for (size_t j = 0; j + 1 < t.size(); ++j) {
+    const double h = t[j + 1].t - t[j].t;
+    double um[6];
+    for (int k = 0; k < dw; ++k) um[k] = 0.5 * (t[j].u[k] + t[j + 1].u[k]);
+    c += h / 6.0 * (seq_sqn(t[j].u, dw) + 4.0 * seq_sqn(um, dw) + seq_sqn(t[j + 1].u, dw));
+  }
+  return c;
+}
+
+struct HostWorld {
+  int dw = 0;
+  std::vector<double> lo, hi;
+  double blo[6] = {0}, bhi[6] = {0};
+  WorldD view() const {
+    WorldD w;
+    w.n_obs = static_cast<int>(lo.size()) / (dw ? dw : 1);
+    w.lo = lo.data();
+    w.hi = hi.data();
+    for (int k = 0; k < 6; ++k) {
+      w.blo[k] = blo[k];
+      w.bhi[k] = bhi[k];
+    }
+    return w;
+  }
+};
+
+static bool point_free_h(const HostWorld& w, const double* y) {
+  bool r = false;
+  dispatch_dw(w.dw, [&]<int DW>() { r = point_free<DW>(w.view(), y); });
+  return r;
+}
+
+static bool nominal_free(const HostWorld& w, const std::vector<HWp>& t, double eps_cc) {  // pump.hpp:64-75
+  const int dw = w.dw;
+  for (const auto& p : t)
+    if (!point_free_h(w, p.p)) return false;
+  for (size_t j = 0; j + 1 < t.size(); ++j) {
+    const double h = t[j + 1].t - t[j].t;
+    if (h <= 0) continue;
+    HMotion m{};
+    std::memcpy(m.p0, t[j].p, sizeof(m.p0));
+    std::memcpy(m.v0, t[j].v, sizeof(m.v0));
+    std::memcpy(m.p1, t[j + 1].p, sizeof(m.p1));
+    std::memcpy(m.v1, t[j + 1].v, sizeof(m.v1));
+    m.tau = h;
+    fixed_time(m, dw);
+    bool hit = false;
+    dispatch_dw(dw, [&]<int DW>() { hit = motion_collides<DW>(as_motion<DW>(m), w.view(), eps_cc); });
+    if (hit) return false;
+  }
+  return true;
+}
+
+// ------------------------------------------------------------ path kernels
+// Walk parent pointers of selected plans and resolve each hop to its edge
+// (first edge v->u in the ascending row, as planner.hpp:297-302).
+__global__ void k_paths(int n_sel, const int32_t* sel, const int32_t* head, const int32_t* parent,
+                        const int64_t* row_ptr, const int32_t* e_to, int max_len, int32_t* nodes, int64_t* edges,
+                        int32_t* lens) {
+  const int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= n_sel) return;
+  int len = 0;
+  for (int id = sel[s]; id != -1 && len < max_len; id = parent[id]) nodes[static_cast<int64_t>(s) * max_len + len++] = head[id];
+  int32_t* nd = nodes + static_cast<int64_t>(s) * max_len;
+  for (int a = 0, b = len - 1; a < b; ++a, --b) {
+    const int t = nd[a];
+    nd[a] = nd[b];
+    nd[b] = t;
+  }
+  for (int h = 0; h + 1 < len; ++h) {
+    const int v = nd[h], u = nd[h + 1];
+    int64_t lo = row_ptr[v], hi = row_ptr[v + 1];  // first index with e_to >= u
+    while (lo < hi) {
+      const int64_t mid = (lo + hi) >> 1;
+      if (e_to[mid] < u)
+        lo = mid + 1;
+      else
+        hi = mid;
+    }
+    edges[static_cast<int64_t>(s) * max_len + h] = (lo < row_ptr[v + 1] && e_to[lo] == u) ? lo : -1;
+  }
+  lens[s] = len;
+}
+
+__global__ void k_gather_members(int n_goal, const int32_t* goal_nodes, const int64_t* mem_off,
+                                 const int64_t* out_off, const int32_t* ids, const double* cost, const double* cp,
+                                 int32_t* out_ids, double* out_cost, double* out_cp) {
+  const int g = blockIdx.x;
+  if (g >= n_goal) return;
+  const int v = goal_nodes[g];
+  const int64_t a = mem_off[v], o = out_off[g], m = out_off[g + 1] - out_off[g];
+  for (int64_t k = threadIdx.x; k < m; k += blockDim.x) {
+    const int id = ids[a + k];
+    out_ids[o + k] = id;
+    out_cost[o + k] = cost[id];
+    out_cp[o + k] = cp[id];
+  }
+}
+
+struct PathSet {
+  std::vector<std::vector<int>> nodes;
+  std::vector<std::vector<int64_t>> edges;
+};
+
+static PathSet resolve_paths(Ctx& c, const DevGraph& G, const DevExplore& X, const std::vector<int>& sel) {
+  PathSet ps;
+  const int ns = static_cast<int>(sel.size());
+  if (ns == 0) return ps;
+  const int max_len = 4096;
+  DBuf& d_sel = c.buf("p_sel", ns * 4 + 256);
+  DBuf& d_nodes = c.buf("p_nodes", static_cast<size_t>(ns) * max_len * 4 + 256);
+  DBuf& d_edges = c.buf("p_edges", static_cast<size_t>(ns) * max_len * 8 + 256);
+  DBuf& d_lens = c.buf("p_lens", ns * 4 + 256);
+  c.h2d(d_sel.p, sel.data(), ns * 4);
+  const DBuf& ids_src = X.head;
+  (void)ids_src;
+  k_paths<<<(ns + 127) / 128, 128, 0, c.stream>>>(ns, d_sel.as<int32_t>(), X.head.as<int32_t>(),
+                                                  X.parent.as<int32_t>(), G.row_ptr.as<int64_t>(), G.e_to.as<int32_t>(),
+                                                  max_len, d_nodes.as<int32_t>(), d_edges.as<int64_t>(),
+                                                  d_lens.as<int32_t>());
+  ++c.launches;
+  PUMP_CUDA(cudaGetLastError());
+  std::vector<int32_t> lens(ns), nodes(static_cast<size_t>(ns) * max_len);
+  std::vector<int64_t> edges(static_cast<size_t>(ns) * max_len);
+  c.d2h(lens.data(), d_lens.p, ns * 4);
+  c.d2h(nodes.data(), d_nodes.p, nodes.size() * 4);
+  c.d2h(edges.data(), d_edges.p, edges.size() * 8);
+  c.sync();
+  for (int s = 0; s < ns; ++s) {
+    ps.nodes.emplace_back(nodes.begin() + static_cast<int64_t>(s) * max_len,
+                          nodes.begin() + static_cast<int64_t>(s) * max_len + lens[s]);
+    ps.edges.emplace_back(edges.begin() + static_cast<int64_t>(s) * max_len,
+                          edges.begin() + static_cast<int64_t>(s) * max_len + std::max(0, lens[s] - 1));
+  }
+  return ps;
+}
+
+// path_trajectory (planner.hpp:292-315) from device edge data
+static std::vector<HWp> path_trajectory(Ctx& c, const DevGraph& G, const std::vector<int>& path,
+                                        const std::vector<int64_t>& edges) {
+  const int dw = G.dw;
+  std::vector<HWp> traj;
+  double offset = 0;
+  for (size_t j = 0; j + 1 < path.size(); ++j) {
+    const int64_t e = edges[j];
+    if (e < 0) throw std::logic_error("path_trajectory: missing edge");
+    HMotion m{};
+    double tau;
+    c.d2h(&tau, G.e_tau.as<double>() + e, 8);
+    c.d2h(m.a, G.e_acc0.as<double>() + e * dw, dw * 8);
+    c.d2h(m.j, G.e_jerk.as<double>() + e * dw, dw * 8);
+    c.sync();
+    m.tau = tau;
+    const int v = path[j], u = path[j + 1];
+    for (int k = 0; k < dw; ++k) {
+      m.p0[k] = G.h_pos[v * dw + k];
+      m.v0[k] = G.h_vel[v * dw + k];
+      m.p1[k] = G.h_pos[u * dw + k];
+      m.v1[k] = G.h_vel[u * dw + k];
+    }
+    auto wps = motion_waypoints(m, dw, G.dt);
+    for (size_t k = (j == 0 ? 0 : 1); k < wps.size(); ++k) {
+      HWp wp = wps[k];
+      wp.t += offset;
+      traj.push_back(wp);
+    }
+    offset += m.tau;
+  }
+  if (path.size() == 1) {
+    HWp w{};
+    for (int k = 0; k < dw; ++k) {
+      w.p[k] = G.h_pos[path[0] * dw + k];
+      w.v[k] = G.h_vel[path[0] * dw + k];
+    }
+    traj.push_back(w);
+  }
+  return traj;
+}
+
+// Batched MC over trajectories (rollouts [0, n_mc)); values = hits / n_mc
+static std::vector<double> mc_values(Ctx& c, const HostLoop& L, const DevWorld& w,
+                                     const std::vector<std::vector<HWp>>& trajs, int n_mc, uint64_t seed,
+                                     double eps_cc, double* mc_ms, int64_t* rollouts) {
+  const int dw = L.dw;
+  std::vector<int64_t> off(trajs.size() + 1, 0);
+  for (size_t j = 0; j < trajs.size(); ++j) off[j + 1] = off[j] + static_cast<int64_t>(trajs[j].size());
+  std::vector<double> y(static_cast<size_t>(off.back()) * dw);
+  int max_pts = 0;
+  for (size_t j = 0; j < trajs.size(); ++j) {
+    if (trajs[j].empty()) throw std::invalid_argument("mc_certify: empty trajectory");
+    max_pts = std::max<int>(max_pts, static_cast<int>(trajs[j].size()));
+    for (size_t t = 0; t < trajs[j].size(); ++t)
+      for (int k = 0; k < dw; ++k) y[(off[j] + t) * dw + k] = trajs[j][t].p[k];
+  }
+  const int nt = static_cast<int>(trajs.size());
+  DBuf& d_off = c.buf("r_mc_off", (nt + 1) * 8 + 256);
+  DBuf& d_y = c.buf("r_mc_y", y.size() * 8 + 256);
+  DBuf& d_h = c.buf("r_mc_hits", nt * 8 + 256);
+  c.h2d(d_off.p, off.data(), (nt + 1) * 8);
+  c.h2d(d_y.p, y.data(), y.size() * 8);
+  PUMP_CUDA(cudaMemsetAsync(d_h.p, 0, nt * 8, c.stream));
+  c.tic();
+  launch_mc(L, w, nt, d_off.as<int64_t>(), d_y.as<double>(), max_pts, 0, n_mc, seed, eps_cc,
+            d_h.as<unsigned long long>(), c.stream, &c.launches);
+  *mc_ms += c.toc();
+  *rollouts += static_cast<int64_t>(n_mc) * nt;
+  std::vector<int64_t> hits(nt);
+  c.d2h(hits.data(), d_h.p, nt * 8);
+  c.sync();
+  std::vector<double> v(nt);
+  for (int j = 0; j < nt; ++j) v[j] = static_cast<double>(hits[j]) / n_mc;
+  return v;
+}
+
+}  // namespace pumpg
+
+struct pump_result {
+  pump_result_summary s{};
+  std::vector<int32_t> path;
+  std::vector<double> pareto_cost, pareto_cp;
+  std::vector<int32_t> mc_ids;
+  std::vector<double> mc_vals;
+  std::vector<pumpg::HWp> traj;
+  int dw = 0;
+};
+
+namespace pumpg {
+
+static void graph_goal_nodes(DevGraph& G, const double* pos, const double* vel, const pump_goal* goal) {
+  const int dw = G.dw;
+  G.goal_nodes.clear();
+  for (int i = 0; i < G.n; ++i) {
+    bool in = true;
+    for (int k = 0; k < dw; ++k)
+      if (pos[i * dw + k] < goal->lo[k] || pos[i * dw + k] > goal->hi[k]) in = false;
+    if (in && std::sqrt(seq_sqn(vel + i * dw, dw)) <= goal->max_speed) G.goal_nodes.push_back(i);
+  }
+}
+
+static double scan_ratio(double tau_max) {  // steer.hpp:130-133 (host libm, as the reference)
+  const double tau_lo = tau_max * 1e-7;
+  return std::pow(tau_max / tau_lo, 1.0 / (64 - 1));
+}
+
+// sample_free (sample.hpp:56-89)
+static double halton(uint64_t index, int base) {
+  double f = 1.0, r = 0.0;
+  while (index > 0) {
+    f /= base;
+    r += f * (index % base);
+    index /= base;
+  }
+  return r;
+}
+
+static void halton_state(uint64_t index, const double* lo, const double* hi, int dw, double ms, double* p, double* v) {
+  static const int kPrimes[] = {2, 3, 5, 7, 11, 13, 17, 19, 23, 29, 31, 37};
+  for (int k = 0; k < dw; ++k) {
+    double u = halton(index, kPrimes[k]);
+    p[k] = lo[k] + u * (hi[k] - lo[k]);
+    double q = halton(index, kPrimes[dw + k]);
+    v[k] = -ms + q * 2 * ms;
+  }
+}
+
+static void sample_nodes(const pumpb::Scenario& s, const HostWorld& w, std::vector<double>& pos,
+                         std::vector<double>& vel) {
+  const int dw = s.workspace_dim();
+  pos.assign(s.start_pos.begin(), s.start_pos.end());
+  vel.assign(s.start_vel.begin(), s.start_vel.end());
+  auto goal_contains = [&](const double* p, const double* v) {
+    for (int k = 0; k < dw; ++k)
+      if (p[k] < s.goal.lo[k] || p[k] > s.goal.hi[k]) return false;
+    return std::sqrt(seq_sqn(v, dw)) <= s.goal_max_speed;
+  };
+  bool have_goal = false;
+  uint64_t index = 1;
+  int got = 0;
+  double p[6], v[6];
+  while (got < s.samples) {
+    halton_state(index++, s.workspace.bounds.lo.data(), s.workspace.bounds.hi.data(), dw, s.max_speed, p, v);
+    if (!point_free_h(w, p)) continue;
+    have_goal = have_goal || goal_contains(p, v);
+    pos.insert(pos.end(), p, p + dw);
+    vel.insert(vel.end(), v, v + dw);
+    ++got;
+  }
+  if (!have_goal) {
+    for (int k = 0; k < dw; ++k) {
+      p[k] = 0.5 * (s.goal.lo[k] + s.goal.hi[k]);
+      v[k] = 0.0;
+    }
+    if (point_free_h(w, p)) {
+      pos.insert(pos.end(), p, p + dw);
+      vel.insert(vel.end(), v, v + dw);
+    } else {
+      bool placed = false;
+      for (uint64_t gi = 1; gi <= 100000 && !placed; ++gi) {
+        halton_state(gi, s.goal.lo.data(), s.goal.hi.data(), dw, s.goal_max_speed, p, v);
+        if (std::sqrt(seq_sqn(v, dw)) > s.goal_max_speed) continue;
+        if (!point_free_h(w, p)) continue;
+        pos.insert(pos.end(), p, p + dw);
+        vel.insert(vel.end(), v, v + dw);
+        placed = true;
+      }
+      if (!placed) throw std::runtime_error("sample_free: goal region appears entirely in collision");
+    }
+  }
+}
+
+static HostWorld host_world(const pumpb::World& sw) {
+  HostWorld w;
+  w.dw = sw.dim();
+  for (int k = 0; k < w.dw; ++k) {
+    w.blo[k] = sw.bounds.lo[k];
+    w.bhi[k] = sw.bounds.hi[k];
+  }
+  for (const auto& b : sw.obstacles) {
+    w.lo.insert(w.lo.end(), b.lo.begin(), b.lo.end());
+    w.hi.insert(w.hi.end(), b.hi.begin(), b.hi.end());
+  }
+  return w;
+}
+
+static HostLoop loop_of(const pumpb::ClosedLoop& cl) {
+  HostLoop L;
+  L.d = cl.d;
+  L.dw = cl.dw;
+  L.F = cl.F.a;
+  L.Gv = cl.Gv.a;
+  L.Gw = cl.Gw.a;
+  L.Sv = cl.Sv.a;
+  L.Sw = cl.Sw.a;
+  L.S0 = cl.S0.a;
+  L.C = cl.C.a;
+  return L;
+}
+
+// run_pump (pump.hpp:170-263)
+static void run_pump_device(Ctx& c, const pumpb::Scenario& s, const DevGraph* prebuilt, pump_result& R) {
+  using clk = std::chrono::steady_clock;
+  auto secs = [](clk::time_point a, clk::time_point b) { return std::chrono::duration<double>(b - a).count(); };
+  const int dw = s.workspace_dim();
+  R.dw = dw;
+  pumpb::ModelBundle mb = s.models();
+  HostLoop L = loop_of(mb.cl);
+  const double eps_cc = s.effective_eps_cc();
+  const double r_n = s.effective_r_n();
+  HostWorld hw = host_world(s.workspace);
+  // upload the workspace once
+  pump_workspace pw{dw, static_cast<int32_t>(s.workspace.obstacles.size()), s.workspace.bounds.lo.data(),
+                    s.workspace.bounds.hi.data(), hw.lo.data(), hw.hi.data()};
+  DevWorld dwld = upload_world(c, &pw, "run_ws_");
+
+  auto t0 = clk::now();
+  DevGraph local;
+  const DevGraph* graph = prebuilt;
+  if (!graph) {
+    std::vector<double> pos, vel;
+    sample_nodes(s, hw, pos, vel);
+    const int n = static_cast<int>(pos.size()) / dw;
+    build_graph_device(local, c, n, dw, pos.data(), vel.data(), dwld, r_n, s.dt, eps_cc, s.effective_tau_max(),
+                       scan_ratio(s.effective_tau_max()));
+    pump_goal g{s.goal.lo.data(), s.goal.hi.data(), s.goal_max_speed};
+    local.h_pos = pos;
+    local.h_vel = vel;
+    graph_goal_nodes(local, pos.data(), vel.data(), &g);
+    graph = &local;
+  }
+  auto t1 = clk::now();
+  R.s.build_graph_seconds = secs(t0, t1);
+  R.s.n_edges = graph->E;
+
+  // bank + explore (the reference times the bank inside explore, pump.hpp:194-208)
+  {
+    const size_t bytes = static_cast<size_t>(s.bank_horizon + 1) * s.particles * dw * sizeof(double);
+    c.bank.ensure(bytes);
+    DBuf& scr = c.buf("bank_scratch", bank_scratch_bytes(L, s.particles, s.bank_horizon));
+    c.tic();
+    launch_bank(L, s.particles, s.bank_horizon, s.seeds.bank, c.bank.as<double>(), scr.p, c.stream, &c.launches);
+    R.s.bank_ms = c.toc();
+    c.bank_n = s.particles;
+    c.bank_horizon = s.bank_horizon;
+    c.bank_dw = dw;
+  }
+  DevExplore X;
+  const double eta = s.effective_eta();
+  ExploreArgs ea{s.alpha / eta, std::min(1.0, eta * s.alpha), s.lambda, r_n};
+  run_explore_device(X, c, *graph, ea);
+  auto t2 = clk::now();
+  R.s.explore_seconds = secs(t1, t2);
+  R.s.explore_kernel_ms = X.kernel_ms;
+  R.s.partial_plans = X.partial_plans;
+  R.s.termination = X.termination;
+  R.s.n_plans = X.n_plans;
+
+  // goal plans = concat over goal nodes (ascending) of pareto[v] (planner.hpp:264-265)
+  std::vector<int32_t> gids;
+  std::vector<double> gcost, gcp;
+  {
+    const int ng = static_cast<int>(graph->goal_nodes.size());
+    std::vector<int32_t> cnt(graph->n);
+    c.d2h(cnt.data(), X.mem_cnt.p, graph->n * 4);
+    c.sync();
+    std::vector<int64_t> goff(ng + 1, 0);
+    for (int g = 0; g < ng; ++g) goff[g + 1] = goff[g] + cnt[graph->goal_nodes[g]];
+    const int64_t total = goff[ng];
+    if (total > 0) {
+      DBuf& d_gn = c.buf("r_gn", ng * 4 + 256);
+      DBuf& d_go = c.buf("r_go", (ng + 1) * 8 + 256);
+      DBuf& d_id = c.buf("r_gid", total * 4 + 256);
+      DBuf& d_c = c.buf("r_gc", total * 8 + 256);
+      DBuf& d_p = c.buf("r_gp", total * 8 + 256);
+      c.h2d(d_gn.p, graph->goal_nodes.data(), ng * 4);
+      c.h2d(d_go.p, goff.data(), (ng + 1) * 8);
+      const DBuf& ids = X.mem_flip ? X.mem_b : X.mem_a;
+      k_gather_members<<<ng, 128, 0, c.stream>>>(ng, d_gn.as<int32_t>(), X.mem_off.as<int64_t>(),
+                                                 d_go.as<int64_t>(), ids.as<int32_t>(), X.cost.as<double>(),
+                                                 X.cp.as<double>(), d_id.as<int32_t>(), d_c.as<double>(),
+                                                 d_p.as<double>());
+      ++c.launches;
+      gids.resize(total);
+      gcost.resize(total);
+      gcp.resize(total);
+      c.d2h(gids.data(), d_id.p, total * 4);
+      c.d2h(gcost.data(), d_c.p, total * 8);
+      c.d2h(gcp.data(), d_p.p, total * 8);
+      c.sync();
+    }
+  }
+  // global front (pump.hpp:212-235)
+  std::vector<int> order(gids.size());
+  std::iota(order.begin(), order.end(), 0);
+  std::stable_sort(order.begin(), order.end(), [&](int a, int b) {
+    if (gcost[a] != gcost[b]) return gcost[a] < gcost[b];
+    if (gcp[a] != gcp[b]) return gcp[a] < gcp[b];
+    return gids[a] < gids[b];
+  });
+  std::vector<int> front;  // indices into gids
+  double min_cp = std::numeric_limits<double>::infinity();
+  for (int k : order)
+    if (gcp[k] < min_cp) {
+      front.push_back(k);
+      min_cp = gcp[k];
+    }
+  for (int k : front) {
+    R.pareto_cost.push_back(gcost[k]);
+    R.pareto_cp.push_back(gcp[k]);
+  }
+  std::vector<int> sorted_ids;  // ascending cp_hat
+  for (auto it = front.rbegin(); it != front.rend(); ++it) sorted_ids.push_back(gids[*it]);
+
+  // Alg. 4 bisection (pump.hpp:23-51): every front plan is certified in one
+  // batched MC launch (speculatively), then the bisection is replayed from
+  // the memo so mc_evaluations lists exactly the probes the reference makes.
+  PathSet ps = resolve_paths(c, *graph, X, sorted_ids);
+  std::vector<std::vector<HWp>> trajs;
+  for (size_t k = 0; k < sorted_ids.size(); ++k) trajs.push_back(path_trajectory(c, *graph, ps.nodes[k], ps.edges[k]));
+  std::vector<double> memo = trajs.empty() ? std::vector<double>{}
+                                           : mc_values(c, L, dwld, trajs, s.mc_samples, s.seeds.mc, eps_cc,
+                                                       &R.s.mc_ms, &R.s.mc_rollouts);
+  const int nf = static_cast<int>(sorted_ids.size());
+  std::vector<char> seen(nf, 0);
+  auto eval = [&](int m) {
+    if (!seen[m - 1]) {
+      seen[m - 1] = 1;
+      R.mc_ids.push_back(sorted_ids[m - 1]);
+      R.mc_vals.push_back(memo[m - 1]);
+    }
+    return memo[m - 1];
+  };
+  bool success = false;
+  int sel = -1;
+  if (nf > 0) {
+    int l = 1, u = nf;
+    while (l < u) {
+      const int m = (l + u + 1) / 2;
+      if (eval(m) > s.alpha)
+        u = m - 1;
+      else
+        l = m;
+    }
+    if (!(eval(l) > s.alpha)) {
+      success = true;
+      sel = l - 1;
+    }
+  }
+  if (!success) {
+    R.s.selection_seconds = secs(t2, clk::now());
+    R.s.success = 0;
+    return;
+  }
+  const int sel_id = sorted_ids[sel];
+  R.path.assign(ps.nodes[sel].begin(), ps.nodes[sel].end());
+  {
+    double cph, cst;
+    c.d2h(&cph, X.cp.as<double>() + sel_id, 8);
+    c.d2h(&cst, X.cost.as<double>() + sel_id, 8);
+    c.sync();
+    R.s.cp_hat = cph;
+    R.s.pre_smoothing_cost = cst;
+  }
+  // smoothing (pump.hpp:84-146)
+  const std::vector<HWp>& plan = trajs[sel];
+  std::vector<HWp> best = plan;
+  double best_cost = trajectory_cost(plan, dw), best_mc = memo[sel], best_s = 0;
+  if (plan.size() >= 2) {
+    HMotion opt{};
+    std::memcpy(opt.p0, plan.front().p, sizeof(opt.p0));
+    std::memcpy(opt.v0, plan.front().v, sizeof(opt.v0));
+    std::memcpy(opt.p1, plan.back().p, sizeof(opt.p1));
+    std::memcpy(opt.v1, plan.back().v, sizeof(opt.v1));
+    opt.tau = plan.back().t;
+    fixed_time(opt, dw);
+    auto blend = [&](double sv) {
+      std::vector<HWp> t(plan.size());
+      for (size_t q = 0; q < plan.size(); ++q) {
+        const HWp& wp = plan[q];
+        HWp& b = t[q];
+        b = HWp{};
+        b.t = wp.t;
+        double op[6], ov[6], ou[6];
+        state_at(opt, dw, wp.t, op, ov);
+        control_at(opt, dw, wp.t, ou);
+        for (int k = 0; k < dw; ++k) {
+          b.p[k] = (1 - sv) * wp.p[k] + sv * op[k];
+          b.v[k] = (1 - sv) * wp.v[k] + sv * ov[k];
+          b.u[k] = (1 - sv) * wp.u[k] + sv * ou[k];
+        }
+      }
+      return t;
+    };
+    auto certify = [&](const std::vector<HWp>& t, double& mc_out) {
+      if (!nominal_free(hw, t, eps_cc)) return false;
+      mc_out = mc_values(c, L, dwld, {t}, s.mc_samples, s.seeds.mc, eps_cc, &R.s.mc_ms, &R.s.mc_rollouts)[0];
+      return mc_out <= s.alpha;
+    };
+    auto accept = [&](double sv, const std::vector<HWp>& t, double mc) {
+      best = t;
+      best_cost = trajectory_cost(t, dw);
+      best_mc = mc;
+      best_s = sv;
+    };
+    bool done = false;
+    {
+      auto t = blend(1.0);
+      double mc;
+      if (certify(t, mc)) {
+        accept(1.0, t, mc);
+        done = true;
+      }
+    }
+    if (!done) {
+      double lo = 0, hi = 1;
+      for (int it = 0; it < 10; ++it) {
+        const double mid = 0.5 * (lo + hi);
+        auto t = blend(mid);
+        double mc;
+        if (certify(t, mc)) {
+          accept(mid, t, mc);
+          lo = mid;
+        } else {
+          hi = mid;
+        }
+      }
+    }
+  }
+  R.traj = best;
+  R.s.cost = best_cost;
+  R.s.certified_cp = best_mc;
+  R.s.smoothing_s = best_s;
+  R.s.success = 1;
+  R.s.selection_seconds = secs(t2, clk::now());
+}
+
+}  // namespace pumpg
+
+extern "C" {
+
+// ------------------------------------------------------------------ graph
+int pump_build_graph(pump_ctx* ctx, int32_t n_nodes, int32_t dw, const double* pos, const double* vel,
+                     const pump_workspace* ws, const pump_goal* goal, double r_n, double dt, double eps_cc,
+                     double tau_max, pump_graph** out) {
+  return guard([&] {
+    Ctx& c = ctx->c;
+    if (!ws || ws->dw != dw) throw std::invalid_argument("build_graph: workspace dimension mismatch");
+    if (r_n <= 0) throw std::invalid_argument("build_graph: r_n must be positive");
+    DevWorld w = upload_world(c, ws, "g_ws_");
+    auto* g = new pump_graph;
+    try {
+      g->owner = ctx;
+      build_graph_device(g->g, c, n_nodes, dw, pos, vel, w, r_n, dt, eps_cc, tau_max, scan_ratio(tau_max));
+      g->g.h_pos.assign(pos, pos + static_cast<size_t>(n_nodes) * dw);
+      g->g.h_vel.assign(vel, vel + static_cast<size_t>(n_nodes) * dw);
+      graph_goal_nodes(g->g, pos, vel, goal);
+    } catch (...) {
+      delete g;
+      throw;
+    }
+    *out = g;
+  });
+}
+
+int pump_graph_upload(pump_ctx* ctx, const pump_graph_view* v, pump_graph** out) {
+  return guard([&] {
+    Ctx& c = ctx->c;
+    auto* gp = new pump_graph;
+    DevGraph& G = gp->g;
+    try {
+      gp->owner = ctx;
+      const int n = v->n_nodes, dw = v->dw;
+      const int64_t E = v->n_edges, NW = v->n_waypoints, H = v->n_halfspaces;
+      G.n = n;
+      G.dw = dw;
+      G.r_n = v->r_n;
+      G.dt = v->dt;
+      G.E = E;
+      G.NW = NW;
+      G.H = H;
+      auto up = [&](DBuf& b, const void* src, size_t bytes) {
+        b.ensure(bytes + 256);
+        c.h2d(b.p, src, bytes);
+      };
+      up(G.pos, v->node_pos, n * dw * 8);
+      up(G.vel, v->node_vel, n * dw * 8);
+      up(G.row_ptr, v->row_ptr, (n + 1) * 8);
+      up(G.e_to, v->edge_to, E * 4);
+      up(G.e_cost, v->edge_cost, E * 8);
+      up(G.e_tau, v->edge_tau, E * 8);
+      up(G.e_acc0, v->edge_acc0, E * dw * 8);
+      up(G.e_jerk, v->edge_jerk, E * dw * 8);
+      up(G.e_nsteps, v->edge_nsteps, E * 4);
+      up(G.wp_off, v->edge_wp_off, (E + 1) * 8);
+      up(G.hs_off, v->wp_hs_off, (NW + 1) * 8);
+      up(G.hs_a, v->hs_a, H * dw * 8);
+      up(G.hs_b, v->hs_b, H * 8);
+      G.hs_fb.ensure(H + 256);
+      if (v->hs_fallback) c.h2d(G.hs_fb.p, v->hs_fallback, H);
+      std::vector<int32_t> from(E);
+      for (int i = 0; i < n; ++i)
+        for (int64_t e = v->row_ptr[i]; e < v->row_ptr[i + 1]; ++e) from[e] = i;
+      up(G.e_from, from.data(), E * 4);
+      G.goal_nodes.assign(v->goal_nodes, v->goal_nodes + v->n_goal);
+      G.h_pos.assign(v->node_pos, v->node_pos + static_cast<size_t>(n) * dw);
+      G.h_vel.assign(v->node_vel, v->node_vel + static_cast<size_t>(n) * dw);
+      c.sync();
+    } catch (...) {
+      delete gp;
+      throw;
+    }
+    *out = gp;
+  });
+}
+
+int pump_graph_counts(const pump_graph* g, pump_graph_view* v) {
+  return guard([&] {
+    const DevGraph& G = g->g;
+    v->n_nodes = G.n;
+    v->dw = G.dw;
+    v->n_edges = G.E;
+    v->n_waypoints = G.NW;
+    v->n_halfspaces = G.H;
+    v->n_goal = static_cast<int32_t>(G.goal_nodes.size());
+    v->r_n = G.r_n;
+    v->dt = G.dt;
+  });
+}
+
+int pump_graph_export(const pump_graph* g, pump_graph_view* v) {
+  return guard([&] {
+    Ctx& c = g->owner->c;
+    const DevGraph& G = g->g;
+    const int n = G.n, dw = G.dw;
+    auto dn = [&](void* dst, const DBuf& b, size_t bytes) {
+      if (dst && bytes) c.d2h(dst, b.p, bytes);
+    };
+    if (v->node_pos) std::memcpy(v->node_pos, G.h_pos.data(), n * dw * 8);
+    if (v->node_vel) std::memcpy(v->node_vel, G.h_vel.data(), n * dw * 8);
+    dn(v->row_ptr, G.row_ptr, (n + 1) * 8);
+    dn(v->edge_to, G.e_to, G.E * 4);
+    dn(v->edge_cost, G.e_cost, G.E * 8);
+    dn(v->edge_tau, G.e_tau, G.E * 8);
+    dn(v->edge_acc0, G.e_acc0, G.E * dw * 8);
+    dn(v->edge_jerk, G.e_jerk, G.E * dw * 8);
+    dn(v->edge_nsteps, G.e_nsteps, G.E * 4);
+    dn(v->edge_wp_off, G.wp_off, (G.E + 1) * 8);
+    dn(v->wp_hs_off, G.hs_off, (G.NW + 1) * 8);
+    dn(v->hs_a, G.hs_a, G.H * dw * 8);
+    dn(v->hs_b, G.hs_b, G.H * 8);
+    dn(v->hs_fallback, G.hs_fb, G.H);
+    if (v->goal_nodes) std::memcpy(v->goal_nodes, G.goal_nodes.data(), G.goal_nodes.size() * 4);
+    c.sync();
+  });
+}
+
+int pump_graph_free(pump_graph* g) {
+  delete g;
+  return PUMP_OK;
+}
+
+// ---------------------------------------------------------------- explore
+int pump_explore_run(pump_ctx* ctx, const pump_graph* g, const pump_explore_params* p, pump_explore** out) {
+  return guard([&] {
+    auto* e = new pump_explore;
+    try {
+      ExploreArgs a{p->alpha_min, p->alpha_max, p->lambda, p->r_n};
+      run_explore_device(e->x, ctx->c, g->g, a);
+      e->owner = ctx;
+      e->goal_nodes = g->g.goal_nodes;
+    } catch (...) {
+      delete e;
+      throw;
+    }
+    *out = e;
+  });
+}
+
+int pump_explore_counts(const pump_explore* e, pump_explore_view* v) {
+  return guard([&] {
+    const DevExplore& X = e->x;
+    Ctx& c = e->owner->c;
+    v->n_plans = X.n_plans;
+    v->n_words = X.W;
+    v->n_nodes = X.n;
+    std::vector<int32_t> cnt(X.n);
+    c.d2h(cnt.data(), X.mem_cnt.p, X.n * 4);
+    c.sync();
+    int64_t tot = 0;
+    for (int x : cnt) tot += x;
+    v->n_pareto = tot;
+    v->n_goal_plans = 0;
+    for (int gnode : e->goal_nodes) v->n_goal_plans += cnt[gnode];
+    v->partial_plans = X.partial_plans;
+    v->discarded_cp = X.disc_cp;
+    v->removed_dominated = X.removed;
+    v->discarded_horizon = X.disc_hor;
+    v->rounds = X.rounds;
+    v->termination = X.termination;
+  });
+}
+
+int pump_explore_export(const pump_explore* e, pump_explore_view* v) {
+  return guard([&] {
+    const DevExplore& X = e->x;
+    Ctx& c = e->owner->c;
+    const int64_t P = X.n_plans;
+    auto dn = [&](void* dst, const DBuf& b, size_t bytes) {
+      if (dst && bytes) c.d2h(dst, b.p, bytes);
+    };
+    dn(v->head, X.head, P * 4);
+    dn(v->parent, X.parent, P * 4);
+    dn(v->cost, X.cost, P * 8);
+    dn(v->cp_hat, X.cp, P * 8);
+    dn(v->t_end, X.t_end, P * 4);
+    dn(v->masks, X.mask, P * X.W * 8);
+    std::vector<int32_t> cnt(X.n);
+    std::vector<int64_t> off(X.n + 1);
+    c.d2h(cnt.data(), X.mem_cnt.p, X.n * 4);
+    c.d2h(off.data(), X.mem_off.p, (X.n + 1) * 8);
+    c.sync();
+    const DBuf& ids = X.mem_flip ? X.mem_b : X.mem_a;
+    const int64_t span = off[X.n];
+    std::vector<int32_t> all(span + 1);
+    if (span > 0) c.d2h(all.data(), ids.p, span * 4);
+    c.sync();
+    int64_t o = 0;
+    if (v->pareto_ptr) v->pareto_ptr[0] = 0;
+    for (int i = 0; i < X.n; ++i) {
+      for (int k = 0; k < cnt[i]; ++k) {
+        if (v->pareto_ids) v->pareto_ids[o] = all[off[i] + k];
+        ++o;
+      }
+      if (v->pareto_ptr) v->pareto_ptr[i + 1] = o;
+    }
+    int64_t q = 0;
+    for (int gnode : e->goal_nodes)
+      for (int k = 0; k < cnt[gnode]; ++k) {
+        if (v->goal_plans) v->goal_plans[q] = all[off[gnode] + k];
+        ++q;
+      }
+  });
+}
+
+int pump_explore_free(pump_explore* e) {
+  delete e;
+  return PUMP_OK;
+}
+
+// ------------------------------------------------------------- pipeline
+int pump_run(pump_ctx* ctx, const pump_scenario* s, const pump_graph* prebuilt, pump_result** out) {
+  return guard([&] {
+    auto* r = new pump_result;
+    try {
+      run_pump_device(ctx->c, s->s, prebuilt ? &prebuilt->g : nullptr, *r);
+      r->s.path_len = static_cast<int32_t>(r->path.size());
+      r->s.n_pareto = static_cast<int32_t>(r->pareto_cost.size());
+      r->s.n_mc_evals = static_cast<int32_t>(r->mc_ids.size());
+      r->s.n_traj_points = static_cast<int32_t>(r->traj.size());
+      r->s.dw = r->dw;
+    } catch (...) {
+      delete r;
+      throw;
+    }
+    *out = r;
+  });
+}
+
+int pump_result_summary_get(const pump_result* r, pump_result_summary* out) {
+  *out = r->s;
+  return PUMP_OK;
+}
+
+int pump_result_arrays(const pump_result* r, int32_t* path, double* pc, double* pcp, int32_t* ids, double* mcs,
+                       double* tt, double* tp, double* tv, double* tu) {
+  const int dw = r->dw;
+  if (path) std::copy(r->path.begin(), r->path.end(), path);
+  if (pc) std::copy(r->pareto_cost.begin(), r->pareto_cost.end(), pc);
+  if (pcp) std::copy(r->pareto_cp.begin(), r->pareto_cp.end(), pcp);
+  if (ids) std::copy(r->mc_ids.begin(), r->mc_ids.end(), ids);
+  if (mcs) std::copy(r->mc_vals.begin(), r->mc_vals.end(), mcs);
+  for (size_t i = 0; i < r->traj.size(); ++i) {
+    if (tt) tt[i] = r->traj[i].t;
+    for (int k = 0; k < dw; ++k) {
+      if (tp) tp[i * dw + k] = r->traj[i].p[k];
+      if (tv) tv[i * dw + k] = r->traj[i].v[k];
+      if (tu) tu[i * dw + k] = r->traj[i].u[k];
+    }
+  }
+  return PUMP_OK;
+}
+
+int pump_result_free(pump_result* r) {
+  delete r;
+  return PUMP_OK;
+}
+
+}  // extern "C"

@@ -92,7 +92,7 @@ __device__ __forceinline__ void cl_step(const LoopP<D, DW>& L, double (&z)[2 * D
 // ----------------------------------------------------------- geometry
 // closed AABB containment (geom.hpp:19-23)
 template <int DW>
-__device__ __forceinline__ bool box_contains(const double* lo, const double* hi, const double* p) {
+__host__ __device__ __forceinline__ bool box_contains(const double* lo, const double* hi, const double* p) {
   bool in = true;
 #pragma unroll
   for (int k = 0; k < DW; ++k) in = in && !(p[k] < lo[k] || p[k] > hi[k]);
@@ -108,7 +108,7 @@ struct WorldD {
 };
 
 template <int DW>
-__device__ __forceinline__ bool point_free(const WorldD& w, const double* y) {  // geom.hpp:56-61
+__host__ __device__ __forceinline__ bool point_free(const WorldD& w, const double* y) {  // geom.hpp:56-61
   if (!box_contains<DW>(w.blo, w.bhi, y)) return false;
   for (int o = 0; o < w.n_obs; ++o)
     if (box_contains<DW>(w.lo + o * DW, w.hi + o * DW, y)) return false;
@@ -117,12 +117,12 @@ __device__ __forceinline__ bool point_free(const WorldD& w, const double* y) {  
 
 // slab test, closed box (geom.hpp:64-80)
 template <int DW>
-__device__ __forceinline__ bool segment_hits(const double* p0, const double* p1, const double* lo, const double* hi) {
+__host__ __device__ __forceinline__ bool segment_hits(const double* p0, const double* p1, const double* lo, const double* hi) {
   double tmin = 0.0, tmax = 1.0;
 #pragma unroll
   for (int k = 0; k < DW; ++k) {
     double d = p1[k] - p0[k];
-    if (fabs(d) < 1e-300) {
+    if ((d < 0 ? -d : d) < 1e-300) {
       if (p0[k] < lo[k] || p0[k] > hi[k]) return false;
       continue;
     }
@@ -141,14 +141,14 @@ __device__ __forceinline__ bool segment_hits(const double* p0, const double* p1,
 }
 
 template <int DW>
-__device__ __forceinline__ bool segment_collides(const WorldD& w, const double* p0, const double* p1) {
+__host__ __device__ __forceinline__ bool segment_collides(const WorldD& w, const double* p0, const double* p1) {
   for (int o = 0; o < w.n_obs; ++o)
     if (segment_hits<DW>(p0, p1, w.lo + o * DW, w.hi + o * DW)) return true;
   return false;
 }
 
 template <int N>
-__device__ __forceinline__ double sqnorm(const double* x) {
+__host__ __device__ __forceinline__ double sqnorm(const double* x) {
   double s = 0.0;
 #pragma unroll
   for (int k = 0; k < N; ++k) s = s + x[k] * x[k];
@@ -164,7 +164,7 @@ struct MotionD {
 };
 
 template <int DW>
-__device__ __forceinline__ void motion_pos(const MotionD<DW>& m, double s, double* out) {
+__host__ __device__ __forceinline__ void motion_pos(const MotionD<DW>& m, double s, double* out) {
   if (s <= 0) {
 #pragma unroll
     for (int k = 0; k < DW; ++k) out[k] = m.p0[k];
@@ -180,7 +180,7 @@ __device__ __forceinline__ void motion_pos(const MotionD<DW>& m, double s, doubl
 }
 
 template <int DW>
-__device__ __forceinline__ void motion_state(const MotionD<DW>& m, double s, double* pos, double* vel) {
+__host__ __device__ __forceinline__ void motion_state(const MotionD<DW>& m, double s, double* pos, double* vel) {
   if (s <= 0) {
 #pragma unroll
     for (int k = 0; k < DW; ++k) {
@@ -206,7 +206,7 @@ __device__ __forceinline__ void motion_state(const MotionD<DW>& m, double s, dou
 
 // c(tau) (steer.hpp:84-94)
 template <int DW>
-__device__ __forceinline__ double steer_cost(const double* ap, const double* av, const double* bp, const double* bv,
+__host__ __device__ __forceinline__ double steer_cost(const double* ap, const double* av, const double* bp, const double* bv,
                                              double tau) {
   double c = tau;
 #pragma unroll
@@ -216,6 +216,50 @@ __device__ __forceinline__ double steer_cost(const double* ap, const double* av,
     c += 12 * dp * dp / (tau * tau * tau) - 12 * dp * dv / (tau * tau) + 4 * dv * dv / tau;
   }
   return c;
+}
+
+// motion_collides (geom.hpp:96-123): adaptive midpoint bisection until the
+// chord is <= eps_cc (or the span < 1e-9 s), exact segment test at leaves.
+// Iterative DFS over (t0, t1) spans; endpoints are recomputed with the same
+// polynomial so they carry the same bits the reference stores.  The result
+// is an OR over a fixed tree of tests, so traversal order cannot change it.
+template <int DW>
+__host__ __device__ inline bool motion_collides(const MotionD<DW>& m, const WorldD& w, double eps_cc) {
+  double p0[DW], p1[DW];
+  motion_pos<DW>(m, 0.0, p0);
+  if (!point_free<DW>(w, p0)) return true;
+  if (m.tau <= 0) return false;
+  motion_pos<DW>(m, m.tau, p1);
+  if (!point_free<DW>(w, p1)) return true;
+  double st0[64], st1[64];
+  int sp = 0;
+  double t0 = 0.0, t1 = m.tau;
+  while (true) {
+    double diff[DW];
+#pragma unroll
+    for (int k = 0; k < DW; ++k) diff[k] = p1[k] - p0[k];
+    if (sqrt(sqnorm<DW>(diff)) <= eps_cc || t1 - t0 < 1e-9) {
+      if (segment_collides<DW>(w, p0, p1)) return true;
+      if (sp == 0) return false;
+      --sp;
+      t0 = st0[sp];
+      t1 = st1[sp];
+      motion_pos<DW>(m, t0, p0);
+      motion_pos<DW>(m, t1, p1);
+      continue;
+    }
+    const double tm = 0.5 * (t0 + t1);
+    double pm[DW];
+    motion_pos<DW>(m, tm, pm);
+    if (!point_free<DW>(w, pm)) return true;
+    if (sp >= 64) return true;  // unreachable: depth is bounded by t1 - t0 >= 1e-9
+    st0[sp] = tm;
+    st1[sp] = t1;
+    ++sp;
+    t1 = tm;
+#pragma unroll
+    for (int k = 0; k < DW; ++k) p1[k] = pm[k];
+  }
 }
 
 }  // namespace pumpg

@@ -1,0 +1,718 @@
+// Explore wavefront (planner.hpp:74-267) on one B200.
+//
+// One round = one group B of open plans (sorted by (bucket, id)) expanded
+// along every outgoing edge.  Device pipeline per round, one host sync:
+//   k_expand      warp per (plan, edge) task: cost/t_end, horizon discard,
+//                 HSMC over the edge's waypoints (ballot kill masks), keep =
+//                 cp < alpha_max                         (planner.hpp:154-177)
+//   scan + k_commit   kept candidates get arena ids in task order; goal
+//                 bookkeeping; newcomers counted per head (planner.hpp:180-196)
+//   k_relayout / k_place_new   per-node Pareto member segments rebuilt
+//   k_dom         CTA per touched node: drop newcomers dominated by any member
+//                 (old or new), evict old members (!= root) dominated by a
+//                 surviving newcomer                     (planner.hpp:198-242)
+//   scan + k_pool_append  surviving newcomers enter the open pool in id order
+//   k_pool_min / k_round_i   next threshold i (skipping empty thresholds)
+//   k_select + multisplit    next group = open pool entries with bucket <=
+//                 min(i, nb-1), stably ordered by (bucket, id) (:248-261)
+//   k_group_post + scan      task offsets (degree prefix sum) of the group
+// The arena, member segments, pool and group stay resident in HBM.
+#include <climits>
+
+#include "dispatch.cuh"
+#include "explore.h"
+#include "scan.cuh"
+
+namespace pumpg {
+
+constexpr int kOpen = 1;
+
+DevExplore::~DevExplore() {
+  if (status_h) cudaFreeHost(status_h);
+}
+
+struct ExpandArgs {
+  const int32_t* group;
+  const int64_t* task_off;
+  const int64_t* d_G;
+  const int64_t* d_T;
+  const int64_t* row_ptr;
+  const int32_t* e_to;
+  const double* e_cost;
+  const int32_t* e_nsteps;
+  const int64_t* wp_off;
+  const int64_t* hs_off;
+  const double* hs_a;
+  const double* hs_b;
+  const int32_t* head;
+  const double* cost;
+  const int32_t* t_end;
+  const uint64_t* mask;
+  const double* dy;
+  int N, horizon, W;
+  double alpha_max;
+  uint8_t* keep;
+  int32_t* c_head;
+  int32_t* c_src;
+  int32_t* c_tend;
+  double* c_cost;
+  double* c_cp;
+  uint64_t* c_mask;
+  ExploreStatus* st;
+};
+
+template <int DW, int CH>
+__global__ void __launch_bounds__(256) k_expand(const ExpandArgs a) {
+  const int64_t task = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  const int64_t T = *a.d_T;
+  if (task >= T) return;
+  const int64_t G = *a.d_G;
+  int64_t lo = 0, hi = G;  // largest g with task_off[g] <= task
+  while (hi - lo > 1) {
+    const int64_t mid = (lo + hi) >> 1;
+    if (a.task_off[mid] <= task)
+      lo = mid;
+    else
+      hi = mid;
+  }
+  const int pid = a.group[lo];
+  const int hv = a.head[pid];
+  const int64_t e = a.row_ptr[hv] + (task - a.task_off[lo]);
+  const double cc = a.cost[pid] + a.e_cost[e];
+  const int pt = a.t_end[pid];
+  const int ns = a.e_nsteps[e];
+  const int te = pt + ns;
+  if (lane == 0) {
+    a.c_head[task] = a.e_to[e];
+    a.c_src[task] = pid;
+    a.c_cost[task] = cc;
+    a.c_tend[task] = te;
+  }
+  if (te > a.horizon) {  // planner.hpp:164-168
+    if (lane == 0) {
+      a.keep[task] = 0;
+      a.c_cp[task] = 2.0;
+      atomicAdd(reinterpret_cast<unsigned long long*>(&a.st->disc_hor), 1ull);
+    }
+    return;
+  }
+  bool kill[CH];
+#pragma unroll
+  for (int c = 0; c < CH; ++c) kill[c] = false;
+  const int64_t w0 = a.wp_off[e];
+  for (int j = 0; j < ns; ++j) {
+    const int64_t h0 = a.hs_off[w0 + j], h1 = a.hs_off[w0 + j + 1];
+    if (h0 == h1) continue;
+    const double* row = a.dy + static_cast<int64_t>(pt + j + 1) * a.N * DW;
+    double p[CH][DW];
+#pragma unroll
+    for (int c = 0; c < CH; ++c) {
+      const int i = c * 32 + lane;
+#pragma unroll
+      for (int k = 0; k < DW; ++k) p[c][k] = (i < a.N) ? row[i * DW + k] : 0.0;
+    }
+    for (int64_t h = h0; h < h1; ++h) {
+      double av[DW];
+#pragma unroll
+      for (int k = 0; k < DW; ++k) av[k] = a.hs_a[h * DW + k];
+      const double b = a.hs_b[h];
+#pragma unroll
+      for (int c = 0; c < CH; ++c) {
+        double s = 0;
+#pragma unroll
+        for (int k = 0; k < DW; ++k) s += av[k] * p[c][k];
+        kill[c] = kill[c] || (s > b);
+      }
+    }
+  }
+  int pop = 0;
+#pragma unroll
+  for (int w = 0; w < (CH + 1) / 2; ++w) {
+    const unsigned lo32 = __ballot_sync(0xffffffffu, kill[2 * w]);
+    const unsigned hi32 = (2 * w + 1 < CH) ? __ballot_sync(0xffffffffu, kill[2 * w + 1]) : 0u;
+    if (w < a.W) {
+      const uint64_t m = a.mask[static_cast<int64_t>(pid) * a.W + w] & ~((static_cast<uint64_t>(hi32) << 32) | lo32);
+      pop += __popcll(m);
+      if (lane == 0) a.c_mask[task * a.W + w] = m;
+    }
+  }
+  if (lane == 0) {
+    const double cp = 1.0 - static_cast<double>(pop) / a.N;  // ParticleMask::cp (cp.hpp:42)
+    a.c_cp[task] = cp;
+    const bool keep = cp < a.alpha_max;
+    a.keep[task] = keep ? 1 : 0;
+    if (!keep) atomicAdd(reinterpret_cast<unsigned long long*>(&a.st->disc_cp), 1ull);
+  }
+}
+
+struct CommitArgs {
+  const int64_t* d_T;
+  const uint8_t* keep;
+  const int64_t* rank;
+  const int32_t* c_head;
+  const int32_t* c_src;
+  const int32_t* c_tend;
+  const double* c_cost;
+  const double* c_cp;
+  const uint64_t* c_mask;
+  int W;
+  double width, alpha_min;
+  const uint8_t* is_goal;
+  int32_t* head;
+  int32_t* parent;
+  double* cost;
+  double* cp;
+  int32_t* t_end;
+  uint64_t* mask;
+  int32_t* bucket;
+  uint8_t* flags;
+  int32_t* new_cnt;
+  int32_t* new_slot;
+  int32_t* touched;
+  ExploreStatus* st;
+};
+
+__global__ void k_commit(const CommitArgs a) {
+  const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (t >= *a.d_T || !a.keep[t]) return;
+  const int64_t P0 = a.st->n_plans;
+  const int64_t r = a.rank[t];
+  const int64_t id = P0 + r;
+  const int hv = a.c_head[t];
+  const double c = a.c_cost[t];
+  const double q = a.c_cp[t];
+  a.head[id] = hv;
+  a.parent[id] = a.c_src[t];
+  a.cost[id] = c;
+  a.cp[id] = q;
+  a.t_end[id] = a.c_tend[t];
+  for (int w = 0; w < a.W; ++w) a.mask[id * a.W + w] = a.c_mask[t * a.W + w];
+  int b = static_cast<int>(ceil(c / a.width - 1e-12));  // planner.hpp:86
+  a.bucket[id] = b < 0 ? 0 : b;
+  a.flags[id] = 0;
+  if (a.is_goal[hv] && q < a.alpha_min)  // note_goal (planner.hpp:95-98)
+    atomicMin(&a.st->best_goal_bits, __double_as_longlong(c));
+  const int slot = atomicAdd(&a.new_cnt[hv], 1);
+  a.new_slot[r] = slot;
+  if (slot == 0) a.touched[atomicAdd(reinterpret_cast<unsigned long long*>(&a.st->touched), 1ull)] = hv;
+}
+
+__global__ void k_after_commit(ExploreStatus* st, const int64_t* rank_total, int64_t* d_K) {
+  const int64_t K = *rank_total;
+  st->K = K;
+  *d_K = K;
+}
+
+__global__ void k_node_sizes(int n, const int32_t* mem_cnt, const int32_t* new_cnt, int32_t* sz) {
+  const int v = blockIdx.x * blockDim.x + threadIdx.x;
+  if (v < n) sz[v] = mem_cnt[v] + new_cnt[v];
+}
+
+__global__ void k_relayout(int n, const int64_t* old_off, const int32_t* mem_cnt, const int32_t* old_ids,
+                           const int64_t* new_off, int32_t* new_ids) {
+  const int64_t gw = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (gw >= n) return;
+  const int v = static_cast<int>(gw);
+  const int m = mem_cnt[v];
+  const int64_t a = old_off[v], b = new_off[v];
+  for (int k = lane; k < m; k += 32) new_ids[b + k] = old_ids[a + k];
+}
+
+__global__ void k_place_new(const int64_t* d_K, const ExploreStatus* st, const int32_t* head, const int64_t* new_off,
+                            const int32_t* mem_cnt, const int32_t* new_slot, int32_t* new_ids) {
+  const int64_t r = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (r >= *d_K) return;
+  const int64_t id = st->n_plans + r;
+  const int hv = head[id];
+  new_ids[new_off[hv] + mem_cnt[hv] + new_slot[r]] = static_cast<int32_t>(id);
+}
+
+// RemoveDominated, both directions, for one touched node per CTA.
+// Segment layout on entry: [old members (ascending ids) | newcomers (any
+// order)].  On exit: [old survivors | surviving newcomers by id].
+__global__ void __launch_bounds__(128) k_dom(const ExploreStatus* st, const int32_t* touched,
+                                             const int64_t* new_off, int32_t* mem_cnt, int32_t* new_cnt,
+                                             int32_t* ids, const double* cost, const double* cp, uint8_t* flags,
+                                             uint8_t* drop, uint8_t* surv, int32_t* fpos, ExploreStatus* stw) {
+  const int64_t P0 = st->n_plans;
+  __shared__ int s_old_surv, s_new_surv, s_drop, s_evict, s_evict_open;
+  constexpr int kMaxLocal = 64;
+  for (int64_t b = blockIdx.x; b < st->touched; b += gridDim.x) {
+    const int v = touched[b];
+    const int64_t base = new_off[v];
+    const int m_old = mem_cnt[v];
+    const int m_new = new_cnt[v];
+    const int m = m_old + m_new;
+    if (threadIdx.x == 0) {
+      s_old_surv = 0;
+      s_new_surv = 0;
+      s_drop = 0;
+      s_evict = 0;
+      s_evict_open = 0;
+    }
+    __syncthreads();
+    // (1) drop newcomers dominated by any member of the pre-removal set,
+    //     old or new (planner.hpp:200-211); dominates(o, q) = q.cost > o.cost
+    //     && q.cp >= o.cp (planner.hpp:58-60)
+    for (int qi = threadIdx.x; qi < m_new; qi += blockDim.x) {
+      const int q = ids[base + m_old + qi];
+      const double qc = cost[q], qp = cp[q];
+      bool d = false;
+      for (int x = 0; x < m && !d; ++x) {
+        const int o = ids[base + x];
+        d = (qc > cost[o]) && (qp >= cp[o]);
+      }
+      drop[q - P0] = d ? 1 : 0;
+      surv[q - P0] = d ? 0 : 1;
+      if (d) atomicAdd(&s_drop, 1);
+    }
+    __syncthreads();
+    // (2) evict old members other than the root that a surviving newcomer
+    //     dominates (planner.hpp:219-238); evicted slots become -1 - id
+    for (int pi = threadIdx.x; pi < m_old; pi += blockDim.x) {
+      const int p = ids[base + pi];
+      if (p == 0) continue;
+      const double pc = cost[p], pp = cp[p];
+      bool ev = false;
+      for (int qi = 0; qi < m_new && !ev; ++qi) {
+        const int q = ids[base + m_old + qi];
+        if (drop[q - P0]) continue;
+        ev = (pc > cost[q]) && (pp >= cp[q]);
+      }
+      if (ev) {
+        atomicAdd(&s_evict, 1);
+        if (flags[p] & kOpen) {  // waiting in a bucket: skipped at collection
+          flags[p] &= static_cast<uint8_t>(~kOpen);
+          atomicAdd(&s_evict_open, 1);
+        }
+        ids[base + pi] = -1 - p;
+      }
+    }
+    __syncthreads();
+    // (3) rank surviving newcomers by id; compact old survivors in order
+    for (int qi = threadIdx.x; qi < m_new; qi += blockDim.x) {
+      const int q = ids[base + m_old + qi];
+      if (drop[q - P0]) continue;
+      int r = 0;
+      for (int xi = 0; xi < m_new; ++xi) {
+        const int x = ids[base + m_old + xi];
+        r += (!drop[x - P0] && x < q) ? 1 : 0;
+      }
+      fpos[q - P0] = r;
+      atomicAdd(&s_new_surv, 1);
+    }
+    if (threadIdx.x == 0) {
+      int w = 0;
+      for (int pi = 0; pi < m_old; ++pi) {
+        const int p = ids[base + pi];
+        if (p >= 0) ids[base + w++] = p;
+      }
+      s_old_surv = w;
+    }
+    // (4) gather surviving newcomers before overwriting their slots
+    int my_q[kMaxLocal];
+    int my_n = 0;
+    for (int qi = threadIdx.x; qi < m_new; qi += blockDim.x) {
+      const int q = ids[base + m_old + qi];
+      if (!drop[q - P0] && my_n < kMaxLocal) my_q[my_n++] = q;
+    }
+    __syncthreads();
+    if (m_new > kMaxLocal * static_cast<int>(blockDim.x)) {
+      if (threadIdx.x == 0) atomicExch(reinterpret_cast<unsigned long long*>(&stw->err), 2ull);
+    } else {
+      for (int k = 0; k < my_n; ++k) ids[base + s_old_surv + fpos[my_q[k] - P0]] = my_q[k];
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      mem_cnt[v] = s_old_surv + s_new_surv;
+      new_cnt[v] = 0;
+      atomicAdd(reinterpret_cast<unsigned long long*>(&stw->removed),
+                static_cast<unsigned long long>(s_drop + s_evict));
+      atomicAdd(reinterpret_cast<unsigned long long*>(&stw->evicted_open),
+                static_cast<unsigned long long>(s_evict_open));
+    }
+    __syncthreads();
+  }
+}
+
+__global__ void k_pool_append(const int64_t* d_K, const ExploreStatus* st, const uint8_t* surv, const int64_t* spos,
+                              const int32_t* bucket, uint8_t* flags, int32_t* pool, ExploreStatus* stw) {
+  const int64_t r = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (r >= *d_K || !surv[r]) return;
+  const int64_t id = st->n_plans + r;
+  pool[st->pool_n + spos[r]] = static_cast<int32_t>(id);
+  flags[id] |= kOpen;
+  atomicMax(&stw->max_bucket, static_cast<long long>(bucket[id]));
+}
+
+// end of round bookkeeping (single thread); spos[K] = surviving newcomers
+__global__ void k_round_end(ExploreStatus* st, const int64_t* d_K, const int64_t* spos) {
+  const int64_t K = *d_K;
+  const int64_t ns = spos[K];
+  st->n_surv = ns;
+  st->pool_n += ns;
+  st->open_count += ns - st->evicted_open - st->G;
+  st->n_plans += K;
+  st->min_bucket = LLONG_MAX;
+}
+
+__global__ void k_pool_min(const ExploreStatus* st, const int32_t* pool, const uint8_t* flags, const int32_t* bucket,
+                           ExploreStatus* stw) {
+  const int64_t x = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (x >= st->pool_n) return;
+  const int id = pool[x];
+  if (flags[id] & kOpen) atomicMin(&stw->min_bucket, static_cast<long long>(bucket[id]));
+}
+
+// i <- max(i + 1, lowest open bucket): the reference's `continue` over empty
+// thresholds (planner.hpp:250-261) collapsed into one step.
+__global__ void k_round_i(ExploreStatus* st, int64_t* d_pool_n, int64_t* limits) {
+  long long i = st->i + 1;
+  if (st->min_bucket != LLONG_MAX && st->min_bucket > i) i = st->min_bucket;
+  st->i = i;
+  const long long limit = i < st->max_bucket ? i : st->max_bucket;
+  limits[0] = limit;
+  limits[1] = st->min_bucket == LLONG_MAX ? 0 : st->min_bucket;
+  *d_pool_n = st->pool_n;
+  st->G = 0;
+  st->T = 0;
+  st->min_group_bits = 0x7ff0000000000000ll;
+  st->touched = 0;
+  st->evicted_open = 0;
+}
+
+__global__ void k_select(const int64_t* d_pool_n, const int64_t* limits, const int32_t* pool, const uint8_t* flags,
+                         const int32_t* bucket, int32_t* keys, uint8_t* stay) {
+  const int64_t x = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (x >= *d_pool_n) return;
+  const int id = pool[x];
+  const bool open = flags[id] & kOpen;
+  const int b = bucket[id];
+  const bool sel = open && b <= limits[0];
+  keys[x] = sel ? static_cast<int32_t>(b - limits[1]) : -1;
+  stay[x] = (open && !sel) ? 1 : 0;
+}
+
+__global__ void k_pool_compact(const int64_t* d_pool_n, const int32_t* pool, const uint8_t* stay, const int64_t* pos,
+                               int32_t* out) {
+  const int64_t x = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (x >= *d_pool_n || !stay[x]) return;
+  out[pos[x]] = pool[x];
+}
+
+__global__ void k_group_post(const int64_t* d_G, const int32_t* group, const int32_t* head, const double* cost,
+                             const int64_t* row_ptr, uint8_t* flags, int32_t* deg, ExploreStatus* st) {
+  const int64_t g = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (g >= *d_G) return;
+  const int id = group[g];
+  flags[id] &= static_cast<uint8_t>(~kOpen);
+  const int hv = head[id];
+  deg[g] = static_cast<int32_t>(row_ptr[hv + 1] - row_ptr[hv]);
+  atomicMin(&st->min_group_bits, __double_as_longlong(cost[id]));
+}
+
+// group size, its task count (task_off[G]) and the compacted pool size
+__global__ void k_group_final(ExploreStatus* st, const int64_t* d_G, const int64_t* task_off,
+                              const int64_t* stay_pos, const int64_t* d_pool_n, int64_t* d_T) {
+  const int64_t G = *d_G;
+  st->G = G;
+  st->T = task_off[G];
+  *d_T = task_off[G];
+  st->pool_n = stay_pos[*d_pool_n];
+}
+
+static void swap_buf(DBuf& a, DBuf& b) {
+  std::swap(a.p, b.p);
+  std::swap(a.cap, b.cap);
+}
+
+// ------------------------------------------------------------------ host
+static inline size_t al(size_t x) { return (x + 255) & ~size_t(255); }
+
+static void ensure_arena(DevExplore& X, int64_t need, cudaStream_t st) {
+  if (need <= X.cap) return;
+  int64_t cap = X.cap ? X.cap : 1 << 16;
+  while (cap < need) cap += cap / 2 + 1024;
+  const int64_t old = X.n_plans;
+  X.head.grow(al(cap * 4), old * 4, st);
+  X.parent.grow(al(cap * 4), old * 4, st);
+  X.cost.grow(al(cap * 8), old * 8, st);
+  X.cp.grow(al(cap * 8), old * 8, st);
+  X.t_end.grow(al(cap * 4), old * 4, st);
+  X.mask.grow(al(cap * X.W * 8), old * X.W * 8, st);
+  X.bucket.grow(al(cap * 4), old * 4, st);
+  X.flags.grow(al(cap), old, st);
+  // member segments and the pool hold at most every plan once
+  X.mem_a.grow(al((cap + 16) * 4), X.mem_a.cap, st);
+  X.mem_b.grow(al((cap + 16) * 4), X.mem_b.cap, st);
+  X.pool_a.grow(al((cap + 16) * 4), X.pool_a.cap, st);
+  X.pool_b.grow(al((cap + 16) * 4), X.pool_b.cap, st);
+  X.cap = cap;
+}
+
+template <class T>
+static T* ptr(DBuf& b) {
+  return b.as<T>();
+}
+
+void run_explore_device(DevExplore& X, Ctx& c, const DevGraph& G, const ExploreArgs& prm) {
+  if (!c.bank.p) throw std::invalid_argument("explore: no particle bank in this context");
+  if (c.bank_dw != G.dw) throw std::invalid_argument("explore: bank / graph dimension mismatch");
+  cudaStream_t st = c.stream;
+  const int n = G.n, N = c.bank_n, W = (N + 63) / 64;
+  X.n = n;
+  X.N = N;
+  X.W = W;
+  if (N > 512) throw std::invalid_argument("explore: at most 512 particles per plan");
+  const int ch = [&] {
+    int q = (N + 31) / 32, p = 1;
+    while (p < q) p <<= 1;
+    return p;
+  }();
+  X.cap = 0;
+  X.n_plans = 0;
+  ensure_arena(X, 1 << 16, st);
+  if (!X.status_h) PUMP_CUDA(cudaMallocHost(&X.status_h, sizeof(ExploreStatus)));
+  X.status_d.ensure(al(sizeof(ExploreStatus)) + 256);
+  ExploreStatus* S = X.status_d.as<ExploreStatus>();
+  int64_t* d_scal = reinterpret_cast<int64_t*>(reinterpret_cast<char*>(X.status_d.p) + al(sizeof(ExploreStatus)));
+  // d_scal: [0] K, [1] pool_n, [2] G, [3] T, [4..5] limits
+  int64_t* d_K = d_scal + 0;
+  int64_t* d_pool_n = d_scal + 1;
+  int64_t* d_G = d_scal + 2;
+  int64_t* d_T = d_scal + 3;
+  int64_t* d_limits = d_scal + 4;
+
+  // per-node state
+  X.mem_off.ensure(al((n + 1) * 8));
+  X.mem_cnt.ensure(al(n * 4));
+  X.new_cnt.ensure(al(n * 4));
+  X.is_goal.ensure(al(n));
+  X.touched.ensure(al(n * 4));
+  DBuf& node_sz = c.buf("x_node_sz", al(n * 4));
+  DBuf& off2 = c.buf("x_off2", al((n + 1) * 8));
+  PUMP_CUDA(cudaMemsetAsync(X.mem_cnt.p, 0, n * 4, st));
+  PUMP_CUDA(cudaMemsetAsync(X.new_cnt.p, 0, n * 4, st));
+  PUMP_CUDA(cudaMemsetAsync(X.mem_off.p, 0, (n + 1) * 8, st));
+  std::vector<uint8_t> goal(n, 0);
+  for (int v : G.goal_nodes) goal[v] = 1;
+  c.h2d(X.is_goal.p, goal.data(), n);
+
+  // root plan (planner.hpp:100-103)
+  {
+    const int32_t zero = 0, minus1 = -1;
+    const double dz = 0.0;
+    c.h2d(X.head.p, &zero, 4);
+    c.h2d(X.parent.p, &minus1, 4);
+    c.h2d(X.cost.p, &dz, 8);
+    c.h2d(X.cp.p, &dz, 8);
+    c.h2d(X.t_end.p, &zero, 4);
+    c.h2d(X.bucket.p, &zero, 4);
+    std::vector<uint64_t> full(W, ~0ull);
+    if (N % 64) full[W - 1] = (1ull << (N % 64)) - 1;
+    c.h2d(X.mask.p, full.data(), W * 8);
+    const uint8_t f0 = 0;
+    c.h2d(X.flags.p, &f0, 1);
+    // pareto[0] = {0}: member segment of node 0 starts at 0 with one entry
+    const int32_t one = 1;
+    c.h2d(X.mem_cnt.p, &one, 4);
+    std::vector<int64_t> off(n + 1, 1);
+    off[0] = 0;
+    c.h2d(X.mem_off.p, off.data(), (n + 1) * 8);
+    c.h2d(X.mem_a.p, &zero, 4);
+    X.mem_flip = false;
+    // group = [0]
+    X.group.ensure(al(64 * 4));
+    c.h2d(X.group.p, &zero, 4);
+  }
+  const bool root_goal = n > 0 && goal[0];
+  ExploreStatus h{};
+  h.G = 1;
+  h.n_plans = 1;
+  h.open_count = 1;
+  h.i = 0;
+  h.max_bucket = 0;
+  h.min_bucket = LLONG_MAX;
+  h.pool_n = 0;
+  h.best_goal_bits = root_goal && 0.0 < prm.alpha_min ? 0ll : 0x7ff0000000000000ll;
+  h.min_group_bits = 0;  // root cost 0
+  // task count of the first group
+  int64_t T0 = 0;
+  {
+    std::vector<int64_t> rp(2);
+    PUMP_CUDA(cudaMemcpyAsync(rp.data(), G.row_ptr.p, 16, cudaMemcpyDeviceToHost, st));
+    c.sync();
+    T0 = rp[1] - rp[0];
+  }
+  h.T = T0;
+  c.h2d(S, &h, sizeof(h));
+  {
+    const int64_t toff[2] = {0, T0};
+    X.task_off.ensure(al(64 * 8));
+    c.h2d(X.task_off.p, toff, 16);
+    const int64_t sc[4] = {0, 0, 1, T0};
+    c.h2d(d_scal, sc, 32);
+  }
+  X.partial_plans = 0;
+  X.rounds = 0;
+  X.pool_flip = false;
+  const double width = prm.lambda * prm.r_n;
+
+  c.tic();
+  for (;;) {
+    // loop-top termination (planner.hpp:126-138); h is the status after the
+    // previous collection
+    const double best_goal = __builtin_bit_cast(double, h.best_goal_bits);
+    const double min_group = __builtin_bit_cast(double, h.min_group_bits);
+    if (h.G > 0 && best_goal != __builtin_inf() && best_goal <= min_group) {
+      X.termination = 0;
+      break;
+    }
+    if (h.G == 0 && h.open_count == 0) {
+      X.termination = best_goal == __builtin_inf() ? 1 : 0;
+      break;
+    }
+    const int64_t T = h.T;
+    X.rounds++;
+    X.partial_plans += T;
+    ensure_arena(X, X.n_plans + T + 1, st);
+    // candidate buffers
+    X.cand_keep.ensure(al(T + 1));
+    X.cand_head.ensure(al((T + 1) * 4));
+    X.cand_src.ensure(al((T + 1) * 4));
+    X.cand_tend.ensure(al((T + 1) * 4));
+    X.cand_cost.ensure(al((T + 1) * 8));
+    X.cand_cp.ensure(al((T + 1) * 8));
+    X.cand_mask.ensure(al((T + 1) * W * 8));
+    X.cand_rank.ensure(al((T + 2) * 8));
+    X.new_slot.ensure(al((T + 1) * 4));
+    X.drop.ensure(al(T + 1));
+    X.surv.ensure(al(T + 1));
+    X.fpos.ensure(al((T + 1) * 4));
+    DBuf& spos = c.buf("x_spos", al((T + 2) * 8));
+    DBuf& stmp = c.buf("x_scan_tmp", scan_temp_bytes(std::max<int64_t>({T, n, X.cap}) + 16));
+
+    if (T > 0) {
+      ExpandArgs ea{X.group.as<int32_t>(), X.task_off.as<int64_t>(), d_G, d_T, G.row_ptr.as<int64_t>(),
+                    G.e_to.as<int32_t>(), G.e_cost.as<double>(), G.e_nsteps.as<int32_t>(), G.wp_off.as<int64_t>(),
+                    G.hs_off.as<int64_t>(), G.hs_a.as<double>(), G.hs_b.as<double>(), X.head.as<int32_t>(),
+                    X.cost.as<double>(), X.t_end.as<int32_t>(), X.mask.as<uint64_t>(), c.bank.as<double>(), N,
+                    c.bank_horizon, W, prm.alpha_max, X.cand_keep.as<uint8_t>(), X.cand_head.as<int32_t>(),
+                    X.cand_src.as<int32_t>(), X.cand_tend.as<int32_t>(), X.cand_cost.as<double>(),
+                    X.cand_cp.as<double>(), X.cand_mask.as<uint64_t>(), S};
+      const unsigned grid = grid_for(T * 32, 256);
+      dispatch_dw(G.dw, [&]<int DW>() {
+        switch (ch) {
+          case 1: k_expand<DW, 1><<<grid, 256, 0, st>>>(ea); break;
+          case 2: k_expand<DW, 2><<<grid, 256, 0, st>>>(ea); break;
+          case 4: k_expand<DW, 4><<<grid, 256, 0, st>>>(ea); break;
+          case 8: k_expand<DW, 8><<<grid, 256, 0, st>>>(ea); break;
+          default: k_expand<DW, 16><<<grid, 256, 0, st>>>(ea); break;
+        }
+      });
+      ++c.launches;
+      PUMP_CUDA(cudaGetLastError());
+    }
+    exclusive_scan<uint8_t>(X.cand_keep.as<uint8_t>(), X.cand_rank.as<int64_t>(), T, stmp.p, st, &c.launches, d_T);
+    if (T == 0) PUMP_CUDA(cudaMemsetAsync(X.cand_rank.p, 0, 8, st));
+    CommitArgs ca{d_T, X.cand_keep.as<uint8_t>(), X.cand_rank.as<int64_t>(), X.cand_head.as<int32_t>(),
+                  X.cand_src.as<int32_t>(), X.cand_tend.as<int32_t>(), X.cand_cost.as<double>(),
+                  X.cand_cp.as<double>(), X.cand_mask.as<uint64_t>(), W, width, prm.alpha_min,
+                  X.is_goal.as<uint8_t>(), X.head.as<int32_t>(), X.parent.as<int32_t>(), X.cost.as<double>(),
+                  X.cp.as<double>(), X.t_end.as<int32_t>(), X.mask.as<uint64_t>(), X.bucket.as<int32_t>(),
+                  X.flags.as<uint8_t>(), X.new_cnt.as<int32_t>(), X.new_slot.as<int32_t>(),
+                  X.touched.as<int32_t>(), S};
+    if (T > 0) {
+      k_commit<<<grid_for(T, 256), 256, 0, st>>>(ca);
+      ++c.launches;
+    }
+    // K = total kept (rank[T]); rank lives at cand_rank[T] with T from host
+    k_after_commit<<<1, 1, 0, st>>>(S, X.cand_rank.as<int64_t>() + T, d_K);
+    ++c.launches;
+    // member relayout
+    DBuf& old_ids = X.mem_flip ? X.mem_b : X.mem_a;
+    DBuf& new_ids = X.mem_flip ? X.mem_a : X.mem_b;
+    k_node_sizes<<<grid_for(n, 256), 256, 0, st>>>(n, X.mem_cnt.as<int32_t>(), X.new_cnt.as<int32_t>(),
+                                                    node_sz.as<int32_t>());
+    exclusive_scan<int32_t>(node_sz.as<int32_t>(), off2.as<int64_t>(), n, stmp.p, st, &c.launches);
+    k_relayout<<<grid_for(static_cast<int64_t>(n) * 32, 256), 256, 0, st>>>(
+        n, X.mem_off.as<int64_t>(), X.mem_cnt.as<int32_t>(), old_ids.as<int32_t>(), off2.as<int64_t>(),
+        new_ids.as<int32_t>());
+    c.launches += 2;
+    if (T > 0) {
+      k_place_new<<<grid_for(T, 256), 256, 0, st>>>(d_K, S, X.head.as<int32_t>(), off2.as<int64_t>(),
+                                                      X.mem_cnt.as<int32_t>(), X.new_slot.as<int32_t>(),
+                                                      new_ids.as<int32_t>());
+      const unsigned gd = static_cast<unsigned>(std::min<int64_t>(std::max<int64_t>(T, 1), 148 * 16));
+      k_dom<<<gd, 128, 0, st>>>(S, X.touched.as<int32_t>(), off2.as<int64_t>(), X.mem_cnt.as<int32_t>(),
+                                X.new_cnt.as<int32_t>(), new_ids.as<int32_t>(), X.cost.as<double>(),
+                                X.cp.as<double>(), X.flags.as<uint8_t>(), X.drop.as<uint8_t>(),
+                                X.surv.as<uint8_t>(), X.fpos.as<int32_t>(), S);
+      c.launches += 2;
+    }
+    swap_buf(X.mem_off, off2);  // new offsets become current
+    X.mem_flip = !X.mem_flip;
+    // surviving newcomers -> open pool in id order
+    exclusive_scan<uint8_t>(X.surv.as<uint8_t>(), spos.as<int64_t>(), std::max<int64_t>(T, 1), stmp.p, st,
+                            &c.launches, d_K);
+    DBuf& pool_cur = X.pool_flip ? X.pool_b : X.pool_a;
+    DBuf& pool_nxt = X.pool_flip ? X.pool_a : X.pool_b;
+    if (T > 0) {
+      k_pool_append<<<grid_for(T, 256), 256, 0, st>>>(d_K, S, X.surv.as<uint8_t>(), spos.as<int64_t>(),
+                                                        X.bucket.as<int32_t>(), X.flags.as<uint8_t>(),
+                                                        pool_cur.as<int32_t>(), S);
+      ++c.launches;
+    }
+    k_round_end<<<1, 1, 0, st>>>(S, d_K, spos.as<int64_t>());
+    ++c.launches;
+    // next group
+    const int64_t pool_ub = h.pool_n + T + 1;
+    k_pool_min<<<grid_for(pool_ub, 256), 256, 0, st>>>(S, pool_cur.as<int32_t>(), X.flags.as<uint8_t>(),
+                                                         X.bucket.as<int32_t>(), S);
+    k_round_i<<<1, 1, 0, st>>>(S, d_pool_n, d_limits);
+    c.launches += 2;
+    DBuf& keys = c.buf("x_sel_keys", al((pool_ub + 1) * 4));
+    DBuf& stay = c.buf("x_sel_stay", al(pool_ub + 1));
+    DBuf& stay_pos = c.buf("x_stay_pos", al((pool_ub + 2) * 8));
+    k_select<<<grid_for(pool_ub, 256), 256, 0, st>>>(d_pool_n, d_limits, pool_cur.as<int32_t>(),
+                                                       X.flags.as<uint8_t>(), X.bucket.as<int32_t>(),
+                                                       keys.as<int32_t>(), stay.as<uint8_t>());
+    ++c.launches;
+    DBuf& stmp2 = c.buf("x_scan_tmp2", scan_temp_bytes(pool_ub + 16));
+    exclusive_scan<uint8_t>(stay.as<uint8_t>(), stay_pos.as<int64_t>(), pool_ub, stmp2.p, st, &c.launches,
+                            d_pool_n);
+    k_pool_compact<<<grid_for(pool_ub, 256), 256, 0, st>>>(d_pool_n, pool_cur.as<int32_t>(), stay.as<uint8_t>(),
+                                                             stay_pos.as<int64_t>(), pool_nxt.as<int32_t>());
+    ++c.launches;
+    X.group.ensure(al((pool_ub + 1) * 4));
+    DBuf& mtmp = c.buf("x_ms_tmp", multisplit_temp_bytes(pool_ub, 1 << 18));
+    stable_multisplit(keys.as<int32_t>(), pool_cur.as<int32_t>(), pool_ub, 1 << 18, X.group.as<int32_t>(), d_G,
+                      mtmp.p, st, &c.launches, d_pool_n);
+    DBuf& deg = c.buf("x_deg", al((pool_ub + 1) * 4));
+    X.task_off.ensure(al((pool_ub + 2) * 8));
+    k_group_post<<<grid_for(pool_ub, 256), 256, 0, st>>>(d_G, X.group.as<int32_t>(), X.head.as<int32_t>(),
+                                                           X.cost.as<double>(), G.row_ptr.as<int64_t>(),
+                                                           X.flags.as<uint8_t>(), deg.as<int32_t>(), S);
+    ++c.launches;
+    DBuf& stmp3 = c.buf("x_scan_tmp3", scan_temp_bytes(pool_ub + 16));
+    exclusive_scan<int32_t>(deg.as<int32_t>(), X.task_off.as<int64_t>(), pool_ub, stmp3.p, st, &c.launches, d_G);
+    k_group_final<<<1, 1, 0, st>>>(S, d_G, X.task_off.as<int64_t>(), stay_pos.as<int64_t>(), d_pool_n, d_T);
+    ++c.launches;
+    X.pool_flip = !X.pool_flip;
+    PUMP_CUDA(cudaGetLastError());
+    PUMP_CUDA(cudaMemcpyAsync(X.status_h, S, sizeof(ExploreStatus), cudaMemcpyDeviceToHost, st));
+    c.sync();
+    h = *X.status_h;
+    X.n_plans = h.n_plans;
+    if (h.err) throw std::runtime_error("explore: device error " + std::to_string(h.err));
+  }
+  X.kernel_ms = c.toc();
+  X.n_plans = h.n_plans;
+  X.disc_cp = h.disc_cp;
+  X.disc_hor = h.disc_hor;
+  X.removed = h.removed;
+}
+
+}  // namespace pumpg

@@ -1,0 +1,47 @@
+// Device-resident explore (planner.hpp:74-267) state and driver.
+#pragma once
+
+#include "graph.h"
+
+namespace pumpg {
+
+struct ExploreStatus {  // read back once per round (pinned)
+  long long G, T, K, n_plans, open_count, i, max_bucket, min_bucket, pool_n;
+  long long best_goal_bits, min_group_bits;
+  long long disc_cp, disc_hor, removed, n_surv, evicted_open, err, touched;
+};
+
+struct DevExplore {
+  int n = 0, W = 0, N = 0;
+  int64_t cap = 0;  // arena capacity (plans)
+  DBuf head, parent, cost, cp, t_end, mask, bucket, flags;
+  DBuf mem_off, mem_cnt, mem_a, mem_b;  // per-node Pareto members (segmented, ascending ids)
+  bool mem_flip = false;
+  DBuf pool_a, pool_b;  // open plans not yet collected (ascending ids)
+  bool pool_flip = false;
+  DBuf group, task_off;
+  DBuf is_goal, new_cnt, touched, drop, surv, fpos;
+  DBuf cand_keep, cand_head, cand_src, cand_tend, cand_cost, cand_cp, cand_mask, cand_rank, new_slot;
+  DBuf status_d;
+  ExploreStatus* status_h = nullptr;  // pinned
+  // results
+  int64_t n_plans = 0, partial_plans = 0, disc_cp = 0, disc_hor = 0, removed = 0;
+  int rounds = 0;
+  int termination = 0;  // 0 goal_below_alpha_min, 1 frontier_exhausted
+  double kernel_ms = 0;
+  ~DevExplore();
+};
+
+struct ExploreArgs {
+  double alpha_min, alpha_max, lambda, r_n;
+};
+
+void run_explore_device(DevExplore& X, Ctx& c, const DevGraph& G, const ExploreArgs& a);
+
+}  // namespace pumpg
+
+struct pump_explore {
+  pumpg::DevExplore x;
+  pump_ctx* owner = nullptr;
+  std::vector<int32_t> goal_nodes;
+};

@@ -1,0 +1,536 @@
+// K_graph: build_graph (graph.hpp:50-95) on sm_100a.
+//
+//  k_connect_rows   one CTA per source row v, one thread per target u:
+//                   velocity prefilter, connect() (64-point geometric scan +
+//                   golden section, steer.hpp:111-182), cost < r_n filter;
+//                   survivors compacted in ascending-u order (warp ballots +
+//                   CTA prefix) into a per-row candidate slab.
+//  k_collide        one thread per candidate: motion_collides (adaptive
+//                   bisection, geom.hpp:96-123, iterative DFS over (t0,t1)
+//                   spans) + waypoint point_free checks (graph.hpp:80-84).
+//  k_emit_edges     order-preserving compaction into the CSR edge arrays.
+//  k_regions        one thread per edge waypoint: local_convex_region
+//                   (geom.hpp:189-225); run twice (count, then write).
+// Obstacles are staged in shared memory.  All floating point follows the
+// reference's operation order (no FMA: --fmad=false).
+#include "dispatch.cuh"
+#include "graph.h"
+#include "scan.cuh"
+
+namespace pumpg {
+
+constexpr int kRowBlock = 256;
+
+struct GraphArgs {
+  int n;
+  const double* pos;  // n x dw
+  const double* vel;
+  double r_n, dt, eps_cc, tau_max, ratio;
+};
+
+// connect() without the motion coefficients: returns ok; tau, cost out.
+template <int DW>
+__device__ bool connect_dev(const double* ap, const double* av, const double* bp, const double* bv, double tau_max,
+                            double ratio, double& tau_out, double& cost_out) {
+  bool same = true;
+#pragma unroll
+  for (int k = 0; k < DW; ++k) same = same && (ap[k] == bp[k]) && (av[k] == bv[k]);
+  if (same) {
+    tau_out = 0.0;
+    cost_out = 0.0;
+    return true;
+  }
+  const double tau_lo = tau_max * 1e-7;
+  double best_tau = tau_lo, best_c = steer_cost<DW>(ap, av, bp, bv, tau_lo);
+  int best_idx = 0;
+  double tau = tau_lo;
+  for (int i = 1; i < 64; ++i) {
+    tau *= ratio;
+    const double c = steer_cost<DW>(ap, av, bp, bv, tau);
+    if (c < best_c) {
+      best_c = c;
+      best_tau = tau;
+      best_idx = i;
+    }
+  }
+  double lo = best_tau / (best_idx > 0 ? ratio : 1.0);
+  double hi = best_tau * ratio;
+  hi = (tau_max < hi) ? tau_max : hi;  // std::min(best_tau * ratio, tau_max)
+  const double gr = 0.5 * (sqrt(5.0) - 1.0);
+  double x1 = hi - gr * (hi - lo), x2 = lo + gr * (hi - lo);
+  double f1 = steer_cost<DW>(ap, av, bp, bv, x1), f2 = steer_cost<DW>(ap, av, bp, bv, x2);
+  while (hi - lo > 1e-9 * hi) {
+    if (f1 < f2) {
+      hi = x2;
+      x2 = x1;
+      f2 = f1;
+      x1 = hi - gr * (hi - lo);
+      f1 = steer_cost<DW>(ap, av, bp, bv, x1);
+    } else {
+      lo = x1;
+      x1 = x2;
+      f1 = f2;
+      x2 = lo + gr * (hi - lo);
+      f2 = steer_cost<DW>(ap, av, bp, bv, x2);
+    }
+  }
+  tau_out = 0.5 * (lo + hi);
+  cost_out = steer_cost<DW>(ap, av, bp, bv, tau_out);
+  if (best_idx == 63 && tau_out > 0.999 * tau_max) {
+    const double eps = 1e-6 * tau_max;
+    if (steer_cost<DW>(ap, av, bp, bv, tau_max) <= steer_cost<DW>(ap, av, bp, bv, tau_max - eps)) return false;
+  }
+  return true;
+}
+
+// fixed_time_coeffs (steer.hpp:63-79): acc0, jerk
+template <int DW>
+__device__ __forceinline__ void coeffs_dev(const double* ap, const double* av, const double* bp, const double* bv,
+                                           double tau, double* acc0, double* jerk) {
+#pragma unroll
+  for (int k = 0; k < DW; ++k) {
+    const double dp = bp[k] - ap[k] - av[k] * tau;
+    const double dv = bv[k] - av[k];
+    acc0[k] = 6 * dp / (tau * tau) - 2 * dv / tau;
+    jerk[k] = -12 * dp / (tau * tau * tau) + 6 * dv / (tau * tau);
+  }
+}
+
+template <int DW>
+__global__ void __launch_bounds__(kRowBlock) k_connect_rows(GraphArgs g, int cap, int32_t* __restrict__ row_cnt,
+                                                            int32_t* __restrict__ cu, double* __restrict__ ctau,
+                                                            double* __restrict__ ccost) {
+  __shared__ int wtot[kRowBlock / 32];
+  __shared__ int base_s;
+  const int v = blockIdx.x;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  double ap[DW], av[DW];
+#pragma unroll
+  for (int k = 0; k < DW; ++k) {
+    ap[k] = g.pos[v * DW + k];
+    av[k] = g.vel[v * DW + k];
+  }
+  if (threadIdx.x == 0) base_s = 0;
+  __syncthreads();
+  for (int u0 = 0; u0 < g.n; u0 += kRowBlock) {
+    const int u = u0 + threadIdx.x;
+    bool keep = false;
+    double tau = 0, cost = 0;
+    if (u < g.n && u != v) {
+      double bp[DW], bv[DW], dv[DW];
+#pragma unroll
+      for (int k = 0; k < DW; ++k) {
+        bp[k] = g.pos[u * DW + k];
+        bv[k] = g.vel[u * DW + k];
+        dv[k] = bv[k] - av[k];
+      }
+      if (!(2.0 * sqrt(sqnorm<DW>(dv)) >= g.r_n)) {  // graph.hpp:70 cheap lower bound
+        const bool ok = connect_dev<DW>(ap, av, bp, bv, g.tau_max, g.ratio, tau, cost);
+        keep = ok && !(cost >= g.r_n) && !(tau <= 0);  // graph.hpp:72
+      }
+    }
+    const unsigned bal = __ballot_sync(0xffffffffu, keep);
+    if (lane == 0) wtot[warp] = __popc(bal);
+    __syncthreads();
+    int off = base_s;
+    for (int w = 0; w < warp; ++w) off += wtot[w];
+    off += __popc(bal & ((1u << lane) - 1u));
+    if (keep && off < cap) {
+      const int64_t slot = static_cast<int64_t>(v) * cap + off;
+      cu[slot] = u;
+      ctau[slot] = tau;
+      ccost[slot] = cost;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int t = 0;
+      for (int w = 0; w < kRowBlock / 32; ++w) t += wtot[w];
+      base_s += t;
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) row_cnt[v] = base_s;
+}
+
+__device__ __forceinline__ int find_row(const int64_t* __restrict__ off, int n, int64_t c) {
+  int lo = 0, hi = n;  // largest r with off[r] <= c
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) >> 1;
+    if (off[mid] <= c)
+      lo = mid;
+    else
+      hi = mid;
+  }
+  return lo;
+}
+
+template <int DW>
+__device__ __forceinline__ WorldD stage_world(const WorldD& w, double* smem) {
+  double* lo = smem;
+  double* hi = smem + w.n_obs * DW;
+  for (int x = threadIdx.x; x < w.n_obs * DW; x += blockDim.x) {
+    lo[x] = w.lo[x];
+    hi[x] = w.hi[x];
+  }
+  __syncthreads();
+  WorldD s = w;
+  s.lo = lo;
+  s.hi = hi;
+  return s;
+}
+
+template <int DW>
+__global__ void __launch_bounds__(128) k_collide(GraphArgs g, WorldD w, int cap, int64_t n_cand,
+                                                 const int64_t* __restrict__ cand_off, const int32_t* __restrict__ cu,
+                                                 const double* __restrict__ ctau, uint8_t* __restrict__ valid,
+                                                 int32_t* __restrict__ nsteps) {
+  extern __shared__ double smem[];
+  const WorldD ws = stage_world<DW>(w, smem);
+  const int64_t c = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (c >= n_cand) return;
+  const int v = find_row(cand_off, g.n, c);
+  const int64_t slot = static_cast<int64_t>(v) * cap + (c - cand_off[v]);
+  const int u = cu[slot];
+  MotionD<DW> m;
+  m.tau = ctau[slot];
+#pragma unroll
+  for (int k = 0; k < DW; ++k) {
+    m.p0[k] = g.pos[v * DW + k];
+    m.v0[k] = g.vel[v * DW + k];
+    m.p1[k] = g.pos[u * DW + k];
+    m.v1[k] = g.vel[u * DW + k];
+  }
+  coeffs_dev<DW>(m.p0, m.v0, m.p1, m.v1, m.tau, m.a, m.j);
+  bool ok = !motion_collides<DW>(m, ws, g.eps_cc);
+  int L = 0;
+  if (ok) {
+    // motion_waypoints (steer.hpp:192-212): k = floor(tau/dt + 1e-9)
+    const int k = static_cast<int>(floor(m.tau / g.dt + 1e-9));
+    const double rem = m.tau - k * g.dt;
+    L = rem > 1e-9 ? k + 1 : k;
+    for (int j = 1; j <= L && ok; ++j) {
+      double p[DW], vv[DW];
+      if (j == L) {
+#pragma unroll
+        for (int q = 0; q < DW; ++q) p[q] = m.p1[q];
+      } else {
+        motion_state<DW>(m, j * g.dt, p, vv);
+      }
+      ok = point_free<DW>(ws, p);
+    }
+  }
+  valid[c] = ok ? 1 : 0;
+  nsteps[c] = ok ? L : 0;
+}
+
+template <int DW>
+__global__ void k_emit_edges(GraphArgs g, int cap, int64_t n_cand, const int64_t* __restrict__ cand_off,
+                             const int32_t* __restrict__ cu, const double* __restrict__ ctau,
+                             const double* __restrict__ ccost, const uint8_t* __restrict__ valid,
+                             const int32_t* __restrict__ nsteps, const int64_t* __restrict__ eoff,
+                             int32_t* __restrict__ e_from, int32_t* __restrict__ e_to, double* __restrict__ e_cost,
+                             double* __restrict__ e_tau, double* __restrict__ e_acc0, double* __restrict__ e_jerk,
+                             int32_t* __restrict__ e_nsteps, int64_t* __restrict__ row_ptr) {
+  const int64_t c = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (c < g.n + 1) {
+    // row_ptr[v] = number of valid candidates before row v's first candidate
+    row_ptr[c] = eoff[cand_off[c]];
+  }
+  if (c >= n_cand || !valid[c]) return;
+  const int v = find_row(cand_off, g.n, c);
+  const int64_t slot = static_cast<int64_t>(v) * cap + (c - cand_off[v]);
+  const int64_t e = eoff[c];
+  const int u = cu[slot];
+  const double tau = ctau[slot];
+  e_from[e] = v;
+  e_to[e] = u;
+  e_cost[e] = ccost[slot];
+  e_tau[e] = tau;
+  e_nsteps[e] = nsteps[c];
+  double a0[DW], j0[DW];
+  coeffs_dev<DW>(g.pos + v * DW, g.vel + v * DW, g.pos + u * DW, g.vel + u * DW, tau, a0, j0);
+#pragma unroll
+  for (int k = 0; k < DW; ++k) {
+    e_acc0[e * DW + k] = a0[k];
+    e_jerk[e * DW + k] = j0[k];
+  }
+}
+
+// local_convex_region (geom.hpp:189-225) with velocity projection
+// (geom.hpp:163-183).  WRITE=false: count half-spaces only.
+template <int DW, bool WRITE>
+__global__ void __launch_bounds__(128) k_regions(GraphArgs g, WorldD w, int64_t n_wp, int64_t n_edges,
+                                                 const int64_t* __restrict__ wp_off, const int32_t* __restrict__ e_from,
+                                                 const int32_t* __restrict__ e_to, const double* __restrict__ e_tau,
+                                                 const double* __restrict__ e_acc0, const double* __restrict__ e_jerk,
+                                                 const int32_t* __restrict__ e_nsteps, int32_t* __restrict__ hcount,
+                                                 const int64_t* __restrict__ hs_off, double* __restrict__ hs_a,
+                                                 double* __restrict__ hs_b, uint8_t* __restrict__ hs_fb,
+                                                 int* __restrict__ err) {
+  extern __shared__ double smem[];
+  const WorldD ws = stage_world<DW>(w, smem);
+  const int64_t x = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (x >= n_wp) return;
+  // edge owning waypoint x
+  int64_t lo = 0, hi = n_edges;
+  while (hi - lo > 1) {
+    const int64_t mid = (lo + hi) >> 1;
+    if (wp_off[mid] <= x)
+      lo = mid;
+    else
+      hi = mid;
+  }
+  const int64_t e = lo;
+  const int j = static_cast<int>(x - wp_off[e]) + 1;
+  const int L = e_nsteps[e];
+  const int v = e_from[e], u = e_to[e];
+  MotionD<DW> m;
+  m.tau = e_tau[e];
+#pragma unroll
+  for (int k = 0; k < DW; ++k) {
+    m.p0[k] = g.pos[v * DW + k];
+    m.v0[k] = g.vel[v * DW + k];
+    m.p1[k] = g.pos[u * DW + k];
+    m.v1[k] = g.vel[u * DW + k];
+    m.a[k] = e_acc0[e * DW + k];
+    m.j[k] = e_jerk[e * DW + k];
+  }
+  double y[DW], yd[DW];
+  if (j == L) {
+#pragma unroll
+    for (int k = 0; k < DW; ++k) {
+      y[k] = m.p1[k];
+      yd[k] = m.v1[k];
+    }
+  } else {
+    motion_state<DW>(m, j * g.dt, y, yd);
+  }
+  constexpr int kMaxObs = 4096;
+  uint32_t pruned[kMaxObs / 32];
+  const int nw = (ws.n_obs + 31) / 32;
+  for (int q = 0; q < nw; ++q) pruned[q] = 0u;
+  int count = 0;
+  int64_t out = WRITE ? hs_off[x] : 0;
+  for (int iter = 0; iter < ws.n_obs; ++iter) {
+    int best = -1;
+    double best_sq = __longlong_as_double(0x7ff0000000000000ll);  // +inf
+    double d[DW];
+    for (int o = 0; o < ws.n_obs; ++o) {
+      if ((pruned[o >> 5] >> (o & 31)) & 1u) continue;
+      double cand[DW];
+#pragma unroll
+      for (int k = 0; k < DW; ++k) {
+        double c = y[k] < ws.lo[o * DW + k] ? ws.lo[o * DW + k] : y[k];  // max(y, lo)
+        c = ws.hi[o * DW + k] < c ? ws.hi[o * DW + k] : c;               // min(., hi)
+        cand[k] = c - y[k];
+      }
+      const double sq = sqnorm<DW>(cand);
+      if (sq < best_sq) {
+        best_sq = sq;
+        best = o;
+#pragma unroll
+        for (int k = 0; k < DW; ++k) d[k] = cand[k];
+      }
+    }
+    if (best < 0) break;
+    const double dd = sqnorm<DW>(d);
+    const double tol = 1e-12 * (1.0 + dd);
+    bool any = false;
+    for (int o = 0; o < ws.n_obs; ++o) {
+      if ((pruned[o >> 5] >> (o & 31)) & 1u) continue;
+      bool inside = true;
+      for (unsigned corner = 0; corner < (1u << DW) && inside; ++corner) {
+        double dot = 0;
+#pragma unroll
+        for (int k = 0; k < DW; ++k) {
+          const double c = ((corner >> k) & 1u) ? ws.hi[o * DW + k] : ws.lo[o * DW + k];
+          dot += d[k] * (c - y[k]);
+        }
+        if (dot < dd - tol) inside = false;
+      }
+      if (inside) {
+        pruned[o >> 5] |= 1u << (o & 31);
+        any = true;
+      }
+    }
+    if (!any) {
+      atomicExch(err, 1);
+      return;
+    }
+    if (WRITE) {
+      // project_halfspace (geom.hpp:163-183), eps_v = eps_a = 1e-6
+      double a[DW];
+      bool fb = false;
+      const double vn = sqrt(sqnorm<DW>(yd));
+      if (vn < 1e-6) {
+        fb = true;
+      } else {
+        double dy = 0.0;
+#pragma unroll
+        for (int k = 0; k < DW; ++k) dy = dy + d[k] * yd[k];
+        const double coef = dy / sqnorm<DW>(yd);
+#pragma unroll
+        for (int k = 0; k < DW; ++k) a[k] = d[k] - coef * yd[k];
+        if (sqrt(sqnorm<DW>(a)) < 1e-6 * sqrt(sqnorm<DW>(d))) fb = true;
+      }
+      if (fb) {
+#pragma unroll
+        for (int k = 0; k < DW; ++k) a[k] = d[k];
+      }
+#pragma unroll
+      for (int k = 0; k < DW; ++k) hs_a[out * DW + k] = a[k];
+      hs_b[out] = sqnorm<DW>(a);
+      hs_fb[out] = fb ? 1 : 0;
+      ++out;
+    }
+    ++count;
+  }
+  if (!WRITE) hcount[x] = count;
+}
+
+// ------------------------------------------------------------------ host
+static inline size_t al(size_t x) { return (x + 255) & ~size_t(255); }
+
+void build_graph_device(DevGraph& G, Ctx& c, int n, int dw, const double* h_pos, const double* h_vel,
+                        const DevWorld& w, double r_n, double dt, double eps_cc, double tau_max, double ratio) {
+  if (r_n <= 0) throw std::invalid_argument("build_graph: r_n must be positive");
+  if (dt <= 0) throw std::invalid_argument("motion_waypoints: dt must be positive");
+  if (w.n_obs > 4096) throw std::invalid_argument("build_graph: more than 4096 obstacles");
+  G.n = n;
+  G.dw = dw;
+  G.r_n = r_n;
+  G.dt = dt;
+  cudaStream_t st = c.stream;
+  G.pos.ensure(al(n * dw * 8));
+  G.vel.ensure(al(n * dw * 8));
+  c.h2d(G.pos.p, h_pos, n * dw * 8);
+  c.h2d(G.vel.p, h_vel, n * dw * 8);
+  GraphArgs ga{n, G.pos.as<double>(), G.vel.as<double>(), r_n, dt, eps_cc, tau_max, ratio};
+  WorldD wd;
+  wd.n_obs = w.n_obs;
+  wd.lo = w.d_lo;
+  wd.hi = w.d_hi;
+  for (int k = 0; k < 6; ++k) {
+    wd.blo[k] = w.blo[k];
+    wd.bhi[k] = w.bhi[k];
+  }
+  const size_t wsmem = 2 * static_cast<size_t>(w.n_obs) * dw * sizeof(double);
+  int cap = 512;
+  int32_t max_cnt = 0;
+  DBuf& rcnt = c.buf("g_rowcnt", al((n + 1) * 4));
+  DBuf& coff = c.buf("g_candoff", al((n + 2) * 8));
+  DBuf& stmp = c.buf("g_scantmp", scan_temp_bytes(static_cast<int64_t>(n) * 4096 + 16));
+  for (;;) {
+    DBuf& cuB = c.buf("g_cu", al(static_cast<size_t>(n) * cap * 4));
+    DBuf& ctB = c.buf("g_ctau", al(static_cast<size_t>(n) * cap * 8));
+    DBuf& ccB = c.buf("g_ccost", al(static_cast<size_t>(n) * cap * 8));
+    dispatch_dw(dw, [&]<int DW>() {
+      k_connect_rows<DW><<<n, kRowBlock, 0, st>>>(ga, cap, rcnt.as<int32_t>(), cuB.as<int32_t>(), ctB.as<double>(),
+                                                 ccB.as<double>());
+    });
+    ++c.launches;
+    PUMP_CUDA(cudaGetLastError());
+    std::vector<int32_t> cnt(n);
+    c.d2h(cnt.data(), rcnt.p, n * 4);
+    c.sync();
+    max_cnt = 0;
+    for (int v = 0; v < n; ++v) max_cnt = std::max(max_cnt, cnt[v]);
+    if (max_cnt <= cap) break;
+    cap = max_cnt;  // exact refit, rerun (deterministic)
+  }
+  int32_t* cu = c.scratch["g_cu"].as<int32_t>();
+  double* ctau = c.scratch["g_ctau"].as<double>();
+  double* ccost = c.scratch["g_ccost"].as<double>();
+  exclusive_scan<int32_t>(rcnt.as<int32_t>(), coff.as<int64_t>(), n, stmp.p, st, &c.launches);
+  int64_t n_cand = 0;
+  c.d2h(&n_cand, coff.as<int64_t>() + n, 8);
+  c.sync();
+  G.n_cand = n_cand;
+  DBuf& valid = c.buf("g_valid", al(n_cand + 1));
+  DBuf& nst = c.buf("g_nsteps", al((n_cand + 1) * 4));
+  DBuf& eoff = c.buf("g_eoff", al((n_cand + 2) * 8));
+  DBuf& stmp2 = c.buf("g_scantmp2", scan_temp_bytes(n_cand + 16));
+  if (n_cand > 0) {
+    dispatch_dw(dw, [&]<int DW>() {
+      if (wsmem > 48 * 1024)
+        PUMP_CUDA(cudaFuncSetAttribute(k_collide<DW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wsmem));
+      k_collide<DW><<<grid_for(n_cand, 128), 128, wsmem, st>>>(ga, wd, cap, n_cand, coff.as<int64_t>(), cu, ctau,
+                                                               valid.as<uint8_t>(), nst.as<int32_t>());
+    });
+    ++c.launches;
+    PUMP_CUDA(cudaGetLastError());
+  }
+  exclusive_scan<uint8_t>(valid.as<uint8_t>(), eoff.as<int64_t>(), n_cand, stmp2.p, st, &c.launches);
+  int64_t E = 0;
+  c.d2h(&E, eoff.as<int64_t>() + n_cand, 8);
+  c.sync();
+  G.E = E;
+  G.e_from.ensure(al((E + 1) * 4));
+  G.e_to.ensure(al((E + 1) * 4));
+  G.e_cost.ensure(al((E + 1) * 8));
+  G.e_tau.ensure(al((E + 1) * 8));
+  G.e_acc0.ensure(al((E + 1) * dw * 8));
+  G.e_jerk.ensure(al((E + 1) * dw * 8));
+  G.e_nsteps.ensure(al((E + 1) * 4));
+  G.row_ptr.ensure(al((n + 1) * 8));
+  G.wp_off.ensure(al((E + 2) * 8));
+  dispatch_dw(dw, [&]<int DW>() {
+    const int64_t items = std::max<int64_t>(n_cand, n + 1);
+    k_emit_edges<DW><<<grid_for(items, 256), 256, 0, st>>>(
+        ga, cap, n_cand, coff.as<int64_t>(), cu, ctau, ccost, valid.as<uint8_t>(), nst.as<int32_t>(),
+        eoff.as<int64_t>(), G.e_from.as<int32_t>(), G.e_to.as<int32_t>(), G.e_cost.as<double>(),
+        G.e_tau.as<double>(), G.e_acc0.as<double>(), G.e_jerk.as<double>(), G.e_nsteps.as<int32_t>(),
+        G.row_ptr.as<int64_t>());
+  });
+  ++c.launches;
+  PUMP_CUDA(cudaGetLastError());
+  DBuf& stmp3 = c.buf("g_scantmp3", scan_temp_bytes(E + 16));
+  exclusive_scan<int32_t>(G.e_nsteps.as<int32_t>(), G.wp_off.as<int64_t>(), E, stmp3.p, st, &c.launches);
+  int64_t NW = 0;
+  c.d2h(&NW, G.wp_off.as<int64_t>() + E, 8);
+  c.sync();
+  G.NW = NW;
+  DBuf& hcnt = c.buf("g_hcnt", al((NW + 1) * 4));
+  DBuf& err = c.buf("g_err", 256);
+  G.hs_off.ensure(al((NW + 2) * 8));
+  PUMP_CUDA(cudaMemsetAsync(err.p, 0, 4, st));
+  if (NW > 0) {
+    dispatch_dw(dw, [&]<int DW>() {
+      if (wsmem > 48 * 1024) {
+        PUMP_CUDA(cudaFuncSetAttribute(k_regions<DW, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wsmem));
+        PUMP_CUDA(cudaFuncSetAttribute(k_regions<DW, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wsmem));
+      }
+      k_regions<DW, false><<<grid_for(NW, 128), 128, wsmem, st>>>(
+          ga, wd, NW, E, G.wp_off.as<int64_t>(), G.e_from.as<int32_t>(), G.e_to.as<int32_t>(), G.e_tau.as<double>(),
+          G.e_acc0.as<double>(), G.e_jerk.as<double>(), G.e_nsteps.as<int32_t>(), hcnt.as<int32_t>(), nullptr,
+          nullptr, nullptr, nullptr, err.as<int>());
+    });
+    ++c.launches;
+    PUMP_CUDA(cudaGetLastError());
+  }
+  DBuf& stmp4 = c.buf("g_scantmp4", scan_temp_bytes(NW + 16));
+  exclusive_scan<int32_t>(hcnt.as<int32_t>(), G.hs_off.as<int64_t>(), NW, stmp4.p, st, &c.launches);
+  int64_t H = 0;
+  int herr = 0;
+  c.d2h(&H, G.hs_off.as<int64_t>() + NW, 8);
+  c.d2h(&herr, err.p, 4);
+  c.sync();
+  if (herr) throw std::runtime_error("local_convex_region: pruning loop failed to make progress");
+  G.H = H;
+  G.hs_a.ensure(al((H + 1) * dw * 8));
+  G.hs_b.ensure(al((H + 1) * 8));
+  G.hs_fb.ensure(al(H + 1));
+  if (NW > 0) {
+    dispatch_dw(dw, [&]<int DW>() {
+      k_regions<DW, true><<<grid_for(NW, 128), 128, wsmem, st>>>(
+          ga, wd, NW, E, G.wp_off.as<int64_t>(), G.e_from.as<int32_t>(), G.e_to.as<int32_t>(), G.e_tau.as<double>(),
+          G.e_acc0.as<double>(), G.e_jerk.as<double>(), G.e_nsteps.as<int32_t>(), nullptr, G.hs_off.as<int64_t>(),
+          G.hs_a.as<double>(), G.hs_b.as<double>(), G.hs_fb.as<uint8_t>(), err.as<int>());
+    });
+    ++c.launches;
+    PUMP_CUDA(cudaGetLastError());
+  }
+  c.sync();
+}
+
+}  // namespace pumpg

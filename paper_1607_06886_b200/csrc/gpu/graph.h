@@ -1,0 +1,30 @@
+// Device-resident SampleGraph (graph.hpp:25-37) in CSR form.
+#pragma once
+
+#include "../ctx.h"
+
+namespace pumpg {
+
+struct DevGraph {
+  int n = 0, dw = 0;
+  double r_n = 0, dt = 0;
+  int64_t E = 0, NW = 0, H = 0, n_cand = 0;
+  DBuf pos, vel;                                          // n x dw
+  DBuf row_ptr;                                           // n + 1 (int64)
+  DBuf e_from, e_to, e_cost, e_tau, e_acc0, e_jerk, e_nsteps;
+  DBuf wp_off;                                            // E + 1 (int64)
+  DBuf hs_off;                                            // NW + 1 (int64)
+  DBuf hs_a, hs_b, hs_fb;                                 // H x dw, H, H
+  std::vector<int32_t> goal_nodes;                        // host, ascending
+  std::vector<double> h_pos, h_vel;                       // host copies of the nodes
+};
+
+void build_graph_device(DevGraph& G, Ctx& c, int n, int dw, const double* h_pos, const double* h_vel,
+                        const DevWorld& w, double r_n, double dt, double eps_cc, double tau_max, double ratio);
+
+}  // namespace pumpg
+
+struct pump_graph {
+  pumpg::DevGraph g;
+  pump_ctx* owner = nullptr;
+};

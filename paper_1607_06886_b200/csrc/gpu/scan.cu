@@ -8,8 +8,9 @@ namespace pumpg {
 
 template <class InT>
 __global__ void __launch_bounds__(kScanBlock) k_tile_sum(const InT* __restrict__ in, int64_t n,
-                                                         int64_t* __restrict__ partial) {
+                                                         int64_t* __restrict__ partial, const int64_t* d_n) {
   __shared__ int64_t wsum[kScanBlock / 32];
+  if (d_n) n = min(n, *d_n);
   const int64_t base = static_cast<int64_t>(blockIdx.x) * kScanTile;
   int64_t s = 0;
 #pragma unroll
@@ -29,9 +30,14 @@ __global__ void __launch_bounds__(kScanBlock) k_tile_sum(const InT* __restrict__
 
 // exclusive scan of partial[0..m) in place (single block); total -> *total
 __global__ void __launch_bounds__(1024) k_scan_partials(int64_t* __restrict__ partial, int64_t m,
-                                                        int64_t* __restrict__ total) {
+                                                        int64_t* __restrict__ out, int64_t n, const int64_t* d_n) {
   __shared__ int64_t wsum[32];
   __shared__ int64_t carry;
+  if (d_n) {
+    n = min(n, *d_n);
+    m = (n + kScanTile - 1) / kScanTile;
+  }
+  int64_t* total = out + n;
   if (threadIdx.x == 0) carry = 0;
   __syncthreads();
   for (int64_t c0 = 0; c0 < m; c0 += 1024) {
@@ -58,9 +64,11 @@ __global__ void __launch_bounds__(1024) k_scan_partials(int64_t* __restrict__ pa
 template <class InT>
 __global__ void __launch_bounds__(kScanBlock) k_tile_scan(const InT* __restrict__ in, int64_t n,
                                                           const int64_t* __restrict__ partial,
-                                                          int64_t* __restrict__ out) {
+                                                          int64_t* __restrict__ out, const int64_t* d_n) {
   __shared__ int64_t tile[kScanTile];
   __shared__ int64_t wsum[kScanBlock / 32];
+  if (d_n) n = min(n, *d_n);
+  if (static_cast<int64_t>(blockIdx.x) * kScanTile >= n && n > 0) return;
   const int64_t base = static_cast<int64_t>(blockIdx.x) * kScanTile;
 #pragma unroll
   for (int k = 0; k < kScanItems; ++k) {
@@ -101,23 +109,27 @@ __global__ void __launch_bounds__(kScanBlock) k_tile_scan(const InT* __restrict_
 size_t scan_temp_bytes(int64_t n) { return static_cast<size_t>((n + kScanTile - 1) / kScanTile + 1) * 8 + 256; }
 
 template <class InT>
-void exclusive_scan(const InT* d_in, int64_t* d_out, int64_t n, void* d_temp, cudaStream_t st, int64_t* launches) {
+void exclusive_scan(const InT* d_in, int64_t* d_out, int64_t n, void* d_temp, cudaStream_t st, int64_t* launches,
+                    const int64_t* d_n) {
   if (n <= 0) {
     PUMP_CUDA(cudaMemsetAsync(d_out, 0, sizeof(int64_t), st));
     return;
   }
   const int64_t tiles = (n + kScanTile - 1) / kScanTile;
   int64_t* partial = static_cast<int64_t*>(d_temp);
-  k_tile_sum<InT><<<static_cast<unsigned>(tiles), kScanBlock, 0, st>>>(d_in, n, partial);
-  k_scan_partials<<<1, 1024, 0, st>>>(partial, tiles, d_out + n);
-  k_tile_scan<InT><<<static_cast<unsigned>(tiles), kScanBlock, 0, st>>>(d_in, n, partial, d_out);
+  k_tile_sum<InT><<<static_cast<unsigned>(tiles), kScanBlock, 0, st>>>(d_in, n, partial, d_n);
+  k_scan_partials<<<1, 1024, 0, st>>>(partial, tiles, d_out, n, d_n);
+  k_tile_scan<InT><<<static_cast<unsigned>(tiles), kScanBlock, 0, st>>>(d_in, n, partial, d_out, d_n);
   *launches += 3;
   PUMP_CUDA(cudaGetLastError());
 }
 
-template void exclusive_scan<int32_t>(const int32_t*, int64_t*, int64_t, void*, cudaStream_t, int64_t*);
-template void exclusive_scan<int64_t>(const int64_t*, int64_t*, int64_t, void*, cudaStream_t, int64_t*);
-template void exclusive_scan<uint8_t>(const uint8_t*, int64_t*, int64_t, void*, cudaStream_t, int64_t*);
+template void exclusive_scan<int32_t>(const int32_t*, int64_t*, int64_t, void*, cudaStream_t, int64_t*,
+                                      const int64_t*);
+template void exclusive_scan<int64_t>(const int64_t*, int64_t*, int64_t, void*, cudaStream_t, int64_t*,
+                                      const int64_t*);
+template void exclusive_scan<uint8_t>(const uint8_t*, int64_t*, int64_t, void*, cudaStream_t, int64_t*,
+                                      const int64_t*);
 
 // ------------------------------------------------------------ multisplit
 constexpr int kMsBlock = 512;
@@ -129,8 +141,9 @@ constexpr int kMsWarps = kMsBlock / 32;
 __device__ __forceinline__ int ms_digit(int key, int shift) { return key < 0 ? -1 : ((key >> shift) & (kMsKeys - 1)); }
 
 __global__ void __launch_bounds__(kMsBlock) k_ms_hist(const int32_t* __restrict__ keys, int64_t n, int shift,
-                                                      int n_tiles, int32_t* __restrict__ counts) {
+                                                      int n_tiles, int32_t* __restrict__ counts, const int64_t* d_n) {
   __shared__ int hist[kMsKeys];
+  if (d_n) n = min(n, *d_n);
   for (int k = threadIdx.x; k < kMsKeys; k += kMsBlock) hist[k] = 0;
   __syncthreads();
   const int64_t base = static_cast<int64_t>(blockIdx.x) * kMsTile;
@@ -148,8 +161,10 @@ __global__ void __launch_bounds__(kMsBlock) k_ms_hist(const int32_t* __restrict_
 __global__ void __launch_bounds__(kMsBlock) k_ms_scatter(const int32_t* __restrict__ keys,
                                                          const int32_t* __restrict__ vals, int64_t n, int shift,
                                                          int n_tiles, const int64_t* __restrict__ offs,
-                                                         int32_t* __restrict__ okeys, int32_t* __restrict__ ovals) {
+                                                         int32_t* __restrict__ okeys, int32_t* __restrict__ ovals,
+                                                         const int64_t* d_n) {
   __shared__ int wcnt[kMsWarps][kMsKeys];
+  if (d_n) n = min(n, *d_n);
   __shared__ int64_t run[kMsKeys];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   for (int k = threadIdx.x; k < kMsKeys; k += kMsBlock) {
@@ -189,14 +204,16 @@ __global__ void __launch_bounds__(kMsBlock) k_ms_scatter(const int32_t* __restri
 static inline size_t al256(size_t x) { return (x + 255) & ~size_t(255); }
 
 size_t multisplit_temp_bytes(int64_t n, int n_keys) {
+  (void)n_keys;
   const int64_t tiles = (n + kMsTile - 1) / kMsTile;
   const int64_t cn = static_cast<int64_t>(kMsKeys) * (tiles > 0 ? tiles : 1);
-  (void)n_keys;
-  return al256(cn * 4) + al256((cn + 1) * 8) + al256(scan_temp_bytes(cn)) + 2 * al256((n + 1) * 4) + 256;
+  return al256(cn * 4) + al256((cn + 1) * 8) + al256(scan_temp_bytes(cn)) + 3 * al256((n + 1) * 4) + 256;
 }
 
+// LSD radix over 9-bit digits: one pass for n_keys <= 512, two for <= 2^18.
+// Pass 1 drops negative keys; pass 2 only sees the kept items.
 void stable_multisplit(const int32_t* d_keys, const int32_t* d_vals, int64_t n, int n_keys, int32_t* d_out,
-                       int64_t* d_count, void* d_temp, cudaStream_t st, int64_t* launches) {
+                       int64_t* d_count, void* d_temp, cudaStream_t st, int64_t* launches, const int64_t* d_n) {
   if (n <= 0) {
     PUMP_CUDA(cudaMemsetAsync(d_count, 0, 8, st));
     return;
@@ -211,27 +228,30 @@ void stable_multisplit(const int32_t* d_keys, const int32_t* d_vals, int64_t n, 
   p += al256((cn + 1) * 8);
   void* stmp = p;
   p += al256(scan_temp_bytes(cn));
-  int32_t* k2 = reinterpret_cast<int32_t*>(p);
+  int32_t* kA = reinterpret_cast<int32_t*>(p);
   p += al256((n + 1) * 4);
-  int32_t* v2 = reinterpret_cast<int32_t*>(p);
+  int32_t* kB = reinterpret_cast<int32_t*>(p);
+  p += al256((n + 1) * 4);
+  int32_t* vA = reinterpret_cast<int32_t*>(p);
   const int passes = n_keys <= kMsKeys ? 1 : 2;
-  // LSD passes: pass 0 on the low 9 bits, pass 1 (if any) on the next 9.
   const int32_t* ck = d_keys;
   const int32_t* cv = d_vals;
+  const int64_t* cur_n = d_n;
   for (int pass = 0; pass < passes; ++pass) {
     const int shift = 9 * pass;
     const bool last = pass == passes - 1;
-    int32_t* ok = last ? k2 : k2;  // keys always go to scratch
-    int32_t* ov = last ? d_out : v2;
-    if (!last) ov = v2;
-    k_ms_hist<<<static_cast<unsigned>(tiles), kMsBlock, 0, st>>>(ck, n, shift, static_cast<int>(tiles), counts);
+    int32_t* ok = pass == 0 ? kA : kB;
+    int32_t* ov = last ? d_out : vA;
+    k_ms_hist<<<static_cast<unsigned>(tiles), kMsBlock, 0, st>>>(ck, n, shift, static_cast<int>(tiles), counts,
+                                                                  cur_n);
     exclusive_scan<int32_t>(counts, offs, cn, stmp, st, launches);
-    if (last) PUMP_CUDA(cudaMemcpyAsync(d_count, offs + cn, 8, cudaMemcpyDeviceToDevice, st));
+    PUMP_CUDA(cudaMemcpyAsync(d_count, offs + cn, 8, cudaMemcpyDeviceToDevice, st));
     k_ms_scatter<<<static_cast<unsigned>(tiles), kMsBlock, 0, st>>>(ck, cv, n, shift, static_cast<int>(tiles), offs,
-                                                                     ok, ov);
+                                                                     ok, ov, cur_n);
     *launches += 2;
-    ck = k2;
-    cv = v2;
+    ck = ok;
+    cv = ov;
+    cur_n = d_count;  // pass 2 sees only the kept items
   }
   PUMP_CUDA(cudaGetLastError());
 }

@@ -17,16 +17,20 @@ constexpr int kScanTile = kScanBlock * kScanItems;  // 4096
 size_t scan_temp_bytes(int64_t n);
 
 // out[0..n] = exclusive prefix sums of in[0..n) (out[n] = total), int64.
+// If d_n is given the item count is read on the device (n is then only the
+// upper bound used to size the grid).
 // InT is int32_t, int64_t or uint8_t.  Stream-ordered, no host sync.
 template <class InT>
-void exclusive_scan(const InT* d_in, int64_t* d_out, int64_t n, void* d_temp, cudaStream_t st, int64_t* launches);
+void exclusive_scan(const InT* d_in, int64_t* d_out, int64_t n, void* d_temp, cudaStream_t st, int64_t* launches,
+                    const int64_t* d_n = nullptr);
 
 // Stable multisplit: given n items with keys in [0, n_keys) (key < 0 means
 // "drop"), writes the values ordered by (key, original position) into out,
 // and the number of kept items to *d_count.  n_keys <= 1024.
 size_t multisplit_temp_bytes(int64_t n, int n_keys);
 void stable_multisplit(const int32_t* d_keys, const int32_t* d_vals, int64_t n, int n_keys, int32_t* d_out,
-                       int64_t* d_count, void* d_temp, cudaStream_t st, int64_t* launches);
+                       int64_t* d_count, void* d_temp, cudaStream_t st, int64_t* launches,
+                       const int64_t* d_n = nullptr);
 
 // ------------------------------------------------------------ warp helpers
 __device__ __forceinline__ int64_t warp_incl_scan(int64_t x) {

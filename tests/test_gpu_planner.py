@@ -1,0 +1,205 @@
+"""GPU parity of graph build (K_graph), the explore wavefront (K_hsmc +
+dominance + frontier compaction) and the full run_pump pipeline against the
+CPU oracle, through the C ABI.
+
+Bar: bit-exact edges (cost/tau/coefficients/half-spaces compared by bit
+pattern), bit-exact plan arenas (head, parent, cost, cp_hat, t_end, masks),
+identical Pareto sets, goal plans, statistics and selected plan; certified CP
+and costs bit-identical.
+"""
+import json
+import os
+
+import numpy as np
+import pytest
+
+from conftest import scenario_text
+
+pytestmark = pytest.mark.gpu
+
+WORKERS = max(1, min(16, os.cpu_count() or 4))
+
+
+def ws_of(j):
+    w = j["workspace"]
+    dw = len(w["bounds"]["lo"])
+    obs = w.get("obstacles", [])
+    return {"bounds_lo": w["bounds"]["lo"], "bounds_hi": w["bounds"]["hi"],
+            "obs_lo": np.array([o["lo"] for o in obs], float).reshape(-1, dw),
+            "obs_hi": np.array([o["hi"] for o in obs], float).reshape(-1, dw)}
+
+
+def goal_of(j):
+    return {"lo": j["goal"]["lo"], "hi": j["goal"]["hi"], "max_speed": j["goal"].get("max_speed", 0.0)}
+
+
+def with_samples(name, samples=None, **kw):
+    j = json.loads(scenario_text(name))
+    if samples is not None:
+        j["samples"] = samples
+    j.update(kw)
+    return json.dumps(j)
+
+
+def assert_graph_equal(a, b):
+    for k in ("n_nodes", "dw", "n_edges", "n_waypoints", "n_halfspaces", "n_goal"):
+        assert a[k] == b[k], k
+    for k in ("row_ptr", "edge_to", "edge_nsteps", "edge_wp_off", "wp_hs_off", "hs_fallback", "goal_nodes"):
+        assert np.array_equal(a[k], b[k]), k
+    for k in ("edge_cost", "edge_tau", "edge_acc0", "edge_jerk", "hs_a", "hs_b"):
+        assert np.array_equal(a[k].view(np.uint64), b[k].view(np.uint64)), k
+
+
+GRAPH_CASES = [("minimal", None), ("three_obstacle", 300), ("indoor", 400), ("quad3d_three_obstacle", 500),
+               ("quad3d_indoor", 600)]
+
+
+@pytest.mark.parametrize("name,samples", GRAPH_CASES)
+def test_build_graph_bit_exact(oracle_lib, gpu_ctx, name, samples):
+    from paper_1607_06886_b200 import api
+
+    txt = with_samples(name, samples)
+    j = json.loads(txt)
+    _, sc = oracle_lib.scenario_models(txt)
+    pos, vel = oracle_lib.scenario_nodes(txt)
+    args = (ws_of(j), goal_of(j), sc["r_n"], sc["dt"], sc["eps_cc"], sc["tau_max"])
+    og = oracle_lib.build_graph(pos, vel, *args, workers=WORKERS).export()
+    gg = api.build_graph(pos, vel, *args, ctx=gpu_ctx).export()
+    assert og["n_edges"] > 0
+    assert_graph_equal(gg, og)
+
+
+def test_build_graph_degenerate_and_complete(oracle_lib, gpu_ctx):
+    """test_plan.cpp:82-101: tiny radius -> no edges; huge radius -> complete."""
+    from paper_1607_06886_b200 import api
+
+    ws = {"bounds_lo": [-10.0, -10.0], "bounds_hi": [10.0, 10.0]}
+    goal = {"lo": [100.0, 100.0], "hi": [101.0, 101.0], "max_speed": 0.0}
+    pos = np.array([[0.0, 0], [5, 0], [9, 0]])
+    vel = np.zeros((3, 2))
+    assert api.build_graph(pos, vel, ws, goal, 1e-6, 0.1, 0.05, 200.0, ctx=gpu_ctx).edge_count == 0
+    g = api.build_graph(pos, vel, ws, goal, 1e6, 0.1, 0.05, 200.0, ctx=gpu_ctx).export()
+    assert g["n_edges"] == 6
+    assert np.array_equal(np.diff(g["edge_wp_off"]), g["edge_nsteps"])
+    with pytest.raises(ValueError):
+        api.build_graph(pos, vel, ws, goal, 0.0, 0.1, 0.05, 200.0, ctx=gpu_ctx)
+
+
+def random_graph_nodes(seed, n, obstacles):
+    """test_plan.cpp:58-78 random_zero_noise_graph node generator."""
+    import oracle
+
+    pos, vel = [[-8.0, -8.0]], [[0.0, 0.0]]
+    ws = {"bounds_lo": [-10.0, -10.0], "bounds_hi": [10.0, 10.0], "obs_lo": [o[0] for o in obstacles],
+          "obs_hi": [o[1] for o in obstacles]}
+    for i in range(n):
+        p = [18 * oracle.uniform(seed, i, 0, 0) - 9, 18 * oracle.uniform(seed, i, 0, 1) - 9]
+        v = [2 * oracle.uniform(seed, i, 1, 0) - 1, 2 * oracle.uniform(seed, i, 1, 1) - 1]
+        if not oracle.point_free(ws, p):
+            continue
+        pos.append(p)
+        vel.append(v)
+    return np.array(pos), np.array(vel), ws
+
+
+def explore_equal(a, b, masks=True):
+    for k in ("n_plans", "n_pareto", "n_goal_plans", "partial_plans", "discarded_cp", "removed_dominated",
+              "discarded_horizon", "rounds", "termination"):
+        assert a[k] == b[k], (k, a[k], b[k])
+    for k in ("head", "parent", "t_end", "pareto_ptr", "pareto_ids", "goal_plans"):
+        assert np.array_equal(a[k], b[k]), k
+    for k in ("cost", "cp_hat"):
+        assert np.array_equal(a[k].view(np.uint64), b[k].view(np.uint64)), k
+    if masks:
+        assert np.array_equal(a["masks"], b["masks"])
+
+
+@pytest.mark.parametrize("seed", [777, 200, 201])
+def test_explore_random_worlds(oracle_lib, gpu_ctx, seed):
+    """test_plan.cpp:188-227 setting (noisy bank, alpha band), records equal."""
+    from paper_1607_06886_b200 import api
+
+    obstacles = [([-1.0, -4.0], [1.0, 6.0])]
+    pos, vel, ws = random_graph_nodes(seed, 80, obstacles)
+    goal = {"lo": [5.0, 5.0], "hi": [9.0, 9.0], "max_speed": 0.6}
+    scn = {"workspace": {"bounds": {"lo": [-10, -10], "hi": [10, 10]},
+                         "obstacles": [{"lo": o[0], "hi": o[1]} for o in obstacles]},
+           "start": {"position": [-8, -8]}, "goal": {"lo": [5, 5], "hi": [9, 9], "max_speed": 0.6},
+           "noise": {"process": [0, 0, 0.02, 0.02], "measurement": 0.01, "initial": 0.005},
+           "dt": 0.25, "samples": 10, "alpha": 0.05}
+    cl, _ = oracle_lib.scenario_models(json.dumps(scn))
+    og = oracle_lib.build_graph(pos, vel, ws, goal, 9.0, 0.25, 0.05, 200.0, workers=WORKERS)
+    gg = api.build_graph(pos, vel, ws, goal, 9.0, 0.25, 0.05, 200.0, ctx=gpu_ctx)
+    assert_graph_equal(gg.export(), og.export())
+    bank = api.presample_bank(cl, 2048, 64, 9, ctx=gpu_ctx)
+    ref = oracle_lib.explore(og, bank, 0.01, 0.2, 0.5, 9.0, workers=WORKERS)
+    got = api.explore(gg, 0.01, 0.2, 0.5, 9.0, ctx=gpu_ctx)
+    assert ref["n_plans"] > 100
+    explore_equal(got, ref)
+
+
+@pytest.mark.parametrize("name,samples", [("minimal", None), ("three_obstacle", None),
+                                          ("quad3d_three_obstacle", 700), ("indoor", 500)])
+def test_explore_scenarios(oracle_lib, gpu_ctx, name, samples):
+    from paper_1607_06886_b200 import api
+
+    txt = with_samples(name, samples)
+    j = json.loads(txt)
+    cl, sc = oracle_lib.scenario_models(txt)
+    pos, vel = oracle_lib.scenario_nodes(txt)
+    args = (ws_of(j), goal_of(j), sc["r_n"], sc["dt"], sc["eps_cc"], sc["tau_max"])
+    og = oracle_lib.build_graph(pos, vel, *args, workers=WORKERS)
+    gg = api.build_graph(pos, vel, *args, ctx=gpu_ctx)
+    bank = api.presample_bank(cl, j.get("bank_horizon", 2048), j.get("particles", 128), 1, ctx=gpu_ctx)
+    eta = sc["eta"]
+    amin, amax = sc["alpha"] / eta, min(1.0, eta * sc["alpha"])
+    ref = oracle_lib.explore(og, bank, amin, amax, sc["lambda"], sc["r_n"], workers=WORKERS)
+    got = api.explore(gg, amin, amax, sc["lambda"], sc["r_n"], ctx=gpu_ctx)
+    explore_equal(got, ref)
+
+
+def test_explore_trivial_and_disconnected(oracle_lib, gpu_ctx):
+    """test_plan.cpp:160-186: start inside the goal; unreachable goal."""
+    from paper_1607_06886_b200 import api
+
+    zero = {"d": 4, "dw": 2, "F": np.eye(8), "Gv": np.zeros((8, 4)), "Gw": np.zeros((8, 2)), "Sv": np.zeros((4, 4)),
+            "Sw": np.zeros((2, 2)), "S0": np.zeros((4, 4)), "C": np.hstack([np.eye(2), np.zeros((2, 2))])}
+    api.presample_bank(zero, 64, 8, 1, ctx=gpu_ctx)
+    ws = {"bounds_lo": [-10.0, -10.0], "bounds_hi": [10.0, 10.0]}
+    pos = np.array([[0.0, 0.0], [5.0, 5.0]])
+    vel = np.zeros((2, 2))
+    g = api.build_graph(pos, vel, ws, {"lo": [-1, -1], "hi": [1, 1], "max_speed": 0.1}, 1e6, 0.25, 0.05, 200.0,
+                        ctx=gpu_ctx)
+    r = api.explore(g, 0.5, 1.0, 0.5, 1e6, ctx=gpu_ctx)
+    assert r["termination"] == "goal_below_alpha_min"
+    assert r["cost"][r["goal_plans"][0]] == 0.0
+    g2 = api.build_graph(pos, vel, ws, {"lo": [100, 100], "hi": [101, 101], "max_speed": 0.0}, 1e6, 0.25, 0.05,
+                         200.0, ctx=gpu_ctx)
+    r2 = api.explore(g2, 0.5, 1.0, 0.5, 1e6, ctx=gpu_ctx)
+    assert len(r2["goal_plans"]) == 0
+    assert r2["termination"] == "frontier_exhausted"
+
+
+def assert_run_equal(got, ref):
+    for k in ("success", "termination", "partial_plans", "path_len", "n_pareto", "n_mc_evals", "n_traj_points"):
+        assert got[k] == ref[k], (k, got[k], ref[k])
+    for k in ("cost", "certified_cp", "cp_hat", "pre_smoothing_cost", "smoothing_s"):
+        assert got[k] == ref[k], (k, got[k], ref[k])
+    assert np.array_equal(got["path"], ref["path"])
+    assert np.array_equal(got["mc_eval_ids"], ref["mc_eval_ids"])
+    assert np.array_equal(got["mc_eval_values"], ref["mc_eval_values"])
+    assert np.array_equal(got["pareto_cost"].view(np.uint64), ref["pareto_cost"].view(np.uint64))
+    assert np.array_equal(got["pareto_cp"], ref["pareto_cp"])
+    for k in ("traj_t", "traj_pos", "traj_vel", "traj_ctrl"):
+        assert np.array_equal(got[k].view(np.uint64), ref[k].view(np.uint64)), k
+
+
+@pytest.mark.parametrize("name,samples,mc", [("minimal", None, 4000), ("three_obstacle", None, 4000),
+                                             ("quad3d_three_obstacle", 800, 4000)])
+def test_run_pump_matches_oracle(oracle_lib, gpu_ctx, name, samples, mc):
+    from paper_1607_06886_b200 import api
+
+    txt = with_samples(name, samples, mc_samples=mc)
+    got = api.run_pump(api.parse_scenario(txt), ctx=gpu_ctx)
+    ref = oracle_lib.run_pump(txt, workers=WORKERS)
+    assert_run_equal(got, ref)
