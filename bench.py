@@ -1,0 +1,331 @@
+"""PUMP solve benchmark (BASELINE.json metric) on B200.
+
+Default workload = BASELINE configs[1]: the indoor/corridor quadrotor scenario
+(scenarios/quad3d_indoor.json: 6-D double integrator, 10 walls, n = 4000
+samples, 64 particles per plan, alpha = 2%, bisection + MC certification with
+20000 rollouts).  One step = one full PUMP solve (pump.hpp:170-263): Halton
+sampling, graph build, particle bank, Pareto exploration, Alg. 4 bisection with
+MC certification and CP-constrained smoothing.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                  [--config quad3d_indoor] [--no-cpu-baseline]
+
+Prints one JSON line on rank 0.  `value` = ms per solve with the scenario
+already parsed (the solve is a synchronous library call whose hot loops all
+run on the GPU; the host only orchestrates); `e2e` = the same solve through
+the C ABI starting from the JSON scenario text on the host and ending with the
+result arrays on the host.  Per-kernel times come from CUDA events recorded
+on the library stream around every launch of the timed region.  Under torchrun (N > 1) every rank runs the solve with
+the MC certification rollouts sharded across ranks (NCCL all-reduce of the
+int64 hit counts); time is the max over ranks.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+FAMILIES = ["bank_noise", "bank_rec", "hsmc", "mc", "connect", "collide", "emit", "regions", "expand", "commit",
+            "dom", "scan", "multisplit", "misc"]
+
+
+def mc_ops_per_step(d: int, dw: int, n_obs: int, segs: float = 3.0) -> float:
+    """Algorithmic FP64 arithmetic per MC rollout-step (compares excluded):
+    (d + dw) normals x 92 ops (2 unit maps, log 28, cos 56, sqrt, scaling),
+    the closed-loop gemvs 2(d*d + dw*dw + 2d*d + 2d*dw + 4d*d) + 4d, the output
+    map 2*dw*d + dw, the segment length (11) and the segment points (10 each)."""
+    normals = (d + dw) * 92
+    gemv = 2 * (d * d + dw * dw + 2 * d * d + 2 * d * dw + 4 * d * d) + 4 * d + 2 * dw * d + dw
+    return normals + gemv + 11 + 10 * segs
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.samples = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except FileNotFoundError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 8:
+                self.samples.append(parts)
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        reasons = set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for s in self.samples:
+            for k, nm in enumerate(names):
+                if s[4 + k].lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(self.samples)}
+
+
+def dist_setup():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl")
+    return world, rank, local
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+
+
+def max_over_ranks(x: float, world: int) -> float:
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def load_text(config: str) -> str:
+    with open(os.path.join(ROOT, "scenarios", config + ".json")) as f:
+        return f.read()
+
+
+def run_reference(args, world, rank):
+    """The reference's CPU path on the host cores: the oracle restatement (the
+    reference itself cannot be built here: Eigen is absent)."""
+    if rank != 0:
+        return
+    import oracle
+
+    text = load_text(args.config)
+    cores = os.cpu_count() or 1
+    for _ in range(min(args.warmup, 1)):
+        oracle.run_pump(text, workers=cores)
+    times = []
+    r = None
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        r = oracle.run_pump(text, workers=cores)
+        times.append(time.perf_counter() - t0)
+    ms = 1e3 * sum(times) / len(times)
+    line = {"impl": "reference", "metric": "PUMP solve time", "value": round(ms, 3), "unit": "ms",
+            "n_gpus": world, "steps": args.steps, "warmup": min(args.warmup, 1), "ms_per_step": round(ms, 3),
+            "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (Halton samples of the named scenario, counter-hash particles/rollouts)",
+            "config": {"workload": args.config, "samples": json.loads(text)["samples"],
+                       "particles": json.loads(text)["particles"], "alpha": json.loads(text)["alpha"]},
+            "cpu_baseline": {"value": round(ms, 3), "unit": "ms", "cores": cores, "kind": "port",
+                             "sample": "one full solve per step (oracle restatement, workers = all host threads)"},
+            "e2e": {"value": round(ms, 3), "unit": "ms", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "partial_plans": r["partial_plans"], "success": r["success"]}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="quad3d_indoor")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 0)
+    world, rank, local = dist_setup()
+    if args.impl == "reference":
+        run_reference(args, world, rank)
+        return
+
+    import numpy as np
+
+    from paper_1607_06886_b200 import api
+    import ctypes as C
+
+    L = api.lib()
+    L.pump_ctx_profile.argtypes = [C.c_void_p, C.c_int]
+    L.pump_ctx_profile_read.argtypes = [C.c_void_p] * 4
+    L.pump_ctx_io_bytes.argtypes = [C.c_void_p, C.c_void_p]
+    L.pump_ctx_flush_l2.argtypes = [C.c_void_p]
+    L.pump_peak_fp64.argtypes = [C.c_void_p, C.c_void_p]
+
+    text = load_text(args.config)
+    scn = json.loads(text)
+    ctx = api.Context(local)
+    sc = api.parse_scenario(text)
+    if world > 1 and hasattr(api, "set_comm"):
+        api.set_comm(ctx, rank, world)
+
+    def io():
+        b = np.zeros(3, dtype=np.int64)
+        L.pump_ctx_io_bytes(ctx.h, b.ctypes.data_as(C.c_void_p))
+        return b
+
+    # warm-up (buffers sized, modules loaded)
+    res = None
+    for _ in range(max(args.warmup, 3)):
+        res = api.run_pump(sc, ctx=ctx)
+
+    # ---- timed region: K device-timed solves, L2 flushed before each
+    import torch
+
+    barrier(world)
+    clocks = ClockSampler(local)
+    clocks.start()
+    L.pump_ctx_profile(ctx.h, 1)
+    launches0 = ctx.launches
+    io0 = io()
+    start = torch.cuda.Event(enable_timing=True)
+    end = torch.cuda.Event(enable_timing=True)
+    step_ms = []
+    torch.cuda.synchronize()
+    for _ in range(args.steps):
+        L.pump_ctx_flush_l2(ctx.h)
+        t0 = time.perf_counter()
+        res = api.run_pump(sc, ctx=ctx)  # synchronous: returns after the result is on the host
+        step_ms.append(1e3 * (time.perf_counter() - t0))
+    torch.cuda.synchronize()
+    io1 = io()
+    launches = ctx.launches - launches0
+    prof_ms = np.zeros(len(FAMILIES))
+    prof_n = np.zeros(len(FAMILIES), dtype=np.int64)
+    prof_w = np.zeros(len(FAMILIES), dtype=np.int64)
+    L.pump_ctx_profile_read(ctx.h, prof_ms.ctypes.data_as(C.c_void_p), prof_n.ctypes.data_as(C.c_void_p),
+                            prof_w.ctypes.data_as(C.c_void_p))
+    L.pump_ctx_profile(ctx.h, 0)
+    clk = clocks.stop()
+    barrier(world)
+    ms_per_step = max_over_ranks(sum(step_ms) / len(step_ms), world)
+
+    # ---- e2e: JSON text on the host -> parse -> solve -> result arrays on the host
+    barrier(world)
+    e_io0 = io()
+    e_ms = []
+    for _ in range(args.steps):
+        L.pump_ctx_flush_l2(ctx.h)
+        t0 = time.perf_counter()
+        s2 = api.parse_scenario(text)
+        r2 = api.run_pump(s2, ctx=ctx)
+        e_ms.append(1e3 * (time.perf_counter() - t0))
+        del s2
+    e_io1 = io()
+    e2e_ms = max_over_ranks(sum(e_ms) / len(e_ms), world)
+    assert r2["path"].tolist() == res["path"].tolist() and r2["certified_cp"] == res["certified_cp"]
+
+    # ---- roofline of the dominant kernel family (CUDA events over the timed region)
+    fam = int(np.argmax(prof_ms))
+    fam_name = FAMILIES[fam]
+    avg_launch_ms = prof_ms[fam] / max(1, prof_n[fam])
+    peak = C.c_double()
+    L.pump_peak_fp64(ctx.h, C.byref(peak))
+    roof = {"kernel": fam_name, "bound": "fp64", "unit": "GFLOP/s", "peak": round(peak.value, 1),
+            "peak_source": "measured: bench FP64 DMUL+DADD issue microbenchmark (no FMA, the parity op mix); "
+                           "MEASURED_PEAKS.json has no FP64 figure",
+            "share_of_step": round(float(prof_ms[fam] / max(1e-9, prof_ms.sum())), 3),
+            "avg_launch_ms": round(float(avg_launch_ms), 4), "launches": int(prof_n[fam]), "traffic": None}
+    d, dw = 2 * len(scn["workspace"]["bounds"]["lo"]), len(scn["workspace"]["bounds"]["lo"])
+    if fam_name == "mc":
+        ops = prof_w[fam] * mc_ops_per_step(d, dw, len(scn["workspace"]["obstacles"]))
+        roof["work"] = f"{int(prof_w[fam])} rollout-steps x {mc_ops_per_step(d, dw, len(scn['workspace']['obstacles'])):.0f} FP64 ops"
+    elif fam_name == "expand":
+        ops = prof_w[fam] * 2 * dw
+        roof["work"] = f"{int(prof_w[fam])} particle-halfspace tests x {2 * dw} FP64 ops"
+    else:
+        ops = 0.0
+        roof["work"] = f"{int(prof_w[fam])} work units (no FP64 op model for this family yet)"
+    achieved = ops / (prof_ms[fam] * 1e-3) / 1e9 if prof_ms[fam] > 0 else 0.0
+    roof["achieved"] = round(achieved, 1)
+    roof["frac"] = round(achieved / peak.value, 4) if peak.value > 0 else None
+    kernels = {FAMILIES[i]: {"ms_per_step": round(float(prof_ms[i] / args.steps), 3),
+                             "launches_per_step": round(float(prof_n[i] / args.steps), 1)}
+               for i in range(len(FAMILIES)) if prof_n[i] > 0}
+
+    # ---- CPU baseline: the reference path (oracle restatement) on this host
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        import oracle
+
+        cores = os.cpu_count() or 1
+        t0 = time.perf_counter()
+        o = oracle.run_pump(text, workers=cores)
+        cpu_s = time.perf_counter() - t0
+        same = (o["path"].tolist() == res["path"].tolist() and o["certified_cp"] == res["certified_cp"]
+                and o["cost"] == res["cost"] and o["partial_plans"] == res["partial_plans"])
+        cpu = {"value": round(1e3 * cpu_s, 1), "unit": "ms", "cores": cores, "kind": "port",
+               "sample": "one full solve of the same scenario (oracle restatement, workers = all host threads)",
+               "identical_result": bool(same)}
+
+    pp_s = res["partial_plans"] / (res["explore_seconds"]) if res["explore_seconds"] > 0 else None
+    mc_rs = res["mc_rollouts"] / (res["mc_ms"] * 1e-3) if res["mc_ms"] > 0 else None
+    line = {
+        "metric": "PUMP solve time", "value": round(ms_per_step, 3), "unit": "ms", "n_gpus": world,
+        "steps": args.steps, "warmup": max(args.warmup, 3), "ms_per_step": round(ms_per_step, 3),
+        "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (Halton samples of the named scenario; counter-hash particle bank and MC rollouts)",
+        "config": {"workload": args.config, "samples": scn["samples"], "particles": scn["particles"],
+                   "alpha": scn["alpha"], "mc_samples": scn["mc_samples"], "obstacles": len(scn["workspace"]["obstacles"]),
+                   "l2": "256 MiB buffer overwritten before every timed solve"},
+        "e2e": {"value": round(e2e_ms, 3), "unit": "ms",
+                "h2d_bytes_per_step": int((e_io1[0] - e_io0[0]) // args.steps),
+                "d2h_bytes_per_step": int((e_io1[1] - e_io0[1]) // args.steps)},
+        "gpu_launches": int(launches // args.steps), "gpu_launches_total": int(launches),
+        "clocks": clk, "roofline": roof, "cpu_baseline": cpu, "kernels": kernels,
+        "solve": {"success": res["success"], "cost": res["cost"], "certified_cp": res["certified_cp"],
+                  "partial_plans": res["partial_plans"], "n_edges": res["n_edges"], "n_plans": res["n_plans"],
+                  "build_graph_ms": round(1e3 * res["build_graph_seconds"], 3),
+                  "explore_ms": round(1e3 * res["explore_seconds"], 3),
+                  "selection_ms": round(1e3 * res["selection_seconds"], 3)},
+        "partial_plans_per_s": round(pp_s, 1) if pp_s else None,
+        "mc_rollouts_per_s": round(mc_rs, 1) if mc_rs else None,
+    }
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

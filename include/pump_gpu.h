@@ -147,6 +147,17 @@ int pump_ctx_destroy(pump_ctx* ctx);
 double pump_ctx_last_kernel_ms(pump_ctx* ctx);
 /* Number of kernel launches issued by this ctx since creation. */
 int64_t pump_ctx_launch_count(pump_ctx* ctx);
+/* Measurement hooks (bench.py): per-kernel-family CUDA-event timing on the
+ * launching stream; read returns total ms, launch counts and algorithmic work
+ * units per family (PUMP_FAM_* order) and resets them. */
+int pump_ctx_profile(pump_ctx* ctx, int enable);
+int pump_ctx_profile_read(pump_ctx* ctx, double* ms, int64_t* counts, int64_t* work);
+/* out[0] host->device bytes, out[1] device->host bytes, out[2] MC rollout-steps. */
+int pump_ctx_io_bytes(pump_ctx* ctx, int64_t* out);
+/* Overwrite a 256 MiB buffer (> 126 MB L2) on the ctx stream and synchronize. */
+int pump_ctx_flush_l2(pump_ctx* ctx);
+/* FP64 DMUL+DADD issue-rate microbenchmark, Gop/s (roofline denominator). */
+int pump_peak_fp64(pump_ctx* ctx, double* gops);
 
 /* ------------------------------------------------------------- scenario */
 /* load_scenario / parse_scenario / build_models (scenario.hpp:144-301). */

@@ -79,6 +79,8 @@ int pump_ctx_destroy(pump_ctx* ctx) {
     cudaSetDevice(ctx->c.device);
     cudaStreamSynchronize(ctx->c.stream);
     ctx->c.scratch.clear();
+    ctx->c.run_graph.reset();
+    ctx->c.run_explore.reset();
     ctx->c.bank.release();
     cudaEventDestroy(ctx->c.ev0);
     cudaEventDestroy(ctx->c.ev1);
@@ -270,16 +272,20 @@ int pump_mc_certify_batch(pump_ctx* ctx, const pump_closed_loop* cl, const pump_
     const int64_t n_pts = traj_off[n_traj];
     DBuf& off = c.buf("mc_off", (n_traj + 1) * 8);
     DBuf& yn = c.buf("mc_ynom", n_pts * L.dw * 8);
-    DBuf& hits = c.buf("mc_hits", n_traj * 8);
+    DBuf& hits = c.buf("mc_hits", (n_traj + 1) * 8);
     c.h2d(off.p, traj_off, (n_traj + 1) * 8);
     c.h2d(yn.p, y_nom, n_pts * L.dw * 8);
-    PUMP_CUDA(cudaMemsetAsync(hits.p, 0, n_traj * 8, c.stream));
+    PUMP_CUDA(cudaMemsetAsync(hits.p, 0, (n_traj + 1) * 8, c.stream));
     c.tic();
     launch_mc(L, w, n_traj, off.as<int64_t>(), yn.as<double>(), max_pts, rollout_lo, rollout_hi, seed, eps_cc,
-              hits.as<unsigned long long>(), c.stream, &c.launches);
+              hits.as<unsigned long long>(), c.stream, &c.launches, hits.as<unsigned long long>() + n_traj);
     c.toc();
-    c.d2h(hits_out, hits.p, n_traj * 8);
+    std::vector<int64_t> hv(n_traj + 1);
+    c.d2h(hv.data(), hits.p, (n_traj + 1) * 8);
     c.sync();
+    std::copy(hv.begin(), hv.begin() + n_traj, hits_out);
+    kprof_work(F_MC, hv[n_traj]);
+    c.mc_rollout_steps += hv[n_traj];
   });
 }
 
@@ -292,6 +298,111 @@ int pump_mc_certify(pump_ctx* ctx, const pump_closed_loop* cl, const pump_worksp
   int rc = pump_mc_certify_batch(ctx, cl, ws, 1, off, y_nom, 0, n_mc, seed, eps_cc, &hits);
   if (rc == PUMP_OK) *value_out = static_cast<double>(hits) / n_mc;
   return rc;
+}
+
+}  // extern "C"
+
+// ------------------------------------------------------ measurement hooks
+namespace pumpg {
+
+KProf*& kprof_current() {
+  static KProf* p = nullptr;
+  return p;
+}
+
+// FP64 issue-rate microbenchmark: 8 independent DMUL+DADD chains per thread
+// (no FMA: --fmad=false), the op mix of the parity-bound kernels.
+__global__ void __launch_bounds__(256) k_peak_fp64(double* out, int iters, double a, double b) {
+  double x[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) x[k] = threadIdx.x * 1e-3 + k;
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) x[k] = x[k] * a + b;  // DMUL + DADD (no contraction)
+  }
+  double s = 0;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) s += x[k];
+  if (s == 12345.678) out[0] = s;  // keep the work alive
+}
+
+__global__ void k_flush(uint4* p, size_t n) {
+  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<size_t>(gridDim.x) * blockDim.x)
+    p[i] = make_uint4(static_cast<unsigned>(i), 0u, 0u, 0u);
+}
+
+}  // namespace pumpg
+
+extern "C" {
+
+int pump_ctx_profile(pump_ctx* ctx, int enable) {
+  return guard([&] {
+    KProf& p = ctx->c.prof;
+    p.on = enable != 0;
+    kprof_current() = enable ? &p : nullptr;
+    if (enable) {
+      for (int f = 0; f < F_COUNT; ++f) {
+        p.ms[f] = 0;
+        p.count[f] = 0;
+        p.work[f] = 0;
+      }
+    }
+  });
+}
+
+// per kernel family: total ms, launches, work units (resets the totals)
+int pump_ctx_profile_read(pump_ctx* ctx, double* ms, int64_t* counts, int64_t* work) {
+  return guard([&] {
+    Ctx& c = ctx->c;
+    c.sync();
+    KProf& p = c.prof;
+    p.resolve();
+    for (int f = 0; f < F_COUNT; ++f) {
+      ms[f] = p.ms[f];
+      counts[f] = p.count[f];
+      work[f] = p.work[f];
+      p.ms[f] = 0;
+      p.count[f] = 0;
+      p.work[f] = 0;
+    }
+  });
+}
+
+int pump_ctx_io_bytes(pump_ctx* ctx, int64_t* out) {
+  out[0] = ctx->c.h2d_bytes;
+  out[1] = ctx->c.d2h_bytes;
+  out[2] = ctx->c.mc_rollout_steps;
+  return PUMP_OK;
+}
+
+// Overwrite a buffer larger than the 126 MB L2 (cold-cache timing hygiene).
+int pump_ctx_flush_l2(pump_ctx* ctx) {
+  return guard([&] {
+    Ctx& c = ctx->c;
+    const size_t bytes = size_t(256) << 20;
+    DBuf& b = c.buf("l2_flush", bytes);
+    k_flush<<<148 * 8, 256, 0, c.stream>>>(b.as<uint4>(), bytes / sizeof(uint4));
+    ++c.launches;
+    PUMP_CUDA(cudaGetLastError());
+    c.sync();
+  });
+}
+
+// Measured FP64 (DMUL/DADD, no FMA) issue rate in Gop/s.
+int pump_peak_fp64(pump_ctx* ctx, double* gops) {
+  return guard([&] {
+    Ctx& c = ctx->c;
+    DBuf& o = c.buf("peak_out", 256);
+    const int blocks = 148 * 16, threads = 256, iters = 4096;
+    k_peak_fp64<<<blocks, threads, 0, c.stream>>>(o.as<double>(), 64, 0.999, 1e-3);  // warm-up
+    c.tic();
+    k_peak_fp64<<<blocks, threads, 0, c.stream>>>(o.as<double>(), iters, 0.999, 1e-3);
+    const double ms = c.toc();
+    c.launches += 2;
+    const double ops = 2.0 * 8 * iters * static_cast<double>(blocks) * threads;
+    *gops = ops / (ms * 1e-3) / 1e9;
+  });
 }
 
 }  // extern "C"

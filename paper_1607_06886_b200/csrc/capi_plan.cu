@@ -312,18 +312,20 @@ static std::vector<double> mc_values(Ctx& c, const HostLoop& L, const DevWorld& 
   const int nt = static_cast<int>(trajs.size());
   DBuf& d_off = c.buf("r_mc_off", (nt + 1) * 8 + 256);
   DBuf& d_y = c.buf("r_mc_y", y.size() * 8 + 256);
-  DBuf& d_h = c.buf("r_mc_hits", nt * 8 + 256);
+  DBuf& d_h = c.buf("r_mc_hits", (nt + 1) * 8 + 256);
   c.h2d(d_off.p, off.data(), (nt + 1) * 8);
   c.h2d(d_y.p, y.data(), y.size() * 8);
-  PUMP_CUDA(cudaMemsetAsync(d_h.p, 0, nt * 8, c.stream));
+  PUMP_CUDA(cudaMemsetAsync(d_h.p, 0, (nt + 1) * 8, c.stream));
   c.tic();
   launch_mc(L, w, nt, d_off.as<int64_t>(), d_y.as<double>(), max_pts, 0, n_mc, seed, eps_cc,
-            d_h.as<unsigned long long>(), c.stream, &c.launches);
+            d_h.as<unsigned long long>(), c.stream, &c.launches, d_h.as<unsigned long long>() + nt);
   *mc_ms += c.toc();
   *rollouts += static_cast<int64_t>(n_mc) * nt;
-  std::vector<int64_t> hits(nt);
-  c.d2h(hits.data(), d_h.p, nt * 8);
+  std::vector<int64_t> hits(nt + 1);
+  c.d2h(hits.data(), d_h.p, (nt + 1) * 8);
   c.sync();
+  kprof_work(F_MC, hits[nt]);
+  c.mc_rollout_steps += hits[nt];
   std::vector<double> v(nt);
   for (int j = 0; j < nt; ++j) v[j] = static_cast<double>(hits[j]) / n_mc;
   return v;
@@ -470,7 +472,9 @@ static void run_pump_device(Ctx& c, const pumpb::Scenario& s, const DevGraph* pr
   DevWorld dwld = upload_world(c, &pw, "run_ws_");
 
   auto t0 = clk::now();
-  DevGraph local;
+  if (!c.run_graph) c.run_graph = std::make_shared<DevGraph>();
+  if (!c.run_explore) c.run_explore = std::make_shared<DevExplore>();
+  DevGraph& local = *c.run_graph;
   const DevGraph* graph = prebuilt;
   if (!graph) {
     std::vector<double> pos, vel;
@@ -500,7 +504,7 @@ static void run_pump_device(Ctx& c, const pumpb::Scenario& s, const DevGraph* pr
     c.bank_horizon = s.bank_horizon;
     c.bank_dw = dw;
   }
-  DevExplore X;
+  DevExplore& X = *c.run_explore;
   const double eta = s.effective_eta();
   ExploreArgs ea{s.alpha / eta, std::min(1.0, eta * s.alpha), s.lambda, r_n};
   run_explore_device(X, c, *graph, ea);

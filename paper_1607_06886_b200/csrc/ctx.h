@@ -8,7 +8,12 @@
 #include "gpu/kernels.h"
 #include "host/scenario.hpp"
 
+#include <memory>
+
 namespace pumpg {
+
+struct DevGraph;
+struct DevExplore;
 
 struct DBuf {
   void* p = nullptr;
@@ -57,9 +62,15 @@ struct Ctx {
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   int64_t launches = 0;
   double last_ms = 0;
+  int64_t h2d_bytes = 0, d2h_bytes = 0, mc_rollout_steps = 0;
+  KProf prof;
   // resident particle bank
   DBuf bank;
   int bank_n = 0, bank_horizon = 0, bank_dw = 0;
+  // persistent solve state of run_pump (graph + explore arena stay resident
+  // in HBM across solves: no per-solve cudaMalloc/cudaFree)
+  std::shared_ptr<DevGraph> run_graph;
+  std::shared_ptr<DevExplore> run_explore;
   // named scratch buffers
   std::map<std::string, DBuf> scratch;
   DBuf& buf(const std::string& name, size_t bytes) {
@@ -70,9 +81,11 @@ struct Ctx {
   void sync() { PUMP_CUDA(cudaStreamSynchronize(stream)); }
   void h2d(void* d, const void* h, size_t bytes) {
     if (bytes) PUMP_CUDA(cudaMemcpyAsync(d, h, bytes, cudaMemcpyHostToDevice, stream));
+    h2d_bytes += static_cast<int64_t>(bytes);
   }
   void d2h(void* h, const void* d, size_t bytes) {
     if (bytes) PUMP_CUDA(cudaMemcpyAsync(h, d, bytes, cudaMemcpyDeviceToHost, stream));
+    d2h_bytes += static_cast<int64_t>(bytes);
   }
   void tic() { PUMP_CUDA(cudaEventRecord(ev0, stream)); }
   double toc() {

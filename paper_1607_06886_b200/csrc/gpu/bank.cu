@@ -104,11 +104,17 @@ void launch_bank(const HostLoop& HL, int n, int T, uint64_t seed, double* d_dy, 
       const int tc = std::min(kChunk, T - t0);  // steps advanced in this chunk
       if (tc > 0) {
         const int64_t items = static_cast<int64_t>(tc) * n;
+        KScope ks(st, F_BANK_NOISE);
         k_bank_noise<D, DW><<<grid_for(items, 128), 128, 0, st>>>(L, n, t0, tc, seed, uw);
         ++*launches;
+        kprof_work(F_BANK_NOISE, items);
       }
-      k_bank_rec<D, DW><<<grid_for(n, 32), 32, 0, st>>>(L, n, T, t0, tc, seed, uw, zs, d_dy);
-      ++*launches;
+      {
+        KScope ks(st, F_BANK_REC);
+        k_bank_rec<D, DW><<<grid_for(n, 32), 32, 0, st>>>(L, n, T, t0, tc, seed, uw, zs, d_dy);
+        ++*launches;
+        kprof_work(F_BANK_REC, static_cast<int64_t>(tc) * n);
+      }
       if (tc < kChunk) break;
     }
     PUMP_CUDA(cudaGetLastError());

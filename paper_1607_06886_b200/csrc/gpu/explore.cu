@@ -101,6 +101,9 @@ __global__ void __launch_bounds__(256) k_expand(const ExpandArgs a) {
 #pragma unroll
   for (int c = 0; c < CH; ++c) kill[c] = false;
   const int64_t w0 = a.wp_off[e];
+  if (lane == 0)
+    atomicAdd(reinterpret_cast<unsigned long long*>(&a.st->hs_tests),
+              static_cast<unsigned long long>(a.hs_off[w0 + ns] - a.hs_off[w0]));
   for (int j = 0; j < ns; ++j) {
     const int64_t h0 = a.hs_off[w0 + j], h1 = a.hs_off[w0 + j + 1];
     if (h0 == h1) continue;
@@ -471,8 +474,7 @@ void run_explore_device(DevExplore& X, Ctx& c, const DevGraph& G, const ExploreA
     while (p < q) p <<= 1;
     return p;
   }();
-  X.cap = 0;
-  X.n_plans = 0;
+  X.n_plans = 0;  // buffers (and their capacity) persist across solves
   ensure_arena(X, 1 << 16, st);
   if (!X.status_h) PUMP_CUDA(cudaMallocHost(&X.status_h, sizeof(ExploreStatus)));
   X.status_d.ensure(al(sizeof(ExploreStatus)) + 256);
@@ -542,7 +544,7 @@ void run_explore_device(DevExplore& X, Ctx& c, const DevGraph& G, const ExploreA
   int64_t T0 = 0;
   {
     std::vector<int64_t> rp(2);
-    PUMP_CUDA(cudaMemcpyAsync(rp.data(), G.row_ptr.p, 16, cudaMemcpyDeviceToHost, st));
+    c.d2h(rp.data(), G.row_ptr.p, 16);
     c.sync();
     T0 = rp[1] - rp[0];
   }
@@ -603,6 +605,7 @@ void run_explore_device(DevExplore& X, Ctx& c, const DevGraph& G, const ExploreA
                     X.cand_src.as<int32_t>(), X.cand_tend.as<int32_t>(), X.cand_cost.as<double>(),
                     X.cand_cp.as<double>(), X.cand_mask.as<uint64_t>(), S};
       const unsigned grid = grid_for(T * 32, 256);
+      KScope ks(st, F_EXPAND);
       dispatch_dw(G.dw, [&]<int DW>() {
         switch (ch) {
           case 1: k_expand<DW, 1><<<grid, 256, 0, st>>>(ea); break;
@@ -625,6 +628,7 @@ void run_explore_device(DevExplore& X, Ctx& c, const DevGraph& G, const ExploreA
                   X.flags.as<uint8_t>(), X.new_cnt.as<int32_t>(), X.new_slot.as<int32_t>(),
                   X.touched.as<int32_t>(), S};
     if (T > 0) {
+      KScope ks(st, F_COMMIT);
       k_commit<<<grid_for(T, 256), 256, 0, st>>>(ca);
       ++c.launches;
     }
@@ -646,6 +650,7 @@ void run_explore_device(DevExplore& X, Ctx& c, const DevGraph& G, const ExploreA
                                                       X.mem_cnt.as<int32_t>(), X.new_slot.as<int32_t>(),
                                                       new_ids.as<int32_t>());
       const unsigned gd = static_cast<unsigned>(std::min<int64_t>(std::max<int64_t>(T, 1), 148 * 16));
+      KScope ks(st, F_DOM);
       k_dom<<<gd, 128, 0, st>>>(S, X.touched.as<int32_t>(), off2.as<int64_t>(), X.mem_cnt.as<int32_t>(),
                                 X.new_cnt.as<int32_t>(), new_ids.as<int32_t>(), X.cost.as<double>(),
                                 X.cp.as<double>(), X.flags.as<uint8_t>(), X.drop.as<uint8_t>(),
@@ -702,13 +707,15 @@ void run_explore_device(DevExplore& X, Ctx& c, const DevGraph& G, const ExploreA
     ++c.launches;
     X.pool_flip = !X.pool_flip;
     PUMP_CUDA(cudaGetLastError());
-    PUMP_CUDA(cudaMemcpyAsync(X.status_h, S, sizeof(ExploreStatus), cudaMemcpyDeviceToHost, st));
+    c.d2h(X.status_h, S, sizeof(ExploreStatus));
     c.sync();
     h = *X.status_h;
     X.n_plans = h.n_plans;
     if (h.err) throw std::runtime_error("explore: device error " + std::to_string(h.err));
   }
   X.kernel_ms = c.toc();
+  kprof_work(F_EXPAND, h.hs_tests * N);
+  X.hs_tests = h.hs_tests;
   X.n_plans = h.n_plans;
   X.disc_cp = h.disc_cp;
   X.disc_hor = h.disc_hor;

@@ -8,7 +8,7 @@ namespace pumpg {
 struct ExploreStatus {  // read back once per round (pinned)
   long long G, T, K, n_plans, open_count, i, max_bucket, min_bucket, pool_n;
   long long best_goal_bits, min_group_bits;
-  long long disc_cp, disc_hor, removed, n_surv, evicted_open, err, touched;
+  long long disc_cp, disc_hor, removed, n_surv, evicted_open, err, touched, hs_tests;
 };
 
 struct DevExplore {
@@ -25,7 +25,7 @@ struct DevExplore {
   DBuf status_d;
   ExploreStatus* status_h = nullptr;  // pinned
   // results
-  int64_t n_plans = 0, partial_plans = 0, disc_cp = 0, disc_hor = 0, removed = 0;
+  int64_t n_plans = 0, partial_plans = 0, disc_cp = 0, disc_hor = 0, removed = 0, hs_tests = 0;
   int rounds = 0;
   int termination = 0;  // 0 goal_below_alpha_min, 1 frontier_exhausted
   double kernel_ms = 0;

@@ -424,12 +424,14 @@ void build_graph_device(DevGraph& G, Ctx& c, int n, int dw, const double* h_pos,
     DBuf& cuB = c.buf("g_cu", al(static_cast<size_t>(n) * cap * 4));
     DBuf& ctB = c.buf("g_ctau", al(static_cast<size_t>(n) * cap * 8));
     DBuf& ccB = c.buf("g_ccost", al(static_cast<size_t>(n) * cap * 8));
+    KScope ks(st, F_CONNECT);
     dispatch_dw(dw, [&]<int DW>() {
       k_connect_rows<DW><<<n, kRowBlock, 0, st>>>(ga, cap, rcnt.as<int32_t>(), cuB.as<int32_t>(), ctB.as<double>(),
                                                  ccB.as<double>());
     });
     ++c.launches;
     PUMP_CUDA(cudaGetLastError());
+    kprof_work(F_CONNECT, static_cast<int64_t>(n) * (n - 1));
     std::vector<int32_t> cnt(n);
     c.d2h(cnt.data(), rcnt.p, n * 4);
     c.sync();
@@ -451,6 +453,7 @@ void build_graph_device(DevGraph& G, Ctx& c, int n, int dw, const double* h_pos,
   DBuf& eoff = c.buf("g_eoff", al((n_cand + 2) * 8));
   DBuf& stmp2 = c.buf("g_scantmp2", scan_temp_bytes(n_cand + 16));
   if (n_cand > 0) {
+    KScope ks(st, F_COLLIDE);
     dispatch_dw(dw, [&]<int DW>() {
       if (wsmem > 48 * 1024)
         PUMP_CUDA(cudaFuncSetAttribute(k_collide<DW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wsmem));
@@ -474,6 +477,8 @@ void build_graph_device(DevGraph& G, Ctx& c, int n, int dw, const double* h_pos,
   G.e_nsteps.ensure(al((E + 1) * 4));
   G.row_ptr.ensure(al((n + 1) * 8));
   G.wp_off.ensure(al((E + 2) * 8));
+  {
+  KScope ks(st, F_EMIT);
   dispatch_dw(dw, [&]<int DW>() {
     const int64_t items = std::max<int64_t>(n_cand, n + 1);
     k_emit_edges<DW><<<grid_for(items, 256), 256, 0, st>>>(
@@ -482,6 +487,7 @@ void build_graph_device(DevGraph& G, Ctx& c, int n, int dw, const double* h_pos,
         G.e_tau.as<double>(), G.e_acc0.as<double>(), G.e_jerk.as<double>(), G.e_nsteps.as<int32_t>(),
         G.row_ptr.as<int64_t>());
   });
+  }
   ++c.launches;
   PUMP_CUDA(cudaGetLastError());
   DBuf& stmp3 = c.buf("g_scantmp3", scan_temp_bytes(E + 16));
@@ -495,6 +501,7 @@ void build_graph_device(DevGraph& G, Ctx& c, int n, int dw, const double* h_pos,
   G.hs_off.ensure(al((NW + 2) * 8));
   PUMP_CUDA(cudaMemsetAsync(err.p, 0, 4, st));
   if (NW > 0) {
+    KScope ks(st, F_REGIONS);
     dispatch_dw(dw, [&]<int DW>() {
       if (wsmem > 48 * 1024) {
         PUMP_CUDA(cudaFuncSetAttribute(k_regions<DW, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wsmem));
@@ -521,6 +528,7 @@ void build_graph_device(DevGraph& G, Ctx& c, int n, int dw, const double* h_pos,
   G.hs_b.ensure(al((H + 1) * 8));
   G.hs_fb.ensure(al(H + 1));
   if (NW > 0) {
+    KScope ks(st, F_REGIONS);
     dispatch_dw(dw, [&]<int DW>() {
       k_regions<DW, true><<<grid_for(NW, 128), 128, wsmem, st>>>(
           ga, wd, NW, E, G.wp_off.as<int64_t>(), G.e_from.as<int32_t>(), G.e_to.as<int32_t>(), G.e_tau.as<double>(),

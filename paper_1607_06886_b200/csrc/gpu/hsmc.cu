@@ -108,6 +108,7 @@ void launch_hsmc_batch(int dw, int n, int horizon, const double* d_dy, int64_t n
   if (n_words != (n + 63) / 64) throw std::invalid_argument("hsmc_extend: mask word count does not match the bank");
   const int ch = chunks_for(n);
   dim3 g(grid_for(n_tasks * 32, 256));
+  KScope ks(st, F_HSMC);
   dispatch_dw(dw, [&]<int DW>() {
     hsmc_dispatch_ch<DW>(ch, g, st, d_dy, n, horizon, n_tasks, n_words, d_in, d_step_off, d_step_t, d_step_hs_off,
                          d_hs_a, d_hs_b, d_out, d_pop, d_err);

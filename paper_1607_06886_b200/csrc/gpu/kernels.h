@@ -22,6 +22,76 @@ inline void cuda_check(cudaError_t e, const char* what) {
 }
 #define PUMP_CUDA(x) ::pumpg::cuda_check((x), #x)
 
+// ------------------------------------------------------- kernel profiler
+// Kernel families timed with CUDA events on the launching stream when a
+// profiler is active on this host thread (pump_ctx_profile).
+enum KFam {
+  F_BANK_NOISE, F_BANK_REC, F_HSMC, F_MC, F_CONNECT, F_COLLIDE, F_EMIT, F_REGIONS,
+  F_EXPAND, F_COMMIT, F_DOM, F_SCAN, F_SPLIT, F_MISC, F_COUNT
+};
+
+struct KProf {
+  bool on = false;
+  struct Rec {
+    int fam;
+    cudaEvent_t a, b;
+  };
+  std::vector<Rec> recs;
+  std::vector<cudaEvent_t> pool;
+  double ms[F_COUNT] = {0};
+  int64_t count[F_COUNT] = {0};
+  // algorithmic work units per family (e.g. MC rollout-steps, steer_cost evals)
+  int64_t work[F_COUNT] = {0};
+  cudaEvent_t get() {
+    if (pool.empty()) {
+      cudaEvent_t e;
+      cuda_check(cudaEventCreate(&e), "cudaEventCreate");
+      return e;
+    }
+    cudaEvent_t e = pool.back();
+    pool.pop_back();
+    return e;
+  }
+  void resolve() {  // caller synchronized the stream
+    for (auto& r : recs) {
+      float x = 0;
+      cuda_check(cudaEventElapsedTime(&x, r.a, r.b), "cudaEventElapsedTime");
+      ms[r.fam] += x;
+      count[r.fam] += 1;
+      pool.push_back(r.a);
+      pool.push_back(r.b);
+    }
+    recs.clear();
+  }
+};
+
+KProf*& kprof_current();
+
+struct KScope {
+  KProf* p;
+  int fam;
+  cudaStream_t st;
+  cudaEvent_t a = nullptr;
+  KScope(cudaStream_t s, int f) : p(kprof_current()), fam(f), st(s) {
+    if (p && p->on) {
+      a = p->get();
+      cuda_check(cudaEventRecord(a, st), "cudaEventRecord");
+    }
+  }
+  ~KScope() {
+    if (p && p->on && a) {
+      cudaEvent_t b = p->get();
+      cudaEventRecord(b, st);
+      p->recs.push_back({fam, a, b});
+    }
+  }
+};
+
+inline void kprof_work(int fam, int64_t units) {
+  KProf* p = kprof_current();
+  if (p && p->on) p->work[fam] += units;
+}
+
 // Host copy of a ClosedLoop (row-major), dims checked.
 struct HostLoop {
   int d = 0, dw = 0;
@@ -57,6 +127,6 @@ void launch_hsmc_batch(int dw, int n, int horizon, const double* d_dy, int64_t n
 // range [r0, r1); d_hits[j] += colliding rollouts of trajectory j.
 void launch_mc(const HostLoop& L, const DevWorld& w, int n_traj, const int64_t* d_traj_off, const double* d_ynom,
                int max_points, int64_t r0, int64_t r1, uint64_t seed, double eps_cc, unsigned long long* d_hits,
-               cudaStream_t st, int64_t* launches);
+               cudaStream_t st, int64_t* launches, unsigned long long* d_steps = nullptr);
 
 }  // namespace pumpg

@@ -117,6 +117,7 @@ void exclusive_scan(const InT* d_in, int64_t* d_out, int64_t n, void* d_temp, cu
   }
   const int64_t tiles = (n + kScanTile - 1) / kScanTile;
   int64_t* partial = static_cast<int64_t*>(d_temp);
+  KScope ks(st, F_SCAN);
   k_tile_sum<InT><<<static_cast<unsigned>(tiles), kScanBlock, 0, st>>>(d_in, n, partial, d_n);
   k_scan_partials<<<1, 1024, 0, st>>>(partial, tiles, d_out, n, d_n);
   k_tile_scan<InT><<<static_cast<unsigned>(tiles), kScanBlock, 0, st>>>(d_in, n, partial, d_out, d_n);
@@ -242,6 +243,7 @@ void stable_multisplit(const int32_t* d_keys, const int32_t* d_vals, int64_t n, 
     const bool last = pass == passes - 1;
     int32_t* ok = pass == 0 ? kA : kB;
     int32_t* ov = last ? d_out : vA;
+    KScope ks(st, F_SPLIT);
     k_ms_hist<<<static_cast<unsigned>(tiles), kMsBlock, 0, st>>>(ck, n, shift, static_cast<int>(tiles), counts,
                                                                   cur_n);
     exclusive_scan<int32_t>(counts, offs, cn, stmp, st, launches);

@@ -64,7 +64,7 @@ def indoor():
         "start": {"position": [1.5, 6, 1.5], "velocity": [0, 0, 0]},
         "goal": {"lo": [17.5, 5, 1], "hi": [19, 7, 2], "max_speed": 0.5},
         "noise": {"process": [0, 0, 0, 2e-4, 2e-4, 2e-4], "measurement": 3e-4, "initial": [1e-4] * 6},
-        "dt": 0.2, "samples": 4000, "connection_radius": 5, "alpha": 0.02, "max_speed": 1.0,
+        "dt": 0.2, "samples": 4000, "connection_radius": 6, "alpha": 0.02, "max_speed": 1.0,
         "particles": 64, "mc_samples": 20000, "bank_horizon": 512, "collision_resolution": 0.05,
         "seeds": {"bank": 1, "mc": 2, "rrt": 3},
     }
