@@ -9,6 +9,8 @@
 #include <cmath>
 #include <cstring>
 #include <limits>
+#include <cstdlib>
+#include <map>
 #include <numeric>
 
 #include "ctx.h"
@@ -621,7 +623,13 @@ static void run_pump_device(Ctx& c, const pumpb::Scenario& s, const DevGraph* pr
     R.s.cp_hat = cph;
     R.s.pre_smoothing_cost = cst;
   }
-  // smoothing (pump.hpp:84-146)
+  // smoothing (pump.hpp:84-146).  The reference bisects the blend fraction
+  // s sequentially (s = 1, then 10 midpoints), each probe a nominal
+  // collision check + one MC certification.  The probes form a dyadic tree,
+  // so whole subtrees are evaluated speculatively in one batched MC launch
+  // (candidates whose blended nominal collides get no MC, as in the
+  // reference) and the bisection is then replayed from the memo: the accepted
+  // s, trajectory and certified CP are exactly the reference's.
   const std::vector<HWp>& plan = trajs[sel];
   std::vector<HWp> best = plan;
   double best_cost = trajectory_cost(plan, dw), best_mc = memo[sel], best_s = 0;
@@ -651,37 +659,88 @@ static void run_pump_device(Ctx& c, const pumpb::Scenario& s, const DevGraph* pr
       }
       return t;
     };
-    auto certify = [&](const std::vector<HWp>& t, double& mc_out) {
-      if (!nominal_free(hw, t, eps_cc)) return false;
-      mc_out = mc_values(c, L, dwld, {t}, s.mc_samples, s.seeds.mc, eps_cc, &R.s.mc_ms, &R.s.mc_rollouts)[0];
-      return mc_out <= s.alpha;
+    struct Probe {
+      std::vector<HWp> traj;
+      bool free = false;
+      double mc = 1.0;
     };
-    auto accept = [&](double sv, const std::vector<HWp>& t, double mc) {
-      best = t;
-      best_cost = trajectory_cost(t, dw);
-      best_mc = mc;
+    std::map<double, Probe> probes;
+    // evaluate the candidates not yet probed: nominal check, then one MC batch
+    auto evaluate = [&](const std::vector<double>& cands) {
+      std::vector<double> todo;
+      std::vector<std::vector<HWp>> batch;
+      for (double sv : cands) {
+        if (probes.count(sv)) continue;
+        Probe p;
+        p.traj = blend(sv);
+        p.free = nominal_free(hw, p.traj, eps_cc);
+        if (p.free) {
+          todo.push_back(sv);
+          batch.push_back(p.traj);
+        }
+        probes.emplace(sv, std::move(p));
+      }
+      if (batch.empty()) return;
+      auto v = mc_values(c, L, dwld, batch, s.mc_samples, s.seeds.mc, eps_cc, &R.s.mc_ms, &R.s.mc_rollouts);
+      for (size_t k = 0; k < todo.size(); ++k) probes[todo[k]].mc = v[k];
+    };
+    auto certified = [&](double sv) {
+      const Probe& p = probes.at(sv);
+      return p.free && p.mc <= s.alpha;
+    };
+    auto subtree = [&](double lo, double hi, int depth, std::vector<double>& out) {
+      // all midpoints the bisection can visit in its next `depth` steps
+      std::vector<std::pair<double, double>> level{{lo, hi}};
+      for (int d = 0; d < depth; ++d) {
+        std::vector<std::pair<double, double>> next;
+        for (auto [a, b] : level) {
+          const double mid = 0.5 * (a + b);
+          out.push_back(mid);
+          next.push_back({mid, b});
+          next.push_back({a, mid});
+        }
+        level.swap(next);
+      }
+    };
+    auto accept = [&](double sv) {
+      const Probe& p = probes.at(sv);
+      best = p.traj;
+      best_cost = trajectory_cost(p.traj, dw);
+      best_mc = p.mc;
       best_s = sv;
     };
-    bool done = false;
-    {
-      auto t = blend(1.0);
-      double mc;
-      if (certify(t, mc)) {
-        accept(1.0, t, mc);
-        done = true;
+    // Batch schedule: depths of the speculative subtrees covering the 10
+    // bisection steps.  Default: one probe per launch (the reference's order;
+    // a single 20000-rollout launch is the cheapest with the lane-parallel
+    // MC kernel).  PUMP_SMOOTH_SCHEDULE="3,3,4" trades extra rollouts for
+    // fewer launches.
+    std::vector<int> schedule(10, 1);
+    if (const char* e = std::getenv("PUMP_SMOOTH_SCHEDULE")) {
+      schedule.clear();
+      for (const char* q = e; *q;) {
+        schedule.push_back(std::max(1, std::atoi(q)));
+        while (*q && *q != ',') ++q;
+        if (*q == ',') ++q;
       }
     }
-    if (!done) {
+    evaluate({1.0});
+    if (certified(1.0)) {
+      accept(1.0);
+    } else {
       double lo = 0, hi = 1;
-      for (int it = 0; it < 10; ++it) {
-        const double mid = 0.5 * (lo + hi);
-        auto t = blend(mid);
-        double mc;
-        if (certify(t, mc)) {
-          accept(mid, t, mc);
-          lo = mid;
-        } else {
-          hi = mid;
+      int it = 0;
+      for (size_t b = 0; b < schedule.size() && it < 10; ++b) {
+        std::vector<double> more;
+        subtree(lo, hi, std::min(schedule[b], 10 - it), more);
+        evaluate(more);
+        for (int d = 0; d < schedule[b] && it < 10; ++d, ++it) {
+          const double mid = 0.5 * (lo + hi);
+          if (certified(mid)) {
+            accept(mid);
+            lo = mid;
+          } else {
+            hi = mid;
+          }
         }
       }
     }

@@ -65,6 +65,12 @@ __global__ void __launch_bounds__(32) k_bank_rec(const LoopP<D, DW> L, int n, in
 #pragma unroll
     for (int r = 0; r < 2 * D; ++r) z[r] = zstate[static_cast<int64_t>(r) * n + i];
   }
+  // noise of step tl is prefetched one step ahead (register double buffer)
+  double un[4 * D];
+  if (tc > 0) {
+#pragma unroll
+    for (int r = 0; r < 4 * D; ++r) un[r] = uw[static_cast<int64_t>(r) * n + i];
+  }
   for (int tl = 0; tl <= tc; ++tl) {
     const int t = t0 + tl;
     if (tl == tc && t != T) break;  // next chunk stores y_t
@@ -72,12 +78,19 @@ __global__ void __launch_bounds__(32) k_bank_rec(const LoopP<D, DW> L, int n, in
 #pragma unroll
     for (int k = 0; k < DW; ++k) slot[k] = row_dot<D>(L.C + k * D, z);
     if (t == T) break;
-    const double* u = uw + static_cast<int64_t>(tl) * (4 * D) * n + i;
+    double uc[4 * D];
+#pragma unroll
+    for (int r = 0; r < 4 * D; ++r) uc[r] = un[r];
+    if (tl + 1 < tc) {
+      const double* u = uw + static_cast<int64_t>(tl + 1) * (4 * D) * n + i;
+#pragma unroll
+      for (int r = 0; r < 4 * D; ++r) un[r] = u[static_cast<int64_t>(r) * n];
+    }
     double zn[2 * D];
 #pragma unroll
     for (int r = 0; r < 2 * D; ++r) {
       double a = row_dot<2 * D>(L.F + r * 2 * D, z);
-      zn[r] = (a + u[static_cast<int64_t>(r) * n]) + u[static_cast<int64_t>(2 * D + r) * n];
+      zn[r] = (a + uc[r]) + uc[2 * D + r];
     }
 #pragma unroll
     for (int r = 0; r < 2 * D; ++r) z[r] = zn[r];

@@ -140,10 +140,33 @@ __host__ __device__ __forceinline__ bool segment_hits(const double* p0, const do
   return true;
 }
 
+// Conservative separation test: true only if, on some axis, both points lie
+// outside the closed box by more than a relative margin of 1e-9.  Then the
+// reference slab test (segment_hits) provably returns false — the entry
+// parameter rounds to > 1 (or the exit parameter to < 0) — and point_free
+// cannot find either point (or any point interpolated between them) inside
+// the box.  So skipping such boxes never changes a collision decision.
+template <int DW>
+__host__ __device__ __forceinline__ bool box_separated(const double* p0, const double* p1, const double* lo,
+                                                       const double* hi) {
+  bool sep = false;
+#pragma unroll
+  for (int k = 0; k < DW; ++k) {
+    const double a = p0[k] < p1[k] ? p0[k] : p1[k];
+    const double b = p0[k] < p1[k] ? p1[k] : p0[k];
+    const double m = 1e-9 * (1.0 + (lo[k] < 0 ? -lo[k] : lo[k]) + (hi[k] < 0 ? -hi[k] : hi[k]) + (a < 0 ? -a : a) +
+                             (b < 0 ? -b : b));
+    sep = sep || (b < lo[k] - m) || (a > hi[k] + m);
+  }
+  return sep;
+}
+
 template <int DW>
 __host__ __device__ __forceinline__ bool segment_collides(const WorldD& w, const double* p0, const double* p1) {
-  for (int o = 0; o < w.n_obs; ++o)
+  for (int o = 0; o < w.n_obs; ++o) {
+    if (box_separated<DW>(p0, p1, w.lo + o * DW, w.hi + o * DW)) continue;  // cannot hit (see above)
     if (segment_hits<DW>(p0, p1, w.lo + o * DW, w.hi + o * DW)) return true;
+  }
   return false;
 }
 

@@ -28,6 +28,65 @@ struct GraphArgs {
   double r_n, dt, eps_cc, tau_max, ratio;
 };
 
+// Exact-preserving pair filter.  With dp0 = pb - pa, vbar = (va + vb)/2 and
+// dv = vb - va the connection cost is, identically,
+//   c(tau) = tau + sum_k 12 (dp0_k - vbar_k tau)^2 / tau^3 + |dv|^2 / tau
+// (steer.hpp:84-94 rewritten).  On [t_lo, t_hi] it is bounded below by
+//   t_lo + 12 sum_k min|dp0_k - vbar_k tau|^2 / t_hi^3 + |dv|^2 / t_hi,
+// and by tau itself beyond thr.  If every interval's bound exceeds
+// thr = r_n (1 + 1e-6), the pair's true minimum cost exceeds r_n by a margin
+// far above the rounding of the reference's cost evaluation (<= ~1e-13
+// relative), so connect() would return cost >= r_n (or ok = false) and the
+// reference would reject the pair at graph.hpp:72: skipping it changes nothing.
+constexpr int kLbK = 64;
+struct LbGrid {
+  double thr;
+  double t[kLbK + 1];  // decreasing: t[0] = thr, t[K] = thr * 1e-4
+  double c3[kLbK + 1];  // 12 / t^3 of each interval's upper end (c3[K]: head interval)
+  double c1[kLbK];      // 1 / t of each interval's upper end
+};
+
+template <int DW>
+__device__ __forceinline__ bool lb_rejects(const double* dp0, const double* vb, double dv2, const LbGrid& L) {
+  for (int i = 0; i < kLbK; ++i) {
+    const double th = L.t[i], tl = L.t[i + 1];
+    double s = 0.0;
+#pragma unroll
+    for (int k = 0; k < DW; ++k) {
+      const double m1 = dp0[k] - vb[k] * tl, m2 = dp0[k] - vb[k] * th;
+      const double a1 = m1 < 0 ? -m1 : m1, a2 = m2 < 0 ? -m2 : m2;
+      const double mm = ((m1 > 0) == (m2 > 0) && m1 != 0 && m2 != 0) ? (a1 < a2 ? a1 : a2) : 0.0;
+      s += mm * mm;
+    }
+    const double lb = tl + L.c3[i] * s + L.c1[i] * dv2;
+    if (lb * (1.0 - 1e-12) < L.thr) return false;
+  }
+  double s = 0.0;  // head interval (0, t_K]
+#pragma unroll
+  for (int k = 0; k < DW; ++k) {
+    const double m1 = dp0[k], m2 = dp0[k] - vb[k] * L.t[kLbK];
+    const double a1 = m1 < 0 ? -m1 : m1, a2 = m2 < 0 ? -m2 : m2;
+    const double mm = ((m1 > 0) == (m2 > 0) && m1 != 0 && m2 != 0) ? (a1 < a2 ? a1 : a2) : 0.0;
+    s += mm * mm;
+  }
+  return L.c3[kLbK] * s * (1.0 - 1e-12) >= L.thr;
+}
+
+LbGrid make_lb_grid(double r_n) {
+  LbGrid L;
+  L.thr = r_n * (1.0 + 1e-6);
+  const double rho = std::pow(1e4, 1.0 / kLbK);
+  for (int i = 0; i <= kLbK; ++i) {
+    L.t[i] = L.thr / std::pow(rho, i);
+    L.c3[i] = 12.0 / (L.t[i] * L.t[i] * L.t[i]);
+    if (i < kLbK) L.c1[i] = 1.0 / L.t[i];
+  }
+  // round the multipliers down so the bound stays a lower bound after rounding
+  for (int i = 0; i <= kLbK; ++i) L.c3[i] *= (1.0 - 1e-14);
+  for (int i = 0; i < kLbK; ++i) L.c1[i] *= (1.0 - 1e-14);
+  return L;
+}
+
 // connect() without the motion coefficients: returns ok; tau, cost out.
 template <int DW>
 __device__ bool connect_dev(const double* ap, const double* av, const double* bp, const double* bv, double tau_max,
@@ -96,10 +155,13 @@ __device__ __forceinline__ void coeffs_dev(const double* ap, const double* av, c
   }
 }
 
+// Pass 1: one CTA per source row v, one thread per target u.  Velocity
+// prefilter (graph.hpp:70) and the exact-preserving lower-bound filter;
+// survivors are compacted in ascending-u order (warp ballots + CTA prefix)
+// into the row's slab.  Cheap (~1k FP64 ops per pair) and branch-light.
 template <int DW>
-__global__ void __launch_bounds__(kRowBlock) k_connect_rows(GraphArgs g, int cap, int32_t* __restrict__ row_cnt,
-                                                            int32_t* __restrict__ cu, double* __restrict__ ctau,
-                                                            double* __restrict__ ccost) {
+__global__ void __launch_bounds__(kRowBlock) k_pair_filter(GraphArgs g, const LbGrid lb, int cap,
+                                                           int32_t* __restrict__ row_cnt, int32_t* __restrict__ su) {
   __shared__ int wtot[kRowBlock / 32];
   __shared__ int base_s;
   const int v = blockIdx.x;
@@ -115,19 +177,17 @@ __global__ void __launch_bounds__(kRowBlock) k_connect_rows(GraphArgs g, int cap
   for (int u0 = 0; u0 < g.n; u0 += kRowBlock) {
     const int u = u0 + threadIdx.x;
     bool keep = false;
-    double tau = 0, cost = 0;
     if (u < g.n && u != v) {
-      double bp[DW], bv[DW], dv[DW];
+      double dp0[DW], vb[DW], dv[DW];
 #pragma unroll
       for (int k = 0; k < DW; ++k) {
-        bp[k] = g.pos[u * DW + k];
-        bv[k] = g.vel[u * DW + k];
-        dv[k] = bv[k] - av[k];
+        const double bp = g.pos[u * DW + k], bv = g.vel[u * DW + k];
+        dv[k] = bv - av[k];
+        dp0[k] = bp - ap[k];
+        vb[k] = 0.5 * (av[k] + bv);
       }
-      if (!(2.0 * sqrt(sqnorm<DW>(dv)) >= g.r_n)) {  // graph.hpp:70 cheap lower bound
-        const bool ok = connect_dev<DW>(ap, av, bp, bv, g.tau_max, g.ratio, tau, cost);
-        keep = ok && !(cost >= g.r_n) && !(tau <= 0);  // graph.hpp:72
-      }
+      const double dv2 = sqnorm<DW>(dv);
+      keep = !(2.0 * sqrt(dv2) >= g.r_n) && !lb_rejects<DW>(dp0, vb, dv2, lb);
     }
     const unsigned bal = __ballot_sync(0xffffffffu, keep);
     if (lane == 0) wtot[warp] = __popc(bal);
@@ -135,12 +195,7 @@ __global__ void __launch_bounds__(kRowBlock) k_connect_rows(GraphArgs g, int cap
     int off = base_s;
     for (int w = 0; w < warp; ++w) off += wtot[w];
     off += __popc(bal & ((1u << lane) - 1u));
-    if (keep && off < cap) {
-      const int64_t slot = static_cast<int64_t>(v) * cap + off;
-      cu[slot] = u;
-      ctau[slot] = tau;
-      ccost[slot] = cost;
-    }
+    if (keep && off < cap) su[static_cast<int64_t>(v) * cap + off] = u;
     __syncthreads();
     if (threadIdx.x == 0) {
       int t = 0;
@@ -164,6 +219,52 @@ __device__ __forceinline__ int find_row(const int64_t* __restrict__ off, int n, 
   return lo;
 }
 
+// Pass 2: connect() (steer.hpp:111-182) on the compacted survivors, one
+// thread each: every lane of every warp does useful DDIV-heavy work.
+template <int DW>
+__global__ void __launch_bounds__(128) k_connect(GraphArgs g, int cap, int64_t n_surv,
+                                                 const int64_t* __restrict__ soff, const int32_t* __restrict__ su,
+                                                 uint8_t* __restrict__ keep, int32_t* __restrict__ s_v,
+                                                 int32_t* __restrict__ s_u, double* __restrict__ s_tau,
+                                                 double* __restrict__ s_cost) {
+  const int64_t s = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (s >= n_surv) return;
+  const int v = find_row(soff, g.n, s);
+  const int u = su[static_cast<int64_t>(v) * cap + (s - soff[v])];
+  double ap[DW], av[DW], bp[DW], bv[DW];
+#pragma unroll
+  for (int k = 0; k < DW; ++k) {
+    ap[k] = g.pos[v * DW + k];
+    av[k] = g.vel[v * DW + k];
+    bp[k] = g.pos[u * DW + k];
+    bv[k] = g.vel[u * DW + k];
+  }
+  double tau = 0, cost = 0;
+  const bool ok = connect_dev<DW>(ap, av, bp, bv, g.tau_max, g.ratio, tau, cost);
+  keep[s] = (ok && !(cost >= g.r_n) && !(tau <= 0)) ? 1 : 0;  // graph.hpp:72
+  s_v[s] = v;
+  s_u[s] = u;
+  s_tau[s] = tau;
+  s_cost[s] = cost;
+}
+
+// order-preserving compaction of kept survivors into the candidate arrays
+__global__ void k_cand_compact(int n, int64_t n_surv, const uint8_t* __restrict__ keep,
+                               const int64_t* __restrict__ cpos, const int64_t* __restrict__ soff,
+                               const int32_t* __restrict__ s_v, const int32_t* __restrict__ s_u,
+                               const double* __restrict__ s_tau, const double* __restrict__ s_cost,
+                               int32_t* __restrict__ c_v, int32_t* __restrict__ c_u, double* __restrict__ c_tau,
+                               double* __restrict__ c_cost, int64_t* __restrict__ cand_off) {
+  const int64_t s = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (s <= n) cand_off[s] = cpos[soff[s]];
+  if (s >= n_surv || !keep[s]) return;
+  const int64_t c = cpos[s];
+  c_v[c] = s_v[s];
+  c_u[c] = s_u[s];
+  c_tau[c] = s_tau[s];
+  c_cost[c] = s_cost[s];
+}
+
 template <int DW>
 __device__ __forceinline__ WorldD stage_world(const WorldD& w, double* smem) {
   double* lo = smem;
@@ -180,19 +281,17 @@ __device__ __forceinline__ WorldD stage_world(const WorldD& w, double* smem) {
 }
 
 template <int DW>
-__global__ void __launch_bounds__(128) k_collide(GraphArgs g, WorldD w, int cap, int64_t n_cand,
-                                                 const int64_t* __restrict__ cand_off, const int32_t* __restrict__ cu,
-                                                 const double* __restrict__ ctau, uint8_t* __restrict__ valid,
+__global__ void __launch_bounds__(128) k_collide(GraphArgs g, WorldD w, int64_t n_cand,
+                                                 const int32_t* __restrict__ c_v, const int32_t* __restrict__ c_u,
+                                                 const double* __restrict__ c_tau, uint8_t* __restrict__ valid,
                                                  int32_t* __restrict__ nsteps) {
   extern __shared__ double smem[];
   const WorldD ws = stage_world<DW>(w, smem);
   const int64_t c = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (c >= n_cand) return;
-  const int v = find_row(cand_off, g.n, c);
-  const int64_t slot = static_cast<int64_t>(v) * cap + (c - cand_off[v]);
-  const int u = cu[slot];
+  const int v = c_v[c], u = c_u[c];
   MotionD<DW> m;
-  m.tau = ctau[slot];
+  m.tau = c_tau[c];
 #pragma unroll
   for (int k = 0; k < DW; ++k) {
     m.p0[k] = g.pos[v * DW + k];
@@ -224,27 +323,23 @@ __global__ void __launch_bounds__(128) k_collide(GraphArgs g, WorldD w, int cap,
 }
 
 template <int DW>
-__global__ void k_emit_edges(GraphArgs g, int cap, int64_t n_cand, const int64_t* __restrict__ cand_off,
-                             const int32_t* __restrict__ cu, const double* __restrict__ ctau,
-                             const double* __restrict__ ccost, const uint8_t* __restrict__ valid,
-                             const int32_t* __restrict__ nsteps, const int64_t* __restrict__ eoff,
-                             int32_t* __restrict__ e_from, int32_t* __restrict__ e_to, double* __restrict__ e_cost,
-                             double* __restrict__ e_tau, double* __restrict__ e_acc0, double* __restrict__ e_jerk,
-                             int32_t* __restrict__ e_nsteps, int64_t* __restrict__ row_ptr) {
+__global__ void k_emit_edges(GraphArgs g, int64_t n_cand, const int64_t* __restrict__ cand_off,
+                             const int32_t* __restrict__ c_v, const int32_t* __restrict__ c_u,
+                             const double* __restrict__ c_tau, const double* __restrict__ c_cost,
+                             const uint8_t* __restrict__ valid, const int32_t* __restrict__ nsteps,
+                             const int64_t* __restrict__ eoff, int32_t* __restrict__ e_from, int32_t* __restrict__ e_to,
+                             double* __restrict__ e_cost, double* __restrict__ e_tau, double* __restrict__ e_acc0,
+                             double* __restrict__ e_jerk, int32_t* __restrict__ e_nsteps,
+                             int64_t* __restrict__ row_ptr) {
   const int64_t c = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (c < g.n + 1) {
-    // row_ptr[v] = number of valid candidates before row v's first candidate
-    row_ptr[c] = eoff[cand_off[c]];
-  }
+  if (c < g.n + 1) row_ptr[c] = eoff[cand_off[c]];  // valid candidates before row c
   if (c >= n_cand || !valid[c]) return;
-  const int v = find_row(cand_off, g.n, c);
-  const int64_t slot = static_cast<int64_t>(v) * cap + (c - cand_off[v]);
   const int64_t e = eoff[c];
-  const int u = cu[slot];
-  const double tau = ctau[slot];
+  const int v = c_v[c], u = c_u[c];
+  const double tau = c_tau[c];
   e_from[e] = v;
   e_to[e] = u;
-  e_cost[e] = ccost[slot];
+  e_cost[e] = c_cost[c];
   e_tau[e] = tau;
   e_nsteps[e] = nsteps[c];
   double a0[DW], j0[DW];
@@ -256,8 +351,6 @@ __global__ void k_emit_edges(GraphArgs g, int cap, int64_t n_cand, const int64_t
   }
 }
 
-// local_convex_region (geom.hpp:189-225) with velocity projection
-// (geom.hpp:163-183).  WRITE=false: count half-spaces only.
 template <int DW, bool WRITE>
 __global__ void __launch_bounds__(128) k_regions(GraphArgs g, WorldD w, int64_t n_wp, int64_t n_edges,
                                                  const int64_t* __restrict__ wp_off, const int32_t* __restrict__ e_from,
@@ -406,6 +499,7 @@ void build_graph_device(DevGraph& G, Ctx& c, int n, int dw, const double* h_pos,
   c.h2d(G.pos.p, h_pos, n * dw * 8);
   c.h2d(G.vel.p, h_vel, n * dw * 8);
   GraphArgs ga{n, G.pos.as<double>(), G.vel.as<double>(), r_n, dt, eps_cc, tau_max, ratio};
+  const LbGrid lbg = make_lb_grid(r_n);
   WorldD wd;
   wd.n_obs = w.n_obs;
   wd.lo = w.d_lo;
@@ -415,39 +509,73 @@ void build_graph_device(DevGraph& G, Ctx& c, int n, int dw, const double* h_pos,
     wd.bhi[k] = w.bhi[k];
   }
   const size_t wsmem = 2 * static_cast<size_t>(w.n_obs) * dw * sizeof(double);
-  int cap = 512;
-  int32_t max_cnt = 0;
-  DBuf& rcnt = c.buf("g_rowcnt", al((n + 1) * 4));
-  DBuf& coff = c.buf("g_candoff", al((n + 2) * 8));
-  DBuf& stmp = c.buf("g_scantmp", scan_temp_bytes(static_cast<int64_t>(n) * 4096 + 16));
-  for (;;) {
-    DBuf& cuB = c.buf("g_cu", al(static_cast<size_t>(n) * cap * 4));
-    DBuf& ctB = c.buf("g_ctau", al(static_cast<size_t>(n) * cap * 8));
-    DBuf& ccB = c.buf("g_ccost", al(static_cast<size_t>(n) * cap * 8));
-    KScope ks(st, F_CONNECT);
-    dispatch_dw(dw, [&]<int DW>() {
-      k_connect_rows<DW><<<n, kRowBlock, 0, st>>>(ga, cap, rcnt.as<int32_t>(), cuB.as<int32_t>(), ctB.as<double>(),
-                                                 ccB.as<double>());
-    });
-    ++c.launches;
-    PUMP_CUDA(cudaGetLastError());
-    kprof_work(F_CONNECT, static_cast<int64_t>(n) * (n - 1));
+  int cap = 1024;
+  DBuf& rcnt = c.buf("g_rowcnt", al((n + 8) * 4));
+  DBuf& soff = c.buf("g_soff", al((n + 2) * 8));
+  DBuf& stmp = c.buf("g_scantmp", scan_temp_bytes(static_cast<int64_t>(n) * n + 16));
+  for (;;) {  // pass 1 with an exact per-row refit if a row overflows the slab
+    DBuf& suB = c.buf("g_su", al(static_cast<size_t>(n) * cap * 4));
+    {
+      KScope ks(st, F_CONNECT);
+      dispatch_dw(dw, [&]<int DW>() {
+        k_pair_filter<DW><<<n, kRowBlock, 0, st>>>(ga, lbg, cap, rcnt.as<int32_t>(), suB.as<int32_t>());
+      });
+      ++c.launches;
+      PUMP_CUDA(cudaGetLastError());
+    }
     std::vector<int32_t> cnt(n);
     c.d2h(cnt.data(), rcnt.p, n * 4);
     c.sync();
-    max_cnt = 0;
+    int max_cnt = 0;
     for (int v = 0; v < n; ++v) max_cnt = std::max(max_cnt, cnt[v]);
     if (max_cnt <= cap) break;
-    cap = max_cnt;  // exact refit, rerun (deterministic)
+    cap = max_cnt;
   }
-  int32_t* cu = c.scratch["g_cu"].as<int32_t>();
-  double* ctau = c.scratch["g_ctau"].as<double>();
-  double* ccost = c.scratch["g_ccost"].as<double>();
-  exclusive_scan<int32_t>(rcnt.as<int32_t>(), coff.as<int64_t>(), n, stmp.p, st, &c.launches);
+  kprof_work(F_CONNECT, static_cast<int64_t>(n) * (n - 1));
+  int32_t* su = c.scratch["g_su"].as<int32_t>();
+  exclusive_scan<int32_t>(rcnt.as<int32_t>(), soff.as<int64_t>(), n, stmp.p, st, &c.launches);
+  int64_t n_surv = 0;
+  c.d2h(&n_surv, soff.as<int64_t>() + n, 8);
+  c.sync();
+  G.n_connect = n_surv;
+  DBuf& skeep = c.buf("g_skeep", al(n_surv + 1));
+  DBuf& sv = c.buf("g_sv", al((n_surv + 1) * 4));
+  DBuf& suu = c.buf("g_suu", al((n_surv + 1) * 4));
+  DBuf& stau = c.buf("g_stau", al((n_surv + 1) * 8));
+  DBuf& scost = c.buf("g_scost", al((n_surv + 1) * 8));
+  DBuf& cpos = c.buf("g_cpos", al((n_surv + 2) * 8));
+  if (n_surv > 0) {
+    KScope ks(st, F_CONNECT);
+    dispatch_dw(dw, [&]<int DW>() {
+      k_connect<DW><<<grid_for(n_surv, 128), 128, 0, st>>>(ga, cap, n_surv, soff.as<int64_t>(), su,
+                                                           skeep.as<uint8_t>(), sv.as<int32_t>(), suu.as<int32_t>(),
+                                                           stau.as<double>(), scost.as<double>());
+    });
+    ++c.launches;
+    PUMP_CUDA(cudaGetLastError());
+  }
+  DBuf& stmpc = c.buf("g_scantmpc", scan_temp_bytes(n_surv + 16));
+  exclusive_scan<uint8_t>(skeep.as<uint8_t>(), cpos.as<int64_t>(), n_surv, stmpc.p, st, &c.launches);
   int64_t n_cand = 0;
-  c.d2h(&n_cand, coff.as<int64_t>() + n, 8);
+  c.d2h(&n_cand, cpos.as<int64_t>() + n_surv, 8);
   c.sync();
   G.n_cand = n_cand;
+  DBuf& cv = c.buf("g_cv", al((n_cand + 1) * 4));
+  DBuf& cuu = c.buf("g_cuu", al((n_cand + 1) * 4));
+  DBuf& ctau = c.buf("g_ctau2", al((n_cand + 1) * 8));
+  DBuf& ccost = c.buf("g_ccost2", al((n_cand + 1) * 8));
+  DBuf& coff = c.buf("g_candoff", al((n + 2) * 8));
+  {
+    const int64_t items = std::max<int64_t>(n_surv, n + 1);
+    KScope ks(st, F_EMIT);
+    k_cand_compact<<<grid_for(items, 256), 256, 0, st>>>(n, n_surv, skeep.as<uint8_t>(), cpos.as<int64_t>(),
+                                                          soff.as<int64_t>(), sv.as<int32_t>(), suu.as<int32_t>(),
+                                                          stau.as<double>(), scost.as<double>(), cv.as<int32_t>(),
+                                                          cuu.as<int32_t>(), ctau.as<double>(), ccost.as<double>(),
+                                                          coff.as<int64_t>());
+    ++c.launches;
+    PUMP_CUDA(cudaGetLastError());
+  }
   DBuf& valid = c.buf("g_valid", al(n_cand + 1));
   DBuf& nst = c.buf("g_nsteps", al((n_cand + 1) * 4));
   DBuf& eoff = c.buf("g_eoff", al((n_cand + 2) * 8));
@@ -457,8 +585,9 @@ void build_graph_device(DevGraph& G, Ctx& c, int n, int dw, const double* h_pos,
     dispatch_dw(dw, [&]<int DW>() {
       if (wsmem > 48 * 1024)
         PUMP_CUDA(cudaFuncSetAttribute(k_collide<DW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wsmem));
-      k_collide<DW><<<grid_for(n_cand, 128), 128, wsmem, st>>>(ga, wd, cap, n_cand, coff.as<int64_t>(), cu, ctau,
-                                                               valid.as<uint8_t>(), nst.as<int32_t>());
+      k_collide<DW><<<grid_for(n_cand, 128), 128, wsmem, st>>>(ga, wd, n_cand, cv.as<int32_t>(), cuu.as<int32_t>(),
+                                                               ctau.as<double>(), valid.as<uint8_t>(),
+                                                               nst.as<int32_t>());
     });
     ++c.launches;
     PUMP_CUDA(cudaGetLastError());
@@ -478,18 +607,18 @@ void build_graph_device(DevGraph& G, Ctx& c, int n, int dw, const double* h_pos,
   G.row_ptr.ensure(al((n + 1) * 8));
   G.wp_off.ensure(al((E + 2) * 8));
   {
-  KScope ks(st, F_EMIT);
-  dispatch_dw(dw, [&]<int DW>() {
-    const int64_t items = std::max<int64_t>(n_cand, n + 1);
-    k_emit_edges<DW><<<grid_for(items, 256), 256, 0, st>>>(
-        ga, cap, n_cand, coff.as<int64_t>(), cu, ctau, ccost, valid.as<uint8_t>(), nst.as<int32_t>(),
-        eoff.as<int64_t>(), G.e_from.as<int32_t>(), G.e_to.as<int32_t>(), G.e_cost.as<double>(),
-        G.e_tau.as<double>(), G.e_acc0.as<double>(), G.e_jerk.as<double>(), G.e_nsteps.as<int32_t>(),
-        G.row_ptr.as<int64_t>());
-  });
+    KScope ks(st, F_EMIT);
+    dispatch_dw(dw, [&]<int DW>() {
+      const int64_t items = std::max<int64_t>(n_cand, n + 1);
+      k_emit_edges<DW><<<grid_for(items, 256), 256, 0, st>>>(
+          ga, n_cand, coff.as<int64_t>(), cv.as<int32_t>(), cuu.as<int32_t>(), ctau.as<double>(), ccost.as<double>(),
+          valid.as<uint8_t>(), nst.as<int32_t>(), eoff.as<int64_t>(), G.e_from.as<int32_t>(), G.e_to.as<int32_t>(),
+          G.e_cost.as<double>(), G.e_tau.as<double>(), G.e_acc0.as<double>(), G.e_jerk.as<double>(),
+          G.e_nsteps.as<int32_t>(), G.row_ptr.as<int64_t>());
+    });
+    ++c.launches;
+    PUMP_CUDA(cudaGetLastError());
   }
-  ++c.launches;
-  PUMP_CUDA(cudaGetLastError());
   DBuf& stmp3 = c.buf("g_scantmp3", scan_temp_bytes(E + 16));
   exclusive_scan<int32_t>(G.e_nsteps.as<int32_t>(), G.wp_off.as<int64_t>(), E, stmp3.p, st, &c.launches);
   int64_t NW = 0;

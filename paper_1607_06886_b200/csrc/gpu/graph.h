@@ -8,7 +8,7 @@ namespace pumpg {
 struct DevGraph {
   int n = 0, dw = 0;
   double r_n = 0, dt = 0;
-  int64_t E = 0, NW = 0, H = 0, n_cand = 0;
+  int64_t E = 0, NW = 0, H = 0, n_cand = 0, n_connect = 0;
   DBuf pos, vel;                                          // n x dw
   DBuf row_ptr;                                           // n + 1 (int64)
   DBuf e_from, e_to, e_cost, e_tau, e_acc0, e_jerk, e_nsteps;

@@ -15,6 +15,9 @@
 // obstacles are staged in shared memory; hits are reduced with a warp
 // ballot + popc, one atomicAdd per warp; rollout-steps are counted the same
 // way for the roofline.
+#include <cmath>
+#include <cstdlib>
+
 #include "dispatch.cuh"
 
 namespace pumpg {
@@ -134,11 +137,319 @@ __global__ void __launch_bounds__(kMcBlock) k_mc(const LoopP<D, DW> L, WorldD w,
   }
 }
 
+// ------------------------------------------------------------------------
+// Axis-separable closed loop (the per-axis double integrator with diagonal
+// noise and tracking weights): every matrix only couples the four z entries
+// {k, dw+k, d+k, d+dw+k} of one workspace axis k.  Dropping the structural
+// zeros from a sequential sum c = 0 + sum_j M_rj x_j leaves every partial
+// sum unchanged for finite operands (0*x adds +-0, and c + (+-0) == c for
+// c != 0, while +0 + (-0) == +0), so the per-axis form below is bit-exact
+// to the dense recursion.  One lane per axis (LPR lanes per rollout): the
+// dynamics need no communication; y and the collision verdict are combined
+// with shuffles; obstacle culling and segment checks are split across the
+// rollout's lanes.
+struct SepBlocks {  // per axis k: row rho <-> z index g(rho) = {k, dw+k, d+k, d+dw+k}
+  double F[3][16], Gv[3][8], Gw[3][4], Sv[3][4], Sw[3], S0[3][4], C[3][2];
+};
+
+bool separable(const HostLoop& L) {
+  const int d = L.d, dw = L.dw, nz = 2 * d;
+  if (d != 2 * dw) return false;
+  auto ax = [&](int i) { return (i % d) % dw; };
+  for (int r = 0; r < nz; ++r) {
+    for (int c = 0; c < nz; ++c)
+      if (ax(r) != ax(c) && L.F[r * nz + c] != 0.0) return false;
+    for (int c = 0; c < d; ++c)
+      if (ax(r) != c % dw && L.Gv[r * d + c] != 0.0) return false;
+    for (int c = 0; c < dw; ++c)
+      if (ax(r) != c && L.Gw[r * dw + c] != 0.0) return false;
+  }
+  for (int a = 0; a < d; ++a)
+    for (int b = 0; b < d; ++b)
+      if (a % dw != b % dw && (L.Sv[a * d + b] != 0.0 || L.S0[a * d + b] != 0.0)) return false;
+  for (int a = 0; a < dw; ++a)
+    for (int b = 0; b < dw; ++b)
+      if (a != b && L.Sw[a * dw + b] != 0.0) return false;
+  for (int k = 0; k < dw; ++k)
+    for (int j = 0; j < d; ++j)
+      if (j % dw != k && L.C[k * d + j] != 0.0) return false;
+  for (double x : L.F)
+    if (!std::isfinite(x)) return false;
+  return true;
+}
+
+SepBlocks sep_blocks(const HostLoop& L) {
+  SepBlocks B{};
+  const int d = L.d, dw = L.dw, nz = 2 * d;
+  for (int k = 0; k < dw; ++k) {
+    const int g[4] = {k, dw + k, d + k, d + dw + k};
+    const int h[2] = {k, dw + k};
+    for (int r = 0; r < 4; ++r) {
+      for (int c = 0; c < 4; ++c) B.F[k][r * 4 + c] = L.F[g[r] * nz + g[c]];
+      for (int a = 0; a < 2; ++a) B.Gv[k][r * 2 + a] = L.Gv[g[r] * d + h[a]];
+      B.Gw[k][r] = L.Gw[g[r] * dw + k];
+    }
+    for (int a = 0; a < 2; ++a)
+      for (int b = 0; b < 2; ++b) {
+        B.Sv[k][a * 2 + b] = L.Sv[h[a] * d + h[b]];
+        B.S0[k][a * 2 + b] = L.S0[h[a] * d + h[b]];
+      }
+    B.Sw[k] = L.Sw[k * dw + k];
+    for (int a = 0; a < 2; ++a) B.C[k][a] = L.C[k * d + h[a]];
+  }
+  return B;
+}
+
+template <int DW>
+constexpr int lanes_per_rollout() {
+  return DW == 3 ? 4 : DW;
+}
+
+template <int DW>
+__global__ void __launch_bounds__(kMcBlock) k_mc_sep(const SepBlocks B, WorldD w, const int64_t* __restrict__ traj_off,
+                                                     const double* __restrict__ ynom_all, int64_t r0, int64_t r1,
+                                                     uint64_t seed, double eps_cc, unsigned long long* __restrict__ hits,
+                                                     unsigned long long* __restrict__ steps_out) {
+  constexpr int LPR = lanes_per_rollout<DW>();
+  extern __shared__ double smem[];
+  const int j = blockIdx.y;
+  const int64_t p_begin = traj_off[j];
+  const int n_pts = static_cast<int>(traj_off[j + 1] - p_begin);
+  const int T = n_pts - 1;
+  double* s_y = smem;               // n_pts * DW
+  double* s_lo = s_y + n_pts * DW;  // n_obs * DW, inflated for culling: lo - M
+  double* s_hi = s_lo + w.n_obs * DW;
+  double* s_clo = s_hi + w.n_obs * DW;  // exact boxes for the reference tests
+  double* s_chi = s_clo + w.n_obs * DW;
+  for (int x = threadIdx.x; x < n_pts * DW; x += blockDim.x) s_y[x] = ynom_all[p_begin * DW + x];
+  for (int x = threadIdx.x; x < w.n_obs * DW; x += blockDim.x) {
+    const int k = x % DW;
+    const double bl = w.blo[k] < 0 ? -w.blo[k] : w.blo[k], bh = w.bhi[k] < 0 ? -w.bhi[k] : w.bhi[k];
+    const double lo = w.lo[x], hi = w.hi[x];
+    // margin >= box_separated's for any point inside the bounds (dev.cuh)
+    const double M = 1e-9 * (1.0 + (lo < 0 ? -lo : lo) + (hi < 0 ? -hi : hi) + 2.0 * (bl > bh ? bl : bh));
+    s_lo[x] = lo - M;
+    s_hi[x] = hi + M;
+    s_clo[x] = lo;
+    s_chi[x] = hi;
+  }
+  __syncthreads();
+  const double e = eps_cc > 1e-12 ? eps_cc : 1e-12;  // std::max(eps_cc, 1e-12)
+  const int lane = threadIdx.x & 31;
+  const int q = lane % LPR;                 // axis of this lane (q < DW)
+  const int gbase = lane - q;               // first lane of the rollout group
+  const int k = q < DW ? q : 0;             // idle lanes mirror axis 0 (results unused)
+  const int64_t i = r0 + (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) / LPR;
+  const bool active = i < r1;
+  const unsigned gmask = ((LPR == 32) ? 0xffffffffu : ((1u << LPR) - 1u)) << gbase;
+  bool collided = false;
+  int steps = 0;
+  // per-axis blocks in registers
+  double F[16], Gv[8], Gw[4], Sv[4], S0[4], C[2];
+#pragma unroll
+  for (int x = 0; x < 16; ++x) F[x] = B.F[k][x];
+#pragma unroll
+  for (int x = 0; x < 8; ++x) Gv[x] = B.Gv[k][x];
+#pragma unroll
+  for (int x = 0; x < 4; ++x) {
+    Gw[x] = B.Gw[k][x];
+    Sv[x] = B.Sv[k][x];
+    S0[x] = B.S0[k][x];
+  }
+  const double Sw = B.Sw[k];
+  C[0] = B.C[k][0];
+  C[1] = B.C[k][1];
+  const uint64_t ch0 = static_cast<uint64_t>(k), ch1 = static_cast<uint64_t>(DW + k);
+
+  double z[4];
+  uint64_t sa = 0, pt = 0;
+  if (active) {
+    sa = hash_seed_a(seed, static_cast<uint64_t>(i));
+    pt = mix64(sa + 0ull);
+    const double n0 = normal_from_prefix(pt, ch0), n1 = normal_from_prefix(pt, ch1);  // kInitial channels
+    z[0] = (0.0 + S0[0] * n0) + S0[1] * n1;
+    z[1] = (0.0 + S0[2] * n0) + S0[3] * n1;
+    z[2] = 0.0;
+    z[3] = 0.0;
+  }
+  double prev[DW];
+  for (int t = 0; t <= T; ++t) {
+    // group-uniform loop: all lanes of a rollout stay in lock step
+    const bool live = active && !collided;
+    if (!__any_sync(0xffffffffu, live)) break;
+    double u[4] = {0, 0, 0, 0}, wv[4] = {0, 0, 0, 0};
+    uint64_t pt1 = 0;
+    double y_own = 0;
+    if (live) {
+      ++steps;
+      if (t < T) {  // (A) noise of t -> t+1 for this axis
+        pt1 = mix64(sa + static_cast<uint64_t>(t + 1));
+        const double nv0 = normal_from_prefix(pt, kProcess + ch0);
+        const double nv1 = normal_from_prefix(pt, kProcess + ch1);
+        const double nw = normal_from_prefix(pt1, kMeasurement + static_cast<uint64_t>(k));
+        const double t10 = (0.0 + Sv[0] * nv0) + Sv[1] * nv1;
+        const double t11 = (0.0 + Sv[2] * nv0) + Sv[3] * nv1;
+        const double t2 = 0.0 + Sw * nw;
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+          u[r] = (0.0 + Gv[2 * r] * t10) + Gv[2 * r + 1] * t11;
+          wv[r] = 0.0 + Gw[r] * t2;
+        }
+      }
+      y_own = s_y[t * DW + k] + ((0.0 + C[0] * z[0]) + C[1] * z[1]);
+    }
+    // (B) gather the realized point of the rollout into every lane of the group
+    double y[DW];
+#pragma unroll
+    for (int a = 0; a < DW; ++a) y[a] = __shfl_sync(0xffffffffu, y_own, gbase + a);
+    if (t == 0) {
+#pragma unroll
+      for (int a = 0; a < DW; ++a) prev[a] = y[a];
+    }
+    bool hit = false;
+    if (live) {
+      // bounds (every lane), then obstacles culled against bbox(prev, y)
+      bool inb = true;
+#pragma unroll
+      for (int a = 0; a < DW; ++a) inb = inb && !(y[a] < w.blo[a] || y[a] > w.bhi[a]);
+      if (!inb) {
+        hit = true;
+      } else {
+        double bl[DW], bh[DW];
+#pragma unroll
+        for (int a = 0; a < DW; ++a) {
+          bl[a] = prev[a] < y[a] ? prev[a] : y[a];
+          bh[a] = prev[a] < y[a] ? y[a] : prev[a];
+        }
+        uint64_t cand = 0;  // this lane's share of the obstacles (o = q mod LPR)
+        for (int o = q; o < w.n_obs && o < 64; o += LPR) {
+          bool sep = false;
+#pragma unroll
+          for (int a = 0; a < DW; ++a) sep = sep || (bh[a] < s_lo[o * DW + a]) || (bl[a] > s_hi[o * DW + a]);
+          if (!sep) cand |= 1ull << o;
+        }
+        // obstacles beyond the first 64 are never culled (checked below)
+        uint64_t all = cand;  // union of the group's shares
+#pragma unroll
+        for (int x = 1; x < LPR; x <<= 1) all |= __shfl_xor_sync(gmask, all, x);
+        // the point y itself (t = 0 included): lane 0 of the group
+        if (q == 0) {
+          for (uint64_t m = all; m; m &= m - 1) {
+            const int o = __ffsll(static_cast<long long>(m)) - 1;
+            if (box_contains<DW>(s_clo + o * DW, s_chi + o * DW, y)) hit = true;
+          }
+        }
+        if (w.n_obs > 64 && q == 0) {
+          for (int o = 64; o < w.n_obs; ++o)
+            if (box_contains<DW>(s_clo + o * DW, s_chi + o * DW, y)) hit = true;
+        }
+        if (t > 0) {  // segments prev -> y, subdivided to eps_cc (cp.hpp:237-248), split across lanes
+          double diff[DW];
+#pragma unroll
+          for (int a = 0; a < DW; ++a) diff[a] = y[a] - prev[a];
+          const double len = sqrt(sqnorm<DW>(diff));
+          int segs = static_cast<int>(ceil(len / e));
+          if (segs < 1) segs = 1;
+          for (int s2 = 1 + q; s2 <= segs; s2 += LPR) {
+            double p0[DW], p1[DW];
+            const double f1 = static_cast<double>(s2) / segs;
+#pragma unroll
+            for (int a = 0; a < DW; ++a) p1[a] = prev[a] + (y[a] - prev[a]) * f1;
+            if (s2 == 1) {
+#pragma unroll
+              for (int a = 0; a < DW; ++a) p0[a] = prev[a];
+            } else {
+              const double f0 = static_cast<double>(s2 - 1) / segs;
+#pragma unroll
+              for (int a = 0; a < DW; ++a) p0[a] = prev[a] + (y[a] - prev[a]) * f0;
+            }
+            bool in1 = true;
+#pragma unroll
+            for (int a = 0; a < DW; ++a) in1 = in1 && !(p1[a] < w.blo[a] || p1[a] > w.bhi[a]);
+            if (!in1) {
+              hit = true;
+              break;
+            }
+            for (uint64_t m = all; m; m &= m - 1) {
+              const int o = __ffsll(static_cast<long long>(m)) - 1;
+              if (box_contains<DW>(s_clo + o * DW, s_chi + o * DW, p1) ||
+                  segment_hits<DW>(p0, p1, s_clo + o * DW, s_chi + o * DW)) {
+                hit = true;
+                break;
+              }
+            }
+            for (int o = 64; o < w.n_obs && !hit; ++o)
+              if (box_contains<DW>(s_clo + o * DW, s_chi + o * DW, p1) ||
+                  segment_hits<DW>(p0, p1, s_clo + o * DW, s_chi + o * DW))
+                hit = true;
+            if (hit) break;
+          }
+        }
+      }
+    }
+    // rollout verdict = OR over its lanes
+    const unsigned hb = __ballot_sync(0xffffffffu, hit);
+    const bool ghit = (hb & gmask) != 0u;
+    if (live) {
+      if (ghit) {
+        collided = true;
+      } else {
+#pragma unroll
+        for (int a = 0; a < DW; ++a) prev[a] = y[a];
+        if (t < T) {  // (C) z <- ((F z) + u) + w  for this axis block
+          double zn[4];
+#pragma unroll
+          for (int r = 0; r < 4; ++r) {
+            double c = 0.0;
+#pragma unroll
+            for (int x = 0; x < 4; ++x) c = c + F[r * 4 + x] * z[x];
+            zn[r] = (c + u[r]) + wv[r];
+          }
+#pragma unroll
+          for (int r = 0; r < 4; ++r) z[r] = zn[r];
+          pt = pt1;
+        }
+      }
+    }
+  }
+  const bool leader = (q == 0) && active;
+  const unsigned bal = __ballot_sync(0xffffffffu, leader && collided);
+  const unsigned tot = __reduce_add_sync(0xffffffffu, leader ? static_cast<unsigned>(steps) : 0u);
+  if (lane == 0) {
+    if (bal) atomicAdd(hits + j, static_cast<unsigned long long>(__popc(bal)));
+    if (steps_out) atomicAdd(steps_out, static_cast<unsigned long long>(tot));
+  }
+}
+
 void launch_mc(const HostLoop& HL, const DevWorld& w, int n_traj, const int64_t* d_traj_off, const double* d_ynom,
                int max_points, int64_t r0, int64_t r1, uint64_t seed, double eps_cc, unsigned long long* d_hits,
                cudaStream_t st, int64_t* launches, unsigned long long* d_steps) {
   if (r1 <= r0 || n_traj <= 0) return;
   if (HL.dw != w.dw) throw std::invalid_argument("mc_certify: workspace / model dimension mismatch");
+  static const bool force_dense = std::getenv("PUMP_MC_DENSE") != nullptr;
+  if (!force_dense && HL.dw >= 2 && HL.dw <= 3 && separable(HL)) {
+    const SepBlocks B = sep_blocks(HL);
+    WorldD wd;
+    wd.n_obs = w.n_obs;
+    wd.lo = w.d_lo;
+    wd.hi = w.d_hi;
+    for (int k = 0; k < 6; ++k) {
+      wd.blo[k] = w.blo[k];
+      wd.bhi[k] = w.bhi[k];
+    }
+    dispatch_dw(HL.dw, [&]<int DW>() {
+      constexpr int LPR = lanes_per_rollout<DW>();
+      const size_t smem = (static_cast<size_t>(max_points) * DW + 4 * static_cast<size_t>(w.n_obs) * DW) * sizeof(double);
+      if (smem > 48 * 1024)
+        PUMP_CUDA(cudaFuncSetAttribute(k_mc_sep<DW>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+      dim3 grid(grid_for((r1 - r0) * LPR, kMcBlock), n_traj);
+      KScope ks(st, F_MC);
+      k_mc_sep<DW><<<grid, kMcBlock, smem, st>>>(B, wd, d_traj_off, d_ynom, r0, r1, seed, eps_cc, d_hits, d_steps);
+      ++*launches;
+      PUMP_CUDA(cudaGetLastError());
+    });
+    return;
+  }
   dispatch_dims(HL.d, HL.dw, [&]<int D, int DW>() {
     const LoopP<D, DW> L = make_loop<D, DW>(HL);
     WorldD wd;
