@@ -89,6 +89,14 @@ __device__ __forceinline__ void cl_step(const LoopP<D, DW>& L, double (&z)[2 * D
   for (int r = 0; r < 2 * D; ++r) z[r] = zn[r];
 }
 
+__host__ __device__ __forceinline__ int __builtin_ctzll_hd(uint64_t x) {
+#if defined(__CUDA_ARCH__)
+  return __ffsll(static_cast<long long>(x)) - 1;
+#else
+  return __builtin_ctzll(x);
+#endif
+}
+
 // ----------------------------------------------------------- geometry
 // closed AABB containment (geom.hpp:19-23)
 template <int DW>
@@ -241,19 +249,115 @@ __host__ __device__ __forceinline__ double steer_cost(const double* ap, const do
   return c;
 }
 
+// Conservative bounding box of a motion's positions on [0, tau]: the cubic
+// per axis attains its extremes at s = 0, s = tau or a root of its
+// derivative; the box is widened by a relative margin (1e-6 of the term
+// magnitudes) that dwarfs every rounding error of the evaluated positions.
+template <int DW>
+__host__ __device__ __forceinline__ void motion_bbox(const MotionD<DW>& m, double* bl, double* bh) {
+  const double tau = m.tau;
+#pragma unroll
+  for (int k = 0; k < DW; ++k) {
+    const double p0 = m.p0[k], v0 = m.v0[k], a = m.a[k], j = m.j[k];
+    double lo = p0 < m.p1[k] ? p0 : m.p1[k], hi = p0 < m.p1[k] ? m.p1[k] : p0;
+    auto at = [&](double s) { return p0 + v0 * s + a * s * s / 2 + j * s * s * s / 6; };
+    const double pt = at(tau);
+    lo = pt < lo ? pt : lo;
+    hi = pt > hi ? pt : hi;
+    // p'(s) = v0 + a s + j s^2 / 2
+    double r[2];
+    int nr = 0;
+    const double aj = j < 0 ? -j : j, aa = a < 0 ? -a : a;
+    if (aj > 1e-300) {
+      const double disc = a * a - 2.0 * j * v0;
+      if (disc >= 0) {
+        const double sq = sqrt(disc);
+        r[nr++] = (-a + sq) / j;
+        r[nr++] = (-a - sq) / j;
+      } else if (disc > -1e-12 * (a * a + (2.0 * j * v0 < 0 ? -2.0 * j * v0 : 2.0 * j * v0))) {
+        r[nr++] = -a / j;  // near-double root
+      }
+    } else if (aa > 1e-300) {
+      r[nr++] = -v0 / a;
+    }
+    for (int x = 0; x < nr; ++x) {
+      if (r[x] > 0 && r[x] < tau) {
+        const double pr = at(r[x]);
+        lo = pr < lo ? pr : lo;
+        hi = pr > hi ? pr : hi;
+      }
+    }
+    const double mag = 1.0 + (p0 < 0 ? -p0 : p0) + (v0 < 0 ? -v0 : v0) * tau + aa * tau * tau / 2 + aj * tau * tau * tau / 6 +
+                       (m.p1[k] < 0 ? -m.p1[k] : m.p1[k]);
+    bl[k] = lo - 1e-6 * mag;
+    bh[k] = hi + 1e-6 * mag;
+  }
+}
+
 // motion_collides (geom.hpp:96-123): adaptive midpoint bisection until the
 // chord is <= eps_cc (or the span < 1e-9 s), exact segment test at leaves.
 // Iterative DFS over (t0, t1) spans; endpoints are recomputed with the same
 // polynomial so they carry the same bits the reference stores.  The result
 // is an OR over a fixed tree of tests, so traversal order cannot change it.
+//
+// Culling (exact-preserving): every tested point lies on the motion and
+// every tested segment joins two such points, so all of them lie in the
+// motion's (widened) bounding box.  Obstacles separated from that box can
+// neither contain a tested point nor be hit by a tested segment, and if the
+// box is strictly inside the workspace bounds no bounds test can fail; when
+// nothing remains the answer is "no collision" without subdividing.
 template <int DW>
 __host__ __device__ inline bool motion_collides(const MotionD<DW>& m, const WorldD& w, double eps_cc) {
+  double bl[DW], bh[DW];
+  motion_bbox<DW>(m, bl, bh);
+  bool inside = true;
+#pragma unroll
+  for (int k = 0; k < DW; ++k) inside = inside && bl[k] > w.blo[k] && bh[k] < w.bhi[k];
+  constexpr int kMaskWords = 4;
+  uint64_t cand[kMaskWords] = {0, 0, 0, 0};
+  const bool masked = w.n_obs <= 64 * kMaskWords;
+  bool any = !masked;
+  if (masked) {
+    for (int o = 0; o < w.n_obs; ++o) {
+      bool sep = false;
+#pragma unroll
+      for (int k = 0; k < DW; ++k) sep = sep || (bh[k] < w.lo[o * DW + k]) || (bl[k] > w.hi[o * DW + k]);
+      if (!sep) {
+        cand[o >> 6] |= 1ull << (o & 63);
+        any = true;
+      }
+    }
+  }
+  if (inside && !any) return false;
+  auto free_pt = [&](const double* p) {
+    if (!inside && !box_contains<DW>(w.blo, w.bhi, p)) return false;
+    if (!masked) {
+      for (int o = 0; o < w.n_obs; ++o)
+        if (box_contains<DW>(w.lo + o * DW, w.hi + o * DW, p)) return false;
+      return true;
+    }
+    for (int q = 0; q < kMaskWords; ++q)
+      for (uint64_t x = cand[q]; x; x &= x - 1) {
+        const int o = q * 64 + __builtin_ctzll_hd(x);
+        if (box_contains<DW>(w.lo + o * DW, w.hi + o * DW, p)) return false;
+      }
+    return true;
+  };
+  auto seg_hit = [&](const double* a, const double* b) {
+    if (!masked) return segment_collides<DW>(w, a, b);
+    for (int q = 0; q < kMaskWords; ++q)
+      for (uint64_t x = cand[q]; x; x &= x - 1) {
+        const int o = q * 64 + __builtin_ctzll_hd(x);
+        if (segment_hits<DW>(a, b, w.lo + o * DW, w.hi + o * DW)) return true;
+      }
+    return false;
+  };
   double p0[DW], p1[DW];
   motion_pos<DW>(m, 0.0, p0);
-  if (!point_free<DW>(w, p0)) return true;
+  if (!free_pt(p0)) return true;
   if (m.tau <= 0) return false;
   motion_pos<DW>(m, m.tau, p1);
-  if (!point_free<DW>(w, p1)) return true;
+  if (!free_pt(p1)) return true;
   double st0[64], st1[64];
   int sp = 0;
   double t0 = 0.0, t1 = m.tau;
@@ -262,7 +366,7 @@ __host__ __device__ inline bool motion_collides(const MotionD<DW>& m, const Worl
 #pragma unroll
     for (int k = 0; k < DW; ++k) diff[k] = p1[k] - p0[k];
     if (sqrt(sqnorm<DW>(diff)) <= eps_cc || t1 - t0 < 1e-9) {
-      if (segment_collides<DW>(w, p0, p1)) return true;
+      if (seg_hit(p0, p1)) return true;
       if (sp == 0) return false;
       --sp;
       t0 = st0[sp];
@@ -274,7 +378,7 @@ __host__ __device__ inline bool motion_collides(const MotionD<DW>& m, const Worl
     const double tm = 0.5 * (t0 + t1);
     double pm[DW];
     motion_pos<DW>(m, tm, pm);
-    if (!point_free<DW>(w, pm)) return true;
+    if (!free_pt(pm)) return true;
     if (sp >= 64) return true;  // unreachable: depth is bounded by t1 - t0 >= 1e-9
     st0[sp] = tm;
     st1[sp] = t1;
