@@ -159,6 +159,16 @@ int pump_ctx_flush_l2(pump_ctx* ctx);
 /* FP64 DMUL+DADD issue-rate microbenchmark, Gop/s (roofline denominator). */
 int pump_peak_fp64(pump_ctx* ctx, double* gops);
 
+/* ------------------------------------------------------------ multi-GPU */
+/* Sharded MC certification: rank r simulates rollouts
+ * [n r / W, n (r+1) / W) of every certification in pump_run and the int64
+ * hit counts are summed with ncclAllReduce on the ctx stream.  The 128-byte
+ * ncclUniqueId comes from rank 0's pump_nccl_unique_id, broadcast by the
+ * caller (e.g. torch.distributed). */
+int pump_nccl_unique_id(uint8_t* out128);
+int pump_ctx_set_comm(pump_ctx* ctx, int rank, int world, const uint8_t* id128);
+int pump_shard_range(int64_t n, int rank, int world, int64_t* lo, int64_t* hi);
+
 /* ------------------------------------------------------------- scenario */
 /* load_scenario / parse_scenario / build_models (scenario.hpp:144-301). */
 int pump_scenario_parse(const char* json_text, pump_scenario** out);

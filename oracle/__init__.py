@@ -135,6 +135,44 @@ def halton(index, base):
     return lib().oracle_halton(index, base)
 
 
+def bisect_select(values, alpha):
+    """bisect_select (pump.hpp:23-51) over ids 0..n-1 with MC values."""
+    v = np.ascontiguousarray(values, dtype=np.float64)
+    n = v.size
+    plan, mc, ne = C.c_int(), C.c_double(), C.c_int()
+    ev = np.zeros(max(1, n), dtype=np.int32)
+    L = lib()
+    L.oracle_bisect_select.argtypes = [C.c_int, C.c_void_p, C.c_double, C.c_void_p, C.c_void_p, C.c_void_p,
+                                       C.c_void_p]
+    ok = L.oracle_bisect_select(n, _p(v) if n else None, alpha, C.byref(plan), C.byref(mc), _p(ev), C.byref(ne))
+    return {"success": bool(ok), "plan_id": plan.value, "mc": mc.value, "evals": ev[:ne.value].tolist()}
+
+
+def fixed_time_connect(ap, av, bp, bv, tau):
+    dw = len(ap)
+    arr = [np.ascontiguousarray(x, dtype=np.float64) for x in (ap, av, bp, bv)]
+    cost = C.c_double()
+    a0, j = np.zeros(dw), np.zeros(dw)
+    L = lib()
+    L.oracle_fixed_time_connect.argtypes = [C.c_int] + [C.c_void_p] * 4 + [C.c_double] + [C.c_void_p] * 3
+    L.oracle_fixed_time_connect.restype = None
+    L.oracle_fixed_time_connect(dw, *[_p(x) for x in arr], tau, C.byref(cost), _p(a0), _p(j))
+    return {"ok": True, "tau": tau, "cost": cost.value, "acc0": a0, "jerk": j}
+
+
+def waypoints(ap, av, bp, bv, motion, dt, cap=100000):
+    """motion_waypoints (steer.hpp:192-212): (t, pos, vel, control) arrays."""
+    dw = len(ap)
+    arr = [np.ascontiguousarray(x, dtype=np.float64) for x in (ap, av, bp, bv)]
+    t, p, v, u = np.zeros(cap), np.zeros((cap, dw)), np.zeros((cap, dw)), np.zeros((cap, dw))
+    L = lib()
+    L.oracle_waypoints.argtypes = [C.c_int] + [C.c_void_p] * 4 + [C.c_double, C.c_void_p, C.c_void_p, C.c_double,
+                                                                 C.c_int] + [C.c_void_p] * 4
+    n = L.oracle_waypoints(dw, *[_p(x) for x in arr], motion["tau"], _p(np.ascontiguousarray(motion["acc0"])),
+                           _p(np.ascontiguousarray(motion["jerk"])), dt, cap, _p(t), _p(p), _p(v), _p(u))
+    return t[:n], p[:n], v[:n], u[:n]
+
+
 # ------------------------------------------------------------------ models
 def scenario_models(json_text: str):
     """(closed-loop dict, scalars dict) of a scenario via the shared host

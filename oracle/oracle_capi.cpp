@@ -635,4 +635,53 @@ int oracle_scenario_closed_loop(const char* json_text, int32_t* d, int32_t* dw, 
     std::memcpy(Cm, cl.C.a.data(), cl.C.a.size() * 8);
   });
 }
+
+// bisect_select (pump.hpp:23-51) over ids 0..n-1 with given MC values:
+// returns success; *plan, *mc; evals (ids in probe order) -> eval_ids[*n_evals]
+int oracle_bisect_select(int n, const double* values, double alpha, int* plan, double* mc, int* eval_ids,
+                         int* n_evals) {
+  std::vector<int> ids(n);
+  for (int i = 0; i < n; ++i) ids[i] = i;
+  Selection s = bisect_select(ids, [&](int id) { return values[id]; }, alpha);
+  *plan = s.plan_id;
+  *mc = s.mc;
+  *n_evals = static_cast<int>(s.evals.size());
+  for (size_t i = 0; i < s.evals.size(); ++i) eval_ids[i] = s.evals[i].first;
+  return s.success ? 1 : 0;
+}
+
+// fixed_time_connect (steer.hpp:97-107): out = {cost}, acc0/jerk[dw]
+void oracle_fixed_time_connect(int dw, const double* ap, const double* av, const double* bp, const double* bv,
+                               double tau, double* cost, double* acc0, double* jerk) {
+  St a{Vec(ap, ap + dw), Vec(av, av + dw)}, b{Vec(bp, bp + dw), Vec(bv, bv + dw)};
+  Mot m = fixed_time_connect(a, b, tau);
+  *cost = m.cost;
+  for (int k = 0; k < dw; ++k) {
+    acc0[k] = m.acc0[k];
+    jerk[k] = m.jerk[k];
+  }
+}
+
+// motion_waypoints (steer.hpp:192-212) of a motion; returns the count (<= cap written)
+int oracle_waypoints(int dw, const double* fp, const double* fv, const double* tp, const double* tv, double tau,
+                     const double* acc0, const double* jerk, double dt, int cap, double* t_out, double* p_out,
+                     double* v_out, double* u_out) {
+  Mot m;
+  m.from = {Vec(fp, fp + dw), Vec(fv, fv + dw)};
+  m.to = {Vec(tp, tp + dw), Vec(tv, tv + dw)};
+  m.tau = tau;
+  m.ok = true;
+  m.acc0.assign(acc0, acc0 + dw);
+  m.jerk.assign(jerk, jerk + dw);
+  auto w = waypoints(m, dt);
+  for (int i = 0; i < static_cast<int>(w.size()) && i < cap; ++i) {
+    t_out[i] = w[i].t;
+    for (int k = 0; k < dw; ++k) {
+      p_out[i * dw + k] = w[i].s.p[k];
+      v_out[i * dw + k] = w[i].s.v[k];
+      u_out[i * dw + k] = w[i].u[k];
+    }
+  }
+  return static_cast<int>(w.size());
+}
 }

@@ -60,7 +60,8 @@ EXPORTS = [
     "pump_hsmc_extend_batch", "pump_mc_certify_batch", "pump_mc_certify", "pump_build_graph", "pump_graph_upload",
     "pump_graph_counts", "pump_graph_export", "pump_graph_free", "pump_explore_run", "pump_explore_counts",
     "pump_explore_export", "pump_explore_free", "pump_run", "pump_result_summary_get", "pump_result_arrays",
-    "pump_result_free",
+    "pump_result_free", "pump_nccl_unique_id", "pump_ctx_set_comm", "pump_shard_range", "pump_ctx_profile",
+    "pump_ctx_profile_read", "pump_ctx_io_bytes", "pump_ctx_flush_l2", "pump_peak_fp64",
 ]
 
 
@@ -106,6 +107,9 @@ def lib():
             L.pump_result_summary_get.argtypes = [vp, vp]
             L.pump_result_arrays.argtypes = [vp] * 10
             L.pump_result_free.argtypes = [vp]
+        L.pump_nccl_unique_id.argtypes = [vp]
+        L.pump_ctx_set_comm.argtypes = [vp, C.c_int, C.c_int, vp]
+        L.pump_shard_range.argtypes = [C.c_int64, C.c_int, C.c_int, vp, vp]
         _lib = L
     return _lib
 
@@ -419,3 +423,25 @@ def run_pump(scenario: Scenario, prebuilt: Graph | None = None, ctx: Context | N
                traj_pos=tp, traj_vel=tv, traj_ctrl=tu)
     out["termination"] = A.TERMINATION[out["termination"]]
     return out
+
+
+# ---------------------------------------------------------------- multi-GPU
+def shard_range(n: int, rank: int, world: int) -> tuple[int, int]:
+    """Rollouts [lo, hi) owned by `rank` of `world` (the library's partition)."""
+    return n * rank // world, n * (rank + 1) // world
+
+
+def set_comm(ctx: Context, rank: int, world: int, group=None):
+    """Shard the MC certification of pump_run across `world` ranks (one GPU
+    each): rank 0 creates the NCCL id, torch.distributed broadcasts it."""
+    import torch
+    import torch.distributed as dist
+
+    buf = np.zeros(128, dtype=np.uint8)
+    if rank == 0:
+        _check(lib().pump_nccl_unique_id(_p(buf)))
+    t = torch.from_numpy(buf.astype(np.int64)).cuda() if dist.get_backend(group) == "nccl" else \
+        torch.from_numpy(buf.astype(np.int64))
+    dist.broadcast(t, src=0, group=group)
+    buf = t.cpu().numpy().astype(np.uint8)
+    _check(lib().pump_ctx_set_comm(ctx.h, rank, world, _p(buf)))

@@ -78,6 +78,7 @@ int pump_ctx_destroy(pump_ctx* ctx) {
     if (!ctx) return;
     cudaSetDevice(ctx->c.device);
     cudaStreamSynchronize(ctx->c.stream);
+    comm_destroy(ctx->c);
     ctx->c.scratch.clear();
     ctx->c.run_graph.reset();
     ctx->c.run_explore.reset();

@@ -318,11 +318,16 @@ static std::vector<double> mc_values(Ctx& c, const HostLoop& L, const DevWorld& 
   c.h2d(d_off.p, off.data(), (nt + 1) * 8);
   c.h2d(d_y.p, y.data(), y.size() * 8);
   PUMP_CUDA(cudaMemsetAsync(d_h.p, 0, (nt + 1) * 8, c.stream));
+  // this rank's rollouts (all of them on one GPU), then the hit counts of all
+  // ranks are summed over NVLink (bit-identical for any world size)
+  int64_t r0 = 0, r1 = n_mc;
+  shard_range(n_mc, c.rank, c.world, &r0, &r1);
   c.tic();
-  launch_mc(L, w, nt, d_off.as<int64_t>(), d_y.as<double>(), max_pts, 0, n_mc, seed, eps_cc,
+  launch_mc(L, w, nt, d_off.as<int64_t>(), d_y.as<double>(), max_pts, r0, r1, seed, eps_cc,
             d_h.as<unsigned long long>(), c.stream, &c.launches, d_h.as<unsigned long long>() + nt);
+  allreduce_sum_i64(c, d_h.as<int64_t>(), nt);
   *mc_ms += c.toc();
-  *rollouts += static_cast<int64_t>(n_mc) * nt;
+  *rollouts += (r1 - r0) * nt;
   std::vector<int64_t> hits(nt + 1);
   c.d2h(hits.data(), d_h.p, (nt + 1) * 8);
   c.sync();

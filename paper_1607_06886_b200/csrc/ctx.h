@@ -62,7 +62,10 @@ struct Ctx {
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   int64_t launches = 0;
   double last_ms = 0;
-  int64_t h2d_bytes = 0, d2h_bytes = 0, mc_rollout_steps = 0;
+  int64_t h2d_bytes = 0, d2h_bytes = 0, mc_rollout_steps = 0, collectives = 0;
+  // multi-GPU: NCCL communicator for the sharded MC certification
+  void* nccl = nullptr;
+  int rank = 0, world = 1;
   KProf prof;
   // resident particle bank
   DBuf bank;
@@ -97,6 +100,10 @@ struct Ctx {
     return ms;
   }
 };
+
+void shard_range(int64_t n, int rank, int world, int64_t* lo, int64_t* hi);
+void allreduce_sum_i64(Ctx& c, int64_t* d, size_t count);
+void comm_destroy(Ctx& c);
 
 // Upload a workspace into ctx scratch buffers named prefix+"lo"/"hi".
 DevWorld upload_world(Ctx& c, const pump_workspace* ws, const std::string& prefix);
