@@ -1,0 +1,114 @@
+"""Oracle vs the literal reference code (CPU).
+
+oracle/_ref/libpumpref.so is the reference's own headers
+(/root/reference/proj/include, compiled in place by oracle/ref/Makefile)
+over the Eigen-subset shim (include/compat).  With glibc normals on both
+sides, the oracle restatement must reproduce the reference's bank bits, and
+every output of run_pump, bit for bit.  This pins the restatement's control
+flow (sampling, graph, explore, dominance, termination, bisection,
+smoothing) against the reference source.  Model-synthesis arithmetic comes
+from the same linalg routines on both sides; Eigen's own rounding stays
+unpinned.
+"""
+import ctypes as C
+import json
+import os
+
+import numpy as np
+import pytest
+
+from conftest import ROOT, scenario_text
+
+REF = os.path.join(ROOT, "oracle", "_ref", "libpumpref.so")
+pytestmark = pytest.mark.skipif(not os.path.exists(REF), reason="reference not built (needs /root/reference)")
+
+
+def ref():
+    L = C.CDLL(REF)
+    L.ref_last_error.restype = C.c_char_p
+    L.ref_presample_bank.argtypes = [C.c_char_p, C.c_int, C.c_int, C.c_ulonglong, C.c_int, C.c_void_p]
+    L.ref_closed_loop_F.argtypes = [C.c_char_p, C.c_void_p]
+    L.ref_run_pump.argtypes = [C.c_char_p, C.c_int] + [C.c_void_p] * 11
+    return L
+
+
+def _p(a):
+    return a.ctypes.data_as(C.c_void_p)
+
+
+def variant(name, **kw):
+    j = json.loads(scenario_text(name))
+    j.update(kw)
+    return json.dumps(j)
+
+
+def ref_run(L, text, workers):
+    sc = np.zeros(8)
+    path = np.zeros(4096, dtype=np.int32)
+    ids, vals = np.zeros(4096, dtype=np.int32), np.zeros(4096)
+    ne, npar, nt = C.c_int(), C.c_int(), C.c_int()
+    pc, pp = np.zeros(4096), np.zeros(4096)
+    tt, tp = np.zeros(100000), np.zeros(300000)
+    rc = L.ref_run_pump(text.encode(), workers, _p(sc), _p(path), _p(ids), _p(vals), C.byref(ne), _p(pc), _p(pp),
+                        C.byref(npar), _p(tt), _p(tp), C.byref(nt))
+    assert rc == 0, L.ref_last_error()
+    dw = len(json.loads(text)["workspace"]["bounds"]["lo"])
+    return {"success": int(sc[0]), "cost": sc[1], "certified_cp": sc[2], "cp_hat": sc[3],
+            "partial_plans": int(sc[4]), "smoothing_s": sc[5], "pre_smoothing_cost": sc[6],
+            "path": path[:int(sc[7])].tolist(), "mc_eval_ids": ids[:ne.value].tolist(),
+            "mc_eval_values": vals[:ne.value].tolist(), "pareto_cost": pc[:npar.value],
+            "pareto_cp": pp[:npar.value], "traj_t": tt[:nt.value], "traj_pos": tp[:nt.value * dw].reshape(-1, dw)}
+
+
+@pytest.mark.parametrize("name", ["minimal", "quad3d_indoor"])
+def test_closed_loop_matches_reference(oracle_lib, name):
+    L = ref()
+    txt = scenario_text(name)
+    cl, _ = oracle_lib.scenario_models(txt)
+    F = np.zeros_like(cl["F"])
+    assert L.ref_closed_loop_F(txt.encode(), _p(F)) == 0
+    assert np.array_equal(F.view(np.uint64), cl["F"].view(np.uint64))
+
+
+@pytest.mark.parametrize("name,T,n", [("minimal", 40, 512), ("quad3d_three_obstacle", 80, 32)])
+def test_bank_bits_match_reference_glibc(oracle_lib, name, T, n):
+    L = ref()
+    txt = scenario_text(name)
+    cl, _ = oracle_lib.scenario_models(txt)
+    dw = cl["dw"]
+    out = np.zeros((T + 1, n, dw))
+    assert L.ref_presample_bank(txt.encode(), T, n, 7, 4, _p(out)) == 0
+    oracle_lib.set_normal_mode(oracle_lib.GLIBC)
+    try:
+        ob = oracle_lib.presample_bank(cl, T, n, 7, workers=4)
+    finally:
+        oracle_lib.set_normal_mode(oracle_lib.PORTABLE)
+    assert np.array_equal(out.view(np.uint64), ob.view(np.uint64))
+
+
+@pytest.mark.parametrize("name,kw", [("minimal", {"mc_samples": 2000}),
+                                     ("three_obstacle", {"mc_samples": 2000}),
+                                     ("quad3d_three_obstacle", {"samples": 500, "mc_samples": 2000})])
+def test_run_pump_matches_reference(oracle_lib, name, kw):
+    L = ref()
+    txt = variant(name, **kw)
+    workers = min(8, os.cpu_count() or 2)
+    r = ref_run(L, txt, workers)
+    for mode in (oracle_lib.GLIBC, oracle_lib.PORTABLE):
+        oracle_lib.set_normal_mode(mode)
+        try:
+            o = oracle_lib.run_pump(txt, workers=workers)
+        finally:
+            oracle_lib.set_normal_mode(oracle_lib.PORTABLE)
+        # decisions (node path, front, probes) agree in both normal modes
+        assert o["path"].tolist() == r["path"], mode
+        assert o["partial_plans"] == r["partial_plans"]
+        assert o["mc_eval_ids"].tolist() == r["mc_eval_ids"]
+        assert np.array_equal(o["pareto_cost"], r["pareto_cost"])
+        assert np.array_equal(o["pareto_cp"], r["pareto_cp"])
+        if mode == oracle_lib.GLIBC:  # the literal reference: every bit
+            assert o["cost"] == r["cost"] and o["certified_cp"] == r["certified_cp"]
+            assert o["mc_eval_values"].tolist() == r["mc_eval_values"]
+            assert o["smoothing_s"] == r["smoothing_s"]
+            assert np.array_equal(o["traj_t"], r["traj_t"])
+            assert np.array_equal(o["traj_pos"].view(np.uint64), r["traj_pos"].view(np.uint64))
