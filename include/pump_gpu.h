@@ -159,6 +159,31 @@ int pump_ctx_flush_l2(pump_ctx* ctx);
 /* FP64 DMUL+DADD issue-rate microbenchmark, Gop/s (roofline denominator). */
 int pump_peak_fp64(pump_ctx* ctx, double* gops);
 
+/* ------------------------------------------------- host geometry queries */
+/* Single-call queries for the drop-in C++ headers; they run the same
+ * __host__ __device__ code as the kernels (bit-identical results). */
+/* connect (steer.hpp:111-182): out3 = {ok, tau, cost}; acc0/jerk[dw] when ok */
+int pump_connect(int32_t dw, const double* ap, const double* av, const double* bp, const double* bv, double tau_max,
+                 double* out3, double* acc0, double* jerk);
+double pump_steer_cost(int32_t dw, const double* ap, const double* av, const double* bp, const double* bv,
+                       double tau);                                                   /* steer.hpp:84-94 */
+int pump_fixed_time_connect(int32_t dw, const double* ap, const double* av, const double* bp, const double* bv,
+                            double tau, double* cost, double* acc0, double* jerk);    /* steer.hpp:97-107 */
+int pump_point_free(const pump_workspace* ws, const double* y);                       /* geom.hpp:56-61 */
+int pump_segment_hits_aabb(int32_t dw, const double* p0, const double* p1, const double* lo,
+                           const double* hi);                                         /* geom.hpp:64-80 */
+int pump_motion_collides(const pump_workspace* ws, const double* fp, const double* fv, const double* tp,
+                         const double* tv, double tau, const double* acc0, const double* jerk, double eps_cc,
+                         int32_t* out);                                               /* geom.hpp:96-123 */
+int pump_local_convex_region(const pump_workspace* ws, const double* y, const double* ydot, int32_t cap,
+                             double* a, double* b, uint8_t* fallback, int32_t* n_out); /* geom.hpp:189-225 */
+int pump_sample_free(int32_t n, const pump_workspace* ws, double max_speed, const pump_goal* goal, int32_t cap,
+                     double* pos, double* vel, int32_t* n_out);                       /* sample.hpp:56-89 */
+/* motion_waypoints (steer.hpp:192-212): returns the count (writes <= cap). */
+int32_t pump_waypoints(int32_t dw, const double* fp, const double* fv, const double* tp, const double* tv,
+                       double tau, const double* acc0, const double* jerk, double dt, int32_t cap, double* t_out,
+                       double* p_out, double* v_out, double* u_out);
+
 /* ------------------------------------------------------------ multi-GPU */
 /* Sharded MC certification: rank r simulates rollouts
  * [n r / W, n (r+1) / W) of every certification in pump_run and the int64

@@ -389,4 +389,159 @@ __host__ __device__ inline bool motion_collides(const MotionD<DW>& m, const Worl
   }
 }
 
+// connect() without the motion coefficients: returns ok; tau, cost out.
+template <int DW>
+__host__ __device__ inline bool connect_dev(const double* ap, const double* av, const double* bp, const double* bv, double tau_max,
+                            double ratio, double& tau_out, double& cost_out) {
+  bool same = true;
+#pragma unroll
+  for (int k = 0; k < DW; ++k) same = same && (ap[k] == bp[k]) && (av[k] == bv[k]);
+  if (same) {
+    tau_out = 0.0;
+    cost_out = 0.0;
+    return true;
+  }
+  const double tau_lo = tau_max * 1e-7;
+  double best_tau = tau_lo, best_c = steer_cost<DW>(ap, av, bp, bv, tau_lo);
+  int best_idx = 0;
+  double tau = tau_lo;
+  for (int i = 1; i < 64; ++i) {
+    tau *= ratio;
+    const double c = steer_cost<DW>(ap, av, bp, bv, tau);
+    if (c < best_c) {
+      best_c = c;
+      best_tau = tau;
+      best_idx = i;
+    }
+  }
+  double lo = best_tau / (best_idx > 0 ? ratio : 1.0);
+  double hi = best_tau * ratio;
+  hi = (tau_max < hi) ? tau_max : hi;  // std::min(best_tau * ratio, tau_max)
+  const double gr = 0.5 * (sqrt(5.0) - 1.0);
+  double x1 = hi - gr * (hi - lo), x2 = lo + gr * (hi - lo);
+  double f1 = steer_cost<DW>(ap, av, bp, bv, x1), f2 = steer_cost<DW>(ap, av, bp, bv, x2);
+  while (hi - lo > 1e-9 * hi) {
+    if (f1 < f2) {
+      hi = x2;
+      x2 = x1;
+      f2 = f1;
+      x1 = hi - gr * (hi - lo);
+      f1 = steer_cost<DW>(ap, av, bp, bv, x1);
+    } else {
+      lo = x1;
+      x1 = x2;
+      f1 = f2;
+      x2 = lo + gr * (hi - lo);
+      f2 = steer_cost<DW>(ap, av, bp, bv, x2);
+    }
+  }
+  tau_out = 0.5 * (lo + hi);
+  cost_out = steer_cost<DW>(ap, av, bp, bv, tau_out);
+  if (best_idx == 63 && tau_out > 0.999 * tau_max) {
+    const double eps = 1e-6 * tau_max;
+    if (steer_cost<DW>(ap, av, bp, bv, tau_max) <= steer_cost<DW>(ap, av, bp, bv, tau_max - eps)) return false;
+  }
+  return true;
+}
+
+// fixed_time_coeffs (steer.hpp:63-79): acc0, jerk
+template <int DW>
+__host__ __device__ __forceinline__ void coeffs_dev(const double* ap, const double* av, const double* bp, const double* bv,
+                                           double tau, double* acc0, double* jerk) {
+#pragma unroll
+  for (int k = 0; k < DW; ++k) {
+    const double dp = bp[k] - ap[k] - av[k] * tau;
+    const double dv = bv[k] - av[k];
+    acc0[k] = 6 * dp / (tau * tau) - 2 * dv / tau;
+    jerk[k] = -12 * dp / (tau * tau * tau) + 6 * dv / (tau * tau);
+  }
+}
+
+// local_convex_region (geom.hpp:189-225) for a free waypoint y with nominal
+// velocity yd: repeatedly take the nearest unpruned obstacle point (first
+// strict minimum of |clamp(y) - y|^2), prune every box whose 2^dw corners lie
+// beyond its half-space (tolerance 1e-12 (1 + d.d)), and project the
+// direction by the velocity (project_halfspace, geom.hpp:163-183, eps 1e-6).
+// Writes the half-spaces when a != nullptr; returns their count, or -1 when
+// the pruning loop fails (the reference's runtime_error).  <= 4096 boxes.
+template <int DW>
+__host__ __device__ inline int convex_region(const WorldD& ws, const double* y, const double* yd, double* a_out,
+                                             double* b_out, uint8_t* fb_out) {
+  constexpr int kMaxObs = 4096;
+  uint32_t pruned[kMaxObs / 32];
+  const int nw = (ws.n_obs + 31) / 32;
+  for (int q = 0; q < nw; ++q) pruned[q] = 0u;
+  int count = 0;
+  for (int iter = 0; iter < ws.n_obs; ++iter) {
+    int best = -1;
+    double best_sq = __builtin_inf();
+    double d[DW];
+    for (int o = 0; o < ws.n_obs; ++o) {
+      if ((pruned[o >> 5] >> (o & 31)) & 1u) continue;
+      double cand[DW];
+#pragma unroll
+      for (int k = 0; k < DW; ++k) {
+        double c = y[k] < ws.lo[o * DW + k] ? ws.lo[o * DW + k] : y[k];  // max(y, lo)
+        c = ws.hi[o * DW + k] < c ? ws.hi[o * DW + k] : c;               // min(., hi)
+        cand[k] = c - y[k];
+      }
+      const double sq = sqnorm<DW>(cand);
+      if (sq < best_sq) {
+        best_sq = sq;
+        best = o;
+#pragma unroll
+        for (int k = 0; k < DW; ++k) d[k] = cand[k];
+      }
+    }
+    if (best < 0) break;
+    const double dd = sqnorm<DW>(d);
+    const double tol = 1e-12 * (1.0 + dd);
+    bool any = false;
+    for (int o = 0; o < ws.n_obs; ++o) {
+      if ((pruned[o >> 5] >> (o & 31)) & 1u) continue;
+      bool inside = true;
+      for (unsigned corner = 0; corner < (1u << DW) && inside; ++corner) {
+        double dot = 0;
+#pragma unroll
+        for (int k = 0; k < DW; ++k) {
+          const double c = ((corner >> k) & 1u) ? ws.hi[o * DW + k] : ws.lo[o * DW + k];
+          dot += d[k] * (c - y[k]);
+        }
+        if (dot < dd - tol) inside = false;
+      }
+      if (inside) {
+        pruned[o >> 5] |= 1u << (o & 31);
+        any = true;
+      }
+    }
+    if (!any) return -1;
+    if (a_out) {
+      double a[DW];
+      bool fb = false;
+      const double vn = sqrt(sqnorm<DW>(yd));
+      if (vn < 1e-6) {
+        fb = true;
+      } else {
+        double dy = 0.0;
+#pragma unroll
+        for (int k = 0; k < DW; ++k) dy = dy + d[k] * yd[k];
+        const double coef = dy / sqnorm<DW>(yd);
+#pragma unroll
+        for (int k = 0; k < DW; ++k) a[k] = d[k] - coef * yd[k];
+        if (sqrt(sqnorm<DW>(a)) < 1e-6 * sqrt(sqnorm<DW>(d))) fb = true;
+      }
+      if (fb) {
+#pragma unroll
+        for (int k = 0; k < DW; ++k) a[k] = d[k];
+      }
+#pragma unroll
+      for (int k = 0; k < DW; ++k) a_out[count * DW + k] = a[k];
+      b_out[count] = sqnorm<DW>(a);
+      fb_out[count] = fb ? 1 : 0;
+    }
+    ++count;
+  }
+  return count;
+}
+
 }  // namespace pumpg

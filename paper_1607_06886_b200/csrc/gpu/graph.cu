@@ -87,74 +87,6 @@ LbGrid make_lb_grid(double r_n) {
   return L;
 }
 
-// connect() without the motion coefficients: returns ok; tau, cost out.
-template <int DW>
-__device__ bool connect_dev(const double* ap, const double* av, const double* bp, const double* bv, double tau_max,
-                            double ratio, double& tau_out, double& cost_out) {
-  bool same = true;
-#pragma unroll
-  for (int k = 0; k < DW; ++k) same = same && (ap[k] == bp[k]) && (av[k] == bv[k]);
-  if (same) {
-    tau_out = 0.0;
-    cost_out = 0.0;
-    return true;
-  }
-  const double tau_lo = tau_max * 1e-7;
-  double best_tau = tau_lo, best_c = steer_cost<DW>(ap, av, bp, bv, tau_lo);
-  int best_idx = 0;
-  double tau = tau_lo;
-  for (int i = 1; i < 64; ++i) {
-    tau *= ratio;
-    const double c = steer_cost<DW>(ap, av, bp, bv, tau);
-    if (c < best_c) {
-      best_c = c;
-      best_tau = tau;
-      best_idx = i;
-    }
-  }
-  double lo = best_tau / (best_idx > 0 ? ratio : 1.0);
-  double hi = best_tau * ratio;
-  hi = (tau_max < hi) ? tau_max : hi;  // std::min(best_tau * ratio, tau_max)
-  const double gr = 0.5 * (sqrt(5.0) - 1.0);
-  double x1 = hi - gr * (hi - lo), x2 = lo + gr * (hi - lo);
-  double f1 = steer_cost<DW>(ap, av, bp, bv, x1), f2 = steer_cost<DW>(ap, av, bp, bv, x2);
-  while (hi - lo > 1e-9 * hi) {
-    if (f1 < f2) {
-      hi = x2;
-      x2 = x1;
-      f2 = f1;
-      x1 = hi - gr * (hi - lo);
-      f1 = steer_cost<DW>(ap, av, bp, bv, x1);
-    } else {
-      lo = x1;
-      x1 = x2;
-      f1 = f2;
-      x2 = lo + gr * (hi - lo);
-      f2 = steer_cost<DW>(ap, av, bp, bv, x2);
-    }
-  }
-  tau_out = 0.5 * (lo + hi);
-  cost_out = steer_cost<DW>(ap, av, bp, bv, tau_out);
-  if (best_idx == 63 && tau_out > 0.999 * tau_max) {
-    const double eps = 1e-6 * tau_max;
-    if (steer_cost<DW>(ap, av, bp, bv, tau_max) <= steer_cost<DW>(ap, av, bp, bv, tau_max - eps)) return false;
-  }
-  return true;
-}
-
-// fixed_time_coeffs (steer.hpp:63-79): acc0, jerk
-template <int DW>
-__device__ __forceinline__ void coeffs_dev(const double* ap, const double* av, const double* bp, const double* bv,
-                                           double tau, double* acc0, double* jerk) {
-#pragma unroll
-  for (int k = 0; k < DW; ++k) {
-    const double dp = bp[k] - ap[k] - av[k] * tau;
-    const double dv = bv[k] - av[k];
-    acc0[k] = 6 * dp / (tau * tau) - 2 * dv / tau;
-    jerk[k] = -12 * dp / (tau * tau * tau) + 6 * dv / (tau * tau);
-  }
-}
-
 // Pass 1: one CTA per source row v, one thread per target u.  Velocity
 // prefilter (graph.hpp:70) and the exact-preserving lower-bound filter;
 // survivors are compacted in ascending-u order (warp ballots + CTA prefix)
@@ -398,85 +330,13 @@ __global__ void __launch_bounds__(128) k_regions(GraphArgs g, WorldD w, int64_t 
   } else {
     motion_state<DW>(m, j * g.dt, y, yd);
   }
-  constexpr int kMaxObs = 4096;
-  uint32_t pruned[kMaxObs / 32];
-  const int nw = (ws.n_obs + 31) / 32;
-  for (int q = 0; q < nw; ++q) pruned[q] = 0u;
-  int count = 0;
-  int64_t out = WRITE ? hs_off[x] : 0;
-  for (int iter = 0; iter < ws.n_obs; ++iter) {
-    int best = -1;
-    double best_sq = __longlong_as_double(0x7ff0000000000000ll);  // +inf
-    double d[DW];
-    for (int o = 0; o < ws.n_obs; ++o) {
-      if ((pruned[o >> 5] >> (o & 31)) & 1u) continue;
-      double cand[DW];
-#pragma unroll
-      for (int k = 0; k < DW; ++k) {
-        double c = y[k] < ws.lo[o * DW + k] ? ws.lo[o * DW + k] : y[k];  // max(y, lo)
-        c = ws.hi[o * DW + k] < c ? ws.hi[o * DW + k] : c;               // min(., hi)
-        cand[k] = c - y[k];
-      }
-      const double sq = sqnorm<DW>(cand);
-      if (sq < best_sq) {
-        best_sq = sq;
-        best = o;
-#pragma unroll
-        for (int k = 0; k < DW; ++k) d[k] = cand[k];
-      }
-    }
-    if (best < 0) break;
-    const double dd = sqnorm<DW>(d);
-    const double tol = 1e-12 * (1.0 + dd);
-    bool any = false;
-    for (int o = 0; o < ws.n_obs; ++o) {
-      if ((pruned[o >> 5] >> (o & 31)) & 1u) continue;
-      bool inside = true;
-      for (unsigned corner = 0; corner < (1u << DW) && inside; ++corner) {
-        double dot = 0;
-#pragma unroll
-        for (int k = 0; k < DW; ++k) {
-          const double c = ((corner >> k) & 1u) ? ws.hi[o * DW + k] : ws.lo[o * DW + k];
-          dot += d[k] * (c - y[k]);
-        }
-        if (dot < dd - tol) inside = false;
-      }
-      if (inside) {
-        pruned[o >> 5] |= 1u << (o & 31);
-        any = true;
-      }
-    }
-    if (!any) {
-      atomicExch(err, 1);
-      return;
-    }
-    if (WRITE) {
-      // project_halfspace (geom.hpp:163-183), eps_v = eps_a = 1e-6
-      double a[DW];
-      bool fb = false;
-      const double vn = sqrt(sqnorm<DW>(yd));
-      if (vn < 1e-6) {
-        fb = true;
-      } else {
-        double dy = 0.0;
-#pragma unroll
-        for (int k = 0; k < DW; ++k) dy = dy + d[k] * yd[k];
-        const double coef = dy / sqnorm<DW>(yd);
-#pragma unroll
-        for (int k = 0; k < DW; ++k) a[k] = d[k] - coef * yd[k];
-        if (sqrt(sqnorm<DW>(a)) < 1e-6 * sqrt(sqnorm<DW>(d))) fb = true;
-      }
-      if (fb) {
-#pragma unroll
-        for (int k = 0; k < DW; ++k) a[k] = d[k];
-      }
-#pragma unroll
-      for (int k = 0; k < DW; ++k) hs_a[out * DW + k] = a[k];
-      hs_b[out] = sqnorm<DW>(a);
-      hs_fb[out] = fb ? 1 : 0;
-      ++out;
-    }
-    ++count;
+  double* ao = WRITE ? hs_a + hs_off[x] * DW : nullptr;
+  double* bo = WRITE ? hs_b + hs_off[x] : nullptr;
+  uint8_t* fo = WRITE ? hs_fb + hs_off[x] : nullptr;
+  const int count = convex_region<DW>(ws, y, yd, ao, bo, fo);
+  if (count < 0) {
+    atomicExch(err, 1);
+    return;
   }
   if (!WRITE) hcount[x] = count;
 }
