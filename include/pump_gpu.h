@@ -152,7 +152,8 @@ int64_t pump_ctx_launch_count(pump_ctx* ctx);
  * units per family (PUMP_FAM_* order) and resets them. */
 int pump_ctx_profile(pump_ctx* ctx, int enable);
 int pump_ctx_profile_read(pump_ctx* ctx, double* ms, int64_t* counts, int64_t* work);
-/* out[0] host->device bytes, out[1] device->host bytes, out[2] MC rollout-steps. */
+/* out[0] host->device bytes, out[1] device->host bytes, out[2] MC rollout-steps,
+ * out[3] device allocations made so far (process-wide). */
 int pump_ctx_io_bytes(pump_ctx* ctx, int64_t* out);
 /* Overwrite a 256 MiB buffer (> 126 MB L2) on the ctx stream and synchronize. */
 int pump_ctx_flush_l2(pump_ctx* ctx);

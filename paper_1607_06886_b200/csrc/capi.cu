@@ -374,6 +374,7 @@ int pump_ctx_io_bytes(pump_ctx* ctx, int64_t* out) {
   out[0] = ctx->c.h2d_bytes;
   out[1] = ctx->c.d2h_bytes;
   out[2] = ctx->c.mc_rollout_steps;
+  out[3] = g_dev_allocs;
   return PUMP_OK;
 }
 

@@ -817,6 +817,9 @@ int pump_graph_upload(pump_ctx* ctx, const pump_graph_view* v, pump_graph** out)
       up(G.e_nsteps, v->edge_nsteps, E * 4);
       up(G.wp_off, v->edge_wp_off, (E + 1) * 8);
       up(G.hs_off, v->wp_hs_off, (NW + 1) * 8);
+      std::vector<int32_t> cnt(NW + 1, 0);
+      for (int64_t w = 0; w < NW; ++w) cnt[w] = static_cast<int32_t>(v->wp_hs_off[w + 1] - v->wp_hs_off[w]);
+      up(G.hs_cnt, cnt.data(), (NW + 1) * 4);
       up(G.hs_a, v->hs_a, H * dw * 8);
       up(G.hs_b, v->hs_b, H * 8);
       G.hs_fb.ensure(H + 256);
@@ -869,10 +872,33 @@ int pump_graph_export(const pump_graph* g, pump_graph_view* v) {
     dn(v->edge_jerk, G.e_jerk, G.E * dw * 8);
     dn(v->edge_nsteps, G.e_nsteps, G.E * 4);
     dn(v->edge_wp_off, G.wp_off, (G.E + 1) * 8);
-    dn(v->wp_hs_off, G.hs_off, (G.NW + 1) * 8);
-    dn(v->hs_a, G.hs_a, G.H * dw * 8);
-    dn(v->hs_b, G.hs_b, G.H * 8);
-    dn(v->hs_fallback, G.hs_fb, G.H);
+    // half-spaces: waypoint w owns [hs_off[w], hs_off[w] + hs_cnt[w]) on the
+    // device; the exported view is the reference's waypoint-ordered CSR
+    if (v->wp_hs_off || v->hs_a || v->hs_b || v->hs_fallback) {
+      const int64_t NW = G.NW, H = G.H;
+      std::vector<int64_t> start(NW + 1);
+      std::vector<int32_t> cnt(NW + 1);
+      std::vector<double> a(static_cast<size_t>(H) * dw + 1), b(H + 1);
+      std::vector<uint8_t> fb(H + 1);
+      c.d2h(start.data(), G.hs_off.p, NW * 8);
+      c.d2h(cnt.data(), G.hs_cnt.p, NW * 4);
+      c.d2h(a.data(), G.hs_a.p, H * dw * 8);
+      c.d2h(b.data(), G.hs_b.p, H * 8);
+      c.d2h(fb.data(), G.hs_fb.p, H);
+      c.sync();
+      int64_t o = 0;
+      if (v->wp_hs_off) v->wp_hs_off[0] = 0;
+      for (int64_t w = 0; w < NW; ++w) {
+        for (int32_t h = 0; h < cnt[w]; ++h, ++o) {
+          const int64_t src = start[w] + h;
+          for (int k = 0; k < dw; ++k)
+            if (v->hs_a) v->hs_a[o * dw + k] = a[src * dw + k];
+          if (v->hs_b) v->hs_b[o] = b[src];
+          if (v->hs_fallback) v->hs_fallback[o] = fb[src];
+        }
+        if (v->wp_hs_off) v->wp_hs_off[w + 1] = o;
+      }
+    }
     if (v->goal_nodes) std::memcpy(v->goal_nodes, G.goal_nodes.data(), G.goal_nodes.size() * 4);
     c.sync();
   });

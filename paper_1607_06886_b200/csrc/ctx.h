@@ -1,6 +1,8 @@
 // pump_ctx internals: device, stream, events and grow-only device buffers.
 #pragma once
 
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <string>
@@ -11,6 +13,9 @@
 #include <memory>
 
 namespace pumpg {
+
+// cudaMalloc calls made by DBuf (a steady-state solve should make none)
+inline int64_t g_dev_allocs = 0;
 
 struct DevGraph;
 struct DevExplore;
@@ -25,6 +30,8 @@ struct DBuf {
     cap = 0;
     size_t want = bytes < 256 ? 256 : bytes;
     PUMP_CUDA(cudaMalloc(&p, want));
+    ++g_dev_allocs;
+    if (std::getenv("PUMP_DEBUG_ALLOC")) std::fprintf(stderr, "[pump alloc] ensure %zu\n", want);
     cap = want;
   }
   // grow keeping the first `keep` bytes
@@ -33,6 +40,8 @@ struct DBuf {
     void* q = nullptr;
     size_t want = bytes + bytes / 2;
     PUMP_CUDA(cudaMalloc(&q, want));
+    ++g_dev_allocs;
+    if (std::getenv("PUMP_DEBUG_ALLOC")) std::fprintf(stderr, "[pump alloc] grow %zu\n", want);
     if (p && keep) PUMP_CUDA(cudaMemcpyAsync(q, p, keep, cudaMemcpyDeviceToDevice, st));
     if (p) {
       PUMP_CUDA(cudaStreamSynchronize(st));
@@ -78,6 +87,7 @@ struct Ctx {
   std::map<std::string, DBuf> scratch;
   DBuf& buf(const std::string& name, size_t bytes) {
     DBuf& b = scratch[name];
+    if (bytes > b.cap && std::getenv("PUMP_DEBUG_ALLOC")) std::fprintf(stderr, "[pump alloc] scratch %s\n", name.c_str());
     b.ensure(bytes);
     return b;
   }

@@ -42,6 +42,7 @@ struct ExpandArgs {
   const int32_t* e_nsteps;
   const int64_t* wp_off;
   const int64_t* hs_off;
+  const int32_t* hs_cnt;
   const double* hs_a;
   const double* hs_b;
   const int32_t* head;
@@ -101,11 +102,10 @@ __global__ void __launch_bounds__(256) k_expand(const ExpandArgs a) {
 #pragma unroll
   for (int c = 0; c < CH; ++c) kill[c] = false;
   const int64_t w0 = a.wp_off[e];
-  if (lane == 0)
-    atomicAdd(reinterpret_cast<unsigned long long*>(&a.st->hs_tests),
-              static_cast<unsigned long long>(a.hs_off[w0 + ns] - a.hs_off[w0]));
+  int64_t tests = 0;
   for (int j = 0; j < ns; ++j) {
-    const int64_t h0 = a.hs_off[w0 + j], h1 = a.hs_off[w0 + j + 1];
+    const int64_t h0 = a.hs_off[w0 + j], h1 = h0 + a.hs_cnt[w0 + j];
+    tests += h1 - h0;
     if (h0 == h1) continue;
     const double* row = a.dy + static_cast<int64_t>(pt + j + 1) * a.N * DW;
     double p[CH][DW];
@@ -129,6 +129,7 @@ __global__ void __launch_bounds__(256) k_expand(const ExpandArgs a) {
       }
     }
   }
+  if (lane == 0) atomicAdd(reinterpret_cast<unsigned long long*>(&a.st->hs_tests), static_cast<unsigned long long>(tests));
   int pop = 0;
 #pragma unroll
   for (int w = 0; w < (CH + 1) / 2; ++w) {
@@ -599,7 +600,8 @@ void run_explore_device(DevExplore& X, Ctx& c, const DevGraph& G, const ExploreA
     if (T > 0) {
       ExpandArgs ea{X.group.as<int32_t>(), X.task_off.as<int64_t>(), d_G, d_T, G.row_ptr.as<int64_t>(),
                     G.e_to.as<int32_t>(), G.e_cost.as<double>(), G.e_nsteps.as<int32_t>(), G.wp_off.as<int64_t>(),
-                    G.hs_off.as<int64_t>(), G.hs_a.as<double>(), G.hs_b.as<double>(), X.head.as<int32_t>(),
+                    G.hs_off.as<int64_t>(), G.hs_cnt.as<int32_t>(), G.hs_a.as<double>(), G.hs_b.as<double>(),
+                    X.head.as<int32_t>(),
                     X.cost.as<double>(), X.t_end.as<int32_t>(), X.mask.as<uint64_t>(), c.bank.as<double>(), N,
                     c.bank_horizon, W, prm.alpha_max, X.cand_keep.as<uint8_t>(), X.cand_head.as<int32_t>(),
                     X.cand_src.as<int32_t>(), X.cand_tend.as<int32_t>(), X.cand_cost.as<double>(),

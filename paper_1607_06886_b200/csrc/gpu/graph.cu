@@ -46,20 +46,29 @@ struct LbGrid {
   double c1[kLbK];      // 1 / t of each interval's upper end
 };
 
+// bound on [tl, th]: tl + c3(th) sum_k min|dp0_k - vbar_k tau|^2 + c1(th) |dv|^2
+template <int DW>
+__device__ __forceinline__ bool interval_clears(const double* dp0, const double* vb, double dv2, double tl, double th,
+                                                double c3, double c1, double thr) {
+  double s = 0.0;
+#pragma unroll
+  for (int k = 0; k < DW; ++k) {
+    const double m1 = dp0[k] - vb[k] * tl, m2 = dp0[k] - vb[k] * th;
+    const double a1 = m1 < 0 ? -m1 : m1, a2 = m2 < 0 ? -m2 : m2;
+    const double mm = ((m1 > 0) == (m2 > 0) && m1 != 0 && m2 != 0) ? (a1 < a2 ? a1 : a2) : 0.0;
+    s += mm * mm;
+  }
+  return (tl + c3 * s + c1 * dv2) * (1.0 - 1e-12) >= thr;
+}
+
+// Coarse-to-fine: 16 coarse intervals (every 4th grid point) first; a coarse
+// interval whose bound fails is re-checked on its 4 fine sub-intervals.
 template <int DW>
 __device__ __forceinline__ bool lb_rejects(const double* dp0, const double* vb, double dv2, const LbGrid& L) {
-  for (int i = 0; i < kLbK; ++i) {
-    const double th = L.t[i], tl = L.t[i + 1];
-    double s = 0.0;
-#pragma unroll
-    for (int k = 0; k < DW; ++k) {
-      const double m1 = dp0[k] - vb[k] * tl, m2 = dp0[k] - vb[k] * th;
-      const double a1 = m1 < 0 ? -m1 : m1, a2 = m2 < 0 ? -m2 : m2;
-      const double mm = ((m1 > 0) == (m2 > 0) && m1 != 0 && m2 != 0) ? (a1 < a2 ? a1 : a2) : 0.0;
-      s += mm * mm;
-    }
-    const double lb = tl + L.c3[i] * s + L.c1[i] * dv2;
-    if (lb * (1.0 - 1e-12) < L.thr) return false;
+  for (int ci = 0; ci < kLbK; ci += 4) {
+    if (interval_clears<DW>(dp0, vb, dv2, L.t[ci + 4], L.t[ci], L.c3[ci], L.c1[ci], L.thr)) continue;
+    for (int i = ci; i < ci + 4; ++i)
+      if (!interval_clears<DW>(dp0, vb, dv2, L.t[i + 1], L.t[i], L.c3[i], L.c1[i], L.thr)) return false;
   }
   double s = 0.0;  // head interval (0, t_K]
 #pragma unroll
@@ -289,7 +298,8 @@ __global__ void __launch_bounds__(128) k_regions(GraphArgs g, WorldD w, int64_t 
                                                  const int32_t* __restrict__ e_to, const double* __restrict__ e_tau,
                                                  const double* __restrict__ e_acc0, const double* __restrict__ e_jerk,
                                                  const int32_t* __restrict__ e_nsteps, int32_t* __restrict__ hcount,
-                                                 const int64_t* __restrict__ hs_off, double* __restrict__ hs_a,
+                                                 const int64_t* __restrict__ hs_off, int32_t* __restrict__ hs_cnt,
+                                                 double* __restrict__ hs_a,
                                                  double* __restrict__ hs_b, uint8_t* __restrict__ hs_fb,
                                                  int* __restrict__ err) {
   extern __shared__ double smem[];
@@ -339,6 +349,99 @@ __global__ void __launch_bounds__(128) k_regions(GraphArgs g, WorldD w, int64_t 
     return;
   }
   if (!WRITE) hcount[x] = count;
+  if (WRITE) hs_cnt[x] = count;
+}
+
+// Single pass for small obstacle sets (<= 16 boxes): each waypoint computes
+// its half-spaces once into registers and reserves output space with one
+// warp-aggregated atomicAdd.  Waypoint w owns [hs_off[w], hs_off[w] +
+// hs_cnt[w]) (not in waypoint order; export rebuilds the CSR).  If the
+// reserved total exceeds cap nothing past cap is written and the host reruns
+// with the exact size (the counter returns it).
+constexpr int kOnceMaxObs = 16;
+template <int DW>
+__global__ void __launch_bounds__(128) k_regions_once(GraphArgs g, WorldD w, int64_t n_wp, int64_t n_edges,
+                                                      const int64_t* __restrict__ wp_off,
+                                                      const int32_t* __restrict__ e_from,
+                                                      const int32_t* __restrict__ e_to, const double* __restrict__ e_tau,
+                                                      const double* __restrict__ e_acc0,
+                                                      const double* __restrict__ e_jerk,
+                                                      const int32_t* __restrict__ e_nsteps, int64_t cap,
+                                                      unsigned long long* __restrict__ counter,
+                                                      int64_t* __restrict__ hs_off, int32_t* __restrict__ hs_cnt,
+                                                      double* __restrict__ hs_a, double* __restrict__ hs_b,
+                                                      uint8_t* __restrict__ hs_fb, int* __restrict__ err) {
+  extern __shared__ double smem[];
+  const WorldD ws = stage_world<DW>(w, smem);
+  const int64_t x = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int lane = threadIdx.x & 31;
+  const bool active = x < n_wp;
+  double la[kOnceMaxObs * DW], lb[kOnceMaxObs];
+  uint8_t lf[kOnceMaxObs];
+  int n = 0;
+  if (active) {
+    int64_t lo = 0, hi = n_edges;
+    while (hi - lo > 1) {
+      const int64_t mid = (lo + hi) >> 1;
+      if (wp_off[mid] <= x)
+        lo = mid;
+      else
+        hi = mid;
+    }
+    const int64_t e = lo;
+    const int j = static_cast<int>(x - wp_off[e]) + 1;
+    const int L = e_nsteps[e];
+    const int v = e_from[e], u = e_to[e];
+    MotionD<DW> m;
+    m.tau = e_tau[e];
+#pragma unroll
+    for (int k = 0; k < DW; ++k) {
+      m.p0[k] = g.pos[v * DW + k];
+      m.v0[k] = g.vel[v * DW + k];
+      m.p1[k] = g.pos[u * DW + k];
+      m.v1[k] = g.vel[u * DW + k];
+      m.a[k] = e_acc0[e * DW + k];
+      m.j[k] = e_jerk[e * DW + k];
+    }
+    double y[DW], yd[DW];
+    if (j == L) {
+#pragma unroll
+      for (int k = 0; k < DW; ++k) {
+        y[k] = m.p1[k];
+        yd[k] = m.v1[k];
+      }
+    } else {
+      motion_state<DW>(m, j * g.dt, y, yd);
+    }
+    n = convex_region<DW>(ws, y, yd, la, lb, lf);
+    if (n < 0) {
+      atomicExch(err, 1);
+      n = 0;
+    }
+  }
+  // warp-aggregated reservation
+  int incl = n;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += y;
+  }
+  const int total = __shfl_sync(0xffffffffu, incl, 31);
+  unsigned long long base = 0;
+  if (lane == 31 && total > 0) base = atomicAdd(counter, static_cast<unsigned long long>(total));
+  base = __shfl_sync(0xffffffffu, base, 31);
+  if (!active) return;
+  const int64_t start = static_cast<int64_t>(base) + (incl - n);
+  hs_off[x] = start;
+  hs_cnt[x] = n;
+  if (start + n <= cap) {
+    for (int h = 0; h < n; ++h) {
+#pragma unroll
+      for (int k = 0; k < DW; ++k) hs_a[(start + h) * DW + k] = la[h * DW + k];
+      hs_b[start + h] = lb[h];
+      hs_fb[start + h] = lf[h];
+    }
+  }
 }
 
 // ------------------------------------------------------------------ host
@@ -485,10 +588,47 @@ void build_graph_device(DevGraph& G, Ctx& c, int n, int dw, const double* h_pos,
   c.d2h(&NW, G.wp_off.as<int64_t>() + E, 8);
   c.sync();
   G.NW = NW;
-  DBuf& hcnt = c.buf("g_hcnt", al((NW + 1) * 4));
   DBuf& err = c.buf("g_err", 256);
   G.hs_off.ensure(al((NW + 2) * 8));
+  G.hs_cnt.ensure(al((NW + 2) * 4));
   PUMP_CUDA(cudaMemsetAsync(err.p, 0, 4, st));
+  if (w.n_obs <= kOnceMaxObs) {
+    DBuf& ctr = c.buf("g_hs_counter", 256);
+    int64_t cap = std::max<int64_t>(G.hs_cap, NW * 4 + 16);
+    for (int attempt = 0; attempt < 2; ++attempt) {
+      G.hs_a.ensure(al((cap + 1) * dw * 8));
+      G.hs_b.ensure(al((cap + 1) * 8));
+      G.hs_fb.ensure(al(cap + 1));
+      G.hs_cap = cap;
+      PUMP_CUDA(cudaMemsetAsync(ctr.p, 0, 8, st));
+      if (NW > 0) {
+        KScope ks(st, F_REGIONS);
+        dispatch_dw(dw, [&]<int DW>() {
+          if (wsmem > 48 * 1024)
+            PUMP_CUDA(cudaFuncSetAttribute(k_regions_once<DW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wsmem));
+          k_regions_once<DW><<<grid_for(NW, 128), 128, wsmem, st>>>(
+              ga, wd, NW, E, G.wp_off.as<int64_t>(), G.e_from.as<int32_t>(), G.e_to.as<int32_t>(),
+              G.e_tau.as<double>(), G.e_acc0.as<double>(), G.e_jerk.as<double>(), G.e_nsteps.as<int32_t>(), cap,
+              ctr.as<unsigned long long>(), G.hs_off.as<int64_t>(), G.hs_cnt.as<int32_t>(), G.hs_a.as<double>(),
+              G.hs_b.as<double>(), G.hs_fb.as<uint8_t>(), err.as<int>());
+        });
+        ++c.launches;
+        PUMP_CUDA(cudaGetLastError());
+      }
+      int64_t H = 0;
+      int herr = 0;
+      c.d2h(&H, ctr.p, 8);
+      c.d2h(&herr, err.p, 4);
+      c.sync();
+      if (herr) throw std::runtime_error("local_convex_region: pruning loop failed to make progress");
+      G.H = H;
+      if (H <= cap) break;
+      cap = H + H / 8;  // rerun with room to spare (per-waypoint content is deterministic)
+    }
+    c.sync();
+    return;
+  }
+  DBuf& hcnt = c.buf("g_hcnt", al((NW + 1) * 4));
   if (NW > 0) {
     KScope ks(st, F_REGIONS);
     dispatch_dw(dw, [&]<int DW>() {
@@ -499,7 +639,7 @@ void build_graph_device(DevGraph& G, Ctx& c, int n, int dw, const double* h_pos,
       k_regions<DW, false><<<grid_for(NW, 128), 128, wsmem, st>>>(
           ga, wd, NW, E, G.wp_off.as<int64_t>(), G.e_from.as<int32_t>(), G.e_to.as<int32_t>(), G.e_tau.as<double>(),
           G.e_acc0.as<double>(), G.e_jerk.as<double>(), G.e_nsteps.as<int32_t>(), hcnt.as<int32_t>(), nullptr,
-          nullptr, nullptr, nullptr, err.as<int>());
+          nullptr, nullptr, nullptr, nullptr, err.as<int>());
     });
     ++c.launches;
     PUMP_CUDA(cudaGetLastError());
@@ -522,7 +662,7 @@ void build_graph_device(DevGraph& G, Ctx& c, int n, int dw, const double* h_pos,
       k_regions<DW, true><<<grid_for(NW, 128), 128, wsmem, st>>>(
           ga, wd, NW, E, G.wp_off.as<int64_t>(), G.e_from.as<int32_t>(), G.e_to.as<int32_t>(), G.e_tau.as<double>(),
           G.e_acc0.as<double>(), G.e_jerk.as<double>(), G.e_nsteps.as<int32_t>(), nullptr, G.hs_off.as<int64_t>(),
-          G.hs_a.as<double>(), G.hs_b.as<double>(), G.hs_fb.as<uint8_t>(), err.as<int>());
+          G.hs_cnt.as<int32_t>(), G.hs_a.as<double>(), G.hs_b.as<double>(), G.hs_fb.as<uint8_t>(), err.as<int>());
     });
     ++c.launches;
     PUMP_CUDA(cudaGetLastError());

@@ -13,7 +13,9 @@ struct DevGraph {
   DBuf row_ptr;                                           // n + 1 (int64)
   DBuf e_from, e_to, e_cost, e_tau, e_acc0, e_jerk, e_nsteps;
   DBuf wp_off;                                            // E + 1 (int64)
-  DBuf hs_off;                                            // NW + 1 (int64)
+  DBuf hs_off;                                            // NW (+1): first half-space of each waypoint
+  int64_t hs_cap = 0;                                     // half-space slots in hs_a/hs_b/hs_fb
+  DBuf hs_cnt;                                            // NW: half-spaces of each waypoint
   DBuf hs_a, hs_b, hs_fb;                                 // H x dw, H, H
   std::vector<int32_t> goal_nodes;                        // host, ascending
   std::vector<double> h_pos, h_vel;                       // host copies of the nodes

@@ -206,7 +206,7 @@ constexpr int lanes_per_rollout() {
 }
 
 template <int DW>
-__global__ void __launch_bounds__(kMcBlock) k_mc_sep(const SepBlocks B, WorldD w, const int64_t* __restrict__ traj_off,
+__global__ void __launch_bounds__(kMcBlock, 5) k_mc_sep(const SepBlocks B, WorldD w, const int64_t* __restrict__ traj_off,
                                                      const double* __restrict__ ynom_all, int64_t r0, int64_t r1,
                                                      uint64_t seed, double eps_cc, unsigned long long* __restrict__ hits,
                                                      unsigned long long* __restrict__ steps_out) {
@@ -244,21 +244,31 @@ __global__ void __launch_bounds__(kMcBlock) k_mc_sep(const SepBlocks B, WorldD w
   const unsigned gmask = ((LPR == 32) ? 0xffffffffu : ((1u << LPR) - 1u)) << gbase;
   bool collided = false;
   int steps = 0;
-  // per-axis blocks in registers
-  double F[16], Gv[8], Gw[4], Sv[4], S0[4], C[2];
-#pragma unroll
-  for (int x = 0; x < 16; ++x) F[x] = B.F[k][x];
-#pragma unroll
-  for (int x = 0; x < 8; ++x) Gv[x] = B.Gv[k][x];
-#pragma unroll
-  for (int x = 0; x < 4; ++x) {
-    Gw[x] = B.Gw[k][x];
-    Sv[x] = B.Sv[k][x];
-    S0[x] = B.S0[k][x];
+  // per-axis blocks in shared memory (39 doubles per axis; the 3 axes of a
+  // warp access land in distinct banks, lane 3 of a group broadcasts axis 0)
+  __shared__ double s_blk[3][40];
+  for (int x = threadIdx.x; x < 3 * 40; x += blockDim.x) {
+    const int ax = x / 40, o = x % 40;
+    double v = 0.0;
+    if (ax < DW) {
+      if (o < 16) v = B.F[ax][o];
+      else if (o < 24) v = B.Gv[ax][o - 16];
+      else if (o < 28) v = B.Gw[ax][o - 24];
+      else if (o < 32) v = B.Sv[ax][o - 28];
+      else if (o < 36) v = B.S0[ax][o - 32];
+      else if (o < 38) v = B.C[ax][o - 36];
+      else if (o == 38) v = B.Sw[ax];
+    }
+    s_blk[ax][o] = v;
   }
-  const double Sw = B.Sw[k];
-  C[0] = B.C[k][0];
-  C[1] = B.C[k][1];
+  __syncthreads();
+  const double* F = &s_blk[k][0];
+  const double* Gv = &s_blk[k][16];
+  const double* Gw = &s_blk[k][24];
+  const double* Sv = &s_blk[k][28];
+  const double* S0 = &s_blk[k][32];
+  const double* C = &s_blk[k][36];
+  const double Sw = s_blk[k][38];
   const uint64_t ch0 = static_cast<uint64_t>(k), ch1 = static_cast<uint64_t>(DW + k);
 
   double z[4];
