@@ -306,6 +306,14 @@ __host__ __device__ __forceinline__ void motion_bbox(const MotionD<DW>& m, doubl
 // neither contain a tested point nor be hit by a tested segment, and if the
 // box is strictly inside the workspace bounds no bounds test can fail; when
 // nothing remains the answer is "no collision" without subdividing.
+//
+// Span pruning (exact-preserving, same argument one level down): every point
+// tested inside a span [t0, t1] and every leaf segment below it lies within
+// the chord box of (p(t0), p(t1)) widened per axis by the interpolation error
+// bound (t1 - t0)^2 / 8 * max|p''| (p'' = a + j s is linear, so its maximum
+// is at an end) plus the rounding margin of motion_bbox.  A span whose box
+// is inside the workspace and separated from every candidate obstacle holds
+// no failing test, so its subtree is skipped.
 template <int DW>
 __host__ __device__ inline bool motion_collides(const MotionD<DW>& m, const WorldD& w, double eps_cc) {
   double bl[DW], bh[DW];
@@ -358,6 +366,36 @@ __host__ __device__ inline bool motion_collides(const MotionD<DW>& m, const Worl
   if (m.tau <= 0) return false;
   motion_pos<DW>(m, m.tau, p1);
   if (!free_pt(p1)) return true;
+  double marg[DW];
+#pragma unroll
+  for (int k = 0; k < DW; ++k) {
+    const double p0k = m.p0[k], v0 = m.v0[k], a = m.a[k], j = m.j[k], tau = m.tau;
+    marg[k] = 1e-6 * (1.0 + (p0k < 0 ? -p0k : p0k) + (v0 < 0 ? -v0 : v0) * tau + (a < 0 ? -a : a) * tau * tau / 2 +
+                      (j < 0 ? -j : j) * tau * tau * tau / 6 + (m.p1[k] < 0 ? -m.p1[k] : m.p1[k]));
+  }
+  auto span_clear = [&](double t0, double t1, const double* q0, const double* q1) {
+    if (!masked) return false;
+    const double h = t1 - t0;
+    double sl[DW], sh[DW];
+#pragma unroll
+    for (int k = 0; k < DW; ++k) {
+      const double d0 = m.a[k] + m.j[k] * t0, d1 = m.a[k] + m.j[k] * t1;
+      const double ad0 = d0 < 0 ? -d0 : d0, ad1 = d1 < 0 ? -d1 : d1;
+      const double dev = 0.125 * h * h * (ad0 > ad1 ? ad0 : ad1) + marg[k];
+      sl[k] = (q0[k] < q1[k] ? q0[k] : q1[k]) - dev;
+      sh[k] = (q0[k] < q1[k] ? q1[k] : q0[k]) + dev;
+      if (!inside && !(sl[k] > w.blo[k] && sh[k] < w.bhi[k])) return false;
+    }
+    for (int q = 0; q < kMaskWords; ++q)
+      for (uint64_t x = cand[q]; x; x &= x - 1) {
+        const int o = q * 64 + __builtin_ctzll_hd(x);
+        bool sep = false;
+#pragma unroll
+        for (int k = 0; k < DW; ++k) sep = sep || (sh[k] < w.lo[o * DW + k]) || (sl[k] > w.hi[o * DW + k]);
+        if (!sep) return false;
+      }
+    return true;
+  };
   double st0[64], st1[64];
   int sp = 0;
   double t0 = 0.0, t1 = m.tau;
@@ -365,8 +403,12 @@ __host__ __device__ inline bool motion_collides(const MotionD<DW>& m, const Worl
     double diff[DW];
 #pragma unroll
     for (int k = 0; k < DW; ++k) diff[k] = p1[k] - p0[k];
-    if (sqrt(sqnorm<DW>(diff)) <= eps_cc || t1 - t0 < 1e-9) {
+    bool span_done = span_clear(t0, t1, p0, p1);
+    if (!span_done && (sqrt(sqnorm<DW>(diff)) <= eps_cc || t1 - t0 < 1e-9)) {
       if (seg_hit(p0, p1)) return true;
+      span_done = true;
+    }
+    if (span_done) {
       if (sp == 0) return false;
       --sp;
       t0 = st0[sp];
