@@ -200,9 +200,15 @@ SepBlocks sep_blocks(const HostLoop& L) {
   return B;
 }
 
+// One lane per axis: a rollout is a group of DW consecutive lanes; a warp
+// holds 32 / DW groups (DW = 3: 10 groups, lanes 30-31 idle).
 template <int DW>
 constexpr int lanes_per_rollout() {
-  return DW == 3 ? 4 : DW;
+  return DW;
+}
+template <int DW>
+constexpr int groups_per_warp() {
+  return 32 / DW;
 }
 
 template <int DW>
@@ -235,17 +241,19 @@ __global__ void __launch_bounds__(kMcBlock, 5) k_mc_sep(const SepBlocks B, World
   }
   __syncthreads();
   const double e = eps_cc > 1e-12 ? eps_cc : 1e-12;  // std::max(eps_cc, 1e-12)
+  constexpr int GPW = groups_per_warp<DW>();
   const int lane = threadIdx.x & 31;
-  const int q = lane % LPR;                 // axis of this lane (q < DW)
+  const int q = lane % LPR;                 // axis of this lane
+  const int g = lane / LPR;                 // rollout group in the warp (g == GPW: idle lanes)
   const int gbase = lane - q;               // first lane of the rollout group
-  const int k = q < DW ? q : 0;             // idle lanes mirror axis 0 (results unused)
-  const int64_t i = r0 + (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) / LPR;
-  const bool active = i < r1;
-  const unsigned gmask = ((LPR == 32) ? 0xffffffffu : ((1u << LPR) - 1u)) << gbase;
+  const int k = q;
+  const int64_t i = r0 + (static_cast<int64_t>(blockIdx.x) * (kMcBlock / 32) + (threadIdx.x >> 5)) * GPW + g;
+  const bool active = g < GPW && i < r1;
+  const unsigned gmask = gbase + LPR <= 32 ? ((1u << LPR) - 1u) << gbase : 0xffffffffu << gbase;
   bool collided = false;
   int steps = 0;
   // per-axis blocks in shared memory (39 doubles per axis; the 3 axes of a
-  // warp access land in distinct banks, lane 3 of a group broadcasts axis 0)
+  // warp access land in distinct banks)
   __shared__ double s_blk[3][40];
   for (int x = threadIdx.x; x < 3 * 40; x += blockDim.x) {
     const int ax = x / 40, o = x % 40;
@@ -339,9 +347,9 @@ __global__ void __launch_bounds__(kMcBlock, 5) k_mc_sep(const SepBlocks B, World
           if (!sep) cand |= 1ull << o;
         }
         // obstacles beyond the first 64 are never culled (checked below)
-        uint64_t all = cand;  // union of the group's shares
+        uint64_t all = 0;  // union of the group's shares
 #pragma unroll
-        for (int x = 1; x < LPR; x <<= 1) all |= __shfl_xor_sync(gmask, all, x);
+        for (int x = 0; x < LPR; ++x) all |= __shfl_sync(gmask, cand, gbase + x);  // group-uniform branch
         // the point y itself (t = 0 included): lane 0 of the group
         if (q == 0) {
           for (uint64_t m = all; m; m &= m - 1) {
@@ -448,11 +456,11 @@ void launch_mc(const HostLoop& HL, const DevWorld& w, int n_traj, const int64_t*
       wd.bhi[k] = w.bhi[k];
     }
     dispatch_dw(HL.dw, [&]<int DW>() {
-      constexpr int LPR = lanes_per_rollout<DW>();
       const size_t smem = (static_cast<size_t>(max_points) * DW + 4 * static_cast<size_t>(w.n_obs) * DW) * sizeof(double);
       if (smem > 48 * 1024)
         PUMP_CUDA(cudaFuncSetAttribute(k_mc_sep<DW>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-      dim3 grid(grid_for((r1 - r0) * LPR, kMcBlock), n_traj);
+      constexpr int per_block = (kMcBlock / 32) * groups_per_warp<DW>();
+      dim3 grid(static_cast<unsigned>((r1 - r0 + per_block - 1) / per_block), n_traj);
       KScope ks(st, F_MC);
       k_mc_sep<DW><<<grid, kMcBlock, smem, st>>>(B, wd, d_traj_off, d_ynom, r0, r1, seed, eps_cc, d_hits, d_steps);
       ++*launches;
