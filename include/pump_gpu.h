@@ -149,7 +149,12 @@ double pump_ctx_last_kernel_ms(pump_ctx* ctx);
 int64_t pump_ctx_launch_count(pump_ctx* ctx);
 /* Measurement hooks (bench.py): per-kernel-family CUDA-event timing on the
  * launching stream; read returns total ms, launch counts and algorithmic work
- * units per family (PUMP_FAM_* order) and resets them. */
+ * units per family (PUMP_FAM_* order, PUMP_FAM_COUNT entries) and resets them. */
+enum {
+  PUMP_FAM_BANK_NOISE, PUMP_FAM_BANK_REC, PUMP_FAM_HSMC, PUMP_FAM_MC, PUMP_FAM_CONNECT, PUMP_FAM_COLLIDE,
+  PUMP_FAM_EMIT, PUMP_FAM_REGIONS, PUMP_FAM_EXPAND, PUMP_FAM_COMMIT, PUMP_FAM_DOM, PUMP_FAM_SCAN,
+  PUMP_FAM_SPLIT, PUMP_FAM_MISC, PUMP_FAM_PAIR, PUMP_FAM_COUNT
+};
 int pump_ctx_profile(pump_ctx* ctx, int enable);
 int pump_ctx_profile_read(pump_ctx* ctx, double* ms, int64_t* counts, int64_t* work);
 /* out[0] host->device bytes, out[1] device->host bytes, out[2] MC rollout-steps,

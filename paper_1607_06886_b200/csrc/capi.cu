@@ -7,6 +7,9 @@
 #include "ctx.h"
 #include "guard.h"
 
+static_assert(static_cast<int>(pumpg::F_COUNT) == PUMP_FAM_COUNT && static_cast<int>(pumpg::F_PAIR) == PUMP_FAM_PAIR,
+              "kernel family order must match pump_gpu.h");
+
 using namespace pumpg;
 
 namespace pumpg {

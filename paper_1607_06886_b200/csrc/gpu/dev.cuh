@@ -431,10 +431,55 @@ __host__ __device__ inline bool motion_collides(const MotionD<DW>& m, const Worl
   }
 }
 
-// connect() without the motion coefficients: returns ok; tau, cost out.
+// Lower bound of the connection cost (graph build filters).  With
+// dp0 = pb - pa, vbar = (va + vb) / 2 and dv = vb - va the cost is,
+// identically (steer.hpp:84-94 rewritten),
+//   c(tau) = tau + 12 q(tau) / tau^3 + D / tau,
+//   q(tau) = |dp0 - vbar tau|^2 = A - 2 B tau + C tau^2,  D = |dv|^2,
+// so on [tl, th]:  c >= tl + 12 min_[tl,th] q / th^3 + D / th.  The quadratic's
+// minimum is exact (vertex B / C or an end); the rounding margin
+// 1e-12 (A + 2|B| th + C th^2) dwarfs its evaluation error, and the caller's
+// threshold carries its own relative margin over r_n.
+struct PairLb {
+  double A, B, C, D, ts;  // ts = B / C (vertex), or -1 when C == 0
+};
+
 template <int DW>
+__host__ __device__ __forceinline__ PairLb pair_lb(const double* ap, const double* av, const double* bp,
+                                                   const double* bv) {
+  PairLb p{0.0, 0.0, 0.0, 0.0, -1.0};
+#pragma unroll
+  for (int k = 0; k < DW; ++k) {
+    const double dp = bp[k] - ap[k], vb = 0.5 * (av[k] + bv[k]), dv = bv[k] - av[k];
+    p.A += dp * dp;
+    p.B += dp * vb;
+    p.C += vb * vb;
+    p.D += dv * dv;
+  }
+  if (p.C > 0) p.ts = p.B / p.C;
+  return p;
+}
+
+// c3 = 12 / th^3 and c1 = 1 / th, both rounded down (the caller's grid).
+__host__ __device__ __forceinline__ bool interval_clears(const PairLb& p, double tl, double th, double c3, double c1,
+                                                         double thr) {
+  const double ql = p.A - 2.0 * p.B * tl + p.C * tl * tl, qh = p.A - 2.0 * p.B * th + p.C * th * th;
+  double qm = ql < qh ? ql : qh;
+  if (p.ts > tl && p.ts < th) qm = p.A - p.B * p.ts;
+  const double ab = p.B < 0 ? -p.B : p.B;
+  qm -= 1e-12 * (p.A + 2.0 * ab * th + p.C * th * th);
+  if (qm < 0) qm = 0;
+  return (tl + c3 * qm + c1 * p.D) * (1.0 - 1e-12) >= thr;
+}
+
+// connect() without the motion coefficients: returns ok; tau, cost out.
+// With kReject (graph build only) a pair is abandoned after the 64-point scan
+// when the cost's lower bound on the golden-section bracket [lo, hi] clears
+// reject_thr on all 16 sub-intervals: the returned tau lies in that bracket,
+// so its cost would be >= r_n and graph.hpp:72 would drop the pair anyway.
+template <int DW, bool kReject = false>
 __host__ __device__ inline bool connect_dev(const double* ap, const double* av, const double* bp, const double* bv, double tau_max,
-                            double ratio, double& tau_out, double& cost_out) {
+                            double ratio, double& tau_out, double& cost_out, double reject_thr = 0.0) {
   bool same = true;
 #pragma unroll
   for (int k = 0; k < DW; ++k) same = same && (ap[k] == bp[k]) && (av[k] == bv[k]);
@@ -459,6 +504,19 @@ __host__ __device__ inline bool connect_dev(const double* ap, const double* av, 
   double lo = best_tau / (best_idx > 0 ? ratio : 1.0);
   double hi = best_tau * ratio;
   hi = (tau_max < hi) ? tau_max : hi;  // std::min(best_tau * ratio, tau_max)
+  if constexpr (kReject) {
+    const PairLb plb = pair_lb<DW>(ap, av, bp, bv);
+    constexpr int kParts = 16;
+    bool clears = lo > 0;
+    double t_hi = hi;
+    for (int p = kParts - 1; p >= 0 && clears; --p) {
+      const double t_lo = p == 0 ? lo : lo + (hi - lo) * (static_cast<double>(p) / kParts);
+      const double c3 = 12.0 / (t_hi * t_hi * t_hi) * (1.0 - 1e-14), c1 = 1.0 / t_hi * (1.0 - 1e-14);
+      clears = interval_clears(plb, t_lo, t_hi, c3, c1, reject_thr);
+      t_hi = t_lo;
+    }
+    if (clears) return false;
+  }
   const double gr = 0.5 * (sqrt(5.0) - 1.0);
   double x1 = hi - gr * (hi - lo), x2 = lo + gr * (hi - lo);
   double f1 = steer_cost<DW>(ap, av, bp, bv, x1), f2 = steer_cost<DW>(ap, av, bp, bv, x2);

@@ -28,57 +28,47 @@ struct GraphArgs {
   double r_n, dt, eps_cc, tau_max, ratio;
 };
 
-// Exact-preserving pair filter.  With dp0 = pb - pa, vbar = (va + vb)/2 and
-// dv = vb - va the connection cost is, identically,
-//   c(tau) = tau + sum_k 12 (dp0_k - vbar_k tau)^2 / tau^3 + |dv|^2 / tau
-// (steer.hpp:84-94 rewritten).  On [t_lo, t_hi] it is bounded below by
-//   t_lo + 12 sum_k min|dp0_k - vbar_k tau|^2 / t_hi^3 + |dv|^2 / t_hi,
-// and by tau itself beyond thr.  If every interval's bound exceeds
-// thr = r_n (1 + 1e-6), the pair's true minimum cost exceeds r_n by a margin
-// far above the rounding of the reference's cost evaluation (<= ~1e-13
-// relative), so connect() would return cost >= r_n (or ok = false) and the
-// reference would reject the pair at graph.hpp:72: skipping it changes nothing.
-constexpr int kLbK = 64;
+// Exact-preserving pair filter (bound in dev.cuh, pair_lb / interval_clears).
+// It is also bounded below by tau itself beyond thr.  If a cover of (0, thr]
+// by intervals whose bounds exceed thr = r_n (1 + 1e-6) exists, the pair's
+// true minimum cost exceeds r_n by a margin far above the rounding of the
+// reference's cost evaluation (<= ~1e-13 relative), so connect() would return
+// cost >= r_n (or ok = false) and the reference would reject the pair at
+// graph.hpp:72: skipping it changes nothing.
+constexpr int kLbK = 256;  // 4^4 leaves: a 4-ary interval tree, coarse to fine
 struct LbGrid {
   double thr;
-  double t[kLbK + 1];  // decreasing: t[0] = thr, t[K] = thr * 1e-4
+  double t[kLbK + 1];   // decreasing: t[0] = thr, t[K] = thr * 1e-4
   double c3[kLbK + 1];  // 12 / t^3 of each interval's upper end (c3[K]: head interval)
   double c1[kLbK];      // 1 / t of each interval's upper end
 };
 
-// bound on [tl, th]: tl + c3(th) sum_k min|dp0_k - vbar_k tau|^2 + c1(th) |dv|^2
-template <int DW>
-__device__ __forceinline__ bool interval_clears(const double* dp0, const double* vb, double dv2, double tl, double th,
-                                                double c3, double c1, double thr) {
-  double s = 0.0;
-#pragma unroll
-  for (int k = 0; k < DW; ++k) {
-    const double m1 = dp0[k] - vb[k] * tl, m2 = dp0[k] - vb[k] * th;
-    const double a1 = m1 < 0 ? -m1 : m1, a2 = m2 < 0 ? -m2 : m2;
-    const double mm = ((m1 > 0) == (m2 > 0) && m1 != 0 && m2 != 0) ? (a1 < a2 ? a1 : a2) : 0.0;
-    s += mm * mm;
+// The interval [t[i + SPAN], t[i]] clears if its own bound does or all four
+// quarters clear (the tree only decides how much work the cover takes).
+template <int SPAN>
+__device__ __forceinline__ bool lb_tree(const PairLb& p, const LbGrid& L, int i) {
+  if (interval_clears(p, L.t[i + SPAN], L.t[i], L.c3[i], L.c1[i], L.thr)) return true;
+  if constexpr (SPAN == 1) {
+    return false;
+  } else {
+#pragma unroll 1
+    for (int q = 0; q < 4; ++q)
+      if (!lb_tree<SPAN / 4>(p, L, i + q * (SPAN / 4))) return false;
+    return true;
   }
-  return (tl + c3 * s + c1 * dv2) * (1.0 - 1e-12) >= thr;
 }
 
-// Coarse-to-fine: 16 coarse intervals (every 4th grid point) first; a coarse
-// interval whose bound fails is re-checked on its 4 fine sub-intervals.
-template <int DW>
-__device__ __forceinline__ bool lb_rejects(const double* dp0, const double* vb, double dv2, const LbGrid& L) {
-  for (int ci = 0; ci < kLbK; ci += 4) {
-    if (interval_clears<DW>(dp0, vb, dv2, L.t[ci + 4], L.t[ci], L.c3[ci], L.c1[ci], L.thr)) continue;
-    for (int i = ci; i < ci + 4; ++i)
-      if (!interval_clears<DW>(dp0, vb, dv2, L.t[i + 1], L.t[i], L.c3[i], L.c1[i], L.thr)) return false;
-  }
-  double s = 0.0;  // head interval (0, t_K]
-#pragma unroll
-  for (int k = 0; k < DW; ++k) {
-    const double m1 = dp0[k], m2 = dp0[k] - vb[k] * L.t[kLbK];
-    const double a1 = m1 < 0 ? -m1 : m1, a2 = m2 < 0 ? -m2 : m2;
-    const double mm = ((m1 > 0) == (m2 > 0) && m1 != 0 && m2 != 0) ? (a1 < a2 ? a1 : a2) : 0.0;
-    s += mm * mm;
-  }
-  return L.c3[kLbK] * s * (1.0 - 1e-12) >= L.thr;
+__device__ __forceinline__ bool lb_rejects(const PairLb& p, const LbGrid& L) {
+  // head interval (0, t_K]: c >= 12 min q / t_K^3
+  const double tk = L.t[kLbK];
+  const double q0 = p.A, qk = p.A - 2.0 * p.B * tk + p.C * tk * tk;
+  double qm = q0 < qk ? q0 : qk;
+  if (p.ts > 0 && p.ts < tk) qm = p.A - p.B * p.ts;
+  const double ab = p.B < 0 ? -p.B : p.B;
+  qm -= 1e-12 * (p.A + 2.0 * ab * tk + p.C * tk * tk);
+  if (qm < 0) qm = 0;
+  if (!(L.c3[kLbK] * qm * (1.0 - 1e-12) >= L.thr)) return false;
+  return lb_tree<kLbK>(p, L, 0);
 }
 
 LbGrid make_lb_grid(double r_n) {
@@ -105,6 +95,12 @@ __global__ void __launch_bounds__(kRowBlock) k_pair_filter(GraphArgs g, const Lb
                                                            int32_t* __restrict__ row_cnt, int32_t* __restrict__ su) {
   __shared__ int wtot[kRowBlock / 32];
   __shared__ int base_s;
+  __shared__ LbGrid sl;  // lanes index the grid divergently: shared, not the constant bank
+  {
+    const double* src = reinterpret_cast<const double*>(&lb);
+    double* dst = reinterpret_cast<double*>(&sl);
+    for (int x = threadIdx.x; x < static_cast<int>(sizeof(LbGrid) / 8); x += blockDim.x) dst[x] = src[x];
+  }
   const int v = blockIdx.x;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   double ap[DW], av[DW];
@@ -119,16 +115,14 @@ __global__ void __launch_bounds__(kRowBlock) k_pair_filter(GraphArgs g, const Lb
     const int u = u0 + threadIdx.x;
     bool keep = false;
     if (u < g.n && u != v) {
-      double dp0[DW], vb[DW], dv[DW];
+      double bp[DW], bv[DW];
 #pragma unroll
       for (int k = 0; k < DW; ++k) {
-        const double bp = g.pos[u * DW + k], bv = g.vel[u * DW + k];
-        dv[k] = bv - av[k];
-        dp0[k] = bp - ap[k];
-        vb[k] = 0.5 * (av[k] + bv);
+        bp[k] = g.pos[u * DW + k];
+        bv[k] = g.vel[u * DW + k];
       }
-      const double dv2 = sqnorm<DW>(dv);
-      keep = !(2.0 * sqrt(dv2) >= g.r_n) && !lb_rejects<DW>(dp0, vb, dv2, lb);
+      const PairLb plb = pair_lb<DW>(ap, av, bp, bv);
+      keep = !(2.0 * sqrt(plb.D) >= g.r_n) && !lb_rejects(plb, sl);
     }
     const unsigned bal = __ballot_sync(0xffffffffu, keep);
     if (lane == 0) wtot[warp] = __popc(bal);
@@ -181,7 +175,7 @@ __global__ void __launch_bounds__(128) k_connect(GraphArgs g, int cap, int64_t n
     bv[k] = g.vel[u * DW + k];
   }
   double tau = 0, cost = 0;
-  const bool ok = connect_dev<DW>(ap, av, bp, bv, g.tau_max, g.ratio, tau, cost);
+  const bool ok = connect_dev<DW, true>(ap, av, bp, bv, g.tau_max, g.ratio, tau, cost, g.r_n * (1.0 + 1e-6));
   keep[s] = (ok && !(cost >= g.r_n) && !(tau <= 0)) ? 1 : 0;  // graph.hpp:72
   s_v[s] = v;
   s_u[s] = u;
@@ -479,7 +473,7 @@ void build_graph_device(DevGraph& G, Ctx& c, int n, int dw, const double* h_pos,
   for (;;) {  // pass 1 with an exact per-row refit if a row overflows the slab
     DBuf& suB = c.buf("g_su", al(static_cast<size_t>(n) * cap * 4));
     {
-      KScope ks(st, F_CONNECT);
+      KScope ks(st, F_PAIR);
       dispatch_dw(dw, [&]<int DW>() {
         k_pair_filter<DW><<<n, kRowBlock, 0, st>>>(ga, lbg, cap, rcnt.as<int32_t>(), suB.as<int32_t>());
       });

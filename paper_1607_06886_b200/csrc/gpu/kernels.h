@@ -25,9 +25,10 @@ inline void cuda_check(cudaError_t e, const char* what) {
 // ------------------------------------------------------- kernel profiler
 // Kernel families timed with CUDA events on the launching stream when a
 // profiler is active on this host thread (pump_ctx_profile).
+// same order as PUMP_FAM_* in pump_gpu.h
 enum KFam {
   F_BANK_NOISE, F_BANK_REC, F_HSMC, F_MC, F_CONNECT, F_COLLIDE, F_EMIT, F_REGIONS,
-  F_EXPAND, F_COMMIT, F_DOM, F_SCAN, F_SPLIT, F_MISC, F_COUNT
+  F_EXPAND, F_COMMIT, F_DOM, F_SCAN, F_SPLIT, F_MISC, F_PAIR, F_COUNT
 };
 
 struct KProf {

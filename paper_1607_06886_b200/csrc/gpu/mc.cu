@@ -211,8 +211,8 @@ constexpr int groups_per_warp() {
   return 32 / DW;
 }
 
-template <int DW>
-__global__ void __launch_bounds__(kMcBlock, 5) k_mc_sep(const SepBlocks B, WorldD w, const int64_t* __restrict__ traj_off,
+template <int DW, int MINB>
+__global__ void __launch_bounds__(kMcBlock, MINB) k_mc_sep(const SepBlocks B, WorldD w, const int64_t* __restrict__ traj_off,
                                                      const double* __restrict__ ynom_all, int64_t r0, int64_t r1,
                                                      uint64_t seed, double eps_cc, unsigned long long* __restrict__ hits,
                                                      unsigned long long* __restrict__ steps_out) {
@@ -457,12 +457,21 @@ void launch_mc(const HostLoop& HL, const DevWorld& w, int n_traj, const int64_t*
     }
     dispatch_dw(HL.dw, [&]<int DW>() {
       const size_t smem = (static_cast<size_t>(max_points) * DW + 4 * static_cast<size_t>(w.n_obs) * DW) * sizeof(double);
-      if (smem > 48 * 1024)
-        PUMP_CUDA(cudaFuncSetAttribute(k_mc_sep<DW>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
       constexpr int per_block = (kMcBlock / 32) * groups_per_warp<DW>();
       dim3 grid(static_cast<unsigned>((r1 - r0 + per_block - 1) / per_block), n_traj);
-      KScope ks(st, F_MC);
-      k_mc_sep<DW><<<grid, kMcBlock, smem, st>>>(B, wd, d_traj_off, d_ynom, r0, r1, seed, eps_cc, d_hits, d_steps);
+      static const int minb = std::getenv("PUMP_MC_MINB") ? std::atoi(std::getenv("PUMP_MC_MINB")) : 5;
+      auto go = [&]<int MINB>() {
+        if (smem > 48 * 1024)
+          PUMP_CUDA(cudaFuncSetAttribute(k_mc_sep<DW, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(smem)));
+        KScope ks(st, F_MC);
+        k_mc_sep<DW, MINB><<<grid, kMcBlock, smem, st>>>(B, wd, d_traj_off, d_ynom, r0, r1, seed, eps_cc, d_hits,
+                                                          d_steps);
+      };
+      if (minb == 4) go.template operator()<4>();
+      else if (minb == 6) go.template operator()<6>();
+      else if (minb == 8) go.template operator()<8>();
+      else go.template operator()<5>();
       ++*launches;
       PUMP_CUDA(cudaGetLastError());
     });
