@@ -1,4 +1,5 @@
 // Ordered device primitives (see scan.cuh).
+#include <cstdlib>
 #include <stdexcept>
 
 #include "kernels.h"
@@ -106,6 +107,97 @@ __global__ void __launch_bounds__(kScanBlock) k_tile_scan(const InT* __restrict_
   }
 }
 
+// Single-pass scan with decoupled look-back: each CTA takes a ticket (tile
+// order independent of block scheduling), publishes its tile aggregate, then
+// resolves its exclusive prefix from its predecessors' published words
+// (aggregate or inclusive prefix, flag in the top 2 bits of one 64-bit word,
+// so a single aligned store publishes both).  The status words and the
+// ticket are zeroed by one memset before the launch.  Values are counts:
+// non-negative and < 2^62.
+constexpr uint64_t kStAgg = 1ull << 62, kStInc = 2ull << 62, kStVal = (1ull << 62) - 1;
+
+template <class InT>
+__global__ void __launch_bounds__(kScanBlock) k_scan_lookback(const InT* __restrict__ in, int64_t n,
+                                                              int64_t* __restrict__ out, uint64_t* __restrict__ status,
+                                                              unsigned* __restrict__ ticket, const int64_t* d_n) {
+  __shared__ int64_t tile[kScanTile];
+  __shared__ int64_t wsum[kScanBlock / 32];
+  __shared__ int64_t s_prefix;
+  __shared__ unsigned s_tile;
+  if (d_n) n = min(n, *d_n);
+  if (threadIdx.x == 0) s_tile = atomicAdd(ticket, 1u);
+  __syncthreads();
+  const unsigned t = s_tile;
+  const int64_t base = static_cast<int64_t>(t) * kScanTile;
+  if (base >= n && !(n <= 0 && t == 0)) return;  // beyond the device-side count
+#pragma unroll
+  for (int k = 0; k < kScanItems; ++k) {
+    const int64_t i = base + k * kScanBlock + threadIdx.x;
+    tile[k * kScanBlock + threadIdx.x] = i < n ? static_cast<int64_t>(in[i]) : 0;
+  }
+  __syncthreads();
+  int64_t v[kScanItems];
+  int64_t s = 0;
+#pragma unroll
+  for (int k = 0; k < kScanItems; ++k) {
+    v[k] = tile[threadIdx.x * kScanItems + k];
+    s += v[k];
+  }
+  const int64_t inc = warp_incl_scan(s);
+  if ((threadIdx.x & 31) == 31) wsum[threadIdx.x >> 5] = inc;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    int64_t w = threadIdx.x < kScanBlock / 32 ? wsum[threadIdx.x] : 0;
+    const int64_t wi = warp_incl_scan(w);
+    if (threadIdx.x < kScanBlock / 32) wsum[threadIdx.x] = wi - w;
+    const int64_t agg = __shfl_sync(0xffffffffu, wi, 31);
+    // publish, then look back (warp 0)
+    volatile uint64_t* vs = status;
+    if (t == 0) {
+      if (threadIdx.x == 0) {
+        vs[0] = kStInc | static_cast<uint64_t>(agg);
+        s_prefix = 0;
+      }
+    } else {
+      if (threadIdx.x == 0) vs[t] = kStAgg | static_cast<uint64_t>(agg);
+      int64_t prefix = 0;
+      int64_t j = static_cast<int64_t>(t) - 1 - threadIdx.x;  // this lane's predecessor
+      while (true) {
+        uint64_t w2 = j >= 0 ? vs[j] : static_cast<uint64_t>(kStInc);  // before tile 0: inclusive 0
+        while (__any_sync(0xffffffffu, (w2 >> 62) == 0)) {
+          if ((w2 >> 62) == 0) w2 = vs[j];
+        }
+        const unsigned incm = __ballot_sync(0xffffffffu, (w2 >> 62) == 2);
+        // lanes up to (and including) the nearest inclusive word contribute
+        const int stop = incm ? __ffs(incm) - 1 : 31;
+        int64_t val = (static_cast<int>(threadIdx.x) <= stop) ? static_cast<int64_t>(w2 & kStVal) : 0;
+        val = warp_sum(val);
+        prefix += val;
+        if (incm) break;
+        j -= 32;
+      }
+      if (threadIdx.x == 0) {
+        vs[t] = kStInc | static_cast<uint64_t>(prefix + agg);
+        s_prefix = prefix;
+      }
+    }
+    if (threadIdx.x == 0 && base + kScanTile >= n) out[n > 0 ? n : 0] = s_prefix + agg;  // total (last tile)
+  }
+  __syncthreads();
+  int64_t run = s_prefix + wsum[threadIdx.x >> 5] + inc - s;
+#pragma unroll
+  for (int k = 0; k < kScanItems; ++k) {
+    tile[threadIdx.x * kScanItems + k] = run;
+    run += v[k];
+  }
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < kScanItems; ++k) {
+    const int64_t i = base + k * kScanBlock + threadIdx.x;
+    if (i < n) out[i] = tile[k * kScanBlock + threadIdx.x];
+  }
+}
+
 size_t scan_temp_bytes(int64_t n) { return static_cast<size_t>((n + kScanTile - 1) / kScanTile + 1) * 8 + 256; }
 
 template <class InT>
@@ -116,12 +208,21 @@ void exclusive_scan(const InT* d_in, int64_t* d_out, int64_t n, void* d_temp, cu
     return;
   }
   const int64_t tiles = (n + kScanTile - 1) / kScanTile;
-  int64_t* partial = static_cast<int64_t*>(d_temp);
+  uint64_t* status = reinterpret_cast<uint64_t*>(static_cast<char*>(d_temp) + 256);
+  unsigned* ticket = static_cast<unsigned*>(d_temp);
   KScope ks(st, F_SCAN);
-  k_tile_sum<InT><<<static_cast<unsigned>(tiles), kScanBlock, 0, st>>>(d_in, n, partial, d_n);
-  k_scan_partials<<<1, 1024, 0, st>>>(partial, tiles, d_out, n, d_n);
-  k_tile_scan<InT><<<static_cast<unsigned>(tiles), kScanBlock, 0, st>>>(d_in, n, partial, d_out, d_n);
-  *launches += 3;
+  static const bool three_pass = std::getenv("PUMP_SCAN_3PASS") != nullptr;
+  if (three_pass) {
+    int64_t* partial = static_cast<int64_t*>(d_temp);
+    k_tile_sum<InT><<<static_cast<unsigned>(tiles), kScanBlock, 0, st>>>(d_in, n, partial, d_n);
+    k_scan_partials<<<1, 1024, 0, st>>>(partial, tiles, d_out, n, d_n);
+    k_tile_scan<InT><<<static_cast<unsigned>(tiles), kScanBlock, 0, st>>>(d_in, n, partial, d_out, d_n);
+    *launches += 3;
+  } else {
+    PUMP_CUDA(cudaMemsetAsync(d_temp, 0, 256 + static_cast<size_t>(tiles) * 8, st));
+    k_scan_lookback<InT><<<static_cast<unsigned>(tiles), kScanBlock, 0, st>>>(d_in, n, d_out, status, ticket, d_n);
+    *launches += 1;
+  }
   PUMP_CUDA(cudaGetLastError());
 }
 
