@@ -34,7 +34,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 FAMILIES = ["bank_noise", "bank_rec", "hsmc", "mc", "connect", "collide", "emit", "regions", "expand", "commit",
-            "dom", "scan", "multisplit", "misc", "pair_filter"]
+            "dom", "scan", "multisplit", "misc", "pair_filter", "mc_table"]
 
 
 def mc_ops_per_step(d: int, dw: int, n_obs: int, segs: float = 3.0) -> float:

@@ -153,7 +153,7 @@ int64_t pump_ctx_launch_count(pump_ctx* ctx);
 enum {
   PUMP_FAM_BANK_NOISE, PUMP_FAM_BANK_REC, PUMP_FAM_HSMC, PUMP_FAM_MC, PUMP_FAM_CONNECT, PUMP_FAM_COLLIDE,
   PUMP_FAM_EMIT, PUMP_FAM_REGIONS, PUMP_FAM_EXPAND, PUMP_FAM_COMMIT, PUMP_FAM_DOM, PUMP_FAM_SCAN,
-  PUMP_FAM_SPLIT, PUMP_FAM_MISC, PUMP_FAM_PAIR, PUMP_FAM_COUNT
+  PUMP_FAM_SPLIT, PUMP_FAM_MISC, PUMP_FAM_PAIR, PUMP_FAM_MC_TABLE, PUMP_FAM_COUNT
 };
 int pump_ctx_profile(pump_ctx* ctx, int enable);
 int pump_ctx_profile_read(pump_ctx* ctx, double* ms, int64_t* counts, int64_t* work);

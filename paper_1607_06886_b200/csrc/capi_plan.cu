@@ -324,7 +324,7 @@ static std::vector<double> mc_values(Ctx& c, const HostLoop& L, const DevWorld& 
   shard_range(n_mc, c.rank, c.world, &r0, &r1);
   c.tic();
   launch_mc(L, w, nt, d_off.as<int64_t>(), d_y.as<double>(), max_pts, r0, r1, seed, eps_cc,
-            d_h.as<unsigned long long>(), c.stream, &c.launches, d_h.as<unsigned long long>() + nt);
+            d_h.as<unsigned long long>(), c.stream, &c.launches, d_h.as<unsigned long long>() + nt, &c.mc_table);
   allreduce_sum_i64(c, d_h.as<int64_t>(), nt);
   *mc_ms += c.toc();
   *rollouts += (r1 - r0) * nt;
@@ -464,6 +464,7 @@ static HostLoop loop_of(const pumpb::ClosedLoop& cl) {
 
 // run_pump (pump.hpp:170-263)
 static void run_pump_device(Ctx& c, const pumpb::Scenario& s, const DevGraph* prebuilt, pump_result& R) {
+  c.mc_table.invalidate();  // the MC table is built inside every solve (no state across solves)
   using clk = std::chrono::steady_clock;
   auto secs = [](clk::time_point a, clk::time_point b) { return std::chrono::duration<double>(b - a).count(); };
   const int dw = s.workspace_dim();

@@ -14,56 +14,10 @@
 
 namespace pumpg {
 
-// cudaMalloc calls made by DBuf (a steady-state solve should make none)
-inline int64_t g_dev_allocs = 0;
-
 struct DevGraph;
 struct DevExplore;
 
-struct DBuf {
-  void* p = nullptr;
-  size_t cap = 0;
-  void ensure(size_t bytes) {
-    if (bytes <= cap) return;
-    if (p) cudaFree(p);
-    p = nullptr;
-    cap = 0;
-    size_t want = bytes < 256 ? 256 : bytes;
-    PUMP_CUDA(cudaMalloc(&p, want));
-    ++g_dev_allocs;
-    if (std::getenv("PUMP_DEBUG_ALLOC")) std::fprintf(stderr, "[pump alloc] ensure %zu\n", want);
-    cap = want;
-  }
-  // grow keeping the first `keep` bytes
-  void grow(size_t bytes, size_t keep, cudaStream_t st) {
-    if (bytes <= cap) return;
-    void* q = nullptr;
-    size_t want = bytes + bytes / 2;
-    PUMP_CUDA(cudaMalloc(&q, want));
-    ++g_dev_allocs;
-    if (std::getenv("PUMP_DEBUG_ALLOC")) std::fprintf(stderr, "[pump alloc] grow %zu\n", want);
-    if (p && keep) PUMP_CUDA(cudaMemcpyAsync(q, p, keep, cudaMemcpyDeviceToDevice, st));
-    if (p) {
-      PUMP_CUDA(cudaStreamSynchronize(st));
-      cudaFree(p);
-    }
-    p = q;
-    cap = want;
-  }
-  template <class T>
-  T* as() const {
-    return static_cast<T*>(p);
-  }
-  void release() {
-    if (p) cudaFree(p);
-    p = nullptr;
-    cap = 0;
-  }
-  ~DBuf() { release(); }
-  DBuf() = default;
-  DBuf(const DBuf&) = delete;
-  DBuf& operator=(const DBuf&) = delete;
-};
+
 
 struct Ctx {
   int device = 0;
@@ -83,6 +37,8 @@ struct Ctx {
   // in HBM across solves: no per-solve cudaMalloc/cudaFree)
   std::shared_ptr<DevGraph> run_graph;
   std::shared_ptr<DevExplore> run_explore;
+  // common-random-number table of the MC rollouts (kernels.h)
+  McTable mc_table;
   // named scratch buffers
   std::map<std::string, DBuf> scratch;
   DBuf& buf(const std::string& name, size_t bytes) {

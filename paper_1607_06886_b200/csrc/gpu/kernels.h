@@ -3,6 +3,8 @@
 #pragma once
 
 #include <cstdint>
+#include <cstdio>
+#include <cstdlib>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -22,13 +24,62 @@ inline void cuda_check(cudaError_t e, const char* what) {
 }
 #define PUMP_CUDA(x) ::pumpg::cuda_check((x), #x)
 
+// cudaMalloc calls made by DBuf (a steady-state solve should make none)
+inline int64_t g_dev_allocs = 0;
+
+// Grow-only device buffer.
+struct DBuf {
+  void* p = nullptr;
+  size_t cap = 0;
+  void ensure(size_t bytes) {
+    if (bytes <= cap) return;
+    if (p) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+    size_t want = bytes < 256 ? 256 : bytes;
+    PUMP_CUDA(cudaMalloc(&p, want));
+    ++g_dev_allocs;
+    if (std::getenv("PUMP_DEBUG_ALLOC")) std::fprintf(stderr, "[pump alloc] ensure %zu\n", want);
+    cap = want;
+  }
+  // grow keeping the first `keep` bytes
+  void grow(size_t bytes, size_t keep, cudaStream_t st) {
+    if (bytes <= cap) return;
+    void* q = nullptr;
+    size_t want = bytes + bytes / 2;
+    PUMP_CUDA(cudaMalloc(&q, want));
+    ++g_dev_allocs;
+    if (std::getenv("PUMP_DEBUG_ALLOC")) std::fprintf(stderr, "[pump alloc] grow %zu\n", want);
+    if (p && keep) PUMP_CUDA(cudaMemcpyAsync(q, p, keep, cudaMemcpyDeviceToDevice, st));
+    if (p) {
+      PUMP_CUDA(cudaStreamSynchronize(st));
+      cudaFree(p);
+    }
+    p = q;
+    cap = want;
+  }
+  template <class T>
+  T* as() const {
+    return static_cast<T*>(p);
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+  }
+  ~DBuf() { release(); }
+  DBuf() = default;
+  DBuf(const DBuf&) = delete;
+  DBuf& operator=(const DBuf&) = delete;
+};
+
 // ------------------------------------------------------- kernel profiler
 // Kernel families timed with CUDA events on the launching stream when a
 // profiler is active on this host thread (pump_ctx_profile).
 // same order as PUMP_FAM_* in pump_gpu.h
 enum KFam {
   F_BANK_NOISE, F_BANK_REC, F_HSMC, F_MC, F_CONNECT, F_COLLIDE, F_EMIT, F_REGIONS,
-  F_EXPAND, F_COMMIT, F_DOM, F_SCAN, F_SPLIT, F_MISC, F_PAIR, F_COUNT
+  F_EXPAND, F_COMMIT, F_DOM, F_SCAN, F_SPLIT, F_MISC, F_PAIR, F_MC_TABLE, F_COUNT
 };
 
 struct KProf {
@@ -126,8 +177,28 @@ void launch_hsmc_batch(int dw, int n, int horizon, const double* d_dy, int64_t n
 // --------------------------------------------------------------------- mc
 // Batched mc_certify (cp.hpp:214-268) over trajectories and the rollout
 // range [r0, r1); d_hits[j] += colliding rollouts of trajectory j.
+// Common-random-number table of the MC rollouts.  The deviation of rollout i
+// from ANY nominal trajectory, dy_t = C z_t, depends only on (closed loop,
+// seed, i, t): z_t is driven by the counter-hash noise alone.  The table
+// holds dy[t][i][k] for the rollouts [r0, r1) and t <= t_done, in HBM, so
+// every trajectory certified against the same (loop, seed) reads its
+// realizations instead of re-drawing ~9 normals per rollout-step.  Extended
+// in place (z_{t_done} kept per rollout) when a longer trajectory arrives.
+struct McTable {
+  DBuf dy;  // [t][i][k], t < t_cap
+  DBuf z;   // z_{t_done} per rollout
+  DBuf flags;  // per (trajectory, rollout) hit flags of one certification
+  int64_t r0 = 0, r1 = 0;
+  int t_done = -1, t_cap = 0;
+  uint64_t seed = 0;
+  HostLoop L;
+  bool valid = false;
+  bool sep = false;
+  void invalidate() { valid = false; }
+};
+
 void launch_mc(const HostLoop& L, const DevWorld& w, int n_traj, const int64_t* d_traj_off, const double* d_ynom,
                int max_points, int64_t r0, int64_t r1, uint64_t seed, double eps_cc, unsigned long long* d_hits,
-               cudaStream_t st, int64_t* launches, unsigned long long* d_steps = nullptr);
+               cudaStream_t st, int64_t* launches, unsigned long long* d_steps = nullptr, McTable* table = nullptr);
 
 }  // namespace pumpg

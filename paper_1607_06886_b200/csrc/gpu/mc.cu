@@ -439,11 +439,396 @@ __global__ void __launch_bounds__(kMcBlock, MINB) k_mc_sep(const SepBlocks B, Wo
   }
 }
 
+// ------------------------------------------------------------------------
+// Common-random-number table (kernels.h, McTable).
+//
+// Build, axis-separable loop: the lane-per-axis recursion of k_mc_sep with
+// the collision checks removed; writes dy_t = (0 + C0 z0) + C1 z1 for
+// t in [t_from, t_to].  zst holds z_{t_from - 1} (t_from > 0) and receives
+// z_{t_to}.  Every operation is the one k_mc_sep performs, in its order.
+template <int DW>
+__global__ void __launch_bounds__(kMcBlock) k_mctab_sep(const SepBlocks B, int64_t r0, int64_t n, uint64_t seed,
+                                                        int t_from, int t_to, double* __restrict__ dy,
+                                                        double* __restrict__ zst) {
+  constexpr int LPR = lanes_per_rollout<DW>();
+  constexpr int GPW = groups_per_warp<DW>();
+  __shared__ double s_blk[3][40];
+  for (int x = threadIdx.x; x < 3 * 40; x += blockDim.x) {
+    const int ax = x / 40, o = x % 40;
+    double v = 0.0;
+    if (ax < DW) {
+      if (o < 16) v = B.F[ax][o];
+      else if (o < 24) v = B.Gv[ax][o - 16];
+      else if (o < 28) v = B.Gw[ax][o - 24];
+      else if (o < 32) v = B.Sv[ax][o - 28];
+      else if (o < 36) v = B.S0[ax][o - 32];
+      else if (o < 38) v = B.C[ax][o - 36];
+      else if (o == 38) v = B.Sw[ax];
+    }
+    s_blk[ax][o] = v;
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const int q = lane % LPR, g = lane / LPR;
+  const int64_t li = (static_cast<int64_t>(blockIdx.x) * (kMcBlock / 32) + (threadIdx.x >> 5)) * GPW + g;
+  if (g >= GPW || li >= n) return;
+  const int64_t i = r0 + li;
+  const int k = q;
+  const double* F = &s_blk[k][0];
+  const double* Gv = &s_blk[k][16];
+  const double* Gw = &s_blk[k][24];
+  const double* Sv = &s_blk[k][28];
+  const double* S0 = &s_blk[k][32];
+  const double* C = &s_blk[k][36];
+  const double Sw = s_blk[k][38];
+  const uint64_t ch0 = static_cast<uint64_t>(k), ch1 = static_cast<uint64_t>(DW + k);
+  const uint64_t sa = hash_seed_a(seed, static_cast<uint64_t>(i));
+  double z[4];
+  double* zs = zst + (li * DW + k) * 4;
+  if (t_from == 0) {
+    const uint64_t pt = mix64(sa + 0ull);
+    const double n0 = normal_from_prefix(pt, ch0), n1 = normal_from_prefix(pt, ch1);  // kInitial channels
+    z[0] = (0.0 + S0[0] * n0) + S0[1] * n1;
+    z[1] = (0.0 + S0[2] * n0) + S0[3] * n1;
+    z[2] = 0.0;
+    z[3] = 0.0;
+  } else {
+#pragma unroll
+    for (int r = 0; r < 4; ++r) z[r] = zs[r];
+  }
+  for (int t = t_from; t <= t_to; ++t) {
+    if (t > 0) {
+      {
+        // z_t = ((F z_{t-1}) + u) + w, noise of the transition t-1 -> t
+        const uint64_t pt = mix64(sa + static_cast<uint64_t>(t - 1));
+        const uint64_t pt1 = mix64(sa + static_cast<uint64_t>(t));
+        const double nv0 = normal_from_prefix(pt, kProcess + ch0);
+        const double nv1 = normal_from_prefix(pt, kProcess + ch1);
+        const double nw = normal_from_prefix(pt1, kMeasurement + static_cast<uint64_t>(k));
+        const double t10 = (0.0 + Sv[0] * nv0) + Sv[1] * nv1;
+        const double t11 = (0.0 + Sv[2] * nv0) + Sv[3] * nv1;
+        const double t2 = 0.0 + Sw * nw;
+        double zn[4];
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+          const double u = (0.0 + Gv[2 * r] * t10) + Gv[2 * r + 1] * t11;
+          const double wv = 0.0 + Gw[r] * t2;
+          double c = 0.0;
+#pragma unroll
+          for (int x = 0; x < 4; ++x) c = c + F[r * 4 + x] * z[x];
+          zn[r] = (c + u) + wv;
+        }
+#pragma unroll
+        for (int r = 0; r < 4; ++r) z[r] = zn[r];
+      }
+    }
+    dy[(static_cast<int64_t>(t) * n + li) * DW + k] = (0.0 + C[0] * z[0]) + C[1] * z[1];
+  }
+#pragma unroll
+  for (int r = 0; r < 4; ++r) zs[r] = z[r];
+}
+
+// Build, general loop: one thread per rollout, the k_mc recursion.
+template <int D, int DW>
+__global__ void __launch_bounds__(kMcBlock) k_mctab_dense(const LoopP<D, DW> L, int64_t r0, int64_t n, uint64_t seed,
+                                                          int t_from, int t_to, double* __restrict__ dy,
+                                                          double* __restrict__ zst) {
+  const int64_t li = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (li >= n) return;
+  const int64_t i = r0 + li;
+  const uint64_t sa = hash_seed_a(seed, static_cast<uint64_t>(i));
+  double z[2 * D];
+  double* zs = zst + li * 2 * D;
+  if (t_from == 0) {
+    const uint64_t pt = mix64(sa + 0ull);
+    double nv[D];
+#pragma unroll
+    for (int k = 0; k < D; ++k) nv[k] = normal_from_prefix(pt, static_cast<uint64_t>(k));  // kInitial
+#pragma unroll
+    for (int r = 0; r < D; ++r) z[r] = row_dot<D>(L.S0 + r * D, nv);
+#pragma unroll
+    for (int r = D; r < 2 * D; ++r) z[r] = 0.0;
+  } else {
+#pragma unroll
+    for (int r = 0; r < 2 * D; ++r) z[r] = zs[r];
+  }
+  for (int t = t_from; t <= t_to; ++t) {
+    if (t > 0) {
+      const uint64_t pt = mix64(sa + static_cast<uint64_t>(t - 1));
+      const uint64_t pt1 = mix64(sa + static_cast<uint64_t>(t));
+      double nv[D], nw[DW], t1[D], t2[DW], u[2 * D], wv[2 * D];
+#pragma unroll
+      for (int k = 0; k < D; ++k) nv[k] = normal_from_prefix(pt, kProcess + k);
+#pragma unroll
+      for (int k = 0; k < DW; ++k) nw[k] = normal_from_prefix(pt1, kMeasurement + k);
+#pragma unroll
+      for (int r = 0; r < D; ++r) t1[r] = row_dot<D>(L.Sv + r * D, nv);
+#pragma unroll
+      for (int r = 0; r < DW; ++r) t2[r] = row_dot<DW>(L.Sw + r * DW, nw);
+#pragma unroll
+      for (int r = 0; r < 2 * D; ++r) {
+        u[r] = row_dot<D>(L.Gv + r * D, t1);
+        wv[r] = row_dot<DW>(L.Gw + r * DW, t2);
+      }
+      double zn[2 * D];
+#pragma unroll
+      for (int r = 0; r < 2 * D; ++r) zn[r] = (row_dot<2 * D>(L.F + r * 2 * D, z) + u[r]) + wv[r];
+#pragma unroll
+      for (int r = 0; r < 2 * D; ++r) z[r] = zn[r];
+    }
+#pragma unroll
+    for (int k = 0; k < DW; ++k) dy[(static_cast<int64_t>(t) * n + li) * DW + k] = row_dot<D>(L.C + k * D, z);
+  }
+#pragma unroll
+  for (int r = 0; r < 2 * D; ++r) zs[r] = z[r];
+}
+
+// Certify against the table.  A rollout's verdict is the OR of independent
+// per-step tests (point y_t, segment y_{t-1} -> y_t; the reference stops at
+// the first hit, which changes the work, not the verdict), so the steps are
+// spread over the grid: thread = (trajectory, rollout, chunk of kMcChunk
+// steps), y_t = ynom_t + dy_t (the addition k_mc performs), the collision
+// tests of k_mc_sep (bounds, bbox-culled obstacles, eps_cc-subdivided
+// segment).  A hit sets flag[j][i]; k_mc_count sums the flags.
+constexpr int kMcChunk = 8;
+template <int DW>
+__global__ void __launch_bounds__(kMcBlock) k_mc_tab(WorldD w, const int64_t* __restrict__ traj_off,
+                                                     const double* __restrict__ ynom_all, int64_t r0, int64_t r1,
+                                                     int64_t tab_r0, int64_t tab_n, const double* __restrict__ dy,
+                                                     double eps_cc, uint8_t* __restrict__ flags) {
+  extern __shared__ double smem[];
+  const int j = blockIdx.y;
+  const int64_t p_begin = traj_off[j];
+  const int n_pts = static_cast<int>(traj_off[j + 1] - p_begin);
+  const int T = n_pts - 1;
+  const int t_lo = blockIdx.z * kMcChunk;
+  if (t_lo > T) return;
+  const int t_hi = min(T, t_lo + kMcChunk - 1);
+  const int s_lo_t = t_lo > 0 ? t_lo - 1 : 0;  // rows staged: [s_lo_t, t_hi]
+  const int rows = t_hi - s_lo_t + 1;
+  double* s_y = smem;
+  double* s_lo = s_y + rows * DW;
+  double* s_hi = s_lo + w.n_obs * DW;
+  double* s_clo = s_hi + w.n_obs * DW;
+  double* s_chi = s_clo + w.n_obs * DW;
+  for (int x = threadIdx.x; x < rows * DW; x += blockDim.x) s_y[x] = ynom_all[(p_begin + s_lo_t) * DW + x];
+  for (int x = threadIdx.x; x < w.n_obs * DW; x += blockDim.x) {
+    const int k = x % DW;
+    const double bl = w.blo[k] < 0 ? -w.blo[k] : w.blo[k], bh = w.bhi[k] < 0 ? -w.bhi[k] : w.bhi[k];
+    const double lo = w.lo[x], hi = w.hi[x];
+    const double M = 1e-9 * (1.0 + (lo < 0 ? -lo : lo) + (hi < 0 ? -hi : hi) + 2.0 * (bl > bh ? bl : bh));
+    s_lo[x] = lo - M;
+    s_hi[x] = hi + M;
+    s_clo[x] = lo;
+    s_chi[x] = hi;
+  }
+  __syncthreads();
+  const double e = eps_cc > 1e-12 ? eps_cc : 1e-12;  // std::max(eps_cc, 1e-12)
+  const int64_t i = r0 + static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= r1) return;
+  const double* d = dy + (i - tab_r0) * DW;
+  const int64_t stride = tab_n * DW;
+  double dv[kMcChunk + 1][DW];  // issue every load of the chunk up front
+#pragma unroll
+  for (int r = 0; r <= kMcChunk; ++r)
+    if (s_lo_t + r <= t_hi) {
+#pragma unroll
+      for (int k = 0; k < DW; ++k) dv[r][k] = d[static_cast<int64_t>(s_lo_t + r) * stride + k];
+    }
+  double prev[DW];
+#pragma unroll
+  for (int k = 0; k < DW; ++k) prev[k] = s_y[k] + dv[0][k];
+  bool hit = false;
+#pragma unroll
+  for (int r = 0; r <= kMcChunk; ++r) {
+    const int t = s_lo_t + r;
+    if (t < t_lo || t > t_hi || hit) continue;  // row 0 of a later chunk only seeds prev
+    double y[DW];
+#pragma unroll
+    for (int k = 0; k < DW; ++k) y[k] = s_y[r * DW + k] + dv[r][k];
+    bool inb = true;
+#pragma unroll
+    for (int a = 0; a < DW; ++a) inb = inb && !(y[a] < w.blo[a] || y[a] > w.bhi[a]);
+    if (!inb) {
+      hit = true;
+      continue;
+    }
+    double bl[DW], bh[DW];
+#pragma unroll
+    for (int a = 0; a < DW; ++a) {
+      bl[a] = prev[a] < y[a] ? prev[a] : y[a];
+      bh[a] = prev[a] < y[a] ? y[a] : prev[a];
+    }
+    uint64_t cand = 0;
+    for (int o = 0; o < w.n_obs && o < 64; ++o) {
+      bool sep = false;
+#pragma unroll
+      for (int a = 0; a < DW; ++a) sep = sep || (bh[a] < s_lo[o * DW + a]) || (bl[a] > s_hi[o * DW + a]);
+      if (!sep) cand |= 1ull << o;
+    }
+    for (uint64_t m = cand; m && !hit; m &= m - 1) {
+      const int o = __ffsll(static_cast<long long>(m)) - 1;
+      if (box_contains<DW>(s_clo + o * DW, s_chi + o * DW, y)) hit = true;
+    }
+    for (int o = 64; o < w.n_obs && !hit; ++o)
+      if (box_contains<DW>(s_clo + o * DW, s_chi + o * DW, y)) hit = true;
+    // every subdivision point lies in bbox(prev, y) up to rounding: with no
+    // candidate obstacle and the box strictly inside the bounds, no
+    // sub-segment test can fail
+    bool clear = cand == 0 && w.n_obs <= 64;
+#pragma unroll
+    for (int a2 = 0; a2 < DW; ++a2) {
+      const double m = 1e-12 * (1.0 + (bl[a2] < 0 ? -bl[a2] : bl[a2]) + (bh[a2] < 0 ? -bh[a2] : bh[a2]));
+      clear = clear && bl[a2] - m > w.blo[a2] && bh[a2] + m < w.bhi[a2];
+    }
+    if (t > 0 && !hit && !clear) {  // segments prev -> y, subdivided to eps_cc (cp.hpp:237-248)
+      double diff[DW];
+#pragma unroll
+      for (int a = 0; a < DW; ++a) diff[a] = y[a] - prev[a];
+      const double len = sqrt(sqnorm<DW>(diff));
+      int segs = static_cast<int>(ceil(len / e));
+      if (segs < 1) segs = 1;
+      double p0[DW];
+#pragma unroll
+      for (int a = 0; a < DW; ++a) p0[a] = prev[a];
+      for (int s2 = 1; s2 <= segs && !hit; ++s2) {
+        double p1[DW];
+        const double f1 = static_cast<double>(s2) / segs;
+#pragma unroll
+        for (int a = 0; a < DW; ++a) p1[a] = prev[a] + (y[a] - prev[a]) * f1;
+        bool in1 = true;
+#pragma unroll
+        for (int a = 0; a < DW; ++a) in1 = in1 && !(p1[a] < w.blo[a] || p1[a] > w.bhi[a]);
+        if (!in1) {
+          hit = true;
+          break;
+        }
+        for (uint64_t m = cand; m; m &= m - 1) {
+          const int o = __ffsll(static_cast<long long>(m)) - 1;
+          if (box_contains<DW>(s_clo + o * DW, s_chi + o * DW, p1) ||
+              segment_hits<DW>(p0, p1, s_clo + o * DW, s_chi + o * DW)) {
+            hit = true;
+            break;
+          }
+        }
+        for (int o = 64; o < w.n_obs && !hit; ++o)
+          if (box_contains<DW>(s_clo + o * DW, s_chi + o * DW, p1) ||
+              segment_hits<DW>(p0, p1, s_clo + o * DW, s_chi + o * DW))
+            hit = true;
+#pragma unroll
+        for (int a = 0; a < DW; ++a) p0[a] = p1[a];
+      }
+    }
+#pragma unroll
+    for (int a = 0; a < DW; ++a) prev[a] = y[a];
+  }
+  if (hit) flags[static_cast<int64_t>(j) * (r1 - r0) + (i - r0)] = 1;
+}
+
+// hits[j] += rollouts flagged for trajectory j; steps += rollouts x (T_j + 1)
+__global__ void __launch_bounds__(256) k_mc_count(const uint8_t* __restrict__ flags, int64_t n,
+                                                  const int64_t* __restrict__ traj_off,
+                                                  unsigned long long* __restrict__ hits,
+                                                  unsigned long long* __restrict__ steps_out) {
+  const int j = blockIdx.y;
+  const uint8_t* f = flags + static_cast<int64_t>(j) * n;
+  unsigned c = 0;
+  for (int64_t x = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; x < n;
+       x += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    c += f[x];
+  c = __reduce_add_sync(0xffffffffu, c);
+  if ((threadIdx.x & 31) == 0 && c) atomicAdd(hits + j, static_cast<unsigned long long>(c));
+  if (steps_out && blockIdx.x == 0 && threadIdx.x == 0)
+    atomicAdd(steps_out, static_cast<unsigned long long>(n) * static_cast<unsigned long long>(traj_off[j + 1] - traj_off[j]));
+}
+
+static bool same_loop(const HostLoop& a, const HostLoop& b) {
+  return a.d == b.d && a.dw == b.dw && a.F == b.F && a.Gv == b.Gv && a.Gw == b.Gw && a.Sv == b.Sv && a.Sw == b.Sw &&
+         a.S0 == b.S0 && a.C == b.C;
+}
+
+// Make the table cover rollouts [r0, r1) and steps t <= T.  Returns false
+// when it would not fit the memory budget (the caller then runs the direct
+// kernels).
+static bool ensure_table(McTable& tab, const HostLoop& HL, int64_t r0, int64_t r1, uint64_t seed, int T,
+                         cudaStream_t st, int64_t* launches) {
+  const int64_t n = r1 - r0;
+  const int dw = HL.dw, d = HL.d;
+  const size_t row = static_cast<size_t>(n) * dw * 8;
+  constexpr size_t kBudget = size_t(24) << 30;  // 24 GiB of HBM at most
+  if (row * static_cast<size_t>(T + 1) > kBudget) return false;
+  if (!tab.valid || tab.seed != seed || tab.r0 != r0 || tab.r1 != r1 || !same_loop(tab.L, HL)) {
+    tab.valid = true;
+    tab.seed = seed;
+    tab.r0 = r0;
+    tab.r1 = r1;
+    tab.L = HL;
+    tab.t_done = -1;
+    tab.sep = HL.dw >= 2 && HL.dw <= 3 && separable(HL);
+    tab.z.ensure(static_cast<size_t>(n) * std::max(4 * dw, 2 * d) * 8 + 256);
+  }
+  if (T <= tab.t_done) return true;
+  const int t_from = tab.t_done + 1;
+  if (static_cast<size_t>(T + 1) * row > tab.dy.cap) {
+    // grow with headroom (the dy prefix is t-major: keep the rows built so far)
+    const int want = T + 1 + (T + 1) / 2;
+    const size_t bytes = std::min(static_cast<size_t>(want) * row, std::max(kBudget, static_cast<size_t>(T + 1) * row));
+    tab.dy.grow(bytes, static_cast<size_t>(t_from) * row, st);
+  }
+  KScope ks(st, F_MC_TABLE);
+  if (tab.sep) {
+    const SepBlocks B = sep_blocks(HL);
+    dispatch_dw(dw, [&]<int DW>() {
+      constexpr int per_block = (kMcBlock / 32) * groups_per_warp<DW>();
+      k_mctab_sep<DW><<<static_cast<unsigned>((n + per_block - 1) / per_block), kMcBlock, 0, st>>>(
+          B, r0, n, seed, t_from, T, tab.dy.as<double>(), tab.z.as<double>());
+    });
+  } else {
+    dispatch_dims(d, dw, [&]<int D, int DW>() {
+      const LoopP<D, DW> L = make_loop<D, DW>(HL);
+      k_mctab_dense<D, DW><<<grid_for(n, kMcBlock), kMcBlock, 0, st>>>(L, r0, n, seed, t_from, T,
+                                                                         tab.dy.as<double>(), tab.z.as<double>());
+    });
+  }
+  ++*launches;
+  PUMP_CUDA(cudaGetLastError());
+  tab.t_done = T;
+  return true;
+}
+
 void launch_mc(const HostLoop& HL, const DevWorld& w, int n_traj, const int64_t* d_traj_off, const double* d_ynom,
                int max_points, int64_t r0, int64_t r1, uint64_t seed, double eps_cc, unsigned long long* d_hits,
-               cudaStream_t st, int64_t* launches, unsigned long long* d_steps) {
+               cudaStream_t st, int64_t* launches, unsigned long long* d_steps, McTable* table) {
   if (r1 <= r0 || n_traj <= 0) return;
   if (HL.dw != w.dw) throw std::invalid_argument("mc_certify: workspace / model dimension mismatch");
+  static const bool direct = std::getenv("PUMP_MC_DIRECT") != nullptr;
+  if (table && !direct && ensure_table(*table, HL, r0, r1, seed, max_points - 1, st, launches)) {
+    WorldD wd;
+    wd.n_obs = w.n_obs;
+    wd.lo = w.d_lo;
+    wd.hi = w.d_hi;
+    for (int k = 0; k < 6; ++k) {
+      wd.blo[k] = w.blo[k];
+      wd.bhi[k] = w.bhi[k];
+    }
+    const int64_t n = r1 - r0;
+    table->flags.ensure(static_cast<size_t>(n) * n_traj + 256);
+    PUMP_CUDA(cudaMemsetAsync(table->flags.p, 0, static_cast<size_t>(n) * n_traj, st));
+    dispatch_dw(HL.dw, [&]<int DW>() {
+      const size_t smem = (static_cast<size_t>(kMcChunk + 1) * DW + 4 * static_cast<size_t>(w.n_obs) * DW) * sizeof(double);
+      if (smem > 48 * 1024)
+        PUMP_CUDA(cudaFuncSetAttribute(k_mc_tab<DW>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+      dim3 grid(grid_for(n, kMcBlock), n_traj, (max_points + kMcChunk - 1) / kMcChunk);
+      KScope ks(st, F_MC);
+      k_mc_tab<DW><<<grid, kMcBlock, smem, st>>>(wd, d_traj_off, d_ynom, r0, r1, table->r0, table->r1 - table->r0,
+                                                 table->dy.as<double>(), eps_cc, table->flags.as<uint8_t>());
+      k_mc_count<<<dim3(static_cast<unsigned>(std::min<int64_t>((n + 255) / 256, 64)), n_traj), 256, 0, st>>>(
+          table->flags.as<uint8_t>(), n, d_traj_off, d_hits, d_steps);
+    });
+    *launches += 2;
+    PUMP_CUDA(cudaGetLastError());
+    return;
+  }
   static const bool force_dense = std::getenv("PUMP_MC_DENSE") != nullptr;
   if (!force_dense && HL.dw >= 2 && HL.dw <= 3 && separable(HL)) {
     const SepBlocks B = sep_blocks(HL);
