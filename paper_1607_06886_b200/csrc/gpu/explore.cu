@@ -103,8 +103,31 @@ __global__ void __launch_bounds__(256) k_expand(const ExpandArgs a) {
   for (int c = 0; c < CH; ++c) kill[c] = false;
   const int64_t w0 = a.wp_off[e];
   int64_t tests = 0;
+  // waypoint metadata of the first 32 waypoints in one parallel load, and
+  // their half-space lines prefetched into L1: the loop below then walks
+  // cached data instead of a chain of dependent DRAM round trips
+  int64_t my_h0 = 0;
+  int my_cnt = 0;
+  if (lane < ns) {
+    my_h0 = a.hs_off[w0 + lane];
+    my_cnt = a.hs_cnt[w0 + lane];
+    if (my_cnt > 0) {
+      asm volatile("prefetch.global.L1 [%0];" ::"l"(a.hs_a + my_h0 * DW));
+      asm volatile("prefetch.global.L1 [%0];" ::"l"(a.hs_b + my_h0));
+      if (my_cnt * DW > 16) asm volatile("prefetch.global.L1 [%0];" ::"l"(a.hs_a + my_h0 * DW + 16));
+    }
+  }
   for (int j = 0; j < ns; ++j) {
-    const int64_t h0 = a.hs_off[w0 + j], h1 = h0 + a.hs_cnt[w0 + j];
+    int64_t h0;
+    int cnt;
+    if (j < 32) {
+      h0 = __shfl_sync(0xffffffffu, my_h0, j);
+      cnt = __shfl_sync(0xffffffffu, my_cnt, j);
+    } else {
+      h0 = a.hs_off[w0 + j];
+      cnt = a.hs_cnt[w0 + j];
+    }
+    const int64_t h1 = h0 + cnt;
     tests += h1 - h0;
     if (h0 == h1) continue;
     const double* row = a.dy + static_cast<int64_t>(pt + j + 1) * a.N * DW;
