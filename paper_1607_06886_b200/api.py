@@ -445,3 +445,71 @@ def set_comm(ctx: Context, rank: int, world: int, group=None):
     dist.broadcast(t, src=0, group=group)
     buf = t.cpu().numpy().astype(np.uint8)
     _check(lib().pump_ctx_set_comm(ctx.h, rank, world, _p(buf)))
+
+
+# ------------------------------------------------------- host-side helpers
+# The reference's scalar geometry / steering functions, evaluated on the host
+# by the same __host__ __device__ code the kernels run (pump_gpu.h "host
+# helpers"); no GPU needed.
+def _host_lib():
+    L = lib()
+    if not getattr(L, "_host_typed", False):
+        vp, d, i32 = C.c_void_p, C.c_double, C.c_int32
+        L.pump_connect.argtypes = [i32, vp, vp, vp, vp, d, vp, vp, vp]
+        L.pump_steer_cost.argtypes = [i32, vp, vp, vp, vp, d]
+        L.pump_steer_cost.restype = d
+        L.pump_point_free.argtypes = [vp, vp]
+        L.pump_motion_collides.argtypes = [vp, vp, vp, vp, vp, d, vp, vp, d, vp]
+        L.pump_local_convex_region.argtypes = [vp, vp, vp, i32, vp, vp, vp, vp]
+        L._host_typed = True
+    return L
+
+
+def _f64(x):
+    return np.ascontiguousarray(np.asarray(x, dtype=np.float64))
+
+
+def connect(ap, av, bp, bv, tau_max):
+    """steer.hpp:111-182 (connect): {'ok', 'tau', 'cost', 'acc0', 'jerk'}."""
+    arr = [_f64(x) for x in (ap, av, bp, bv)]
+    dw = arr[0].size
+    o, a0, j = np.zeros(3), np.zeros(dw), np.zeros(dw)
+    _check(_host_lib().pump_connect(dw, *[_p(x) for x in arr], tau_max, _p(o), _p(a0), _p(j)))
+    return {"ok": bool(o[0]), "tau": o[1], "cost": o[2], "acc0": a0, "jerk": j}
+
+
+def steer_cost(ap, av, bp, bv, tau):
+    """steer.hpp:84-94."""
+    arr = [_f64(x) for x in (ap, av, bp, bv)]
+    return _host_lib().pump_steer_cost(arr[0].size, *[_p(x) for x in arr], tau)
+
+
+def point_free(ws: dict, y) -> bool:
+    """geom.hpp:56-61."""
+    keep = A.Keep()
+    s = A.workspace_struct(ws, keep)
+    return bool(_host_lib().pump_point_free(C.byref(s), _p(keep.f64(y))))
+
+
+def motion_collides(ws: dict, fp, fv, tp, tv, tau, acc0, jerk, eps_cc) -> bool:
+    """geom.hpp:96-123."""
+    keep = A.Keep()
+    s = A.workspace_struct(ws, keep)
+    out = C.c_int32()
+    _check(_host_lib().pump_motion_collides(C.byref(s), *[_p(keep.f64(x)) for x in (fp, fv, tp, tv)], tau,
+                                            _p(keep.f64(acc0)), _p(keep.f64(jerk)), eps_cc, C.byref(out)))
+    return bool(out.value)
+
+
+def local_convex_region(ws: dict, y, ydot, cap: int = 4096):
+    """geom.hpp:189-225: (a [n, dw], b [n], fallback [n])."""
+    keep = A.Keep()
+    s = A.workspace_struct(ws, keep)
+    yy = keep.f64(y)
+    dw = yy.size
+    a, b, fb = np.zeros((cap, dw)), np.zeros(cap), np.zeros(cap, dtype=np.uint8)
+    n = C.c_int32()
+    _check(_host_lib().pump_local_convex_region(C.byref(s), _p(yy), _p(keep.f64(ydot)), cap, _p(a), _p(b), _p(fb),
+                                                C.byref(n)))
+    k = n.value
+    return a[:k], b[:k], fb[:k].astype(bool)

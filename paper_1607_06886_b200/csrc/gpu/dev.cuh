@@ -564,11 +564,17 @@ __host__ __device__ __forceinline__ void coeffs_dev(const double* ap, const doub
 // direction by the velocity (project_halfspace, geom.hpp:163-183, eps 1e-6).
 // Writes the half-spaces when a != nullptr; returns their count, or -1 when
 // the pruning loop fails (the reference's runtime_error).  <= 4096 boxes.
-template <int DW>
+//
+// The prune test "every corner c has d.(c - y) >= dd - tol" is evaluated on
+// the single corner that minimizes each term: fl(d_k (c_k - y_k)) is monotone
+// in c_k and rounded addition is monotone, so that corner's computed dot is
+// <= every corner's computed dot, and it is itself one of the corners: the
+// test is decided exactly by it (1 dot instead of 2^dw).  kWords bounds the
+// pruned bitmap (1 word keeps it in a register for <= 32 boxes).
+template <int DW, int kWords = 128>
 __host__ __device__ inline int convex_region(const WorldD& ws, const double* y, const double* yd, double* a_out,
                                              double* b_out, uint8_t* fb_out) {
-  constexpr int kMaxObs = 4096;
-  uint32_t pruned[kMaxObs / 32];
+  uint32_t pruned[kWords];
   const int nw = (ws.n_obs + 31) / 32;
   for (int q = 0; q < nw; ++q) pruned[q] = 0u;
   int count = 0;
@@ -599,16 +605,13 @@ __host__ __device__ inline int convex_region(const WorldD& ws, const double* y, 
     bool any = false;
     for (int o = 0; o < ws.n_obs; ++o) {
       if ((pruned[o >> 5] >> (o & 31)) & 1u) continue;
-      bool inside = true;
-      for (unsigned corner = 0; corner < (1u << DW) && inside; ++corner) {
-        double dot = 0;
+      double dot = 0;
 #pragma unroll
-        for (int k = 0; k < DW; ++k) {
-          const double c = ((corner >> k) & 1u) ? ws.hi[o * DW + k] : ws.lo[o * DW + k];
-          dot += d[k] * (c - y[k]);
-        }
-        if (dot < dd - tol) inside = false;
+      for (int k = 0; k < DW; ++k) {
+        const double tl = d[k] * (ws.lo[o * DW + k] - y[k]), th = d[k] * (ws.hi[o * DW + k] - y[k]);
+        dot += tl < th ? tl : th;
       }
+      const bool inside = !(dot < dd - tol);
       if (inside) {
         pruned[o >> 5] |= 1u << (o & 31);
         any = true;

@@ -407,7 +407,7 @@ __global__ void __launch_bounds__(128) k_regions_once(GraphArgs g, WorldD w, int
     } else {
       motion_state<DW>(m, j * g.dt, y, yd);
     }
-    n = convex_region<DW>(ws, y, yd, la, lb, lf);
+    n = convex_region<DW, 1>(ws, y, yd, la, lb, lf);
     if (n < 0) {
       atomicExch(err, 1);
       n = 0;

@@ -1,0 +1,70 @@
+"""The library's host-side geometry / steering helpers (the same
+__host__ __device__ code the kernels run) against the CPU oracle, bit for
+bit, on random worlds.  CPU only: these entry points need no GPU.
+
+Covers the exact-preserving rewrites inside that shared code: the single
+min-corner prune test of local_convex_region (geom.hpp:189-225), the span
+pruning and obstacle culling of motion_collides (geom.hpp:96-123), and the
+connect() scan + golden section (steer.hpp:111-182)."""
+import numpy as np
+import pytest
+
+from paper_1607_06886_b200 import api
+
+
+def _world(rng, dw, n_obs):
+    lo = np.zeros(dw)
+    hi = np.full(dw, 10.0)
+    c = rng.uniform(1.0, 9.0, size=(n_obs, dw))
+    h = rng.uniform(0.2, 1.5, size=(n_obs, dw))
+    return {"bounds_lo": lo, "bounds_hi": hi, "obs_lo": c - h, "obs_hi": c + h}
+
+
+@pytest.mark.parametrize("dw", [2, 3])
+def test_local_convex_region_matches_oracle(oracle_lib, dw):
+    rng = np.random.default_rng(11 + dw)
+    checked = 0
+    for trial in range(60):
+        ws = _world(rng, dw, int(rng.integers(1, 24)))
+        for _ in range(20):
+            y = rng.uniform(0.0, 10.0, size=dw)
+            if not oracle_lib.point_free(ws, y):
+                continue
+            yd = rng.normal(size=dw) * (0.0 if trial % 7 == 0 else 1.0)
+            try:
+                ea, eb, ef = oracle_lib.local_convex_region(ws, y, yd)
+            except Exception as e:  # the reference's runtime_error: the library must raise too
+                with pytest.raises(api.PumpError):
+                    api.local_convex_region(ws, y, yd)
+                continue
+            ga, gb, gf = api.local_convex_region(ws, y, yd)
+            assert ga.view(np.uint64).tolist() == ea.view(np.uint64).tolist()
+            assert gb.view(np.uint64).tolist() == eb.view(np.uint64).tolist()
+            assert gf.tolist() == ef.tolist()
+            checked += 1
+    assert checked > 300
+
+
+@pytest.mark.parametrize("dw", [2, 3])
+def test_connect_and_motion_collides_match_oracle(oracle_lib, dw):
+    rng = np.random.default_rng(5 + dw)
+    ws = _world(rng, dw, 12)
+    n_hit = n_free = 0
+    for _ in range(300):
+        ap, bp = rng.uniform(0.5, 9.5, size=(2, dw))
+        av, bv = rng.normal(size=(2, dw))
+        g = api.connect(ap, av, bp, bv, 5.0)
+        e = oracle_lib.connect(ap, av, bp, bv, 5.0)
+        assert g["ok"] == e["ok"]
+        assert np.float64(g["tau"]).tobytes() == np.float64(e["tau"]).tobytes()
+        assert np.float64(g["cost"]).tobytes() == np.float64(e["cost"]).tobytes()
+        assert api.steer_cost(ap, av, bp, bv, 0.7) == oracle_lib.steer_cost(ap, av, bp, bv, 0.7)
+        if not e["ok"]:
+            continue
+        for eps in (0.05, 0.5):
+            got = api.motion_collides(ws, ap, av, bp, bv, e["tau"], e["acc0"], e["jerk"], eps)
+            exp = oracle_lib.motion_collides(ws, ap, av, bp, bv, e["tau"], e["acc0"], e["jerk"], eps)
+            assert got == exp
+            n_hit += exp
+            n_free += not exp
+    assert n_hit > 20 and n_free > 20
