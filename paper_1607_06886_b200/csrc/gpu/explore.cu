@@ -411,14 +411,16 @@ __global__ void k_round_i(ExploreStatus* st, int64_t* d_pool_n, int64_t* limits)
 }
 
 __global__ void k_select(const int64_t* d_pool_n, const int64_t* limits, const int32_t* pool, const uint8_t* flags,
-                         const int32_t* bucket, int32_t* keys, uint8_t* stay) {
+                         const int32_t* bucket, int32_t* keys, uint8_t* stay, int64_t n_keys, ExploreStatus* st) {
   const int64_t x = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (x >= *d_pool_n) return;
   const int id = pool[x];
   const bool open = flags[id] & kOpen;
   const int b = bucket[id];
   const bool sel = open && b <= limits[0];
-  keys[x] = sel ? static_cast<int32_t>(b - limits[1]) : -1;
+  const int64_t key = b - limits[1];
+  if (sel && key >= n_keys) atomicExch(reinterpret_cast<unsigned long long*>(&st->err), 3ull);  // bound violated
+  keys[x] = sel ? static_cast<int32_t>(key) : -1;
   stay[x] = (open && !sel) ? 1 : 0;
 }
 
@@ -706,9 +708,17 @@ void run_explore_device(DevExplore& X, Ctx& c, const DevGraph& G, const ExploreA
     DBuf& keys = c.buf("x_sel_keys", al((pool_ub + 1) * 4));
     DBuf& stay = c.buf("x_sel_stay", al(pool_ub + 1));
     DBuf& stay_pos = c.buf("x_stay_pos", al((pool_ub + 2) * 8));
+    // Distinct selection keys this round: the group takes buckets in
+    // [min_bucket, min(i, max_bucket)].  Costs only grow along a plan, so the
+    // new min_bucket >= the previous one, and i = max(i_prev + 1, min_bucket):
+    // at most i_prev + 2 - min_bucket_prev keys (1 when i jumps to min_bucket).
+    // Within 512 the stable multisplit needs one radix pass instead of two;
+    // k_select flags a violated bound (never expected) as a device error.
+    int64_t n_keys = 1 << 18;
+    if (h.min_bucket != LLONG_MAX && h.i + 2 - h.min_bucket <= 512) n_keys = std::max<int64_t>(1, h.i + 2 - h.min_bucket);
     k_select<<<grid_for(pool_ub, 256), 256, 0, st>>>(d_pool_n, d_limits, pool_cur.as<int32_t>(),
                                                        X.flags.as<uint8_t>(), X.bucket.as<int32_t>(),
-                                                       keys.as<int32_t>(), stay.as<uint8_t>());
+                                                       keys.as<int32_t>(), stay.as<uint8_t>(), n_keys, S);
     ++c.launches;
     DBuf& stmp2 = c.buf("x_scan_tmp2", scan_temp_bytes(pool_ub + 16));
     exclusive_scan<uint8_t>(stay.as<uint8_t>(), stay_pos.as<int64_t>(), pool_ub, stmp2.p, st, &c.launches,
@@ -718,7 +728,7 @@ void run_explore_device(DevExplore& X, Ctx& c, const DevGraph& G, const ExploreA
     ++c.launches;
     X.group.ensure(al((pool_ub + 1) * 4));
     DBuf& mtmp = c.buf("x_ms_tmp", multisplit_temp_bytes(pool_ub, 1 << 18));
-    stable_multisplit(keys.as<int32_t>(), pool_cur.as<int32_t>(), pool_ub, 1 << 18, X.group.as<int32_t>(), d_G,
+    stable_multisplit(keys.as<int32_t>(), pool_cur.as<int32_t>(), pool_ub, static_cast<int>(n_keys), X.group.as<int32_t>(), d_G,
                       mtmp.p, st, &c.launches, d_pool_n);
     DBuf& deg = c.buf("x_deg", al((pool_ub + 1) * 4));
     X.task_off.ensure(al((pool_ub + 2) * 8));
