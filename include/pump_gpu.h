@@ -147,6 +147,9 @@ int pump_ctx_destroy(pump_ctx* ctx);
 double pump_ctx_last_kernel_ms(pump_ctx* ctx);
 /* Number of kernel launches issued by this ctx since creation. */
 int64_t pump_ctx_launch_count(pump_ctx* ctx);
+/* The context's CUDA stream (cudaStream_t) every call of this ctx is ordered
+ * on: callers time or order their own work against it. */
+int pump_ctx_stream(pump_ctx* ctx, void** stream_out);
 /* Measurement hooks (bench.py): per-kernel-family CUDA-event timing on the
  * launching stream; read returns total ms, launch counts and algorithmic work
  * units per family (PUMP_FAM_* order, PUMP_FAM_COUNT entries) and resets them. */

@@ -61,7 +61,7 @@ EXPORTS = [
     "pump_graph_counts", "pump_graph_export", "pump_graph_free", "pump_explore_run", "pump_explore_counts",
     "pump_explore_export", "pump_explore_free", "pump_run", "pump_result_summary_get", "pump_result_arrays",
     "pump_result_free", "pump_nccl_unique_id", "pump_ctx_set_comm", "pump_shard_range", "pump_ctx_profile",
-    "pump_ctx_profile_read", "pump_ctx_io_bytes", "pump_ctx_flush_l2", "pump_peak_fp64",
+    "pump_ctx_profile_read", "pump_ctx_io_bytes", "pump_ctx_flush_l2", "pump_peak_fp64", "pump_ctx_stream",
 ]
 
 

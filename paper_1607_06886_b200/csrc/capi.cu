@@ -95,6 +95,11 @@ int pump_ctx_destroy(pump_ctx* ctx) {
 
 double pump_ctx_last_kernel_ms(pump_ctx* ctx) { return ctx ? ctx->c.last_ms : 0.0; }
 int64_t pump_ctx_launch_count(pump_ctx* ctx) { return ctx ? ctx->c.launches : 0; }
+int pump_ctx_stream(pump_ctx* ctx, void** stream_out) {
+  if (!ctx || !stream_out) return PUMP_E_INVALID_ARGUMENT;
+  *stream_out = static_cast<void*>(ctx->c.stream);
+  return PUMP_OK;
+}
 
 // ------------------------------------------------------------- scenario
 int pump_scenario_parse(const char* json_text, pump_scenario** out) {
