@@ -616,6 +616,10 @@ void build_graph_device(DevGraph& G, Ctx& c, int n, int dw, const double* h_pos,
       c.sync();
       if (herr) throw std::runtime_error("local_convex_region: pruning loop failed to make progress");
       G.H = H;
+      if (H <= cap && std::getenv("PUMP_DEBUG_GRAPH"))
+        std::fprintf(stderr, "[pump graph] n=%d pairs=%lld survivors=%lld candidates=%lld edges=%lld waypoints=%lld "
+                     "halfspaces=%lld\n", n, (long long)n * (n - 1), (long long)G.n_connect, (long long)G.n_cand,
+                     (long long)G.E, (long long)NW, (long long)H);
       if (H <= cap) break;
       cap = H + H / 8;  // rerun with room to spare (per-waypoint content is deterministic)
     }
