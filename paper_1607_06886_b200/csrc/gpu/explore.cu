@@ -34,6 +34,7 @@ DevExplore::~DevExplore() {
 struct ExpandArgs {
   const int32_t* group;
   const int64_t* task_off;
+  const int32_t* task_grp;
   const int64_t* d_G;
   const int64_t* d_T;
   const int64_t* row_ptr;
@@ -68,15 +69,7 @@ __global__ void __launch_bounds__(256) k_expand(const ExpandArgs a) {
   const int lane = threadIdx.x & 31;
   const int64_t T = *a.d_T;
   if (task >= T) return;
-  const int64_t G = *a.d_G;
-  int64_t lo = 0, hi = G;  // largest g with task_off[g] <= task
-  while (hi - lo > 1) {
-    const int64_t mid = (lo + hi) >> 1;
-    if (a.task_off[mid] <= task)
-      lo = mid;
-    else
-      hi = mid;
-  }
+  const int64_t lo = a.task_grp[task];  // the group entry owning this task (k_task_map)
   const int pid = a.group[lo];
   const int hv = a.head[pid];
   const int64_t e = a.row_ptr[hv] + (task - a.task_off[lo]);
@@ -442,6 +435,15 @@ __global__ void k_group_post(const int64_t* d_G, const int32_t* group, const int
   atomicMin(&st->min_group_bits, __double_as_longlong(cost[id]));
 }
 
+// task -> group entry (warp per group), so k_expand starts without a search
+__global__ void k_task_map(const int64_t* d_G, const int64_t* task_off, int32_t* task_grp) {
+  const int64_t g = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (g >= *d_G) return;
+  const int64_t t1 = task_off[g + 1];
+  for (int64_t t = task_off[g] + lane; t < t1; t += 32) task_grp[t] = static_cast<int32_t>(g);
+}
+
 // group size, its task count (task_off[G]) and the compacted pool size
 __global__ void k_group_final(ExploreStatus* st, const int64_t* d_G, const int64_t* task_off,
                               const int64_t* stay_pos, const int64_t* d_pool_n, int64_t* d_T) {
@@ -623,7 +625,11 @@ void run_explore_device(DevExplore& X, Ctx& c, const DevGraph& G, const ExploreA
     DBuf& stmp = c.buf("x_scan_tmp", scan_temp_bytes(std::max<int64_t>({T, n, X.cap}) + 16));
 
     if (T > 0) {
-      ExpandArgs ea{X.group.as<int32_t>(), X.task_off.as<int64_t>(), d_G, d_T, G.row_ptr.as<int64_t>(),
+      X.task_grp.ensure(al((T + 1) * 4));
+      k_task_map<<<grid_for(h.G * 32, 256), 256, 0, st>>>(d_G, X.task_off.as<int64_t>(), X.task_grp.as<int32_t>());
+      ++c.launches;
+      ExpandArgs ea{X.group.as<int32_t>(), X.task_off.as<int64_t>(), X.task_grp.as<int32_t>(), d_G, d_T,
+                    G.row_ptr.as<int64_t>(),
                     G.e_to.as<int32_t>(), G.e_cost.as<double>(), G.e_nsteps.as<int32_t>(), G.wp_off.as<int64_t>(),
                     G.hs_off.as<int64_t>(), G.hs_cnt.as<int32_t>(), G.hs_a.as<double>(), G.hs_b.as<double>(),
                     X.head.as<int32_t>(),
