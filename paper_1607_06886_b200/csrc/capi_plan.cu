@@ -821,8 +821,12 @@ int pump_graph_upload(pump_ctx* ctx, const pump_graph_view* v, pump_graph** out)
       std::vector<int32_t> cnt(NW + 1, 0);
       for (int64_t w = 0; w < NW; ++w) cnt[w] = static_cast<int32_t>(v->wp_hs_off[w + 1] - v->wp_hs_off[w]);
       up(G.hs_cnt, cnt.data(), (NW + 1) * 4);
-      up(G.hs_a, v->hs_a, H * dw * 8);
-      up(G.hs_b, v->hs_b, H * 8);
+      std::vector<double> pk(static_cast<size_t>(H) * 4 + 4, 0.0);
+      for (int64_t h = 0; h < H; ++h) {
+        for (int k = 0; k < dw; ++k) pk[h * 4 + k] = v->hs_a[h * dw + k];
+        pk[h * 4 + 3] = v->hs_b[h];
+      }
+      up(G.hs_pk, pk.data(), H * 32);
       G.hs_fb.ensure(H + 256);
       if (v->hs_fallback) c.h2d(G.hs_fb.p, v->hs_fallback, H);
       std::vector<int32_t> from(E);
@@ -879,12 +883,11 @@ int pump_graph_export(const pump_graph* g, pump_graph_view* v) {
       const int64_t NW = G.NW, H = G.H;
       std::vector<int64_t> start(NW + 1);
       std::vector<int32_t> cnt(NW + 1);
-      std::vector<double> a(static_cast<size_t>(H) * dw + 1), b(H + 1);
+      std::vector<double> pk(static_cast<size_t>(H) * 4 + 4);
       std::vector<uint8_t> fb(H + 1);
       c.d2h(start.data(), G.hs_off.p, NW * 8);
       c.d2h(cnt.data(), G.hs_cnt.p, NW * 4);
-      c.d2h(a.data(), G.hs_a.p, H * dw * 8);
-      c.d2h(b.data(), G.hs_b.p, H * 8);
+      c.d2h(pk.data(), G.hs_pk.p, H * 32);
       c.d2h(fb.data(), G.hs_fb.p, H);
       c.sync();
       int64_t o = 0;
@@ -893,8 +896,8 @@ int pump_graph_export(const pump_graph* g, pump_graph_view* v) {
         for (int32_t h = 0; h < cnt[w]; ++h, ++o) {
           const int64_t src = start[w] + h;
           for (int k = 0; k < dw; ++k)
-            if (v->hs_a) v->hs_a[o * dw + k] = a[src * dw + k];
-          if (v->hs_b) v->hs_b[o] = b[src];
+            if (v->hs_a) v->hs_a[o * dw + k] = pk[src * 4 + k];
+          if (v->hs_b) v->hs_b[o] = pk[src * 4 + 3];
           if (v->hs_fallback) v->hs_fallback[o] = fb[src];
         }
         if (v->wp_hs_off) v->wp_hs_off[w + 1] = o;

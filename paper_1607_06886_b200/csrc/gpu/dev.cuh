@@ -573,7 +573,7 @@ __host__ __device__ __forceinline__ void coeffs_dev(const double* ap, const doub
 // pruned bitmap (1 word keeps it in a register for <= 32 boxes).
 template <int DW, int kWords = 128>
 __host__ __device__ inline int convex_region(const WorldD& ws, const double* y, const double* yd, double* a_out,
-                                             double* b_out, uint8_t* fb_out) {
+                                             double* b_out, uint8_t* fb_out, int a_stride = DW, int b_stride = 1) {
   uint32_t pruned[kWords];
   const int nw = (ws.n_obs + 31) / 32;
   for (int q = 0; q < nw; ++q) pruned[q] = 0u;
@@ -638,8 +638,8 @@ __host__ __device__ inline int convex_region(const WorldD& ws, const double* y, 
         for (int k = 0; k < DW; ++k) a[k] = d[k];
       }
 #pragma unroll
-      for (int k = 0; k < DW; ++k) a_out[count * DW + k] = a[k];
-      b_out[count] = sqnorm<DW>(a);
+      for (int k = 0; k < DW; ++k) a_out[count * a_stride + k] = a[k];
+      b_out[count * b_stride] = sqnorm<DW>(a);
       fb_out[count] = fb ? 1 : 0;
     }
     ++count;

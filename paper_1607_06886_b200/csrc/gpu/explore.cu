@@ -44,8 +44,7 @@ struct ExpandArgs {
   const int64_t* wp_off;
   const int64_t* hs_off;
   const int32_t* hs_cnt;
-  const double* hs_a;
-  const double* hs_b;
+  const double* hs_pk;  // H x 4 {a, (pad), b}
   const int32_t* head;
   const double* cost;
   const int32_t* t_end;
@@ -63,10 +62,47 @@ struct ExpandArgs {
   ExploreStatus* st;
 };
 
+// The particle test of one half-space (cp.hpp:197-201): s = 0 + a0 p0 + ...
+// evaluated without the leading "0 +" (it can only turn a -0 partial sum
+// into +0, and the verdict s > b is identical for both zeros).
 template <int DW, int CH>
-__global__ void __launch_bounds__(256) k_expand(const ExpandArgs a) {
+__device__ __forceinline__ void hs_test(const double2 q0, const double2 q1, const double (&p)[CH][DW],
+                                        bool (&kill)[CH]) {
+  const double av[3] = {q0.x, q0.y, q1.x};  // {a0, a1}, {a2 | pad, b}
+  const double b = q1.y;
+#pragma unroll
+  for (int c = 0; c < CH; ++c) {
+    double s = av[0] * p[c][0];
+#pragma unroll
+    for (int k = 1; k < DW; ++k) s += av[k] * p[c][k];
+    kill[c] = kill[c] || (s > b);
+  }
+}
+
+template <int DW, int CH>
+__device__ __forceinline__ void load_row(const double* row, int N, int lane, double (&p)[CH][DW]) {
+#pragma unroll
+  for (int c = 0; c < CH; ++c) {
+    const int i = c * 32 + lane;
+#pragma unroll
+    for (int k = 0; k < DW; ++k) p[c][k] = (i < N) ? row[i * DW + k] : 0.0;
+  }
+}
+
+constexpr int kExpBlock = 256;
+constexpr int kExpStage = 64;  // half-spaces staged per warp (2 KB of shared memory)
+
+// One warp per task (planner.hpp:140-176): the parent plan's particle mask is
+// extended along the edge's waypoints with their half-spaces.  For edges of
+// <= 32 waypoints whose half-spaces fit kExpStage, the warp first copies them
+// into shared memory (every lane its own waypoint's, all loads in flight at
+// once) and prefetches each next waypoint's bank row while testing the
+// current one, so the loop does not wait on a chain of global round trips.
+template <int DW, int CH>
+__global__ void __launch_bounds__(kExpBlock) k_expand(const ExpandArgs a) {
+  __shared__ double2 s_hs[kExpBlock / 32][kExpStage][2];
   const int64_t task = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int64_t T = *a.d_T;
   if (task >= T) return;
   const int64_t lo = a.task_grp[task];  // the group entry owning this task (k_task_map)
@@ -95,54 +131,65 @@ __global__ void __launch_bounds__(256) k_expand(const ExpandArgs a) {
 #pragma unroll
   for (int c = 0; c < CH; ++c) kill[c] = false;
   const int64_t w0 = a.wp_off[e];
+  const double2* hpk = reinterpret_cast<const double2*>(a.hs_pk);
   int64_t tests = 0;
-  // waypoint metadata of the first 32 waypoints in one parallel load, and
-  // their half-space lines prefetched into L1: the loop below then walks
-  // cached data instead of a chain of dependent DRAM round trips
+  // waypoint metadata of the first 32 waypoints in one parallel load
   int64_t my_h0 = 0;
   int my_cnt = 0;
   if (lane < ns) {
     my_h0 = a.hs_off[w0 + lane];
     my_cnt = a.hs_cnt[w0 + lane];
-    if (my_cnt > 0) {
-      asm volatile("prefetch.global.L1 [%0];" ::"l"(a.hs_a + my_h0 * DW));
-      asm volatile("prefetch.global.L1 [%0];" ::"l"(a.hs_b + my_h0));
-      if (my_cnt * DW > 16) asm volatile("prefetch.global.L1 [%0];" ::"l"(a.hs_a + my_h0 * DW + 16));
-    }
   }
-  for (int j = 0; j < ns; ++j) {
-    int64_t h0;
-    int cnt;
-    if (j < 32) {
-      h0 = __shfl_sync(0xffffffffu, my_h0, j);
-      cnt = __shfl_sync(0xffffffffu, my_cnt, j);
-    } else {
-      h0 = a.hs_off[w0 + j];
-      cnt = a.hs_cnt[w0 + j];
+  int incl = my_cnt;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += y;
+  }
+  const int total = __shfl_sync(0xffffffffu, incl, 31);
+  if (ns <= 32 && total <= kExpStage) {
+    const int my_pre = incl - my_cnt;
+    for (int q = 0; q < my_cnt; ++q) {
+      s_hs[wib][my_pre + q][0] = hpk[(my_h0 + q) * 2];
+      s_hs[wib][my_pre + q][1] = hpk[(my_h0 + q) * 2 + 1];
     }
-    const int64_t h1 = h0 + cnt;
-    tests += h1 - h0;
-    if (h0 == h1) continue;
-    const double* row = a.dy + static_cast<int64_t>(pt + j + 1) * a.N * DW;
-    double p[CH][DW];
+    __syncwarp();
+    tests = total;
+    unsigned live = __ballot_sync(0xffffffffu, my_cnt > 0);  // waypoints with half-spaces
+    double p[CH][DW], pn[CH][DW];
+    int j = live ? __ffs(live) - 1 : -1;
+    if (j >= 0) load_row<DW, CH>(a.dy + static_cast<int64_t>(pt + j + 1) * a.N * DW, a.N, lane, p);
+    while (j >= 0) {
+      live &= ~(1u << j);
+      const int jn = live ? __ffs(live) - 1 : -1;
+      if (jn >= 0) load_row<DW, CH>(a.dy + static_cast<int64_t>(pt + jn + 1) * a.N * DW, a.N, lane, pn);
+      const int cnt = __shfl_sync(0xffffffffu, my_cnt, j);
+      const int pre = __shfl_sync(0xffffffffu, incl, j) - cnt;
+      for (int h = 0; h < cnt; ++h) hs_test<DW, CH>(s_hs[wib][pre + h][0], s_hs[wib][pre + h][1], p, kill);
+      if (jn >= 0) {
 #pragma unroll
-    for (int c = 0; c < CH; ++c) {
-      const int i = c * 32 + lane;
+        for (int c = 0; c < CH; ++c)
 #pragma unroll
-      for (int k = 0; k < DW; ++k) p[c][k] = (i < a.N) ? row[i * DW + k] : 0.0;
-    }
-    for (int64_t h = h0; h < h1; ++h) {
-      double av[DW];
-#pragma unroll
-      for (int k = 0; k < DW; ++k) av[k] = a.hs_a[h * DW + k];
-      const double b = a.hs_b[h];
-#pragma unroll
-      for (int c = 0; c < CH; ++c) {
-        double s = 0;
-#pragma unroll
-        for (int k = 0; k < DW; ++k) s += av[k] * p[c][k];
-        kill[c] = kill[c] || (s > b);
+          for (int k = 0; k < DW; ++k) p[c][k] = pn[c][k];
       }
+      j = jn;
+    }
+  } else {
+    for (int j = 0; j < ns; ++j) {
+      int64_t h0;
+      int cnt;
+      if (j < 32) {
+        h0 = __shfl_sync(0xffffffffu, my_h0, j);
+        cnt = __shfl_sync(0xffffffffu, my_cnt, j);
+      } else {
+        h0 = a.hs_off[w0 + j];
+        cnt = a.hs_cnt[w0 + j];
+      }
+      tests += cnt;
+      if (cnt == 0) continue;
+      double p[CH][DW];
+      load_row<DW, CH>(a.dy + static_cast<int64_t>(pt + j + 1) * a.N * DW, a.N, lane, p);
+      for (int64_t h = h0; h < h0 + cnt; ++h) hs_test<DW, CH>(hpk[h * 2], hpk[h * 2 + 1], p, kill);
     }
   }
   if (lane == 0) atomicAdd(reinterpret_cast<unsigned long long*>(&a.st->hs_tests), static_cast<unsigned long long>(tests));
@@ -631,7 +678,7 @@ void run_explore_device(DevExplore& X, Ctx& c, const DevGraph& G, const ExploreA
       ExpandArgs ea{X.group.as<int32_t>(), X.task_off.as<int64_t>(), X.task_grp.as<int32_t>(), d_G, d_T,
                     G.row_ptr.as<int64_t>(),
                     G.e_to.as<int32_t>(), G.e_cost.as<double>(), G.e_nsteps.as<int32_t>(), G.wp_off.as<int64_t>(),
-                    G.hs_off.as<int64_t>(), G.hs_cnt.as<int32_t>(), G.hs_a.as<double>(), G.hs_b.as<double>(),
+                    G.hs_off.as<int64_t>(), G.hs_cnt.as<int32_t>(), G.hs_pk.as<double>(),
                     X.head.as<int32_t>(),
                     X.cost.as<double>(), X.t_end.as<int32_t>(), X.mask.as<uint64_t>(), c.bank.as<double>(), N,
                     c.bank_horizon, W, prm.alpha_max, X.cand_keep.as<uint8_t>(), X.cand_head.as<int32_t>(),

@@ -293,8 +293,7 @@ __global__ void __launch_bounds__(128) k_regions(GraphArgs g, WorldD w, int64_t 
                                                  const double* __restrict__ e_acc0, const double* __restrict__ e_jerk,
                                                  const int32_t* __restrict__ e_nsteps, int32_t* __restrict__ hcount,
                                                  const int64_t* __restrict__ hs_off, int32_t* __restrict__ hs_cnt,
-                                                 double* __restrict__ hs_a,
-                                                 double* __restrict__ hs_b, uint8_t* __restrict__ hs_fb,
+                                                 double* __restrict__ hs_pk, uint8_t* __restrict__ hs_fb,
                                                  int* __restrict__ err) {
   extern __shared__ double smem[];
   const WorldD ws = stage_world<DW>(w, smem);
@@ -334,10 +333,10 @@ __global__ void __launch_bounds__(128) k_regions(GraphArgs g, WorldD w, int64_t 
   } else {
     motion_state<DW>(m, j * g.dt, y, yd);
   }
-  double* ao = WRITE ? hs_a + hs_off[x] * DW : nullptr;
-  double* bo = WRITE ? hs_b + hs_off[x] : nullptr;
+  double* ao = WRITE ? hs_pk + hs_off[x] * 4 : nullptr;
+  double* bo = WRITE ? hs_pk + hs_off[x] * 4 + 3 : nullptr;
   uint8_t* fo = WRITE ? hs_fb + hs_off[x] : nullptr;
-  const int count = convex_region<DW>(ws, y, yd, ao, bo, fo);
+  const int count = convex_region<DW>(ws, y, yd, ao, bo, fo, 4, 4);
   if (count < 0) {
     atomicExch(err, 1);
     return;
@@ -363,8 +362,8 @@ __global__ void __launch_bounds__(128) k_regions_once(GraphArgs g, WorldD w, int
                                                       const int32_t* __restrict__ e_nsteps, int64_t cap,
                                                       unsigned long long* __restrict__ counter,
                                                       int64_t* __restrict__ hs_off, int32_t* __restrict__ hs_cnt,
-                                                      double* __restrict__ hs_a, double* __restrict__ hs_b,
-                                                      uint8_t* __restrict__ hs_fb, int* __restrict__ err) {
+                                                      double* __restrict__ hs_pk, uint8_t* __restrict__ hs_fb,
+                                                      int* __restrict__ err) {
   extern __shared__ double smem[];
   const WorldD ws = stage_world<DW>(w, smem);
   const int64_t x = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -431,8 +430,8 @@ __global__ void __launch_bounds__(128) k_regions_once(GraphArgs g, WorldD w, int
   if (start + n <= cap) {
     for (int h = 0; h < n; ++h) {
 #pragma unroll
-      for (int k = 0; k < DW; ++k) hs_a[(start + h) * DW + k] = la[h * DW + k];
-      hs_b[start + h] = lb[h];
+      for (int k = 0; k < DW; ++k) hs_pk[(start + h) * 4 + k] = la[h * DW + k];
+      hs_pk[(start + h) * 4 + 3] = lb[h];
       hs_fb[start + h] = lf[h];
     }
   }
@@ -590,8 +589,7 @@ void build_graph_device(DevGraph& G, Ctx& c, int n, int dw, const double* h_pos,
     DBuf& ctr = c.buf("g_hs_counter", 256);
     int64_t cap = std::max<int64_t>(G.hs_cap, NW * 4 + 16);
     for (int attempt = 0; attempt < 2; ++attempt) {
-      G.hs_a.ensure(al((cap + 1) * dw * 8));
-      G.hs_b.ensure(al((cap + 1) * 8));
+      G.hs_pk.ensure(al((cap + 1) * 32));
       G.hs_fb.ensure(al(cap + 1));
       G.hs_cap = cap;
       PUMP_CUDA(cudaMemsetAsync(ctr.p, 0, 8, st));
@@ -603,8 +601,8 @@ void build_graph_device(DevGraph& G, Ctx& c, int n, int dw, const double* h_pos,
           k_regions_once<DW><<<grid_for(NW, 128), 128, wsmem, st>>>(
               ga, wd, NW, E, G.wp_off.as<int64_t>(), G.e_from.as<int32_t>(), G.e_to.as<int32_t>(),
               G.e_tau.as<double>(), G.e_acc0.as<double>(), G.e_jerk.as<double>(), G.e_nsteps.as<int32_t>(), cap,
-              ctr.as<unsigned long long>(), G.hs_off.as<int64_t>(), G.hs_cnt.as<int32_t>(), G.hs_a.as<double>(),
-              G.hs_b.as<double>(), G.hs_fb.as<uint8_t>(), err.as<int>());
+              ctr.as<unsigned long long>(), G.hs_off.as<int64_t>(), G.hs_cnt.as<int32_t>(), G.hs_pk.as<double>(),
+              G.hs_fb.as<uint8_t>(), err.as<int>());
         });
         ++c.launches;
         PUMP_CUDA(cudaGetLastError());
@@ -637,7 +635,7 @@ void build_graph_device(DevGraph& G, Ctx& c, int n, int dw, const double* h_pos,
       k_regions<DW, false><<<grid_for(NW, 128), 128, wsmem, st>>>(
           ga, wd, NW, E, G.wp_off.as<int64_t>(), G.e_from.as<int32_t>(), G.e_to.as<int32_t>(), G.e_tau.as<double>(),
           G.e_acc0.as<double>(), G.e_jerk.as<double>(), G.e_nsteps.as<int32_t>(), hcnt.as<int32_t>(), nullptr,
-          nullptr, nullptr, nullptr, nullptr, err.as<int>());
+          nullptr, nullptr, nullptr, err.as<int>());
     });
     ++c.launches;
     PUMP_CUDA(cudaGetLastError());
@@ -651,8 +649,7 @@ void build_graph_device(DevGraph& G, Ctx& c, int n, int dw, const double* h_pos,
   c.sync();
   if (herr) throw std::runtime_error("local_convex_region: pruning loop failed to make progress");
   G.H = H;
-  G.hs_a.ensure(al((H + 1) * dw * 8));
-  G.hs_b.ensure(al((H + 1) * 8));
+  G.hs_pk.ensure(al((H + 1) * 32));
   G.hs_fb.ensure(al(H + 1));
   if (NW > 0) {
     KScope ks(st, F_REGIONS);
@@ -660,7 +657,7 @@ void build_graph_device(DevGraph& G, Ctx& c, int n, int dw, const double* h_pos,
       k_regions<DW, true><<<grid_for(NW, 128), 128, wsmem, st>>>(
           ga, wd, NW, E, G.wp_off.as<int64_t>(), G.e_from.as<int32_t>(), G.e_to.as<int32_t>(), G.e_tau.as<double>(),
           G.e_acc0.as<double>(), G.e_jerk.as<double>(), G.e_nsteps.as<int32_t>(), nullptr, G.hs_off.as<int64_t>(),
-          G.hs_cnt.as<int32_t>(), G.hs_a.as<double>(), G.hs_b.as<double>(), G.hs_fb.as<uint8_t>(), err.as<int>());
+          G.hs_cnt.as<int32_t>(), G.hs_pk.as<double>(), G.hs_fb.as<uint8_t>(), err.as<int>());
     });
     ++c.launches;
     PUMP_CUDA(cudaGetLastError());

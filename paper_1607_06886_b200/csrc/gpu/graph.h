@@ -14,9 +14,11 @@ struct DevGraph {
   DBuf e_from, e_to, e_cost, e_tau, e_acc0, e_jerk, e_nsteps;
   DBuf wp_off;                                            // E + 1 (int64)
   DBuf hs_off;                                            // NW (+1): first half-space of each waypoint
-  int64_t hs_cap = 0;                                     // half-space slots in hs_a/hs_b/hs_fb
+  int64_t hs_cap = 0;                                     // half-space slots in hs_pk/hs_fb
   DBuf hs_cnt;                                            // NW: half-spaces of each waypoint
-  DBuf hs_a, hs_b, hs_fb;                                 // H x dw, H, H
+  // half-spaces packed 32 B each {a_0 .. a_{dw-1}, (pad), b at [3]}: one
+  // pair of 16-byte loads per half-space in the explore expand kernel
+  DBuf hs_pk, hs_fb;                                      // H x 4 doubles, H
   std::vector<int32_t> goal_nodes;                        // host, ascending
   std::vector<double> h_pos, h_vel;                       // host copies of the nodes
 };
