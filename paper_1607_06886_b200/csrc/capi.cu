@@ -70,8 +70,11 @@ int pump_ctx_create(int device, pump_ctx** out) {
     auto* x = new pump_ctx;
     x->c.device = device;
     PUMP_CUDA(cudaStreamCreateWithFlags(&x->c.stream, cudaStreamNonBlocking));
+    PUMP_CUDA(cudaStreamCreateWithFlags(&x->c.side, cudaStreamNonBlocking));
     PUMP_CUDA(cudaEventCreate(&x->c.ev0));
     PUMP_CUDA(cudaEventCreate(&x->c.ev1));
+    PUMP_CUDA(cudaEventCreateWithFlags(&x->c.fork, cudaEventDisableTiming));
+    PUMP_CUDA(cudaEventCreateWithFlags(&x->c.join, cudaEventDisableTiming));
     *out = x;
   });
 }
@@ -88,6 +91,9 @@ int pump_ctx_destroy(pump_ctx* ctx) {
     ctx->c.bank.release();
     cudaEventDestroy(ctx->c.ev0);
     cudaEventDestroy(ctx->c.ev1);
+    cudaEventDestroy(ctx->c.fork);
+    cudaEventDestroy(ctx->c.join);
+    cudaStreamDestroy(ctx->c.side);
     cudaStreamDestroy(ctx->c.stream);
     delete ctx;
   });

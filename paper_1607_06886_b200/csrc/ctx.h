@@ -22,6 +22,10 @@ struct DevExplore;
 struct Ctx {
   int device = 0;
   cudaStream_t stream = nullptr;
+  // side stream for work independent of the main chain (the particle bank
+  // overlaps the graph build); fork/join events order it against `stream`
+  cudaStream_t side = nullptr;
+  cudaEvent_t fork = nullptr, join = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   int64_t launches = 0;
   double last_ms = 0;

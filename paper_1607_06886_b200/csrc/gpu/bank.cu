@@ -11,6 +11,8 @@
 //                   z <- ((F z) + u) + w, exactly the reference's rounding.
 // Noise is laid out component-major [t][r][i] so the recurrence's loads are
 // coalesced across particles.
+#include <cstdlib>
+
 #include "dispatch.cuh"
 
 namespace pumpg {
@@ -99,6 +101,74 @@ __global__ void __launch_bounds__(32) k_bank_rec(const LoopP<D, DW> L, int n, in
   for (int r = 0; r < 2 * D; ++r) zstate[static_cast<int64_t>(r) * n + i] = z[r];
 }
 
+// Axis-separable recurrence: one lane per (particle, axis), the 4x4 axis
+// block of F and the axis' 4 rows of the (dense, bit-identical) u and w the
+// noise kernel wrote.  Dropping F's structural zeros leaves every partial
+// sum unchanged (mc.cu, k_mc_sep); y_k = (0 + C_k0 z_k) + C_k1 z_{dw+k}.
+// The dense recurrence issues a 2d x 2d gemv per step from ~n/32 warps; this
+// one issues 16 products per lane from n * dw lanes.
+template <int DW>
+__global__ void __launch_bounds__(32) k_bank_rec_sep(const SepBlocks B, int n, int T, int t0, int tc, uint64_t seed,
+                                                     const double* __restrict__ uw, double* __restrict__ zstate,
+                                                     double* __restrict__ dy) {
+  constexpr int D = 2 * DW;
+  const int x = blockIdx.x * blockDim.x + threadIdx.x;
+  if (x >= n * DW) return;
+  const int i = x / DW, k = x - i * DW;
+  const double* F = B.F[k];
+  const int g[4] = {k, DW + k, D + k, D + DW + k};
+  double z[4];
+  if (t0 == 0) {
+    const uint64_t p0 = mix64(hash_seed_a(seed, static_cast<uint64_t>(i)) + 0ull);
+    const double n0 = normal_from_prefix(p0, static_cast<uint64_t>(k));       // kInitial + k
+    const double n1 = normal_from_prefix(p0, static_cast<uint64_t>(DW + k));  // kInitial + dw + k
+    z[0] = (0.0 + B.S0[k][0] * n0) + B.S0[k][1] * n1;
+    z[1] = (0.0 + B.S0[k][2] * n0) + B.S0[k][3] * n1;
+    z[2] = 0.0;
+    z[3] = 0.0;
+  } else {
+#pragma unroll
+    for (int r = 0; r < 4; ++r) z[r] = zstate[static_cast<int64_t>(x) * 4 + r];
+  }
+  double un[8];
+  if (tc > 0) {
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      un[r] = uw[static_cast<int64_t>(g[r]) * n + i];
+      un[4 + r] = uw[static_cast<int64_t>(D * 2 + g[r]) * n + i];
+    }
+  }
+  for (int tl = 0; tl <= tc; ++tl) {
+    const int t = t0 + tl;
+    if (tl == tc && t != T) break;  // next chunk stores y_t
+    dy[(static_cast<int64_t>(t) * n + i) * DW + k] = (0.0 + B.C[k][0] * z[0]) + B.C[k][1] * z[1];
+    if (t == T) break;
+    double uc[8];
+#pragma unroll
+    for (int r = 0; r < 8; ++r) uc[r] = un[r];
+    if (tl + 1 < tc) {
+      const double* u = uw + static_cast<int64_t>(tl + 1) * (4 * D) * n + i;
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        un[r] = u[static_cast<int64_t>(g[r]) * n];
+        un[4 + r] = u[static_cast<int64_t>(2 * D + g[r]) * n];
+      }
+    }
+    double zn[4];
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      double c = 0.0;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) c = c + F[r * 4 + q] * z[q];
+      zn[r] = (c + uc[r]) + uc[4 + r];
+    }
+#pragma unroll
+    for (int r = 0; r < 4; ++r) z[r] = zn[r];
+  }
+#pragma unroll
+  for (int r = 0; r < 4; ++r) zstate[static_cast<int64_t>(x) * 4 + r] = z[r];
+}
+
 size_t bank_scratch_bytes(const HostLoop& L, int n, int T) {
   (void)T;
   const int D = L.d;
@@ -109,6 +179,9 @@ void launch_bank(const HostLoop& HL, int n, int T, uint64_t seed, double* d_dy, 
                  int64_t* launches) {
   if (n < 1) throw std::invalid_argument("presample_bank: need at least one particle");
   if (T < 1) throw std::invalid_argument("presample_bank: horizon must be at least 1");
+  static const bool dense = std::getenv("PUMP_BANK_DENSE") != nullptr;
+  const bool sep = !dense && HL.dw >= 2 && HL.dw <= 3 && separable(HL);
+  const SepBlocks B = sep ? sep_blocks(HL) : SepBlocks{};
   dispatch_dims(HL.d, HL.dw, [&]<int D, int DW>() {
     const LoopP<D, DW> L = make_loop<D, DW>(HL);
     double* uw = static_cast<double*>(d_scratch);
@@ -124,7 +197,15 @@ void launch_bank(const HostLoop& HL, int n, int T, uint64_t seed, double* d_dy, 
       }
       {
         KScope ks(st, F_BANK_REC);
-        k_bank_rec<D, DW><<<grid_for(n, 32), 32, 0, st>>>(L, n, T, t0, tc, seed, uw, zs, d_dy);
+        if constexpr (D == 2 * DW) {
+          if (sep)
+            k_bank_rec_sep<DW><<<grid_for(static_cast<int64_t>(n) * DW, 32), 32, 0, st>>>(B, n, T, t0, tc, seed, uw,
+                                                                                         zs, d_dy);
+          else
+            k_bank_rec<D, DW><<<grid_for(n, 32), 32, 0, st>>>(L, n, T, t0, tc, seed, uw, zs, d_dy);
+        } else {
+          k_bank_rec<D, DW><<<grid_for(n, 32), 32, 0, st>>>(L, n, T, t0, tc, seed, uw, zs, d_dy);
+        }
         ++*launches;
         kprof_work(F_BANK_REC, static_cast<int64_t>(tc) * n);
       }

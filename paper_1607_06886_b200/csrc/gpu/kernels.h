@@ -177,6 +177,14 @@ void launch_hsmc_batch(int dw, int n, int horizon, const double* d_dy, int64_t n
 // --------------------------------------------------------------------- mc
 // Batched mc_certify (cp.hpp:214-268) over trajectories and the rollout
 // range [r0, r1); d_hits[j] += colliding rollouts of trajectory j.
+// Axis-separable closed loop (mc.cu): per axis k the 4 z entries
+// g(rho) = {k, dw+k, d+k, d+dw+k} couple only among themselves.
+struct SepBlocks {
+  double F[3][16], Gv[3][8], Gw[3][4], Sv[3][4], Sw[3], S0[3][4], C[3][2];
+};
+bool separable(const HostLoop& L);
+SepBlocks sep_blocks(const HostLoop& L);
+
 // Common-random-number table of the MC rollouts.  The deviation of rollout i
 // from ANY nominal trajectory, dy_t = C z_t, depends only on (closed loop,
 // seed, i, t): z_t is driven by the counter-hash noise alone.  The table

@@ -148,9 +148,6 @@ __global__ void __launch_bounds__(kMcBlock) k_mc(const LoopP<D, DW> L, WorldD w,
 // dynamics need no communication; y and the collision verdict are combined
 // with shuffles; obstacle culling and segment checks are split across the
 // rollout's lanes.
-struct SepBlocks {  // per axis k: row rho <-> z index g(rho) = {k, dw+k, d+k, d+dw+k}
-  double F[3][16], Gv[3][8], Gw[3][4], Sv[3][4], Sw[3], S0[3][4], C[3][2];
-};
 
 bool separable(const HostLoop& L) {
   const int d = L.d, dw = L.dw, nz = 2 * d;
