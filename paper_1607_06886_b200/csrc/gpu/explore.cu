@@ -265,14 +265,17 @@ __global__ void k_commit(const CommitArgs a) {
   if (slot == 0) a.touched[atomicAdd(reinterpret_cast<unsigned long long*>(&a.st->touched), 1ull)] = hv;
 }
 
-__global__ void k_after_commit(ExploreStatus* st, const int64_t* rank_total, int64_t* d_K) {
-  const int64_t K = *rank_total;
-  st->K = K;
-  *d_K = K;
-}
-
-__global__ void k_node_sizes(int n, const int32_t* mem_cnt, const int32_t* new_cnt, int32_t* sz) {
+// node sizes for the member relayout; thread 0 also publishes K = kept
+// candidates (rank[T]) and resets min_bucket for this round's k_pool_min
+__global__ void k_node_sizes(int n, const int32_t* mem_cnt, const int32_t* new_cnt, int32_t* sz, ExploreStatus* st,
+                             const int64_t* rank_total, int64_t* d_K) {
   const int v = blockIdx.x * blockDim.x + threadIdx.x;
+  if (v == 0) {
+    const int64_t K = *rank_total;
+    st->K = K;
+    *d_K = K;
+    st->min_bucket = LLONG_MAX;
+  }
   if (v < n) sz[v] = mem_cnt[v] + new_cnt[v];
 }
 
@@ -414,28 +417,29 @@ __global__ void k_pool_append(const int64_t* d_K, const ExploreStatus* st, const
   atomicMax(&stw->max_bucket, static_cast<long long>(bucket[id]));
 }
 
-// end of round bookkeeping (single thread); spos[K] = surviving newcomers
-__global__ void k_round_end(ExploreStatus* st, const int64_t* d_K, const int64_t* spos) {
-  const int64_t K = *d_K;
-  const int64_t ns = spos[K];
-  st->n_surv = ns;
-  st->pool_n += ns;
-  st->open_count += ns - st->evicted_open - st->G;
-  st->n_plans += K;
-  st->min_bucket = LLONG_MAX;
-}
-
-__global__ void k_pool_min(const ExploreStatus* st, const int32_t* pool, const uint8_t* flags, const int32_t* bucket,
-                           ExploreStatus* stw) {
+// lowest open bucket of the pool after this round's appends (spos[K] =
+// surviving newcomers appended behind the st->pool_n carried in)
+__global__ void k_pool_min(const ExploreStatus* st, const int64_t* d_K, const int64_t* spos, const int32_t* pool,
+                           const uint8_t* flags, const int32_t* bucket, ExploreStatus* stw) {
   const int64_t x = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (x >= st->pool_n) return;
+  if (x >= st->pool_n + spos[*d_K]) return;
   const int id = pool[x];
   if (flags[id] & kOpen) atomicMin(&stw->min_bucket, static_cast<long long>(bucket[id]));
 }
 
-// i <- max(i + 1, lowest open bucket): the reference's `continue` over empty
-// thresholds (planner.hpp:250-261) collapsed into one step.
-__global__ void k_round_i(ExploreStatus* st, int64_t* d_pool_n, int64_t* limits) {
+// End of round bookkeeping, then i <- max(i + 1, lowest open bucket): the
+// reference's `continue` over empty thresholds (planner.hpp:250-261)
+// collapsed into one step.  Single thread.
+__global__ void k_round_i(ExploreStatus* st, const int64_t* d_K, const int64_t* spos, int64_t* d_pool_n,
+                          int64_t* limits) {
+  {
+    const int64_t K = *d_K;
+    const int64_t ns = spos[K];
+    st->n_surv = ns;
+    st->pool_n += ns;
+    st->open_count += ns - st->evicted_open - st->G;
+    st->n_plans += K;
+  }
   long long i = st->i + 1;
   if (st->min_bucket != LLONG_MAX && st->min_bucket > i) i = st->min_bucket;
   st->i = i;
@@ -712,14 +716,12 @@ void run_explore_device(DevExplore& X, Ctx& c, const DevGraph& G, const ExploreA
       k_commit<<<grid_for(T, 256), 256, 0, st>>>(ca);
       ++c.launches;
     }
-    // K = total kept (rank[T]); rank lives at cand_rank[T] with T from host
-    k_after_commit<<<1, 1, 0, st>>>(S, X.cand_rank.as<int64_t>() + T, d_K);
-    ++c.launches;
-    // member relayout
+    // member relayout; K = total kept (rank[T], T from host) published on the way
     DBuf& old_ids = X.mem_flip ? X.mem_b : X.mem_a;
     DBuf& new_ids = X.mem_flip ? X.mem_a : X.mem_b;
-    k_node_sizes<<<grid_for(n, 256), 256, 0, st>>>(n, X.mem_cnt.as<int32_t>(), X.new_cnt.as<int32_t>(),
-                                                    node_sz.as<int32_t>());
+    k_node_sizes<<<grid_for(std::max(n, 1), 256), 256, 0, st>>>(n, X.mem_cnt.as<int32_t>(), X.new_cnt.as<int32_t>(),
+                                                                 node_sz.as<int32_t>(), S,
+                                                                 X.cand_rank.as<int64_t>() + T, d_K);
     exclusive_scan<int32_t>(node_sz.as<int32_t>(), off2.as<int64_t>(), n, stmp.p, st, &c.launches);
     k_relayout<<<grid_for(static_cast<int64_t>(n) * 32, 256), 256, 0, st>>>(
         n, X.mem_off.as<int64_t>(), X.mem_cnt.as<int32_t>(), old_ids.as<int32_t>(), off2.as<int64_t>(),
@@ -750,13 +752,11 @@ void run_explore_device(DevExplore& X, Ctx& c, const DevGraph& G, const ExploreA
                                                         pool_cur.as<int32_t>(), S);
       ++c.launches;
     }
-    k_round_end<<<1, 1, 0, st>>>(S, d_K, spos.as<int64_t>());
-    ++c.launches;
     // next group
     const int64_t pool_ub = h.pool_n + T + 1;
-    k_pool_min<<<grid_for(pool_ub, 256), 256, 0, st>>>(S, pool_cur.as<int32_t>(), X.flags.as<uint8_t>(),
-                                                         X.bucket.as<int32_t>(), S);
-    k_round_i<<<1, 1, 0, st>>>(S, d_pool_n, d_limits);
+    k_pool_min<<<grid_for(pool_ub, 256), 256, 0, st>>>(S, d_K, spos.as<int64_t>(), pool_cur.as<int32_t>(),
+                                                         X.flags.as<uint8_t>(), X.bucket.as<int32_t>(), S);
+    k_round_i<<<1, 1, 0, st>>>(S, d_K, spos.as<int64_t>(), d_pool_n, d_limits);
     c.launches += 2;
     DBuf& keys = c.buf("x_sel_keys", al((pool_ub + 1) * 4));
     DBuf& stay = c.buf("x_sel_stay", al(pool_ub + 1));

@@ -125,7 +125,8 @@ __global__ void __launch_bounds__(kScanBlock) k_scan_lookback(const InT* __restr
   __shared__ int64_t s_prefix;
   __shared__ unsigned s_tile;
   if (d_n) n = min(n, *d_n);
-  if (threadIdx.x == 0) s_tile = atomicAdd(ticket, 1u);
+  // one tile (ticket == nullptr): no predecessors, no status, no memset
+  if (threadIdx.x == 0) s_tile = ticket ? atomicAdd(ticket, 1u) : 0u;
   __syncthreads();
   const unsigned t = s_tile;
   const int64_t base = static_cast<int64_t>(t) * kScanTile;
@@ -155,7 +156,7 @@ __global__ void __launch_bounds__(kScanBlock) k_scan_lookback(const InT* __restr
     volatile uint64_t* vs = status;
     if (t == 0) {
       if (threadIdx.x == 0) {
-        vs[0] = kStInc | static_cast<uint64_t>(agg);
+        if (ticket) vs[0] = kStInc | static_cast<uint64_t>(agg);
         s_prefix = 0;
       }
     } else {
@@ -218,6 +219,9 @@ void exclusive_scan(const InT* d_in, int64_t* d_out, int64_t n, void* d_temp, cu
     k_scan_partials<<<1, 1024, 0, st>>>(partial, tiles, d_out, n, d_n);
     k_tile_scan<InT><<<static_cast<unsigned>(tiles), kScanBlock, 0, st>>>(d_in, n, partial, d_out, d_n);
     *launches += 3;
+  } else if (tiles == 1) {
+    k_scan_lookback<InT><<<1, kScanBlock, 0, st>>>(d_in, n, d_out, status, nullptr, d_n);
+    *launches += 1;
   } else {
     PUMP_CUDA(cudaMemsetAsync(d_temp, 0, 256 + static_cast<size_t>(tiles) * 8, st));
     k_scan_lookback<InT><<<static_cast<unsigned>(tiles), kScanBlock, 0, st>>>(d_in, n, d_out, status, ticket, d_n);
