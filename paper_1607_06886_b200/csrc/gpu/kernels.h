@@ -196,6 +196,7 @@ struct McTable {
   DBuf dy;  // [t][i][k], t < t_cap
   DBuf z;   // z_{t_done} per rollout
   DBuf flags;  // per (trajectory, rollout) hit flags of one certification
+  DBuf maxdev;  // [t][k]: max over rollouts of |dy| (bits of a non-negative double)
   int64_t r0 = 0, r1 = 0;
   int t_done = -1, t_cap = 0;
   uint64_t seed = 0;

@@ -592,8 +592,12 @@ template <int DW>
 __global__ void __launch_bounds__(kMcBlock) k_mc_tab(WorldD w, const int64_t* __restrict__ traj_off,
                                                      const double* __restrict__ ynom_all, int64_t r0, int64_t r1,
                                                      int64_t tab_r0, int64_t tab_n, const double* __restrict__ dy,
-                                                     double eps_cc, uint8_t* __restrict__ flags) {
+                                                     const unsigned long long* __restrict__ maxdev, double eps_cc,
+                                                     uint8_t* __restrict__ flags) {
   extern __shared__ double smem[];
+  __shared__ uint64_t s_cand[kMcChunk + 1];
+  __shared__ int s_skip[kMcChunk + 1];
+  __shared__ int s_all_skip;
   const int j = blockIdx.y;
   const int64_t p_begin = traj_off[j];
   const int n_pts = static_cast<int>(traj_off[j + 1] - p_begin);
@@ -619,27 +623,73 @@ __global__ void __launch_bounds__(kMcBlock) k_mc_tab(WorldD w, const int64_t* __
     s_clo[x] = lo;
     s_chi[x] = hi;
   }
+  if (threadIdx.x == 0) s_all_skip = 1;
   __syncthreads();
+  // Per step, the box every rollout's realized points (and the subdivision
+  // points between them) lie in: ynom -/+ the largest |dy| over the table's
+  // rollouts (fl is monotone, so fl(ynom +- maxdev) bounds fl(ynom + dy)),
+  // widened by the sub-segment rounding margin.  Steps whose box is inside
+  // the workspace and meets no (inflated) obstacle hold no failing test for
+  // any rollout: the block skips them, loads included.
+  if (threadIdx.x <= kMcChunk) {
+    const int r = threadIdx.x, t = s_lo_t + r;
+    int skip = 1;
+    uint64_t cand = 0;
+    if (t >= t_lo && t <= t_hi) {
+      double bl[DW], bh[DW];
+      bool inside = true;
+#pragma unroll
+      for (int k = 0; k < DW; ++k) {
+        const double m1 = __longlong_as_double(static_cast<long long>(maxdev[t * DW + k]));
+        double lo = s_y[r * DW + k] - m1, hi = s_y[r * DW + k] + m1;
+        if (t > 0) {
+          const double m0 = __longlong_as_double(static_cast<long long>(maxdev[(t - 1) * DW + k]));
+          const double lo0 = s_y[(r - 1) * DW + k] - m0, hi0 = s_y[(r - 1) * DW + k] + m0;
+          lo = lo0 < lo ? lo0 : lo;
+          hi = hi0 > hi ? hi0 : hi;
+        }
+        const double mg = 1e-12 * (1.0 + (lo < 0 ? -lo : lo) + (hi < 0 ? -hi : hi));
+        bl[k] = lo - mg;
+        bh[k] = hi + mg;
+        inside = inside && bl[k] > w.blo[k] && bh[k] < w.bhi[k];
+      }
+      for (int o = 0; o < w.n_obs && o < 64; ++o) {
+        bool sep = false;
+#pragma unroll
+        for (int k = 0; k < DW; ++k) sep = sep || (bh[k] < s_lo[o * DW + k]) || (bl[k] > s_hi[o * DW + k]);
+        if (!sep) cand |= 1ull << o;
+      }
+      skip = (inside && cand == 0 && w.n_obs <= 64) ? 1 : 0;
+    }
+    s_cand[r] = w.n_obs <= 64 ? cand : ~0ull;
+    s_skip[r] = skip;
+    if (!skip) s_all_skip = 0;
+  }
+  __syncthreads();
+  if (s_all_skip) return;
   const double e = eps_cc > 1e-12 ? eps_cc : 1e-12;  // std::max(eps_cc, 1e-12)
   const int64_t i = r0 + static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i >= r1) return;
   const double* d = dy + (i - tab_r0) * DW;
   const int64_t stride = tab_n * DW;
-  double dv[kMcChunk + 1][DW];  // issue every load of the chunk up front
+  double dv[kMcChunk + 1][DW];  // issue every needed load of the chunk up front
 #pragma unroll
-  for (int r = 0; r <= kMcChunk; ++r)
-    if (s_lo_t + r <= t_hi) {
+  for (int r = 0; r <= kMcChunk; ++r) {
+    const bool need = s_lo_t + r <= t_hi && (!s_skip[r] || (r < kMcChunk && !s_skip[r + 1]));
+    if (need) {
 #pragma unroll
       for (int k = 0; k < DW; ++k) dv[r][k] = d[static_cast<int64_t>(s_lo_t + r) * stride + k];
     }
-  double prev[DW];
-#pragma unroll
-  for (int k = 0; k < DW; ++k) prev[k] = s_y[k] + dv[0][k];
+  }
   bool hit = false;
 #pragma unroll
   for (int r = 0; r <= kMcChunk; ++r) {
     const int t = s_lo_t + r;
-    if (t < t_lo || t > t_hi || hit) continue;  // row 0 of a later chunk only seeds prev
+    if (t < t_lo || t > t_hi || hit || s_skip[r]) continue;  // row 0 of a later chunk only seeds prev
+    double prev[DW];
+    const int rp = t > 0 ? r - 1 : r;  // t = 0: the step's box is the point itself
+#pragma unroll
+    for (int k = 0; k < DW; ++k) prev[k] = s_y[rp * DW + k] + dv[rp][k];
     double y[DW];
 #pragma unroll
     for (int k = 0; k < DW; ++k) y[k] = s_y[r * DW + k] + dv[r][k];
@@ -656,8 +706,9 @@ __global__ void __launch_bounds__(kMcBlock) k_mc_tab(WorldD w, const int64_t* __
       bl[a] = prev[a] < y[a] ? prev[a] : y[a];
       bh[a] = prev[a] < y[a] ? y[a] : prev[a];
     }
-    uint64_t cand = 0;
-    for (int o = 0; o < w.n_obs && o < 64; ++o) {
+    uint64_t cand = 0;  // this rollout's culling, within the step's block-wide candidates
+    for (uint64_t m = s_cand[r] & (w.n_obs >= 64 ? ~0ull : ((1ull << w.n_obs) - 1)); m; m &= m - 1) {
+      const int o = __ffsll(static_cast<long long>(m)) - 1;
       bool sep = false;
 #pragma unroll
       for (int a = 0; a < DW; ++a) sep = sep || (bh[a] < s_lo[o * DW + a]) || (bl[a] > s_hi[o * DW + a]);
@@ -716,8 +767,6 @@ __global__ void __launch_bounds__(kMcBlock) k_mc_tab(WorldD w, const int64_t* __
         for (int a = 0; a < DW; ++a) p0[a] = p1[a];
       }
     }
-#pragma unroll
-    for (int a = 0; a < DW; ++a) prev[a] = y[a];
   }
   if (hit) flags[static_cast<int64_t>(j) * (r1 - r0) + (i - r0)] = 1;
 }
@@ -737,6 +786,36 @@ __global__ void __launch_bounds__(256) k_mc_count(const uint8_t* __restrict__ fl
   if ((threadIdx.x & 31) == 0 && c) atomicAdd(hits + j, static_cast<unsigned long long>(c));
   if (steps_out && blockIdx.x == 0 && threadIdx.x == 0)
     atomicAdd(steps_out, static_cast<unsigned long long>(n) * static_cast<unsigned long long>(traj_off[j + 1] - traj_off[j]));
+}
+
+// maxdev[t][k] = max_i |dy[t][i][k]| over the table's rollouts, as the bit
+// pattern of a non-negative double (ordered like the value) for atomicMax
+__global__ void __launch_bounds__(256) k_mctab_maxdev(const double* __restrict__ dy, int64_t n, int dw, int t_from,
+                                                      unsigned long long* __restrict__ maxdev) {
+  const int t = t_from + blockIdx.y;
+  __shared__ unsigned long long s_m[3];
+  if (threadIdx.x < 3) s_m[threadIdx.x] = 0ull;
+  __syncthreads();
+  unsigned long long m[3] = {0ull, 0ull, 0ull};
+  const double* row = dy + static_cast<int64_t>(t) * n * dw;
+  for (int64_t x = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; x < n * dw;
+       x += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const double v = row[x];
+    const unsigned long long b = static_cast<unsigned long long>(__double_as_longlong(v < 0 ? -v : v));
+    const int k = static_cast<int>(x % dw);
+    m[k] = b > m[k] ? b : m[k];
+  }
+  for (int k = 0; k < dw; ++k) {
+    unsigned long long v = m[k];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const unsigned long long y = __shfl_xor_sync(0xffffffffu, v, o);
+      v = y > v ? y : v;
+    }
+    if ((threadIdx.x & 31) == 0) atomicMax(&s_m[k], v);
+  }
+  __syncthreads();
+  if (threadIdx.x < dw) atomicMax(&maxdev[t * dw + threadIdx.x], s_m[threadIdx.x]);
 }
 
 static bool same_loop(const HostLoop& a, const HostLoop& b) {
@@ -787,7 +866,14 @@ static bool ensure_table(McTable& tab, const HostLoop& HL, int64_t r0, int64_t r
                                                                          tab.dy.as<double>(), tab.z.as<double>());
     });
   }
-  ++*launches;
+  // per-step max deviation of the new rows (the certification's skip test)
+  const size_t md_bytes = static_cast<size_t>(T + 1) * dw * 8;
+  if (md_bytes > tab.maxdev.cap) tab.maxdev.grow(md_bytes * 2, static_cast<size_t>(t_from) * dw * 8, st);
+  PUMP_CUDA(cudaMemsetAsync(tab.maxdev.as<char>() + static_cast<size_t>(t_from) * dw * 8, 0,
+                            static_cast<size_t>(T + 1 - t_from) * dw * 8, st));
+  k_mctab_maxdev<<<dim3(static_cast<unsigned>(std::min<int64_t>((n * dw + 255) / 256, 16)), T + 1 - t_from), 256, 0,
+                   st>>>(tab.dy.as<double>(), n, dw, t_from, tab.maxdev.as<unsigned long long>());
+  *launches += 2;
   PUMP_CUDA(cudaGetLastError());
   tab.t_done = T;
   return true;
@@ -818,7 +904,9 @@ void launch_mc(const HostLoop& HL, const DevWorld& w, int n_traj, const int64_t*
       dim3 grid(grid_for(n, kMcBlock), n_traj, (max_points + kMcChunk - 1) / kMcChunk);
       KScope ks(st, F_MC);
       k_mc_tab<DW><<<grid, kMcBlock, smem, st>>>(wd, d_traj_off, d_ynom, r0, r1, table->r0, table->r1 - table->r0,
-                                                 table->dy.as<double>(), eps_cc, table->flags.as<uint8_t>());
+                                                 table->dy.as<double>(),
+                                                 table->maxdev.as<unsigned long long>(), eps_cc,
+                                                 table->flags.as<uint8_t>());
       k_mc_count<<<dim3(static_cast<unsigned>(std::min<int64_t>((n + 255) / 256, 64)), n_traj), 256, 0, st>>>(
           table->flags.as<uint8_t>(), n, d_traj_off, d_hits, d_steps);
     });
