@@ -525,6 +525,98 @@ __global__ void __launch_bounds__(kMcBlock) k_mctab_sep(const SepBlocks B, int64
   for (int r = 0; r < 4; ++r) zs[r] = z[r];
 }
 
+// Build in two phases for the axis-separable loop (the default path): the
+// noise of every (transition t-1 -> t, rollout, axis) is a pure function of
+// the key, so k_mcnoise_sep draws all of it in parallel (3 normals and the
+// Sv / Sw products per item, the operations k_mc_sep performs), and
+// k_mcrec_sep then runs only the short per-axis recurrence, reading the noise
+// kMcPf steps at a time.  Same operations in the same order as k_mctab_sep.
+template <int DW>
+__global__ void __launch_bounds__(256) k_mcnoise_sep(const SepBlocks B, int64_t r0, int64_t n, uint64_t seed, int tn0,
+                                                     int steps, double* __restrict__ nz) {
+  const int64_t x = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (x >= static_cast<int64_t>(steps) * n * DW) return;
+  const int64_t tt = x / (n * DW);
+  const int64_t rem = x - tt * n * DW;
+  const int64_t li = rem / DW;
+  const int k = static_cast<int>(rem - li * DW);
+  const int t = tn0 + static_cast<int>(tt);
+  const uint64_t sa = hash_seed_a(seed, static_cast<uint64_t>(r0 + li));
+  const uint64_t pt = mix64(sa + static_cast<uint64_t>(t - 1));
+  const uint64_t pt1 = mix64(sa + static_cast<uint64_t>(t));
+  const uint64_t ch0 = static_cast<uint64_t>(k), ch1 = static_cast<uint64_t>(DW + k);
+  const double nv0 = normal_from_prefix(pt, kProcess + ch0);
+  const double nv1 = normal_from_prefix(pt, kProcess + ch1);
+  const double nw = normal_from_prefix(pt1, kMeasurement + static_cast<uint64_t>(k));
+  const double* Sv = B.Sv[k];
+  double* o = nz + x * 3;
+  o[0] = (0.0 + Sv[0] * nv0) + Sv[1] * nv1;
+  o[1] = (0.0 + Sv[2] * nv0) + Sv[3] * nv1;
+  o[2] = 0.0 + B.Sw[k] * nw;
+}
+
+constexpr int kMcPf = 8;
+template <int DW>
+__global__ void __launch_bounds__(128) k_mcrec_sep(const SepBlocks B, int64_t r0, int64_t n, uint64_t seed,
+                                                   int t_from, int t_to, int tn0, const double* __restrict__ nz,
+                                                   double* __restrict__ dy, double* __restrict__ zst) {
+  const int64_t x = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (x >= n * DW) return;
+  const int64_t li = x / DW;
+  const int k = static_cast<int>(x - li * DW);
+  const double* F = B.F[k];
+  const double* Gv = B.Gv[k];
+  const double* Gw = B.Gw[k];
+  const double* C = B.C[k];
+  double z[4];
+  double* zs = zst + x * 4;
+  if (t_from == 0) {
+    const uint64_t pt = mix64(hash_seed_a(seed, static_cast<uint64_t>(r0 + li)) + 0ull);
+    const double n0 = normal_from_prefix(pt, static_cast<uint64_t>(k));
+    const double n1 = normal_from_prefix(pt, static_cast<uint64_t>(DW + k));  // kInitial channels
+    z[0] = (0.0 + B.S0[k][0] * n0) + B.S0[k][1] * n1;
+    z[1] = (0.0 + B.S0[k][2] * n0) + B.S0[k][3] * n1;
+    z[2] = 0.0;
+    z[3] = 0.0;
+    dy[x] = (0.0 + C[0] * z[0]) + C[1] * z[1];  // t = 0
+  } else {
+#pragma unroll
+    for (int r = 0; r < 4; ++r) z[r] = zs[r];
+  }
+  const int64_t stride = n * DW * 3;
+  for (int tb = tn0; tb <= t_to; tb += kMcPf) {
+    double q[kMcPf][3];
+#pragma unroll
+    for (int u = 0; u < kMcPf; ++u)
+      if (tb + u <= t_to) {
+        const double* src = nz + static_cast<int64_t>(tb + u - tn0) * stride + x * 3;
+        q[u][0] = src[0];
+        q[u][1] = src[1];
+        q[u][2] = src[2];
+      }
+#pragma unroll
+    for (int u = 0; u < kMcPf; ++u) {
+      const int t = tb + u;
+      if (t > t_to) break;
+      double zn[4];
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        const double uu = (0.0 + Gv[2 * r] * q[u][0]) + Gv[2 * r + 1] * q[u][1];
+        const double wv = 0.0 + Gw[r] * q[u][2];
+        double c = 0.0;
+#pragma unroll
+        for (int y = 0; y < 4; ++y) c = c + F[r * 4 + y] * z[y];
+        zn[r] = (c + uu) + wv;
+      }
+#pragma unroll
+      for (int r = 0; r < 4; ++r) z[r] = zn[r];
+      dy[static_cast<int64_t>(t) * n * DW + x] = (0.0 + C[0] * z[0]) + C[1] * z[1];
+    }
+  }
+#pragma unroll
+  for (int r = 0; r < 4; ++r) zs[r] = z[r];
+}
+
 // Build, general loop: one thread per rollout, the k_mc recursion.
 template <int D, int DW>
 __global__ void __launch_bounds__(kMcBlock) k_mctab_dense(const LoopP<D, DW> L, int64_t r0, int64_t n, uint64_t seed,
@@ -852,7 +944,22 @@ static bool ensure_table(McTable& tab, const HostLoop& HL, int64_t r0, int64_t r
     tab.dy.grow(bytes, static_cast<size_t>(t_from) * row, st);
   }
   KScope ks(st, F_MC_TABLE);
-  if (tab.sep) {
+  static const bool fused = std::getenv("PUMP_MCTAB_FUSED") != nullptr;
+  if (tab.sep && !fused) {
+    const SepBlocks B = sep_blocks(HL);
+    const int tn0 = std::max(1, t_from);
+    const int steps = T - tn0 + 1;
+    if (steps > 0) tab.nz.ensure(static_cast<size_t>(steps) * n * dw * 3 * 8 + 256);
+    dispatch_dw(dw, [&]<int DW>() {
+      if (steps > 0) {
+        const int64_t items = static_cast<int64_t>(steps) * n * DW;
+        k_mcnoise_sep<DW><<<grid_for(items, 256), 256, 0, st>>>(B, r0, n, seed, tn0, steps, tab.nz.as<double>());
+        ++*launches;
+      }
+      k_mcrec_sep<DW><<<grid_for(n * DW, 128), 128, 0, st>>>(B, r0, n, seed, t_from, T, tn0, tab.nz.as<double>(),
+                                                            tab.dy.as<double>(), tab.z.as<double>());
+    });
+  } else if (tab.sep) {
     const SepBlocks B = sep_blocks(HL);
     dispatch_dw(dw, [&]<int DW>() {
       constexpr int per_block = (kMcBlock / 32) * groups_per_warp<DW>();
