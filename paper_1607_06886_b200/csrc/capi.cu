@@ -69,8 +69,13 @@ int pump_ctx_create(int device, pump_ctx** out) {
     PUMP_CUDA(cudaSetDevice(device));
     auto* x = new pump_ctx;
     x->c.device = device;
-    PUMP_CUDA(cudaStreamCreateWithFlags(&x->c.stream, cudaStreamNonBlocking));
-    PUMP_CUDA(cudaStreamCreateWithFlags(&x->c.side, cudaStreamNonBlocking));
+    // the main chain runs at the highest priority, the side stream (bank, MC
+    // table) at the lowest: its blocks fill idle SMs without delaying the
+    // latency-critical main-chain kernels queued behind them
+    int prio_low = 0, prio_high = 0;
+    PUMP_CUDA(cudaDeviceGetStreamPriorityRange(&prio_low, &prio_high));
+    PUMP_CUDA(cudaStreamCreateWithPriority(&x->c.stream, cudaStreamNonBlocking, prio_high));
+    PUMP_CUDA(cudaStreamCreateWithPriority(&x->c.side, cudaStreamNonBlocking, prio_low));
     PUMP_CUDA(cudaEventCreate(&x->c.ev0));
     PUMP_CUDA(cudaEventCreate(&x->c.ev1));
     PUMP_CUDA(cudaEventCreateWithFlags(&x->c.fork, cudaEventDisableTiming));

@@ -203,7 +203,8 @@ __global__ void k_paths(int n_sel, const int32_t* sel, const int32_t* head, cons
 
 __global__ void k_gather_members(int n_goal, const int32_t* goal_nodes, const int64_t* mem_off,
                                  const int64_t* out_off, const int32_t* ids, const double* cost, const double* cp,
-                                 int32_t* out_ids, double* out_cost, double* out_cp) {
+                                 const int32_t* t_end, int32_t* out_ids, double* out_cost, double* out_cp,
+                                 int32_t* out_tend) {
   const int g = blockIdx.x;
   if (g >= n_goal) return;
   const int v = goal_nodes[g];
@@ -213,63 +214,111 @@ __global__ void k_gather_members(int n_goal, const int32_t* goal_nodes, const in
     out_ids[o + k] = id;
     out_cost[o + k] = cost[id];
     out_cp[o + k] = cp[id];
+    out_tend[o + k] = t_end[id];
   }
 }
 
 struct PathSet {
   std::vector<std::vector<int>> nodes;
   std::vector<std::vector<int64_t>> edges;
+  // per path edge: tau, acc0[dw], jerk[dw] (gathered on the device, one copy)
+  std::vector<std::vector<double>> motion;
 };
+
+// compact the resolved paths (k_paths' fixed-stride slots) and gather each
+// path edge's motion coefficients next to it
+__global__ void k_path_compact(int ns, int max_len, int dw, const int32_t* __restrict__ nodes,
+                               const int64_t* __restrict__ edges, const int64_t* __restrict__ off,
+                               const double* __restrict__ e_tau, const double* __restrict__ e_acc0,
+                               const double* __restrict__ e_jerk, int32_t* __restrict__ c_nodes,
+                               int64_t* __restrict__ c_edges, double* __restrict__ c_motion) {
+  const int s = blockIdx.x;
+  if (s >= ns) return;
+  const int64_t o = off[s], len = off[s + 1] - off[s];
+  for (int64_t j = threadIdx.x; j < len; j += blockDim.x) {
+    c_nodes[o + j] = nodes[static_cast<int64_t>(s) * max_len + j];
+    if (j + 1 < len) {
+      const int64_t e = edges[static_cast<int64_t>(s) * max_len + j];
+      c_edges[o + j] = e;
+      double* m = c_motion + (o + j) * (1 + 2 * dw);
+      if (e >= 0) {
+        m[0] = e_tau[e];
+        for (int k = 0; k < dw; ++k) {
+          m[1 + k] = e_acc0[e * dw + k];
+          m[1 + dw + k] = e_jerk[e * dw + k];
+        }
+      }
+    }
+  }
+}
 
 static PathSet resolve_paths(Ctx& c, const DevGraph& G, const DevExplore& X, const std::vector<int>& sel) {
   PathSet ps;
   const int ns = static_cast<int>(sel.size());
   if (ns == 0) return ps;
+  const int dw = G.dw;
   const int max_len = 4096;
   DBuf& d_sel = c.buf("p_sel", ns * 4 + 256);
   DBuf& d_nodes = c.buf("p_nodes", static_cast<size_t>(ns) * max_len * 4 + 256);
   DBuf& d_edges = c.buf("p_edges", static_cast<size_t>(ns) * max_len * 8 + 256);
   DBuf& d_lens = c.buf("p_lens", ns * 4 + 256);
   c.h2d(d_sel.p, sel.data(), ns * 4);
-  const DBuf& ids_src = X.head;
-  (void)ids_src;
   k_paths<<<(ns + 127) / 128, 128, 0, c.stream>>>(ns, d_sel.as<int32_t>(), X.head.as<int32_t>(),
                                                   X.parent.as<int32_t>(), G.row_ptr.as<int64_t>(), G.e_to.as<int32_t>(),
                                                   max_len, d_nodes.as<int32_t>(), d_edges.as<int64_t>(),
                                                   d_lens.as<int32_t>());
   ++c.launches;
   PUMP_CUDA(cudaGetLastError());
-  std::vector<int32_t> lens(ns), nodes(static_cast<size_t>(ns) * max_len);
-  std::vector<int64_t> edges(static_cast<size_t>(ns) * max_len);
+  std::vector<int32_t> lens(ns);
   c.d2h(lens.data(), d_lens.p, ns * 4);
-  c.d2h(nodes.data(), d_nodes.p, nodes.size() * 4);
-  c.d2h(edges.data(), d_edges.p, edges.size() * 8);
   c.sync();
-  for (int s = 0; s < ns; ++s) {
-    ps.nodes.emplace_back(nodes.begin() + static_cast<int64_t>(s) * max_len,
-                          nodes.begin() + static_cast<int64_t>(s) * max_len + lens[s]);
-    ps.edges.emplace_back(edges.begin() + static_cast<int64_t>(s) * max_len,
-                          edges.begin() + static_cast<int64_t>(s) * max_len + std::max(0, lens[s] - 1));
+  std::vector<int64_t> off(ns + 1, 0);
+  for (int q = 0; q < ns; ++q) off[q + 1] = off[q] + lens[q];
+  const int64_t total = off[ns];
+  const int mw = 1 + 2 * dw;
+  DBuf& d_off = c.buf("p_off", (ns + 1) * 8 + 256);
+  DBuf& c_nodes = c.buf("p_cnodes", total * 4 + 256);
+  DBuf& c_edges = c.buf("p_cedges", total * 8 + 256);
+  DBuf& c_motion = c.buf("p_cmotion", total * mw * 8 + 256);
+  c.h2d(d_off.p, off.data(), (ns + 1) * 8);
+  k_path_compact<<<ns, 128, 0, c.stream>>>(ns, max_len, dw, d_nodes.as<int32_t>(), d_edges.as<int64_t>(),
+                                           d_off.as<int64_t>(), G.e_tau.as<double>(), G.e_acc0.as<double>(),
+                                           G.e_jerk.as<double>(), c_nodes.as<int32_t>(), c_edges.as<int64_t>(),
+                                           c_motion.as<double>());
+  ++c.launches;
+  PUMP_CUDA(cudaGetLastError());
+  std::vector<int32_t> nodes(total);
+  std::vector<int64_t> edges(total);
+  std::vector<double> motion(static_cast<size_t>(total) * mw);
+  c.d2h(nodes.data(), c_nodes.p, total * 4);
+  c.d2h(edges.data(), c_edges.p, total * 8);
+  c.d2h(motion.data(), c_motion.p, total * mw * 8);
+  c.sync();
+  for (int q = 0; q < ns; ++q) {
+    ps.nodes.emplace_back(nodes.begin() + off[q], nodes.begin() + off[q + 1]);
+    const int64_t ne = std::max<int64_t>(0, lens[q] - 1);
+    ps.edges.emplace_back(edges.begin() + off[q], edges.begin() + off[q] + ne);
+    ps.motion.emplace_back(motion.begin() + off[q] * mw, motion.begin() + (off[q] + ne) * mw);
   }
   return ps;
 }
 
-// path_trajectory (planner.hpp:292-315) from device edge data
-static std::vector<HWp> path_trajectory(Ctx& c, const DevGraph& G, const std::vector<int>& path,
-                                        const std::vector<int64_t>& edges) {
+// path_trajectory (planner.hpp:292-315) from the gathered edge data
+static std::vector<HWp> path_trajectory(const DevGraph& G, const std::vector<int>& path,
+                                        const std::vector<int64_t>& edges, const std::vector<double>& motion) {
   const int dw = G.dw;
+  const int mw = 1 + 2 * dw;
   std::vector<HWp> traj;
   double offset = 0;
   for (size_t j = 0; j + 1 < path.size(); ++j) {
     const int64_t e = edges[j];
     if (e < 0) throw std::logic_error("path_trajectory: missing edge");
     HMotion m{};
-    double tau;
-    c.d2h(&tau, G.e_tau.as<double>() + e, 8);
-    c.d2h(m.a, G.e_acc0.as<double>() + e * dw, dw * 8);
-    c.d2h(m.j, G.e_jerk.as<double>() + e * dw, dw * 8);
-    c.sync();
-    m.tau = tau;
+    m.tau = motion[j * mw];
+    for (int k = 0; k < dw; ++k) {
+      m.a[k] = motion[j * mw + 1 + k];
+      m.j[k] = motion[j * mw + 1 + dw + k];
+    }
     const int v = path[j], u = path[j + 1];
     for (int k = 0; k < dw; ++k) {
       m.p0[k] = G.h_pos[v * dw + k];
@@ -322,6 +371,10 @@ static std::vector<double> mc_values(Ctx& c, const HostLoop& L, const DevWorld& 
   // ranks are summed over NVLink (bit-identical for any world size)
   int64_t r0 = 0, r1 = n_mc;
   shard_range(n_mc, c.rank, c.world, &r0, &r1);
+  if (c.mc_join_pending) {
+    PUMP_CUDA(cudaStreamWaitEvent(c.stream, c.join, 0));
+    c.mc_join_pending = false;
+  }
   c.tic();
   launch_mc(L, w, nt, d_off.as<int64_t>(), d_y.as<double>(), max_pts, r0, r1, seed, eps_cc,
             d_h.as<unsigned long long>(), c.stream, &c.launches, d_h.as<unsigned long long>() + nt, &c.mc_table);
@@ -524,6 +577,10 @@ static void run_pump_device(Ctx& c, const pumpb::Scenario& s, const DevGraph* pr
   ExploreArgs ea{s.alpha / eta, std::min(1.0, eta * s.alpha), s.lambda, r_n};
   run_explore_device(X, c, *graph, ea);
   auto t2 = clk::now();
+  static const bool dbg_t = std::getenv("PUMP_DEBUG_TIMING") != nullptr;
+  auto mark = [&](const char* what) {
+    if (dbg_t) std::fprintf(stderr, "[pump t] %-24s %8.3f ms\n", what, 1e3 * secs(t2, clk::now()));
+  };
   R.s.explore_seconds = secs(t1, t2);
   R.s.explore_kernel_ms = X.kernel_ms;
   R.s.partial_plans = X.partial_plans;
@@ -531,7 +588,7 @@ static void run_pump_device(Ctx& c, const pumpb::Scenario& s, const DevGraph* pr
   R.s.n_plans = X.n_plans;
 
   // goal plans = concat over goal nodes (ascending) of pareto[v] (planner.hpp:264-265)
-  std::vector<int32_t> gids;
+  std::vector<int32_t> gids, gtend;
   std::vector<double> gcost, gcp;
   {
     const int ng = static_cast<int>(graph->goal_nodes.size());
@@ -547,17 +604,20 @@ static void run_pump_device(Ctx& c, const pumpb::Scenario& s, const DevGraph* pr
       DBuf& d_id = c.buf("r_gid", total * 4 + 256);
       DBuf& d_c = c.buf("r_gc", total * 8 + 256);
       DBuf& d_p = c.buf("r_gp", total * 8 + 256);
+      DBuf& d_t = c.buf("r_gt", total * 4 + 256);
       c.h2d(d_gn.p, graph->goal_nodes.data(), ng * 4);
       c.h2d(d_go.p, goff.data(), (ng + 1) * 8);
       const DBuf& ids = X.mem_flip ? X.mem_b : X.mem_a;
       k_gather_members<<<ng, 128, 0, c.stream>>>(ng, d_gn.as<int32_t>(), X.mem_off.as<int64_t>(),
                                                  d_go.as<int64_t>(), ids.as<int32_t>(), X.cost.as<double>(),
-                                                 X.cp.as<double>(), d_id.as<int32_t>(), d_c.as<double>(),
-                                                 d_p.as<double>());
+                                                 X.cp.as<double>(), X.t_end.as<int32_t>(), d_id.as<int32_t>(),
+                                                 d_c.as<double>(), d_p.as<double>(), d_t.as<int32_t>());
       ++c.launches;
       gids.resize(total);
       gcost.resize(total);
       gcp.resize(total);
+      gtend.resize(total);
+      c.d2h(gtend.data(), d_t.p, total * 4);
       c.d2h(gids.data(), d_id.p, total * 4);
       c.d2h(gcost.data(), d_c.p, total * 8);
       c.d2h(gcp.data(), d_p.p, total * 8);
@@ -589,9 +649,28 @@ static void run_pump_device(Ctx& c, const pumpb::Scenario& s, const DevGraph* pr
   // Alg. 4 bisection (pump.hpp:23-51): every front plan is certified in one
   // batched MC launch (speculatively), then the bisection is replayed from
   // the memo so mc_evaluations lists exactly the probes the reference makes.
+  // The certifications below all read the common-random-number MC table up
+  // to the longest front trajectory (t_end + 1 waypoints; smoothing keeps the
+  // length): build it on the side stream now, under the host work of
+  // resolving the paths and their waypoints.
+  if (!front.empty()) {
+    int t_max = 0;
+    for (int k : front) t_max = std::max(t_max, static_cast<int>(gtend[k]));
+    int64_t r0 = 0, r1 = s.mc_samples;
+    shard_range(s.mc_samples, c.rank, c.world, &r0, &r1);
+    PUMP_CUDA(cudaEventRecord(c.fork, c.stream));
+    PUMP_CUDA(cudaStreamWaitEvent(c.side, c.fork, 0));
+    mc_table_prepare(c.mc_table, L, r0, r1, s.seeds.mc, t_max, c.side, &c.launches);
+    PUMP_CUDA(cudaEventRecord(c.join, c.side));
+    c.mc_join_pending = true;  // the first certification waits for it (mc_values)
+  }
+  mark("front");
   PathSet ps = resolve_paths(c, *graph, X, sorted_ids);
+  mark("resolve_paths");
   std::vector<std::vector<HWp>> trajs;
-  for (size_t k = 0; k < sorted_ids.size(); ++k) trajs.push_back(path_trajectory(c, *graph, ps.nodes[k], ps.edges[k]));
+  for (size_t k = 0; k < sorted_ids.size(); ++k)
+    trajs.push_back(path_trajectory(*graph, ps.nodes[k], ps.edges[k], ps.motion[k]));
+  mark("path_trajectory");
   std::vector<double> memo = trajs.empty() ? std::vector<double>{}
                                            : mc_values(c, L, dwld, trajs, s.mc_samples, s.seeds.mc, eps_cc,
                                                        &R.s.mc_ms, &R.s.mc_rollouts);
@@ -626,6 +705,7 @@ static void run_pump_device(Ctx& c, const pumpb::Scenario& s, const DevGraph* pr
     R.s.success = 0;
     return;
   }
+  mark("front mc");
   const int sel_id = sorted_ids[sel];
   R.path.assign(ps.nodes[sel].begin(), ps.nodes[sel].end());
   {
@@ -758,6 +838,7 @@ static void run_pump_device(Ctx& c, const pumpb::Scenario& s, const DevGraph* pr
       }
     }
   }
+  mark("smoothing");
   R.traj = best;
   R.s.cost = best_cost;
   R.s.certified_cp = best_mc;

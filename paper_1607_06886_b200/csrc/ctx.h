@@ -26,6 +26,7 @@ struct Ctx {
   // overlaps the graph build); fork/join events order it against `stream`
   cudaStream_t side = nullptr;
   cudaEvent_t fork = nullptr, join = nullptr;
+  bool mc_join_pending = false;  // the MC table was built on `side`: wait before certifying
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   int64_t launches = 0;
   double last_ms = 0;

@@ -986,6 +986,14 @@ static bool ensure_table(McTable& tab, const HostLoop& HL, int64_t r0, int64_t r
   return true;
 }
 
+void mc_table_prepare(McTable& tab, const HostLoop& HL, int64_t r0, int64_t r1, uint64_t seed, int T,
+                      cudaStream_t st, int64_t* launches) {
+  if (r1 <= r0 || T < 0) return;
+  static const bool direct = std::getenv("PUMP_MC_DIRECT") != nullptr;
+  if (direct) return;
+  ensure_table(tab, HL, r0, r1, seed, T, st, launches);
+}
+
 void launch_mc(const HostLoop& HL, const DevWorld& w, int n_traj, const int64_t* d_traj_off, const double* d_ynom,
                int max_points, int64_t r0, int64_t r1, uint64_t seed, double eps_cc, unsigned long long* d_hits,
                cudaStream_t st, int64_t* launches, unsigned long long* d_steps, McTable* table) {
