@@ -302,12 +302,21 @@ __global__ void k_place_new(const int64_t* d_K, const ExploreStatus* st, const i
 // RemoveDominated, both directions, for one touched node per CTA.
 // Segment layout on entry: [old members (ascending ids) | newcomers (any
 // order)].  On exit: [old survivors | surviving newcomers by id].
+// RemoveDominated at one touched node per CTA (planner.hpp:200-238).  The
+// node's members (ids, cost, cp) are first staged in shared memory with one
+// batch of independent loads, so the O(m_new * m) dominance scans read shared
+// memory instead of chasing ids through global memory; nodes with more than
+// kDomCap members take the same steps on global memory.
+constexpr int kDomCap = 1024;
 __global__ void __launch_bounds__(128) k_dom(const ExploreStatus* st, const int32_t* touched,
                                              const int64_t* new_off, int32_t* mem_cnt, int32_t* new_cnt,
                                              int32_t* ids, const double* cost, const double* cp, uint8_t* flags,
                                              uint8_t* drop, uint8_t* surv, int32_t* fpos, ExploreStatus* stw) {
   const int64_t P0 = st->n_plans;
   __shared__ int s_old_surv, s_new_surv, s_drop, s_evict, s_evict_open;
+  __shared__ int32_t s_id[kDomCap];
+  __shared__ double s_c[kDomCap], s_p[kDomCap];
+  __shared__ uint8_t s_dr[kDomCap];
   constexpr int kMaxLocal = 64;
   for (int64_t b = blockIdx.x; b < st->touched; b += gridDim.x) {
     const int v = touched[b];
@@ -315,6 +324,7 @@ __global__ void __launch_bounds__(128) k_dom(const ExploreStatus* st, const int3
     const int m_old = mem_cnt[v];
     const int m_new = new_cnt[v];
     const int m = m_old + m_new;
+    const bool staged = m <= kDomCap;
     if (threadIdx.x == 0) {
       s_old_surv = 0;
       s_new_surv = 0;
@@ -322,34 +332,43 @@ __global__ void __launch_bounds__(128) k_dom(const ExploreStatus* st, const int3
       s_evict = 0;
       s_evict_open = 0;
     }
+    if (staged) {
+      for (int x = threadIdx.x; x < m; x += blockDim.x) {
+        const int id = ids[base + x];
+        s_id[x] = id;
+        s_c[x] = cost[id];
+        s_p[x] = cp[id];
+      }
+    }
     __syncthreads();
+    auto ID = [&](int x) { return staged ? s_id[x] : ids[base + x]; };
+    auto CO = [&](int x) { return staged ? s_c[x] : cost[ids[base + x]]; };
+    auto CP = [&](int x) { return staged ? s_p[x] : cp[ids[base + x]]; };
     // (1) drop newcomers dominated by any member of the pre-removal set,
     //     old or new (planner.hpp:200-211); dominates(o, q) = q.cost > o.cost
     //     && q.cp >= o.cp (planner.hpp:58-60)
     for (int qi = threadIdx.x; qi < m_new; qi += blockDim.x) {
-      const int q = ids[base + m_old + qi];
-      const double qc = cost[q], qp = cp[q];
+      const int q = ID(m_old + qi);
+      const double qc = CO(m_old + qi), qp = CP(m_old + qi);
       bool d = false;
-      for (int x = 0; x < m && !d; ++x) {
-        const int o = ids[base + x];
-        d = (qc > cost[o]) && (qp >= cp[o]);
-      }
+      for (int x = 0; x < m && !d; ++x) d = (qc > CO(x)) && (qp >= CP(x));
       drop[q - P0] = d ? 1 : 0;
       surv[q - P0] = d ? 0 : 1;
+      if (staged) s_dr[m_old + qi] = d ? 1 : 0;
       if (d) atomicAdd(&s_drop, 1);
     }
     __syncthreads();
+    auto DROPPED = [&](int qi) { return staged ? s_dr[m_old + qi] != 0 : drop[ids[base + m_old + qi] - P0] != 0; };
     // (2) evict old members other than the root that a surviving newcomer
     //     dominates (planner.hpp:219-238); evicted slots become -1 - id
     for (int pi = threadIdx.x; pi < m_old; pi += blockDim.x) {
-      const int p = ids[base + pi];
+      const int p = ID(pi);
       if (p == 0) continue;
-      const double pc = cost[p], pp = cp[p];
+      const double pc = CO(pi), pp = CP(pi);
       bool ev = false;
       for (int qi = 0; qi < m_new && !ev; ++qi) {
-        const int q = ids[base + m_old + qi];
-        if (drop[q - P0]) continue;
-        ev = (pc > cost[q]) && (pp >= cp[q]);
+        if (DROPPED(qi)) continue;
+        ev = (pc > CO(m_old + qi)) && (pp >= CP(m_old + qi));
       }
       if (ev) {
         atomicAdd(&s_evict, 1);
@@ -357,42 +376,53 @@ __global__ void __launch_bounds__(128) k_dom(const ExploreStatus* st, const int3
           flags[p] &= static_cast<uint8_t>(~kOpen);
           atomicAdd(&s_evict_open, 1);
         }
-        ids[base + pi] = -1 - p;
+        if (staged)
+          s_id[pi] = -1 - p;
+        else
+          ids[base + pi] = -1 - p;
       }
     }
     __syncthreads();
     // (3) rank surviving newcomers by id; compact old survivors in order
     for (int qi = threadIdx.x; qi < m_new; qi += blockDim.x) {
-      const int q = ids[base + m_old + qi];
-      if (drop[q - P0]) continue;
+      if (DROPPED(qi)) continue;
+      const int q = ID(m_old + qi);
       int r = 0;
-      for (int xi = 0; xi < m_new; ++xi) {
-        const int x = ids[base + m_old + xi];
-        r += (!drop[x - P0] && x < q) ? 1 : 0;
-      }
+      for (int xi = 0; xi < m_new; ++xi) r += (!DROPPED(xi) && ID(m_old + xi) < q) ? 1 : 0;
       fpos[q - P0] = r;
       atomicAdd(&s_new_surv, 1);
     }
     if (threadIdx.x == 0) {
       int w = 0;
       for (int pi = 0; pi < m_old; ++pi) {
-        const int p = ids[base + pi];
+        const int p = ID(pi);
         if (p >= 0) ids[base + w++] = p;
       }
       s_old_surv = w;
     }
-    // (4) gather surviving newcomers before overwriting their slots
-    int my_q[kMaxLocal];
-    int my_n = 0;
-    for (int qi = threadIdx.x; qi < m_new; qi += blockDim.x) {
-      const int q = ids[base + m_old + qi];
-      if (!drop[q - P0] && my_n < kMaxLocal) my_q[my_n++] = q;
-    }
-    __syncthreads();
-    if (m_new > kMaxLocal * static_cast<int>(blockDim.x)) {
-      if (threadIdx.x == 0) atomicExch(reinterpret_cast<unsigned long long*>(&stw->err), 2ull);
+    if (staged) {
+      __syncthreads();
+      // (4) surviving newcomers after the old survivors, in id order (their
+      //     ids are still in shared memory)
+      for (int qi = threadIdx.x; qi < m_new; qi += blockDim.x) {
+        if (DROPPED(qi)) continue;
+        const int q = s_id[m_old + qi];
+        ids[base + s_old_surv + fpos[q - P0]] = q;
+      }
     } else {
-      for (int k = 0; k < my_n; ++k) ids[base + s_old_surv + fpos[my_q[k] - P0]] = my_q[k];
+      // (4) gather surviving newcomers before overwriting their slots
+      int my_q[kMaxLocal];
+      int my_n = 0;
+      for (int qi = threadIdx.x; qi < m_new; qi += blockDim.x) {
+        const int q = ids[base + m_old + qi];
+        if (!drop[q - P0] && my_n < kMaxLocal) my_q[my_n++] = q;
+      }
+      __syncthreads();
+      if (m_new > kMaxLocal * static_cast<int>(blockDim.x)) {
+        if (threadIdx.x == 0) atomicExch(reinterpret_cast<unsigned long long*>(&stw->err), 2ull);
+      } else {
+        for (int k = 0; k < my_n; ++k) ids[base + s_old_surv + fpos[my_q[k] - P0]] = my_q[k];
+      }
     }
     __syncthreads();
     if (threadIdx.x == 0) {
