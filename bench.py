@@ -272,6 +272,26 @@ def main():
     e2e_ms = max_over_ranks(sum(e_ms) / len(e_ms), world)
     assert r2["path"].tolist() == res["path"].tolist() and r2["certified_cp"] == res["certified_cp"]
 
+    # ---- the same solve with a prebuilt graph (run_pump's `prebuilt`,
+    # pump.hpp:170-171; SURVEY §8d asks for both): the graph is built once from
+    # the scenario's own node set outside the timed solves
+    prm = sc.params()
+    pos, vel = sc.nodes()
+    g_pre = api.build_graph(pos, vel, sc.workspace(), sc.goal(), prm["r_n"], prm["dt"], prm["eps_cc"],
+                            prm["tau_max"], ctx=ctx)
+    for _ in range(2):
+        api.run_pump(sc, prebuilt=g_pre, ctx=ctx)
+    p_evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    for k in range(args.steps):
+        L.pump_ctx_flush_l2(ctx.h)
+        p_evs[k][0].record(lib_stream)
+        r3 = api.run_pump(sc, prebuilt=g_pre, ctx=ctx)
+        p_evs[k][1].record(lib_stream)
+    torch.cuda.synchronize()
+    pre_ms = max_over_ranks(sum(a.elapsed_time(b) for a, b in p_evs) / args.steps, world)
+    assert r3["path"].tolist() == res["path"].tolist() and r3["certified_cp"] == res["certified_cp"]
+    del g_pre
+
     # ---- roofline of the dominant kernel family (CUDA events, profiled pass)
     fam = int(np.argmax(prof_ms))
     fam_name = FAMILIES[fam]
@@ -330,6 +350,8 @@ def main():
         "e2e": {"value": round(e2e_ms, 3), "unit": "ms",
                 "h2d_bytes_per_step": int((e_io1[0] - e_io0[0]) // args.steps),
                 "d2h_bytes_per_step": int((e_io1[1] - e_io0[1]) // args.steps)},
+        "prebuilt_graph": {"value": round(pre_ms, 3), "unit": "ms",
+                           "note": "run_pump with a prebuilt graph (graph built once from the scenario's nodes)"},
         "gpu_launches": int(launches // args.steps), "gpu_launches_total": int(launches),
         "device_allocs_timed": int(io1[3] - io0[3] + e_io1[3] - e_io0[3]),
         "clocks": clk, "roofline": roof, "cpu_baseline": cpu, "kernels": kernels,

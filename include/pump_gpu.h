@@ -214,6 +214,11 @@ int pump_scenario_closed_loop(const pump_scenario* s, int32_t* d, int32_t* dw, d
                               double* Sv, double* Sw, double* S0, double* C);
 /* JSON-scenario scalars: eps_cc, r_n, tau_max, alpha, eta, lambda, dt. */
 int pump_scenario_params(const pump_scenario* s, double out[8], int64_t iout[8]);
+/* The node set run_pump plans over (pump.hpp:184-189): x_init, then the
+ * accepted Halton states (sample.hpp:56-89), then the appended goal sample if
+ * any.  Writes n_out; fills pos/vel (n x dw, row-major) when both are given
+ * (PUMP_E_OUT_OF_RANGE if n > cap).  Host only. */
+int pump_scenario_nodes(const pump_scenario* s, int32_t cap, double* pos, double* vel, int32_t* n_out);
 
 /* ---------------------------------------------------- particle bank (K_bank) */
 /* presample_bank (lti.hpp:257-292).  The bank stays resident in the ctx;

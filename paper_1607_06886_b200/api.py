@@ -62,6 +62,7 @@ EXPORTS = [
     "pump_explore_export", "pump_explore_free", "pump_run", "pump_result_summary_get", "pump_result_arrays",
     "pump_result_free", "pump_nccl_unique_id", "pump_ctx_set_comm", "pump_shard_range", "pump_ctx_profile",
     "pump_ctx_profile_read", "pump_ctx_io_bytes", "pump_ctx_flush_l2", "pump_peak_fp64", "pump_ctx_stream",
+    "pump_scenario_nodes",
 ]
 
 
@@ -213,6 +214,23 @@ class Scenario:
         out = dict(zip(keys_f, f.tolist()))
         out.update(dict(zip(keys_i, [int(x) for x in i])))
         return out
+
+    def nodes(self):
+        """(pos, vel), n x dw each: the node set run_pump plans over."""
+        L = lib()
+        L.pump_scenario_nodes.argtypes = [C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p]
+        n = C.c_int32()
+        _check(L.pump_scenario_nodes(self.h, 0, None, None, C.byref(n)))
+        dw = self.params()["dw"]
+        pos, vel = np.zeros((n.value, dw)), np.zeros((n.value, dw))
+        _check(L.pump_scenario_nodes(self.h, n.value, _p(pos), _p(vel), C.byref(n)))
+        return pos, vel
+
+    def goal(self) -> dict:
+        j = _json.loads(self.text)
+        g = j["goal"]
+        return {"lo": np.array(g["lo"], float), "hi": np.array(g["hi"], float),
+                "max_speed": float(g.get("max_speed", 0.0))}  # scenario.hpp default
 
     def workspace(self) -> dict:
         j = _json.loads(self.text)

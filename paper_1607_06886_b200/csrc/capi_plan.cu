@@ -875,6 +875,23 @@ int pump_build_graph(pump_ctx* ctx, int32_t n_nodes, int32_t dw, const double* p
   });
 }
 
+int pump_scenario_nodes(const pump_scenario* s, int32_t cap, double* pos, double* vel, int32_t* n_out) {
+  return guard([&] {
+    if (!s || !n_out) throw std::invalid_argument("scenario_nodes: null argument");
+    HostWorld hw = host_world(s->s.workspace);
+    std::vector<double> p, v;
+    sample_nodes(s->s, hw, p, v);
+    const int dw = s->s.workspace_dim();
+    const int n = static_cast<int>(p.size()) / dw;
+    *n_out = n;
+    if (pos && vel) {
+      if (n > cap) throw std::out_of_range("scenario_nodes: capacity " + std::to_string(cap) + " < " + std::to_string(n));
+      std::copy(p.begin(), p.end(), pos);
+      std::copy(v.begin(), v.end(), vel);
+    }
+  });
+}
+
 int pump_graph_upload(pump_ctx* ctx, const pump_graph_view* v, pump_graph** out) {
   return guard([&] {
     Ctx& c = ctx->c;

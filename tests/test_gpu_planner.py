@@ -203,3 +203,24 @@ def test_run_pump_matches_oracle(oracle_lib, gpu_ctx, name, samples, mc):
     got = api.run_pump(api.parse_scenario(txt), ctx=gpu_ctx)
     ref = oracle_lib.run_pump(txt, workers=WORKERS)
     assert_run_equal(got, ref)
+
+
+@pytest.mark.parametrize("name,samples", [("three_obstacle", None), ("quad3d_three_obstacle", 600)])
+def test_run_pump_prebuilt_graph(oracle_lib, gpu_ctx, name, samples):
+    """run_pump(s, workers, prebuilt) (pump.hpp:170-171): a graph built from
+    the scenario's own node set gives the solve without prebuilt, bit for bit."""
+    from paper_1607_06886_b200 import api
+
+    txt = with_samples(name, samples, mc_samples=3000)
+    sc = api.parse_scenario(txt)
+    pos, vel = sc.nodes()
+    p = sc.params()
+    g = api.build_graph(pos, vel, sc.workspace(), sc.goal(), p["r_n"], p["dt"], p["eps_cc"], p["tau_max"],
+                        ctx=gpu_ctx)
+    a = api.run_pump(sc, prebuilt=g, ctx=gpu_ctx)
+    b = api.run_pump(sc, ctx=gpu_ctx)
+    assert a["path"].tolist() == b["path"].tolist()
+    assert a["cost"] == b["cost"] and a["certified_cp"] == b["certified_cp"]
+    assert a["partial_plans"] == b["partial_plans"] and a["n_edges"] == b["n_edges"]
+    ref = oracle_lib.run_pump(txt, workers=WORKERS)
+    assert_run_equal(a, ref)

@@ -68,3 +68,15 @@ def test_connect_and_motion_collides_match_oracle(oracle_lib, dw):
             n_hit += exp
             n_free += not exp
     assert n_hit > 20 and n_free > 20
+
+
+@pytest.mark.parametrize("name", ["minimal", "three_obstacle", "quad3d_three_obstacle"])
+def test_scenario_nodes_match_oracle(oracle_lib, name):
+    """The node set run_pump plans over (pump.hpp:184-189, sample.hpp:56-89)."""
+    from conftest import scenario_text
+
+    txt = scenario_text(name)
+    pos, vel = api.parse_scenario(txt).nodes()
+    epos, evel = oracle_lib.scenario_nodes(txt)
+    assert pos.view(np.uint64).tolist() == np.asarray(epos).view(np.uint64).tolist()
+    assert vel.view(np.uint64).tolist() == np.asarray(evel).view(np.uint64).tolist()
