@@ -174,6 +174,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="quad3d_indoor")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-mc-sweep", action="store_true")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 0)
     world, rank, local = dist_setup()
@@ -292,6 +293,35 @@ def main():
     assert r3["path"].tolist() == res["path"].tolist() and r3["certified_cp"] == res["certified_cp"]
     del g_pre
 
+    # ---- MC certification sweep: mc_certify of the
+    # certified trajectory with n_mc in {1e4 .. 1e7}, rollouts sharded over
+    # the ranks ([n r / W, n (r+1) / W)), hit counts summed across ranks
+    sweep = []
+    if not args.no_mc_sweep:
+        cl, wsd = sc.closed_loop(), sc.workspace()
+        traj = np.ascontiguousarray(res["traj_pos"])
+        for n_mc in (10 ** 4, 10 ** 5, 10 ** 6, 10 ** 7):
+            lo, hi = api.shard_range(n_mc, rank, world)
+            api.mc_certify_batch(cl, wsd, [traj], lo, min(hi, lo + 256), prm["seed_mc"], prm["eps_cc"], ctx)
+            barrier(world)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            torch.cuda.synchronize()
+            e0.record(lib_stream)
+            hits = api.mc_certify_batch(cl, wsd, [traj], lo, hi, prm["seed_mc"], prm["eps_cc"], ctx)
+            e1.record(lib_stream)
+            torch.cuda.synchronize()
+            ms = max_over_ranks(e0.elapsed_time(e1), world)
+            total = int(hits[0])
+            if world > 1:
+                import torch.distributed as dist
+
+                t = torch.tensor([total], dtype=torch.int64, device="cuda")
+                dist.all_reduce(t)
+                total = int(t.item())
+            sweep.append({"n_mc": n_mc, "ms": round(ms, 3), "rollouts_per_s": round(n_mc / (ms * 1e-3), 1),
+                          "rollout_steps_per_s": round(n_mc * len(traj) / (ms * 1e-3), 1),
+                          "cp": total / n_mc})
+
     # ---- roofline of the dominant kernel family (CUDA events, profiled pass)
     fam = int(np.argmax(prof_ms))
     fam_name = FAMILIES[fam]
@@ -350,6 +380,7 @@ def main():
         "e2e": {"value": round(e2e_ms, 3), "unit": "ms",
                 "h2d_bytes_per_step": int((e_io1[0] - e_io0[0]) // args.steps),
                 "d2h_bytes_per_step": int((e_io1[1] - e_io0[1]) // args.steps)},
+        "mc_sweep": sweep,
         "prebuilt_graph": {"value": round(pre_ms, 3), "unit": "ms",
                            "note": "run_pump with a prebuilt graph (graph built once from the scenario's nodes)"},
         "gpu_launches": int(launches // args.steps), "gpu_launches_total": int(launches),

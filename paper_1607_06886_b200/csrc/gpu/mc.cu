@@ -946,19 +946,25 @@ static bool ensure_table(McTable& tab, const HostLoop& HL, int64_t r0, int64_t r
   KScope ks(st, F_MC_TABLE);
   static const bool fused = std::getenv("PUMP_MCTAB_FUSED") != nullptr;
   if (tab.sep && !fused) {
+    // time slices of kTabSlice steps bound the noise scratch (n x slice x 3 x dw doubles)
+    constexpr int kTabSlice = 64;
     const SepBlocks B = sep_blocks(HL);
-    const int tn0 = std::max(1, t_from);
-    const int steps = T - tn0 + 1;
-    if (steps > 0) tab.nz.ensure(static_cast<size_t>(steps) * n * dw * 3 * 8 + 256);
-    dispatch_dw(dw, [&]<int DW>() {
-      if (steps > 0) {
-        const int64_t items = static_cast<int64_t>(steps) * n * DW;
-        k_mcnoise_sep<DW><<<grid_for(items, 256), 256, 0, st>>>(B, r0, n, seed, tn0, steps, tab.nz.as<double>());
-        ++*launches;
-      }
-      k_mcrec_sep<DW><<<grid_for(n * DW, 128), 128, 0, st>>>(B, r0, n, seed, t_from, T, tn0, tab.nz.as<double>(),
-                                                            tab.dy.as<double>(), tab.z.as<double>());
-    });
+    tab.nz.ensure(static_cast<size_t>(kTabSlice) * n * dw * 3 * 8 + 256);
+    for (int tc0 = t_from; tc0 <= T; tc0 += kTabSlice) {
+      const int tc1 = std::min(T, tc0 + kTabSlice - 1);
+      const int tn0 = std::max(1, tc0);
+      const int steps = tc1 - tn0 + 1;
+      dispatch_dw(dw, [&]<int DW>() {
+        if (steps > 0) {
+          const int64_t items = static_cast<int64_t>(steps) * n * DW;
+          k_mcnoise_sep<DW><<<grid_for(items, 256), 256, 0, st>>>(B, r0, n, seed, tn0, steps, tab.nz.as<double>());
+          ++*launches;
+        }
+        k_mcrec_sep<DW><<<grid_for(n * DW, 128), 128, 0, st>>>(B, r0, n, seed, tc0, tc1, tn0, tab.nz.as<double>(),
+                                                              tab.dy.as<double>(), tab.z.as<double>());
+      });
+      if (tc0 + kTabSlice > T) break;
+    }
   } else if (tab.sep) {
     const SepBlocks B = sep_blocks(HL);
     dispatch_dw(dw, [&]<int DW>() {
@@ -1000,6 +1006,15 @@ void launch_mc(const HostLoop& HL, const DevWorld& w, int n_traj, const int64_t*
   if (r1 <= r0 || n_traj <= 0) return;
   if (HL.dw != w.dw) throw std::invalid_argument("mc_certify: workspace / model dimension mismatch");
   static const bool direct = std::getenv("PUMP_MC_DIRECT") != nullptr;
+  // Large certifications (SURVEY config 4: up to 1e7 rollouts) go through the
+  // table in rollout chunks; each chunk's hits accumulate into d_hits.
+  constexpr int64_t kTabRollouts = int64_t(1) << 19;
+  if (table && !direct && r1 - r0 > kTabRollouts) {
+    for (int64_t c0 = r0; c0 < r1; c0 += kTabRollouts)
+      launch_mc(HL, w, n_traj, d_traj_off, d_ynom, max_points, c0, std::min(r1, c0 + kTabRollouts), seed, eps_cc,
+                d_hits, st, launches, d_steps, table);
+    return;
+  }
   if (table && !direct && ensure_table(*table, HL, r0, r1, seed, max_points - 1, st, launches)) {
     WorldD wd;
     wd.n_obs = w.n_obs;
