@@ -297,12 +297,14 @@ int pump_mc_certify_batch(pump_ctx* ctx, const pump_closed_loop* cl, const pump_
     c.h2d(yn.p, y_nom, n_pts * L.dw * 8);
     PUMP_CUDA(cudaMemsetAsync(hits.p, 0, (n_traj + 1) * 8, c.stream));
     c.tic();
-    // several trajectories share the rollouts' noise: certify them against one
-    // common-random-number table (built within this call, not kept across calls)
+    // certify against a common-random-number table built within this call
+    // (not kept across calls); its parallel noise phase beats the fused
+    // kernel even for one trajectory.  PUMP_MC_DIRECT=1 forces the fused
+    // kernels (tests/test_gpu_kernels.py checks both paths).
     c.mc_table.invalidate();
     launch_mc(L, w, n_traj, off.as<int64_t>(), yn.as<double>(), max_pts, rollout_lo, rollout_hi, seed, eps_cc,
               hits.as<unsigned long long>(), c.stream, &c.launches, hits.as<unsigned long long>() + n_traj,
-              n_traj > 1 ? &c.mc_table : nullptr);
+              &c.mc_table);
     c.toc();
     std::vector<int64_t> hv(n_traj + 1);
     c.d2h(hv.data(), hits.p, (n_traj + 1) * 8);

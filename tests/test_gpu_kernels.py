@@ -5,6 +5,7 @@ Bar: bit-exact (bank doubles compared by their bit patterns, masks word for
 word, hit counts and per-rollout flags exactly).
 """
 import json
+import os
 
 import numpy as np
 import pytest
@@ -157,3 +158,17 @@ def test_mc_trajectories_match_oracle(oracle_lib, gpu_ctx, name, n_mc):
     for i in idx:
         h = int(api.mc_certify_batch(cl, ws, [y], i, i + 1, 2, sc["eps_cc"], gpu_ctx)[0])
         assert h == int(ref_flags[i])
+
+
+@pytest.mark.parametrize("env", [{"PUMP_MC_DIRECT": "1"}, {"PUMP_MC_DIRECT": "1", "PUMP_MC_DENSE": "1"},
+                                 {"PUMP_MCTAB_FUSED": "1"}])
+def test_mc_kernel_paths(env):
+    """Every MC kernel path stays bit-exact: the fused lane-per-axis kernel,
+    the dense kernel and the fused table build (selected per process)."""
+    import subprocess
+    import sys
+
+    e = dict(os.environ, **env)
+    r = subprocess.run([sys.executable, os.path.join(os.path.dirname(__file__), "mc_paths_check.py")], env=e,
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
