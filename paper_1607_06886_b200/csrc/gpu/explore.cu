@@ -18,6 +18,8 @@
 //   k_group_post + scan      task offsets (degree prefix sum) of the group
 // The arena, member segments, pool and group stay resident in HBM.
 #include <climits>
+#include <cstdio>
+#include <cstdlib>
 
 #include "dispatch.cuh"
 #include "explore.h"
@@ -99,12 +101,8 @@ constexpr int kExpStage = 64;  // half-spaces staged per warp (2 KB of shared me
 // once) and prefetches each next waypoint's bank row while testing the
 // current one, so the loop does not wait on a chain of global round trips.
 template <int DW, int CH>
-__global__ void __launch_bounds__(kExpBlock) k_expand(const ExpandArgs a) {
-  __shared__ double2 s_hs[kExpBlock / 32][kExpStage][2];
-  const int64_t task = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-  const int64_t T = *a.d_T;
-  if (task >= T) return;
+__device__ __forceinline__ void expand_task(const ExpandArgs& a, int64_t task, int lane, int wib,
+                                            double2 (*s_hs)[kExpStage][2]) {
   const int64_t lo = a.task_grp[task];  // the group entry owning this task (k_task_map)
   const int pid = a.group[lo];
   const int hv = a.head[pid];
@@ -213,6 +211,15 @@ __global__ void __launch_bounds__(kExpBlock) k_expand(const ExpandArgs a) {
   }
 }
 
+template <int DW, int CH>
+__global__ void __launch_bounds__(kExpBlock) k_expand(const ExpandArgs a) {
+  __shared__ double2 s_hs[kExpBlock / 32][kExpStage][2];
+  const int64_t task = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  if (task >= *a.d_T) return;
+  expand_task<DW, CH>(a, task, lane, wib, s_hs);
+}
+
 struct CommitArgs {
   const int64_t* d_T;
   const uint8_t* keep;
@@ -240,11 +247,9 @@ struct CommitArgs {
   ExploreStatus* st;
 };
 
-__global__ void k_commit(const CommitArgs a) {
-  const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (t >= *a.d_T || !a.keep[t]) return;
+// commit candidate t (kept) as arena plan n_plans + r (r = its rank)
+__device__ __forceinline__ void commit_one(const CommitArgs& a, int64_t t, int64_t r) {
   const int64_t P0 = a.st->n_plans;
-  const int64_t r = a.rank[t];
   const int64_t id = P0 + r;
   const int hv = a.c_head[t];
   const double c = a.c_cost[t];
@@ -263,6 +268,12 @@ __global__ void k_commit(const CommitArgs a) {
   const int slot = atomicAdd(&a.new_cnt[hv], 1);
   a.new_slot[r] = slot;
   if (slot == 0) a.touched[atomicAdd(reinterpret_cast<unsigned long long*>(&a.st->touched), 1ull)] = hv;
+}
+
+__global__ void k_commit(const CommitArgs a) {
+  const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (t >= *a.d_T || !a.keep[t]) return;
+  commit_one(a, t, a.rank[t]);
 }
 
 // node sizes for the member relayout; thread 0 also publishes K = kept
@@ -302,48 +313,61 @@ __global__ void k_place_new(const int64_t* d_K, const ExploreStatus* st, const i
 // RemoveDominated, both directions, for one touched node per CTA.
 // Segment layout on entry: [old members (ascending ids) | newcomers (any
 // order)].  On exit: [old survivors | surviving newcomers by id].
-// RemoveDominated at one touched node per CTA (planner.hpp:200-238).  The
-// node's members (ids, cost, cp) are first staged in shared memory with one
-// batch of independent loads, so the O(m_new * m) dominance scans read shared
-// memory instead of chasing ids through global memory; nodes with more than
-// kDomCap members take the same steps on global memory.
 constexpr int kDomCap = 1024;
-__global__ void __launch_bounds__(128) k_dom(const ExploreStatus* st, const int32_t* touched,
-                                             const int64_t* new_off, int32_t* mem_cnt, int32_t* new_cnt,
-                                             int32_t* ids, const double* cost, const double* cp, uint8_t* flags,
-                                             uint8_t* drop, uint8_t* surv, int32_t* fpos, ExploreStatus* stw) {
-  const int64_t P0 = st->n_plans;
-  __shared__ int s_old_surv, s_new_surv, s_drop, s_evict, s_evict_open;
-  __shared__ int32_t s_id[kDomCap];
-  __shared__ double s_c[kDomCap], s_p[kDomCap];
-  __shared__ uint8_t s_dr[kDomCap];
+struct DomShared {
+  int old_surv, new_surv, drop, evict, evict_open;
+  int32_t id[kDomCap];
+  double c[kDomCap], p[kDomCap];
+  uint8_t dr[kDomCap];
+};
+struct DomArgs {
+  const int32_t* touched;
+  const int64_t* new_off;
+  int32_t* mem_cnt;
+  int32_t* new_cnt;
+  int32_t* ids;
+  const double* cost;
+  const double* cp;
+  uint8_t* flags;
+  uint8_t* drop;
+  uint8_t* surv;
+  int32_t* fpos;
+  ExploreStatus* stw;
+};
+
+// one touched node b; all threads of the block call it together
+__device__ void dom_node(const DomArgs& A, DomShared& sh, int64_t b, int64_t P0) {
+  int32_t* ids = A.ids;
+  const double* cost = A.cost;
+  const double* cp = A.cp;
+  uint8_t* drop = A.drop;
   constexpr int kMaxLocal = 64;
-  for (int64_t b = blockIdx.x; b < st->touched; b += gridDim.x) {
-    const int v = touched[b];
-    const int64_t base = new_off[v];
-    const int m_old = mem_cnt[v];
-    const int m_new = new_cnt[v];
+  {
+    const int v = A.touched[b];
+    const int64_t base = A.new_off[v];
+    const int m_old = A.mem_cnt[v];
+    const int m_new = A.new_cnt[v];
     const int m = m_old + m_new;
     const bool staged = m <= kDomCap;
     if (threadIdx.x == 0) {
-      s_old_surv = 0;
-      s_new_surv = 0;
-      s_drop = 0;
-      s_evict = 0;
-      s_evict_open = 0;
+      sh.old_surv = 0;
+      sh.new_surv = 0;
+      sh.drop = 0;
+      sh.evict = 0;
+      sh.evict_open = 0;
     }
     if (staged) {
       for (int x = threadIdx.x; x < m; x += blockDim.x) {
         const int id = ids[base + x];
-        s_id[x] = id;
-        s_c[x] = cost[id];
-        s_p[x] = cp[id];
+        sh.id[x] = id;
+        sh.c[x] = cost[id];
+        sh.p[x] = cp[id];
       }
     }
     __syncthreads();
-    auto ID = [&](int x) { return staged ? s_id[x] : ids[base + x]; };
-    auto CO = [&](int x) { return staged ? s_c[x] : cost[ids[base + x]]; };
-    auto CP = [&](int x) { return staged ? s_p[x] : cp[ids[base + x]]; };
+    auto ID = [&](int x) { return staged ? sh.id[x] : ids[base + x]; };
+    auto CO = [&](int x) { return staged ? sh.c[x] : cost[ids[base + x]]; };
+    auto CP = [&](int x) { return staged ? sh.p[x] : cp[ids[base + x]]; };
     // (1) drop newcomers dominated by any member of the pre-removal set,
     //     old or new (planner.hpp:200-211); dominates(o, q) = q.cost > o.cost
     //     && q.cp >= o.cp (planner.hpp:58-60)
@@ -353,12 +377,12 @@ __global__ void __launch_bounds__(128) k_dom(const ExploreStatus* st, const int3
       bool d = false;
       for (int x = 0; x < m && !d; ++x) d = (qc > CO(x)) && (qp >= CP(x));
       drop[q - P0] = d ? 1 : 0;
-      surv[q - P0] = d ? 0 : 1;
-      if (staged) s_dr[m_old + qi] = d ? 1 : 0;
-      if (d) atomicAdd(&s_drop, 1);
+      A.surv[q - P0] = d ? 0 : 1;
+      if (staged) sh.dr[m_old + qi] = d ? 1 : 0;
+      if (d) atomicAdd(&sh.drop, 1);
     }
     __syncthreads();
-    auto DROPPED = [&](int qi) { return staged ? s_dr[m_old + qi] != 0 : drop[ids[base + m_old + qi] - P0] != 0; };
+    auto DROPPED = [&](int qi) { return staged ? sh.dr[m_old + qi] != 0 : drop[ids[base + m_old + qi] - P0] != 0; };
     // (2) evict old members other than the root that a surviving newcomer
     //     dominates (planner.hpp:219-238); evicted slots become -1 - id
     for (int pi = threadIdx.x; pi < m_old; pi += blockDim.x) {
@@ -371,13 +395,13 @@ __global__ void __launch_bounds__(128) k_dom(const ExploreStatus* st, const int3
         ev = (pc > CO(m_old + qi)) && (pp >= CP(m_old + qi));
       }
       if (ev) {
-        atomicAdd(&s_evict, 1);
-        if (flags[p] & kOpen) {  // waiting in a bucket: skipped at collection
-          flags[p] &= static_cast<uint8_t>(~kOpen);
-          atomicAdd(&s_evict_open, 1);
+        atomicAdd(&sh.evict, 1);
+        if (A.flags[p] & kOpen) {  // waiting in a bucket: skipped at collection
+          A.flags[p] &= static_cast<uint8_t>(~kOpen);
+          atomicAdd(&sh.evict_open, 1);
         }
         if (staged)
-          s_id[pi] = -1 - p;
+          sh.id[pi] = -1 - p;
         else
           ids[base + pi] = -1 - p;
       }
@@ -389,8 +413,8 @@ __global__ void __launch_bounds__(128) k_dom(const ExploreStatus* st, const int3
       const int q = ID(m_old + qi);
       int r = 0;
       for (int xi = 0; xi < m_new; ++xi) r += (!DROPPED(xi) && ID(m_old + xi) < q) ? 1 : 0;
-      fpos[q - P0] = r;
-      atomicAdd(&s_new_surv, 1);
+      A.fpos[q - P0] = r;
+      atomicAdd(&sh.new_surv, 1);
     }
     if (threadIdx.x == 0) {
       int w = 0;
@@ -398,7 +422,7 @@ __global__ void __launch_bounds__(128) k_dom(const ExploreStatus* st, const int3
         const int p = ID(pi);
         if (p >= 0) ids[base + w++] = p;
       }
-      s_old_surv = w;
+      sh.old_surv = w;
     }
     if (staged) {
       __syncthreads();
@@ -406,8 +430,8 @@ __global__ void __launch_bounds__(128) k_dom(const ExploreStatus* st, const int3
       //     ids are still in shared memory)
       for (int qi = threadIdx.x; qi < m_new; qi += blockDim.x) {
         if (DROPPED(qi)) continue;
-        const int q = s_id[m_old + qi];
-        ids[base + s_old_surv + fpos[q - P0]] = q;
+        const int q = sh.id[m_old + qi];
+        ids[base + sh.old_surv + A.fpos[q - P0]] = q;
       }
     } else {
       // (4) gather surviving newcomers before overwriting their slots
@@ -419,22 +443,37 @@ __global__ void __launch_bounds__(128) k_dom(const ExploreStatus* st, const int3
       }
       __syncthreads();
       if (m_new > kMaxLocal * static_cast<int>(blockDim.x)) {
-        if (threadIdx.x == 0) atomicExch(reinterpret_cast<unsigned long long*>(&stw->err), 2ull);
+        if (threadIdx.x == 0) atomicExch(reinterpret_cast<unsigned long long*>(&A.stw->err), 2ull);
       } else {
-        for (int k = 0; k < my_n; ++k) ids[base + s_old_surv + fpos[my_q[k] - P0]] = my_q[k];
+        for (int k = 0; k < my_n; ++k) ids[base + sh.old_surv + A.fpos[my_q[k] - P0]] = my_q[k];
       }
     }
     __syncthreads();
     if (threadIdx.x == 0) {
-      mem_cnt[v] = s_old_surv + s_new_surv;
-      new_cnt[v] = 0;
-      atomicAdd(reinterpret_cast<unsigned long long*>(&stw->removed),
-                static_cast<unsigned long long>(s_drop + s_evict));
-      atomicAdd(reinterpret_cast<unsigned long long*>(&stw->evicted_open),
-                static_cast<unsigned long long>(s_evict_open));
+      A.mem_cnt[v] = sh.old_surv + sh.new_surv;
+      A.new_cnt[v] = 0;
+      atomicAdd(reinterpret_cast<unsigned long long*>(&A.stw->removed),
+                static_cast<unsigned long long>(sh.drop + sh.evict));
+      atomicAdd(reinterpret_cast<unsigned long long*>(&A.stw->evicted_open),
+                static_cast<unsigned long long>(sh.evict_open));
     }
     __syncthreads();
   }
+}
+
+// RemoveDominated at one touched node per CTA (planner.hpp:200-238).  The
+// node's members (ids, cost, cp) are first staged in shared memory with one
+// batch of independent loads, so the O(m_new * m) dominance scans read shared
+// memory instead of chasing ids through global memory; nodes with more than
+// kDomCap members take the same steps on global memory.
+__global__ void __launch_bounds__(128) k_dom(const ExploreStatus* st, const int32_t* touched,
+                                             const int64_t* new_off, int32_t* mem_cnt, int32_t* new_cnt,
+                                             int32_t* ids, const double* cost, const double* cp, uint8_t* flags,
+                                             uint8_t* drop, uint8_t* surv, int32_t* fpos, ExploreStatus* stw) {
+  __shared__ DomShared sh;
+  const DomArgs A{touched, new_off, mem_cnt, new_cnt, ids, cost, cp, flags, drop, surv, fpos, stw};
+  const int64_t P0 = st->n_plans;
+  for (int64_t b = blockIdx.x; b < st->touched; b += gridDim.x) dom_node(A, sh, b, P0);
 }
 
 __global__ void k_pool_append(const int64_t* d_K, const ExploreStatus* st, const uint8_t* surv, const int64_t* spos,
@@ -533,6 +572,335 @@ __global__ void k_group_final(ExploreStatus* st, const int64_t* d_G, const int64
   st->T = task_off[G];
   *d_T = task_off[G];
   st->pool_n = stay_pos[*d_pool_n];
+}
+
+// ======================================================================
+// Cooperative round: one persistent launch per explore round.  Every phase
+// after the expand (merge, relayout, RemoveDominated, pool append, bucket
+// selection, frontier compaction and multisplit, task offsets) and the next
+// round's task map run as grid-stride phases of one kernel separated by grid
+// barriers, instead of ~25 launches of tiny kernels.  The phases are the
+// per-item bodies of the kernels above (shared device functions where they
+// are non-trivial), so both paths compute the same records.
+struct GridBar {
+  unsigned int count;
+  unsigned int gen;
+};
+
+// all blocks are co-resident (cooperative launch): sense-reversal barrier
+__device__ __forceinline__ void grid_sync(GridBar* bar) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    volatile unsigned int* vgen = &bar->gen;
+    const unsigned int g = *vgen;
+    __threadfence();
+    if (atomicAdd(&bar->count, 1u) == gridDim.x - 1) {
+      bar->count = 0;
+      __threadfence();
+      atomicAdd(&bar->gen, 1u);
+    } else {
+      while (*vgen == g) __nanosleep(32);
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+constexpr int kCoopBlock = kExpBlock;  // 256
+__device__ __forceinline__ int64_t block_sum(int64_t v, int64_t* red) {
+  v = warp_sum(v);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  __syncthreads();
+  if (l == 0) red[w] = v;
+  __syncthreads();
+  int64_t t = 0;
+  for (int k = 0; k < kCoopBlock / 32; ++k) t += red[k];
+  return t;
+}
+
+// exclusive scan across the block; *tot = block total
+__device__ __forceinline__ int64_t block_excl(int64_t v, int64_t* red, int64_t* tot) {
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  const int64_t inc = warp_incl_scan(v);
+  __syncthreads();
+  if (l == 31) red[w] = inc;
+  __syncthreads();
+  int64_t before = 0, all = 0;
+  for (int k = 0; k < kCoopBlock / 32; ++k) {
+    const int64_t x = red[k];
+    before += k < w ? x : 0;
+    all += x;
+  }
+  *tot = all;
+  return before + inc - v;
+}
+
+// Grid-wide exclusive scan of val(i) for i < n into out[0..n] (out[n] =
+// total); post(i, excl, v) runs for every i in the second pass.  val(i, pass)
+// is evaluated twice (pass 0: reduce, pass 1: scan).  One grid barrier inside;
+// the caller syncs before anyone reads out[] of another block or reuses blk.
+template <class Val, class Post>
+__device__ int64_t coop_scan(int64_t n, Val val, Post post, int64_t* out, int64_t* blk, GridBar* bar, int64_t* red) {
+  const int64_t nb = gridDim.x, b = blockIdx.x;
+  const int64_t chunk = (n + nb - 1) / nb;
+  const int64_t lo = min(n, b * chunk), hi = min(n, lo + chunk);
+  int64_t s = 0;
+  for (int64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) s += val(i, 0);
+  s = block_sum(s, red);
+  if (threadIdx.x == 0) blk[b] = s;
+  grid_sync(bar);
+  int64_t pre = 0, tot = 0;
+  for (int64_t c = threadIdx.x; c < nb; c += blockDim.x) {
+    const int64_t x = blk[c];
+    tot += x;
+    pre += c < b ? x : 0;
+  }
+  pre = block_sum(pre, red);
+  tot = block_sum(tot, red);
+  for (int64_t base = lo; base < hi; base += blockDim.x) {
+    const int64_t i = base + threadIdx.x;
+    const int64_t v = i < hi ? val(i, 1) : 0;
+    int64_t tile = 0;
+    const int64_t ex = block_excl(v, red, &tile);
+    if (i < hi) {
+      out[i] = pre + ex;
+      post(i, pre + ex, v);
+    }
+    pre += tile;
+  }
+  if (b == nb - 1 && threadIdx.x == 0) out[n] = tot;
+  return tot;
+}
+
+struct CoopArgs {
+  ExpandArgs ex;
+  CommitArgs cm;
+  int n;
+  GridBar* bar;
+  int64_t* blk;  // gridDim.x + 1 scan partials
+  ExploreStatus* S;
+  int64_t *d_K, *d_pool_n, *d_G, *d_T, *limits;
+  // members: old layout (mem_off, old_ids) -> new layout (off2, new_ids)
+  const int64_t* mem_off;
+  int32_t* mem_cnt;
+  int32_t* new_cnt;
+  const int32_t* old_ids;
+  int64_t* off2;
+  int32_t* new_ids;
+  const int32_t* new_slot;
+  int32_t* touched;
+  uint8_t *drop, *surv;
+  int32_t* fpos;
+  int64_t* spos;
+  // pool and frontier
+  int32_t* pool_cur;
+  int32_t* pool_nxt;
+  int32_t* keys;
+  int64_t* stay_pos;
+  int64_t n_keys;  // <= kCoopKeys
+  int32_t* ms_counts;
+  int64_t* ms_offs;
+  int32_t* group;
+  int64_t* task_off;
+  int32_t* task_grp;
+  const int64_t* row_ptr;
+  unsigned long long* stamps;  // optional phase timestamps (PUMP_DEBUG_COOP)
+};
+constexpr int kCoopKeys = 512;
+
+__global__ void __launch_bounds__(kCoopBlock, 2) k_round_tail(const CoopArgs A) {
+  __shared__ DomShared dsh;
+  __shared__ int s_hist[kCoopKeys];
+  __shared__ int64_t s_run[kCoopKeys];
+  __shared__ int64_t red[kCoopBlock / 32];
+  ExploreStatus* S = A.S;
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const int64_t gtid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t gthreads = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  const int64_t gwarp = gtid >> 5, gwarps = gthreads >> 5;
+  const int nb = gridDim.x;
+  int stamp_i = 0;
+  auto STAMP = [&]() {
+    if (A.stamps && gtid == 0) {
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      A.stamps[stamp_i] = t;
+    }
+    ++stamp_i;
+  };
+  STAMP();
+
+  // (k_task_map and k_expand ran as their own launches before this one)
+  const int64_t T = *A.d_T;
+  (void)wib;
+  // keep -> rank, commit as plan n_plans + rank
+  const int64_t P0 = S->n_plans;
+  const uint8_t* keep = A.cm.keep;
+  const int64_t K = coop_scan(
+      T, [&](int64_t i, int) -> int64_t { return keep[i]; },
+      [&](int64_t i, int64_t ex, int64_t v) {
+        if (v) commit_one(A.cm, i, ex);
+      },
+      A.cm.rank == nullptr ? nullptr : const_cast<int64_t*>(A.cm.rank), A.blk, A.bar, red);
+  if (gtid == 0) {
+    S->K = K;
+    *A.d_K = K;
+    S->min_bucket = LLONG_MAX;
+  }
+  grid_sync(A.bar);
+  STAMP();
+  // member relayout: new offsets, old members, newcomers at their slots
+  const int n = A.n;
+  coop_scan(
+      n, [&](int64_t v, int) -> int64_t { return A.mem_cnt[v] + A.new_cnt[v]; }, [](int64_t, int64_t, int64_t) {},
+      A.off2, A.blk, A.bar, red);
+  grid_sync(A.bar);
+  STAMP();
+  for (int64_t v = gwarp; v < n; v += gwarps) {
+    const int m = A.mem_cnt[v];
+    const int64_t a0 = A.mem_off[v], b0 = A.off2[v];
+    for (int k = lane; k < m; k += 32) A.new_ids[b0 + k] = A.old_ids[a0 + k];
+  }
+  for (int64_t r = gtid; r < K; r += gthreads) {
+    const int64_t id = P0 + r;
+    const int hv = A.ex.head[id];
+    A.new_ids[A.off2[hv] + A.mem_cnt[hv] + A.new_slot[r]] = static_cast<int32_t>(id);
+  }
+  grid_sync(A.bar);
+  STAMP();
+  // RemoveDominated, block per touched node
+  {
+    const DomArgs D{A.touched, A.off2, A.mem_cnt, A.new_cnt, A.new_ids, A.cm.cost, A.cm.cp, A.cm.flags,
+                    A.drop, A.surv, A.fpos, S};
+    const int64_t nt = S->touched;
+    for (int64_t b = blockIdx.x; b < nt; b += nb) dom_node(D, dsh, b, P0);
+  }
+  grid_sync(A.bar);
+  STAMP();
+  // surviving newcomers -> open pool (id order); lowest open bucket
+  const int64_t pool_old = S->pool_n;
+  const int32_t* bucket = A.cm.bucket;
+  uint8_t* flags = A.cm.flags;
+  const int64_t NS = coop_scan(
+      K, [&](int64_t r, int) -> int64_t { return A.surv[r]; },
+      [&](int64_t r, int64_t ex, int64_t v) {
+        if (v) {
+          const int64_t id = P0 + r;
+          A.pool_cur[pool_old + ex] = static_cast<int32_t>(id);
+          flags[id] |= kOpen;
+          atomicMax(&S->max_bucket, static_cast<long long>(bucket[id]));
+          atomicMin(&S->min_bucket, static_cast<long long>(bucket[id]));
+        }
+      },
+      A.spos, A.blk, A.bar, red);
+  for (int64_t x = gtid; x < pool_old; x += gthreads) {
+    const int id = A.pool_cur[x];
+    if (flags[id] & kOpen) atomicMin(&S->min_bucket, static_cast<long long>(bucket[id]));
+  }
+  grid_sync(A.bar);
+  STAMP();
+  // end-of-round bookkeeping and the next threshold (k_round_i)
+  if (gtid == 0) {
+    S->n_surv = NS;
+    S->pool_n += NS;
+    S->open_count += NS - S->evicted_open - S->G;
+    S->n_plans += K;
+    long long i = S->i + 1;
+    if (S->min_bucket != LLONG_MAX && S->min_bucket > i) i = S->min_bucket;
+    S->i = i;
+    const long long limit = i < S->max_bucket ? i : S->max_bucket;
+    A.limits[0] = limit;
+    A.limits[1] = S->min_bucket == LLONG_MAX ? 0 : S->min_bucket;
+    *A.d_pool_n = S->pool_n;
+    S->G = 0;
+    S->T = 0;
+    S->min_group_bits = 0x7ff0000000000000ll;
+    S->touched = 0;
+    S->evicted_open = 0;
+  }
+  grid_sync(A.bar);
+  STAMP();
+  // bucket selection (k_select) fused into the stay scan; stayers compacted
+  const int64_t m = *A.d_pool_n;
+  const int64_t lim0 = A.limits[0], lim1 = A.limits[1];
+  const int64_t stay_n = coop_scan(
+      m,
+      [&](int64_t x, int pass) -> int64_t {
+        const int id = A.pool_cur[x];
+        const bool open = flags[id] & kOpen;
+        const int b = bucket[id];
+        const bool sel = open && b <= lim0;
+        if (pass) {
+          const int64_t key = b - lim1;
+          if (sel && key >= A.n_keys) atomicExch(reinterpret_cast<unsigned long long*>(&S->err), 3ull);
+          A.keys[x] = sel ? static_cast<int32_t>(key) : -1;
+        }
+        return (open && !sel) ? 1 : 0;
+      },
+      [&](int64_t x, int64_t ex, int64_t v) {
+        if (v) A.pool_nxt[ex] = A.pool_cur[x];
+      },
+      A.stay_pos, A.blk, A.bar, red);
+  grid_sync(A.bar);
+  STAMP();
+  // stable multisplit by key (one radix pass, keys < n_keys <= 512):
+  // per-block histograms over contiguous chunks, key-major scan, ordered scatter
+  const int64_t chunk = (m + nb - 1) / nb;
+  const int64_t lo = min(m, static_cast<int64_t>(blockIdx.x) * chunk), hi = min(m, lo + chunk);
+  const int nk = static_cast<int>(A.n_keys);
+  for (int k = threadIdx.x; k < nk; k += blockDim.x) s_hist[k] = 0;
+  __syncthreads();
+  for (int64_t x = lo + threadIdx.x; x < hi; x += blockDim.x) {
+    const int key = A.keys[x];
+    if (key >= 0) atomicAdd(&s_hist[key], 1);
+  }
+  __syncthreads();
+  for (int k = threadIdx.x; k < nk; k += blockDim.x) A.ms_counts[static_cast<int64_t>(k) * nb + blockIdx.x] = s_hist[k];
+  grid_sync(A.bar);
+  STAMP();
+  const int64_t Gn = coop_scan(
+      static_cast<int64_t>(nk) * nb, [&](int64_t i, int) -> int64_t { return A.ms_counts[i]; },
+      [](int64_t, int64_t, int64_t) {}, A.ms_offs, A.blk, A.bar, red);
+  grid_sync(A.bar);
+  STAMP();
+  for (int k = threadIdx.x; k < nk; k += blockDim.x) s_run[k] = A.ms_offs[static_cast<int64_t>(k) * nb + blockIdx.x];
+  __syncthreads();
+  if (wib == 0) {
+    const unsigned lt = (1u << lane) - 1u;
+    for (int64_t base = lo; base < hi; base += 32) {
+      const int64_t x = base + lane;
+      const int key = x < hi ? A.keys[x] : -1;
+      const unsigned peers = __match_any_sync(0xffffffffu, key);
+      const int rank = __popc(peers & lt);
+      if (key >= 0) A.group[s_run[key] + rank] = A.pool_cur[x];
+      __syncwarp();
+      if (key >= 0 && rank == __popc(peers) - 1) s_run[key] += __popc(peers);
+      __syncwarp();
+    }
+  }
+  if (gtid == 0) *A.d_G = Gn;
+  grid_sync(A.bar);
+  STAMP();
+  // the new group: close it, its degrees -> task offsets, cheapest cost
+  const int64_t Tn = coop_scan(
+      Gn,
+      [&](int64_t g, int pass) -> int64_t {
+        const int id = A.group[g];
+        const int hv = A.ex.head[id];
+        if (pass) {
+          flags[id] &= static_cast<uint8_t>(~kOpen);
+          atomicMin(&S->min_group_bits, __double_as_longlong(A.cm.cost[id]));
+        }
+        return A.row_ptr[hv + 1] - A.row_ptr[hv];
+      },
+      [](int64_t, int64_t, int64_t) {}, A.task_off, A.blk, A.bar, red);
+  if (gtid == 0) {
+    S->G = Gn;
+    S->T = Tn;
+    *A.d_T = Tn;
+    S->pool_n = stay_n;
+  }
+  STAMP();
 }
 
 static void swap_buf(DBuf& a, DBuf& b) {
@@ -671,6 +1039,19 @@ void run_explore_device(DevExplore& X, Ctx& c, const DevGraph& G, const ExploreA
   X.pool_flip = false;
   const double width = prm.lambda * prm.r_n;
 
+  // cooperative round kernel for this (dw, particle-words) instance
+  static const bool legacy_env = std::getenv("PUMP_EXPLORE_LEGACY") != nullptr;
+  const void* coop_fn = reinterpret_cast<const void*>(&k_round_tail);
+  int coop_blocks = 0;
+  {
+    int per_sm = 0, sms = 0, coop_attr = 0;
+    PUMP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, coop_fn, kCoopBlock, 0));
+    per_sm = std::min(per_sm, 2);  // fewer blocks: cheaper grid barriers; the tail phases are small
+    PUMP_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c.device));
+    PUMP_CUDA(cudaDeviceGetAttribute(&coop_attr, cudaDevAttrCooperativeLaunch, c.device));
+    coop_blocks = coop_attr ? per_sm * sms : 0;
+  }
+  const bool coop_ok = !legacy_env && coop_blocks > 0;
   c.tic();
   for (;;) {
     // loop-top termination (planner.hpp:126-138); h is the status after the
@@ -705,126 +1086,232 @@ void run_explore_device(DevExplore& X, Ctx& c, const DevGraph& G, const ExploreA
     DBuf& spos = c.buf("x_spos", al((T + 2) * 8));
     DBuf& stmp = c.buf("x_scan_tmp", scan_temp_bytes(std::max<int64_t>({T, n, X.cap}) + 16));
 
-    if (T > 0) {
+    int64_t n_keys_r = 1 << 18;  // see k_select: distinct bucket keys this round
+    if (h.min_bucket != LLONG_MAX && h.i + 2 - h.min_bucket <= 512) n_keys_r = std::max<int64_t>(1, h.i + 2 - h.min_bucket);
+    if (coop_ok && T > 0 && n_keys_r <= kCoopKeys) {
+      // ---- one cooperative launch for the whole round
+      const int64_t pool_ub = h.pool_n + T + 1;
       X.task_grp.ensure(al((T + 1) * 4));
+      X.group.grow(al((pool_ub + 1) * 4), static_cast<size_t>(h.G) * 4, st);
+      X.task_off.grow(al((pool_ub + 2) * 8), static_cast<size_t>(h.G + 1) * 8, st);
+      DBuf& keys = c.buf("x_sel_keys", al((pool_ub + 1) * 4));
+      DBuf& stay_pos = c.buf("x_stay_pos", al((pool_ub + 2) * 8));
+      DBuf& msc = c.buf("x_coop_counts", al(static_cast<size_t>(kCoopKeys) * coop_blocks * 4));
+      DBuf& mso = c.buf("x_coop_offs", al((static_cast<size_t>(kCoopKeys) * coop_blocks + 2) * 8));
+      DBuf& blk = c.buf("x_coop_blk", al((coop_blocks + 2) * 8));
+      DBuf& bar = c.buf("x_coop_bar", 256);
+      DBuf& old_ids = X.mem_flip ? X.mem_b : X.mem_a;
+      DBuf& new_ids = X.mem_flip ? X.mem_a : X.mem_b;
+      DBuf& pool_cur = X.pool_flip ? X.pool_b : X.pool_a;
+      DBuf& pool_nxt = X.pool_flip ? X.pool_a : X.pool_b;
+      PUMP_CUDA(cudaMemsetAsync(bar.p, 0, 8, st));
+      CoopArgs A{};
+      A.ex = ExpandArgs{X.group.as<int32_t>(), X.task_off.as<int64_t>(), X.task_grp.as<int32_t>(), d_G, d_T,
+                        G.row_ptr.as<int64_t>(), G.e_to.as<int32_t>(), G.e_cost.as<double>(),
+                        G.e_nsteps.as<int32_t>(), G.wp_off.as<int64_t>(), G.hs_off.as<int64_t>(),
+                        G.hs_cnt.as<int32_t>(), G.hs_pk.as<double>(), X.head.as<int32_t>(), X.cost.as<double>(),
+                        X.t_end.as<int32_t>(), X.mask.as<uint64_t>(), c.bank.as<double>(), N, c.bank_horizon, W,
+                        prm.alpha_max, X.cand_keep.as<uint8_t>(), X.cand_head.as<int32_t>(),
+                        X.cand_src.as<int32_t>(), X.cand_tend.as<int32_t>(), X.cand_cost.as<double>(),
+                        X.cand_cp.as<double>(), X.cand_mask.as<uint64_t>(), S};
+      A.cm = CommitArgs{d_T, X.cand_keep.as<uint8_t>(), X.cand_rank.as<int64_t>(), X.cand_head.as<int32_t>(),
+                        X.cand_src.as<int32_t>(), X.cand_tend.as<int32_t>(), X.cand_cost.as<double>(),
+                        X.cand_cp.as<double>(), X.cand_mask.as<uint64_t>(), W, width, prm.alpha_min,
+                        X.is_goal.as<uint8_t>(), X.head.as<int32_t>(), X.parent.as<int32_t>(), X.cost.as<double>(),
+                        X.cp.as<double>(), X.t_end.as<int32_t>(), X.mask.as<uint64_t>(), X.bucket.as<int32_t>(),
+                        X.flags.as<uint8_t>(), X.new_cnt.as<int32_t>(), X.new_slot.as<int32_t>(),
+                        X.touched.as<int32_t>(), S};
+      A.n = n;
+      A.bar = bar.as<GridBar>();
+      A.blk = blk.as<int64_t>();
+      A.S = S;
+      A.d_K = d_K;
+      A.d_pool_n = d_pool_n;
+      A.d_G = d_G;
+      A.d_T = d_T;
+      A.limits = d_limits;
+      A.mem_off = X.mem_off.as<int64_t>();
+      A.mem_cnt = X.mem_cnt.as<int32_t>();
+      A.new_cnt = X.new_cnt.as<int32_t>();
+      A.old_ids = old_ids.as<int32_t>();
+      A.off2 = off2.as<int64_t>();
+      A.new_ids = new_ids.as<int32_t>();
+      A.new_slot = X.new_slot.as<int32_t>();
+      A.touched = X.touched.as<int32_t>();
+      A.drop = X.drop.as<uint8_t>();
+      A.surv = X.surv.as<uint8_t>();
+      A.fpos = X.fpos.as<int32_t>();
+      A.spos = spos.as<int64_t>();
+      A.pool_cur = pool_cur.as<int32_t>();
+      A.pool_nxt = pool_nxt.as<int32_t>();
+      A.keys = keys.as<int32_t>();
+      A.stay_pos = stay_pos.as<int64_t>();
+      A.n_keys = n_keys_r;
+      A.ms_counts = msc.as<int32_t>();
+      A.ms_offs = mso.as<int64_t>();
+      A.group = X.group.as<int32_t>();
+      A.task_off = X.task_off.as<int64_t>();
+      A.task_grp = X.task_grp.as<int32_t>();
+      A.row_ptr = G.row_ptr.as<int64_t>();
+      static const bool dbg_coop = std::getenv("PUMP_DEBUG_COOP") != nullptr;
+      DBuf& stamps = c.buf("x_coop_stamps", 64 * 8);
+      A.stamps = dbg_coop ? stamps.as<unsigned long long>() : nullptr;
       k_task_map<<<grid_for(h.G * 32, 256), 256, 0, st>>>(d_G, X.task_off.as<int64_t>(), X.task_grp.as<int32_t>());
       ++c.launches;
-      ExpandArgs ea{X.group.as<int32_t>(), X.task_off.as<int64_t>(), X.task_grp.as<int32_t>(), d_G, d_T,
-                    G.row_ptr.as<int64_t>(),
-                    G.e_to.as<int32_t>(), G.e_cost.as<double>(), G.e_nsteps.as<int32_t>(), G.wp_off.as<int64_t>(),
-                    G.hs_off.as<int64_t>(), G.hs_cnt.as<int32_t>(), G.hs_pk.as<double>(),
-                    X.head.as<int32_t>(),
-                    X.cost.as<double>(), X.t_end.as<int32_t>(), X.mask.as<uint64_t>(), c.bank.as<double>(), N,
-                    c.bank_horizon, W, prm.alpha_max, X.cand_keep.as<uint8_t>(), X.cand_head.as<int32_t>(),
-                    X.cand_src.as<int32_t>(), X.cand_tend.as<int32_t>(), X.cand_cost.as<double>(),
-                    X.cand_cp.as<double>(), X.cand_mask.as<uint64_t>(), S};
-      const unsigned grid = grid_for(T * 32, 256);
-      KScope ks(st, F_EXPAND);
-      dispatch_dw(G.dw, [&]<int DW>() {
-        switch (ch) {
-          case 1: k_expand<DW, 1><<<grid, 256, 0, st>>>(ea); break;
-          case 2: k_expand<DW, 2><<<grid, 256, 0, st>>>(ea); break;
-          case 4: k_expand<DW, 4><<<grid, 256, 0, st>>>(ea); break;
-          case 8: k_expand<DW, 8><<<grid, 256, 0, st>>>(ea); break;
-          default: k_expand<DW, 16><<<grid, 256, 0, st>>>(ea); break;
-        }
-      });
+      {
+        const unsigned grid = grid_for(T * 32, 256);
+        KScope ks(st, F_EXPAND);
+        dispatch_dw(G.dw, [&]<int DW>() {
+          switch (ch) {
+            case 1: k_expand<DW, 1><<<grid, 256, 0, st>>>(A.ex); break;
+            case 2: k_expand<DW, 2><<<grid, 256, 0, st>>>(A.ex); break;
+            case 4: k_expand<DW, 4><<<grid, 256, 0, st>>>(A.ex); break;
+            case 8: k_expand<DW, 8><<<grid, 256, 0, st>>>(A.ex); break;
+            default: k_expand<DW, 16><<<grid, 256, 0, st>>>(A.ex); break;
+          }
+        });
+        ++c.launches;
+      }
+      {
+        KScope ks(st, F_COMMIT);
+        void* args[] = {&A};
+        PUMP_CUDA(cudaLaunchCooperativeKernel(coop_fn, dim3(coop_blocks), dim3(kCoopBlock), args, 0, st));
+      }
       ++c.launches;
       PUMP_CUDA(cudaGetLastError());
-    }
-    exclusive_scan<uint8_t>(X.cand_keep.as<uint8_t>(), X.cand_rank.as<int64_t>(), T, stmp.p, st, &c.launches, d_T);
-    if (T == 0) PUMP_CUDA(cudaMemsetAsync(X.cand_rank.p, 0, 8, st));
-    CommitArgs ca{d_T, X.cand_keep.as<uint8_t>(), X.cand_rank.as<int64_t>(), X.cand_head.as<int32_t>(),
-                  X.cand_src.as<int32_t>(), X.cand_tend.as<int32_t>(), X.cand_cost.as<double>(),
-                  X.cand_cp.as<double>(), X.cand_mask.as<uint64_t>(), W, width, prm.alpha_min,
-                  X.is_goal.as<uint8_t>(), X.head.as<int32_t>(), X.parent.as<int32_t>(), X.cost.as<double>(),
-                  X.cp.as<double>(), X.t_end.as<int32_t>(), X.mask.as<uint64_t>(), X.bucket.as<int32_t>(),
-                  X.flags.as<uint8_t>(), X.new_cnt.as<int32_t>(), X.new_slot.as<int32_t>(),
-                  X.touched.as<int32_t>(), S};
-    if (T > 0) {
-      KScope ks(st, F_COMMIT);
-      k_commit<<<grid_for(T, 256), 256, 0, st>>>(ca);
-      ++c.launches;
-    }
-    // member relayout; K = total kept (rank[T], T from host) published on the way
-    DBuf& old_ids = X.mem_flip ? X.mem_b : X.mem_a;
-    DBuf& new_ids = X.mem_flip ? X.mem_a : X.mem_b;
-    k_node_sizes<<<grid_for(std::max(n, 1), 256), 256, 0, st>>>(n, X.mem_cnt.as<int32_t>(), X.new_cnt.as<int32_t>(),
-                                                                 node_sz.as<int32_t>(), S,
-                                                                 X.cand_rank.as<int64_t>() + T, d_K);
-    exclusive_scan<int32_t>(node_sz.as<int32_t>(), off2.as<int64_t>(), n, stmp.p, st, &c.launches);
-    k_relayout<<<grid_for(static_cast<int64_t>(n) * 32, 256), 256, 0, st>>>(
-        n, X.mem_off.as<int64_t>(), X.mem_cnt.as<int32_t>(), old_ids.as<int32_t>(), off2.as<int64_t>(),
-        new_ids.as<int32_t>());
-    c.launches += 2;
-    if (T > 0) {
-      k_place_new<<<grid_for(T, 256), 256, 0, st>>>(d_K, S, X.head.as<int32_t>(), off2.as<int64_t>(),
-                                                      X.mem_cnt.as<int32_t>(), X.new_slot.as<int32_t>(),
-                                                      new_ids.as<int32_t>());
-      const unsigned gd = static_cast<unsigned>(std::min<int64_t>(std::max<int64_t>(T, 1), 148 * 16));
-      KScope ks(st, F_DOM);
-      k_dom<<<gd, 128, 0, st>>>(S, X.touched.as<int32_t>(), off2.as<int64_t>(), X.mem_cnt.as<int32_t>(),
-                                X.new_cnt.as<int32_t>(), new_ids.as<int32_t>(), X.cost.as<double>(),
-                                X.cp.as<double>(), X.flags.as<uint8_t>(), X.drop.as<uint8_t>(),
-                                X.surv.as<uint8_t>(), X.fpos.as<int32_t>(), S);
+      if (dbg_coop) {
+        unsigned long long ts[32];
+        c.d2h(ts, stamps.p, sizeof(ts));
+        c.sync();
+        std::fprintf(stderr, "[coop] T=%lld", (long long)T);
+        for (int q = 1; q < 16; ++q) std::fprintf(stderr, " %.1f", (ts[q] - ts[q - 1]) * 1e-3);
+        std::fprintf(stderr, "\n");
+      }
+      swap_buf(X.mem_off, off2);  // new offsets become current
+      X.mem_flip = !X.mem_flip;
+      X.pool_flip = !X.pool_flip;
+    } else {
+      if (T > 0) {
+        X.task_grp.ensure(al((T + 1) * 4));
+        k_task_map<<<grid_for(h.G * 32, 256), 256, 0, st>>>(d_G, X.task_off.as<int64_t>(), X.task_grp.as<int32_t>());
+        ++c.launches;
+        ExpandArgs ea{X.group.as<int32_t>(), X.task_off.as<int64_t>(), X.task_grp.as<int32_t>(), d_G, d_T,
+                      G.row_ptr.as<int64_t>(),
+                      G.e_to.as<int32_t>(), G.e_cost.as<double>(), G.e_nsteps.as<int32_t>(), G.wp_off.as<int64_t>(),
+                      G.hs_off.as<int64_t>(), G.hs_cnt.as<int32_t>(), G.hs_pk.as<double>(),
+                      X.head.as<int32_t>(),
+                      X.cost.as<double>(), X.t_end.as<int32_t>(), X.mask.as<uint64_t>(), c.bank.as<double>(), N,
+                      c.bank_horizon, W, prm.alpha_max, X.cand_keep.as<uint8_t>(), X.cand_head.as<int32_t>(),
+                      X.cand_src.as<int32_t>(), X.cand_tend.as<int32_t>(), X.cand_cost.as<double>(),
+                      X.cand_cp.as<double>(), X.cand_mask.as<uint64_t>(), S};
+        const unsigned grid = grid_for(T * 32, 256);
+        KScope ks(st, F_EXPAND);
+        dispatch_dw(G.dw, [&]<int DW>() {
+          switch (ch) {
+            case 1: k_expand<DW, 1><<<grid, 256, 0, st>>>(ea); break;
+            case 2: k_expand<DW, 2><<<grid, 256, 0, st>>>(ea); break;
+            case 4: k_expand<DW, 4><<<grid, 256, 0, st>>>(ea); break;
+            case 8: k_expand<DW, 8><<<grid, 256, 0, st>>>(ea); break;
+            default: k_expand<DW, 16><<<grid, 256, 0, st>>>(ea); break;
+          }
+        });
+        ++c.launches;
+        PUMP_CUDA(cudaGetLastError());
+      }
+      exclusive_scan<uint8_t>(X.cand_keep.as<uint8_t>(), X.cand_rank.as<int64_t>(), T, stmp.p, st, &c.launches, d_T);
+      if (T == 0) PUMP_CUDA(cudaMemsetAsync(X.cand_rank.p, 0, 8, st));
+      CommitArgs ca{d_T, X.cand_keep.as<uint8_t>(), X.cand_rank.as<int64_t>(), X.cand_head.as<int32_t>(),
+                    X.cand_src.as<int32_t>(), X.cand_tend.as<int32_t>(), X.cand_cost.as<double>(),
+                    X.cand_cp.as<double>(), X.cand_mask.as<uint64_t>(), W, width, prm.alpha_min,
+                    X.is_goal.as<uint8_t>(), X.head.as<int32_t>(), X.parent.as<int32_t>(), X.cost.as<double>(),
+                    X.cp.as<double>(), X.t_end.as<int32_t>(), X.mask.as<uint64_t>(), X.bucket.as<int32_t>(),
+                    X.flags.as<uint8_t>(), X.new_cnt.as<int32_t>(), X.new_slot.as<int32_t>(),
+                    X.touched.as<int32_t>(), S};
+      if (T > 0) {
+        KScope ks(st, F_COMMIT);
+        k_commit<<<grid_for(T, 256), 256, 0, st>>>(ca);
+        ++c.launches;
+      }
+      // member relayout; K = total kept (rank[T], T from host) published on the way
+      DBuf& old_ids = X.mem_flip ? X.mem_b : X.mem_a;
+      DBuf& new_ids = X.mem_flip ? X.mem_a : X.mem_b;
+      k_node_sizes<<<grid_for(std::max(n, 1), 256), 256, 0, st>>>(n, X.mem_cnt.as<int32_t>(), X.new_cnt.as<int32_t>(),
+                                                                   node_sz.as<int32_t>(), S,
+                                                                   X.cand_rank.as<int64_t>() + T, d_K);
+      exclusive_scan<int32_t>(node_sz.as<int32_t>(), off2.as<int64_t>(), n, stmp.p, st, &c.launches);
+      k_relayout<<<grid_for(static_cast<int64_t>(n) * 32, 256), 256, 0, st>>>(
+          n, X.mem_off.as<int64_t>(), X.mem_cnt.as<int32_t>(), old_ids.as<int32_t>(), off2.as<int64_t>(),
+          new_ids.as<int32_t>());
       c.launches += 2;
-    }
-    swap_buf(X.mem_off, off2);  // new offsets become current
-    X.mem_flip = !X.mem_flip;
-    // surviving newcomers -> open pool in id order
-    exclusive_scan<uint8_t>(X.surv.as<uint8_t>(), spos.as<int64_t>(), std::max<int64_t>(T, 1), stmp.p, st,
-                            &c.launches, d_K);
-    DBuf& pool_cur = X.pool_flip ? X.pool_b : X.pool_a;
-    DBuf& pool_nxt = X.pool_flip ? X.pool_a : X.pool_b;
-    if (T > 0) {
-      k_pool_append<<<grid_for(T, 256), 256, 0, st>>>(d_K, S, X.surv.as<uint8_t>(), spos.as<int64_t>(),
-                                                        X.bucket.as<int32_t>(), X.flags.as<uint8_t>(),
-                                                        pool_cur.as<int32_t>(), S);
+      if (T > 0) {
+        k_place_new<<<grid_for(T, 256), 256, 0, st>>>(d_K, S, X.head.as<int32_t>(), off2.as<int64_t>(),
+                                                        X.mem_cnt.as<int32_t>(), X.new_slot.as<int32_t>(),
+                                                        new_ids.as<int32_t>());
+        const unsigned gd = static_cast<unsigned>(std::min<int64_t>(std::max<int64_t>(T, 1), 148 * 16));
+        KScope ks(st, F_DOM);
+        k_dom<<<gd, 128, 0, st>>>(S, X.touched.as<int32_t>(), off2.as<int64_t>(), X.mem_cnt.as<int32_t>(),
+                                  X.new_cnt.as<int32_t>(), new_ids.as<int32_t>(), X.cost.as<double>(),
+                                  X.cp.as<double>(), X.flags.as<uint8_t>(), X.drop.as<uint8_t>(),
+                                  X.surv.as<uint8_t>(), X.fpos.as<int32_t>(), S);
+        c.launches += 2;
+      }
+      swap_buf(X.mem_off, off2);  // new offsets become current
+      X.mem_flip = !X.mem_flip;
+      // surviving newcomers -> open pool in id order
+      exclusive_scan<uint8_t>(X.surv.as<uint8_t>(), spos.as<int64_t>(), std::max<int64_t>(T, 1), stmp.p, st,
+                              &c.launches, d_K);
+      DBuf& pool_cur = X.pool_flip ? X.pool_b : X.pool_a;
+      DBuf& pool_nxt = X.pool_flip ? X.pool_a : X.pool_b;
+      if (T > 0) {
+        k_pool_append<<<grid_for(T, 256), 256, 0, st>>>(d_K, S, X.surv.as<uint8_t>(), spos.as<int64_t>(),
+                                                          X.bucket.as<int32_t>(), X.flags.as<uint8_t>(),
+                                                          pool_cur.as<int32_t>(), S);
+        ++c.launches;
+      }
+      // next group
+      const int64_t pool_ub = h.pool_n + T + 1;
+      k_pool_min<<<grid_for(pool_ub, 256), 256, 0, st>>>(S, d_K, spos.as<int64_t>(), pool_cur.as<int32_t>(),
+                                                           X.flags.as<uint8_t>(), X.bucket.as<int32_t>(), S);
+      k_round_i<<<1, 1, 0, st>>>(S, d_K, spos.as<int64_t>(), d_pool_n, d_limits);
+      c.launches += 2;
+      DBuf& keys = c.buf("x_sel_keys", al((pool_ub + 1) * 4));
+      DBuf& stay = c.buf("x_sel_stay", al(pool_ub + 1));
+      DBuf& stay_pos = c.buf("x_stay_pos", al((pool_ub + 2) * 8));
+      // Distinct selection keys this round: the group takes buckets in
+      // [min_bucket, min(i, max_bucket)].  Costs only grow along a plan, so the
+      // new min_bucket >= the previous one, and i = max(i_prev + 1, min_bucket):
+      // at most i_prev + 2 - min_bucket_prev keys (1 when i jumps to min_bucket).
+      // Within 512 the stable multisplit needs one radix pass instead of two;
+      // k_select flags a violated bound (never expected) as a device error.
+      int64_t n_keys = 1 << 18;
+      if (h.min_bucket != LLONG_MAX && h.i + 2 - h.min_bucket <= 512) n_keys = std::max<int64_t>(1, h.i + 2 - h.min_bucket);
+      k_select<<<grid_for(pool_ub, 256), 256, 0, st>>>(d_pool_n, d_limits, pool_cur.as<int32_t>(),
+                                                         X.flags.as<uint8_t>(), X.bucket.as<int32_t>(),
+                                                         keys.as<int32_t>(), stay.as<uint8_t>(), n_keys, S);
       ++c.launches;
+      DBuf& stmp2 = c.buf("x_scan_tmp2", scan_temp_bytes(pool_ub + 16));
+      exclusive_scan<uint8_t>(stay.as<uint8_t>(), stay_pos.as<int64_t>(), pool_ub, stmp2.p, st, &c.launches,
+                              d_pool_n);
+      k_pool_compact<<<grid_for(pool_ub, 256), 256, 0, st>>>(d_pool_n, pool_cur.as<int32_t>(), stay.as<uint8_t>(),
+                                                               stay_pos.as<int64_t>(), pool_nxt.as<int32_t>());
+      ++c.launches;
+      X.group.ensure(al((pool_ub + 1) * 4));
+      DBuf& mtmp = c.buf("x_ms_tmp", multisplit_temp_bytes(pool_ub, 1 << 18));
+      stable_multisplit(keys.as<int32_t>(), pool_cur.as<int32_t>(), pool_ub, static_cast<int>(n_keys), X.group.as<int32_t>(), d_G,
+                        mtmp.p, st, &c.launches, d_pool_n);
+      DBuf& deg = c.buf("x_deg", al((pool_ub + 1) * 4));
+      X.task_off.ensure(al((pool_ub + 2) * 8));
+      k_group_post<<<grid_for(pool_ub, 256), 256, 0, st>>>(d_G, X.group.as<int32_t>(), X.head.as<int32_t>(),
+                                                             X.cost.as<double>(), G.row_ptr.as<int64_t>(),
+                                                             X.flags.as<uint8_t>(), deg.as<int32_t>(), S);
+      ++c.launches;
+      DBuf& stmp3 = c.buf("x_scan_tmp3", scan_temp_bytes(pool_ub + 16));
+      exclusive_scan<int32_t>(deg.as<int32_t>(), X.task_off.as<int64_t>(), pool_ub, stmp3.p, st, &c.launches, d_G);
+      k_group_final<<<1, 1, 0, st>>>(S, d_G, X.task_off.as<int64_t>(), stay_pos.as<int64_t>(), d_pool_n, d_T);
+      ++c.launches;
+      X.pool_flip = !X.pool_flip;
+      PUMP_CUDA(cudaGetLastError());
     }
-    // next group
-    const int64_t pool_ub = h.pool_n + T + 1;
-    k_pool_min<<<grid_for(pool_ub, 256), 256, 0, st>>>(S, d_K, spos.as<int64_t>(), pool_cur.as<int32_t>(),
-                                                         X.flags.as<uint8_t>(), X.bucket.as<int32_t>(), S);
-    k_round_i<<<1, 1, 0, st>>>(S, d_K, spos.as<int64_t>(), d_pool_n, d_limits);
-    c.launches += 2;
-    DBuf& keys = c.buf("x_sel_keys", al((pool_ub + 1) * 4));
-    DBuf& stay = c.buf("x_sel_stay", al(pool_ub + 1));
-    DBuf& stay_pos = c.buf("x_stay_pos", al((pool_ub + 2) * 8));
-    // Distinct selection keys this round: the group takes buckets in
-    // [min_bucket, min(i, max_bucket)].  Costs only grow along a plan, so the
-    // new min_bucket >= the previous one, and i = max(i_prev + 1, min_bucket):
-    // at most i_prev + 2 - min_bucket_prev keys (1 when i jumps to min_bucket).
-    // Within 512 the stable multisplit needs one radix pass instead of two;
-    // k_select flags a violated bound (never expected) as a device error.
-    int64_t n_keys = 1 << 18;
-    if (h.min_bucket != LLONG_MAX && h.i + 2 - h.min_bucket <= 512) n_keys = std::max<int64_t>(1, h.i + 2 - h.min_bucket);
-    k_select<<<grid_for(pool_ub, 256), 256, 0, st>>>(d_pool_n, d_limits, pool_cur.as<int32_t>(),
-                                                       X.flags.as<uint8_t>(), X.bucket.as<int32_t>(),
-                                                       keys.as<int32_t>(), stay.as<uint8_t>(), n_keys, S);
-    ++c.launches;
-    DBuf& stmp2 = c.buf("x_scan_tmp2", scan_temp_bytes(pool_ub + 16));
-    exclusive_scan<uint8_t>(stay.as<uint8_t>(), stay_pos.as<int64_t>(), pool_ub, stmp2.p, st, &c.launches,
-                            d_pool_n);
-    k_pool_compact<<<grid_for(pool_ub, 256), 256, 0, st>>>(d_pool_n, pool_cur.as<int32_t>(), stay.as<uint8_t>(),
-                                                             stay_pos.as<int64_t>(), pool_nxt.as<int32_t>());
-    ++c.launches;
-    X.group.ensure(al((pool_ub + 1) * 4));
-    DBuf& mtmp = c.buf("x_ms_tmp", multisplit_temp_bytes(pool_ub, 1 << 18));
-    stable_multisplit(keys.as<int32_t>(), pool_cur.as<int32_t>(), pool_ub, static_cast<int>(n_keys), X.group.as<int32_t>(), d_G,
-                      mtmp.p, st, &c.launches, d_pool_n);
-    DBuf& deg = c.buf("x_deg", al((pool_ub + 1) * 4));
-    X.task_off.ensure(al((pool_ub + 2) * 8));
-    k_group_post<<<grid_for(pool_ub, 256), 256, 0, st>>>(d_G, X.group.as<int32_t>(), X.head.as<int32_t>(),
-                                                           X.cost.as<double>(), G.row_ptr.as<int64_t>(),
-                                                           X.flags.as<uint8_t>(), deg.as<int32_t>(), S);
-    ++c.launches;
-    DBuf& stmp3 = c.buf("x_scan_tmp3", scan_temp_bytes(pool_ub + 16));
-    exclusive_scan<int32_t>(deg.as<int32_t>(), X.task_off.as<int64_t>(), pool_ub, stmp3.p, st, &c.launches, d_G);
-    k_group_final<<<1, 1, 0, st>>>(S, d_G, X.task_off.as<int64_t>(), stay_pos.as<int64_t>(), d_pool_n, d_T);
-    ++c.launches;
-    X.pool_flip = !X.pool_flip;
-    PUMP_CUDA(cudaGetLastError());
     c.d2h(X.status_h, S, sizeof(ExploreStatus));
     c.sync();
     h = *X.status_h;
