@@ -461,6 +461,106 @@ __device__ void dom_node(const DomArgs& A, DomShared& sh, int64_t b, int64_t P0)
   }
 }
 
+// The same RemoveDominated steps for a node of <= kDomWarpCap members, one
+// warp per node (the cooperative round's dom phase: thousands of small
+// nodes, so a warp each keeps many in flight); members staged per warp.
+constexpr int kDomWarpCap = 128;
+struct DomWarpShared {
+  int32_t id[kDomWarpCap];
+  double c[kDomWarpCap], p[kDomWarpCap];
+  uint8_t dr[kDomWarpCap];
+};
+
+__device__ void dom_node_warp(const DomArgs& A, DomWarpShared& sh, int v, int64_t P0, int lane) {
+  int32_t* ids = A.ids;
+  const int64_t base = A.new_off[v];
+  const int m_old = A.mem_cnt[v];
+  const int m_new = A.new_cnt[v];
+  const int m = m_old + m_new;
+  for (int x = lane; x < m; x += 32) {
+    const int id = ids[base + x];
+    sh.id[x] = id;
+    sh.c[x] = A.cost[id];
+    sh.p[x] = A.cp[id];
+  }
+  __syncwarp();
+  // (1) drop newcomers dominated by any member (old or new)
+  unsigned n_drop = 0;
+  for (int qi = lane; qi < m_new; qi += 32) {
+    const int q = sh.id[m_old + qi];
+    const double qc = sh.c[m_old + qi], qp = sh.p[m_old + qi];
+    bool d = false;
+    for (int x = 0; x < m && !d; ++x) d = (qc > sh.c[x]) && (qp >= sh.p[x]);
+    A.drop[q - P0] = d ? 1 : 0;
+    A.surv[q - P0] = d ? 0 : 1;
+    sh.dr[m_old + qi] = d ? 1 : 0;
+    n_drop += d ? 1u : 0u;
+  }
+  __syncwarp();
+  // (2) evict old members (not the root) a surviving newcomer dominates
+  unsigned n_ev = 0, n_ev_open = 0;
+  for (int pi = lane; pi < m_old; pi += 32) {
+    const int p = sh.id[pi];
+    if (p == 0) continue;
+    const double pc = sh.c[pi], pp = sh.p[pi];
+    bool ev = false;
+    for (int qi = 0; qi < m_new && !ev; ++qi) {
+      if (sh.dr[m_old + qi]) continue;
+      ev = (pc > sh.c[m_old + qi]) && (pp >= sh.p[m_old + qi]);
+    }
+    if (ev) {
+      ++n_ev;
+      if (A.flags[p] & kOpen) {
+        A.flags[p] &= static_cast<uint8_t>(~kOpen);
+        ++n_ev_open;
+      }
+      sh.id[pi] = -1 - p;
+    }
+  }
+  __syncwarp();
+  // (3) surviving newcomers ranked by id; old survivors compacted in order
+  unsigned n_new_surv = 0;
+  for (int qi = lane; qi < m_new; qi += 32) {
+    if (sh.dr[m_old + qi]) continue;
+    const int q = sh.id[m_old + qi];
+    int r = 0;
+    for (int xi = 0; xi < m_new; ++xi) r += (!sh.dr[m_old + xi] && sh.id[m_old + xi] < q) ? 1 : 0;
+    A.fpos[q - P0] = r;
+    ++n_new_surv;
+  }
+  int w = 0;
+  const unsigned lt = (1u << lane) - 1u;
+  for (int c0 = 0; c0 < m_old; c0 += 32) {
+    const int pi = c0 + lane;
+    const int p = pi < m_old ? sh.id[pi] : -1;
+    const unsigned keepm = __ballot_sync(0xffffffffu, p >= 0);
+    if (p >= 0) ids[base + w + __popc(keepm & lt)] = p;
+    w += __popc(keepm);
+  }
+  __syncwarp();
+  // (4) surviving newcomers after the old survivors, in id order
+  for (int qi = lane; qi < m_new; qi += 32) {
+    if (sh.dr[m_old + qi]) continue;
+    const int q = sh.id[m_old + qi];
+    ids[base + w + A.fpos[q - P0]] = q;
+  }
+  n_drop = __reduce_add_sync(0xffffffffu, n_drop);
+  n_ev = __reduce_add_sync(0xffffffffu, n_ev);
+  n_ev_open = __reduce_add_sync(0xffffffffu, n_ev_open);
+  n_new_surv = __reduce_add_sync(0xffffffffu, n_new_surv);
+  if (lane == 0) {
+    // new_cnt first: the block pass (k_round_tail) reads mem_cnt + new_cnt of
+    // every touched node concurrently to pick the big ones; with this order it
+    // never sees a sum above the node's original size
+    A.new_cnt[v] = 0;
+    __threadfence();
+    A.mem_cnt[v] = w + static_cast<int>(n_new_surv);
+    atomicAdd(reinterpret_cast<unsigned long long*>(&A.stw->removed), static_cast<unsigned long long>(n_drop + n_ev));
+    atomicAdd(reinterpret_cast<unsigned long long*>(&A.stw->evicted_open), static_cast<unsigned long long>(n_ev_open));
+  }
+  __syncwarp();
+}
+
 // RemoveDominated at one touched node per CTA (planner.hpp:200-238).  The
 // node's members (ids, cost, cp) are first staged in shared memory with one
 // batch of independent loads, so the O(m_new * m) dominance scans read shared
@@ -708,8 +808,15 @@ struct CoopArgs {
 };
 constexpr int kCoopKeys = 512;
 
+union DomSmem {  // the warp pass and the block pass of the dom phase run one after the other
+  DomShared blk;
+  DomWarpShared warp[kCoopBlock / 32];
+};
+
 __global__ void __launch_bounds__(kCoopBlock, 2) k_round_tail(const CoopArgs A) {
-  __shared__ DomShared dsh;
+  __shared__ DomSmem dsm;
+  DomShared& dsh = dsm.blk;
+  DomWarpShared* wsh = dsm.warp;
   __shared__ int s_hist[kCoopKeys];
   __shared__ int64_t s_run[kCoopKeys];
   __shared__ int64_t red[kCoopBlock / 32];
@@ -773,7 +880,17 @@ __global__ void __launch_bounds__(kCoopBlock, 2) k_round_tail(const CoopArgs A) 
     const DomArgs D{A.touched, A.off2, A.mem_cnt, A.new_cnt, A.new_ids, A.cm.cost, A.cm.cp, A.cm.flags,
                     A.drop, A.surv, A.fpos, S};
     const int64_t nt = S->touched;
-    for (int64_t b = blockIdx.x; b < nt; b += nb) dom_node(D, dsh, b, P0);
+    // small nodes: a warp each; then nodes over kDomWarpCap: a block each
+    for (int64_t b = gwarp; b < nt; b += gwarps) {
+      const int v = A.touched[b];
+      if (A.mem_cnt[v] + A.new_cnt[v] <= kDomWarpCap) dom_node_warp(D, wsh[threadIdx.x >> 5], v, P0, lane);
+    }
+    __syncthreads();  // the block pass reuses the warps' shared memory
+    for (int64_t b = blockIdx.x; b < nt; b += nb) {
+      const int v = A.touched[b];
+      const bool big = A.mem_cnt[v] + A.new_cnt[v] > kDomWarpCap;  // block-uniform
+      if (big) dom_node(D, dsh, b, P0);
+    }
   }
   grid_sync(A.bar);
   STAMP();
