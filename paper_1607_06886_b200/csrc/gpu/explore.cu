@@ -736,27 +736,54 @@ __device__ __forceinline__ int64_t block_excl(int64_t v, int64_t* red, int64_t* 
 }
 
 // Grid-wide exclusive scan of val(i) for i < n into out[0..n] (out[n] =
-// total); post(i, excl, v) runs for every i in the second pass.  val(i, pass)
-// is evaluated twice (pass 0: reduce, pass 1: scan).  One grid barrier inside;
-// the caller syncs before anyone reads out[] of another block or reuses blk.
+// total, written by the last block); post(i, excl, v) runs for every i.
+// val(i, pass) is evaluated twice (pass 0: block reduce, pass 1: scan).
+// Decoupled look-back across the co-resident blocks instead of a barrier:
+// block b publishes its aggregate in status[b] tagged with the scan's epoch
+// (every block writes its entry in every scan, so an entry with the current
+// epoch is this scan's), then sums predecessors back to the nearest
+// inclusive prefix.  The caller syncs the grid before reading out[] of
+// other blocks.  Returns the total on the last block only (others: -1).
 template <class Val, class Post>
-__device__ int64_t coop_scan(int64_t n, Val val, Post post, int64_t* out, int64_t* blk, GridBar* bar, int64_t* red) {
+__device__ int64_t coop_scan(int64_t n, Val val, Post post, int64_t* out, unsigned long long* status, unsigned epoch,
+                             int64_t* red, int64_t* s_pre) {
+  constexpr unsigned long long kAgg = 1ull << 46, kInc = 2ull << 46, kVal = (1ull << 46) - 1;
+  const unsigned long long tag = static_cast<unsigned long long>(epoch & 0xffffu) << 48;
   const int64_t nb = gridDim.x, b = blockIdx.x;
   const int64_t chunk = (n + nb - 1) / nb;
   const int64_t lo = min(n, b * chunk), hi = min(n, lo + chunk);
   int64_t s = 0;
   for (int64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) s += val(i, 0);
   s = block_sum(s, red);
-  if (threadIdx.x == 0) blk[b] = s;
-  grid_sync(bar);
-  int64_t pre = 0, tot = 0;
-  for (int64_t c = threadIdx.x; c < nb; c += blockDim.x) {
-    const int64_t x = blk[c];
-    tot += x;
-    pre += c < b ? x : 0;
+  volatile unsigned long long* vs = status;
+  if (threadIdx.x < 32) {
+    const int lane = threadIdx.x;
+    int64_t pre = 0;
+    if (b == 0) {
+      if (lane == 0) vs[0] = tag | kInc | static_cast<unsigned long long>(s);
+    } else {
+      if (lane == 0) vs[b] = tag | kAgg | static_cast<unsigned long long>(s);
+      int64_t j = b - 1 - lane;
+      while (true) {
+        unsigned long long w = j >= 0 ? vs[j] : (tag | kInc);
+        auto ready = [&](unsigned long long x) { return (x & (0xffffull << 48)) == tag && (x & (3ull << 46)) != 0; };
+        while (__any_sync(0xffffffffu, !ready(w))) {
+          if (!ready(w)) w = vs[j];
+        }
+        const unsigned incm = __ballot_sync(0xffffffffu, (w & (3ull << 46)) == kInc);
+        const int stop = incm ? __ffs(incm) - 1 : 31;
+        int64_t v = lane <= stop ? static_cast<int64_t>(w & kVal) : 0;
+        pre += warp_sum(v);
+        if (incm) break;
+        j -= 32;
+      }
+      if (lane == 0) vs[b] = tag | kInc | static_cast<unsigned long long>(pre + s);
+    }
+    if (lane == 0) *s_pre = pre;
   }
-  pre = block_sum(pre, red);
-  tot = block_sum(tot, red);
+  __syncthreads();
+  int64_t pre = *s_pre;
+  const int64_t total = pre + s;  // meaningful on the last block
   for (int64_t base = lo; base < hi; base += blockDim.x) {
     const int64_t i = base + threadIdx.x;
     const int64_t v = i < hi ? val(i, 1) : 0;
@@ -768,8 +795,11 @@ __device__ int64_t coop_scan(int64_t n, Val val, Post post, int64_t* out, int64_
     }
     pre += tile;
   }
-  if (b == nb - 1 && threadIdx.x == 0) out[n] = tot;
-  return tot;
+  if (b == nb - 1) {
+    if (threadIdx.x == 0) out[n] = total;
+    return total;
+  }
+  return -1;
 }
 
 struct CoopArgs {
@@ -777,7 +807,8 @@ struct CoopArgs {
   CommitArgs cm;
   int n;
   GridBar* bar;
-  int64_t* blk;  // gridDim.x + 1 scan partials
+  unsigned long long* scan_status;  // gridDim.x look-back words
+  unsigned epoch;                   // per launch (tags the scans' status words)
   ExploreStatus* S;
   int64_t *d_K, *d_pool_n, *d_G, *d_T, *limits;
   // members: old layout (mem_off, old_ids) -> new layout (off2, new_ids)
@@ -820,6 +851,7 @@ __global__ void __launch_bounds__(kCoopBlock, 2) k_round_tail(const CoopArgs A) 
   __shared__ int s_hist[kCoopKeys];
   __shared__ int64_t s_run[kCoopKeys];
   __shared__ int64_t red[kCoopBlock / 32];
+  __shared__ int64_t s_pre;
   ExploreStatus* S = A.S;
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int64_t gtid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -843,24 +875,27 @@ __global__ void __launch_bounds__(kCoopBlock, 2) k_round_tail(const CoopArgs A) 
   // keep -> rank, commit as plan n_plans + rank
   const int64_t P0 = S->n_plans;
   const uint8_t* keep = A.cm.keep;
-  const int64_t K = coop_scan(
+  unsigned ep = A.epoch * 8u;
+  int64_t* rank = const_cast<int64_t*>(A.cm.rank);
+  coop_scan(
       T, [&](int64_t i, int) -> int64_t { return keep[i]; },
       [&](int64_t i, int64_t ex, int64_t v) {
         if (v) commit_one(A.cm, i, ex);
       },
-      A.cm.rank == nullptr ? nullptr : const_cast<int64_t*>(A.cm.rank), A.blk, A.bar, red);
+      rank, A.scan_status, ep++, red, &s_pre);
+  grid_sync(A.bar);
+  const int64_t K = rank[T];
   if (gtid == 0) {
     S->K = K;
     *A.d_K = K;
     S->min_bucket = LLONG_MAX;
   }
-  grid_sync(A.bar);
   STAMP();
   // member relayout: new offsets, old members, newcomers at their slots
   const int n = A.n;
   coop_scan(
       n, [&](int64_t v, int) -> int64_t { return A.mem_cnt[v] + A.new_cnt[v]; }, [](int64_t, int64_t, int64_t) {},
-      A.off2, A.blk, A.bar, red);
+      A.off2, A.scan_status, ep++, red, &s_pre);
   grid_sync(A.bar);
   STAMP();
   for (int64_t v = gwarp; v < n; v += gwarps) {
@@ -898,7 +933,7 @@ __global__ void __launch_bounds__(kCoopBlock, 2) k_round_tail(const CoopArgs A) 
   const int64_t pool_old = S->pool_n;
   const int32_t* bucket = A.cm.bucket;
   uint8_t* flags = A.cm.flags;
-  const int64_t NS = coop_scan(
+  coop_scan(
       K, [&](int64_t r, int) -> int64_t { return A.surv[r]; },
       [&](int64_t r, int64_t ex, int64_t v) {
         if (v) {
@@ -909,7 +944,7 @@ __global__ void __launch_bounds__(kCoopBlock, 2) k_round_tail(const CoopArgs A) 
           atomicMin(&S->min_bucket, static_cast<long long>(bucket[id]));
         }
       },
-      A.spos, A.blk, A.bar, red);
+      A.spos, A.scan_status, ep++, red, &s_pre);
   for (int64_t x = gtid; x < pool_old; x += gthreads) {
     const int id = A.pool_cur[x];
     if (flags[id] & kOpen) atomicMin(&S->min_bucket, static_cast<long long>(bucket[id]));
@@ -917,6 +952,7 @@ __global__ void __launch_bounds__(kCoopBlock, 2) k_round_tail(const CoopArgs A) 
   grid_sync(A.bar);
   STAMP();
   // end-of-round bookkeeping and the next threshold (k_round_i)
+  const int64_t NS = A.spos[K];
   if (gtid == 0) {
     S->n_surv = NS;
     S->pool_n += NS;
@@ -940,7 +976,7 @@ __global__ void __launch_bounds__(kCoopBlock, 2) k_round_tail(const CoopArgs A) 
   // bucket selection (k_select) fused into the stay scan; stayers compacted
   const int64_t m = *A.d_pool_n;
   const int64_t lim0 = A.limits[0], lim1 = A.limits[1];
-  const int64_t stay_n = coop_scan(
+  coop_scan(
       m,
       [&](int64_t x, int pass) -> int64_t {
         const int id = A.pool_cur[x];
@@ -957,8 +993,9 @@ __global__ void __launch_bounds__(kCoopBlock, 2) k_round_tail(const CoopArgs A) 
       [&](int64_t x, int64_t ex, int64_t v) {
         if (v) A.pool_nxt[ex] = A.pool_cur[x];
       },
-      A.stay_pos, A.blk, A.bar, red);
+      A.stay_pos, A.scan_status, ep++, red, &s_pre);
   grid_sync(A.bar);
+  const int64_t stay_n = A.stay_pos[m];
   STAMP();
   // stable multisplit by key (one radix pass, keys < n_keys <= 512):
   // per-block histograms over contiguous chunks, key-major scan, ordered scatter
@@ -975,10 +1012,11 @@ __global__ void __launch_bounds__(kCoopBlock, 2) k_round_tail(const CoopArgs A) 
   for (int k = threadIdx.x; k < nk; k += blockDim.x) A.ms_counts[static_cast<int64_t>(k) * nb + blockIdx.x] = s_hist[k];
   grid_sync(A.bar);
   STAMP();
-  const int64_t Gn = coop_scan(
+  coop_scan(
       static_cast<int64_t>(nk) * nb, [&](int64_t i, int) -> int64_t { return A.ms_counts[i]; },
-      [](int64_t, int64_t, int64_t) {}, A.ms_offs, A.blk, A.bar, red);
+      [](int64_t, int64_t, int64_t) {}, A.ms_offs, A.scan_status, ep++, red, &s_pre);
   grid_sync(A.bar);
+  const int64_t Gn = A.ms_offs[static_cast<int64_t>(nk) * nb];
   STAMP();
   for (int k = threadIdx.x; k < nk; k += blockDim.x) s_run[k] = A.ms_offs[static_cast<int64_t>(k) * nb + blockIdx.x];
   __syncthreads();
@@ -999,7 +1037,7 @@ __global__ void __launch_bounds__(kCoopBlock, 2) k_round_tail(const CoopArgs A) 
   grid_sync(A.bar);
   STAMP();
   // the new group: close it, its degrees -> task offsets, cheapest cost
-  const int64_t Tn = coop_scan(
+  const int64_t Tn_last = coop_scan(
       Gn,
       [&](int64_t g, int pass) -> int64_t {
         const int id = A.group[g];
@@ -1010,11 +1048,11 @@ __global__ void __launch_bounds__(kCoopBlock, 2) k_round_tail(const CoopArgs A) 
         }
         return A.row_ptr[hv + 1] - A.row_ptr[hv];
       },
-      [](int64_t, int64_t, int64_t) {}, A.task_off, A.blk, A.bar, red);
-  if (gtid == 0) {
+      [](int64_t, int64_t, int64_t) {}, A.task_off, A.scan_status, ep++, red, &s_pre);
+  if (blockIdx.x == gridDim.x - 1 && threadIdx.x == 0) {  // the scan's last block holds the total
     S->G = Gn;
-    S->T = Tn;
-    *A.d_T = Tn;
+    S->T = Tn_last;
+    *A.d_T = Tn_last;
     S->pool_n = stay_n;
   }
   STAMP();
@@ -1169,6 +1207,10 @@ void run_explore_device(DevExplore& X, Ctx& c, const DevGraph& G, const ExploreA
     coop_blocks = coop_attr ? per_sm * sms : 0;
   }
   const bool coop_ok = !legacy_env && coop_blocks > 0;
+  if (coop_ok) {  // look-back status words start untagged
+    DBuf& scan_st = c.buf("x_coop_scan_status", al((coop_blocks + 2) * 8));
+    PUMP_CUDA(cudaMemsetAsync(scan_st.p, 0, (coop_blocks + 2) * 8, st));
+  }
   c.tic();
   for (;;) {
     // loop-top termination (planner.hpp:126-138); h is the status after the
@@ -1215,7 +1257,7 @@ void run_explore_device(DevExplore& X, Ctx& c, const DevGraph& G, const ExploreA
       DBuf& stay_pos = c.buf("x_stay_pos", al((pool_ub + 2) * 8));
       DBuf& msc = c.buf("x_coop_counts", al(static_cast<size_t>(kCoopKeys) * coop_blocks * 4));
       DBuf& mso = c.buf("x_coop_offs", al((static_cast<size_t>(kCoopKeys) * coop_blocks + 2) * 8));
-      DBuf& blk = c.buf("x_coop_blk", al((coop_blocks + 2) * 8));
+      DBuf& scan_st = c.buf("x_coop_scan_status", al((coop_blocks + 2) * 8));
       DBuf& bar = c.buf("x_coop_bar", 256);
       DBuf& old_ids = X.mem_flip ? X.mem_b : X.mem_a;
       DBuf& new_ids = X.mem_flip ? X.mem_a : X.mem_b;
@@ -1240,7 +1282,8 @@ void run_explore_device(DevExplore& X, Ctx& c, const DevGraph& G, const ExploreA
                         X.touched.as<int32_t>(), S};
       A.n = n;
       A.bar = bar.as<GridBar>();
-      A.blk = blk.as<int64_t>();
+      A.scan_status = scan_st.as<unsigned long long>();
+      A.epoch = ++X.coop_epoch;
       A.S = S;
       A.d_K = d_K;
       A.d_pool_n = d_pool_n;

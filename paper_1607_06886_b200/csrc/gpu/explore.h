@@ -27,6 +27,7 @@ struct DevExplore {
   // results
   int64_t n_plans = 0, partial_plans = 0, disc_cp = 0, disc_hor = 0, removed = 0, hs_tests = 0;
   int rounds = 0;
+  unsigned coop_epoch = 0;  // tags the cooperative round's scan status words
   int termination = 0;  // 0 goal_below_alpha_min, 1 frontier_exhausted
   double kernel_ms = 0;
   ~DevExplore();
