@@ -17,6 +17,7 @@
 #include "gpu/dispatch.cuh"
 #include "gpu/explore.h"
 #include "gpu/graph.h"
+#include "gpu/scan.cuh"
 #include "guard.h"
 
 using namespace pumpg;
@@ -487,6 +488,159 @@ static void sample_nodes(const pumpb::Scenario& s, const HostWorld& w, std::vect
   }
 }
 
+// ---- node sampling on the device (sample.hpp:56-89, pump.hpp:184-189):
+// the Halton candidates of a whole index window are drawn and tested in
+// parallel, then the first `samples` free ones are taken in index order (a
+// scan of the free flags), which is exactly the reference's sequential
+// accept loop.  Same arithmetic as halton_state / point_free above.
+static inline size_t al(size_t x) { return (x + 255) & ~size_t(255); }
+
+struct SampleBox {
+  double lo[6], hi[6], ms;     // workspace bounds, max speed
+  double glo[6], ghi[6], gms;  // goal region
+};
+
+__device__ double halton_dev(uint64_t index, int base) {
+  double f = 1.0, r = 0.0;
+  while (index > 0) {
+    f /= base;
+    r += f * (index % base);
+    index /= base;
+  }
+  return r;
+}
+
+template <int DW>
+__global__ void k_halton_cand(SampleBox B, WorldD w, uint64_t idx0, int64_t M, double* __restrict__ cp,
+                              double* __restrict__ cv, uint8_t* __restrict__ fr, uint8_t* __restrict__ ing) {
+  const int64_t x = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (x >= M) return;
+  constexpr int kPrimes[12] = {2, 3, 5, 7, 11, 13, 17, 19, 23, 29, 31, 37};
+  const uint64_t index = idx0 + static_cast<uint64_t>(x);
+  double p[DW], v[DW];
+#pragma unroll
+  for (int k = 0; k < DW; ++k) {
+    const double u = halton_dev(index, kPrimes[k]);
+    p[k] = B.lo[k] + u * (B.hi[k] - B.lo[k]);
+    const double q = halton_dev(index, kPrimes[DW + k]);
+    v[k] = -B.ms + q * 2 * B.ms;
+  }
+  const bool free = point_free<DW>(w, p);
+  bool in = free;
+#pragma unroll
+  for (int k = 0; k < DW; ++k) in = in && !(p[k] < B.glo[k] || p[k] > B.ghi[k]);
+  in = in && sqrt(sqnorm<DW>(v)) <= B.gms;
+#pragma unroll
+  for (int k = 0; k < DW; ++k) {
+    cp[x * DW + k] = p[k];
+    cv[x * DW + k] = v[k];
+  }
+  fr[x] = free ? 1 : 0;
+  ing[x] = in ? 1 : 0;
+}
+
+// take the free candidates ranked below `need` into rows row0 + rank
+__global__ void k_halton_take(int dw, int64_t M, int64_t need, int64_t row0, const int64_t* __restrict__ rank,
+                              const uint8_t* __restrict__ fr, const uint8_t* __restrict__ ing,
+                              const double* __restrict__ cp, const double* __restrict__ cv, double* __restrict__ pos,
+                              double* __restrict__ vel, int* __restrict__ goal_flag) {
+  const int64_t x = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (x >= M || !fr[x]) return;
+  const int64_t r = rank[x];
+  if (r >= need) return;
+  for (int k = 0; k < dw; ++k) {
+    pos[(row0 + r) * dw + k] = cp[x * dw + k];
+    vel[(row0 + r) * dw + k] = cv[x * dw + k];
+  }
+  if (ing[x]) atomicOr(goal_flag, 1);
+}
+
+static void sample_nodes_device(Ctx& c, const pumpb::Scenario& s, const HostWorld& hw, const DevWorld& dwld,
+                                DevGraph& G, std::vector<double>& pos, std::vector<double>& vel) {
+  const int dw = s.workspace_dim();
+  const int64_t need_total = s.samples;
+  const int64_t rows_cap = 1 + need_total + 1;
+  G.pos.ensure(al(rows_cap * dw * 8));
+  G.vel.ensure(al(rows_cap * dw * 8));
+  c.h2d(G.pos.p, s.start_pos.data(), dw * 8);
+  c.h2d(G.vel.p, s.start_vel.data(), dw * 8);
+  SampleBox B{};
+  for (int k = 0; k < dw; ++k) {
+    B.lo[k] = s.workspace.bounds.lo[k];
+    B.hi[k] = s.workspace.bounds.hi[k];
+    B.glo[k] = s.goal.lo[k];
+    B.ghi[k] = s.goal.hi[k];
+  }
+  B.ms = s.max_speed;
+  B.gms = s.goal_max_speed;
+  WorldD wd;
+  wd.n_obs = dwld.n_obs;
+  wd.lo = dwld.d_lo;
+  wd.hi = dwld.d_hi;
+  for (int k = 0; k < 6; ++k) {
+    wd.blo[k] = dwld.blo[k];
+    wd.bhi[k] = dwld.bhi[k];
+  }
+  int64_t got = 0;
+  uint64_t idx0 = 1;
+  int64_t M = need_total + need_total / 2 + 256;
+  DBuf& gflag = c.buf("s_goal_flag", 256);
+  PUMP_CUDA(cudaMemsetAsync(gflag.p, 0, 4, c.stream));
+  while (got < need_total) {
+    DBuf& cp = c.buf("s_cp", al(M * dw * 8));
+    DBuf& cv = c.buf("s_cv", al(M * dw * 8));
+    DBuf& fr = c.buf("s_fr", al(M + 8));
+    DBuf& ing = c.buf("s_ing", al(M + 8));
+    DBuf& rank = c.buf("s_rank", al((M + 2) * 8));
+    DBuf& stmp = c.buf("s_scantmp", scan_temp_bytes(M + 16));
+    dispatch_dw(dw, [&]<int DW>() {
+      k_halton_cand<DW><<<grid_for(M, 128), 128, 0, c.stream>>>(B, wd, idx0, M, cp.as<double>(), cv.as<double>(),
+                                                                fr.as<uint8_t>(), ing.as<uint8_t>());
+    });
+    ++c.launches;
+    exclusive_scan<uint8_t>(fr.as<uint8_t>(), rank.as<int64_t>(), M, stmp.p, c.stream, &c.launches);
+    k_halton_take<<<grid_for(M, 256), 256, 0, c.stream>>>(dw, M, need_total - got, 1 + got, rank.as<int64_t>(),
+                                                          fr.as<uint8_t>(), ing.as<uint8_t>(), cp.as<double>(),
+                                                          cv.as<double>(), G.pos.as<double>(), G.vel.as<double>(),
+                                                          gflag.as<int>());
+    ++c.launches;
+    PUMP_CUDA(cudaGetLastError());
+    int64_t acc = 0;
+    c.d2h(&acc, rank.as<int64_t>() + M, 8);
+    c.sync();
+    got += std::min(acc, need_total - got);
+    idx0 += static_cast<uint64_t>(M);
+    M = 2 * (need_total - got) + 256;
+  }
+  int have_goal = 0;
+  const int64_t n = 1 + need_total;
+  pos.resize(n * dw);
+  vel.resize(n * dw);
+  c.d2h(&have_goal, gflag.p, 4);
+  c.d2h(pos.data(), G.pos.p, n * dw * 8);
+  c.d2h(vel.data(), G.vel.p, n * dw * 8);
+  c.sync();
+  if (!have_goal) {  // goal centre, else a goal Halton sample (sample.hpp:63-88), on the host
+    double p[6], v[6];
+    for (int k = 0; k < dw; ++k) {
+      p[k] = 0.5 * (s.goal.lo[k] + s.goal.hi[k]);
+      v[k] = 0.0;
+    }
+    bool placed = point_free_h(hw, p);
+    for (uint64_t gi = 1; gi <= 100000 && !placed; ++gi) {
+      halton_state(gi, s.goal.lo.data(), s.goal.hi.data(), dw, s.goal_max_speed, p, v);
+      if (std::sqrt(seq_sqn(v, dw)) > s.goal_max_speed) continue;
+      if (!point_free_h(hw, p)) continue;
+      placed = true;
+    }
+    if (!placed) throw std::runtime_error("sample_free: goal region appears entirely in collision");
+    pos.insert(pos.end(), p, p + dw);
+    vel.insert(vel.end(), v, v + dw);
+    c.h2d(G.pos.as<double>() + n * dw, p, dw * 8);
+    c.h2d(G.vel.as<double>() + n * dw, v, dw * 8);
+  }
+}
+
 static HostWorld host_world(const pumpb::World& sw) {
   HostWorld w;
   w.dw = sw.dim();
@@ -555,10 +709,17 @@ static void run_pump_device(Ctx& c, const pumpb::Scenario& s, const DevGraph* pr
   const DevGraph* graph = prebuilt;
   if (!graph) {
     std::vector<double> pos, vel;
-    sample_nodes(s, hw, pos, vel);
+    static const bool host_sampling = std::getenv("PUMP_HOST_SAMPLING") != nullptr;
+    if (host_sampling)
+      sample_nodes(s, hw, pos, vel);
+    else
+      sample_nodes_device(c, s, hw, dwld, local, pos, vel);
+    if (std::getenv("PUMP_DEBUG_TIMING"))
+      std::fprintf(stderr, "[pump g] %-24s %8.3f ms (from solve start)\n", "sample_nodes",
+                   1e3 * secs(t0, clk::now()));
     const int n = static_cast<int>(pos.size()) / dw;
-    build_graph_device(local, c, n, dw, pos.data(), vel.data(), dwld, r_n, s.dt, eps_cc, s.effective_tau_max(),
-                       scan_ratio(s.effective_tau_max()));
+    build_graph_device(local, c, n, dw, host_sampling ? pos.data() : nullptr, host_sampling ? vel.data() : nullptr,
+                       dwld, r_n, s.dt, eps_cc, s.effective_tau_max(), scan_ratio(s.effective_tau_max()));
     pump_goal g{s.goal.lo.data(), s.goal.hi.data(), s.goal_max_speed};
     local.h_pos = pos;
     local.h_vel = vel;

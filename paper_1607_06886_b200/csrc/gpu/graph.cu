@@ -13,6 +13,10 @@
 //                   (geom.hpp:189-225); run twice (count, then write).
 // Obstacles are staged in shared memory.  All floating point follows the
 // reference's operation order (no FMA: --fmad=false).
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
+
 #include "dispatch.cuh"
 #include "graph.h"
 #include "scan.cuh"
@@ -445,15 +449,24 @@ void build_graph_device(DevGraph& G, Ctx& c, int n, int dw, const double* h_pos,
   if (r_n <= 0) throw std::invalid_argument("build_graph: r_n must be positive");
   if (dt <= 0) throw std::invalid_argument("motion_waypoints: dt must be positive");
   if (w.n_obs > 4096) throw std::invalid_argument("build_graph: more than 4096 obstacles");
+  static const bool dbg_t = std::getenv("PUMP_DEBUG_TIMING") != nullptr;
+  const auto t_start = std::chrono::steady_clock::now();
+  auto mark = [&](const char* what) {
+    if (dbg_t)
+      std::fprintf(stderr, "[pump g] %-24s %8.3f ms\n", what,
+                   1e3 * std::chrono::duration<double>(std::chrono::steady_clock::now() - t_start).count());
+  };
   G.n = n;
   G.dw = dw;
   G.r_n = r_n;
   G.dt = dt;
   cudaStream_t st = c.stream;
-  G.pos.ensure(al(n * dw * 8));
-  G.vel.ensure(al(n * dw * 8));
-  c.h2d(G.pos.p, h_pos, n * dw * 8);
-  c.h2d(G.vel.p, h_vel, n * dw * 8);
+  if (h_pos) {  // else the caller already placed the nodes in G.pos / G.vel (device sampler)
+    G.pos.ensure(al(n * dw * 8));
+    G.vel.ensure(al(n * dw * 8));
+    c.h2d(G.pos.p, h_pos, n * dw * 8);
+    c.h2d(G.vel.p, h_vel, n * dw * 8);
+  }
   GraphArgs ga{n, G.pos.as<double>(), G.vel.as<double>(), r_n, dt, eps_cc, tau_max, ratio};
   const LbGrid lbg = make_lb_grid(r_n);
   WorldD wd;
@@ -482,6 +495,7 @@ void build_graph_device(DevGraph& G, Ctx& c, int n, int dw, const double* h_pos,
     std::vector<int32_t> cnt(n);
     c.d2h(cnt.data(), rcnt.p, n * 4);
     c.sync();
+    mark("pair_filter");
     int max_cnt = 0;
     for (int v = 0; v < n; ++v) max_cnt = std::max(max_cnt, cnt[v]);
     if (max_cnt <= cap) break;
@@ -493,6 +507,7 @@ void build_graph_device(DevGraph& G, Ctx& c, int n, int dw, const double* h_pos,
   int64_t n_surv = 0;
   c.d2h(&n_surv, soff.as<int64_t>() + n, 8);
   c.sync();
+  mark("survivor scan");
   G.n_connect = n_surv;
   DBuf& skeep = c.buf("g_skeep", al(n_surv + 1));
   DBuf& sv = c.buf("g_sv", al((n_surv + 1) * 4));
@@ -515,6 +530,7 @@ void build_graph_device(DevGraph& G, Ctx& c, int n, int dw, const double* h_pos,
   int64_t n_cand = 0;
   c.d2h(&n_cand, cpos.as<int64_t>() + n_surv, 8);
   c.sync();
+  mark("connect");
   G.n_cand = n_cand;
   DBuf& cv = c.buf("g_cv", al((n_cand + 1) * 4));
   DBuf& cuu = c.buf("g_cuu", al((n_cand + 1) * 4));
@@ -552,6 +568,7 @@ void build_graph_device(DevGraph& G, Ctx& c, int n, int dw, const double* h_pos,
   int64_t E = 0;
   c.d2h(&E, eoff.as<int64_t>() + n_cand, 8);
   c.sync();
+  mark("collide");
   G.E = E;
   G.e_from.ensure(al((E + 1) * 4));
   G.e_to.ensure(al((E + 1) * 4));
@@ -580,6 +597,7 @@ void build_graph_device(DevGraph& G, Ctx& c, int n, int dw, const double* h_pos,
   int64_t NW = 0;
   c.d2h(&NW, G.wp_off.as<int64_t>() + E, 8);
   c.sync();
+  mark("emit + waypoint scan");
   G.NW = NW;
   DBuf& err = c.buf("g_err", 256);
   G.hs_off.ensure(al((NW + 2) * 8));
@@ -612,6 +630,7 @@ void build_graph_device(DevGraph& G, Ctx& c, int n, int dw, const double* h_pos,
       c.d2h(&H, ctr.p, 8);
       c.d2h(&herr, err.p, 4);
       c.sync();
+      mark("regions");
       if (herr) throw std::runtime_error("local_convex_region: pruning loop failed to make progress");
       G.H = H;
       if (H <= cap && std::getenv("PUMP_DEBUG_GRAPH"))
