@@ -736,6 +736,26 @@ static void run_pump_device(Ctx& c, const pumpb::Scenario& s, const DevGraph* pr
   DevExplore& X = *c.run_explore;
   const double eta = s.effective_eta();
   ExploreArgs ea{s.alpha / eta, std::min(1.0, eta * s.alpha), s.lambda, r_n};
+  // The certified trajectories are paths of goal-node plans, so the largest
+  // t_end of any plan committed at a goal node bounds their length: grow the
+  // MC table (mc.cu) to it on the low-priority side stream while the
+  // latency-bound wavefront runs.
+  int64_t mr0 = 0, mr1 = s.mc_samples;
+  shard_range(s.mc_samples, c.rank, c.world, &mr0, &mr1);
+  bool side_forked = false;
+  ea.on_round = [&](const ExploreStatus& h) {
+    if (h.max_goal_tend <= 0) return;
+    const int want = static_cast<int>(std::min<int64_t>(s.bank_horizon, h.max_goal_tend));
+    if (c.mc_table.valid && want <= c.mc_table.t_done) return;
+    if (!side_forked) {
+      PUMP_CUDA(cudaEventRecord(c.fork, c.stream));
+      PUMP_CUDA(cudaStreamWaitEvent(c.side, c.fork, 0));
+      side_forked = true;
+    }
+    mc_table_prepare(c.mc_table, L, mr0, mr1, s.seeds.mc, want, c.side, &c.launches);
+    PUMP_CUDA(cudaEventRecord(c.join, c.side));
+    c.mc_join_pending = true;
+  };
   run_explore_device(X, c, *graph, ea);
   auto t2 = clk::now();
   static const bool dbg_t = std::getenv("PUMP_DEBUG_TIMING") != nullptr;

@@ -263,8 +263,11 @@ __device__ __forceinline__ void commit_one(const CommitArgs& a, int64_t t, int64
   int b = static_cast<int>(ceil(c / a.width - 1e-12));  // planner.hpp:86
   a.bucket[id] = b < 0 ? 0 : b;
   a.flags[id] = 0;
-  if (a.is_goal[hv] && q < a.alpha_min)  // note_goal (planner.hpp:95-98)
-    atomicMin(&a.st->best_goal_bits, __double_as_longlong(c));
+  if (a.is_goal[hv]) {
+    if (q < a.alpha_min)  // note_goal (planner.hpp:95-98)
+      atomicMin(&a.st->best_goal_bits, __double_as_longlong(c));
+    atomicMax(&a.st->max_goal_tend, static_cast<long long>(a.c_tend[t]));
+  }
   const int slot = atomicAdd(&a.new_cnt[hv], 1);
   a.new_slot[r] = slot;
   if (slot == 0) a.touched[atomicAdd(reinterpret_cast<unsigned long long*>(&a.st->touched), 1ull)] = hv;
@@ -1477,6 +1480,7 @@ void run_explore_device(DevExplore& X, Ctx& c, const DevGraph& G, const ExploreA
     h = *X.status_h;
     X.n_plans = h.n_plans;
     if (h.err) throw std::runtime_error("explore: device error " + std::to_string(h.err));
+    if (prm.on_round) prm.on_round(h);
   }
   X.kernel_ms = c.toc();
   kprof_work(F_EXPAND, h.hs_tests * N);

@@ -1,6 +1,8 @@
 // Device-resident explore (planner.hpp:74-267) state and driver.
 #pragma once
 
+#include <functional>
+
 #include "graph.h"
 
 namespace pumpg {
@@ -9,6 +11,7 @@ struct ExploreStatus {  // read back once per round (pinned)
   long long G, T, K, n_plans, open_count, i, max_bucket, min_bucket, pool_n;
   long long best_goal_bits, min_group_bits;
   long long disc_cp, disc_hor, removed, n_surv, evicted_open, err, touched, hs_tests;
+  long long max_goal_tend;  // largest t_end of any plan committed at a goal node
 };
 
 struct DevExplore {
@@ -35,6 +38,9 @@ struct DevExplore {
 
 struct ExploreArgs {
   double alpha_min, alpha_max, lambda, r_n;
+  // called after every round's status readback (run_pump extends the MC
+  // table on the side stream up to the goal plans' largest t_end)
+  std::function<void(const ExploreStatus&)> on_round = nullptr;
 };
 
 void run_explore_device(DevExplore& X, Ctx& c, const DevGraph& G, const ExploreArgs& a);
