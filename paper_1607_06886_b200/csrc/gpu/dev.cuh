@@ -314,28 +314,65 @@ __host__ __device__ __forceinline__ void motion_bbox(const MotionD<DW>& m, doubl
 // is at an end) plus the rounding margin of motion_bbox.  A span whose box
 // is inside the workspace and separated from every candidate obstacle holds
 // no failing test, so its subtree is skipped.
+// The culling state of one motion: its widened bounding box strictly inside
+// the workspace bounds (no bounds test can fail) and the obstacles not
+// separated from the box (the only ones any point on the motion, or any
+// segment between such points, can touch).
+constexpr int kCullWords = 4;
+struct MotionCull {
+  bool inside, masked, any;
+  uint64_t cand[kCullWords];
+};
+
 template <int DW>
-__host__ __device__ inline bool motion_collides(const MotionD<DW>& m, const WorldD& w, double eps_cc) {
+__host__ __device__ inline MotionCull motion_cull(const MotionD<DW>& m, const WorldD& w) {
+  MotionCull c;
   double bl[DW], bh[DW];
   motion_bbox<DW>(m, bl, bh);
-  bool inside = true;
+  c.inside = true;
 #pragma unroll
-  for (int k = 0; k < DW; ++k) inside = inside && bl[k] > w.blo[k] && bh[k] < w.bhi[k];
-  constexpr int kMaskWords = 4;
-  uint64_t cand[kMaskWords] = {0, 0, 0, 0};
-  const bool masked = w.n_obs <= 64 * kMaskWords;
-  bool any = !masked;
-  if (masked) {
+  for (int k = 0; k < DW; ++k) c.inside = c.inside && bl[k] > w.blo[k] && bh[k] < w.bhi[k];
+  for (int q = 0; q < kCullWords; ++q) c.cand[q] = 0;
+  c.masked = w.n_obs <= 64 * kCullWords;
+  c.any = !c.masked;
+  if (c.masked) {
     for (int o = 0; o < w.n_obs; ++o) {
       bool sep = false;
 #pragma unroll
       for (int k = 0; k < DW; ++k) sep = sep || (bh[k] < w.lo[o * DW + k]) || (bl[k] > w.hi[o * DW + k]);
       if (!sep) {
-        cand[o >> 6] |= 1ull << (o & 63);
-        any = true;
+        c.cand[o >> 6] |= 1ull << (o & 63);
+        c.any = true;
       }
     }
   }
+  return c;
+}
+
+// point_free (geom.hpp:56-61) for a point on the motion `c` was computed for
+template <int DW>
+__host__ __device__ inline bool point_free_culled(const WorldD& w, const MotionCull& c, const double* p) {
+  if (!c.inside && !box_contains<DW>(w.blo, w.bhi, p)) return false;
+  if (!c.masked) {
+    for (int o = 0; o < w.n_obs; ++o)
+      if (box_contains<DW>(w.lo + o * DW, w.hi + o * DW, p)) return false;
+    return true;
+  }
+  for (int q = 0; q < kCullWords; ++q)
+    for (uint64_t x = c.cand[q]; x; x &= x - 1) {
+      const int o = q * 64 + __builtin_ctzll_hd(x);
+      if (box_contains<DW>(w.lo + o * DW, w.hi + o * DW, p)) return false;
+    }
+  return true;
+}
+
+template <int DW>
+__host__ __device__ inline bool motion_collides(const MotionD<DW>& m, const WorldD& w, double eps_cc,
+                                                const MotionCull* pre = nullptr) {
+  const MotionCull cull = pre ? *pre : motion_cull<DW>(m, w);
+  const bool inside = cull.inside, masked = cull.masked, any = cull.any;
+  constexpr int kMaskWords = kCullWords;
+  const uint64_t* cand = cull.cand;
   if (inside && !any) return false;
   auto free_pt = [&](const double* p) {
     if (!inside && !box_contains<DW>(w.blo, w.bhi, p)) return false;

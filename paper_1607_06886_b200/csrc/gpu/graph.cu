@@ -239,14 +239,18 @@ __global__ void __launch_bounds__(128) k_collide(GraphArgs g, WorldD w, int64_t 
     m.v1[k] = g.vel[u * DW + k];
   }
   coeffs_dev<DW>(m.p0, m.v0, m.p1, m.v1, m.tau, m.a, m.j);
-  bool ok = !motion_collides<DW>(m, ws, g.eps_cc);
+  const MotionCull cull = motion_cull<DW>(m, ws);
+  bool ok = !motion_collides<DW>(m, ws, g.eps_cc, &cull);
   int L = 0;
   if (ok) {
     // motion_waypoints (steer.hpp:192-212): k = floor(tau/dt + 1e-9)
     const int k = static_cast<int>(floor(m.tau / g.dt + 1e-9));
     const double rem = m.tau - k * g.dt;
     L = rem > 1e-9 ? k + 1 : k;
-    for (int j = 1; j <= L && ok; ++j) {
+    // the waypoints lie on the motion, inside the box the cull was made for:
+    // with the box inside the bounds and clear of every obstacle all are free
+    const bool all_free = cull.inside && !cull.any;
+    for (int j = 1; j <= L && ok && !all_free; ++j) {
       double p[DW], vv[DW];
       if (j == L) {
 #pragma unroll
@@ -254,7 +258,7 @@ __global__ void __launch_bounds__(128) k_collide(GraphArgs g, WorldD w, int64_t 
       } else {
         motion_state<DW>(m, j * g.dt, p, vv);
       }
-      ok = point_free<DW>(ws, p);
+      ok = point_free_culled<DW>(ws, cull, p);
     }
   }
   valid[c] = ok ? 1 : 0;
