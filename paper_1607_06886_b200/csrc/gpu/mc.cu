@@ -687,7 +687,9 @@ __global__ void __launch_bounds__(kMcBlock) k_mc_tab(WorldD w, const int64_t* __
                                                      const unsigned long long* __restrict__ maxdev, double eps_cc,
                                                      uint8_t* __restrict__ flags) {
   extern __shared__ double smem[];
-  __shared__ uint64_t s_cand[kMcChunk + 1];
+  constexpr int kStepCap = 64;  // block-wide candidate obstacles per step (more: test all)
+  __shared__ uint16_t s_list[kMcChunk + 1][kStepCap];
+  __shared__ int s_nlist[kMcChunk + 1];  // -1: more than kStepCap candidates
   __shared__ int s_skip[kMcChunk + 1];
   __shared__ int s_all_skip;
   const int j = blockIdx.y;
@@ -720,42 +722,57 @@ __global__ void __launch_bounds__(kMcBlock) k_mc_tab(WorldD w, const int64_t* __
   // Per step, the box every rollout's realized points (and the subdivision
   // points between them) lie in: ynom -/+ the largest |dy| over the table's
   // rollouts (fl is monotone, so fl(ynom +- maxdev) bounds fl(ynom + dy)),
-  // widened by the sub-segment rounding margin.  Steps whose box is inside
-  // the workspace and meets no (inflated) obstacle hold no failing test for
-  // any rollout: the block skips them, loads included.
-  if (threadIdx.x <= kMcChunk) {
-    const int r = threadIdx.x, t = s_lo_t + r;
-    int skip = 1;
-    uint64_t cand = 0;
-    if (t >= t_lo && t <= t_hi) {
-      double bl[DW], bh[DW];
-      bool inside = true;
+  // widened by the sub-segment rounding margin.  The (inflated) obstacles
+  // meeting that box are the only ones any rollout can touch at this step:
+  // listed per step (a warp per step, ballot compaction); a step with an
+  // empty list and its box inside the workspace holds no failing test for
+  // any rollout and is skipped, loads included.
+  {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (int r = warp; r <= kMcChunk; r += kMcBlock / 32) {
+      const int t = s_lo_t + r;
+      int skip = 1, nl = 0;
+      if (t >= t_lo && t <= t_hi) {
+        double bl[DW], bh[DW];
+        bool inside = true;
 #pragma unroll
-      for (int k = 0; k < DW; ++k) {
-        const double m1 = __longlong_as_double(static_cast<long long>(maxdev[t * DW + k]));
-        double lo = s_y[r * DW + k] - m1, hi = s_y[r * DW + k] + m1;
-        if (t > 0) {
-          const double m0 = __longlong_as_double(static_cast<long long>(maxdev[(t - 1) * DW + k]));
-          const double lo0 = s_y[(r - 1) * DW + k] - m0, hi0 = s_y[(r - 1) * DW + k] + m0;
-          lo = lo0 < lo ? lo0 : lo;
-          hi = hi0 > hi ? hi0 : hi;
+        for (int k = 0; k < DW; ++k) {
+          const double m1 = __longlong_as_double(static_cast<long long>(maxdev[t * DW + k]));
+          double lo = s_y[r * DW + k] - m1, hi = s_y[r * DW + k] + m1;
+          if (t > 0) {
+            const double m0 = __longlong_as_double(static_cast<long long>(maxdev[(t - 1) * DW + k]));
+            const double lo0 = s_y[(r - 1) * DW + k] - m0, hi0 = s_y[(r - 1) * DW + k] + m0;
+            lo = lo0 < lo ? lo0 : lo;
+            hi = hi0 > hi ? hi0 : hi;
+          }
+          const double mg = 1e-12 * (1.0 + (lo < 0 ? -lo : lo) + (hi < 0 ? -hi : hi));
+          bl[k] = lo - mg;
+          bh[k] = hi + mg;
+          inside = inside && bl[k] > w.blo[k] && bh[k] < w.bhi[k];
         }
-        const double mg = 1e-12 * (1.0 + (lo < 0 ? -lo : lo) + (hi < 0 ? -hi : hi));
-        bl[k] = lo - mg;
-        bh[k] = hi + mg;
-        inside = inside && bl[k] > w.blo[k] && bh[k] < w.bhi[k];
-      }
-      for (int o = 0; o < w.n_obs && o < 64; ++o) {
-        bool sep = false;
+        for (int o0 = 0; o0 < w.n_obs; o0 += 32) {
+          const int o = o0 + lane;
+          bool meet = false;
+          if (o < w.n_obs) {
+            bool sep = false;
 #pragma unroll
-        for (int k = 0; k < DW; ++k) sep = sep || (bh[k] < s_lo[o * DW + k]) || (bl[k] > s_hi[o * DW + k]);
-        if (!sep) cand |= 1ull << o;
+            for (int k = 0; k < DW; ++k) sep = sep || (bh[k] < s_lo[o * DW + k]) || (bl[k] > s_hi[o * DW + k]);
+            meet = !sep;
+          }
+          const unsigned bal = __ballot_sync(0xffffffffu, meet);
+          const int at = nl + __popc(bal & ((1u << lane) - 1u));
+          if (meet && at < kStepCap) s_list[r][at] = static_cast<uint16_t>(o);
+          nl += __popc(bal);
+        }
+        if (nl > kStepCap) nl = -1;
+        skip = (inside && nl == 0) ? 1 : 0;
       }
-      skip = (inside && cand == 0 && w.n_obs <= 64) ? 1 : 0;
+      if (lane == 0) {
+        s_nlist[r] = nl;
+        s_skip[r] = skip;
+        if (!skip) s_all_skip = 0;
+      }
     }
-    s_cand[r] = w.n_obs <= 64 ? cand : ~0ull;
-    s_skip[r] = skip;
-    if (!skip) s_all_skip = 0;
   }
   __syncthreads();
   if (s_all_skip) return;
@@ -798,24 +815,29 @@ __global__ void __launch_bounds__(kMcBlock) k_mc_tab(WorldD w, const int64_t* __
       bl[a] = prev[a] < y[a] ? prev[a] : y[a];
       bh[a] = prev[a] < y[a] ? y[a] : prev[a];
     }
-    uint64_t cand = 0;  // this rollout's culling, within the step's block-wide candidates
-    for (uint64_t m = s_cand[r] & (w.n_obs >= 64 ? ~0ull : ((1ull << w.n_obs) - 1)); m; m &= m - 1) {
-      const int o = __ffsll(static_cast<long long>(m)) - 1;
+    const int nl = s_nlist[r];
+    // this rollout's culling within the step's list (bit q <-> s_list[r][q])
+    uint64_t cand = 0;
+    for (int q = 0; q < nl; ++q) {
+      const int o = s_list[r][q];
       bool sep = false;
 #pragma unroll
       for (int a = 0; a < DW; ++a) sep = sep || (bh[a] < s_lo[o * DW + a]) || (bl[a] > s_hi[o * DW + a]);
-      if (!sep) cand |= 1ull << o;
+      if (!sep) cand |= 1ull << q;
     }
-    for (uint64_t m = cand; m && !hit; m &= m - 1) {
-      const int o = __ffsll(static_cast<long long>(m)) - 1;
-      if (box_contains<DW>(s_clo + o * DW, s_chi + o * DW, y)) hit = true;
+    if (nl >= 0) {
+      for (uint64_t m = cand; m && !hit; m &= m - 1) {
+        const int o = s_list[r][__ffsll(static_cast<long long>(m)) - 1];
+        if (box_contains<DW>(s_clo + o * DW, s_chi + o * DW, y)) hit = true;
+      }
+    } else {
+      for (int o = 0; o < w.n_obs && !hit; ++o)
+        if (box_contains<DW>(s_clo + o * DW, s_chi + o * DW, y)) hit = true;
     }
-    for (int o = 64; o < w.n_obs && !hit; ++o)
-      if (box_contains<DW>(s_clo + o * DW, s_chi + o * DW, y)) hit = true;
     // every subdivision point lies in bbox(prev, y) up to rounding: with no
     // candidate obstacle and the box strictly inside the bounds, no
     // sub-segment test can fail
-    bool clear = cand == 0 && w.n_obs <= 64;
+    bool clear = nl >= 0 && cand == 0;
 #pragma unroll
     for (int a2 = 0; a2 < DW; ++a2) {
       const double m = 1e-12 * (1.0 + (bl[a2] < 0 ? -bl[a2] : bl[a2]) + (bh[a2] < 0 ? -bh[a2] : bh[a2]));
@@ -843,18 +865,21 @@ __global__ void __launch_bounds__(kMcBlock) k_mc_tab(WorldD w, const int64_t* __
           hit = true;
           break;
         }
-        for (uint64_t m = cand; m; m &= m - 1) {
-          const int o = __ffsll(static_cast<long long>(m)) - 1;
-          if (box_contains<DW>(s_clo + o * DW, s_chi + o * DW, p1) ||
-              segment_hits<DW>(p0, p1, s_clo + o * DW, s_chi + o * DW)) {
-            hit = true;
-            break;
+        if (nl >= 0) {
+          for (uint64_t m = cand; m; m &= m - 1) {
+            const int o = s_list[r][__ffsll(static_cast<long long>(m)) - 1];
+            if (box_contains<DW>(s_clo + o * DW, s_chi + o * DW, p1) ||
+                segment_hits<DW>(p0, p1, s_clo + o * DW, s_chi + o * DW)) {
+              hit = true;
+              break;
+            }
           }
+        } else {
+          for (int o = 0; o < w.n_obs && !hit; ++o)
+            if (box_contains<DW>(s_clo + o * DW, s_chi + o * DW, p1) ||
+                segment_hits<DW>(p0, p1, s_clo + o * DW, s_chi + o * DW))
+              hit = true;
         }
-        for (int o = 64; o < w.n_obs && !hit; ++o)
-          if (box_contains<DW>(s_clo + o * DW, s_chi + o * DW, p1) ||
-              segment_hits<DW>(p0, p1, s_clo + o * DW, s_chi + o * DW))
-            hit = true;
 #pragma unroll
         for (int a = 0; a < DW; ++a) p0[a] = p1[a];
       }
