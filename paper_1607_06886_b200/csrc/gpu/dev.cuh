@@ -610,7 +610,8 @@ __host__ __device__ __forceinline__ void coeffs_dev(const double* ap, const doub
 // pruned bitmap (1 word keeps it in a register for <= 32 boxes).
 template <int DW, int kWords = 128>
 __host__ __device__ inline int convex_region(const WorldD& ws, const double* y, const double* yd, double* a_out,
-                                             double* b_out, uint8_t* fb_out, int a_stride = DW, int b_stride = 1) {
+                                             double* b_out, uint8_t* fb_out, int a_stride = DW, int b_stride = 1,
+                                             int out_cap = 1 << 30) {
   uint32_t pruned[kWords];
   const int nw = (ws.n_obs + 31) / 32;
   for (int q = 0; q < nw; ++q) pruned[q] = 0u;
@@ -655,7 +656,7 @@ __host__ __device__ inline int convex_region(const WorldD& ws, const double* y, 
       }
     }
     if (!any) return -1;
-    if (a_out) {
+    if (a_out && count < out_cap) {  // (past out_cap only the count is kept)
       double a[DW];
       bool fb = false;
       const double vn = sqrt(sqnorm<DW>(yd));

@@ -294,12 +294,20 @@ __global__ void k_emit_edges(GraphArgs g, int64_t n_cand, const int64_t* __restr
   }
 }
 
-template <int DW, bool WRITE>
+// Regions for larger obstacle sets, in two launches without recomputation:
+// MOVE = false computes every waypoint's half-spaces once, keeping the count
+// and the first kRegSlots half-spaces in a per-waypoint slot buffer; after
+// the count scan, MOVE = true copies the slots to the packed CSR position
+// (and recomputes, writing directly, only waypoints with more than
+// kRegSlots half-spaces).
+constexpr int kRegSlots = 16;
+template <int DW, bool MOVE>
 __global__ void __launch_bounds__(128) k_regions(GraphArgs g, WorldD w, int64_t n_wp, int64_t n_edges,
                                                  const int64_t* __restrict__ wp_off, const int32_t* __restrict__ e_from,
                                                  const int32_t* __restrict__ e_to, const double* __restrict__ e_tau,
                                                  const double* __restrict__ e_acc0, const double* __restrict__ e_jerk,
                                                  const int32_t* __restrict__ e_nsteps, int32_t* __restrict__ hcount,
+                                                 double* __restrict__ slot_pk, uint8_t* __restrict__ slot_fb,
                                                  const int64_t* __restrict__ hs_off, int32_t* __restrict__ hs_cnt,
                                                  double* __restrict__ hs_pk, uint8_t* __restrict__ hs_fb,
                                                  int* __restrict__ err) {
@@ -307,6 +315,21 @@ __global__ void __launch_bounds__(128) k_regions(GraphArgs g, WorldD w, int64_t 
   const WorldD ws = stage_world<DW>(w, smem);
   const int64_t x = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (x >= n_wp) return;
+  if (MOVE) {
+    const int cnt = hcount[x];
+    hs_cnt[x] = cnt;
+    if (cnt <= kRegSlots) {
+      const int64_t o = hs_off[x];
+      const double2* src = reinterpret_cast<const double2*>(slot_pk) + x * kRegSlots * 2;
+      double2* dst = reinterpret_cast<double2*>(hs_pk) + o * 2;
+      for (int h = 0; h < cnt; ++h) {
+        dst[2 * h] = src[2 * h];
+        dst[2 * h + 1] = src[2 * h + 1];
+        hs_fb[o + h] = slot_fb[x * kRegSlots + h];
+      }
+      return;
+    }
+  }
   // edge owning waypoint x
   int64_t lo = 0, hi = n_edges;
   while (hi - lo > 1) {
@@ -341,16 +364,19 @@ __global__ void __launch_bounds__(128) k_regions(GraphArgs g, WorldD w, int64_t 
   } else {
     motion_state<DW>(m, j * g.dt, y, yd);
   }
-  double* ao = WRITE ? hs_pk + hs_off[x] * 4 : nullptr;
-  double* bo = WRITE ? hs_pk + hs_off[x] * 4 + 3 : nullptr;
-  uint8_t* fo = WRITE ? hs_fb + hs_off[x] : nullptr;
-  const int count = convex_region<DW>(ws, y, yd, ao, bo, fo, 4, 4);
-  if (count < 0) {
-    atomicExch(err, 1);
+  if (MOVE) {  // more than kRegSlots half-spaces: recompute straight into place
+    const int64_t o = hs_off[x];
+    convex_region<DW>(ws, y, yd, hs_pk + o * 4, hs_pk + o * 4 + 3, hs_fb + o, 4, 4);
     return;
   }
-  if (!WRITE) hcount[x] = count;
-  if (WRITE) hs_cnt[x] = count;
+  double* ao = slot_pk + x * kRegSlots * 4;
+  const int count = convex_region<DW>(ws, y, yd, ao, ao + 3, slot_fb + x * kRegSlots, 4, 4, kRegSlots);
+  if (count < 0) {
+    atomicExch(err, 1);
+    hcount[x] = 0;
+    return;
+  }
+  hcount[x] = count;
 }
 
 // Single pass for small obstacle sets (<= 16 boxes): each waypoint computes
@@ -648,6 +674,8 @@ void build_graph_device(DevGraph& G, Ctx& c, int n, int dw, const double* h_pos,
     return;
   }
   DBuf& hcnt = c.buf("g_hcnt", al((NW + 1) * 4));
+  DBuf& slot_pk = c.buf("g_reg_slots", al(static_cast<size_t>(NW) * kRegSlots * 32 + 32));
+  DBuf& slot_fb = c.buf("g_reg_slot_fb", al(static_cast<size_t>(NW) * kRegSlots + 8));
   if (NW > 0) {
     KScope ks(st, F_REGIONS);
     dispatch_dw(dw, [&]<int DW>() {
@@ -657,8 +685,8 @@ void build_graph_device(DevGraph& G, Ctx& c, int n, int dw, const double* h_pos,
       }
       k_regions<DW, false><<<grid_for(NW, 128), 128, wsmem, st>>>(
           ga, wd, NW, E, G.wp_off.as<int64_t>(), G.e_from.as<int32_t>(), G.e_to.as<int32_t>(), G.e_tau.as<double>(),
-          G.e_acc0.as<double>(), G.e_jerk.as<double>(), G.e_nsteps.as<int32_t>(), hcnt.as<int32_t>(), nullptr,
-          nullptr, nullptr, nullptr, err.as<int>());
+          G.e_acc0.as<double>(), G.e_jerk.as<double>(), G.e_nsteps.as<int32_t>(), hcnt.as<int32_t>(),
+          slot_pk.as<double>(), slot_fb.as<uint8_t>(), nullptr, nullptr, nullptr, nullptr, err.as<int>());
     });
     ++c.launches;
     PUMP_CUDA(cudaGetLastError());
@@ -679,8 +707,9 @@ void build_graph_device(DevGraph& G, Ctx& c, int n, int dw, const double* h_pos,
     dispatch_dw(dw, [&]<int DW>() {
       k_regions<DW, true><<<grid_for(NW, 128), 128, wsmem, st>>>(
           ga, wd, NW, E, G.wp_off.as<int64_t>(), G.e_from.as<int32_t>(), G.e_to.as<int32_t>(), G.e_tau.as<double>(),
-          G.e_acc0.as<double>(), G.e_jerk.as<double>(), G.e_nsteps.as<int32_t>(), nullptr, G.hs_off.as<int64_t>(),
-          G.hs_cnt.as<int32_t>(), G.hs_pk.as<double>(), G.hs_fb.as<uint8_t>(), err.as<int>());
+          G.e_acc0.as<double>(), G.e_jerk.as<double>(), G.e_nsteps.as<int32_t>(), hcnt.as<int32_t>(),
+          slot_pk.as<double>(), slot_fb.as<uint8_t>(), G.hs_off.as<int64_t>(), G.hs_cnt.as<int32_t>(),
+          G.hs_pk.as<double>(), G.hs_fb.as<uint8_t>(), err.as<int>());
     });
     ++c.launches;
     PUMP_CUDA(cudaGetLastError());

@@ -51,7 +51,7 @@ def assert_graph_equal(a, b):
 
 
 GRAPH_CASES = [("minimal", None), ("three_obstacle", 300), ("indoor", 400), ("quad3d_three_obstacle", 500),
-               ("quad3d_indoor", 600)]
+               ("quad3d_indoor", 600), ("quad3d_forest", 500)]  # forest: 200 boxes (multi-pass regions)
 
 
 @pytest.mark.parametrize("name,samples", GRAPH_CASES)
@@ -195,7 +195,7 @@ def assert_run_equal(got, ref):
 
 
 @pytest.mark.parametrize("name,samples,mc", [("minimal", None, 4000), ("three_obstacle", None, 4000),
-                                             ("quad3d_three_obstacle", 800, 4000)])
+                                             ("quad3d_three_obstacle", 800, 4000), ("quad3d_forest", 700, 3000)])
 def test_run_pump_matches_oracle(oracle_lib, gpu_ctx, name, samples, mc):
     from paper_1607_06886_b200 import api
 
