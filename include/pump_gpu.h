@@ -261,6 +261,15 @@ int pump_mc_certify(pump_ctx* ctx, const pump_closed_loop* cl, const pump_worksp
 int pump_build_graph(pump_ctx* ctx, int32_t n_nodes, int32_t dw, const double* pos, const double* vel,
                      const pump_workspace* ws, const pump_goal* goal, double r_n, double dt, double eps_cc,
                      double tau_max, pump_graph** out);
+/* The edges of source rows [row_lo, row_hi) only (a multi-GPU rank's slice,
+ * SURVEY §8e): row_ptr is 0 before the slice and the slice's edge count after
+ * it; regions are built for the slice's edges.  The slices of a partition of
+ * [0, n) concatenate (edges, waypoints, half-spaces) and sum (row_ptr) to the
+ * full graph.  With a communicator set, pump_build_graph does exactly this per
+ * rank and gathers the slices over NCCL. */
+int pump_build_graph_rows(pump_ctx* ctx, int32_t n_nodes, int32_t dw, const double* pos, const double* vel,
+                          const pump_workspace* ws, const pump_goal* goal, double r_n, double dt, double eps_cc,
+                          double tau_max, int32_t row_lo, int32_t row_hi, pump_graph** out);
 /* Upload a prebuilt graph (pump.hpp:170 "prebuilt"). Reads every field. */
 int pump_graph_upload(pump_ctx* ctx, const pump_graph_view* view, pump_graph** out);
 /* Sizes into view (pointers untouched); then export into caller buffers

@@ -62,7 +62,7 @@ EXPORTS = [
     "pump_explore_export", "pump_explore_free", "pump_run", "pump_result_summary_get", "pump_result_arrays",
     "pump_result_free", "pump_nccl_unique_id", "pump_ctx_set_comm", "pump_shard_range", "pump_ctx_profile",
     "pump_ctx_profile_read", "pump_ctx_io_bytes", "pump_ctx_flush_l2", "pump_peak_fp64", "pump_ctx_stream",
-    "pump_scenario_nodes",
+    "pump_scenario_nodes", "pump_build_graph_rows",
 ]
 
 
@@ -381,6 +381,27 @@ def build_graph(pos, vel, ws: dict, goal: dict, r_n: float, dt: float, eps_cc: f
     h = C.c_void_p()
     _check(lib().pump_build_graph(ctx.h, n, dw, _p(pos), _p(vel), C.byref(wss), C.byref(gs), r_n, dt, eps_cc,
                                   tau_max, C.byref(h)))
+    return Graph(h, ctx)
+
+
+def build_graph_rows(pos, vel, ws: dict, goal: dict, r_n: float, dt: float, eps_cc: float, tau_max: float,
+                     row_lo: int, row_hi: int, ctx: Context | None = None) -> Graph:
+    """The edges of source rows [row_lo, row_hi) only: one rank's slice of the
+    multi-GPU graph build (pump_build_graph_rows)."""
+    ctx = ctx or default_context()
+    keep = A.Keep()
+    pos = keep.f64(pos)
+    vel = keep.f64(vel)
+    n, dw = pos.shape
+    wss = A.workspace_struct(ws, keep)
+    gs = A.goal_struct(goal, keep)
+    h = C.c_void_p()
+    L = lib()
+    L.pump_build_graph_rows.argtypes = [C.c_void_p, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p,
+                                        C.c_void_p, C.c_double, C.c_double, C.c_double, C.c_double, C.c_int32,
+                                        C.c_int32, C.c_void_p]
+    _check(L.pump_build_graph_rows(ctx.h, n, dw, _p(pos), _p(vel), C.byref(wss), C.byref(gs), r_n, dt, eps_cc,
+                                   tau_max, row_lo, row_hi, C.byref(h)))
     return Graph(h, ctx)
 
 

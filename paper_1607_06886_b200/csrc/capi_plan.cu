@@ -718,8 +718,13 @@ static void run_pump_device(Ctx& c, const pumpb::Scenario& s, const DevGraph* pr
       std::fprintf(stderr, "[pump g] %-24s %8.3f ms (from solve start)\n", "sample_nodes",
                    1e3 * secs(t0, clk::now()));
     const int n = static_cast<int>(pos.size()) / dw;
+    // multi-GPU: each rank builds the rows of its slice; the slices are
+    // gathered over NVLink into the full graph on every rank
+    int64_t rlo = 0, rhi = n;
+    if (c.world > 1) shard_range(n, c.rank, c.world, &rlo, &rhi);
     build_graph_device(local, c, n, dw, host_sampling ? pos.data() : nullptr, host_sampling ? vel.data() : nullptr,
-                       dwld, r_n, s.dt, eps_cc, s.effective_tau_max(), scan_ratio(s.effective_tau_max()));
+                       dwld, r_n, s.dt, eps_cc, s.effective_tau_max(), scan_ratio(s.effective_tau_max()),
+                       static_cast<int>(rlo), static_cast<int>(rhi), c.world > 1);
     pump_goal g{s.goal.lo.data(), s.goal.hi.data(), s.goal_max_speed};
     local.h_pos = pos;
     local.h_vel = vel;
@@ -1033,9 +1038,9 @@ static void run_pump_device(Ctx& c, const pumpb::Scenario& s, const DevGraph* pr
 extern "C" {
 
 // ------------------------------------------------------------------ graph
-int pump_build_graph(pump_ctx* ctx, int32_t n_nodes, int32_t dw, const double* pos, const double* vel,
-                     const pump_workspace* ws, const pump_goal* goal, double r_n, double dt, double eps_cc,
-                     double tau_max, pump_graph** out) {
+static int build_graph_rows(pump_ctx* ctx, int32_t n_nodes, int32_t dw, const double* pos, const double* vel,
+                            const pump_workspace* ws, const pump_goal* goal, double r_n, double dt, double eps_cc,
+                            double tau_max, int32_t row_lo, int32_t row_hi, bool gather, pump_graph** out) {
   return guard([&] {
     Ctx& c = ctx->c;
     if (!ws || ws->dw != dw) throw std::invalid_argument("build_graph: workspace dimension mismatch");
@@ -1044,7 +1049,8 @@ int pump_build_graph(pump_ctx* ctx, int32_t n_nodes, int32_t dw, const double* p
     auto* g = new pump_graph;
     try {
       g->owner = ctx;
-      build_graph_device(g->g, c, n_nodes, dw, pos, vel, w, r_n, dt, eps_cc, tau_max, scan_ratio(tau_max));
+      build_graph_device(g->g, c, n_nodes, dw, pos, vel, w, r_n, dt, eps_cc, tau_max, scan_ratio(tau_max), row_lo,
+                         row_hi, gather);
       g->g.h_pos.assign(pos, pos + static_cast<size_t>(n_nodes) * dw);
       g->g.h_vel.assign(vel, vel + static_cast<size_t>(n_nodes) * dw);
       graph_goal_nodes(g->g, pos, vel, goal);
@@ -1054,6 +1060,24 @@ int pump_build_graph(pump_ctx* ctx, int32_t n_nodes, int32_t dw, const double* p
     }
     *out = g;
   });
+}
+
+int pump_build_graph(pump_ctx* ctx, int32_t n_nodes, int32_t dw, const double* pos, const double* vel,
+                     const pump_workspace* ws, const pump_goal* goal, double r_n, double dt, double eps_cc,
+                     double tau_max, pump_graph** out) {
+  if (!ctx) return PUMP_E_INVALID_ARGUMENT;
+  int64_t lo = 0, hi = n_nodes;
+  const bool shard = ctx->c.world > 1 && ctx->c.nccl;
+  if (shard) shard_range(n_nodes, ctx->c.rank, ctx->c.world, &lo, &hi);
+  return build_graph_rows(ctx, n_nodes, dw, pos, vel, ws, goal, r_n, dt, eps_cc, tau_max, static_cast<int32_t>(lo),
+                          static_cast<int32_t>(hi), shard, out);
+}
+
+int pump_build_graph_rows(pump_ctx* ctx, int32_t n_nodes, int32_t dw, const double* pos, const double* vel,
+                          const pump_workspace* ws, const pump_goal* goal, double r_n, double dt, double eps_cc,
+                          double tau_max, int32_t row_lo, int32_t row_hi, pump_graph** out) {
+  return build_graph_rows(ctx, n_nodes, dw, pos, vel, ws, goal, r_n, dt, eps_cc, tau_max, row_lo, row_hi, false,
+                          out);
 }
 
 int pump_scenario_nodes(const pump_scenario* s, int32_t cap, double* pos, double* vel, int32_t* n_out) {

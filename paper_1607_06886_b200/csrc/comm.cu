@@ -7,6 +7,7 @@
 #include <nccl.h>
 
 #include <cstring>
+#include <vector>
 
 #include "ctx.h"
 #include "guard.h"
@@ -24,6 +25,9 @@ struct NcclApi {
                             cudaStream_t) = nullptr;
   ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
   const char* (*GetErrorString)(ncclResult_t) = nullptr;
+  ncclResult_t (*Broadcast)(const void*, void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*GroupStart)() = nullptr;
+  ncclResult_t (*GroupEnd)() = nullptr;
 };
 
 static NcclApi& nccl() {
@@ -38,7 +42,11 @@ static NcclApi& nccl() {
     api.AllReduce = reinterpret_cast<decltype(api.AllReduce)>(dlsym(h, "ncclAllReduce"));
     api.CommDestroy = reinterpret_cast<decltype(api.CommDestroy)>(dlsym(h, "ncclCommDestroy"));
     api.GetErrorString = reinterpret_cast<decltype(api.GetErrorString)>(dlsym(h, "ncclGetErrorString"));
-    if (!api.GetUniqueId || !api.CommInitRank || !api.AllReduce || !api.CommDestroy || !api.GetErrorString)
+    api.Broadcast = reinterpret_cast<decltype(api.Broadcast)>(dlsym(h, "ncclBroadcast"));
+    api.GroupStart = reinterpret_cast<decltype(api.GroupStart)>(dlsym(h, "ncclGroupStart"));
+    api.GroupEnd = reinterpret_cast<decltype(api.GroupEnd)>(dlsym(h, "ncclGroupEnd"));
+    if (!api.GetUniqueId || !api.CommInitRank || !api.AllReduce || !api.CommDestroy || !api.GetErrorString ||
+        !api.Broadcast || !api.GroupStart || !api.GroupEnd)
       throw CudaError("libnccl.so.2 lacks a required symbol");
     loaded = true;
   }
@@ -54,6 +62,27 @@ void allreduce_sum_i64(Ctx& c, int64_t* d, size_t count) {
   if (c.world <= 1 || !c.nccl) return;
   const ncclResult_t r = nccl().AllReduce(d, d, count, ncclInt64, ncclSum, static_cast<ncclComm_t>(c.nccl), c.stream);
   if (r != ncclSuccess) throw CudaError(std::string("ncclAllReduce: ") + nccl().GetErrorString(r));
+  ++c.collectives;
+}
+
+// Concatenate per-rank segments: rank r's `len[r]` bytes at `send` land at
+// byte offset off[r] of `recv` on every rank (one grouped ncclBroadcast per
+// root; the root's own copy is the broadcast's send -> recv).
+void gather_segments(Ctx& c, const void* send, void* recv, const std::vector<int64_t>& off,
+                     const std::vector<int64_t>& len) {
+  if (c.world <= 1 || !c.nccl) throw CudaError("gather_segments: no communicator");
+  auto& A = nccl();
+  auto chk = [&](ncclResult_t r, const char* what) {
+    if (r != ncclSuccess) throw CudaError(std::string(what) + ": " + A.GetErrorString(r));
+  };
+  chk(A.GroupStart(), "ncclGroupStart");
+  for (int r = 0; r < c.world; ++r) {
+    if (len[r] == 0) continue;
+    chk(A.Broadcast(r == c.rank ? send : nullptr, static_cast<char*>(recv) + off[r], static_cast<size_t>(len[r]),
+                    ncclChar, r, static_cast<ncclComm_t>(c.nccl), c.stream),
+        "ncclBroadcast");
+  }
+  chk(A.GroupEnd(), "ncclGroupEnd");
   ++c.collectives;
 }
 

@@ -74,6 +74,8 @@ struct Ctx {
 
 void shard_range(int64_t n, int rank, int world, int64_t* lo, int64_t* hi);
 void allreduce_sum_i64(Ctx& c, int64_t* d, size_t count);
+void gather_segments(Ctx& c, const void* send, void* recv, const std::vector<int64_t>& off,
+                     const std::vector<int64_t>& len);
 void comm_destroy(Ctx& c);
 
 // Upload a workspace into ctx scratch buffers named prefix+"lo"/"hi".

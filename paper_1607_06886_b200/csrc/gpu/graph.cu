@@ -95,7 +95,7 @@ LbGrid make_lb_grid(double r_n) {
 // survivors are compacted in ascending-u order (warp ballots + CTA prefix)
 // into the row's slab.  Cheap (~1k FP64 ops per pair) and branch-light.
 template <int DW>
-__global__ void __launch_bounds__(kRowBlock) k_pair_filter(GraphArgs g, const LbGrid lb, int cap,
+__global__ void __launch_bounds__(kRowBlock) k_pair_filter(GraphArgs g, const LbGrid lb, int cap, int row0,
                                                            int32_t* __restrict__ row_cnt, int32_t* __restrict__ su) {
   __shared__ int wtot[kRowBlock / 32];
   __shared__ int base_s;
@@ -105,7 +105,7 @@ __global__ void __launch_bounds__(kRowBlock) k_pair_filter(GraphArgs g, const Lb
     double* dst = reinterpret_cast<double*>(&sl);
     for (int x = threadIdx.x; x < static_cast<int>(sizeof(LbGrid) / 8); x += blockDim.x) dst[x] = src[x];
   }
-  const int v = blockIdx.x;
+  const int v = row0 + blockIdx.x;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   double ap[DW], av[DW];
 #pragma unroll
@@ -475,7 +475,10 @@ __global__ void __launch_bounds__(128) k_regions_once(GraphArgs g, WorldD w, int
 static inline size_t al(size_t x) { return (x + 255) & ~size_t(255); }
 
 void build_graph_device(DevGraph& G, Ctx& c, int n, int dw, const double* h_pos, const double* h_vel,
-                        const DevWorld& w, double r_n, double dt, double eps_cc, double tau_max, double ratio) {
+                        const DevWorld& w, double r_n, double dt, double eps_cc, double tau_max, double ratio,
+                        int row_lo, int row_hi, bool gather) {
+  if (row_hi < 0) row_hi = n;
+  if (row_lo < 0 || row_lo > row_hi || row_hi > n) throw std::invalid_argument("build_graph: bad row range");
   if (r_n <= 0) throw std::invalid_argument("build_graph: r_n must be positive");
   if (dt <= 0) throw std::invalid_argument("motion_waypoints: dt must be positive");
   if (w.n_obs > 4096) throw std::invalid_argument("build_graph: more than 4096 obstacles");
@@ -510,6 +513,7 @@ void build_graph_device(DevGraph& G, Ctx& c, int n, int dw, const double* h_pos,
   const size_t wsmem = 2 * static_cast<size_t>(w.n_obs) * dw * sizeof(double);
   int cap = 1024;
   DBuf& rcnt = c.buf("g_rowcnt", al((n + 8) * 4));
+  PUMP_CUDA(cudaMemsetAsync(rcnt.p, 0, (n + 8) * 4, st));  // rows outside [row_lo, row_hi) stay empty
   DBuf& soff = c.buf("g_soff", al((n + 2) * 8));
   DBuf& stmp = c.buf("g_scantmp", scan_temp_bytes(static_cast<int64_t>(n) * n + 16));
   for (;;) {  // pass 1 with an exact per-row refit if a row overflows the slab
@@ -517,7 +521,9 @@ void build_graph_device(DevGraph& G, Ctx& c, int n, int dw, const double* h_pos,
     {
       KScope ks(st, F_PAIR);
       dispatch_dw(dw, [&]<int DW>() {
-        k_pair_filter<DW><<<n, kRowBlock, 0, st>>>(ga, lbg, cap, rcnt.as<int32_t>(), suB.as<int32_t>());
+        if (row_hi > row_lo)
+          k_pair_filter<DW><<<row_hi - row_lo, kRowBlock, 0, st>>>(ga, lbg, cap, row_lo, rcnt.as<int32_t>(),
+                                                                   suB.as<int32_t>());
       });
       ++c.launches;
       PUMP_CUDA(cudaGetLastError());
@@ -621,6 +627,44 @@ void build_graph_device(DevGraph& G, Ctx& c, int n, int dw, const double* h_pos,
     });
     ++c.launches;
     PUMP_CUDA(cudaGetLastError());
+  }
+  if (gather && c.world > 1) {
+    // ---- concatenate the ranks' row slices (graph sharded by source row)
+    DBuf& cnts = c.buf("g_rank_edges", al(static_cast<size_t>(c.world) * 8 + 8));
+    PUMP_CUDA(cudaMemsetAsync(cnts.p, 0, static_cast<size_t>(c.world) * 8, st));
+    c.h2d(cnts.as<int64_t>() + c.rank, &E, 8);
+    allreduce_sum_i64(c, cnts.as<int64_t>(), c.world);
+    std::vector<int64_t> per(c.world);
+    c.d2h(per.data(), cnts.p, static_cast<size_t>(c.world) * 8);
+    c.sync();
+    std::vector<int64_t> off(c.world + 1, 0);
+    for (int r = 0; r < c.world; ++r) off[r + 1] = off[r] + per[r];
+    const int64_t Et = off[c.world];
+    auto gather_array = [&](DBuf& local, size_t elem) {
+      DBuf& glob = c.buf("g_gather_tmp", al((Et + 1) * elem));
+      std::vector<int64_t> bo(c.world), bl(c.world);
+      for (int r = 0; r < c.world; ++r) {
+        bo[r] = off[r] * static_cast<int64_t>(elem);
+        bl[r] = per[r] * static_cast<int64_t>(elem);
+      }
+      gather_segments(c, local.p, glob.p, bo, bl);
+      local.ensure(al((Et + 1) * elem));  // (reallocates only when growing; content replaced below)
+      PUMP_CUDA(cudaMemcpyAsync(local.p, glob.p, Et * elem, cudaMemcpyDeviceToDevice, st));
+    };
+    gather_array(G.e_from, 4);
+    gather_array(G.e_to, 4);
+    gather_array(G.e_cost, 8);
+    gather_array(G.e_tau, 8);
+    gather_array(G.e_acc0, static_cast<size_t>(dw) * 8);
+    gather_array(G.e_jerk, static_cast<size_t>(dw) * 8);
+    gather_array(G.e_nsteps, 4);
+    // a row's local row_ptr is 0 before the rank's slice and E_r after it, so
+    // the global row_ptr is the element-wise sum over the ranks
+    allreduce_sum_i64(c, G.row_ptr.as<int64_t>(), n + 1);
+    E = Et;
+    G.E = E;
+    G.wp_off.ensure(al((E + 2) * 8));
+    mark("gather");
   }
   DBuf& stmp3 = c.buf("g_scantmp3", scan_temp_bytes(E + 16));
   exclusive_scan<int32_t>(G.e_nsteps.as<int32_t>(), G.wp_off.as<int64_t>(), E, stmp3.p, st, &c.launches);

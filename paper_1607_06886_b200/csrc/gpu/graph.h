@@ -23,8 +23,15 @@ struct DevGraph {
   std::vector<double> h_pos, h_vel;                       // host copies of the nodes
 };
 
+// Edges of source rows [row_lo, row_hi) (default: all).  With gather, the
+// row slices of all ranks of c's communicator are concatenated over NCCL into
+// the full graph on every rank (rows are contiguous per rank and edges are
+// row-major, so the global arrays are the rank-ordered concatenation and
+// row_ptr is the sum of the ranks' local row_ptr).  Regions are then built
+// for every edge present.
 void build_graph_device(DevGraph& G, Ctx& c, int n, int dw, const double* h_pos, const double* h_vel,
-                        const DevWorld& w, double r_n, double dt, double eps_cc, double tau_max, double ratio);
+                        const DevWorld& w, double r_n, double dt, double eps_cc, double tau_max, double ratio,
+                        int row_lo = 0, int row_hi = -1, bool gather = false);
 
 }  // namespace pumpg
 

@@ -224,3 +224,38 @@ def test_run_pump_prebuilt_graph(oracle_lib, gpu_ctx, name, samples):
     assert a["partial_plans"] == b["partial_plans"] and a["n_edges"] == b["n_edges"]
     ref = oracle_lib.run_pump(txt, workers=WORKERS)
     assert_run_equal(a, ref)
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_graph_row_slices_concatenate(oracle_lib, gpu_ctx, world):
+    """SURVEY §8e, graph sharded by source row: the per-rank slices
+    (pump_build_graph_rows, what each rank builds before the NCCL gather)
+    concatenate to the full graph bit for bit, and row_ptr is their sum."""
+    from paper_1607_06886_b200 import api
+
+    txt = with_samples("quad3d_indoor", 500)
+    j = json.loads(txt)
+    _, sc = oracle_lib.scenario_models(txt)
+    pos, vel = oracle_lib.scenario_nodes(txt)
+    args = (ws_of(j), goal_of(j), sc["r_n"], sc["dt"], sc["eps_cc"], sc["tau_max"])
+    full = api.build_graph(pos, vel, *args, ctx=gpu_ctx).export()
+    n = pos.shape[0]
+    parts = []
+    for r in range(world):
+        lo, hi = api.shard_range(n, r, world)
+        parts.append(api.build_graph_rows(pos, vel, *args, lo, hi, ctx=gpu_ctx).export())
+    row_ptr = sum(p["row_ptr"].astype(np.int64) for p in parts)
+    assert np.array_equal(row_ptr, full["row_ptr"])
+    for k in ("edge_to", "edge_nsteps", "hs_fallback"):
+        assert np.array_equal(np.concatenate([p[k] for p in parts]), full[k]), k
+    for k in ("edge_cost", "edge_tau", "edge_acc0", "edge_jerk", "hs_a", "hs_b"):
+        assert np.array_equal(np.concatenate([p[k] for p in parts]).view(np.uint64), full[k].view(np.uint64)), k
+    # CSR offsets: each slice starts at 0
+    wp, hs, wbase, hbase = [np.zeros(1, np.int64)], [np.zeros(1, np.int64)], 0, 0
+    for p in parts:
+        wp.append(p["edge_wp_off"][1:] + wbase)
+        hs.append(p["wp_hs_off"][1:] + hbase)
+        wbase += int(p["edge_wp_off"][-1])
+        hbase += int(p["wp_hs_off"][-1])
+    assert np.array_equal(np.concatenate(wp), full["edge_wp_off"])
+    assert np.array_equal(np.concatenate(hs), full["wp_hs_off"])
