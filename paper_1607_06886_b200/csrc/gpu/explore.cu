@@ -1204,7 +1204,8 @@ void run_explore_device(DevExplore& X, Ctx& c, const DevGraph& G, const ExploreA
   {
     int per_sm = 0, sms = 0, coop_attr = 0;
     PUMP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, coop_fn, kCoopBlock, 0));
-    per_sm = std::min(per_sm, 2);  // fewer blocks: cheaper grid barriers; the tail phases are small
+    static const int coop_per_sm = std::getenv("PUMP_COOP_PER_SM") ? std::atoi(std::getenv("PUMP_COOP_PER_SM")) : 1;
+    per_sm = std::min(per_sm, coop_per_sm);  // fewer blocks: cheaper grid barriers; the tail phases are small
     PUMP_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c.device));
     PUMP_CUDA(cudaDeviceGetAttribute(&coop_attr, cudaDevAttrCooperativeLaunch, c.device));
     coop_blocks = coop_attr ? per_sm * sms : 0;
