@@ -525,17 +525,86 @@ __host__ __device__ inline bool connect_dev(const double* ap, const double* av, 
     cost_out = 0.0;
     return true;
   }
+  // Lazy exact evaluation (exact-preserving).  With P = bp - ap, V = av and
+  // dv = bv - av the cost is, identically, the cubic in u = 1/tau
+  //   c = tau + 12 A u^3 + (-24 B - 12 E) u^2 + (12 C + 12 F + 4 D) u
+  // (A = |P|^2, B = P.V, C = |V|^2, E = P.dv, F = V.dv, D = |dv|^2).  Its
+  // value, computed without divisions, differs from the reference's
+  // evaluation (steer_cost) by far less than err = 1e-11 * S, S the sum of the
+  // absolute values of every constituent term (both evaluations err by a few
+  // ulps of S).  A comparison the reference makes is decided from the cubic
+  // when the two intervals [c - err, c + err] are disjoint, and from
+  // steer_cost otherwise, so every decision (scan argmin, golden-section
+  // branch) and every returned value is the reference's.
+  double cA = 0, cB = 0, cC = 0, cE = 0, cF = 0, cD = 0, aB = 0, aE = 0, aF = 0;
+#pragma unroll
+  for (int k = 0; k < DW; ++k) {
+    const double P = bp[k] - ap[k], V = av[k], dv = bv[k] - av[k];
+    cA += P * P;
+    cB += P * V;
+    cC += V * V;
+    cE += P * dv;
+    cF += V * dv;
+    cD += dv * dv;
+    aB += (P < 0 ? -P : P) * (V < 0 ? -V : V);
+    aE += (P < 0 ? -P : P) * (dv < 0 ? -dv : dv);
+    aF += (V < 0 ? -V : V) * (dv < 0 ? -dv : dv);
+  }
+  const double k3 = 12.0 * cA, k2 = -24.0 * cB - 12.0 * cE, k1 = 12.0 * cC + 12.0 * cF + 4.0 * cD;
+  const double s3 = 12.0 * cA, s2 = 24.0 * aB + 12.0 * aE, s1 = 12.0 * cC + 12.0 * aF + 4.0 * cD;
+  struct Lazy {
+    double tau, approx, err, exact;
+    bool known;
+  };
+  auto lazy = [&](double t) {
+    const double u = 1.0 / t;
+    Lazy z;
+    z.tau = t;
+    z.approx = t + ((k3 * u + k2) * u + k1) * u;
+    z.err = 1e-11 * (t + ((s3 * u + s2) * u + s1) * u);
+    z.known = false;
+    return z;
+  };
+  auto exact = [&](Lazy& z) {
+    if (!z.known) {
+      z.exact = steer_cost<DW>(ap, av, bp, bv, z.tau);
+      z.known = true;
+    }
+    return z.exact;
+  };
+  auto less = [&](Lazy& a, Lazy& b) {  // the reference's `f(a) < f(b)`
+    if (a.approx + a.err < b.approx - b.err) return true;
+    if (a.approx - a.err > b.approx + b.err) return false;
+    return exact(a) < exact(b);
+  };
   const double tau_lo = tau_max * 1e-7;
-  double best_tau = tau_lo, best_c = steer_cost<DW>(ap, av, bp, bv, tau_lo);
+  // scan: an upper bound of the minimum from the cubic, then exact costs only
+  // where the cubic cannot rule the point out, in index order with the
+  // reference's strict update (the first index attaining the minimum)
+  double m_hi = __builtin_inf();
+  {
+    double tau = tau_lo;
+    for (int i = 0; i < 64; ++i) {
+      if (i > 0) tau *= ratio;
+      const Lazy z = lazy(tau);
+      const double h = z.approx + z.err;
+      m_hi = h < m_hi ? h : m_hi;
+    }
+  }
+  double best_tau = tau_lo, best_c = __builtin_inf();
   int best_idx = 0;
-  double tau = tau_lo;
-  for (int i = 1; i < 64; ++i) {
-    tau *= ratio;
-    const double c = steer_cost<DW>(ap, av, bp, bv, tau);
-    if (c < best_c) {
-      best_c = c;
-      best_tau = tau;
-      best_idx = i;
+  {
+    double tau = tau_lo;
+    for (int i = 0; i < 64; ++i) {
+      if (i > 0) tau *= ratio;
+      Lazy z = lazy(tau);
+      if (z.approx - z.err > m_hi) continue;  // above the minimum
+      const double c = exact(z);
+      if (c < best_c) {
+        best_c = c;
+        best_tau = tau;
+        best_idx = i;
+      }
     }
   }
   double lo = best_tau / (best_idx > 0 ? ratio : 1.0);
@@ -556,20 +625,20 @@ __host__ __device__ inline bool connect_dev(const double* ap, const double* av, 
   }
   const double gr = 0.5 * (sqrt(5.0) - 1.0);
   double x1 = hi - gr * (hi - lo), x2 = lo + gr * (hi - lo);
-  double f1 = steer_cost<DW>(ap, av, bp, bv, x1), f2 = steer_cost<DW>(ap, av, bp, bv, x2);
+  Lazy f1 = lazy(x1), f2 = lazy(x2);
   while (hi - lo > 1e-9 * hi) {
-    if (f1 < f2) {
+    if (less(f1, f2)) {
       hi = x2;
       x2 = x1;
       f2 = f1;
       x1 = hi - gr * (hi - lo);
-      f1 = steer_cost<DW>(ap, av, bp, bv, x1);
+      f1 = lazy(x1);
     } else {
       lo = x1;
       x1 = x2;
       f1 = f2;
       x2 = lo + gr * (hi - lo);
-      f2 = steer_cost<DW>(ap, av, bp, bv, x2);
+      f2 = lazy(x2);
     }
   }
   tau_out = 0.5 * (lo + hi);

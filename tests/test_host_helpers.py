@@ -50,9 +50,17 @@ def test_connect_and_motion_collides_match_oracle(oracle_lib, dw):
     rng = np.random.default_rng(5 + dw)
     ws = _world(rng, dw, 12)
     n_hit = n_free = 0
-    for _ in range(300):
+    for trial in range(1500):
         ap, bp = rng.uniform(0.5, 9.5, size=(2, dw))
         av, bv = rng.normal(size=(2, dw))
+        if trial % 5 == 1:  # near-equal states / aligned motion: flat cost curves, near-ties
+            bp = ap + rng.normal(size=dw) * 1e-3
+            bv = av + rng.normal(size=dw) * 1e-4
+        elif trial % 5 == 2:
+            av = np.zeros(dw)
+            bv = np.zeros(dw)
+        elif trial % 5 == 3:
+            bp = ap + av * rng.uniform(0.1, 3.0)
         g = api.connect(ap, av, bp, bv, 5.0)
         e = oracle_lib.connect(ap, av, bp, bv, 5.0)
         assert g["ok"] == e["ok"]
