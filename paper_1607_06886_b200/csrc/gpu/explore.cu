@@ -52,6 +52,7 @@ struct ExpandArgs {
   const int32_t* t_end;
   const uint64_t* mask;
   const double* dy;
+  const double* bank_box;  // per bank row: particle box lo[DW], hi[DW]
   int N, horizon, W;
   double alpha_max;
   uint8_t* keep;
@@ -147,13 +148,42 @@ __device__ __forceinline__ void expand_task(const ExpandArgs& a, int64_t task, i
   const int total = __shfl_sync(0xffffffffu, incl, 31);
   if (ns <= 32 && total <= kExpStage) {
     const int my_pre = incl - my_cnt;
+    // Each lane stages its waypoint's half-spaces and decides which of them
+    // can kill any particle of the bank row the waypoint reads: with the
+    // row's per-axis particle box [lo, hi], fl(a_k p_k) <= M_k =
+    // max(fl(a_k lo_k), fl(a_k hi_k)) by monotone rounding, and the sum is
+    // formed in the test's order, so bound <= b proves s <= b (no kill) for
+    // every particle of the row, bit-exactly.  Waypoints without such a
+    // half-space skip the row load and the tests.
+    uint64_t my_need = 0;
+    const double* box = my_cnt > 0 ? a.bank_box + static_cast<int64_t>(pt + lane + 1) * 2 * DW : nullptr;
+    double blo[DW], bhi[DW];
+    if (my_cnt > 0) {
+#pragma unroll
+      for (int k = 0; k < DW; ++k) {
+        blo[k] = box[k];
+        bhi[k] = box[DW + k];
+      }
+    }
     for (int q = 0; q < my_cnt; ++q) {
-      s_hs[wib][my_pre + q][0] = hpk[(my_h0 + q) * 2];
-      s_hs[wib][my_pre + q][1] = hpk[(my_h0 + q) * 2 + 1];
+      const double2 q0 = hpk[(my_h0 + q) * 2], q1 = hpk[(my_h0 + q) * 2 + 1];
+      s_hs[wib][my_pre + q][0] = q0;
+      s_hs[wib][my_pre + q][1] = q1;
+      const double av[3] = {q0.x, q0.y, q1.x};
+      double bound = 0;
+#pragma unroll
+      for (int k = 0; k < DW; ++k) {
+        const double m1 = av[k] * blo[k], m2 = av[k] * bhi[k];
+        const double mk = m1 > m2 ? m1 : m2;
+        bound = k == 0 ? mk : bound + mk;
+      }
+      if (bound > q1.y) my_need |= 1ull << q;
     }
     __syncwarp();
-    tests = total;
-    unsigned live = __ballot_sync(0xffffffffu, my_cnt > 0);  // waypoints with half-spaces
+    unsigned live = __ballot_sync(0xffffffffu, my_need != 0);  // waypoints whose row can lose a particle
+    tests = __popcll(my_need);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) tests += __shfl_xor_sync(0xffffffffu, tests, o);
     double p[CH][DW], pn[CH][DW];
     int j = live ? __ffs(live) - 1 : -1;
     if (j >= 0) load_row<DW, CH>(a.dy + static_cast<int64_t>(pt + j + 1) * a.N * DW, a.N, lane, p);
@@ -163,7 +193,9 @@ __device__ __forceinline__ void expand_task(const ExpandArgs& a, int64_t task, i
       if (jn >= 0) load_row<DW, CH>(a.dy + static_cast<int64_t>(pt + jn + 1) * a.N * DW, a.N, lane, pn);
       const int cnt = __shfl_sync(0xffffffffu, my_cnt, j);
       const int pre = __shfl_sync(0xffffffffu, incl, j) - cnt;
-      for (int h = 0; h < cnt; ++h) hs_test<DW, CH>(s_hs[wib][pre + h][0], s_hs[wib][pre + h][1], p, kill);
+      const uint64_t need = __shfl_sync(0xffffffffu, my_need, j);
+      for (int h = 0; h < cnt; ++h)
+        if ((need >> h) & 1ull) hs_test<DW, CH>(s_hs[wib][pre + h][0], s_hs[wib][pre + h][1], p, kill);
       if (jn >= 0) {
 #pragma unroll
         for (int c = 0; c < CH; ++c)
@@ -1061,6 +1093,35 @@ __global__ void __launch_bounds__(kCoopBlock, 2) k_round_tail(const CoopArgs A) 
   STAMP();
 }
 
+// per bank row t: the particles' per-axis box lo[DW], hi[DW] (expand's no-kill test)
+__global__ void __launch_bounds__(128) k_bank_box(const double* __restrict__ dy, int n, int dw,
+                                                  double* __restrict__ box) {
+  const int t = blockIdx.x;
+  __shared__ double s_lo[128][3], s_hi[128][3];
+  double lo[3] = {__builtin_inf(), __builtin_inf(), __builtin_inf()}, hi[3] = {-lo[0], -lo[1], -lo[2]};
+  for (int i = threadIdx.x; i < n; i += blockDim.x)
+    for (int k = 0; k < dw; ++k) {
+      const double v = dy[(static_cast<int64_t>(t) * n + i) * dw + k];
+      lo[k] = v < lo[k] ? v : lo[k];
+      hi[k] = v > hi[k] ? v : hi[k];
+    }
+  for (int k = 0; k < 3; ++k) {
+    s_lo[threadIdx.x][k] = lo[k];
+    s_hi[threadIdx.x][k] = hi[k];
+  }
+  __syncthreads();
+  if (threadIdx.x < dw) {
+    const int k = threadIdx.x;
+    double a = __builtin_inf(), b = -__builtin_inf();
+    for (int x = 0; x < static_cast<int>(blockDim.x); ++x) {
+      a = s_lo[x][k] < a ? s_lo[x][k] : a;
+      b = s_hi[x][k] > b ? s_hi[x][k] : b;
+    }
+    box[static_cast<int64_t>(t) * 2 * dw + k] = a;
+    box[static_cast<int64_t>(t) * 2 * dw + dw + k] = b;
+  }
+}
+
 static void swap_buf(DBuf& a, DBuf& b) {
   std::swap(a.p, b.p);
   std::swap(a.cap, b.cap);
@@ -1109,6 +1170,10 @@ void run_explore_device(DevExplore& X, Ctx& c, const DevGraph& G, const ExploreA
     while (p < q) p <<= 1;
     return p;
   }();
+  // particle box of every bank row (k_expand skips rows no half-space can cut)
+  DBuf& box = c.buf("x_bank_box", al(static_cast<size_t>(c.bank_horizon + 2) * 2 * G.dw * 8));
+  k_bank_box<<<c.bank_horizon + 1, 128, 0, st>>>(c.bank.as<double>(), N, G.dw, box.as<double>());
+  ++c.launches;
   X.n_plans = 0;  // buffers (and their capacity) persist across solves
   ensure_arena(X, 1 << 16, st);
   if (!X.status_h) PUMP_CUDA(cudaMallocHost(&X.status_h, sizeof(ExploreStatus)));
@@ -1273,7 +1338,8 @@ void run_explore_device(DevExplore& X, Ctx& c, const DevGraph& G, const ExploreA
                         G.row_ptr.as<int64_t>(), G.e_to.as<int32_t>(), G.e_cost.as<double>(),
                         G.e_nsteps.as<int32_t>(), G.wp_off.as<int64_t>(), G.hs_off.as<int64_t>(),
                         G.hs_cnt.as<int32_t>(), G.hs_pk.as<double>(), X.head.as<int32_t>(), X.cost.as<double>(),
-                        X.t_end.as<int32_t>(), X.mask.as<uint64_t>(), c.bank.as<double>(), N, c.bank_horizon, W,
+                        X.t_end.as<int32_t>(), X.mask.as<uint64_t>(), c.bank.as<double>(), box.as<double>(), N,
+                        c.bank_horizon, W,
                         prm.alpha_max, X.cand_keep.as<uint8_t>(), X.cand_head.as<int32_t>(),
                         X.cand_src.as<int32_t>(), X.cand_tend.as<int32_t>(), X.cand_cost.as<double>(),
                         X.cand_cp.as<double>(), X.cand_mask.as<uint64_t>(), S};
@@ -1364,7 +1430,8 @@ void run_explore_device(DevExplore& X, Ctx& c, const DevGraph& G, const ExploreA
                       G.e_to.as<int32_t>(), G.e_cost.as<double>(), G.e_nsteps.as<int32_t>(), G.wp_off.as<int64_t>(),
                       G.hs_off.as<int64_t>(), G.hs_cnt.as<int32_t>(), G.hs_pk.as<double>(),
                       X.head.as<int32_t>(),
-                      X.cost.as<double>(), X.t_end.as<int32_t>(), X.mask.as<uint64_t>(), c.bank.as<double>(), N,
+                      X.cost.as<double>(), X.t_end.as<int32_t>(), X.mask.as<uint64_t>(), c.bank.as<double>(),
+                    box.as<double>(), N,
                       c.bank_horizon, W, prm.alpha_max, X.cand_keep.as<uint8_t>(), X.cand_head.as<int32_t>(),
                       X.cand_src.as<int32_t>(), X.cand_tend.as<int32_t>(), X.cand_cost.as<double>(),
                       X.cand_cp.as<double>(), X.cand_mask.as<uint64_t>(), S};
