@@ -33,21 +33,18 @@ import time
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-FAMILIES = ["bank_noise", "bank_rec", "hsmc", "mc", "connect", "collide", "emit", "regions", "expand", "commit",
+FAMILIES = ["bank_noise", "bank_rec", "hsmc", "mc", "connect", "collide", "emit", "regions", "expand", "round_tail",
             "dom", "scan", "multisplit", "misc", "pair_filter", "mc_table"]
 
 
-def mc_ops_per_step(d: int, dw: int, n_obs: int, segs: float = 3.0) -> float:
-    """Algorithmic FP64 arithmetic per MC rollout-step (compares excluded),
-    counting only the non-zero terms of the axis-separable closed loop the
-    kernel evaluates (so the figure is not inflated by structural zeros):
-    (d + dw) normals x 92 ops (2 unit maps, log 28, cos 56, sqrt, scaling);
-    per axis the 2x2 Sv, 1x1 Sw, 4x2 Gv, 4x1 Gw, 4x4 F blocks, the state sum
-    and the output map (79 ops); the segment length (11) and the segment
-    points (10 each, ~3 segments per step)."""
-    normals = (d + dw) * 92
-    gemv = 79 * dw
-    return normals + gemv + 11 + 10 * segs
+def mc_table_ops_per_step(d: int, dw: int) -> float:
+    """Algorithmic FP64 arithmetic per rollout-step of the MC table build
+    (compares excluded), counting only the non-zero terms of the
+    axis-separable closed loop the kernels evaluate: (d + dw) normals x 92 ops
+    (2 unit maps, log 28, cos 56 by the definition form, sqrt, scaling); per
+    axis the 2x2 Sv, 1x1 Sw, 4x2 Gv, 4x1 Gw, 4x4 F blocks, the state sum and
+    the output map (79 ops)."""
+    return (d + dw) * 92 + 79 * dw
 
 
 class ClockSampler:
@@ -322,30 +319,53 @@ def main():
                           "rollout_steps_per_s": round(n_mc * len(traj) / (ms * 1e-3), 1),
                           "cp": total / n_mc})
 
-    # ---- roofline of the dominant kernel family (CUDA events, profiled pass)
-    fam = int(np.argmax(prof_ms))
-    fam_name = FAMILIES[fam]
-    avg_launch_ms = prof_ms[fam] / max(1, prof_n[fam])
+    # ---- roofline of the dominant kernel family (CUDA events, profiled pass),
+    # plus the same figures for every family with a work model
     peak = C.c_double()
     L.pump_peak_fp64(ctx.h, C.byref(peak))
-    roof = {"kernel": fam_name, "bound": "fp64", "unit": "GFLOP/s", "peak": round(peak.value, 1),
-            "peak_source": "measured: bench FP64 DMUL+DADD issue microbenchmark (no FMA, the parity op mix); "
-                           "MEASURED_PEAKS.json has no FP64 figure",
-            "share_of_step": round(float(prof_ms[fam] / max(1e-9, prof_ms.sum())), 3),
-            "avg_launch_ms": round(float(avg_launch_ms), 4), "launches": int(prof_n[fam]), "traffic": None}
+    hbm = None
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            hbm = float(json.load(f)["hbm_gbs"])
+    except Exception:
+        hbm = None
     d, dw = 2 * len(scn["workspace"]["bounds"]["lo"]), len(scn["workspace"]["bounds"]["lo"])
-    if fam_name == "mc":
-        ops = prof_w[fam] * mc_ops_per_step(d, dw, len(scn["workspace"]["obstacles"]))
-        roof["work"] = f"{int(prof_w[fam])} rollout-steps x {mc_ops_per_step(d, dw, len(scn['workspace']['obstacles'])):.0f} FP64 ops"
-    elif fam_name == "expand":
-        ops = prof_w[fam] * 2 * dw
-        roof["work"] = f"{int(prof_w[fam])} particle-halfspace tests x {2 * dw} FP64 ops"
-    else:
-        ops = 0.0
-        roof["work"] = f"{int(prof_w[fam])} work units (no FP64 op model for this family yet)"
-    achieved = ops / (prof_ms[fam] * 1e-3) / 1e9 if prof_ms[fam] > 0 else 0.0
-    roof["achieved"] = round(achieved, 1)
-    roof["frac"] = round(achieved / peak.value, 4) if peak.value > 0 else None
+    n_obs = len(scn["workspace"]["obstacles"])
+
+    def roofline_of(fam):
+        name = FAMILIES[fam]
+        r = {"kernel": name, "bound": "fp64", "unit": "GFLOP/s", "peak": round(peak.value, 1),
+             "peak_source": "measured: bench FP64 DMUL+DADD issue microbenchmark (no FMA, the parity op mix); "
+                            "MEASURED_PEAKS.json has no FP64 figure",
+             "share_of_step": round(float(prof_ms[fam] / max(1e-9, prof_ms.sum())), 3),
+             "avg_launch_ms": round(float(prof_ms[fam] / max(1, prof_n[fam])), 4), "launches": int(prof_n[fam]),
+             "traffic": None}
+        t = prof_ms[fam] * 1e-3
+        if name == "mc_table":
+            opw = mc_table_ops_per_step(d, dw)
+            work = prof_w[fam] * opw
+            r["work"] = f"{int(prof_w[fam])} rollout-steps drawn x {opw:.0f} FP64 ops"
+        elif name == "expand":
+            work = prof_w[fam] * 2 * dw
+            r["work"] = f"{int(prof_w[fam])} particle-halfspace tests performed x {2 * dw} FP64 ops"
+        elif name == "round_tail":
+            r.update({"bound": "hbm", "unit": "GB/s", "peak": hbm,
+                      "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy bandwidth)"})
+            work = prof_w[fam]
+            r["work"] = f"{int(prof_w[fam])} algorithmic bytes (candidate records, arena writes, pool, group)"
+        else:
+            r["work"] = None
+            r["achieved"] = None
+            r["frac"] = None
+            return r
+        achieved = work / t / 1e9 if t > 0 else 0.0
+        r["achieved"] = round(achieved, 1)
+        r["frac"] = round(achieved / r["peak"], 5) if r.get("peak") else None
+        return r
+
+    roof = roofline_of(int(np.argmax(prof_ms)))
+    rooflines = [roofline_of(FAMILIES.index(f)) for f in ("expand", "round_tail", "mc_table")
+                 if prof_n[FAMILIES.index(f)] > 0]
     kernels = {FAMILIES[i]: {"ms_per_step": round(float(prof_ms[i] / args.steps), 3),
                              "launches_per_step": round(float(prof_n[i] / args.steps), 1)}
                for i in range(len(FAMILIES)) if prof_n[i] > 0}
@@ -385,7 +405,7 @@ def main():
                            "note": "run_pump with a prebuilt graph (graph built once from the scenario's nodes)"},
         "gpu_launches": int(launches // args.steps), "gpu_launches_total": int(launches),
         "device_allocs_timed": int(io1[3] - io0[3] + e_io1[3] - e_io0[3]),
-        "clocks": clk, "roofline": roof, "cpu_baseline": cpu, "kernels": kernels,
+        "clocks": clk, "roofline": roof, "rooflines": rooflines, "cpu_baseline": cpu, "kernels": kernels,
         "solve": {"success": res["success"], "cost": res["cost"], "certified_cp": res["certified_cp"],
                   "partial_plans": res["partial_plans"], "n_edges": res["n_edges"], "n_plans": res["n_plans"],
                   "build_graph_ms": round(1e3 * res["build_graph_seconds"], 3),

@@ -1545,9 +1545,18 @@ void run_explore_device(DevExplore& X, Ctx& c, const DevGraph& G, const ExploreA
     }
     c.d2h(X.status_h, S, sizeof(ExploreStatus));
     c.sync();
+    const ExploreStatus hp = h;
     h = *X.status_h;
     X.n_plans = h.n_plans;
     if (h.err) throw std::runtime_error("explore: device error " + std::to_string(h.err));
+    {
+      // algorithmic bytes of the round after expand (SURVEY §8d K_merge/K_dom/
+      // K_bucket): candidate records read and ranked, kept plans written to the
+      // arena, node sizes, the pool scanned, the new group read
+      const int64_t Tr = hp.T, Kr = h.K;
+      kprof_work(F_COMMIT, Tr * (37 + 8 * W) + Kr * (33 + 8 * W) + static_cast<int64_t>(n) * 16 +
+                               (hp.pool_n + Kr) * 9 + h.G * 28);
+    }
     if (prm.on_round) prm.on_round(h);
   }
   X.kernel_ms = c.toc();

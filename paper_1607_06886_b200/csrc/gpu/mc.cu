@@ -1004,6 +1004,7 @@ static bool ensure_table(McTable& tab, const HostLoop& HL, int64_t r0, int64_t r
                                                                          tab.dy.as<double>(), tab.z.as<double>());
     });
   }
+  kprof_work(F_MC_TABLE, n * static_cast<int64_t>(T + 1 - t_from));  // rollout-steps drawn
   // per-step max deviation of the new rows (the certification's skip test)
   const size_t md_bytes = static_cast<size_t>(T + 1) * dw * 8;
   if (md_bytes > tab.maxdev.cap) tab.maxdev.grow(md_bytes * 2, static_cast<size_t>(t_from) * dw * 8, st);
