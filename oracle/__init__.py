@@ -393,3 +393,23 @@ def run_pump(json_text: str, workers: int = 1, prebuilt: Graph | None = None) ->
                traj_pos=tp, traj_vel=tv, traj_ctrl=tu)
     out["termination"] = A.TERMINATION[out["termination"]]
     return out
+
+
+def repeated_rrt(json_text: str, trials: int = 0, alpha: float = -1.0, n_mc: int = 0, workers: int = 1) -> dict:
+    """rrt.hpp:50-147 on the scenario (trials / alpha / n_mc <= defaults: the scenario's)."""
+    import json as _json
+
+    dw = len(_json.loads(json_text)["workspace"]["bounds"]["lo"])
+    L = lib()
+    L.oracle_repeated_rrt.argtypes = [C.c_char_p, C.c_int, C.c_double, C.c_int, C.c_int] + [C.c_void_p] * 2 + \
+        [C.c_int32] + [C.c_void_p] * 5
+    out3, out2, n = np.zeros(3), np.zeros(2, dtype=np.int32), C.c_int32()
+    _check(L.oracle_repeated_rrt(json_text.encode(), trials, alpha, n_mc, workers, _p(out3), _p(out2), 0, None, None,
+                                 None, None, C.byref(n)))
+    m = n.value
+    t, pos, vel, u = np.zeros(m), np.zeros((m, dw)), np.zeros((m, dw)), np.zeros((m, dw))
+    _check(L.oracle_repeated_rrt(json_text.encode(), trials, alpha, n_mc, workers, _p(out3), _p(out2), m, _p(t),
+                                 _p(pos), _p(vel), _p(u), C.byref(n)))
+    return {"success": bool(out3[0]), "cost": float(out3[1]), "certified_cp": float(out3[2]),
+            "trials_reaching_goal": int(out2[0]), "certification_attempts": int(out2[1]),
+            "traj_t": t, "traj_pos": pos, "traj_vel": vel, "traj_ctrl": u}

@@ -685,3 +685,40 @@ int oracle_waypoints(int dw, const double* fp, const double* fv, const double* t
   return static_cast<int>(w.size());
 }
 }
+
+// ------------------------------------------------------------ repeated_rrt
+// rrt.hpp:50-147 for a scenario; trials <= 0 / alpha < 0 / n_mc <= 0 take the
+// scenario's rrt.trials / alpha / mc_samples.  out3 = {success, cost,
+// certified_cp}, out2 = {trials_reaching_goal, certification_attempts};
+// the trajectory (when successful) into t / pos / vel / u (cap points).
+extern "C" int oracle_repeated_rrt(const char* json_text, int trials, double alpha, int n_mc, int workers, double* out3,
+                                   int32_t* out2, int32_t cap, double* t, double* pos, double* vel, double* u,
+                                   int32_t* n_pts) {
+  return guard([&] {
+    pumpb::Scenario s = pumpb::parse_scenario_text(json_text);
+    RrtIn in;
+    in.p = pump_in_from(s);
+    in.trials = s.rrt.trials;
+    in.max_iterations = s.rrt.max_iterations;
+    in.goal_bias = s.rrt.goal_bias;
+    in.seed_rrt = s.seeds.rrt;
+    const RrtOut r = repeated_rrt(in, trials > 0 ? trials : s.rrt.trials, alpha >= 0 ? alpha : s.alpha,
+                                  n_mc > 0 ? n_mc : s.mc_samples, workers);
+    out3[0] = r.success ? 1.0 : 0.0;
+    out3[1] = r.cost;
+    out3[2] = r.certified_cp;
+    out2[0] = r.trials_reaching_goal;
+    out2[1] = r.certification_attempts;
+    *n_pts = static_cast<int32_t>(r.traj.size());
+    const int dw = s.workspace_dim();
+    if (static_cast<int>(r.traj.size()) > cap) return;
+    for (std::size_t i = 0; i < r.traj.size(); ++i) {
+      if (t) t[i] = r.traj[i].t;
+      for (int k = 0; k < dw; ++k) {
+        if (pos) pos[i * dw + k] = r.traj[i].s.p[k];
+        if (vel) vel[i * dw + k] = r.traj[i].s.v[k];
+        if (u) u[i * dw + k] = r.traj[i].u[k];
+      }
+    }
+  });
+}

@@ -1054,4 +1054,154 @@ PumpOut run_pump(const PumpIn& in, int workers, const Graph* prebuilt) {  // pum
   return res;
 }
 
+// ================================================================ rrt.hpp
+// Accumulated cost of the prefix [0, s] of a motion (steer.hpp:214-225).
+double motion_partial_cost(const Mot& m, double s) {
+  if (s <= 0) return 0;
+  s = std::min(s, m.tau);
+  double c = s;
+  for (std::size_t k = 0; k < m.acc0.size(); ++k) {
+    const double a = m.acc0[k], j = m.jerk[k];
+    c += a * a * s + a * j * s * s + j * j * s * s * s / 3;
+  }
+  return c;
+}
+
+// Prefix of a motion cut so its accumulated cost equals target_cost (:228-243).
+Mot truncate_motion(const Mot& m, double target_cost) {
+  if (!m.ok || m.cost <= target_cost) return m;
+  double lo = 0, hi = m.tau;
+  for (int it = 0; it < 60; ++it) {
+    const double mid = 0.5 * (lo + hi);
+    if (motion_partial_cost(m, mid) < target_cost)
+      lo = mid;
+    else
+      hi = mid;
+  }
+  Mot out = m;
+  out.tau = 0.5 * (lo + hi);
+  out.to = state_at(m, out.tau);
+  out.cost = motion_partial_cost(m, out.tau);
+  return out;
+}
+
+namespace {
+St rrt_sample(const RrtIn& in, std::uint64_t seed, std::uint64_t trial, std::uint64_t iter) {  // rrt.hpp:27-44
+  const int dw = in.p.w.dw;
+  St st;
+  st.p.resize(dw);
+  st.v.resize(dw);
+  const double bias = uniform(seed, trial, iter, 0);
+  const bool g = bias < in.goal_bias;
+  const double* lo = g ? in.p.goal.lo.data() : in.p.w.blo.data();
+  const double* hi = g ? in.p.goal.hi.data() : in.p.w.bhi.data();
+  const double vmax = g ? in.p.goal.max_speed : in.p.max_speed;
+  for (int k = 0; k < dw; ++k) {
+    const double u = uniform(seed, trial, iter, 1 + k);
+    st.p[k] = lo[k] + u * (hi[k] - lo[k]);
+    const double v = uniform(seed, trial, iter, 1 + dw + k);
+    st.v[k] = -vmax + v * 2 * vmax;
+  }
+  return st;
+}
+
+double sqn_diff(const Vec& a, const Vec& b) {  // Eigen squaredNorm of a - b: sequential from +0
+  double s = 0;
+  for (std::size_t k = 0; k < a.size(); ++k) {
+    const double d = a[k] - b[k];
+    s += d * d;
+  }
+  return s;
+}
+}  // namespace
+
+// Goal-biased kinodynamic RRT, repeated independent trials (rrt.hpp:50-147).
+RrtOut repeated_rrt(const RrtIn& in, int trials, double alpha, int n_mc, int workers) {
+  if (trials < 1) throw std::invalid_argument("repeated_rrt: trials must be at least 1");
+  const PumpIn& P = in.p;
+  const int dw = P.w.dw;
+  const double ratio = scan_ratio(P.tau_max);
+  struct Node {
+    St s;
+    int parent = -1;
+    Mot incoming;
+  };
+  struct Outcome {
+    bool reached = false;
+    std::vector<Wp> traj;
+    double cost = 0;
+  };
+  std::vector<Outcome> outcomes(trials);
+  parallel_for(trials, workers, [&](std::size_t lo, std::size_t hi) {
+    for (std::size_t trial = lo; trial < hi; ++trial) {
+      std::vector<Node> tree;
+      tree.push_back({P.x_init, -1, {}});
+      for (int iter = 0; iter < in.max_iterations; ++iter) {
+        const St target = rrt_sample(in, in.seed_rrt, trial, iter);
+        if (!point_free(P.w, target.p.data())) continue;
+        int nearest = -1;
+        double best_d = std::numeric_limits<double>::infinity();
+        for (int ni = 0; ni < static_cast<int>(tree.size()); ++ni) {
+          const double dist = sqn_diff(tree[ni].s.p, target.p) + sqn_diff(tree[ni].s.v, target.v);
+          if (dist < best_d) {
+            best_d = dist;
+            nearest = ni;
+          }
+        }
+        const Mot toward = connect(tree[nearest].s, target, P.tau_max, ratio);
+        if (!toward.ok || toward.tau <= 0) continue;
+        const Mot step = truncate_motion(toward, P.r_n);
+        if (step.tau <= 0) continue;
+        if (motion_collides(P.w, step, P.eps_cc)) continue;
+        tree.push_back({step.to, nearest, step});
+        if (goal_contains(P.goal, tree.back().s)) {
+          std::vector<int> chain;
+          for (int id = static_cast<int>(tree.size()) - 1; id != -1; id = tree[id].parent) chain.push_back(id);
+          std::reverse(chain.begin(), chain.end());
+          std::vector<Wp> traj;
+          double offset = 0;
+          for (std::size_t j = 0; j < chain.size(); ++j) {
+            if (j == 0) {
+              traj.push_back({0.0, tree[chain[0]].s, Vec(dw, 0.0)});
+              continue;
+            }
+            auto wps = waypoints(tree[chain[j]].incoming, P.dt);
+            for (std::size_t k = 1; k < wps.size(); ++k) {
+              Wp wp = wps[k];
+              wp.t += offset;
+              traj.push_back(std::move(wp));
+            }
+            offset += tree[chain[j]].incoming.tau;
+          }
+          outcomes[trial].reached = true;
+          outcomes[trial].cost = trajectory_cost(traj);
+          outcomes[trial].traj = std::move(traj);
+          break;
+        }
+      }
+    }
+  });
+  RrtOut res;
+  std::vector<int> reached;
+  for (int t = 0; t < trials; ++t)
+    if (outcomes[t].reached) reached.push_back(t);
+  res.trials_reaching_goal = static_cast<int>(reached.size());
+  std::stable_sort(reached.begin(), reached.end(),
+                   [&](int a, int b) { return outcomes[a].cost < outcomes[b].cost; });
+  for (int t : reached) {
+    res.certification_attempts++;
+    std::vector<Vec> pos;
+    for (const auto& w : outcomes[t].traj) pos.push_back(w.s.p);
+    const double mc = static_cast<double>(mc_hits(pos, P.cl, P.w, 0, n_mc, P.seed_mc, P.eps_cc, workers)) / n_mc;
+    if (mc <= alpha) {
+      res.success = true;
+      res.traj = std::move(outcomes[t].traj);
+      res.cost = outcomes[t].cost;
+      res.certified_cp = mc;
+      break;
+    }
+  }
+  return res;
+}
+
 }  // namespace oracle

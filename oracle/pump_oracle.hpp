@@ -219,4 +219,21 @@ struct PumpIn {  // what run_pump needs from a Scenario (scenario.hpp:34-77)
 };
 PumpOut run_pump(const PumpIn& in, int workers, const Graph* prebuilt = nullptr);
 
+// ------------------------------------------------------------- rrt.hpp
+double motion_partial_cost(const Mot& m, double s);
+Mot truncate_motion(const Mot& m, double target_cost);
+struct RrtIn {
+  PumpIn p;
+  int trials = 1000, max_iterations = 200;
+  double goal_bias = 0.05;
+  std::uint64_t seed_rrt = 3;
+};
+struct RrtOut {
+  bool success = false;
+  std::vector<Wp> traj;
+  double cost = 0, certified_cp = 0;
+  int trials_reaching_goal = 0, certification_attempts = 0;
+};
+RrtOut repeated_rrt(const RrtIn& in, int trials, double alpha, int n_mc, int workers);
+
 }  // namespace oracle

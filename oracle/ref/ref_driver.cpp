@@ -9,6 +9,7 @@
 #include <string>
 
 #include "pump/pump.hpp"
+#include "pump/rrt.hpp"
 #include "pump/scenario.hpp"
 
 namespace {
@@ -80,6 +81,32 @@ int ref_run_pump(const char* text, int workers, double* scalars, int* path, int*
     const int dw = s.workspace_dim();
     *n_traj = static_cast<int>(r.trajectory.points.size());
     for (size_t i = 0; i < r.trajectory.points.size() && i < 100000; ++i) {
+      traj_t[i] = r.trajectory.points[i].t;
+      for (int k = 0; k < dw; ++k) traj_pos[i * dw + k] = r.trajectory.points[i].state.position[k];
+    }
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return 1;
+  }
+}
+
+// repeated_rrt (rrt.hpp:50-147): out4 = success, cost, certified_cp,
+// n_points; out2 = trials_reaching_goal, certification_attempts; trajectory
+// times / positions (cap points, positions n x dw)
+int ref_repeated_rrt(const char* text, int trials, double alpha, int n_mc, int workers, double* out4, int* out2,
+                     int cap, double* traj_t, double* traj_pos) {
+  try {
+    pump::Scenario s = scn(text);
+    pump::RrtResult r = pump::repeated_rrt(s, trials, alpha, n_mc, workers);
+    out4[0] = r.success ? 1.0 : 0.0;
+    out4[1] = r.cost;
+    out4[2] = r.certified_cp;
+    out4[3] = static_cast<double>(r.trajectory.points.size());
+    out2[0] = r.trials_reaching_goal;
+    out2[1] = r.certification_attempts;
+    const int dw = s.workspace_dim();
+    for (std::size_t i = 0; i < r.trajectory.points.size() && static_cast<int>(i) < cap; ++i) {
       traj_t[i] = r.trajectory.points[i].t;
       for (int k = 0; k < dw; ++k) traj_pos[i * dw + k] = r.trajectory.points[i].state.position[k];
     }

@@ -468,3 +468,25 @@ def test_glibc_and_portable_normals_give_the_same_decisions():
     rp = oracle.explore(g, bp, 0.01, 0.2, 0.5, 9.0, workers=W)
     for k in ("head", "parent", "cost", "cp_hat", "masks", "goal_plans"):
         assert np.array_equal(rg[k], rp[k]), k
+
+
+def test_repeated_rrt_kat(oracle_lib):
+    """test_plan.cpp:279-306: empty workspace succeeds (cost above the direct
+    connection to the reached end state), sealed goal fails."""
+    import json as _json
+
+    base = {"name": "rrt_kat", "workspace": {"bounds": {"lo": [-10, -10], "hi": [10, 10]}, "obstacles": []},
+            "start": {"position": [-5, 0], "velocity": [0, 0]},
+            "goal": {"lo": [4, -1], "hi": [6, 1], "max_speed": 0.5},
+            "noise": {"process": [0, 0, 0, 0], "measurement": 0, "initial": 0},
+            "dt": 0.25, "alpha": 0.05, "max_speed": 1.0, "connection_radius": 6.0, "mc_samples": 200,
+            "rrt": {"max_iterations": 80}, "samples": 10}
+    ok = oracle_lib.repeated_rrt(_json.dumps(base), 40, 0.05, 200, workers=4)
+    assert ok["success"] and len(ok["traj_t"]) > 0
+    end_p, end_v = ok["traj_pos"][-1], ok["traj_vel"][-1]
+    direct = oracle_lib.connect([-5, 0], [0, 0], end_p, end_v, 200.0)
+    assert ok["cost"] >= direct["cost"] - 1e-6
+    sealed = dict(base)
+    sealed["workspace"] = {"bounds": {"lo": [-10, -10], "hi": [10, 10]}, "obstacles": [{"lo": [3, -3], "hi": [7, 3]}]}
+    fail = oracle_lib.repeated_rrt(_json.dumps(sealed), 20, 0.05, 200, workers=4)
+    assert not fail["success"]

@@ -112,3 +112,47 @@ def test_run_pump_matches_reference(oracle_lib, name, kw):
             assert o["smoothing_s"] == r["smoothing_s"]
             assert np.array_equal(o["traj_t"], r["traj_t"])
             assert np.array_equal(o["traj_pos"].view(np.uint64), r["traj_pos"].view(np.uint64))
+
+
+def rrt_kat_text(obstacles=()):
+    """test_plan.cpp:279-306 setting: empty 2-D world, zero noise."""
+    return json.dumps({"name": "rrt_kat", "workspace": {"bounds": {"lo": [-10, -10], "hi": [10, 10]},
+                                                        "obstacles": [{"lo": o[0], "hi": o[1]} for o in obstacles]},
+                       "start": {"position": [-5, 0], "velocity": [0, 0]},
+                       "goal": {"lo": [4, -1], "hi": [6, 1], "max_speed": 0.5},
+                       "noise": {"process": [0, 0, 0, 0], "measurement": 0, "initial": 0},
+                       "dt": 0.25, "alpha": 0.05, "max_speed": 1.0, "connection_radius": 6.0, "mc_samples": 200,
+                       "rrt": {"max_iterations": 80}, "samples": 10})
+
+
+@pytest.mark.parametrize("case", ["kat", "minimal", "three_obstacle"])
+def test_repeated_rrt_matches_reference(oracle_lib, case):
+    """rrt.hpp:50-147: the oracle's repeated_rrt reproduces the literal
+    reference (glibc normals for the MC certification) bit for bit."""
+    L = ref()
+    L.ref_repeated_rrt.argtypes = [C.c_char_p, C.c_int, C.c_double, C.c_int, C.c_int] + [C.c_void_p] * 2 + \
+        [C.c_int] + [C.c_void_p] * 2
+    if case == "kat":
+        txt, trials, n_mc = rrt_kat_text(), 40, 200
+    else:
+        txt, trials, n_mc = variant(case, mc_samples=2000), 60, 2000
+    alpha = json.loads(txt).get("alpha", 0.05)
+    workers = min(8, os.cpu_count() or 2)
+    o4, o2 = np.zeros(4), np.zeros(2, dtype=np.int32)
+    tt, tp = np.zeros(100000), np.zeros(300000)
+    rc = L.ref_repeated_rrt(txt.encode(), trials, alpha, n_mc, workers, _p(o4), _p(o2), 100000, _p(tt), _p(tp))
+    assert rc == 0, L.ref_last_error()
+    oracle_lib.set_normal_mode(oracle_lib.GLIBC)
+    try:
+        o = oracle_lib.repeated_rrt(txt, trials, alpha, n_mc, workers=workers)
+    finally:
+        oracle_lib.set_normal_mode(oracle_lib.PORTABLE)
+    assert o["success"] == bool(o4[0])
+    assert o["trials_reaching_goal"] == o2[0] and o["certification_attempts"] == o2[1]
+    assert o["cost"] == o4[1] and o["certified_cp"] == o4[2]
+    n = int(o4[3])
+    dw = len(json.loads(txt)["workspace"]["bounds"]["lo"])
+    assert np.array_equal(o["traj_t"], tt[:n])
+    assert np.array_equal(o["traj_pos"].view(np.uint64), tp[:n * dw].reshape(-1, dw).view(np.uint64))
+    if case == "kat":
+        assert o["success"] and o["trials_reaching_goal"] > 0
