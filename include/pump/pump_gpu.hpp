@@ -1208,6 +1208,46 @@ inline PumpResult run_pump(const Scenario& s, int workers = 1, const SampleGraph
   return r;
 }
 
+// ============================================================== rrt.hpp
+struct RrtResult {  // rrt.hpp:11-18
+  bool success = false;
+  Trajectory trajectory;
+  double cost = 0;
+  double certified_cp = 0;
+  int trials_reaching_goal = 0;
+  int certification_attempts = 0;
+};
+
+// repeated_rrt (rrt.hpp:50-147): the trials run on the GPU (one warp each),
+// certification in cost order on the GPU; `workers` is accepted, unused
+inline RrtResult repeated_rrt(const Scenario& s, int trials, double alpha, int n_mc, int workers = 1) {
+  (void)workers;
+  if (trials < 1) throw std::invalid_argument("repeated_rrt: trials must be at least 1");
+  const std::string text = detail::to_json(s).dump();
+  pump_scenario* sh = nullptr;
+  detail::check(pump_scenario_parse(text.c_str(), &sh));
+  std::unique_ptr<pump_scenario, int (*)(pump_scenario*)> sg(sh, pump_scenario_free);
+  pump_result* rh = nullptr;
+  detail::check(pump_rrt_run(detail::ctx(), sh, trials, alpha, n_mc, &rh));
+  std::unique_ptr<pump_result, int (*)(pump_result*)> rg(rh, pump_result_free);
+  pump_result_summary sum{};
+  detail::check(pump_result_summary_get(rh, &sum));
+  const int dw = sum.dw, nt = sum.n_traj_points;
+  std::vector<double> tt(nt + 1), tp(static_cast<size_t>(nt) * dw + 1), tv(tp.size()), tu(tp.size());
+  detail::check(pump_result_arrays(rh, nullptr, nullptr, nullptr, nullptr, nullptr, tt.data(), tp.data(), tv.data(),
+                                   tu.data()));
+  RrtResult r;
+  r.success = sum.success != 0;
+  r.cost = sum.cost;
+  r.certified_cp = sum.certified_cp;
+  r.trials_reaching_goal = sum.rrt_trials_reaching_goal;
+  r.certification_attempts = sum.rrt_certification_attempts;
+  for (int i = 0; i < nt; ++i)
+    r.trajectory.points.push_back({tt[i], {detail::vec(tp.data() + i * dw, dw), detail::vec(tv.data() + i * dw, dw)},
+                                   detail::vec(tu.data() + i * dw, dw)});
+  return r;
+}
+
 // ============================================================ report.hpp
 namespace detail {
 inline void write_text(const std::string& path, const std::string& text) {
@@ -1258,6 +1298,20 @@ inline Trajectory load_trajectory(const std::string& path) {
   json j;
   in >> j;
   return parse_trajectory(j);
+}
+
+inline json rrt_report_json(const Scenario& s, const RrtResult& r, int trials, int workers) {  // report.hpp:99-111
+  return {{"schema_version", 1},
+          {"scenario", s.name},
+          {"algorithm", "rrt"},
+          {"workers", workers},
+          {"success", r.success},
+          {"cost", r.cost},
+          {"certified_cp", r.certified_cp},
+          {"alpha", s.alpha},
+          {"trials", trials},
+          {"trials_reaching_goal", r.trials_reaching_goal},
+          {"certification_attempts", r.certification_attempts}};
 }
 
 inline json plan_report_json(const Scenario& s, const PumpResult& r, int workers) {  // report.hpp:72-97

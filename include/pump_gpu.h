@@ -132,6 +132,8 @@ typedef struct pump_result_summary {
   /* device-side breakdown (CUDA events), not in the reference report */
   double bank_ms, explore_kernel_ms, mc_ms;
   int64_t n_edges, n_plans, mc_rollouts;
+  /* repeated_rrt results (pump_rrt_run; 0 for pump_run) */
+  int32_t rrt_trials_reaching_goal, rrt_certification_attempts;
 } pump_result_summary;
 
 typedef struct pump_ctx pump_ctx;
@@ -214,6 +216,14 @@ int pump_scenario_closed_loop(const pump_scenario* s, int32_t* d, int32_t* dw, d
                               double* Sv, double* Sw, double* S0, double* C);
 /* JSON-scenario scalars: eps_cc, r_n, tau_max, alpha, eta, lambda, dt. */
 int pump_scenario_params(const pump_scenario* s, double out[8], int64_t iout[8]);
+/* repeated_rrt (rrt.hpp:50-147), the goal-biased kinodynamic RRT baseline of
+ * the paper's Table 1, on the GPU (one warp per trial) with the reference's
+ * certification order.  trials <= 0 / alpha < 0 / n_mc <= 0 take the
+ * scenario's rrt.trials / alpha / mc_samples.  The result carries success,
+ * cost, certified_cp, the trajectory (pump_result_arrays) and
+ * rrt_trials_reaching_goal / rrt_certification_attempts. */
+int pump_rrt_run(pump_ctx* ctx, const pump_scenario* scenario, int32_t trials, double alpha, int32_t n_mc,
+                 pump_result** out);
 /* The node set run_pump plans over (pump.hpp:184-189): x_init, then the
  * accepted Halton states (sample.hpp:56-89), then the appended goal sample if
  * any.  Writes n_out; fills pos/vel (n x dw, row-major) when both are given

@@ -62,7 +62,7 @@ EXPORTS = [
     "pump_explore_export", "pump_explore_free", "pump_run", "pump_result_summary_get", "pump_result_arrays",
     "pump_result_free", "pump_nccl_unique_id", "pump_ctx_set_comm", "pump_shard_range", "pump_ctx_profile",
     "pump_ctx_profile_read", "pump_ctx_io_bytes", "pump_ctx_flush_l2", "pump_peak_fp64", "pump_ctx_stream",
-    "pump_scenario_nodes", "pump_build_graph_rows",
+    "pump_scenario_nodes", "pump_build_graph_rows", "pump_rrt_run",
 ]
 
 
@@ -462,6 +462,31 @@ def run_pump(scenario: Scenario, prebuilt: Graph | None = None, ctx: Context | N
                traj_pos=tp, traj_vel=tv, traj_ctrl=tu)
     out["termination"] = A.TERMINATION[out["termination"]]
     return out
+
+
+def repeated_rrt(scenario: Scenario, trials: int = 0, alpha: float = -1.0, n_mc: int = 0,
+                 ctx: Context | None = None) -> dict:
+    """repeated_rrt (rrt.hpp:50-147) on the GPU: success, cost, certified_cp,
+    trials_reaching_goal, certification_attempts and the trajectory.  Zero /
+    negative arguments take the scenario's rrt.trials / alpha / mc_samples."""
+    ctx = ctx or default_context()
+    L = lib()
+    L.pump_rrt_run.argtypes = [C.c_void_p, C.c_void_p, C.c_int32, C.c_double, C.c_int32, C.c_void_p]
+    h = C.c_void_p()
+    _check(L.pump_rrt_run(ctx.h, scenario.h, trials, alpha, n_mc, C.byref(h)))
+    try:
+        s = A.ResultSummaryC()
+        _check(L.pump_result_summary_get(h, C.byref(s)))
+        dw, n = s.dw, s.n_traj_points
+        tt, tp, tv, tu = np.zeros(n), np.zeros((n, dw)), np.zeros((n, dw)), np.zeros((n, dw))
+        _check(L.pump_result_arrays(h, None, None, None, None, None, *[_p(x) if x.size else None
+                                                                       for x in (tt, tp, tv, tu)]))
+    finally:
+        L.pump_result_free(h)
+    return {"success": bool(s.success), "cost": s.cost, "certified_cp": s.certified_cp,
+            "trials_reaching_goal": s.rrt_trials_reaching_goal,
+            "certification_attempts": s.rrt_certification_attempts,
+            "traj_t": tt, "traj_pos": tp, "traj_vel": tv, "traj_ctrl": tu}
 
 
 # ---------------------------------------------------------------- multi-GPU

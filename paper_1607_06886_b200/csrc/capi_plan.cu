@@ -1033,6 +1033,340 @@ static void run_pump_device(Ctx& c, const pumpb::Scenario& s, const DevGraph* pr
   R.s.selection_seconds = secs(t2, clk::now());
 }
 
+// ==================================================================== RRT
+// repeated_rrt (rrt.hpp:50-147), the Table 1 baseline: one warp per trial.
+// Each iteration draws the target (counter-hash uniforms, rrt.hpp:27-44),
+// finds the nearest tree node (lanes over the nodes, warp argmin with the
+// first index on ties, as the reference's strict `<` scan), then lane 0
+// steers (connect, the graph build's code), truncates the motion at cost r_n
+// (steer.hpp:214-243) and checks it (motion_collides); the tree lives in
+// global memory.  The host assembles the reached trials' trajectories,
+// orders them by cost and certifies them in that order on the MC table.
+struct RrtArgs {
+  int trials, max_it, n_max;
+  uint64_t seed;
+  double goal_bias, max_speed, goal_ms, tau_max, ratio, r_n, eps_cc;
+  double blo[6], bhi[6], glo[6], ghi[6], x0p[6], x0v[6];
+  double* np;    // [trial][n_max][dw] node positions
+  double* nv;    // node velocities
+  int32_t* par;  // [trial][n_max]
+  double* itau;  // incoming motion: tau, acc0[dw], jerk[dw]
+  double* ia;
+  double* ij;
+  int32_t* reached;  // goal node index or -1
+};
+
+__device__ __forceinline__ double uniform_dev(uint64_t seed, uint64_t a, uint64_t b, uint64_t c) {
+  return to_unit(mix64(mix64(hash_seed_a(seed, a) + b) + c));
+}
+
+// motion_partial_cost (steer.hpp:214-225), the reference's operation order
+template <int DW>
+__host__ __device__ __forceinline__ double partial_cost(const double* a, const double* j, double tau, double s) {
+  if (s <= 0) return 0;
+  s = s < tau ? s : tau;
+  double c = s;
+#pragma unroll
+  for (int k = 0; k < DW; ++k) c += a[k] * a[k] * s + a[k] * j[k] * s * s + j[k] * j[k] * s * s * s / 3;
+  return c;
+}
+
+template <int DW>
+__global__ void __launch_bounds__(128) k_rrt(RrtArgs A, WorldD w) {
+  extern __shared__ double smem[];
+  const WorldD ws = stage_world<DW>(w, smem);
+  const int lane = threadIdx.x & 31;
+  const int trial = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (trial >= A.trials) return;
+  double* np = A.np + static_cast<int64_t>(trial) * A.n_max * DW;
+  double* nv = A.nv + static_cast<int64_t>(trial) * A.n_max * DW;
+  int32_t* par = A.par + static_cast<int64_t>(trial) * A.n_max;
+  double* itau = A.itau + static_cast<int64_t>(trial) * A.n_max;
+  double* ia = A.ia + static_cast<int64_t>(trial) * A.n_max * DW;
+  double* ij = A.ij + static_cast<int64_t>(trial) * A.n_max * DW;
+  if (lane == 0) {
+    for (int k = 0; k < DW; ++k) {
+      np[k] = A.x0p[k];
+      nv[k] = A.x0v[k];
+    }
+    par[0] = -1;
+    itau[0] = 0;
+  }
+  __syncwarp();
+  int n_nodes = 1, reached = -1;
+  for (int iter = 0; iter < A.max_it; ++iter) {
+    double tp[DW], tv[DW];
+    {
+      const double bias = uniform_dev(A.seed, trial, iter, 0);
+      const bool g = bias < A.goal_bias;
+      const double vmax = g ? A.goal_ms : A.max_speed;
+#pragma unroll
+      for (int k = 0; k < DW; ++k) {
+        const double lo = g ? A.glo[k] : A.blo[k], hi = g ? A.ghi[k] : A.bhi[k];
+        const double u = uniform_dev(A.seed, trial, iter, 1 + k);
+        tp[k] = lo + u * (hi - lo);
+        const double v = uniform_dev(A.seed, trial, iter, 1 + DW + k);
+        tv[k] = -vmax + v * 2 * vmax;
+      }
+    }
+    if (!point_free<DW>(ws, tp)) continue;
+    // nearest node: squaredNorm(p - tp) + squaredNorm(v - tv), first strict minimum
+    double bd = __builtin_inf();
+    int bi = 0x7fffffff;
+    for (int ni = lane; ni < n_nodes; ni += 32) {
+      double dp[DW], dv[DW];
+#pragma unroll
+      for (int k = 0; k < DW; ++k) {
+        dp[k] = np[ni * DW + k] - tp[k];
+        dv[k] = nv[ni * DW + k] - tv[k];
+      }
+      const double dist = sqnorm<DW>(dp) + sqnorm<DW>(dv);
+      if (dist < bd) {
+        bd = dist;
+        bi = ni;
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double od = __shfl_xor_sync(0xffffffffu, bd, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (od < bd || (od == bd && oi < bi)) {
+        bd = od;
+        bi = oi;
+      }
+    }
+    const int nearest = bi;
+    int added = 0;
+    if (lane == 0) {
+      double ap[DW], av[DW];
+#pragma unroll
+      for (int k = 0; k < DW; ++k) {
+        ap[k] = np[nearest * DW + k];
+        av[k] = nv[nearest * DW + k];
+      }
+      double tau = 0, cost = 0;
+      const bool ok = connect_dev<DW>(ap, av, tp, tv, A.tau_max, A.ratio, tau, cost);
+      if (ok && tau > 0) {
+        MotionD<DW> m;
+        m.tau = tau;
+#pragma unroll
+        for (int k = 0; k < DW; ++k) {
+          m.p0[k] = ap[k];
+          m.v0[k] = av[k];
+          m.p1[k] = tp[k];
+          m.v1[k] = tv[k];
+        }
+        coeffs_dev<DW>(ap, av, tp, tv, tau, m.a, m.j);
+        if (cost > A.r_n) {  // truncate_motion (steer.hpp:228-243)
+          double lo = 0, hi = tau;
+          for (int it = 0; it < 60; ++it) {
+            const double mid = 0.5 * (lo + hi);
+            if (partial_cost<DW>(m.a, m.j, tau, mid) < A.r_n)
+              lo = mid;
+            else
+              hi = mid;
+          }
+          const double tt = 0.5 * (lo + hi);
+          motion_state<DW>(m, tt, m.p1, m.v1);
+          m.tau = tt;
+        }
+        if (m.tau > 0 && !motion_collides<DW>(m, ws, A.eps_cc)) {
+          const int id = n_nodes;
+#pragma unroll
+          for (int k = 0; k < DW; ++k) {
+            np[id * DW + k] = m.p1[k];
+            nv[id * DW + k] = m.v1[k];
+            ia[id * DW + k] = m.a[k];
+            ij[id * DW + k] = m.j[k];
+          }
+          par[id] = nearest;
+          itau[id] = m.tau;
+          added = 1;
+          bool in = true;  // GoalRegion::contains (sample.hpp:26-28)
+#pragma unroll
+          for (int k = 0; k < DW; ++k) in = in && !(m.p1[k] < A.glo[k] || m.p1[k] > A.ghi[k]);
+          if (in && sqrt(sqnorm<DW>(m.v1)) <= A.goal_ms) added = 2;
+        }
+      }
+    }
+    added = __shfl_sync(0xffffffffu, added, 0);
+    __syncwarp();
+    if (added) {
+      ++n_nodes;
+      if (added == 2) {
+        reached = n_nodes - 1;
+        break;
+      }
+    }
+  }
+  if (lane == 0) A.reached[trial] = reached;
+}
+
+struct RrtOutcome {
+  bool success = false;
+  std::vector<HWp> traj;
+  double cost = 0, certified_cp = 0;
+  int reached = 0, attempts = 0;
+};
+
+static RrtOutcome run_rrt_device(Ctx& c, const pumpb::Scenario& s, int trials, double alpha, int n_mc) {
+  if (trials < 1) throw std::invalid_argument("repeated_rrt: trials must be at least 1");
+  c.mc_table.invalidate();
+  const int dw = s.workspace_dim();
+  pumpb::ModelBundle mb = s.models();
+  HostLoop L = loop_of(mb.cl);
+  HostWorld hw = host_world(s.workspace);
+  pump_workspace pw{dw, static_cast<int32_t>(s.workspace.obstacles.size()), s.workspace.bounds.lo.data(),
+                    s.workspace.bounds.hi.data(), hw.lo.data(), hw.hi.data()};
+  DevWorld dwld = upload_world(c, &pw, "rrt_ws_");
+  const int n_max = s.rrt.max_iterations + 1;
+  RrtArgs A{};
+  A.trials = trials;
+  A.max_it = s.rrt.max_iterations;
+  A.n_max = n_max;
+  A.seed = s.seeds.rrt;
+  A.goal_bias = s.rrt.goal_bias;
+  A.max_speed = s.max_speed;
+  A.goal_ms = s.goal_max_speed;
+  A.tau_max = s.effective_tau_max();
+  A.ratio = scan_ratio(A.tau_max);
+  A.r_n = s.effective_r_n();
+  A.eps_cc = s.effective_eps_cc();
+  for (int k = 0; k < dw; ++k) {
+    A.blo[k] = s.workspace.bounds.lo[k];
+    A.bhi[k] = s.workspace.bounds.hi[k];
+    A.glo[k] = s.goal.lo[k];
+    A.ghi[k] = s.goal.hi[k];
+    A.x0p[k] = s.start_pos[k];
+    A.x0v[k] = s.start_vel[k];
+  }
+  const size_t tn = static_cast<size_t>(trials) * n_max;
+  DBuf& bp = c.buf("rrt_np", al(tn * dw * 8));
+  DBuf& bv = c.buf("rrt_nv", al(tn * dw * 8));
+  DBuf& bpar = c.buf("rrt_par", al(tn * 4));
+  DBuf& btau = c.buf("rrt_tau", al(tn * 8));
+  DBuf& ba = c.buf("rrt_a", al(tn * dw * 8));
+  DBuf& bj = c.buf("rrt_j", al(tn * dw * 8));
+  DBuf& brc = c.buf("rrt_reached", al(static_cast<size_t>(trials) * 4));
+  A.np = bp.as<double>();
+  A.nv = bv.as<double>();
+  A.par = bpar.as<int32_t>();
+  A.itau = btau.as<double>();
+  A.ia = ba.as<double>();
+  A.ij = bj.as<double>();
+  A.reached = brc.as<int32_t>();
+  WorldD wd;
+  wd.n_obs = dwld.n_obs;
+  wd.lo = dwld.d_lo;
+  wd.hi = dwld.d_hi;
+  for (int k = 0; k < 6; ++k) {
+    wd.blo[k] = dwld.blo[k];
+    wd.bhi[k] = dwld.bhi[k];
+  }
+  const size_t wsmem = 2 * static_cast<size_t>(dwld.n_obs) * dw * sizeof(double);
+  dispatch_dw(dw, [&]<int DW>() {
+    if (wsmem > 48 * 1024)
+      PUMP_CUDA(cudaFuncSetAttribute(k_rrt<DW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wsmem));
+    k_rrt<DW><<<grid_for(static_cast<int64_t>(trials) * 32, 128), 128, wsmem, c.stream>>>(A, wd);
+  });
+  ++c.launches;
+  PUMP_CUDA(cudaGetLastError());
+  std::vector<int32_t> reached(trials);
+  c.d2h(reached.data(), brc.p, trials * 4);
+  c.sync();
+  // reached trials: walk the chain on the host and assemble the trajectory
+  // (rrt.hpp:95-113) from the nodes and incoming motions
+  struct Tr {
+    int trial;
+    std::vector<HWp> traj;
+    double cost;
+  };
+  std::vector<Tr> got;
+  std::vector<double> hp, hv, ht, ha, hj;
+  std::vector<int32_t> hpar;
+  for (int t = 0; t < trials; ++t) {
+    if (reached[t] < 0) continue;
+    const size_t base = static_cast<size_t>(t) * n_max;
+    const int nn = reached[t] + 1;
+    hp.resize(static_cast<size_t>(nn) * dw);
+    hv.resize(static_cast<size_t>(nn) * dw);
+    ha.resize(static_cast<size_t>(nn) * dw);
+    hj.resize(static_cast<size_t>(nn) * dw);
+    ht.resize(nn);
+    hpar.resize(nn);
+    c.d2h(hp.data(), bp.as<double>() + base * dw, nn * dw * 8);
+    c.d2h(hv.data(), bv.as<double>() + base * dw, nn * dw * 8);
+    c.d2h(ha.data(), ba.as<double>() + base * dw, nn * dw * 8);
+    c.d2h(hj.data(), bj.as<double>() + base * dw, nn * dw * 8);
+    c.d2h(ht.data(), btau.as<double>() + base, nn * 8);
+    c.d2h(hpar.data(), bpar.as<int32_t>() + base, nn * 4);
+    c.sync();
+    std::vector<int> chain;
+    for (int id = reached[t]; id != -1; id = hpar[id]) chain.push_back(id);
+    std::reverse(chain.begin(), chain.end());
+    Tr tr;
+    tr.trial = t;
+    double offset = 0;
+    for (size_t q = 0; q < chain.size(); ++q) {
+      const int id = chain[q];
+      if (q == 0) {
+        HWp w0{};
+        w0.t = 0.0;
+        for (int k = 0; k < dw; ++k) {
+          w0.p[k] = hp[id * dw + k];
+          w0.v[k] = hv[id * dw + k];
+        }
+        tr.traj.push_back(w0);
+        continue;
+      }
+      const int pid = hpar[id];
+      HMotion m{};
+      for (int k = 0; k < dw; ++k) {
+        m.p0[k] = hp[pid * dw + k];
+        m.v0[k] = hv[pid * dw + k];
+        m.p1[k] = hp[id * dw + k];
+        m.v1[k] = hv[id * dw + k];
+        m.a[k] = ha[id * dw + k];
+        m.j[k] = hj[id * dw + k];
+      }
+      m.tau = ht[id];
+      auto wps = motion_waypoints(m, dw, s.dt);
+      for (size_t k = 1; k < wps.size(); ++k) {
+        HWp wp = wps[k];
+        wp.t += offset;
+        tr.traj.push_back(wp);
+      }
+      offset += m.tau;
+    }
+    tr.cost = trajectory_cost(tr.traj, dw);
+    got.push_back(std::move(tr));
+  }
+  RrtOutcome out;
+  out.reached = static_cast<int>(got.size());
+  std::stable_sort(got.begin(), got.end(), [](const Tr& a, const Tr& b) { return a.cost < b.cost; });
+  // certify in cost order until one passes; batches of 8 certified together
+  // (the reference stops at the first pass: attempts = its position + 1)
+  constexpr size_t kBatch = 8;
+  for (size_t b0 = 0; b0 < got.size() && !out.success; b0 += kBatch) {
+    std::vector<std::vector<HWp>> batch;
+    for (size_t q = b0; q < std::min(got.size(), b0 + kBatch); ++q) batch.push_back(got[q].traj);
+    double mc_ms = 0;
+    int64_t rollouts = 0;
+    auto v = mc_values(c, L, dwld, batch, n_mc, s.seeds.mc, A.eps_cc, &mc_ms, &rollouts);
+    for (size_t q = 0; q < batch.size(); ++q) {
+      out.attempts++;
+      if (v[q] <= alpha) {
+        out.success = true;
+        out.traj = got[b0 + q].traj;
+        out.cost = got[b0 + q].cost;
+        out.certified_cp = v[q];
+        break;
+      }
+    }
+  }
+  return out;
+}
+
 }  // namespace pumpg
 
 extern "C" {
@@ -1078,6 +1412,32 @@ int pump_build_graph_rows(pump_ctx* ctx, int32_t n_nodes, int32_t dw, const doub
                           double tau_max, int32_t row_lo, int32_t row_hi, pump_graph** out) {
   return build_graph_rows(ctx, n_nodes, dw, pos, vel, ws, goal, r_n, dt, eps_cc, tau_max, row_lo, row_hi, false,
                           out);
+}
+
+int pump_rrt_run(pump_ctx* ctx, const pump_scenario* scn, int32_t trials, double alpha, int32_t n_mc,
+                 pump_result** out) {
+  return guard([&] {
+    if (!ctx || !scn || !out) throw std::invalid_argument("repeated_rrt: null argument");
+    const auto& s = scn->s;
+    auto* r = new pump_result;
+    try {
+      const RrtOutcome o = run_rrt_device(ctx->c, s, trials > 0 ? trials : s.rrt.trials, alpha >= 0 ? alpha : s.alpha,
+                                          n_mc > 0 ? n_mc : s.mc_samples);
+      r->dw = s.workspace_dim();
+      r->s.dw = r->dw;
+      r->s.success = o.success ? 1 : 0;
+      r->s.cost = o.cost;
+      r->s.certified_cp = o.certified_cp;
+      r->s.rrt_trials_reaching_goal = o.reached;
+      r->s.rrt_certification_attempts = o.attempts;
+      r->traj = o.traj;
+      r->s.n_traj_points = static_cast<int32_t>(o.traj.size());
+    } catch (...) {
+      delete r;
+      throw;
+    }
+    *out = r;
+  });
 }
 
 int pump_scenario_nodes(const pump_scenario* s, int32_t cap, double* pos, double* vel, int32_t* n_out) {

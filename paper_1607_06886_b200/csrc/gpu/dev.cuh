@@ -754,4 +754,20 @@ __host__ __device__ inline int convex_region(const WorldD& ws, const double* y, 
   return count;
 }
 
+// obstacle boxes staged in shared memory (block-wide; returns the view on them)
+template <int DW>
+__device__ __forceinline__ WorldD stage_world(const WorldD& w, double* smem) {
+  double* lo = smem;
+  double* hi = smem + w.n_obs * DW;
+  for (int x = threadIdx.x; x < w.n_obs * DW; x += blockDim.x) {
+    lo[x] = w.lo[x];
+    hi[x] = w.hi[x];
+  }
+  __syncthreads();
+  WorldD s = w;
+  s.lo = lo;
+  s.hi = hi;
+  return s;
+}
+
 }  // namespace pumpg

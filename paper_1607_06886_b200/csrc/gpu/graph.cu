@@ -204,20 +204,6 @@ __global__ void k_cand_compact(int n, int64_t n_surv, const uint8_t* __restrict_
   c_cost[c] = s_cost[s];
 }
 
-template <int DW>
-__device__ __forceinline__ WorldD stage_world(const WorldD& w, double* smem) {
-  double* lo = smem;
-  double* hi = smem + w.n_obs * DW;
-  for (int x = threadIdx.x; x < w.n_obs * DW; x += blockDim.x) {
-    lo[x] = w.lo[x];
-    hi[x] = w.hi[x];
-  }
-  __syncthreads();
-  WorldD s = w;
-  s.lo = lo;
-  s.hi = hi;
-  return s;
-}
 
 template <int DW>
 __global__ void __launch_bounds__(128) k_collide(GraphArgs g, WorldD w, int64_t n_cand,

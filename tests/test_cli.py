@@ -85,3 +85,21 @@ def test_cpp_dropin_api():
     r = subprocess.run([DROPIN, SCEN], capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "0 failed" in r.stdout
+
+
+@pytest.mark.gpu
+def test_rrt_subcommand_matches_oracle(oracle_lib, tmp_path):
+    """pump rrt (pump_cli.cpp:63-76): report fields equal the oracle's
+    repeated_rrt with the scenario's trials / alpha / mc_samples."""
+    sc = os.path.join(SCEN, "minimal.json")
+    r = run("rrt", "--scenario", sc, "--out", str(tmp_path / "rrt"))
+    assert r.returncode in (0, 2), r.stderr
+    rep = json.loads((tmp_path / "rrt" / "report.json").read_text())
+    assert rep["algorithm"] == "rrt"
+    with open(sc) as f:
+        o = oracle_lib.repeated_rrt(f.read(), workers=os.cpu_count() or 4)
+    assert rep["success"] == o["success"] and (r.returncode == 0) == o["success"]
+    assert rep["trials_reaching_goal"] == o["trials_reaching_goal"]
+    assert rep["certification_attempts"] == o["certification_attempts"]
+    assert rep["cost"] == o["cost"] and rep["certified_cp"] == o["certified_cp"]
+    assert (tmp_path / "rrt" / "trajectory.json").exists() == o["success"]

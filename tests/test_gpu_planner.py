@@ -259,3 +259,41 @@ def test_graph_row_slices_concatenate(oracle_lib, gpu_ctx, world):
         hbase += int(p["wp_hs_off"][-1])
     assert np.array_equal(np.concatenate(wp), full["edge_wp_off"])
     assert np.array_equal(np.concatenate(hs), full["wp_hs_off"])
+
+
+def rrt_kat_text(obstacles=()):
+    """test_plan.cpp:279-306 setting: empty 2-D world, zero noise."""
+    return json.dumps({"name": "rrt_kat", "workspace": {"bounds": {"lo": [-10, -10], "hi": [10, 10]},
+                                                        "obstacles": [{"lo": o[0], "hi": o[1]} for o in obstacles]},
+                       "start": {"position": [-5, 0], "velocity": [0, 0]},
+                       "goal": {"lo": [4, -1], "hi": [6, 1], "max_speed": 0.5},
+                       "noise": {"process": [0, 0, 0, 0], "measurement": 0, "initial": 0},
+                       "dt": 0.25, "alpha": 0.05, "max_speed": 1.0, "connection_radius": 6.0, "mc_samples": 200,
+                       "rrt": {"max_iterations": 80}, "samples": 10})
+
+
+@pytest.mark.parametrize("case", ["kat", "sealed", "minimal", "three_obstacle", "quad3d_three_obstacle"])
+def test_repeated_rrt_matches_oracle(oracle_lib, gpu_ctx, case):
+    """rrt.hpp:50-147 (the Table 1 baseline) on the GPU: trials reaching the
+    goal, certification attempts, cost, certified CP and trajectory bits."""
+    from paper_1607_06886_b200 import api
+
+    if case == "kat":
+        txt, trials, n_mc = rrt_kat_text(), 40, 200
+    elif case == "sealed":
+        txt, trials, n_mc = rrt_kat_text([([3, -3], [7, 3])]), 20, 200
+    else:
+        txt, trials, n_mc = with_samples(case, None, mc_samples=2000), 64, 2000
+    alpha = json.loads(txt).get("alpha", 0.05)
+    got = api.repeated_rrt(api.parse_scenario(txt), trials, alpha, n_mc, ctx=gpu_ctx)
+    ref = oracle_lib.repeated_rrt(txt, trials, alpha, n_mc, workers=WORKERS)
+    for k in ("success", "trials_reaching_goal", "certification_attempts"):
+        assert got[k] == ref[k], (k, got[k], ref[k])
+    assert got["cost"] == ref["cost"] and got["certified_cp"] == ref["certified_cp"]
+    assert np.array_equal(got["traj_t"], ref["traj_t"])
+    for k in ("traj_pos", "traj_vel", "traj_ctrl"):
+        assert np.array_equal(got[k].view(np.uint64), ref[k].view(np.uint64)), k
+    if case == "kat":
+        assert got["success"]
+    if case == "sealed":
+        assert not got["success"]

@@ -1,8 +1,9 @@
 // pump command-line front end (tools/pump_cli.cpp of the reference, same
 // subcommands, flags and exit codes) over the drop-in API: `plan` runs the
 // whole solve on the GPU, `certify` Monte-Carlo-certifies a trajectory on the
-// GPU.  `rrt` and `cp-compare` are outside the accelerated path (DESIGN.md
-// §8) and exit with an input error.  Argument parsing is hand-rolled (CLI11
+// GPU, `rrt` runs the repeated-RRT baseline (trials and certification on the
+// GPU).  `cp-compare` is outside the accelerated path and
+// exits with an input error.  Argument parsing is hand-rolled (CLI11
 // is not in the image).
 #include <cstdio>
 #include <cstdlib>
@@ -51,6 +52,18 @@ int run_plan(const Opts& o) {
   return r.success ? kExitSuccess : kExitPlannerFailure;
 }
 
+int run_rrt(const Opts& o) {  // pump_cli.cpp:63-76
+  pump::Scenario s = load(o);
+  pump::RrtResult r = pump::repeated_rrt(s, s.rrt.trials, s.alpha, s.mc_samples, o.workers);
+  pump::json report = pump::rrt_report_json(s, r, s.rrt.trials, o.workers);
+  pump::detail::write_text(out_path(o, "report.json"), report.dump(2) + "\n");
+  if (r.success)
+    pump::detail::write_text(out_path(o, "trajectory.json"), pump::trajectory_json(r.trajectory).dump(2) + "\n");
+  std::printf("%s cost=%.6f certified_cp=%.6f trials_reaching_goal=%d\n", r.success ? "success" : "failure", r.cost,
+              r.certified_cp, r.trials_reaching_goal);
+  return r.success ? kExitSuccess : kExitPlannerFailure;
+}
+
 int run_certify(const Opts& o) {
   pump::Scenario s = load(o);
   pump::Trajectory traj = pump::load_trajectory(o.trajectory);
@@ -68,7 +81,7 @@ int run_certify(const Opts& o) {
 
 int usage() {
   std::fprintf(stderr,
-               "usage: pump {plan|certify} --scenario FILE [--seed N] [--workers N] [--out DIR] "
+               "usage: pump {plan|certify|rrt} --scenario FILE [--seed N] [--workers N] [--out DIR] "
                "[--trajectory FILE]\n");
   return kExitInputError;
 }
@@ -107,7 +120,8 @@ int main(int argc, char** argv) {
       if (o.trajectory.empty()) return usage();
       return run_certify(o);
     }
-    if (cmd == "rrt" || cmd == "cp-compare") {
+    if (cmd == "rrt") return run_rrt(o);
+    if (cmd == "cp-compare") {
       std::fprintf(stderr, "error: '%s' is outside the accelerated path of this build\n", cmd.c_str());
       return kExitInputError;
     }
