@@ -172,6 +172,7 @@ def main():
     ap.add_argument("--config", default="quad3d_indoor")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-mc-sweep", action="store_true")
+    ap.add_argument("--no-rrt", action="store_true")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 0)
     world, rank, local = dist_setup()
@@ -290,6 +291,24 @@ def main():
     assert r3["path"].tolist() == res["path"].tolist() and r3["certified_cp"] == res["certified_cp"]
     del g_pre
 
+    # ---- the Table 1 baseline on the same scenario: repeated RRT (rrt.hpp,
+    # the scenario's trials / alpha / mc_samples), trials and certification on the GPU
+    rrt = None
+    if not args.no_rrt:
+        api.repeated_rrt(sc, ctx=ctx)  # warm-up (buffers)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        e0.record(lib_stream)
+        rr = api.repeated_rrt(sc, ctx=ctx)
+        e1.record(lib_stream)
+        torch.cuda.synchronize()
+        rrt = {"ms": round(max_over_ranks(e0.elapsed_time(e1), world), 3), "success": rr["success"],
+               "cost": rr["cost"], "certified_cp": rr["certified_cp"],
+               "trials": int(scn.get("rrt", {}).get("trials", 1000)),
+               "trials_reaching_goal": rr["trials_reaching_goal"],
+               "certification_attempts": rr["certification_attempts"],
+               "pump_cost_le_rrt_cost": bool(res["success"] and (not rr["success"] or res["cost"] <= rr["cost"] + 1e-9))}
+
     # ---- MC certification sweep: mc_certify of the
     # certified trajectory with n_mc in {1e4 .. 1e7}, rollouts sharded over
     # the ranks ([n r / W, n (r+1) / W)), hit counts summed across ranks
@@ -401,6 +420,7 @@ def main():
                 "h2d_bytes_per_step": int((e_io1[0] - e_io0[0]) // args.steps),
                 "d2h_bytes_per_step": int((e_io1[1] - e_io0[1]) // args.steps)},
         "mc_sweep": sweep,
+        "rrt_baseline": rrt,
         "prebuilt_graph": {"value": round(pre_ms, 3), "unit": "ms",
                            "note": "run_pump with a prebuilt graph (graph built once from the scenario's nodes)"},
         "gpu_launches": int(launches // args.steps), "gpu_launches_total": int(launches),
