@@ -36,7 +36,8 @@ DevExplore::~DevExplore() {
 struct ExpandArgs {
   const int32_t* group;
   const int64_t* task_off;
-  const int32_t* task_grp;
+  const int32_t* task_pid;
+  const int64_t* task_e;
   const int64_t* d_G;
   const int64_t* d_T;
   const int64_t* row_ptr;
@@ -104,10 +105,8 @@ constexpr int kExpStage = 64;  // half-spaces staged per warp (2 KB of shared me
 template <int DW, int CH>
 __device__ __forceinline__ void expand_task(const ExpandArgs& a, int64_t task, int lane, int wib,
                                             double2 (*s_hs)[kExpStage][2]) {
-  const int64_t lo = a.task_grp[task];  // the group entry owning this task (k_task_map)
-  const int pid = a.group[lo];
-  const int hv = a.head[pid];
-  const int64_t e = a.row_ptr[hv] + (task - a.task_off[lo]);
+  const int pid = a.task_pid[task];  // the task's plan and edge (k_task_map)
+  const int64_t e = a.task_e[task];
   const double cc = a.cost[pid] + a.e_cost[e];
   const int pt = a.t_end[pid];
   const int ns = a.e_nsteps[e];
@@ -691,12 +690,20 @@ __global__ void k_group_post(const int64_t* d_G, const int32_t* group, const int
 }
 
 // task -> group entry (warp per group), so k_expand starts without a search
-__global__ void k_task_map(const int64_t* d_G, const int64_t* task_off, int32_t* task_grp) {
+// per task: its plan and edge (warp per group entry), so k_expand starts
+// from two independent loads instead of a chain group -> plan -> head -> row
+__global__ void k_task_map(const int64_t* d_G, const int64_t* task_off, const int32_t* group, const int32_t* head,
+                           const int64_t* row_ptr, int32_t* task_pid, int64_t* task_e) {
   const int64_t g = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (g >= *d_G) return;
-  const int64_t t1 = task_off[g + 1];
-  for (int64_t t = task_off[g] + lane; t < t1; t += 32) task_grp[t] = static_cast<int32_t>(g);
+  const int64_t t0 = task_off[g], t1 = task_off[g + 1];
+  const int pid = group[g];
+  const int64_t e0 = row_ptr[head[pid]];
+  for (int64_t t = t0 + lane; t < t1; t += 32) {
+    task_pid[t] = pid;
+    task_e[t] = e0 + (t - t0);
+  }
 }
 
 // group size, its task count (task_off[G]) and the compacted pool size
@@ -1320,6 +1327,7 @@ void run_explore_device(DevExplore& X, Ctx& c, const DevGraph& G, const ExploreA
       // ---- one cooperative launch for the whole round
       const int64_t pool_ub = h.pool_n + T + 1;
       X.task_grp.ensure(al((T + 1) * 4));
+      X.task_e.ensure(al((T + 1) * 8));
       X.group.grow(al((pool_ub + 1) * 4), static_cast<size_t>(h.G) * 4, st);
       X.task_off.grow(al((pool_ub + 2) * 8), static_cast<size_t>(h.G + 1) * 8, st);
       DBuf& keys = c.buf("x_sel_keys", al((pool_ub + 1) * 4));
@@ -1334,7 +1342,7 @@ void run_explore_device(DevExplore& X, Ctx& c, const DevGraph& G, const ExploreA
       DBuf& pool_nxt = X.pool_flip ? X.pool_a : X.pool_b;
       PUMP_CUDA(cudaMemsetAsync(bar.p, 0, 8, st));
       CoopArgs A{};
-      A.ex = ExpandArgs{X.group.as<int32_t>(), X.task_off.as<int64_t>(), X.task_grp.as<int32_t>(), d_G, d_T,
+      A.ex = ExpandArgs{X.group.as<int32_t>(), X.task_off.as<int64_t>(), X.task_grp.as<int32_t>(), X.task_e.as<int64_t>(), d_G, d_T,
                         G.row_ptr.as<int64_t>(), G.e_to.as<int32_t>(), G.e_cost.as<double>(),
                         G.e_nsteps.as<int32_t>(), G.wp_off.as<int64_t>(), G.hs_off.as<int64_t>(),
                         G.hs_cnt.as<int32_t>(), G.hs_pk.as<double>(), X.head.as<int32_t>(), X.cost.as<double>(),
@@ -1386,7 +1394,9 @@ void run_explore_device(DevExplore& X, Ctx& c, const DevGraph& G, const ExploreA
       static const bool dbg_coop = std::getenv("PUMP_DEBUG_COOP") != nullptr;
       DBuf& stamps = c.buf("x_coop_stamps", 64 * 8);
       A.stamps = dbg_coop ? stamps.as<unsigned long long>() : nullptr;
-      k_task_map<<<grid_for(h.G * 32, 256), 256, 0, st>>>(d_G, X.task_off.as<int64_t>(), X.task_grp.as<int32_t>());
+      k_task_map<<<grid_for(h.G * 32, 256), 256, 0, st>>>(d_G, X.task_off.as<int64_t>(), X.group.as<int32_t>(),
+                                                            X.head.as<int32_t>(), G.row_ptr.as<int64_t>(),
+                                                            X.task_grp.as<int32_t>(), X.task_e.as<int64_t>());
       ++c.launches;
       {
         const unsigned grid = grid_for(T * 32, 256);
@@ -1423,9 +1433,12 @@ void run_explore_device(DevExplore& X, Ctx& c, const DevGraph& G, const ExploreA
     } else {
       if (T > 0) {
         X.task_grp.ensure(al((T + 1) * 4));
-        k_task_map<<<grid_for(h.G * 32, 256), 256, 0, st>>>(d_G, X.task_off.as<int64_t>(), X.task_grp.as<int32_t>());
+        X.task_e.ensure(al((T + 1) * 8));
+        k_task_map<<<grid_for(h.G * 32, 256), 256, 0, st>>>(d_G, X.task_off.as<int64_t>(), X.group.as<int32_t>(),
+                                                              X.head.as<int32_t>(), G.row_ptr.as<int64_t>(),
+                                                              X.task_grp.as<int32_t>(), X.task_e.as<int64_t>());
         ++c.launches;
-        ExpandArgs ea{X.group.as<int32_t>(), X.task_off.as<int64_t>(), X.task_grp.as<int32_t>(), d_G, d_T,
+        ExpandArgs ea{X.group.as<int32_t>(), X.task_off.as<int64_t>(), X.task_grp.as<int32_t>(), X.task_e.as<int64_t>(), d_G, d_T,
                       G.row_ptr.as<int64_t>(),
                       G.e_to.as<int32_t>(), G.e_cost.as<double>(), G.e_nsteps.as<int32_t>(), G.wp_off.as<int64_t>(),
                       G.hs_off.as<int64_t>(), G.hs_cnt.as<int32_t>(), G.hs_pk.as<double>(),

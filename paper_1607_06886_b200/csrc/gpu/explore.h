@@ -22,7 +22,7 @@ struct DevExplore {
   bool mem_flip = false;
   DBuf pool_a, pool_b;  // open plans not yet collected (ascending ids)
   bool pool_flip = false;
-  DBuf group, task_off, task_grp;  // task_grp[t]: group index of task t
+  DBuf group, task_off, task_grp, task_e;  // per task t: its plan (task_grp) and edge (task_e)
   DBuf is_goal, new_cnt, touched, drop, surv, fpos;
   DBuf cand_keep, cand_head, cand_src, cand_tend, cand_cost, cand_cp, cand_mask, cand_rank, new_slot;
   DBuf status_d;
