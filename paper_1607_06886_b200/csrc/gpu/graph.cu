@@ -62,6 +62,18 @@ __device__ __forceinline__ bool lb_tree(const PairLb& p, const LbGrid& L, int i)
   }
 }
 
+__device__ __forceinline__ bool lb_head_clears(const PairLb& p, const LbGrid& L) {
+  // head interval (0, t_K]: c >= 12 min q / t_K^3
+  const double tk = L.t[kLbK];
+  const double q0 = p.A, qk = p.A - 2.0 * p.B * tk + p.C * tk * tk;
+  double qm = q0 < qk ? q0 : qk;
+  if (p.ts > 0 && p.ts < tk) qm = p.A - p.B * p.ts;
+  const double ab = p.B < 0 ? -p.B : p.B;
+  qm -= 1e-12 * (p.A + 2.0 * ab * tk + p.C * tk * tk);
+  if (qm < 0) qm = 0;
+  return L.c3[kLbK] * qm * (1.0 - 1e-12) >= L.thr;
+}
+
 __device__ __forceinline__ bool lb_rejects(const PairLb& p, const LbGrid& L) {
   // head interval (0, t_K]: c >= 12 min q / t_K^3
   const double tk = L.t[kLbK];
@@ -143,6 +155,129 @@ __global__ void __launch_bounds__(kRowBlock) k_pair_filter(GraphArgs g, const Lb
     }
     __syncthreads();
   }
+  if (threadIdx.x == 0) row_cnt[v] = base_s;
+}
+
+// Pass 1, lane-refill form.  The tree cover of lb_tree costs 1 interval test
+// for most pairs and hundreds for near-threshold ones; one pair per lane left
+// ~1/3 of the lanes active.  Here every lane runs the same loop body -- one
+// interval test of an explicit depth-first walk over the 4-ary tree -- and a
+// lane whose pair is decided takes the next u of the row (warp ballot + one
+// shared atomic per warp).  Survivors land in a bitmask over a chunk of u and
+// are compacted in ascending-u order after it, so the slab is identical to
+// k_pair_filter's (the decision per pair is the same pure function).
+constexpr int kPfChunk = 32 * kRowBlock;
+template <int DW>
+__global__ void __launch_bounds__(kRowBlock) k_pair_filter_q(GraphArgs g, const LbGrid lb, int cap, int row0, int refill,
+                                                             int32_t* __restrict__ row_cnt,
+                                                             int32_t* __restrict__ su) {
+  __shared__ LbGrid sl;
+  __shared__ uint32_t bits[kPfChunk / 32];
+  __shared__ int wtot[kRowBlock / 32];
+  __shared__ int s_next, base_s;
+  {
+    const double* src = reinterpret_cast<const double*>(&lb);
+    double* dst = reinterpret_cast<double*>(&sl);
+    for (int x = threadIdx.x; x < static_cast<int>(sizeof(LbGrid) / 8); x += blockDim.x) dst[x] = src[x];
+  }
+  const int v = row0 + blockIdx.x;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const unsigned lt = (1u << lane) - 1u;
+  double ap[DW], av[DW];
+#pragma unroll
+  for (int k = 0; k < DW; ++k) {
+    ap[k] = g.pos[v * DW + k];
+    av[k] = g.vel[v * DW + k];
+  }
+  if (threadIdx.x == 0) base_s = 0;
+  for (int c0 = 0; c0 < g.n; c0 += kPfChunk) {
+    const int c1 = min(g.n, c0 + kPfChunk);
+    bits[threadIdx.x] = 0u;  // kPfChunk / 32 == kRowBlock
+    if (threadIdx.x == 0) s_next = c0;
+    __syncthreads();
+    bool active = false, exhausted = false;
+    PairLb p{};
+    int i = 0, s = 0, u = 0;
+    for (;;) {
+      while (!exhausted) {  // warp-uniform
+        const unsigned need = __ballot_sync(0xffffffffu, !active);
+        // refill in bulk: the refill body (loads, pair_lb, head test) is
+        // several interval tests long, so it waits for half the warp
+        if (need == 0 || (need != 0xffffffffu && __popc(need) < refill)) break;
+        int base = 0;
+        if (lane == 0) base = atomicAdd(&s_next, __popc(need));
+        base = __shfl_sync(0xffffffffu, base, 0);
+        if (base >= c1) {
+          exhausted = true;
+          break;
+        }
+        if (!active) {
+          u = base + __popc(need & lt);
+          if (u < c1 && u != v) {
+            double bp[DW], bv[DW];
+#pragma unroll
+            for (int k = 0; k < DW; ++k) {
+              bp[k] = g.pos[u * DW + k];
+              bv[k] = g.vel[u * DW + k];
+            }
+            p = pair_lb<DW>(ap, av, bp, bv);
+            if (!(2.0 * sqrt(p.D) >= g.r_n)) {
+              if (!lb_head_clears(p, sl)) {
+                atomicOr(&bits[(u - c0) >> 5], 1u << ((u - c0) & 31));
+              } else {
+                active = true;
+                i = 0;
+                s = 4;  // span 4^s: the root
+              }
+            }
+          }
+        }
+      }
+      if (!__any_sync(0xffffffffu, active)) break;
+      if (active) {
+        const int span = 1 << (2 * s);
+        if (interval_clears(p, sl.t[i + span], sl.t[i], sl.c3[i], sl.c1[i], sl.thr)) {
+          i += span;  // a multiple of 4^s: climb past every finished parent
+          const int z = (__ffs(i) - 1) >> 1;
+          s = z < 4 ? (z > s ? z : s) : 4;
+          if (i == kLbK) active = false;  // covered: rejected
+        } else if (s == 0) {
+          atomicOr(&bits[(u - c0) >> 5], 1u << ((u - c0) & 31));  // a leaf fails: survivor
+          active = false;
+        } else {
+          --s;
+        }
+      }
+    }
+    __syncthreads();
+    // ascending-u compaction of the chunk's bitmask, one word per thread
+    const uint32_t wb = bits[threadIdx.x];
+    const int cnt = __popc(wb);
+    int inc = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, inc, o);
+      if (lane >= o) inc += y;
+    }
+    if (lane == 31) wtot[warp] = inc;
+    __syncthreads();
+    int off = base_s + inc - cnt;
+    for (int w = 0; w < warp; ++w) off += wtot[w];
+    uint32_t m = wb;
+    while (m) {
+      const int b = __ffs(m) - 1;
+      m &= m - 1;
+      if (off < cap) su[static_cast<int64_t>(v) * cap + off] = c0 + threadIdx.x * 32 + b;
+      ++off;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int t = 0;
+      for (int w = 0; w < kRowBlock / 32; ++w) t += wtot[w];
+      base_s += t;
+    }
+  }
+  __syncthreads();
   if (threadIdx.x == 0) row_cnt[v] = base_s;
 }
 
@@ -507,9 +642,14 @@ void build_graph_device(DevGraph& G, Ctx& c, int n, int dw, const double* h_pos,
     {
       KScope ks(st, F_PAIR);
       dispatch_dw(dw, [&]<int DW>() {
-        if (row_hi > row_lo)
+        static const bool legacy = getenv("PUMP_PAIR_LEGACY") != nullptr;
+        static const int refill = getenv("PUMP_PF_REFILL") ? atoi(getenv("PUMP_PF_REFILL")) : 16;
+        if (row_hi > row_lo && legacy)
           k_pair_filter<DW><<<row_hi - row_lo, kRowBlock, 0, st>>>(ga, lbg, cap, row_lo, rcnt.as<int32_t>(),
                                                                    suB.as<int32_t>());
+        else if (row_hi > row_lo)
+          k_pair_filter_q<DW><<<row_hi - row_lo, kRowBlock, 0, st>>>(ga, lbg, cap, row_lo, refill, rcnt.as<int32_t>(),
+                                                                     suB.as<int32_t>());
       });
       ++c.launches;
       PUMP_CUDA(cudaGetLastError());
