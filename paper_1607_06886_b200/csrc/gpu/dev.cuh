@@ -97,6 +97,23 @@ __host__ __device__ __forceinline__ int __builtin_ctzll_hd(uint64_t x) {
 #endif
 }
 
+// Reciprocal to within a few ulps (not correctly rounded): MUFU seed + two
+// Newton steps.  Only for values that carry their own error margin (the lazy
+// cubic's 1e-11 S, the filter multipliers' rounding-down factor), never for
+// a value the reference computes.  x > 0, finite, normal.
+__host__ __device__ __forceinline__ double rcp_approx(double x) {
+#if defined(__CUDA_ARCH__)
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  double e = fma(-x, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-x, r, 1.0);
+  return fma(r, e, r);
+#else
+  return 1.0 / x;
+#endif
+}
+
 // ----------------------------------------------------------- geometry
 // closed AABB containment (geom.hpp:19-23)
 template <int DW>
@@ -556,8 +573,8 @@ __host__ __device__ inline bool connect_dev(const double* ap, const double* av, 
     double tau, approx, err, exact;
     bool known;
   };
-  auto lazy = [&](double t) {
-    const double u = 1.0 / t;
+  // u = 1/t only needs a few ulps: its error moves the cubic by <~1e-13 S
+  auto lazy_u = [&](double t, double u) {
     Lazy z;
     z.tau = t;
     z.approx = t + ((k3 * u + k2) * u + k1) * u;
@@ -565,6 +582,7 @@ __host__ __device__ inline bool connect_dev(const double* ap, const double* av, 
     z.known = false;
     return z;
   };
+  auto lazy = [&](double t) { return lazy_u(t, rcp_approx(t)); };
   auto exact = [&](Lazy& z) {
     if (!z.known) {
       z.exact = steer_cost<DW>(ap, av, bp, bv, z.tau);
@@ -581,12 +599,18 @@ __host__ __device__ inline bool connect_dev(const double* ap, const double* av, 
   // scan: an upper bound of the minimum from the cubic, then exact costs only
   // where the cubic cannot rule the point out, in index order with the
   // reference's strict update (the first index attaining the minimum)
+  // u runs down its own product chain (<= 2 ulps per step: <~1.5e-14 after
+  // 64), tau keeps the reference's chain exactly
   double m_hi = __builtin_inf();
+  const double u_lo = 1.0 / tau_lo, u_r = 1.0 / ratio;
   {
-    double tau = tau_lo;
+    double tau = tau_lo, u = u_lo;
     for (int i = 0; i < 64; ++i) {
-      if (i > 0) tau *= ratio;
-      const Lazy z = lazy(tau);
+      if (i > 0) {
+        tau *= ratio;
+        u *= u_r;
+      }
+      const Lazy z = lazy_u(tau, u);
       const double h = z.approx + z.err;
       m_hi = h < m_hi ? h : m_hi;
     }
@@ -594,10 +618,13 @@ __host__ __device__ inline bool connect_dev(const double* ap, const double* av, 
   double best_tau = tau_lo, best_c = __builtin_inf();
   int best_idx = 0;
   {
-    double tau = tau_lo;
+    double tau = tau_lo, u = u_lo;
     for (int i = 0; i < 64; ++i) {
-      if (i > 0) tau *= ratio;
-      Lazy z = lazy(tau);
+      if (i > 0) {
+        tau *= ratio;
+        u *= u_r;
+      }
+      Lazy z = lazy_u(tau, u);
       if (z.approx - z.err > m_hi) continue;  // above the minimum
       const double c = exact(z);
       if (c < best_c) {
@@ -617,7 +644,9 @@ __host__ __device__ inline bool connect_dev(const double* ap, const double* av, 
     double t_hi = hi;
     for (int p = kParts - 1; p >= 0 && clears; --p) {
       const double t_lo = p == 0 ? lo : lo + (hi - lo) * (static_cast<double>(p) / kParts);
-      const double c3 = 12.0 / (t_hi * t_hi * t_hi) * (1.0 - 1e-14), c1 = 1.0 / t_hi * (1.0 - 1e-14);
+      // multipliers rounded down by far more than rcp_approx's few ulps
+      const double r = rcp_approx(t_hi) * (1.0 - 1e-13);
+      const double c3 = 12.0 * (r * r * r) * (1.0 - 1e-13), c1 = r;
       clears = interval_clears(plb, t_lo, t_hi, c3, c1, reject_thr);
       t_hi = t_lo;
     }
