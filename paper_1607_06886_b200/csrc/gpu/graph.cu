@@ -281,6 +281,327 @@ __global__ void __launch_bounds__(kRowBlock) k_pair_filter_q(GraphArgs g, const 
   if (threadIdx.x == 0) row_cnt[v] = base_s;
 }
 
+// ---------------------------------------------------------------- cell grid
+// Exact-preserving spatial cull in front of the pair filter.  For tau in
+// (0, thr] and |vbar| <= V (V = the nodes' largest speed), the cost
+// c(tau) >= 12 |dp0 - vbar tau|^2 / tau^3 >= 12 (d - V thr)^2 / thr^3 once the
+// distance d = |dp0| exceeds V thr, and that exceeds thr once
+// d > R = V thr + thr^2 / sqrt(12); beyond thr, c >= tau > thr.  So a node
+// farther than R from v has true cost above thr = r_n (1 + 1e-6) for every
+// tau (the host tightens R interval by interval, below) -- the premise the interval-tree filter itself rests on (connect would
+// return cost >= r_n or ok = false; graph.hpp:72 drops the pair).  Nodes are
+// bucketed into cells of edge >= R / 2 with exact per-cell bounding boxes; a
+// row visits only the cells whose box lies within R (squared distance against
+// R^2 (1 + 1e-9), far above the distance's rounding).  Survivors land in a
+// bitmask over all n and are compacted in ascending u, so the per-row slab
+// holds exactly the pairs k_pair_filter_q keeps among the cells visited.
+constexpr int kCellMaxList = 512;  // (2 kr + 1)^DW with kr <= 3
+struct CellGrid {
+  double lo[3];
+  double inv_h;
+  double R2;
+  int dims[3];
+  int kr;
+};
+
+__device__ __forceinline__ unsigned long long ord_of(double x) {
+  const unsigned long long b = static_cast<unsigned long long>(__double_as_longlong(x));
+  return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+}
+__host__ __device__ __forceinline__ double dbl_of(unsigned long long o) {
+  const unsigned long long b = (o >> 63) ? (o & 0x7fffffffffffffffull) : ~o;
+  double x;
+  memcpy(&x, &b, 8);
+  return x;
+}
+
+// stats[0..DW) = ord(min pos), stats[3..3+DW) = ord(max pos), stats[6] = ord(max |v|^2)
+template <int DW>
+__global__ void k_node_stats(int n, const double* __restrict__ pos, const double* __restrict__ vel,
+                             unsigned long long* __restrict__ stats) {
+  double lo[DW], hi[DW], v2 = 0.0;
+#pragma unroll
+  for (int k = 0; k < DW; ++k) {
+    lo[k] = INFINITY;
+    hi[k] = -INFINITY;
+  }
+  for (int u = blockIdx.x * blockDim.x + threadIdx.x; u < n; u += gridDim.x * blockDim.x) {
+    double s = 0.0;
+#pragma unroll
+    for (int k = 0; k < DW; ++k) {
+      const double p = pos[u * DW + k], w = vel[u * DW + k];
+      lo[k] = fmin(lo[k], p);
+      hi[k] = fmax(hi[k], p);
+      s += w * w;
+    }
+    v2 = fmax(v2, s);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+#pragma unroll
+    for (int k = 0; k < DW; ++k) {
+      lo[k] = fmin(lo[k], __shfl_xor_sync(0xffffffffu, lo[k], o));
+      hi[k] = fmax(hi[k], __shfl_xor_sync(0xffffffffu, hi[k], o));
+    }
+    v2 = fmax(v2, __shfl_xor_sync(0xffffffffu, v2, o));
+  }
+  if ((threadIdx.x & 31) == 0) {
+#pragma unroll
+    for (int k = 0; k < DW; ++k) {
+      atomicMin(&stats[k], ord_of(lo[k]));
+      atomicMax(&stats[3 + k], ord_of(hi[k]));
+    }
+    atomicMax(&stats[6], ord_of(v2));
+  }
+}
+
+__global__ void k_cell_box_init(int n_cells, unsigned long long* __restrict__ cbox) {
+  const int x = blockIdx.x * blockDim.x + threadIdx.x;
+  if (x >= n_cells * 6) return;
+  cbox[x] = (x % 6) < 3 ? ~0ull : 0ull;  // min words start at the top of the order, max words at the bottom
+}
+
+template <int DW>
+__device__ __forceinline__ int cell_coord(const CellGrid& G, const double* p, int k) {
+  const double x = floor((p[k] - G.lo[k]) * G.inv_h);
+  return x < 0 ? 0 : (x >= G.dims[k] ? G.dims[k] - 1 : static_cast<int>(x));
+}
+
+// per node: its cell, rank within the cell, and the cell's exact bounding box
+template <int DW>
+__global__ void k_cell_count(int n, const double* __restrict__ pos, const CellGrid G, int32_t* __restrict__ cnt,
+                             unsigned long long* __restrict__ cbox, int32_t* __restrict__ ncell,
+                             int32_t* __restrict__ nrank) {
+  const int u = blockIdx.x * blockDim.x + threadIdx.x;
+  if (u >= n) return;
+  double p[DW];
+#pragma unroll
+  for (int k = 0; k < DW; ++k) p[k] = pos[u * DW + k];
+  int id = 0;
+#pragma unroll
+  for (int k = DW - 1; k >= 0; --k) id = id * G.dims[k] + cell_coord<DW>(G, p, k);
+  ncell[u] = id;
+  nrank[u] = atomicAdd(&cnt[id], 1);
+#pragma unroll
+  for (int k = 0; k < DW; ++k) {
+    atomicMin(&cbox[static_cast<int64_t>(id) * 6 + k], ord_of(p[k]));
+    atomicMax(&cbox[static_cast<int64_t>(id) * 6 + 3 + k], ord_of(p[k]));
+  }
+}
+
+template <int DW>
+__global__ void k_cell_scatter(int n, const double* __restrict__ pos, const double* __restrict__ vel,
+                               const int32_t* __restrict__ ncell, const int32_t* __restrict__ nrank,
+                               const int64_t* __restrict__ cstart, int32_t* __restrict__ sidx,
+                               double* __restrict__ spos, double* __restrict__ svel) {
+  const int u = blockIdx.x * blockDim.x + threadIdx.x;
+  if (u >= n) return;
+  const int64_t j = cstart[ncell[u]] + nrank[u];
+  sidx[j] = u;
+#pragma unroll
+  for (int k = 0; k < DW; ++k) {
+    spos[j * DW + k] = pos[u * DW + k];
+    svel[j * DW + k] = vel[u * DW + k];
+  }
+}
+
+// Pass 1 over the cells within R of the row's node; the per-pair decision and
+// the lane-refill walk are k_pair_filter_q's.
+template <int DW>
+__global__ void __launch_bounds__(kRowBlock) k_pair_filter_grid(
+    GraphArgs g, const LbGrid lb, const CellGrid G, int cap, int row0, int refill,
+    const int32_t* __restrict__ ccnt, const int64_t* __restrict__ cstart,
+    const unsigned long long* __restrict__ cbox, const int32_t* __restrict__ sidx, const double* __restrict__ spos,
+    const double* __restrict__ svel, int32_t* __restrict__ row_cnt, int32_t* __restrict__ su) {
+  __shared__ LbGrid sl;
+  __shared__ int cl_start[kCellMaxList];
+  __shared__ int cl_pref[kCellMaxList + 1];
+  __shared__ int wtot[kRowBlock / 32];
+  __shared__ int s_next, s_ncl;
+  extern __shared__ uint32_t bits[];  // ceil(n / 32) words
+  {
+    const double* src = reinterpret_cast<const double*>(&lb);
+    double* dst = reinterpret_cast<double*>(&sl);
+    for (int x = threadIdx.x; x < static_cast<int>(sizeof(LbGrid) / 8); x += blockDim.x) dst[x] = src[x];
+  }
+  const int v = row0 + blockIdx.x;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const unsigned lt = (1u << lane) - 1u;
+  const int nw = (g.n + 31) >> 5;
+  double ap[DW], av[DW];
+#pragma unroll
+  for (int k = 0; k < DW; ++k) {
+    ap[k] = g.pos[v * DW + k];
+    av[k] = g.vel[v * DW + k];
+  }
+  for (int x = threadIdx.x; x < nw; x += blockDim.x) bits[x] = 0u;
+  if (threadIdx.x == 0) {
+    s_ncl = 0;
+    s_next = 0;
+  }
+  __syncthreads();
+  // candidate cells: the (2 kr + 1)^DW neighbourhood, kept when non-empty and
+  // its exact box lies within R of the node
+  {
+    int cc[DW];
+#pragma unroll
+    for (int k = 0; k < DW; ++k) cc[k] = cell_coord<DW>(G, ap, k);
+    const int side = 2 * G.kr + 1;
+    int tot = 1;
+#pragma unroll
+    for (int k = 0; k < DW; ++k) tot *= side;
+    for (int o = threadIdx.x; o < tot; o += blockDim.x) {
+      int r = o, id = 0, mul = 1;
+      bool in = true;
+#pragma unroll
+      for (int k = 0; k < DW; ++k) {
+        const int c = cc[k] + (r % side) - G.kr;
+        r /= side;
+        in = in && c >= 0 && c < G.dims[k];
+        id += c * mul;
+        mul *= G.dims[k];
+      }
+      if (!in) continue;
+      const int cnt = ccnt[id];
+      if (cnt == 0) continue;
+      double d2 = 0.0;
+#pragma unroll
+      for (int k = 0; k < DW; ++k) {
+        const double blo = dbl_of(cbox[static_cast<int64_t>(id) * 6 + k]);
+        const double bhi = dbl_of(cbox[static_cast<int64_t>(id) * 6 + 3 + k]);
+        const double e = ap[k] < blo ? blo - ap[k] : (ap[k] > bhi ? ap[k] - bhi : 0.0);
+        d2 += e * e;
+      }
+      if (d2 > G.R2) continue;
+      const int slot = atomicAdd(&s_ncl, 1);
+      cl_start[slot] = static_cast<int>(cstart[id]);
+      cl_pref[slot + 1] = cnt;
+    }
+  }
+  __syncthreads();
+  const int ncl = s_ncl;
+  if (warp == 0) {  // inclusive prefix of the list's counts: 16 entries per lane + a warp scan
+    constexpr int kPer = kCellMaxList / 32;
+    int run = 0;
+    for (int q = 0; q < kPer; ++q) {
+      const int e = lane * kPer + q;
+      if (e < ncl) run += cl_pref[e + 1];
+    }
+    int inc = run;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, inc, o);
+      if (lane >= o) inc += y;
+    }
+    int acc = inc - run;
+    for (int q = 0; q < kPer; ++q) {
+      const int e = lane * kPer + q;
+      if (e < ncl) {
+        acc += cl_pref[e + 1];
+        cl_pref[e + 1] = acc;
+      }
+    }
+    if (lane == 0) cl_pref[0] = 0;
+  }
+  __syncthreads();
+  const int total = cl_pref[ncl];
+  bool active = false, exhausted = false;
+  PairLb p{};
+  int i = 0, s = 0, u = 0;
+  for (;;) {
+    while (!exhausted) {  // warp-uniform
+      const unsigned need = __ballot_sync(0xffffffffu, !active);
+      if (need == 0 || (need != 0xffffffffu && __popc(need) < refill)) break;
+      int base = 0;
+      if (lane == 0) base = atomicAdd(&s_next, __popc(need));
+      base = __shfl_sync(0xffffffffu, base, 0);
+      if (base >= total) {
+        exhausted = true;
+        break;
+      }
+      if (!active) {
+        const int j = base + __popc(need & lt);
+        if (j < total) {
+          int lo = 0, hi = ncl;  // largest c with cl_pref[c] <= j
+          while (hi - lo > 1) {
+            const int mid = (lo + hi) >> 1;
+            if (cl_pref[mid] <= j)
+              lo = mid;
+            else
+              hi = mid;
+          }
+          const int js = cl_start[lo] + (j - cl_pref[lo]);
+          u = sidx[js];
+          if (u != v) {
+            double bp[DW], bv[DW];
+#pragma unroll
+            for (int k = 0; k < DW; ++k) {
+              bp[k] = spos[static_cast<int64_t>(js) * DW + k];
+              bv[k] = svel[static_cast<int64_t>(js) * DW + k];
+            }
+            p = pair_lb<DW>(ap, av, bp, bv);
+            if (!(2.0 * sqrt(p.D) >= g.r_n)) {
+              if (!lb_head_clears(p, sl)) {
+                atomicOr(&bits[u >> 5], 1u << (u & 31));
+              } else {
+                active = true;
+                i = 0;
+                s = 4;
+              }
+            }
+          }
+        }
+      }
+    }
+    if (!__any_sync(0xffffffffu, active)) break;
+    if (active) {
+      const int span = 1 << (2 * s);
+      if (interval_clears(p, sl.t[i + span], sl.t[i], sl.c3[i], sl.c1[i], sl.thr)) {
+        i += span;
+        const int z = (__ffs(i) - 1) >> 1;
+        s = z < 4 ? (z > s ? z : s) : 4;
+        if (i == kLbK) active = false;
+      } else if (s == 0) {
+        atomicOr(&bits[u >> 5], 1u << (u & 31));
+        active = false;
+      } else {
+        --s;
+      }
+    }
+  }
+  __syncthreads();
+  // ascending-u compaction of the bitmask, kRowBlock words per pass
+  int base_run = 0;
+  for (int w0 = 0; w0 < nw; w0 += kRowBlock) {
+    const int x = w0 + threadIdx.x;
+    const uint32_t wb = x < nw ? bits[x] : 0u;
+    const int cnt = __popc(wb);
+    int inc = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, inc, o);
+      if (lane >= o) inc += y;
+    }
+    if (lane == 31) wtot[warp] = inc;
+    __syncthreads();
+    int off = base_run + inc - cnt, blk = 0;
+    for (int w = 0; w < kRowBlock / 32; ++w) {
+      if (w < warp) off += wtot[w];
+      blk += wtot[w];
+    }
+    uint32_t m = wb;
+    while (m) {
+      const int b = __ffs(m) - 1;
+      m &= m - 1;
+      if (off < cap) su[static_cast<int64_t>(v) * cap + off] = x * 32 + b;
+      ++off;
+    }
+    base_run += blk;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) row_cnt[v] = base_run;
+}
+
 __device__ __forceinline__ int find_row(const int64_t* __restrict__ off, int n, int64_t c) {
   int lo = 0, hi = n;  // largest r with off[r] <= c
   while (hi - lo > 1) {
@@ -637,6 +958,102 @@ void build_graph_device(DevGraph& G, Ctx& c, int n, int dw, const double* h_pos,
   PUMP_CUDA(cudaMemsetAsync(rcnt.p, 0, (n + 8) * 4, st));  // rows outside [row_lo, row_hi) stay empty
   DBuf& soff = c.buf("g_soff", al((n + 2) * 8));
   DBuf& stmp = c.buf("g_scantmp", scan_temp_bytes(static_cast<int64_t>(n) * n + 16));
+  // ---- cell grid of the nodes for the exact spatial cull (k_pair_filter_grid)
+  static const bool nogrid = getenv("PUMP_PAIR_NOGRID") != nullptr;
+  const size_t bits_bytes = static_cast<size_t>((n + 31) / 32) * 4;
+  const bool use_grid = !nogrid && n > 0 && row_hi > row_lo && bits_bytes <= 160 * 1024;
+  CellGrid cg{};
+  if (use_grid) {
+    KScope ks(st, F_PAIR);
+    DBuf& stats = c.buf("g_nstats", 256);
+    PUMP_CUDA(cudaMemsetAsync(stats.p, 0xff, 24, st));
+    PUMP_CUDA(cudaMemsetAsync(stats.as<char>() + 24, 0, 32, st));
+    dispatch_dw(dw, [&]<int DW>() {
+      k_node_stats<DW><<<std::min(64, (n + 255) / 256), 256, 0, st>>>(n, G.pos.as<double>(), G.vel.as<double>(),
+                                                                      stats.as<unsigned long long>());
+    });
+    ++c.launches;
+    PUMP_CUDA(cudaGetLastError());
+    unsigned long long hs[7];
+    c.d2h(hs, stats.p, 56);
+    c.sync();
+    double lo[3] = {0, 0, 0}, hi[3] = {0, 0, 0};
+    for (int k = 0; k < dw; ++k) {
+      lo[k] = dbl_of(hs[k]);
+      hi[k] = dbl_of(hs[3 + k]);
+    }
+    const double V = std::sqrt(dbl_of(hs[6])) * (1.0 + 1e-12);
+    const double thr = r_n * (1.0 + 1e-6);
+    // R: on each interval [tl, th] of a geometric cover of (0, thr],
+    // c >= tl + 12 (d - V th)^2 / th^3, which exceeds thr once
+    // d >= V th + sqrt((thr - tl) th^3 / 12); the head (0, tk] needs
+    // d >= V tk + sqrt(thr tk^3 / 12).  R is the largest requirement.
+    double R = 0.0;
+    {
+      constexpr int kK = 4096;
+      const double rho = std::pow(1e6, 1.0 / kK);
+      double th = thr;
+      for (int i = 0; i < kK; ++i) {
+        const double tl = th / rho;
+        R = std::max(R, V * th + std::sqrt((thr - tl) * th * th * th / 12.0));
+        th = tl;
+      }
+      R = std::max(R, V * th + std::sqrt(thr * th * th * th / 12.0));
+      R *= 1.0 + 1e-9;
+    }
+    double h = 0.5 * R;
+    bool finite = std::isfinite(R) && R > 0;
+    for (int k = 0; k < dw; ++k) finite = finite && std::isfinite(lo[k]) && std::isfinite(hi[k]);
+    if (finite) {
+      for (;;) {
+        int64_t cells = 1;
+        for (int k = 0; k < dw; ++k) {
+          cg.dims[k] = static_cast<int>(std::min(1024.0, std::floor((hi[k] - lo[k]) / h) + 1.0));
+          cells *= cg.dims[k];
+        }
+        cg.kr = static_cast<int>(std::ceil(R / h)) + 1;
+        int side = 1;
+        for (int k = 0; k < dw; ++k) side *= 2 * cg.kr + 1;
+        if (cells <= (int64_t(1) << 22) && side <= kCellMaxList) break;
+        h *= 1.03;
+      }
+      for (int k = 0; k < dw; ++k) cg.lo[k] = lo[k];
+      cg.inv_h = 1.0 / h;
+      cg.R2 = R * R * (1.0 + 1e-9);
+    } else {
+      cg.dims[0] = cg.dims[1] = cg.dims[2] = 1;  // one cell: every node is visited
+      cg.inv_h = 0.0;
+      cg.kr = 0;
+      cg.R2 = INFINITY;
+    }
+    int n_cells = 1;
+    for (int k = 0; k < dw; ++k) n_cells *= cg.dims[k];
+    DBuf& ccnt = c.buf("g_ccnt", al((n_cells + 8) * 4));
+    DBuf& cbox = c.buf("g_cbox", al(static_cast<size_t>(n_cells) * 48 + 64));
+    DBuf& cst = c.buf("g_cstart", al((n_cells + 2) * 8));
+    DBuf& nci = c.buf("g_ncell", al((n + 8) * 4));
+    DBuf& nrk = c.buf("g_nrank", al((n + 8) * 4));
+    DBuf& sidx = c.buf("g_sidx", al((n + 8) * 4));
+    DBuf& spos = c.buf("g_spos", al(static_cast<size_t>(n) * dw * 8 + 64));
+    DBuf& svel = c.buf("g_svel", al(static_cast<size_t>(n) * dw * 8 + 64));
+    DBuf& ctmp = c.buf("g_cscantmp", scan_temp_bytes(n_cells + 16));
+    PUMP_CUDA(cudaMemsetAsync(ccnt.p, 0, static_cast<size_t>(n_cells) * 4, st));
+    dispatch_dw(dw, [&]<int DW>() {
+      k_cell_box_init<<<grid_for(static_cast<int64_t>(n_cells) * 6, 256), 256, 0, st>>>(n_cells, cbox.as<unsigned long long>());
+      k_cell_count<DW><<<grid_for(n, 256), 256, 0, st>>>(n, G.pos.as<double>(), cg, ccnt.as<int32_t>(),
+                                                         cbox.as<unsigned long long>(), nci.as<int32_t>(),
+                                                         nrk.as<int32_t>());
+    });
+    c.launches += 2;
+    exclusive_scan<int32_t>(ccnt.as<int32_t>(), cst.as<int64_t>(), n_cells, ctmp.p, st, &c.launches);
+    dispatch_dw(dw, [&]<int DW>() {
+      k_cell_scatter<DW><<<grid_for(n, 256), 256, 0, st>>>(n, G.pos.as<double>(), G.vel.as<double>(), nci.as<int32_t>(),
+                                                           nrk.as<int32_t>(), cst.as<int64_t>(), sidx.as<int32_t>(),
+                                                           spos.as<double>(), svel.as<double>());
+    });
+    ++c.launches;
+    PUMP_CUDA(cudaGetLastError());
+  }
   for (;;) {  // pass 1 with an exact per-row refit if a row overflows the slab
     DBuf& suB = c.buf("g_su", al(static_cast<size_t>(n) * cap * 4));
     {
@@ -644,7 +1061,16 @@ void build_graph_device(DevGraph& G, Ctx& c, int n, int dw, const double* h_pos,
       dispatch_dw(dw, [&]<int DW>() {
         static const bool legacy = getenv("PUMP_PAIR_LEGACY") != nullptr;
         static const int refill = getenv("PUMP_PF_REFILL") ? atoi(getenv("PUMP_PF_REFILL")) : 16;
-        if (row_hi > row_lo && legacy)
+        if (use_grid) {
+          const int sm = static_cast<int>(bits_bytes);
+          if (sm > 32 * 1024)
+            PUMP_CUDA(cudaFuncSetAttribute(k_pair_filter_grid<DW>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+          k_pair_filter_grid<DW><<<row_hi - row_lo, kRowBlock, sm, st>>>(
+              ga, lbg, cg, cap, row_lo, refill, c.scratch["g_ccnt"].as<int32_t>(), c.scratch["g_cstart"].as<int64_t>(),
+              c.scratch["g_cbox"].as<unsigned long long>(), c.scratch["g_sidx"].as<int32_t>(),
+              c.scratch["g_spos"].as<double>(), c.scratch["g_svel"].as<double>(), rcnt.as<int32_t>(),
+              suB.as<int32_t>());
+        } else if (row_hi > row_lo && legacy)
           k_pair_filter<DW><<<row_hi - row_lo, kRowBlock, 0, st>>>(ga, lbg, cap, row_lo, rcnt.as<int32_t>(),
                                                                    suB.as<int32_t>());
         else if (row_hi > row_lo)
