@@ -783,6 +783,100 @@ __host__ __device__ inline int convex_region(const WorldD& ws, const double* y, 
   return count;
 }
 
+// convex_region for <= 32 boxes with the per-box squared distances kept (in
+// shared memory, stride sq_stride); one pass per iteration.  Identical output to convex_region:
+//  - |clamp(y) - y|^2 of a box does not depend on the iteration, so it is
+//    computed once; the next iteration's nearest box (first strict minimum
+//    among the boxes still unpruned) is tracked inside the prune pass, which
+//    visits the boxes in index order with the same strict comparison.
+//  - the prune test's minimizing corner is chosen by the sign of d_k (lo for
+//    d_k >= 0, hi otherwise).  For d_k != 0 that is the corner min(tl, th)
+//    picks (monotone rounding); for d_k = +-0 both terms are +-0, and a zero
+//    term of either sign leaves the sum from +0 unchanged, so the dot is the
+//    same number.
+template <int DW>
+__device__ __forceinline__ int convex_region_fused(const WorldD& ws, const double* y, const double* yd, double* sq,
+                                                   int sq_stride, double* a_out, double* b_out, uint8_t* fb_out) {
+  int best = -1;
+  double best_sq = __builtin_inf();
+  for (int o = 0; o < ws.n_obs; ++o) {
+    double cand[DW];
+#pragma unroll
+    for (int k = 0; k < DW; ++k) {
+      double c = y[k] < ws.lo[o * DW + k] ? ws.lo[o * DW + k] : y[k];
+      c = ws.hi[o * DW + k] < c ? ws.hi[o * DW + k] : c;
+      cand[k] = c - y[k];
+    }
+    const double q = sqnorm<DW>(cand);
+    sq[o * sq_stride] = q;
+    if (q < best_sq) {
+      best_sq = q;
+      best = o;
+    }
+  }
+  uint32_t pruned = 0u;  // <= 32 boxes
+  int count = 0;
+  while (best >= 0) {
+    double d[DW];
+#pragma unroll
+    for (int k = 0; k < DW; ++k) {
+      double c = y[k] < ws.lo[best * DW + k] ? ws.lo[best * DW + k] : y[k];
+      c = ws.hi[best * DW + k] < c ? ws.hi[best * DW + k] : c;
+      d[k] = c - y[k];
+    }
+    const double dd = sqnorm<DW>(d);
+    const double lim = dd - 1e-12 * (1.0 + dd);
+    bool any = false;
+    int nb = -1;
+    double nsq = __builtin_inf();
+    for (int o = 0; o < ws.n_obs; ++o) {
+      if ((pruned >> o) & 1u) continue;
+      double dot = 0;
+#pragma unroll
+      for (int k = 0; k < DW; ++k) {
+        const double c = d[k] >= 0 ? ws.lo[o * DW + k] : ws.hi[o * DW + k];
+        dot += d[k] * (c - y[k]);
+      }
+      if (!(dot < lim)) {
+        pruned |= 1u << o;
+        any = true;
+      } else {
+        const double q = sq[o * sq_stride];
+        if (q < nsq) {
+          nsq = q;
+          nb = o;
+        }
+      }
+    }
+    if (!any) return -1;
+    double a[DW];
+    bool fb = false;
+    const double vn = sqrt(sqnorm<DW>(yd));
+    if (vn < 1e-6) {
+      fb = true;
+    } else {
+      double dy = 0.0;
+#pragma unroll
+      for (int k = 0; k < DW; ++k) dy = dy + d[k] * yd[k];
+      const double coef = dy / sqnorm<DW>(yd);
+#pragma unroll
+      for (int k = 0; k < DW; ++k) a[k] = d[k] - coef * yd[k];
+      if (sqrt(sqnorm<DW>(a)) < 1e-6 * sqrt(sqnorm<DW>(d))) fb = true;
+    }
+    if (fb) {
+#pragma unroll
+      for (int k = 0; k < DW; ++k) a[k] = d[k];
+    }
+#pragma unroll
+    for (int k = 0; k < DW; ++k) a_out[count * DW + k] = a[k];
+    b_out[count] = sqnorm<DW>(a);
+    fb_out[count] = fb ? 1 : 0;
+    ++count;
+    best = nb;
+  }
+  return count;
+}
+
 // obstacle boxes staged in shared memory (block-wide; returns the view on them)
 template <int DW>
 __device__ __forceinline__ WorldD stage_world(const WorldD& w, double* smem) {

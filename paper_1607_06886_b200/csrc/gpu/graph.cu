@@ -826,16 +826,27 @@ __global__ void __launch_bounds__(128) k_regions(GraphArgs g, WorldD w, int64_t 
 // warp-aggregated atomicAdd.  Waypoint w owns [hs_off[w], hs_off[w] +
 // hs_cnt[w]) (not in waypoint order; export rebuilds the CSR).  If the
 // reserved total exceeds cap nothing past cap is written and the host reruns
-// with the exact size (the counter returns it).
+// with the exact size (the counter returns it).  The region itself is
+// convex_region_fused (per-box squared distances computed once into shared
+// memory, one pass per iteration; PUMP_REGIONS_LEGACY=1 runs convex_region),
+// and each waypoint finds its edge in the k_wp_edge map.
 constexpr int kOnceMaxObs = 16;
-template <int DW>
+
+// waypoint -> owning edge (one thread per edge fills its waypoint range)
+__global__ void k_wp_edge(int64_t n_edges, const int64_t* __restrict__ wp_off, int32_t* __restrict__ wp_edge) {
+  const int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (e >= n_edges) return;
+  for (int64_t x = wp_off[e]; x < wp_off[e + 1]; ++x) wp_edge[x] = static_cast<int32_t>(e);
+}
+template <int DW, bool REG>
 __global__ void __launch_bounds__(128) k_regions_once(GraphArgs g, WorldD w, int64_t n_wp, int64_t n_edges,
                                                       const int64_t* __restrict__ wp_off,
                                                       const int32_t* __restrict__ e_from,
                                                       const int32_t* __restrict__ e_to, const double* __restrict__ e_tau,
                                                       const double* __restrict__ e_acc0,
                                                       const double* __restrict__ e_jerk,
-                                                      const int32_t* __restrict__ e_nsteps, int64_t cap,
+                                                      const int32_t* __restrict__ e_nsteps,
+                                                      const int32_t* __restrict__ wp_edge, int64_t cap,
                                                       unsigned long long* __restrict__ counter,
                                                       int64_t* __restrict__ hs_off, int32_t* __restrict__ hs_cnt,
                                                       double* __restrict__ hs_pk, uint8_t* __restrict__ hs_fb,
@@ -849,15 +860,7 @@ __global__ void __launch_bounds__(128) k_regions_once(GraphArgs g, WorldD w, int
   uint8_t lf[kOnceMaxObs];
   int n = 0;
   if (active) {
-    int64_t lo = 0, hi = n_edges;
-    while (hi - lo > 1) {
-      const int64_t mid = (lo + hi) >> 1;
-      if (wp_off[mid] <= x)
-        lo = mid;
-      else
-        hi = mid;
-    }
-    const int64_t e = lo;
+    const int64_t e = wp_edge[x];
     const int j = static_cast<int>(x - wp_off[e]) + 1;
     const int L = e_nsteps[e];
     const int v = e_from[e], u = e_to[e];
@@ -882,7 +885,10 @@ __global__ void __launch_bounds__(128) k_regions_once(GraphArgs g, WorldD w, int
     } else {
       motion_state<DW>(m, j * g.dt, y, yd);
     }
-    n = convex_region<DW, 1>(ws, y, yd, la, lb, lf);
+    if constexpr (REG)
+      n = convex_region_fused<DW>(ws, y, yd, smem + 2 * w.n_obs * DW + threadIdx.x, blockDim.x, la, lb, lf);
+    else
+      n = convex_region<DW, 1>(ws, y, yd, la, lb, lf);
     if (n < 0) {
       atomicExch(err, 1);
       n = 0;
@@ -1230,6 +1236,12 @@ void build_graph_device(DevGraph& G, Ctx& c, int n, int dw, const double* h_pos,
   G.hs_cnt.ensure(al((NW + 2) * 4));
   PUMP_CUDA(cudaMemsetAsync(err.p, 0, 4, st));
   if (w.n_obs <= kOnceMaxObs) {
+    DBuf& wpe = c.buf("g_wp_edge", al((NW + 8) * 4));
+    if (E > 0) {
+      KScope ks(st, F_REGIONS);
+      k_wp_edge<<<grid_for(E, 256), 256, 0, st>>>(E, G.wp_off.as<int64_t>(), wpe.as<int32_t>());
+      ++c.launches;
+    }
     DBuf& ctr = c.buf("g_hs_counter", 256);
     int64_t cap = std::max<int64_t>(G.hs_cap, NW * 4 + 16);
     for (int attempt = 0; attempt < 2; ++attempt) {
@@ -1240,11 +1252,15 @@ void build_graph_device(DevGraph& G, Ctx& c, int n, int dw, const double* h_pos,
       if (NW > 0) {
         KScope ks(st, F_REGIONS);
         dispatch_dw(dw, [&]<int DW>() {
-          if (wsmem > 48 * 1024)
-            PUMP_CUDA(cudaFuncSetAttribute(k_regions_once<DW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wsmem));
-          k_regions_once<DW><<<grid_for(NW, 128), 128, wsmem, st>>>(
+          static const bool reg = getenv("PUMP_REGIONS_LEGACY") == nullptr;
+          auto kern = reg ? k_regions_once<DW, true> : k_regions_once<DW, false>;
+          const size_t sm = wsmem + (reg ? static_cast<size_t>(w.n_obs) * 128 * 8 : 0);
+          if (sm > 48 * 1024)
+            PUMP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+          kern<<<grid_for(NW, 128), 128, sm, st>>>(
               ga, wd, NW, E, G.wp_off.as<int64_t>(), G.e_from.as<int32_t>(), G.e_to.as<int32_t>(),
-              G.e_tau.as<double>(), G.e_acc0.as<double>(), G.e_jerk.as<double>(), G.e_nsteps.as<int32_t>(), cap,
+              G.e_tau.as<double>(), G.e_acc0.as<double>(), G.e_jerk.as<double>(), G.e_nsteps.as<int32_t>(),
+              c.scratch["g_wp_edge"].as<int32_t>(), cap,
               ctr.as<unsigned long long>(), G.hs_off.as<int64_t>(), G.hs_cnt.as<int32_t>(), G.hs_pk.as<double>(),
               G.hs_fb.as<uint8_t>(), err.as<int>());
         });
