@@ -336,60 +336,81 @@ __host__ __device__ __forceinline__ void motion_bbox(const MotionD<DW>& m, doubl
 // separated from the box (the only ones any point on the motion, or any
 // segment between such points, can touch).
 constexpr int kCullWords = 4;
-struct MotionCull {
+constexpr int kCullList = 64;  // candidate index list when there are more boxes than bitmask bits
+// LIST = 0: bitmask only (<= 64 kCullWords boxes; more boxes are all tested);
+// LIST = kCullList: an index list of up to LIST candidates for larger worlds
+template <int LIST>
+struct MotionCullT {
   bool inside, masked, any;
+  int nlist;  // -1: candidates in the bitmask; else list[0..nlist)
   uint64_t cand[kCullWords];
+  uint16_t list[LIST > 0 ? LIST : 1];
 };
+using MotionCull = MotionCullT<0>;
 
-template <int DW>
-__host__ __device__ inline MotionCull motion_cull(const MotionD<DW>& m, const WorldD& w) {
-  MotionCull c;
+// f(o) for every candidate box o (ascending); true as soon as one f is true
+template <int LIST, class F>
+__host__ __device__ __forceinline__ bool cull_any(const MotionCullT<LIST>& c, F f) {
+  if (LIST == 0 || c.nlist < 0) {
+    for (int q = 0; q < kCullWords; ++q)
+      for (uint64_t x = c.cand[q]; x; x &= x - 1)
+        if (f(q * 64 + __builtin_ctzll_hd(x))) return true;
+    return false;
+  }
+  for (int i = 0; i < c.nlist; ++i)
+    if (f(static_cast<int>(c.list[i]))) return true;
+  return false;
+}
+
+template <int DW, int LIST = 0>
+__host__ __device__ inline MotionCullT<LIST> motion_cull(const MotionD<DW>& m, const WorldD& w) {
+  MotionCullT<LIST> c;
   double bl[DW], bh[DW];
   motion_bbox<DW>(m, bl, bh);
   c.inside = true;
 #pragma unroll
   for (int k = 0; k < DW; ++k) c.inside = c.inside && bl[k] > w.blo[k] && bh[k] < w.bhi[k];
   for (int q = 0; q < kCullWords; ++q) c.cand[q] = 0;
-  c.masked = w.n_obs <= 64 * kCullWords;
-  c.any = !c.masked;
-  if (c.masked) {
-    for (int o = 0; o < w.n_obs; ++o) {
-      bool sep = false;
+  c.nlist = w.n_obs <= 64 * kCullWords ? -1 : 0;
+  c.masked = true;
+  c.any = false;
+  for (int o = 0; o < w.n_obs; ++o) {
+    bool sep = false;
 #pragma unroll
-      for (int k = 0; k < DW; ++k) sep = sep || (bh[k] < w.lo[o * DW + k]) || (bl[k] > w.hi[o * DW + k]);
-      if (!sep) {
-        c.cand[o >> 6] |= 1ull << (o & 63);
-        c.any = true;
-      }
+    for (int k = 0; k < DW; ++k) sep = sep || (bh[k] < w.lo[o * DW + k]) || (bl[k] > w.hi[o * DW + k]);
+    if (sep) continue;
+    c.any = true;
+    if (c.nlist < 0) {
+      c.cand[o >> 6] |= 1ull << (o & 63);
+    } else if (c.nlist < LIST) {
+      c.list[c.nlist++] = static_cast<uint16_t>(o);
+    } else {
+      c.masked = false;  // too many candidates: test every box
+      break;
     }
   }
   return c;
 }
 
 // point_free (geom.hpp:56-61) for a point on the motion `c` was computed for
-template <int DW>
-__host__ __device__ inline bool point_free_culled(const WorldD& w, const MotionCull& c, const double* p) {
+template <int DW, int LIST>
+__host__ __device__ inline bool point_free_culled(const WorldD& w, const MotionCullT<LIST>& c, const double* p) {
   if (!c.inside && !box_contains<DW>(w.blo, w.bhi, p)) return false;
   if (!c.masked) {
     for (int o = 0; o < w.n_obs; ++o)
       if (box_contains<DW>(w.lo + o * DW, w.hi + o * DW, p)) return false;
     return true;
   }
-  for (int q = 0; q < kCullWords; ++q)
-    for (uint64_t x = c.cand[q]; x; x &= x - 1) {
-      const int o = q * 64 + __builtin_ctzll_hd(x);
-      if (box_contains<DW>(w.lo + o * DW, w.hi + o * DW, p)) return false;
-    }
-  return true;
+  return !cull_any(c, [&](int o) { return box_contains<DW>(w.lo + o * DW, w.hi + o * DW, p); });
 }
 
-template <int DW>
+template <int DW, int LIST = 0>
 __host__ __device__ inline bool motion_collides(const MotionD<DW>& m, const WorldD& w, double eps_cc,
-                                                const MotionCull* pre = nullptr) {
-  const MotionCull cull = pre ? *pre : motion_cull<DW>(m, w);
+                                                const MotionCullT<LIST>* pre = nullptr) {
+  MotionCullT<LIST> own;
+  if (!pre) own = motion_cull<DW, LIST>(m, w);
+  const MotionCullT<LIST>& cull = pre ? *pre : own;
   const bool inside = cull.inside, masked = cull.masked, any = cull.any;
-  constexpr int kMaskWords = kCullWords;
-  const uint64_t* cand = cull.cand;
   if (inside && !any) return false;
   auto free_pt = [&](const double* p) {
     if (!inside && !box_contains<DW>(w.blo, w.bhi, p)) return false;
@@ -398,21 +419,11 @@ __host__ __device__ inline bool motion_collides(const MotionD<DW>& m, const Worl
         if (box_contains<DW>(w.lo + o * DW, w.hi + o * DW, p)) return false;
       return true;
     }
-    for (int q = 0; q < kMaskWords; ++q)
-      for (uint64_t x = cand[q]; x; x &= x - 1) {
-        const int o = q * 64 + __builtin_ctzll_hd(x);
-        if (box_contains<DW>(w.lo + o * DW, w.hi + o * DW, p)) return false;
-      }
-    return true;
+    return !cull_any(cull, [&](int o) { return box_contains<DW>(w.lo + o * DW, w.hi + o * DW, p); });
   };
   auto seg_hit = [&](const double* a, const double* b) {
     if (!masked) return segment_collides<DW>(w, a, b);
-    for (int q = 0; q < kMaskWords; ++q)
-      for (uint64_t x = cand[q]; x; x &= x - 1) {
-        const int o = q * 64 + __builtin_ctzll_hd(x);
-        if (segment_hits<DW>(a, b, w.lo + o * DW, w.hi + o * DW)) return true;
-      }
-    return false;
+    return cull_any(cull, [&](int o) { return segment_hits<DW>(a, b, w.lo + o * DW, w.hi + o * DW); });
   };
   double p0[DW], p1[DW];
   motion_pos<DW>(m, 0.0, p0);
@@ -440,15 +451,12 @@ __host__ __device__ inline bool motion_collides(const MotionD<DW>& m, const Worl
       sh[k] = (q0[k] < q1[k] ? q1[k] : q0[k]) + dev;
       if (!inside && !(sl[k] > w.blo[k] && sh[k] < w.bhi[k])) return false;
     }
-    for (int q = 0; q < kMaskWords; ++q)
-      for (uint64_t x = cand[q]; x; x &= x - 1) {
-        const int o = q * 64 + __builtin_ctzll_hd(x);
-        bool sep = false;
+    return !cull_any(cull, [&](int o) {
+      bool sep = false;
 #pragma unroll
-        for (int k = 0; k < DW; ++k) sep = sep || (sh[k] < w.lo[o * DW + k]) || (sl[k] > w.hi[o * DW + k]);
-        if (!sep) return false;
-      }
-    return true;
+      for (int k = 0; k < DW; ++k) sep = sep || (sh[k] < w.lo[o * DW + k]) || (sl[k] > w.hi[o * DW + k]);
+      return !sep;
+    });
   };
   double st0[64], st1[64];
   int sp = 0;

@@ -661,7 +661,7 @@ __global__ void k_cand_compact(int n, int64_t n_surv, const uint8_t* __restrict_
 }
 
 
-template <int DW>
+template <int DW, int LIST>
 __global__ void __launch_bounds__(128) k_collide(GraphArgs g, WorldD w, int64_t n_cand,
                                                  const int32_t* __restrict__ c_v, const int32_t* __restrict__ c_u,
                                                  const double* __restrict__ c_tau, uint8_t* __restrict__ valid,
@@ -681,8 +681,8 @@ __global__ void __launch_bounds__(128) k_collide(GraphArgs g, WorldD w, int64_t 
     m.v1[k] = g.vel[u * DW + k];
   }
   coeffs_dev<DW>(m.p0, m.v0, m.p1, m.v1, m.tau, m.a, m.j);
-  const MotionCull cull = motion_cull<DW>(m, ws);
-  bool ok = !motion_collides<DW>(m, ws, g.eps_cc, &cull);
+  const MotionCullT<LIST> cull = motion_cull<DW, LIST>(m, ws);
+  bool ok = !motion_collides<DW, LIST>(m, ws, g.eps_cc, &cull);
   int L = 0;
   if (ok) {
     // motion_waypoints (steer.hpp:192-212): k = floor(tau/dt + 1e-9)
@@ -1149,11 +1149,11 @@ void build_graph_device(DevGraph& G, Ctx& c, int n, int dw, const double* h_pos,
   if (n_cand > 0) {
     KScope ks(st, F_COLLIDE);
     dispatch_dw(dw, [&]<int DW>() {
+      auto kern = w.n_obs <= 64 * kCullWords ? k_collide<DW, 0> : k_collide<DW, kCullList>;
       if (wsmem > 48 * 1024)
-        PUMP_CUDA(cudaFuncSetAttribute(k_collide<DW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wsmem));
-      k_collide<DW><<<grid_for(n_cand, 128), 128, wsmem, st>>>(ga, wd, n_cand, cv.as<int32_t>(), cuu.as<int32_t>(),
-                                                               ctau.as<double>(), valid.as<uint8_t>(),
-                                                               nst.as<int32_t>());
+        PUMP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wsmem));
+      kern<<<grid_for(n_cand, 128), 128, wsmem, st>>>(ga, wd, n_cand, cv.as<int32_t>(), cuu.as<int32_t>(),
+                                                      ctau.as<double>(), valid.as<uint8_t>(), nst.as<int32_t>());
     });
     ++c.launches;
     PUMP_CUDA(cudaGetLastError());

@@ -69,6 +69,28 @@ def test_build_graph_bit_exact(oracle_lib, gpu_ctx, name, samples):
     assert_graph_equal(gg, og)
 
 
+@pytest.mark.parametrize("n_boxes,samples", [(300, 500), (1000, 400)])
+def test_build_graph_many_obstacles(oracle_lib, gpu_ctx, n_boxes, samples):
+    """> 256 boxes: the motion cull keeps a candidate index list instead of the bitmask."""
+    import sys
+
+    from paper_1607_06886_b200 import api
+
+    sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "scenarios"))
+    import make_scenarios
+
+    j = make_scenarios.forest(n_boxes=n_boxes)
+    j["samples"] = samples
+    txt = json.dumps(j)
+    _, sc = oracle_lib.scenario_models(txt)
+    pos, vel = oracle_lib.scenario_nodes(txt)
+    args = (ws_of(j), goal_of(j), sc["r_n"], sc["dt"], sc["eps_cc"], sc["tau_max"])
+    og = oracle_lib.build_graph(pos, vel, *args, workers=WORKERS).export()
+    gg = api.build_graph(pos, vel, *args, ctx=gpu_ctx).export()
+    assert og["n_edges"] > 0
+    assert_graph_equal(gg, og)
+
+
 def test_build_graph_degenerate_and_complete(oracle_lib, gpu_ctx):
     """test_plan.cpp:82-101: tiny radius -> no edges; huge radius -> complete."""
     from paper_1607_06886_b200 import api
