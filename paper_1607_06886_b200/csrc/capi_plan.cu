@@ -171,6 +171,57 @@ static bool nominal_free(const HostWorld& w, const std::vector<HWp>& t, double e
   return true;
 }
 
+// ------------------------------------------------------------ smoothing kernels
+// Smoothing probes on the device (pump.hpp:84-146): for each probed blend
+// fraction s the blended trajectory (1 - s) plan + s opt (positions and
+// velocities, the host blend's expressions), then nominal_free of it
+// (pump.hpp:64-75: every waypoint point_free, every positive-length segment's
+// cubic Hermite motion_collides).  The positions feed the MC batch directly.
+template <int DW>
+__global__ void k_smooth_blend(int n_probe, int n_wp, const double* __restrict__ sv, const double* __restrict__ pt,
+                               const double* __restrict__ pp, const double* __restrict__ pv, MotionD<DW> opt,
+                               double* __restrict__ y, double* __restrict__ yv) {
+  const int64_t x = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (x >= static_cast<int64_t>(n_probe) * n_wp) return;
+  const int q = static_cast<int>(x % n_wp);
+  const double s = sv[x / n_wp];
+  double op[DW], ov[DW];
+  motion_state<DW>(opt, pt[q], op, ov);
+#pragma unroll
+  for (int k = 0; k < DW; ++k) {
+    y[x * DW + k] = (1 - s) * pp[q * DW + k] + s * op[k];
+    yv[x * DW + k] = (1 - s) * pv[q * DW + k] + s * ov[k];
+  }
+}
+
+template <int DW>
+__global__ void k_smooth_check(WorldD w, int n_probe, int n_wp, const double* __restrict__ pt,
+                               const double* __restrict__ y, const double* __restrict__ yv, double eps_cc,
+                               int32_t* __restrict__ free_flag) {
+  const int64_t x = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (x >= static_cast<int64_t>(n_probe) * n_wp) return;
+  const int64_t pr = x / n_wp;
+  const int j = static_cast<int>(x % n_wp);
+  bool ok = point_free<DW>(w, y + x * DW);
+  if (ok && j + 1 < n_wp) {
+    const double h = pt[j + 1] - pt[j];
+    if (h > 0) {
+      MotionD<DW> m;
+#pragma unroll
+      for (int k = 0; k < DW; ++k) {
+        m.p0[k] = y[x * DW + k];
+        m.v0[k] = yv[x * DW + k];
+        m.p1[k] = y[(x + 1) * DW + k];
+        m.v1[k] = yv[(x + 1) * DW + k];
+      }
+      m.tau = h;
+      coeffs_dev<DW>(m.p0, m.v0, m.p1, m.v1, m.tau, m.a, m.j);
+      ok = !motion_collides<DW>(m, w, eps_cc);
+    }
+  }
+  if (!ok) free_flag[pr] = 0;
+}
+
 // ------------------------------------------------------------ path kernels
 // Walk parent pointers of selected plans and resolve each hop to its edge
 // (first edge v->u in the ascending row, as planner.hpp:297-302).
@@ -963,6 +1014,97 @@ static void run_pump_device(Ctx& c, const pumpb::Scenario& s, const DevGraph* pr
       auto v = mc_values(c, L, dwld, batch, s.mc_samples, s.seeds.mc, eps_cc, &R.s.mc_ms, &R.s.mc_rollouts);
       for (size_t k = 0; k < todo.size(); ++k) probes[todo[k]].mc = v[k];
     };
+    // the same on the device: blend, nominal check and MC of every new
+    // candidate in one batch (one synchronisation); MC of a candidate whose
+    // nominal collides is computed but never used (the reference skips it)
+    static const bool host_probes = std::getenv("PUMP_SMOOTH_HOST") != nullptr;
+    const int n_wp = static_cast<int>(plan.size());
+    if (!host_probes) {
+      // the plan's times, positions and velocities in one upload
+      std::vector<double> pl(static_cast<size_t>(n_wp) * (1 + 2 * dw));
+      for (int q = 0; q < n_wp; ++q) {
+        pl[q] = plan[q].t;
+        for (int k = 0; k < dw; ++k) {
+          pl[n_wp + q * dw + k] = plan[q].p[k];
+          pl[n_wp * (1 + dw) + q * dw + k] = plan[q].v[k];
+        }
+      }
+      c.h2d(c.buf("sm_plan", pl.size() * 8 + 256).p, pl.data(), pl.size() * 8);
+    }
+    auto evaluate_dev = [&](const std::vector<double>& cands) {
+      std::vector<double> todo;
+      for (double sv : cands)
+        if (!probes.count(sv) && std::find(todo.begin(), todo.end(), sv) == todo.end()) todo.push_back(sv);
+      const int np = static_cast<int>(todo.size());
+      if (np == 0) return;
+      const int64_t items = static_cast<int64_t>(np) * n_wp;
+      DBuf& d_y = c.buf("sm_y", items * dw * 8 + 256);
+      DBuf& d_yv = c.buf("sm_yv", items * dw * 8 + 256);
+      // one upload (s values, MC offsets) and one download (hits, free flags)
+      DBuf& d_in = c.buf("sm_in", (2 * np + 1) * 8 + 256);
+      DBuf& d_out = c.buf("sm_out", (np + 1) * 8 + np * 4 + 256);
+      std::vector<int64_t> in(2 * np + 1);
+      std::memcpy(in.data(), todo.data(), np * 8);
+      for (int k = 0; k <= np; ++k) in[np + k] = static_cast<int64_t>(k) * n_wp;
+      c.h2d(d_in.p, in.data(), (2 * np + 1) * 8);
+      const double* d_s = d_in.as<double>();
+      const int64_t* d_off = d_in.as<int64_t>() + np;
+      unsigned long long* d_h = d_out.as<unsigned long long>();
+      int32_t* d_free = reinterpret_cast<int32_t*>(d_out.as<int64_t>() + np + 1);
+      PUMP_CUDA(cudaMemsetAsync(d_h, 0, (np + 1) * 8, c.stream));
+      PUMP_CUDA(cudaMemsetAsync(d_free, 1, np * 4, c.stream));  // nonzero: free until a check fails
+      WorldD wd;
+      wd.n_obs = dwld.n_obs;
+      wd.lo = dwld.d_lo;
+      wd.hi = dwld.d_hi;
+      for (int k = 0; k < 6; ++k) {
+        wd.blo[k] = dwld.blo[k];
+        wd.bhi[k] = dwld.bhi[k];
+      }
+      c.tic();
+      dispatch_dw(dw, [&]<int DW>() {
+        HMotion o = opt;
+        k_smooth_blend<DW><<<grid_for(items, 128), 128, 0, c.stream>>>(
+            np, n_wp, d_s, c.scratch["sm_plan"].as<double>(), c.scratch["sm_plan"].as<double>() + n_wp,
+            c.scratch["sm_plan"].as<double>() + n_wp * (1 + dw), as_motion<DW>(o), d_y.as<double>(), d_yv.as<double>());
+        k_smooth_check<DW><<<grid_for(items, 128), 128, 0, c.stream>>>(
+            wd, np, n_wp, c.scratch["sm_plan"].as<double>(), d_y.as<double>(), d_yv.as<double>(), eps_cc, d_free);
+      });
+      c.launches += 2;
+      PUMP_CUDA(cudaGetLastError());
+      int64_t r0 = 0, r1 = s.mc_samples;
+      shard_range(s.mc_samples, c.rank, c.world, &r0, &r1);
+      if (c.mc_join_pending) {
+        PUMP_CUDA(cudaStreamWaitEvent(c.stream, c.join, 0));
+        c.mc_join_pending = false;
+      }
+      launch_mc(L, dwld, np, d_off, d_y.as<double>(), n_wp, r0, r1, s.seeds.mc, eps_cc, d_h, c.stream, &c.launches,
+                d_h + np, &c.mc_table, d_free);
+      allreduce_sum_i64(c, reinterpret_cast<int64_t*>(d_h), np);
+      std::vector<int64_t> outv(np + 1 + (np + 1) / 2);
+      c.d2h(outv.data(), d_out.p, (np + 1) * 8 + np * 4);
+      const int64_t* hits = outv.data();
+      const int32_t* fr = reinterpret_cast<const int32_t*>(outv.data() + np + 1);
+      R.s.mc_ms += c.toc();
+      c.sync();
+      kprof_work(F_MC, hits[np]);
+      c.mc_rollout_steps += hits[np];
+      for (int k = 0; k < np; ++k) {
+        Probe p;
+        p.free = fr[k] != 0;
+        if (p.free) {
+          p.mc = static_cast<double>(hits[k]) / s.mc_samples;
+          R.s.mc_rollouts += r1 - r0;
+        }
+        probes.emplace(todo[k], std::move(p));
+      }
+    };
+    auto run_probes = [&](const std::vector<double>& cands) {
+      if (host_probes)
+        evaluate(cands);
+      else
+        evaluate_dev(cands);
+    };
     auto certified = [&](double sv) {
       const Probe& p = probes.at(sv);
       return p.free && p.mc <= s.alpha;
@@ -982,18 +1124,20 @@ static void run_pump_device(Ctx& c, const pumpb::Scenario& s, const DevGraph* pr
       }
     };
     auto accept = [&](double sv) {
-      const Probe& p = probes.at(sv);
+      Probe& p = probes.at(sv);
+      if (p.traj.empty()) p.traj = blend(sv);  // device probes keep only the verdicts
       best = p.traj;
       best_cost = trajectory_cost(p.traj, dw);
       best_mc = p.mc;
       best_s = sv;
     };
     // Batch schedule: depths of the speculative subtrees covering the 10
-    // bisection steps.  Default: one probe per launch (the reference's order;
-    // a single 20000-rollout launch is the cheapest with the lane-parallel
-    // MC kernel).  PUMP_SMOOTH_SCHEDULE="3,3,4" trades extra rollouts for
-    // fewer launches.
+    // bisection steps.  Host probes (PUMP_SMOOTH_HOST=1): one probe per MC
+    // launch.  Device probes (default): depth-2 subtrees, 3 candidates per
+    // batch (blend + nominal check + MC in one round trip).
+    // PUMP_SMOOTH_SCHEDULE="3,3,4" overrides.
     std::vector<int> schedule(10, 1);
+    if (!host_probes) schedule = {2, 2, 2, 2, 2};  // device probes: 3-candidate subtrees, 6 round trips
     if (const char* e = std::getenv("PUMP_SMOOTH_SCHEDULE")) {
       schedule.clear();
       for (const char* q = e; *q;) {
@@ -1002,7 +1146,7 @@ static void run_pump_device(Ctx& c, const pumpb::Scenario& s, const DevGraph* pr
         if (*q == ',') ++q;
       }
     }
-    evaluate({1.0});
+    run_probes({1.0});
     if (certified(1.0)) {
       accept(1.0);
     } else {
@@ -1011,7 +1155,7 @@ static void run_pump_device(Ctx& c, const pumpb::Scenario& s, const DevGraph* pr
       for (size_t b = 0; b < schedule.size() && it < 10; ++b) {
         std::vector<double> more;
         subtree(lo, hi, std::min(schedule[b], 10 - it), more);
-        evaluate(more);
+        run_probes(more);
         for (int d = 0; d < schedule[b] && it < 10; ++d, ++it) {
           const double mid = 0.5 * (lo + hi);
           if (certified(mid)) {

@@ -213,6 +213,7 @@ void mc_table_prepare(McTable& tab, const HostLoop& L, int64_t r0, int64_t r1, u
                       cudaStream_t st, int64_t* launches);
 void launch_mc(const HostLoop& L, const DevWorld& w, int n_traj, const int64_t* d_traj_off, const double* d_ynom,
                int max_points, int64_t r0, int64_t r1, uint64_t seed, double eps_cc, unsigned long long* d_hits,
-               cudaStream_t st, int64_t* launches, unsigned long long* d_steps = nullptr, McTable* table = nullptr);
+               cudaStream_t st, int64_t* launches, unsigned long long* d_steps = nullptr, McTable* table = nullptr,
+               const int32_t* d_live = nullptr);  // d_live[j] == 0: skip trajectory j (table path; hits stay 0)
 
 }  // namespace pumpg

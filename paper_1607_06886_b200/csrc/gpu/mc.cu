@@ -685,7 +685,7 @@ __global__ void __launch_bounds__(kMcBlock) k_mc_tab(WorldD w, const int64_t* __
                                                      const double* __restrict__ ynom_all, int64_t r0, int64_t r1,
                                                      int64_t tab_r0, int64_t tab_n, const double* __restrict__ dy,
                                                      const unsigned long long* __restrict__ maxdev, double eps_cc,
-                                                     uint8_t* __restrict__ flags) {
+                                                     uint8_t* __restrict__ flags, const int32_t* __restrict__ live) {
   extern __shared__ double smem[];
   constexpr int kStepCap = 64;  // block-wide candidate obstacles per step (more: test all)
   __shared__ uint16_t s_list[kMcChunk + 1][kStepCap];
@@ -693,6 +693,7 @@ __global__ void __launch_bounds__(kMcBlock) k_mc_tab(WorldD w, const int64_t* __
   __shared__ int s_skip[kMcChunk + 1];
   __shared__ int s_all_skip;
   const int j = blockIdx.y;
+  if (live && !live[j]) return;  // trajectory not certified (its nominal collides): flags stay 0
   const int64_t p_begin = traj_off[j];
   const int n_pts = static_cast<int>(traj_off[j + 1] - p_begin);
   const int T = n_pts - 1;
@@ -892,8 +893,10 @@ __global__ void __launch_bounds__(kMcBlock) k_mc_tab(WorldD w, const int64_t* __
 __global__ void __launch_bounds__(256) k_mc_count(const uint8_t* __restrict__ flags, int64_t n,
                                                   const int64_t* __restrict__ traj_off,
                                                   unsigned long long* __restrict__ hits,
-                                                  unsigned long long* __restrict__ steps_out) {
+                                                  unsigned long long* __restrict__ steps_out,
+                                                  const int32_t* __restrict__ live) {
   const int j = blockIdx.y;
+  if (live && !live[j]) return;
   const uint8_t* f = flags + static_cast<int64_t>(j) * n;
   unsigned c = 0;
   for (int64_t x = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; x < n;
@@ -1028,7 +1031,8 @@ void mc_table_prepare(McTable& tab, const HostLoop& HL, int64_t r0, int64_t r1, 
 
 void launch_mc(const HostLoop& HL, const DevWorld& w, int n_traj, const int64_t* d_traj_off, const double* d_ynom,
                int max_points, int64_t r0, int64_t r1, uint64_t seed, double eps_cc, unsigned long long* d_hits,
-               cudaStream_t st, int64_t* launches, unsigned long long* d_steps, McTable* table) {
+               cudaStream_t st, int64_t* launches, unsigned long long* d_steps, McTable* table,
+               const int32_t* d_live) {
   if (r1 <= r0 || n_traj <= 0) return;
   if (HL.dw != w.dw) throw std::invalid_argument("mc_certify: workspace / model dimension mismatch");
   static const bool direct = std::getenv("PUMP_MC_DIRECT") != nullptr;
@@ -1038,7 +1042,7 @@ void launch_mc(const HostLoop& HL, const DevWorld& w, int n_traj, const int64_t*
   if (table && !direct && r1 - r0 > kTabRollouts) {
     for (int64_t c0 = r0; c0 < r1; c0 += kTabRollouts)
       launch_mc(HL, w, n_traj, d_traj_off, d_ynom, max_points, c0, std::min(r1, c0 + kTabRollouts), seed, eps_cc,
-                d_hits, st, launches, d_steps, table);
+                d_hits, st, launches, d_steps, table, d_live);
     return;
   }
   if (table && !direct && ensure_table(*table, HL, r0, r1, seed, max_points - 1, st, launches)) {
@@ -1062,9 +1066,9 @@ void launch_mc(const HostLoop& HL, const DevWorld& w, int n_traj, const int64_t*
       k_mc_tab<DW><<<grid, kMcBlock, smem, st>>>(wd, d_traj_off, d_ynom, r0, r1, table->r0, table->r1 - table->r0,
                                                  table->dy.as<double>(),
                                                  table->maxdev.as<unsigned long long>(), eps_cc,
-                                                 table->flags.as<uint8_t>());
+                                                 table->flags.as<uint8_t>(), d_live);
       k_mc_count<<<dim3(static_cast<unsigned>(std::min<int64_t>((n + 255) / 256, 64)), n_traj), 256, 0, st>>>(
-          table->flags.as<uint8_t>(), n, d_traj_off, d_hits, d_steps);
+          table->flags.as<uint8_t>(), n, d_traj_off, d_hits, d_steps, d_live);
     });
     *launches += 2;
     PUMP_CUDA(cudaGetLastError());
