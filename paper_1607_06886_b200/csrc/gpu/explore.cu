@@ -247,7 +247,8 @@ __global__ void __launch_bounds__(kExpBlock) k_expand(const ExpandArgs a) {
   __shared__ double2 s_hs[kExpBlock / 32][kExpStage][2];
   const int64_t task = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-  if (task >= *a.d_T) return;
+  // (a pipelined round's grid covers its task capacity; a halted round has none)
+  if (task >= *a.d_T || a.st->halt) return;
   expand_task<DW, CH>(a, task, lane, wib, s_hs);
 }
 
@@ -693,17 +694,48 @@ __global__ void k_group_post(const int64_t* d_G, const int32_t* group, const int
 // per task: its plan and edge (warp per group entry), so k_expand starts
 // from two independent loads instead of a chain group -> plan -> head -> row
 __global__ void k_task_map(const int64_t* d_G, const int64_t* task_off, const int32_t* group, const int32_t* head,
-                           const int64_t* row_ptr, int32_t* task_pid, int64_t* task_e) {
-  const int64_t g = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+                           const int64_t* row_ptr, int32_t* task_pid, int64_t* task_e, const ExploreStatus* st) {
   const int lane = threadIdx.x & 31;
-  if (g >= *d_G) return;
-  const int64_t t0 = task_off[g], t1 = task_off[g + 1];
-  const int pid = group[g];
-  const int64_t e0 = row_ptr[head[pid]];
-  for (int64_t t = t0 + lane; t < t1; t += 32) {
-    task_pid[t] = pid;
-    task_e[t] = e0 + (t - t0);
+  if (st->halt) return;
+  const int64_t Gn = *d_G;
+  const int64_t stride = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  for (int64_t g = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; g < Gn; g += stride) {
+    const int64_t t0 = task_off[g], t1 = task_off[g + 1];
+    const int pid = group[g];
+    const int64_t e0 = row_ptr[head[pid]];
+    for (int64_t t = t0 + lane; t < t1; t += 32) {
+      task_pid[t] = pid;
+      task_e[t] = e0 + (t - t0);
+    }
   }
+}
+
+// Pipelined rounds: the loop-top decisions of run_explore_device made on the
+// device before each enqueued round (planner.hpp:126-138 termination, the
+// cooperative path's key-range and buffer-capacity conditions).  A round that
+// may not run sets halt; every later kernel of it, and every later round,
+// then exits at once, and the host takes over from the status it reads.
+struct GateCaps {
+  long long T, arena, pool;
+};
+__global__ void k_round_gate(ExploreStatus* S, GateCaps cap) {
+  if (S->halt) return;
+  const double best_goal = __longlong_as_double(S->best_goal_bits);
+  const double min_group = __longlong_as_double(S->min_group_bits);
+  if ((S->G > 0 && best_goal != __builtin_inf() && best_goal <= min_group) || (S->G == 0 && S->open_count == 0)) {
+    S->halt = 1;
+    return;
+  }
+  const long long T = S->T;
+  long long nk = 1 << 18;
+  if (S->min_bucket != LLONG_MAX && S->i + 2 - S->min_bucket <= 512) nk = S->i + 2 - S->min_bucket > 1 ? S->i + 2 - S->min_bucket : 1;
+  if (T <= 0 || nk > 512 || T + 1 > cap.T || S->n_plans + T + 1 > cap.arena || S->pool_n + T + 1 > cap.pool) {
+    S->halt = 2;
+    return;
+  }
+  S->n_keys = nk;
+  S->rounds += 1;
+  S->partial_plans += T;
 }
 
 // group size, its task count (task_off[G]) and the compacted pool size
@@ -910,6 +942,8 @@ __global__ void __launch_bounds__(kCoopBlock, 2) k_round_tail(const CoopArgs A) 
     ++stamp_i;
   };
   STAMP();
+  if (S->halt) return;  // pipelined round that does not run (uniform: the gate ran before this launch)
+  const int64_t n_keys = A.n_keys > 0 ? A.n_keys : S->n_keys;
 
   // (k_task_map and k_expand ran as their own launches before this one)
   const int64_t T = *A.d_T;
@@ -1027,7 +1061,7 @@ __global__ void __launch_bounds__(kCoopBlock, 2) k_round_tail(const CoopArgs A) 
         const bool sel = open && b <= lim0;
         if (pass) {
           const int64_t key = b - lim1;
-          if (sel && key >= A.n_keys) atomicExch(reinterpret_cast<unsigned long long*>(&S->err), 3ull);
+          if (sel && key >= n_keys) atomicExch(reinterpret_cast<unsigned long long*>(&S->err), 3ull);
           A.keys[x] = sel ? static_cast<int32_t>(key) : -1;
         }
         return (open && !sel) ? 1 : 0;
@@ -1043,7 +1077,7 @@ __global__ void __launch_bounds__(kCoopBlock, 2) k_round_tail(const CoopArgs A) 
   // per-block histograms over contiguous chunks, key-major scan, ordered scatter
   const int64_t chunk = (m + nb - 1) / nb;
   const int64_t lo = min(m, static_cast<int64_t>(blockIdx.x) * chunk), hi = min(m, lo + chunk);
-  const int nk = static_cast<int>(A.n_keys);
+  const int nk = static_cast<int>(n_keys);
   for (int k = threadIdx.x; k < nk; k += blockDim.x) s_hist[k] = 0;
   __syncthreads();
   for (int64_t x = lo + threadIdx.x; x < hi; x += blockDim.x) {
@@ -1096,6 +1130,10 @@ __global__ void __launch_bounds__(kCoopBlock, 2) k_round_tail(const CoopArgs A) 
     S->T = Tn_last;
     *A.d_T = Tn_last;
     S->pool_n = stay_n;
+    // algorithmic bytes of the round (see the host's per-round formula)
+    const long long Wd = A.cm.W;
+    S->commit_bytes += T * (37 + 8 * Wd) + K * (33 + 8 * Wd) + static_cast<long long>(n) * 16 + (pool_old + K) * 9 +
+                       Gn * 28;
   }
   STAMP();
 }
@@ -1287,6 +1325,15 @@ void run_explore_device(DevExplore& X, Ctx& c, const DevGraph& G, const ExploreA
     DBuf& scan_st = c.buf("x_coop_scan_status", al((coop_blocks + 2) * 8));
     PUMP_CUDA(cudaMemsetAsync(scan_st.p, 0, (coop_blocks + 2) * 8, st));
   }
+  // Pipelined rounds: with the cooperative path and no round hook, batches of
+  // kBatch rounds are enqueued behind device-side gates (k_round_gate) and the
+  // status is read once per batch; buffers are sized for Tcap tasks per round
+  // and a round that does not fit (or needs the per-kernel path) halts the
+  // batch, after which the host runs that round synchronously.
+  static const int kBatch = std::getenv("PUMP_EXPLORE_BATCH") ? std::max(1, std::atoi(std::getenv("PUMP_EXPLORE_BATCH"))) : 8;
+  bool force_sync = false;
+  int64_t max_T = 0;
+  long long commit_bytes_legacy = 0;
   c.tic();
   for (;;) {
     // loop-top termination (planner.hpp:126-138); h is the status after the
@@ -1301,10 +1348,18 @@ void run_explore_device(DevExplore& X, Ctx& c, const DevGraph& G, const ExploreA
       X.termination = best_goal == __builtin_inf() ? 1 : 0;
       break;
     }
-    const int64_t T = h.T;
-    X.rounds++;
-    X.partial_plans += T;
-    ensure_arena(X, X.n_plans + T + 1, st);
+    const int64_t Th = h.T;
+    max_T = std::max<int64_t>(max_T, Th);
+    const bool pipe = coop_ok && kBatch > 1 && !prm.on_round && !force_sync;
+    force_sync = false;
+    // buffer sizes: this round's T, or a per-round capacity for a batch
+    const int64_t T = pipe ? std::max<int64_t>({Th, 2 * max_T, 4096}) : Th;
+    const int64_t nrounds = pipe ? kBatch : 1;
+    if (!pipe) {
+      X.rounds++;
+      X.partial_plans += Th;
+    }
+    ensure_arena(X, X.n_plans + (pipe ? kBatch * T / 2 : T) + 1, st);
     // candidate buffers
     X.cand_keep.ensure(al(T + 1));
     X.cand_head.ensure(al((T + 1) * 4));
@@ -1323,9 +1378,18 @@ void run_explore_device(DevExplore& X, Ctx& c, const DevGraph& G, const ExploreA
 
     int64_t n_keys_r = 1 << 18;  // see k_select: distinct bucket keys this round
     if (h.min_bucket != LLONG_MAX && h.i + 2 - h.min_bucket <= 512) n_keys_r = std::max<int64_t>(1, h.i + 2 - h.min_bucket);
-    if (coop_ok && T > 0 && n_keys_r <= kCoopKeys) {
+    bool ran_coop = false;
+    if (pipe || (coop_ok && T > 0 && n_keys_r <= kCoopKeys)) {
+     ran_coop = true;
+     const long long rounds0 = h.rounds;  // (pipelined: the status counts the rounds that ran)
+     const int64_t pool_ub = h.pool_n + (pipe ? kBatch * T : T) + 1;
+     for (int64_t rr = 0; rr < nrounds; ++rr) {
       // ---- one cooperative launch for the whole round
-      const int64_t pool_ub = h.pool_n + T + 1;
+      if (pipe) {
+        const GateCaps caps{T, X.cap, pool_ub};
+        k_round_gate<<<1, 1, 0, st>>>(S, caps);
+        ++c.launches;
+      }
       X.task_grp.ensure(al((T + 1) * 4));
       X.task_e.ensure(al((T + 1) * 8));
       X.group.grow(al((pool_ub + 1) * 4), static_cast<size_t>(h.G) * 4, st);
@@ -1384,7 +1448,7 @@ void run_explore_device(DevExplore& X, Ctx& c, const DevGraph& G, const ExploreA
       A.pool_nxt = pool_nxt.as<int32_t>();
       A.keys = keys.as<int32_t>();
       A.stay_pos = stay_pos.as<int64_t>();
-      A.n_keys = n_keys_r;
+      A.n_keys = pipe ? 0 : n_keys_r;  // pipelined: the gate's value in the status
       A.ms_counts = msc.as<int32_t>();
       A.ms_offs = mso.as<int64_t>();
       A.group = X.group.as<int32_t>();
@@ -1394,12 +1458,14 @@ void run_explore_device(DevExplore& X, Ctx& c, const DevGraph& G, const ExploreA
       static const bool dbg_coop = std::getenv("PUMP_DEBUG_COOP") != nullptr;
       DBuf& stamps = c.buf("x_coop_stamps", 64 * 8);
       A.stamps = dbg_coop ? stamps.as<unsigned long long>() : nullptr;
-      k_task_map<<<grid_for(h.G * 32, 256), 256, 0, st>>>(d_G, X.task_off.as<int64_t>(), X.group.as<int32_t>(),
-                                                            X.head.as<int32_t>(), G.row_ptr.as<int64_t>(),
-                                                            X.task_grp.as<int32_t>(), X.task_e.as<int64_t>());
+      const int64_t grid_cap = static_cast<int64_t>(coop_blocks) * 8;
+      k_task_map<<<pipe ? static_cast<unsigned>(std::min<int64_t>(grid_for(pool_ub * 32, 256), grid_cap))
+                        : grid_for(h.G * 32, 256),
+                   256, 0, st>>>(d_G, X.task_off.as<int64_t>(), X.group.as<int32_t>(), X.head.as<int32_t>(),
+                                 G.row_ptr.as<int64_t>(), X.task_grp.as<int32_t>(), X.task_e.as<int64_t>(), S);
       ++c.launches;
       {
-        const unsigned grid = grid_for(T * 32, 256);
+        const unsigned grid = grid_for(T * 32, 256);  // pipelined: T is the per-round task capacity
         KScope ks(st, F_EXPAND);
         dispatch_dw(G.dw, [&]<int DW>() {
           switch (ch) {
@@ -1430,13 +1496,15 @@ void run_explore_device(DevExplore& X, Ctx& c, const DevGraph& G, const ExploreA
       swap_buf(X.mem_off, off2);  // new offsets become current
       X.mem_flip = !X.mem_flip;
       X.pool_flip = !X.pool_flip;
+     }
+     (void)rounds0;
     } else {
       if (T > 0) {
         X.task_grp.ensure(al((T + 1) * 4));
         X.task_e.ensure(al((T + 1) * 8));
         k_task_map<<<grid_for(h.G * 32, 256), 256, 0, st>>>(d_G, X.task_off.as<int64_t>(), X.group.as<int32_t>(),
                                                               X.head.as<int32_t>(), G.row_ptr.as<int64_t>(),
-                                                              X.task_grp.as<int32_t>(), X.task_e.as<int64_t>());
+                                                              X.task_grp.as<int32_t>(), X.task_e.as<int64_t>(), S);
         ++c.launches;
         ExpandArgs ea{X.group.as<int32_t>(), X.task_off.as<int64_t>(), X.task_grp.as<int32_t>(), X.task_e.as<int64_t>(), d_G, d_T,
                       G.row_ptr.as<int64_t>(),
@@ -1562,17 +1630,35 @@ void run_explore_device(DevExplore& X, Ctx& c, const DevGraph& G, const ExploreA
     h = *X.status_h;
     X.n_plans = h.n_plans;
     if (h.err) throw std::runtime_error("explore: device error " + std::to_string(h.err));
-    {
+    if (pipe) {
+      // rounds that did not run left the buffers as they were: undo their flips
+      const long long ran = h.rounds - hp.rounds;
+      for (long long q = ran; q < nrounds; ++q) {
+        swap_buf(X.mem_off, off2);
+        X.mem_flip = !X.mem_flip;
+        X.pool_flip = !X.pool_flip;
+      }
+      X.rounds += static_cast<int>(ran);
+      X.partial_plans += h.partial_plans - hp.partial_plans;
+      if (h.halt) {
+        if (h.halt == 2) force_sync = true;  // the next round runs synchronously
+        h.halt = 0;
+        const long long zero = 0;
+        c.h2d(&S->halt, &zero, 8);
+      }
+    }
+    if (!ran_coop) {
       // algorithmic bytes of the round after expand (SURVEY §8d K_merge/K_dom/
       // K_bucket): candidate records read and ranked, kept plans written to the
       // arena, node sizes, the pool scanned, the new group read
       const int64_t Tr = hp.T, Kr = h.K;
-      kprof_work(F_COMMIT, Tr * (37 + 8 * W) + Kr * (33 + 8 * W) + static_cast<int64_t>(n) * 16 +
-                               (hp.pool_n + Kr) * 9 + h.G * 28);
+      commit_bytes_legacy += Tr * (37 + 8 * W) + Kr * (33 + 8 * W) + static_cast<int64_t>(n) * 16 +
+                             (hp.pool_n + Kr) * 9 + h.G * 28;
     }
     if (prm.on_round) prm.on_round(h);
   }
   X.kernel_ms = c.toc();
+  kprof_work(F_COMMIT, commit_bytes_legacy + h.commit_bytes);  // (the cooperative rounds count on the device)
   kprof_work(F_EXPAND, h.hs_tests * N);
   X.hs_tests = h.hs_tests;
   X.n_plans = h.n_plans;
