@@ -74,6 +74,27 @@ __device__ __forceinline__ bool lb_head_clears(const PairLb& p, const LbGrid& L)
   return L.c3[kLbK] * qm * (1.0 - 1e-12) >= L.thr;
 }
 
+// Global bound, tried when the root interval does not clear.  On (0, thr]
+// q(tau) >= q* = min over [0, thr] of the quadratic (less the rounding margin
+// of interval_clears), so c(tau) >= g(tau) = tau + 12 q* / tau^3 + D / tau.
+// g is convex on tau > 0 with its minimum at tau*^2 = (D + sqrt(D^2 + 144 q*)) / 2
+// (g' = 1 - 36 q* / tau^4 - D / tau^2); g at the computed tau* exceeds min g by
+// O(eps^2) and is evaluated to a few ulps, so g(tau*) (1 - 1e-12) is a lower
+// bound of c on (0, thr]: at or above thr the pair is rejected (as by a cover).
+__device__ __forceinline__ bool lb_global_clears(const PairLb& p, double thr) {
+  const double q0 = p.A, q1 = p.A - 2.0 * p.B * thr + p.C * thr * thr;
+  double qm = q0 < q1 ? q0 : q1;
+  if (p.ts > 0 && p.ts < thr) qm = p.A - p.B * p.ts;
+  const double ab = p.B < 0 ? -p.B : p.B;
+  qm -= 1e-12 * (p.A + 2.0 * ab * thr + p.C * thr * thr);
+  if (!(qm > 0)) return false;
+  const double a = 12.0 * qm;
+  const double t2 = 0.5 * (p.D + sqrt(p.D * p.D + 12.0 * a));
+  const double t = sqrt(t2);
+  const double g = t + a / (t2 * t) + p.D / t;
+  return g * (1.0 - 1e-12) >= thr;
+}
+
 __device__ __forceinline__ bool lb_rejects(const PairLb& p, const LbGrid& L) {
   // head interval (0, t_K]: c >= 12 min q / t_K^3
   const double tk = L.t[kLbK];
@@ -412,7 +433,7 @@ __global__ void __launch_bounds__(kRowBlock) k_pair_filter_grid(
     GraphArgs g, const LbGrid lb, const CellGrid G, int cap, int row0, int refill,
     const int32_t* __restrict__ ccnt, const int64_t* __restrict__ cstart,
     const unsigned long long* __restrict__ cbox, const int32_t* __restrict__ sidx, const double* __restrict__ spos,
-    const double* __restrict__ svel, int32_t* __restrict__ row_cnt, int32_t* __restrict__ su) {
+    const double* __restrict__ svel, int32_t* __restrict__ row_cnt, int32_t* __restrict__ su, int use_global) {
   __shared__ LbGrid sl;
   __shared__ int cl_start[kCellMaxList];
   __shared__ int cl_pref[kCellMaxList + 1];
@@ -564,6 +585,8 @@ __global__ void __launch_bounds__(kRowBlock) k_pair_filter_grid(
       } else if (s == 0) {
         atomicOr(&bits[u >> 5], 1u << (u & 31));
         active = false;
+      } else if (s == 4 && use_global && lb_global_clears(p, sl.thr)) {
+        active = false;  // the root did not clear, the global bound does: rejected
       } else {
         --s;
       }
@@ -1075,7 +1098,7 @@ void build_graph_device(DevGraph& G, Ctx& c, int n, int dw, const double* h_pos,
               ga, lbg, cg, cap, row_lo, refill, c.scratch["g_ccnt"].as<int32_t>(), c.scratch["g_cstart"].as<int64_t>(),
               c.scratch["g_cbox"].as<unsigned long long>(), c.scratch["g_sidx"].as<int32_t>(),
               c.scratch["g_spos"].as<double>(), c.scratch["g_svel"].as<double>(), rcnt.as<int32_t>(),
-              suB.as<int32_t>());
+              suB.as<int32_t>(), getenv("PUMP_PF_NOGLOBAL") ? 0 : 1);
         } else if (row_hi > row_lo && legacy)
           k_pair_filter<DW><<<row_hi - row_lo, kRowBlock, 0, st>>>(ga, lbg, cap, row_lo, rcnt.as<int32_t>(),
                                                                    suB.as<int32_t>());
