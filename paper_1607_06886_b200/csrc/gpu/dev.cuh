@@ -99,7 +99,7 @@ __host__ __device__ __forceinline__ int __builtin_ctzll_hd(uint64_t x) {
 
 // Reciprocal to within a few ulps (not correctly rounded): MUFU seed + two
 // Newton steps.  Only for values that carry their own error margin (the lazy
-// cubic's 1e-11 S, the filter multipliers' rounding-down factor), never for
+// cubic's 1e-12 S, the filter multipliers' rounding-down factor), never for
 // a value the reference computes.  x > 0, finite, normal.
 __host__ __device__ __forceinline__ double rcp_approx(double x) {
 #if defined(__CUDA_ARCH__)
@@ -539,6 +539,7 @@ __host__ __device__ __forceinline__ bool interval_clears(const PairLb& p, double
 // when the cost's lower bound on the golden-section bracket [lo, hi] clears
 // reject_thr on all 16 sub-intervals: the returned tau lies in that bracket,
 // so its cost would be >= r_n and graph.hpp:72 would drop the pair anyway.
+constexpr double kLazyErr = 1e-12;
 template <int DW, bool kReject = false>
 __host__ __device__ inline bool connect_dev(const double* ap, const double* av, const double* bp, const double* bv, double tau_max,
                             double ratio, double& tau_out, double& cost_out, double reject_thr = 0.0) {
@@ -555,12 +556,16 @@ __host__ __device__ inline bool connect_dev(const double* ap, const double* av, 
   //   c = tau + 12 A u^3 + (-24 B - 12 E) u^2 + (12 C + 12 F + 4 D) u
   // (A = |P|^2, B = P.V, C = |V|^2, E = P.dv, F = V.dv, D = |dv|^2).  Its
   // value, computed without divisions, differs from the reference's
-  // evaluation (steer_cost) by far less than err = 1e-11 * S, S the sum of the
-  // absolute values of every constituent term (both evaluations err by a few
-  // ulps of S).  A comparison the reference makes is decided from the cubic
-  // when the two intervals [c - err, c + err] are disjoint, and from
-  // steer_cost otherwise, so every decision (scan argmin, golden-section
-  // branch) and every returned value is the reference's.
+  // evaluation (steer_cost) by far less than err = 1e-12 * S, S the sum of the
+  // absolute values of every constituent term: the reference's evaluation errs
+  // by <~3e-15 S (dp's rounding is bounded by the |P|, |V| tau terms of S; ~10
+  // roundings of partial sums <= S), the cubic by as much plus its u error
+  // (rcp_approx: a few ulps; the scan's product chain: <~1.5e-14, i.e.
+  // <~5e-14 S through u^3), so the margin is >= 15x.  A comparison the
+  // reference makes is decided from the cubic when the two intervals
+  // [c - err, c + err] are disjoint, and from steer_cost otherwise, so every
+  // decision (scan argmin, golden-section branch) and every returned value is
+  // the reference's.
   double cA = 0, cB = 0, cC = 0, cE = 0, cF = 0, cD = 0, aB = 0, aE = 0, aF = 0;
 #pragma unroll
   for (int k = 0; k < DW; ++k) {
@@ -586,7 +591,7 @@ __host__ __device__ inline bool connect_dev(const double* ap, const double* av, 
     Lazy z;
     z.tau = t;
     z.approx = t + ((k3 * u + k2) * u + k1) * u;
-    z.err = 1e-11 * (t + ((s3 * u + s2) * u + s1) * u);
+    z.err = kLazyErr * (t + ((s3 * u + s2) * u + s1) * u);
     z.known = false;
     return z;
   };

@@ -78,6 +78,39 @@ def test_connect_and_motion_collides_match_oracle(oracle_lib, dw):
     assert n_hit > 20 and n_free > 20
 
 
+def test_connect_lazy_decisions_stress(oracle_lib):
+    """connect()'s lazily decided comparisons (cubic in 1/tau within kLazyErr S,
+    steer_cost only when ambiguous) against the literal scan + golden section
+    on 20000 pairs across scales: flat cost curves, near-ties, cancellation."""
+    rng = np.random.default_rng(11)
+    for trial in range(20000):
+        dw = 2 + trial % 2
+        scale = 10.0 ** rng.uniform(-3, 3)
+        ap = rng.uniform(-1, 1, size=dw) * scale
+        av = rng.normal(size=dw) * 10.0 ** rng.uniform(-3, 1)
+        kind = trial % 6
+        if kind == 0:
+            bp, bv = ap + rng.normal(size=dw) * scale, rng.normal(size=dw)
+        elif kind == 1:  # nearly identical states
+            bp, bv = ap + rng.normal(size=dw) * scale * 1e-7, av + rng.normal(size=dw) * 1e-7
+        elif kind == 2:  # the straight line the start velocity follows
+            bp, bv = ap + av * rng.uniform(0.01, 10.0), av.copy()
+        elif kind == 3:  # offsets far below the positions' magnitude (cancellation in dp)
+            bp = ap + rng.normal(size=dw) * 1e-9 * scale
+            bv = rng.normal(size=dw) * 1e-3
+        elif kind == 4:
+            bp, bv = ap + rng.normal(size=dw) * scale, np.zeros(dw)
+            av = np.zeros(dw)
+        else:
+            bp, bv = ap + rng.normal(size=dw), -av
+        tau_max = 10.0 ** rng.uniform(-1, 2)
+        g = api.connect(ap, av, bp, bv, tau_max)
+        e = oracle_lib.connect(ap, av, bp, bv, tau_max)
+        assert g["ok"] == e["ok"], trial
+        assert np.float64(g["tau"]).tobytes() == np.float64(e["tau"]).tobytes(), trial
+        assert np.float64(g["cost"]).tobytes() == np.float64(e["cost"]).tobytes(), trial
+
+
 @pytest.mark.parametrize("name", ["minimal", "three_obstacle", "quad3d_three_obstacle"])
 def test_scenario_nodes_match_oracle(oracle_lib, name):
     """The node set run_pump plans over (pump.hpp:184-189, sample.hpp:56-89)."""
