@@ -63,7 +63,7 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+                 "-lms", "20"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.thread = threading.Thread(target=self._read, daemon=True)
             self.thread.start()
         except FileNotFoundError:
@@ -166,7 +166,7 @@ def run_reference(args, world, rank):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=30)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="quad3d_indoor")
@@ -404,6 +404,18 @@ def main():
                "sample": "one full solve of the same scenario (oracle restatement, workers = all host threads)",
                "identical_result": bool(same)}
 
+    # per-kernel roofline table from the committed ncu --set full captures
+    # (tools/ncu_kernels.py; static evidence, not measured in this run)
+    ncu_tab = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "r1_ncu_kernels.json")) as f:
+            nk = json.load(f)
+        ncu_tab = {"source": "profiles/r1_ncu_kernels.json (ncu --set full, one launch each; not this run)",
+                   "kernels": [{k: d.get(k) for k in ("kernel", "dur_us", "bound", "frac", "fp64_pipe_pct",
+                                                       "issue_pct", "dram_gbs")} for d in nk["kernels"]]}
+    except Exception:
+        ncu_tab = None
+
     pp_s = res["partial_plans"] / (res["explore_seconds"]) if res["explore_seconds"] > 0 else None
     mc_rs = res["mc_rollouts"] / (res["mc_ms"] * 1e-3) if res["mc_ms"] > 0 else None
     line = {
@@ -425,7 +437,8 @@ def main():
                            "note": "run_pump with a prebuilt graph (graph built once from the scenario's nodes)"},
         "gpu_launches": int(launches // args.steps), "gpu_launches_total": int(launches),
         "device_allocs_timed": int(io1[3] - io0[3] + e_io1[3] - e_io0[3]),
-        "clocks": clk, "roofline": roof, "rooflines": rooflines, "cpu_baseline": cpu, "kernels": kernels,
+        "clocks": clk, "roofline": roof, "rooflines": rooflines, "ncu_kernels": ncu_tab, "cpu_baseline": cpu,
+        "kernels": kernels,
         "solve": {"success": res["success"], "cost": res["cost"], "certified_cp": res["certified_cp"],
                   "partial_plans": res["partial_plans"], "n_edges": res["n_edges"], "n_plans": res["n_plans"],
                   "build_graph_ms": round(1e3 * res["build_graph_seconds"], 3),
