@@ -675,31 +675,32 @@ __global__ void __launch_bounds__(kMcBlock) k_mctab_dense(const LoopP<D, DW> L, 
 // Certify against the table.  A rollout's verdict is the OR of independent
 // per-step tests (point y_t, segment y_{t-1} -> y_t; the reference stops at
 // the first hit, which changes the work, not the verdict), so the steps are
-// spread over the grid: thread = (trajectory, rollout, chunk of kMcChunk
+// spread over the grid: thread = (trajectory, rollout, span of kMcSpan
 // steps), y_t = ynom_t + dy_t (the addition k_mc performs), the collision
 // tests of k_mc_sep (bounds, bbox-culled obstacles, eps_cc-subdivided
 // segment).  A hit sets flag[j][i]; k_mc_count sums the flags.
-constexpr int kMcChunk = 8;
-template <int DW>
+constexpr int kMcChunk = 8;   // steps whose table rows a thread loads up front
+template <int DW, int kMcSub>  // kMcSub sub-chunks per block: a block spans kMcSpan steps
 __global__ void __launch_bounds__(kMcBlock) k_mc_tab(WorldD w, const int64_t* __restrict__ traj_off,
                                                      const double* __restrict__ ynom_all, int64_t r0, int64_t r1,
                                                      int64_t tab_r0, int64_t tab_n, const double* __restrict__ dy,
                                                      const unsigned long long* __restrict__ maxdev, double eps_cc,
                                                      uint8_t* __restrict__ flags, const int32_t* __restrict__ live) {
   extern __shared__ double smem[];
+  constexpr int kMcSpan = kMcChunk * kMcSub;
   constexpr int kStepCap = 64;  // block-wide candidate obstacles per step (more: test all)
-  __shared__ uint16_t s_list[kMcChunk + 1][kStepCap];
-  __shared__ int s_nlist[kMcChunk + 1];  // -1: more than kStepCap candidates
-  __shared__ int s_skip[kMcChunk + 1];
+  __shared__ uint16_t s_list[kMcSpan + 1][kStepCap];
+  __shared__ int s_nlist[kMcSpan + 1];  // -1: more than kStepCap candidates
+  __shared__ int s_skip[kMcSpan + 1];
   __shared__ int s_all_skip;
   const int j = blockIdx.y;
   if (live && !live[j]) return;  // trajectory not certified (its nominal collides): flags stay 0
   const int64_t p_begin = traj_off[j];
   const int n_pts = static_cast<int>(traj_off[j + 1] - p_begin);
   const int T = n_pts - 1;
-  const int t_lo = blockIdx.z * kMcChunk;
+  const int t_lo = blockIdx.z * kMcSpan;
   if (t_lo > T) return;
-  const int t_hi = min(T, t_lo + kMcChunk - 1);
+  const int t_hi = min(T, t_lo + kMcSpan - 1);
   const int s_lo_t = t_lo > 0 ? t_lo - 1 : 0;  // rows staged: [s_lo_t, t_hi]
   const int rows = t_hi - s_lo_t + 1;
   double* s_y = smem;
@@ -730,7 +731,7 @@ __global__ void __launch_bounds__(kMcBlock) k_mc_tab(WorldD w, const int64_t* __
   // any rollout and is skipped, loads included.
   {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    for (int r = warp; r <= kMcChunk; r += kMcBlock / 32) {
+    for (int r = warp; r <= kMcSpan; r += kMcBlock / 32) {
       const int t = s_lo_t + r;
       int skip = 1, nl = 0;
       if (t >= t_lo && t <= t_hi) {
@@ -782,27 +783,32 @@ __global__ void __launch_bounds__(kMcBlock) k_mc_tab(WorldD w, const int64_t* __
   if (i >= r1) return;
   const double* d = dy + (i - tab_r0) * DW;
   const int64_t stride = tab_n * DW;
-  double dv[kMcChunk + 1][DW];  // issue every needed load of the chunk up front
+  bool hit = false;
+  // the block's span in sub-chunks of kMcChunk steps; row rb of a sub-chunk
+  // seeds prev (it was the previous sub-chunk's last step)
+  for (int rb = 0; rb < kMcSpan && s_lo_t + rb <= t_hi && !hit; rb += kMcChunk) {
+  double dv[kMcChunk + 1][DW];  // issue every needed load of the sub-chunk up front
 #pragma unroll
   for (int r = 0; r <= kMcChunk; ++r) {
-    const bool need = s_lo_t + r <= t_hi && (!s_skip[r] || (r < kMcChunk && !s_skip[r + 1]));
+    const int rr = rb + r;
+    const bool need = s_lo_t + rr <= t_hi && (!s_skip[rr] || (r < kMcChunk && !s_skip[rr + 1]));
     if (need) {
 #pragma unroll
-      for (int k = 0; k < DW; ++k) dv[r][k] = d[static_cast<int64_t>(s_lo_t + r) * stride + k];
+      for (int k = 0; k < DW; ++k) dv[r][k] = d[static_cast<int64_t>(s_lo_t + rr) * stride + k];
     }
   }
-  bool hit = false;
 #pragma unroll
   for (int r = 0; r <= kMcChunk; ++r) {
-    const int t = s_lo_t + r;
-    if (t < t_lo || t > t_hi || hit || s_skip[r]) continue;  // row 0 of a later chunk only seeds prev
+    const int rr = rb + r;
+    const int t = s_lo_t + rr;
+    if (t < t_lo || t > t_hi || hit || s_skip[rr] || (r == 0 && rb > 0)) continue;  // row 0 only seeds prev
     double prev[DW];
     const int rp = t > 0 ? r - 1 : r;  // t = 0: the step's box is the point itself
 #pragma unroll
-    for (int k = 0; k < DW; ++k) prev[k] = s_y[rp * DW + k] + dv[rp][k];
+    for (int k = 0; k < DW; ++k) prev[k] = s_y[(rb + rp) * DW + k] + dv[rp][k];
     double y[DW];
 #pragma unroll
-    for (int k = 0; k < DW; ++k) y[k] = s_y[r * DW + k] + dv[r][k];
+    for (int k = 0; k < DW; ++k) y[k] = s_y[rr * DW + k] + dv[r][k];
     bool inb = true;
 #pragma unroll
     for (int a = 0; a < DW; ++a) inb = inb && !(y[a] < w.blo[a] || y[a] > w.bhi[a]);
@@ -816,11 +822,11 @@ __global__ void __launch_bounds__(kMcBlock) k_mc_tab(WorldD w, const int64_t* __
       bl[a] = prev[a] < y[a] ? prev[a] : y[a];
       bh[a] = prev[a] < y[a] ? y[a] : prev[a];
     }
-    const int nl = s_nlist[r];
-    // this rollout's culling within the step's list (bit q <-> s_list[r][q])
+    const int nl = s_nlist[rr];
+    // this rollout's culling within the step's list (bit q <-> s_list[rr][q])
     uint64_t cand = 0;
     for (int q = 0; q < nl; ++q) {
-      const int o = s_list[r][q];
+      const int o = s_list[rr][q];
       bool sep = false;
 #pragma unroll
       for (int a = 0; a < DW; ++a) sep = sep || (bh[a] < s_lo[o * DW + a]) || (bl[a] > s_hi[o * DW + a]);
@@ -828,7 +834,7 @@ __global__ void __launch_bounds__(kMcBlock) k_mc_tab(WorldD w, const int64_t* __
     }
     if (nl >= 0) {
       for (uint64_t m = cand; m && !hit; m &= m - 1) {
-        const int o = s_list[r][__ffsll(static_cast<long long>(m)) - 1];
+        const int o = s_list[rr][__ffsll(static_cast<long long>(m)) - 1];
         if (box_contains<DW>(s_clo + o * DW, s_chi + o * DW, y)) hit = true;
       }
     } else {
@@ -868,7 +874,7 @@ __global__ void __launch_bounds__(kMcBlock) k_mc_tab(WorldD w, const int64_t* __
         }
         if (nl >= 0) {
           for (uint64_t m = cand; m; m &= m - 1) {
-            const int o = s_list[r][__ffsll(static_cast<long long>(m)) - 1];
+            const int o = s_list[rr][__ffsll(static_cast<long long>(m)) - 1];
             if (box_contains<DW>(s_clo + o * DW, s_chi + o * DW, p1) ||
                 segment_hits<DW>(p0, p1, s_clo + o * DW, s_chi + o * DW)) {
               hit = true;
@@ -885,6 +891,7 @@ __global__ void __launch_bounds__(kMcBlock) k_mc_tab(WorldD w, const int64_t* __
         for (int a = 0; a < DW; ++a) p0[a] = p1[a];
       }
     }
+  }
   }
   if (hit) flags[static_cast<int64_t>(j) * (r1 - r0) + (i - r0)] = 1;
 }
@@ -1058,15 +1065,23 @@ void launch_mc(const HostLoop& HL, const DevWorld& w, int n_traj, const int64_t*
     table->flags.ensure(static_cast<size_t>(n) * n_traj + 256);
     PUMP_CUDA(cudaMemsetAsync(table->flags.p, 0, static_cast<size_t>(n) * n_traj, st));
     dispatch_dw(HL.dw, [&]<int DW>() {
-      const size_t smem = (static_cast<size_t>(kMcChunk + 1) * DW + 4 * static_cast<size_t>(w.n_obs) * DW) * sizeof(double);
-      if (smem > 48 * 1024)
-        PUMP_CUDA(cudaFuncSetAttribute(k_mc_tab<DW>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-      dim3 grid(grid_for(n, kMcBlock), n_traj, (max_points + kMcChunk - 1) / kMcChunk);
+      static const int sub = std::getenv("PUMP_MC_SUB") ? std::atoi(std::getenv("PUMP_MC_SUB")) : 2;
+      auto go = [&]<int SUB>() {
+        constexpr int span = kMcChunk * SUB;
+        const size_t smem = (static_cast<size_t>(span + 1) * DW + 4 * static_cast<size_t>(w.n_obs) * DW) * sizeof(double);
+        if (smem > 48 * 1024)
+          PUMP_CUDA(cudaFuncSetAttribute(k_mc_tab<DW, SUB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(smem)));
+        dim3 grid(grid_for(n, kMcBlock), n_traj, (max_points + span - 1) / span);
+        k_mc_tab<DW, SUB><<<grid, kMcBlock, smem, st>>>(wd, d_traj_off, d_ynom, r0, r1, table->r0,
+                                                        table->r1 - table->r0, table->dy.as<double>(),
+                                                        table->maxdev.as<unsigned long long>(), eps_cc,
+                                                        table->flags.as<uint8_t>(), d_live);
+      };
       KScope ks(st, F_MC);
-      k_mc_tab<DW><<<grid, kMcBlock, smem, st>>>(wd, d_traj_off, d_ynom, r0, r1, table->r0, table->r1 - table->r0,
-                                                 table->dy.as<double>(),
-                                                 table->maxdev.as<unsigned long long>(), eps_cc,
-                                                 table->flags.as<uint8_t>(), d_live);
+      if (sub == 2) go.template operator()<2>();
+      else if (sub == 4) go.template operator()<4>();
+      else go.template operator()<1>();
       k_mc_count<<<dim3(static_cast<unsigned>(std::min<int64_t>((n + 255) / 256, 64)), n_traj), 256, 0, st>>>(
           table->flags.as<uint8_t>(), n, d_traj_off, d_hits, d_steps, d_live);
     });
