@@ -780,7 +780,7 @@ __device__ __forceinline__ void grid_sync(GridBar* bar) {
   __syncthreads();
 }
 
-constexpr int kCoopBlock = kExpBlock;  // 256
+constexpr int kCoopBlock = kExpBlock;  // 256 (512 measured no faster: the phases are dependent-latency bound)
 __device__ __forceinline__ int64_t block_sum(int64_t v, int64_t* red) {
   v = warp_sum(v);
   const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
@@ -919,11 +919,19 @@ union DomSmem {  // the warp pass and the block pass of the dom phase run one af
 };
 
 __global__ void __launch_bounds__(kCoopBlock, 2) k_round_tail(const CoopArgs A) {
-  __shared__ DomSmem dsm;
+  // the dom phase's staging and the multisplit's histograms never live at once
+  __shared__ union {
+    DomSmem dom;
+    struct {
+      int hist[kCoopKeys];
+      int64_t run[kCoopKeys];
+    } ms;
+  } csm;
+  DomSmem& dsm = csm.dom;
   DomShared& dsh = dsm.blk;
   DomWarpShared* wsh = dsm.warp;
-  __shared__ int s_hist[kCoopKeys];
-  __shared__ int64_t s_run[kCoopKeys];
+  int* s_hist = csm.ms.hist;
+  int64_t* s_run = csm.ms.run;
   __shared__ int64_t red[kCoopBlock / 32];
   __shared__ int64_t s_pre;
   ExploreStatus* S = A.S;
