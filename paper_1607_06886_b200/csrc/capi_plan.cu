@@ -202,6 +202,7 @@ __global__ void k_smooth_check(WorldD w, int n_probe, int n_wp, const double* __
   if (x >= static_cast<int64_t>(n_probe) * n_wp) return;
   const int64_t pr = x / n_wp;
   const int j = static_cast<int>(x % n_wp);
+  if (free_flag[pr] == 0) return;  // already colliding (or a chained step that does not run)
   bool ok = point_free<DW>(w, y + x * DW);
   if (ok && j + 1 < n_wp) {
     const double h = pt[j + 1] - pt[j];
@@ -220,6 +221,43 @@ __global__ void k_smooth_check(WorldD w, int n_probe, int n_wp, const double* __
     }
   }
   if (!ok) free_flag[pr] = 0;
+}
+
+// The reference's smoothing bisection (pump.hpp:118-141) chained on the
+// stream: step 0 probes s = 1; step k >= 1 decides from step k-1's verdict
+// (free and hits / n_mc <= alpha, the host's expressions) and probes
+// s_k = 0.5 (lo + hi).  After s = 1 certifies, every later step is marked
+// done: its check and MC do nothing.  The host reads the history once and
+// replays the bisection from it.
+struct SmoothChain {
+  double lo, hi;
+  int32_t done, pad;
+  double s[12];
+  unsigned long long hits[12];
+  int32_t live[12];  // 1 until the nominal check fails (0: no MC; also when done)
+  unsigned long long steps;
+};
+__global__ void k_smooth_decide(SmoothChain* c, int k, int64_t n_mc, double alpha) {
+  if (k == 0) {
+    c->done = 0;
+    c->s[0] = 1.0;
+    c->steps = 0;
+  } else if (!c->done) {
+    const int q = k - 1;
+    const bool cert = c->live[q] != 0 && static_cast<double>(c->hits[q]) / n_mc <= alpha;
+    if (k == 1) {
+      if (cert) c->done = 1;
+      c->lo = 0;
+      c->hi = 1;
+    } else if (cert) {
+      c->lo = c->s[q];
+    } else {
+      c->hi = c->s[q];
+    }
+    c->s[k] = 0.5 * (c->lo + c->hi);
+  }
+  c->live[k] = c->done ? 0 : 1;
+  c->hits[k] = 0;
 }
 
 // ------------------------------------------------------------ path kernels
@@ -1137,7 +1175,7 @@ static void run_pump_device(Ctx& c, const pumpb::Scenario& s, const DevGraph* pr
     // batch (blend + nominal check + MC in one round trip).
     // PUMP_SMOOTH_SCHEDULE="3,3,4" overrides.
     std::vector<int> schedule(10, 1);
-    if (!host_probes) schedule = {2, 2, 2, 2, 2};  // device probes: 3-candidate subtrees, 6 round trips
+    if (!host_probes) schedule = {2, 2, 2, 2, 2};  // PUMP_SMOOTH_SCHEDULE with device probes: speculative subtrees
     if (const char* e = std::getenv("PUMP_SMOOTH_SCHEDULE")) {
       schedule.clear();
       for (const char* q = e; *q;) {
@@ -1146,6 +1184,85 @@ static void run_pump_device(Ctx& c, const pumpb::Scenario& s, const DevGraph* pr
         if (*q == ',') ++q;
       }
     }
+    static const bool spec = std::getenv("PUMP_SMOOTH_SCHEDULE") != nullptr;
+    if (!host_probes && !spec) {
+      // all 11 probes enqueued at once, each deciding on the device from the
+      // previous verdict; one synchronisation for the whole bisection
+      const int64_t items = n_wp;
+      DBuf& d_y = c.buf("sm_y", items * dw * 8 + 256);
+      DBuf& d_yv = c.buf("sm_yv", items * dw * 8 + 256);
+      DBuf& d_ch = c.buf("sm_chain", sizeof(SmoothChain) + 256);
+      DBuf& d_off = c.buf("sm_choff", 256);
+      const int64_t off2[2] = {0, static_cast<int64_t>(n_wp)};
+      c.h2d(d_off.p, off2, 16);
+      SmoothChain* ch = d_ch.as<SmoothChain>();
+      WorldD wd;
+      wd.n_obs = dwld.n_obs;
+      wd.lo = dwld.d_lo;
+      wd.hi = dwld.d_hi;
+      for (int k = 0; k < 6; ++k) {
+        wd.blo[k] = dwld.blo[k];
+        wd.bhi[k] = dwld.bhi[k];
+      }
+      int64_t r0 = 0, r1 = s.mc_samples;
+      shard_range(s.mc_samples, c.rank, c.world, &r0, &r1);
+      if (c.mc_join_pending) {
+        PUMP_CUDA(cudaStreamWaitEvent(c.stream, c.join, 0));
+        c.mc_join_pending = false;
+      }
+      c.tic();
+      for (int k = 0; k <= 10; ++k) {
+        k_smooth_decide<<<1, 1, 0, c.stream>>>(ch, k, s.mc_samples, s.alpha);
+        dispatch_dw(dw, [&]<int DW>() {
+          HMotion o = opt;
+          k_smooth_blend<DW><<<grid_for(items, 128), 128, 0, c.stream>>>(
+              1, n_wp, &ch->s[k], c.scratch["sm_plan"].as<double>(), c.scratch["sm_plan"].as<double>() + n_wp,
+              c.scratch["sm_plan"].as<double>() + n_wp * (1 + dw), as_motion<DW>(o), d_y.as<double>(),
+              d_yv.as<double>());
+          k_smooth_check<DW><<<grid_for(items, 128), 128, 0, c.stream>>>(
+              wd, 1, n_wp, c.scratch["sm_plan"].as<double>(), d_y.as<double>(), d_yv.as<double>(), eps_cc,
+              &ch->live[k]);
+        });
+        c.launches += 3;
+        launch_mc(L, dwld, 1, d_off.as<int64_t>(), d_y.as<double>(), n_wp, r0, r1, s.seeds.mc, eps_cc,
+                  &ch->hits[k], c.stream, &c.launches, &ch->steps, &c.mc_table, &ch->live[k]);
+        allreduce_sum_i64(c, reinterpret_cast<int64_t*>(&ch->hits[k]), 1);
+        PUMP_CUDA(cudaGetLastError());
+      }
+      SmoothChain hc{};
+      c.d2h(&hc, ch, sizeof(SmoothChain));
+      R.s.mc_ms += c.toc();
+      c.sync();
+      kprof_work(F_MC, static_cast<int64_t>(hc.steps));
+      c.mc_rollout_steps += static_cast<int64_t>(hc.steps);
+      // replay (pump.hpp:118-141) from the history
+      auto record = [&](int k) {
+        Probe p;
+        p.free = hc.live[k] != 0;
+        if (p.free) {
+          p.mc = static_cast<double>(hc.hits[k]) / s.mc_samples;
+          R.s.mc_rollouts += r1 - r0;
+        }
+        probes.emplace(hc.s[k], std::move(p));
+      };
+      record(0);
+      if (certified(1.0)) {
+        accept(1.0);
+      } else {
+        double lo = 0, hi = 1;
+        for (int k = 1; k <= 10; ++k) {
+          const double mid = 0.5 * (lo + hi);
+          if (hc.s[k] != mid) throw std::runtime_error("smoothing: device bisection diverged from the host replay");
+          record(k);
+          if (certified(mid)) {
+            accept(mid);
+            lo = mid;
+          } else {
+            hi = mid;
+          }
+        }
+      }
+    } else {
     run_probes({1.0});
     if (certified(1.0)) {
       accept(1.0);
@@ -1166,6 +1283,7 @@ static void run_pump_device(Ctx& c, const pumpb::Scenario& s, const DevGraph* pr
           }
         }
       }
+    }
     }
   }
   mark("smoothing");
