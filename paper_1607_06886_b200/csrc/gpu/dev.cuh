@@ -842,14 +842,15 @@ __device__ __forceinline__ int convex_region_fused(const WorldD& ws, const doubl
     bool any = false;
     int nb = -1;
     double nsq = __builtin_inf();
-    for (int o = 0; o < ws.n_obs; ++o) {
-      if ((pruned >> o) & 1u) continue;
+    const double* cp[DW];  // the minimizing corner's coordinate array per axis
+#pragma unroll
+    for (int k = 0; k < DW; ++k) cp[k] = (d[k] >= 0 ? ws.lo : ws.hi) + k;
+    const uint32_t all = ws.n_obs >= 32 ? ~0u : ((1u << ws.n_obs) - 1u);
+    for (uint32_t rest = all & ~pruned; rest; rest &= rest - 1) {  // unpruned boxes, ascending
+      const int o = __builtin_ctzll_hd(rest);
       double dot = 0;
 #pragma unroll
-      for (int k = 0; k < DW; ++k) {
-        const double c = d[k] >= 0 ? ws.lo[o * DW + k] : ws.hi[o * DW + k];
-        dot += d[k] * (c - y[k]);
-      }
+      for (int k = 0; k < DW; ++k) dot += d[k] * (cp[k][o * DW] - y[k]);
       if (!(dot < lim)) {
         pruned |= 1u << o;
         any = true;
