@@ -458,7 +458,7 @@ __host__ __device__ inline bool motion_collides(const MotionD<DW>& m, const Worl
       return !sep;
     });
   };
-  double st0[64], st1[64];
+  double st1[64];  // right siblings' ends (their starts are implied, see the pop)
   int sp = 0;
   double t0 = 0.0, t1 = m.tau;
   while (true) {
@@ -473,9 +473,12 @@ __host__ __device__ inline bool motion_collides(const MotionD<DW>& m, const Worl
     if (span_done) {
       if (sp == 0) return false;
       --sp;
-      t0 = st0[sp];
+      t0 = t1;
       t1 = st1[sp];
-      motion_pos<DW>(m, t0, p0);
+      // depth-first, left to right: the popped span starts where the span just
+      // finished ended (t0 == the old t1), so p(t0) is the old p1, bit for bit
+#pragma unroll
+      for (int k = 0; k < DW; ++k) p0[k] = p1[k];
       motion_pos<DW>(m, t1, p1);
       continue;
     }
@@ -484,7 +487,6 @@ __host__ __device__ inline bool motion_collides(const MotionD<DW>& m, const Worl
     motion_pos<DW>(m, tm, pm);
     if (!free_pt(pm)) return true;
     if (sp >= 64) return true;  // unreachable: depth is bounded by t1 - t0 >= 1e-9
-    st0[sp] = tm;
     st1[sp] = t1;
     ++sp;
     t1 = tm;
