@@ -21,6 +21,7 @@
 #include <unsupported/Eigen/MatrixFunctions>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdint>
 #include <cstdlib>
@@ -1347,6 +1348,175 @@ inline std::string pareto_csv(const PumpResult& r) {  // report.hpp:113-120
     json row = {cost, cp};
     out += row[0].dump() + "," + row[1].dump() + "\n";
   }
+  return out;
+}
+
+// ============================================================ compare.hpp
+// The Fig. 4 estimator study (compare.hpp:38-96 with the estimators of
+// cp.hpp:51-169).  The sampling estimators run on the GPU through the calls
+// above (mc_certify, presample_bank, hsmc_extend); the analytical ones are a
+// handful of 12x12 products per waypoint and stay on the host, written with
+// the same (Eigen-compatible) products and summation order as the reference.
+inline double gauss_tail(double x) { return 0.5 * std::erfc(x / std::sqrt(2.0)); }  // P(N(0,1) > x)
+
+namespace detail {
+// half-spaces of a region without repeats: a later (a, b) equal to an earlier
+// one (b equal, a equal componentwise) is skipped (cp.hpp:56-70)
+inline std::vector<const HalfSpace*> distinct_halfspaces(const ConvexRegion& region) {
+  std::vector<const HalfSpace*> kept;
+  for (const HalfSpace& h : region.halfspaces) {
+    const bool seen = std::any_of(kept.begin(), kept.end(), [&](const HalfSpace* g) {
+      return g->b == h.b && g->a.size() == h.a.size() && (g->a - h.a).cwiseAbs().maxCoeff() == 0;
+    });
+    if (!seen) kept.push_back(&h);
+  }
+  return kept;
+}
+}  // namespace detail
+
+// union bound over the region's half-spaces with exact Gaussian marginals (cp.hpp:75-91)
+inline double pointwise_cp(const MatrixXd& cov, const ConvexRegion& region) {
+  double sum = 0;
+  for (const HalfSpace* h : detail::distinct_halfspaces(region)) {
+    const double var = h->a.dot(cov * h->a);
+    sum += var < 1e-30 ? (h->b <= 0 ? 1.0 : 0.0) : gauss_tail(h->b / std::sqrt(var));
+    if (sum >= 1.0) return 1.0;
+  }
+  return sum;
+}
+
+inline double additive_cp(const std::vector<double>& pointwise) {  // cp.hpp:94-98
+  double sum = 0;
+  for (double p : pointwise) sum += p;
+  return std::min(1.0, sum);
+}
+
+inline double multiplicative_cp(const std::vector<double>& pointwise) {  // cp.hpp:101-105
+  double free_all = 1;
+  for (double p : pointwise) free_all *= 1.0 - p;
+  return 1.0 - free_all;
+}
+
+// Gaussian filter over the joint deviation with one-sided moment-matched
+// truncation per half-space (cp.hpp:113-169).
+inline double conditional_multiplicative_cp(const DiscreteModel& dm, const GainSchedule& gs, const MatrixXd& sigma0,
+                                            const std::vector<const ConvexRegion*>& regions) {
+  const ClosedLoopDynamics cl = closed_loop(dm, gs, sigma0);
+  const int d = cl.d, nz = 2 * d;
+  VectorXd mean = VectorXd::Zero(nz);
+  MatrixXd cov = MatrixXd::Zero(nz, nz);
+  cov.topLeftCorner(d, d) = sigma0;
+  const MatrixXd vq = cl.Sv * cl.Sv.transpose(), wq = cl.Sw * cl.Sw.transpose();
+  double survive = 1.0;
+  for (std::size_t t = 0; t < regions.size(); ++t) {
+    if (regions[t]) {
+      double p_step = 0;
+      for (const HalfSpace* h : detail::distinct_halfspaces(*regions[t])) {
+        VectorXd g = VectorXd::Zero(nz);
+        g.head(d) = cl.C.transpose() * h->a;  // the half-space seen from the joint state
+        const double mu = g.dot(mean), var = g.dot(cov * g);
+        if (var < 1e-14) {  // no spread along g: a deterministic test
+          if (mu > h->b) p_step = 1.0;
+          continue;
+        }
+        const double sd = std::sqrt(var), beta = (h->b - mu) / sd;
+        const double tail = gauss_tail(beta), keep = 1.0 - tail;
+        p_step += tail;
+        if (keep < 1e-12) {
+          p_step = 1.0;
+          continue;
+        }
+        const double ratio = std::exp(-0.5 * beta * beta) / std::sqrt(2.0 * 3.14159265358979323846) / keep;
+        const double mu_t = mu - sd * ratio;
+        const double var_t = std::max(var * (1.0 - beta * ratio - ratio * ratio), 0.0);
+        const VectorXd cg = cov * g;
+        mean += ((mu_t - mu) / var) * cg;
+        cov += ((var_t - var) / (var * var)) * (cg * cg.transpose());
+      }
+      survive *= 1.0 - std::min(1.0, p_step);
+      if (survive <= 0) return 1.0;
+    }
+    if (t + 1 < regions.size()) {
+      mean = cl.F * mean;
+      cov = cl.F * cov * cl.F.transpose() + cl.Gv * vq * cl.Gv.transpose() + cl.Gw * wq * cl.Gw.transpose();
+    }
+  }
+  return 1.0 - survive;
+}
+
+// the stored trajectory as a piecewise cubic Hermite of its waypoint states (compare.hpp:13-24)
+inline State trajectory_state_at(const Trajectory& traj, double t) {
+  if (traj.points.empty()) throw std::invalid_argument("trajectory_state_at: empty");
+  if (t <= traj.points.front().t) return traj.points.front().state;
+  if (t >= traj.points.back().t) return traj.points.back().state;
+  std::size_t j = 0;
+  while (j + 2 < traj.points.size() && traj.points[j + 1].t <= t) ++j;
+  const Waypoint& a = traj.points[j];
+  const Waypoint& b = traj.points[j + 1];
+  return fixed_time_connect(a.state, b.state, b.t - a.t).state_at(t - a.t);
+}
+
+struct CpComparisonRow {
+  std::string method;
+  int waypoints = 0;
+  double estimate = 0, mc_reference = 0, seconds = 0;
+};
+
+// compare.hpp:38-96: for each waypoint count, re-discretize the trajectory,
+// then every estimator against the MC reference at that resolution
+inline std::vector<CpComparisonRow> cp_compare(const Scenario& s, const Trajectory& traj,
+                                               const std::vector<int>& waypoint_counts, int particles, int n_mc,
+                                               int workers = 1) {
+  using clk = std::chrono::steady_clock;
+  auto secs = [](clk::time_point a) { return std::chrono::duration<double>(clk::now() - a).count(); };
+  std::vector<CpComparisonRow> rows;
+  const double eps_cc = s.effective_eps_cc();
+  for (int count : waypoint_counts) {
+    if (count < 2) throw std::invalid_argument("cp_compare: need at least 2 waypoints");
+    const int T = count - 1;
+    Scenario sk = s;
+    sk.dt = traj.duration() / T;
+    const ModelBundle mb = build_models(sk);
+    std::vector<VectorXd> y(count);
+    std::vector<ConvexRegion> regions(count);
+    for (int t = 0; t <= T; ++t) {
+      const State st = trajectory_state_at(traj, t * sk.dt);
+      y[t] = st.position;
+      regions[t] = local_convex_region(s.workspace, st.position, st.velocity);
+    }
+    auto t0 = clk::now();
+    const double mc = mc_certify(y, mb.cl, s.workspace, n_mc, s.seeds.mc, eps_cc, workers).value;
+    rows.push_back({"mc", count, mc, mc, secs(t0)});
+
+    const std::vector<MatrixXd> covs = propagate_covariances(mb.dm, mb.gains, s.initial_covariance, T);
+    t0 = clk::now();
+    std::vector<double> pw(count);
+    for (int t = 0; t <= T; ++t) pw[t] = pointwise_cp(covs[t], regions[t]);
+    const double pw_secs = secs(t0);
+    rows.push_back({"additive", count, additive_cp(pw), mc, pw_secs});
+    rows.push_back({"multiplicative", count, multiplicative_cp(pw), mc, pw_secs});
+
+    t0 = clk::now();
+    std::vector<const ConvexRegion*> rp(count);
+    for (int t = 0; t <= T; ++t) rp[t] = &regions[t];
+    const double cm = conditional_multiplicative_cp(mb.dm, mb.gains, s.initial_covariance, rp);
+    rows.push_back({"conditional_multiplicative", count, cm, mc, secs(t0)});
+
+    t0 = clk::now();
+    const DeviationBank bank = presample_bank(mb.dm, mb.gains, s.initial_covariance, T, particles, s.seeds.bank, workers);
+    std::vector<HsmcStep> steps(count);
+    for (int t = 0; t <= T; ++t) steps[t] = {t, &regions[t]};
+    const double hs = hsmc_extend(ParticleMask::full(particles), bank, steps).second;
+    rows.push_back({"hsmc", count, hs, mc, secs(t0)});
+  }
+  return rows;
+}
+
+inline std::string cp_compare_csv(const std::vector<CpComparisonRow>& rows) {  // report.hpp:122-129
+  std::string out = "method,waypoints,estimate,mc_reference,wall_time\n";
+  for (const auto& r : rows)
+    out += r.method + "," + std::to_string(r.waypoints) + "," + json(r.estimate).dump() + "," +
+           json(r.mc_reference).dump() + "," + json(r.seconds).dump() + "\n";
   return out;
 }
 

@@ -9,6 +9,8 @@
 #include <string>
 
 #include "pump/pump.hpp"
+#include "pump/compare.hpp"
+#include "pump/report.hpp"
 #include "pump/rrt.hpp"
 #include "pump/scenario.hpp"
 
@@ -110,6 +112,23 @@ int ref_repeated_rrt(const char* text, int trials, double alpha, int n_mc, int w
       traj_t[i] = r.trajectory.points[i].t;
       for (int k = 0; k < dw; ++k) traj_pos[i * dw + k] = r.trajectory.points[i].state.position[k];
     }
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return 1;
+  }
+}
+
+// cp_compare (compare.hpp:38-96) on a trajectory given as report.hpp JSON
+// text: est[5 i + m] for count i, methods in the reference's row order (mc,
+// additive, multiplicative, conditional_multiplicative, hsmc)
+int ref_cp_compare(const char* text, const char* traj_text, const int* counts, int n_counts, int particles, int n_mc,
+                   int workers, double* est) {
+  try {
+    pump::Scenario s = scn(text);
+    pump::Trajectory traj = pump::parse_trajectory(pump::json::parse(traj_text));
+    auto rows = pump::cp_compare(s, traj, std::vector<int>(counts, counts + n_counts), particles, n_mc, workers);
+    for (std::size_t r = 0; r < rows.size(); ++r) est[r] = rows[r].estimate;
     return 0;
   } catch (const std::exception& e) {
     g_err = e.what();

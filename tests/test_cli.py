@@ -103,3 +103,52 @@ def test_rrt_subcommand_matches_oracle(oracle_lib, tmp_path):
     assert rep["certification_attempts"] == o["certification_attempts"]
     assert rep["cost"] == o["cost"] and rep["certified_cp"] == o["certified_cp"]
     assert (tmp_path / "rrt" / "trajectory.json").exists() == o["success"]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", ["minimal", "three_obstacle"])
+def test_cp_compare_matches_reference(tmp_path, name):
+    """pump cp-compare (compare.hpp:38-96, pump_cli.cpp:77-90): the CSV rows
+    against the reference's own cp_compare compiled in place (oracle/_ref).
+    Analytical estimators (additive, multiplicative, conditional) to 1e-12;
+    the MC and HSMC rows use portable normals here and glibc log/cos in the
+    reference build, so they may differ by a flipped rollout or particle."""
+    import ctypes as C
+
+    import numpy as np
+
+    ref_so = os.path.join(ROOT, "oracle", "_ref", "libpumpref.so")
+    if not os.path.exists(ref_so):
+        pytest.skip("reference not built (needs /root/reference)")
+    sc = os.path.join(SCEN, name + ".json")
+    r = run("plan", "--scenario", sc, "--out", str(tmp_path / "plan"))
+    assert r.returncode == 0, r.stderr
+    traj = tmp_path / "plan" / "trajectory.json"
+    counts, n_mc = [8, 16, 40], 3000
+    r = run("cp-compare", "--scenario", sc, "--trajectory", str(traj), "--waypoints", *map(str, counts),
+            "--mc-samples", str(n_mc), "--out", str(tmp_path / "cmp"))
+    assert r.returncode == 0, r.stderr
+    lines = (tmp_path / "cmp" / "cp_compare.csv").read_text().splitlines()
+    assert lines[0] == "method,waypoints,estimate,mc_reference,wall_time"
+    rows = [ln.split(",") for ln in lines[1:]]
+    methods = ["mc", "additive", "multiplicative", "conditional_multiplicative", "hsmc"]
+    assert [x[0] for x in rows] == methods * len(counts)
+    assert [int(x[1]) for x in rows] == [c for c in counts for _ in methods]
+    L = C.CDLL(ref_so)
+    L.ref_last_error.restype = C.c_char_p
+    text = open(sc).read()
+    particles = json.loads(text)["particles"]
+    est = np.zeros(5 * len(counts))
+    cnt = np.array(counts, dtype=np.int32)
+    rc = L.ref_cp_compare(text.encode(), traj.read_text().encode(), cnt.ctypes.data_as(C.c_void_p), len(counts),
+                          particles, n_mc, 4, est.ctypes.data_as(C.c_void_p))
+    assert rc == 0, L.ref_last_error()
+    for i, x in enumerate(rows):
+        got, exp = float(x[2]), est[i]
+        if x[0] == "mc":
+            assert abs(got - exp) <= 2.0 / n_mc, (x, exp)
+            assert float(x[3]) == got
+        elif x[0] == "hsmc":
+            assert abs(got - exp) <= 2.0 / particles, (x, exp)
+        else:
+            assert abs(got - exp) <= 1e-12 * max(1.0, abs(exp)), (x, exp)

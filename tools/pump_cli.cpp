@@ -2,15 +2,15 @@
 // subcommands, flags and exit codes) over the drop-in API: `plan` runs the
 // whole solve on the GPU, `certify` Monte-Carlo-certifies a trajectory on the
 // GPU, `rrt` runs the repeated-RRT baseline (trials and certification on the
-// GPU).  `cp-compare` is outside the accelerated path and
-// exits with an input error.  Argument parsing is hand-rolled (CLI11
-// is not in the image).
+// GPU), `cp-compare` runs the Fig. 4 estimator study (MC, bank and HSMC on
+// the GPU).  Argument parsing is hand-rolled (CLI11 is not in the image).
 #include <cstdio>
 #include <cstdlib>
 #include <filesystem>
 #include <string>
 #include <vector>
 
+#include "pump/compare.hpp"
 #include "pump/report.hpp"
 
 namespace {
@@ -23,6 +23,8 @@ struct Opts {
   std::string scenario, out = ".", trajectory;
   std::uint64_t seed = 0;
   int workers = 1;
+  std::vector<int> waypoints;  // cp-compare
+  int mc_samples = 0;          // cp-compare
 };
 
 pump::Scenario load(const Opts& o) {
@@ -50,6 +52,19 @@ int run_plan(const Opts& o) {
   std::printf("%s cost=%.6f certified_cp=%.6f alpha=%g partial_plans=%ld\n", r.success ? "success" : "failure",
               r.cost, r.certified_cp, s.alpha, r.partial_plans);
   return r.success ? kExitSuccess : kExitPlannerFailure;
+}
+
+int run_cp_compare(const Opts& o) {  // pump_cli.cpp:77-90
+  pump::Scenario s = load(o);
+  pump::Trajectory traj = pump::load_trajectory(o.trajectory);
+  std::vector<int> waypoints = o.waypoints.empty() ? std::vector<int>{25, 50, 100, 200} : o.waypoints;
+  auto rows = pump::cp_compare(s, traj, waypoints, s.particles, o.mc_samples > 0 ? o.mc_samples : s.mc_samples,
+                               o.workers);
+  pump::detail::write_text(out_path(o, "cp_compare.csv"), pump::cp_compare_csv(rows));
+  for (const auto& r : rows)
+    std::printf("%-28s waypoints=%-4d estimate=%.6f mc=%.6f %.3fs\n", r.method.c_str(), r.waypoints, r.estimate,
+                r.mc_reference, r.seconds);
+  return kExitSuccess;
 }
 
 int run_rrt(const Opts& o) {  // pump_cli.cpp:63-76
@@ -81,8 +96,8 @@ int run_certify(const Opts& o) {
 
 int usage() {
   std::fprintf(stderr,
-               "usage: pump {plan|certify|rrt} --scenario FILE [--seed N] [--workers N] [--out DIR] "
-               "[--trajectory FILE]\n");
+               "usage: pump {plan|certify|rrt|cp-compare} --scenario FILE [--seed N] [--workers N] [--out DIR] "
+               "[--trajectory FILE] [--waypoints N...] [--mc-samples N]\n");
   return kExitInputError;
 }
 
@@ -105,6 +120,11 @@ int main(int argc, char** argv) {
     else if (a == "--out") o.out = next();
     else if (a == "--trajectory") o.trajectory = next();
     else if (a == "--seed") o.seed = std::strtoull(next().c_str(), nullptr, 10);
+    else if (a == "--mc-samples") o.mc_samples = std::atoi(next().c_str());
+    else if (a == "--waypoints") {  // one or more counts (CLI11 vector option)
+      o.waypoints.push_back(std::atoi(next().c_str()));
+      while (i + 1 < argc && std::string(argv[i + 1]).rfind("--", 0) != 0) o.waypoints.push_back(std::atoi(argv[++i]));
+    }
     else if (a == "--workers") {
       o.workers = std::atoi(next().c_str());
       if (o.workers < 1) return usage();
@@ -122,8 +142,8 @@ int main(int argc, char** argv) {
     }
     if (cmd == "rrt") return run_rrt(o);
     if (cmd == "cp-compare") {
-      std::fprintf(stderr, "error: '%s' is outside the accelerated path of this build\n", cmd.c_str());
-      return kExitInputError;
+      if (o.trajectory.empty()) return usage();
+      return run_cp_compare(o);
     }
   } catch (const std::exception& e) {
     std::fprintf(stderr, "error: %s\n", e.what());
