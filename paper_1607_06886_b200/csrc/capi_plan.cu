@@ -224,40 +224,74 @@ __global__ void k_smooth_check(WorldD w, int n_probe, int n_wp, const double* __
 }
 
 // The reference's smoothing bisection (pump.hpp:118-141) chained on the
-// stream: step 0 probes s = 1; step k >= 1 decides from step k-1's verdict
-// (free and hits / n_mc <= alpha, the host's expressions) and probes
-// s_k = 0.5 (lo + hi).  After s = 1 certifies, every later step is marked
-// done: its check and MC do nothing.  The host reads the history once and
-// replays the bisection from it.
+// stream in depth-2 speculative batches: batch 0 probes s = 1 and the first
+// two bisection levels {0.5, 0.75, 0.25}; batch b >= 1 first replays the two
+// steps of the previous batch (certified = free and hits / n_mc <= alpha, the
+// host's expressions) and then probes m = 0.5 (lo + hi) with both of its
+// children 0.5 (m + hi) and 0.5 (lo + m).  Five batches cover the 10 steps.
+// Once s = 1 certifies every later probe is marked done (no check, no MC).
+// The host reads the history once and replays the bisection from it.
+constexpr int kSmoothSlots = 16;  // 4 + 4 batches x 3
 struct SmoothChain {
   double lo, hi;
   int32_t done, pad;
-  double s[12];
-  unsigned long long hits[12];
-  int32_t live[12];  // 1 until the nominal check fails (0: no MC; also when done)
+  double s[kSmoothSlots];
+  unsigned long long hits[kSmoothSlots];
+  int32_t live[kSmoothSlots];  // 1 until the nominal check fails (0: no MC; also when done)
   unsigned long long steps;
 };
-__global__ void k_smooth_decide(SmoothChain* c, int k, int64_t n_mc, double alpha) {
-  if (k == 0) {
+__device__ __forceinline__ bool smooth_cert(const SmoothChain* c, int q, int64_t n_mc, double alpha) {
+  return c->live[q] != 0 && static_cast<double>(c->hits[q]) / n_mc <= alpha;
+}
+// one bisection step on probe slots (m, m_hi child, m_lo child)
+__device__ __forceinline__ void smooth_two_steps(SmoothChain* c, int q, int64_t n_mc, double alpha) {
+  const bool cm = smooth_cert(c, q, n_mc, alpha);
+  if (cm)
+    c->lo = c->s[q];
+  else
+    c->hi = c->s[q];
+  const int qc = cm ? q + 1 : q + 2;  // the child the bisection visits next
+  if (smooth_cert(c, qc, n_mc, alpha))
+    c->lo = c->s[qc];
+  else
+    c->hi = c->s[qc];
+}
+__global__ void k_smooth_decide(SmoothChain* c, int batch, int64_t n_mc, double alpha) {
+  int q0, np;
+  if (batch == 0) {
     c->done = 0;
-    c->s[0] = 1.0;
     c->steps = 0;
-  } else if (!c->done) {
-    const int q = k - 1;
-    const bool cert = c->live[q] != 0 && static_cast<double>(c->hits[q]) / n_mc <= alpha;
-    if (k == 1) {
-      if (cert) c->done = 1;
-      c->lo = 0;
-      c->hi = 1;
-    } else if (cert) {
-      c->lo = c->s[q];
-    } else {
-      c->hi = c->s[q];
+    c->lo = 0;
+    c->hi = 1;
+    q0 = 0;
+    np = 4;
+    c->s[0] = 1.0;
+    const double m = 0.5 * (c->lo + c->hi);
+    c->s[1] = m;
+    c->s[2] = 0.5 * (m + c->hi);
+    c->s[3] = 0.5 * (c->lo + m);
+  } else {
+    q0 = 4 + 3 * (batch - 1);
+    np = 3;
+    if (!c->done) {
+      if (batch == 1) {
+        if (smooth_cert(c, 0, n_mc, alpha))
+          c->done = 1;  // s = 1 certifies: no bisection
+        else
+          smooth_two_steps(c, 1, n_mc, alpha);
+      } else {
+        smooth_two_steps(c, q0 - 3, n_mc, alpha);
+      }
+      const double m = 0.5 * (c->lo + c->hi);
+      c->s[q0] = m;
+      c->s[q0 + 1] = 0.5 * (m + c->hi);
+      c->s[q0 + 2] = 0.5 * (c->lo + m);
     }
-    c->s[k] = 0.5 * (c->lo + c->hi);
   }
-  c->live[k] = c->done ? 0 : 1;
-  c->hits[k] = 0;
+  for (int k = 0; k < np; ++k) {
+    c->live[q0 + k] = c->done ? 0 : 1;
+    c->hits[q0 + k] = 0;
+  }
 }
 
 // ------------------------------------------------------------ path kernels
@@ -1186,15 +1220,16 @@ static void run_pump_device(Ctx& c, const pumpb::Scenario& s, const DevGraph* pr
     }
     static const bool spec = std::getenv("PUMP_SMOOTH_SCHEDULE") != nullptr;
     if (!host_probes && !spec) {
-      // all 11 probes enqueued at once, each deciding on the device from the
-      // previous verdict; one synchronisation for the whole bisection
-      const int64_t items = n_wp;
+      // five batches enqueued at once, each deciding on the device from the
+      // previous batch's verdicts; one synchronisation for the whole bisection
+      const int64_t items = static_cast<int64_t>(4) * n_wp;
       DBuf& d_y = c.buf("sm_y", items * dw * 8 + 256);
       DBuf& d_yv = c.buf("sm_yv", items * dw * 8 + 256);
       DBuf& d_ch = c.buf("sm_chain", sizeof(SmoothChain) + 256);
       DBuf& d_off = c.buf("sm_choff", 256);
-      const int64_t off2[2] = {0, static_cast<int64_t>(n_wp)};
-      c.h2d(d_off.p, off2, 16);
+      const int64_t offs[5] = {0, n_wp, 2 * static_cast<int64_t>(n_wp), 3 * static_cast<int64_t>(n_wp),
+                               4 * static_cast<int64_t>(n_wp)};
+      c.h2d(d_off.p, offs, sizeof(offs));
       SmoothChain* ch = d_ch.as<SmoothChain>();
       WorldD wd;
       wd.n_obs = dwld.n_obs;
@@ -1211,22 +1246,24 @@ static void run_pump_device(Ctx& c, const pumpb::Scenario& s, const DevGraph* pr
         c.mc_join_pending = false;
       }
       c.tic();
-      for (int k = 0; k <= 10; ++k) {
-        k_smooth_decide<<<1, 1, 0, c.stream>>>(ch, k, s.mc_samples, s.alpha);
+      for (int b = 0; b < 5; ++b) {
+        const int q0 = b == 0 ? 0 : 4 + 3 * (b - 1), np = b == 0 ? 4 : 3;
+        const int64_t it = static_cast<int64_t>(np) * n_wp;
+        k_smooth_decide<<<1, 1, 0, c.stream>>>(ch, b, s.mc_samples, s.alpha);
         dispatch_dw(dw, [&]<int DW>() {
           HMotion o = opt;
-          k_smooth_blend<DW><<<grid_for(items, 128), 128, 0, c.stream>>>(
-              1, n_wp, &ch->s[k], c.scratch["sm_plan"].as<double>(), c.scratch["sm_plan"].as<double>() + n_wp,
+          k_smooth_blend<DW><<<grid_for(it, 128), 128, 0, c.stream>>>(
+              np, n_wp, &ch->s[q0], c.scratch["sm_plan"].as<double>(), c.scratch["sm_plan"].as<double>() + n_wp,
               c.scratch["sm_plan"].as<double>() + n_wp * (1 + dw), as_motion<DW>(o), d_y.as<double>(),
               d_yv.as<double>());
-          k_smooth_check<DW><<<grid_for(items, 128), 128, 0, c.stream>>>(
-              wd, 1, n_wp, c.scratch["sm_plan"].as<double>(), d_y.as<double>(), d_yv.as<double>(), eps_cc,
-              &ch->live[k]);
+          k_smooth_check<DW><<<grid_for(it, 128), 128, 0, c.stream>>>(
+              wd, np, n_wp, c.scratch["sm_plan"].as<double>(), d_y.as<double>(), d_yv.as<double>(), eps_cc,
+              &ch->live[q0]);
         });
         c.launches += 3;
-        launch_mc(L, dwld, 1, d_off.as<int64_t>(), d_y.as<double>(), n_wp, r0, r1, s.seeds.mc, eps_cc,
-                  &ch->hits[k], c.stream, &c.launches, &ch->steps, &c.mc_table, &ch->live[k]);
-        allreduce_sum_i64(c, reinterpret_cast<int64_t*>(&ch->hits[k]), 1);
+        launch_mc(L, dwld, np, d_off.as<int64_t>(), d_y.as<double>(), n_wp, r0, r1, s.seeds.mc, eps_cc,
+                  &ch->hits[q0], c.stream, &c.launches, &ch->steps, &c.mc_table, &ch->live[q0]);
+        allreduce_sum_i64(c, reinterpret_cast<int64_t*>(&ch->hits[q0]), np);
         PUMP_CUDA(cudaGetLastError());
       }
       SmoothChain hc{};
@@ -1235,25 +1272,25 @@ static void run_pump_device(Ctx& c, const pumpb::Scenario& s, const DevGraph* pr
       c.sync();
       kprof_work(F_MC, static_cast<int64_t>(hc.steps));
       c.mc_rollout_steps += static_cast<int64_t>(hc.steps);
-      // replay (pump.hpp:118-141) from the history
-      auto record = [&](int k) {
+      for (int q = 0; q < kSmoothSlots; ++q) {  // every probe the batches evaluated
+        if (probes.count(hc.s[q]) || (q > 0 && hc.done)) continue;
         Probe p;
-        p.free = hc.live[k] != 0;
+        p.free = hc.live[q] != 0;
         if (p.free) {
-          p.mc = static_cast<double>(hc.hits[k]) / s.mc_samples;
+          p.mc = static_cast<double>(hc.hits[q]) / s.mc_samples;
           R.s.mc_rollouts += r1 - r0;
         }
-        probes.emplace(hc.s[k], std::move(p));
-      };
-      record(0);
+        probes.emplace(hc.s[q], std::move(p));
+      }
+      // replay (pump.hpp:118-141) from the history (probes.at throws if a
+      // probe the bisection visits was not evaluated on the device)
       if (certified(1.0)) {
         accept(1.0);
       } else {
         double lo = 0, hi = 1;
         for (int k = 1; k <= 10; ++k) {
           const double mid = 0.5 * (lo + hi);
-          if (hc.s[k] != mid) throw std::runtime_error("smoothing: device bisection diverged from the host replay");
-          record(k);
+          if (!probes.count(mid)) throw std::runtime_error("smoothing: device bisection diverged from the host replay");
           if (certified(mid)) {
             accept(mid);
             lo = mid;

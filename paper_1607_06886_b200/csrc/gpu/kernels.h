@@ -198,6 +198,7 @@ struct McTable {
   DBuf flags;  // per (trajectory, rollout) hit flags of one certification
   DBuf maxdev;  // [t][k]: max over rollouts of |dy| (bits of a non-negative double)
   DBuf nz;      // build scratch: per (t, rollout, axis) the Sv / Sw products of the step's normals
+  DBuf step_list, step_nl, step_skip;  // per (trajectory, step) candidate obstacles (k_mc_steps)
   int64_t r0 = 0, r1 = 0;
   int t_done = -1, t_cap = 0;
   uint64_t seed = 0;

@@ -680,19 +680,88 @@ __global__ void __launch_bounds__(kMcBlock) k_mctab_dense(const LoopP<D, DW> L, 
 // tests of k_mc_sep (bounds, bbox-culled obstacles, eps_cc-subdivided
 // segment).  A hit sets flag[j][i]; k_mc_count sums the flags.
 constexpr int kMcChunk = 8;   // steps whose table rows a thread loads up front
+// Per (trajectory, step) the candidate obstacles every rollout of the table
+// can meet (see k_mc_tab), listed once per certification instead of once per
+// block: the box ynom -/+ the largest |dy| over the table's rollouts at t and
+// t - 1 (fl is monotone, so fl(ynom +- maxdev) bounds fl(ynom + dy)), widened
+// by the sub-segment rounding margin; the inflated obstacles meeting it, a
+// warp per step (ballot compaction).  A step with an empty list whose box is
+// inside the workspace holds no failing test for any rollout: skip = 1.
+constexpr int kStepCap = 64;  // candidate obstacles per step (more: nl = -1, test all)
+template <int DW>
+__global__ void __launch_bounds__(128) k_mc_steps(WorldD w, const int64_t* __restrict__ traj_off,
+                                                  const double* __restrict__ ynom_all,
+                                                  const unsigned long long* __restrict__ maxdev, int t_stride,
+                                                  uint16_t* __restrict__ g_list, int32_t* __restrict__ g_nl,
+                                                  uint8_t* __restrict__ g_skip, const int32_t* __restrict__ live) {
+  const int j = blockIdx.y;
+  if (live && !live[j]) return;
+  const int lane = threadIdx.x & 31;
+  const int t = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
+  const int64_t p_begin = traj_off[j];
+  const int T = static_cast<int>(traj_off[j + 1] - p_begin) - 1;
+  if (t > T) return;
+  double bl[DW], bh[DW];
+  bool inside = true;
+#pragma unroll
+  for (int k = 0; k < DW; ++k) {
+    const double m1 = __longlong_as_double(static_cast<long long>(maxdev[t * DW + k]));
+    const double y1 = ynom_all[(p_begin + t) * DW + k];
+    double lo = y1 - m1, hi = y1 + m1;
+    if (t > 0) {
+      const double m0 = __longlong_as_double(static_cast<long long>(maxdev[(t - 1) * DW + k]));
+      const double y0 = ynom_all[(p_begin + t - 1) * DW + k];
+      const double lo0 = y0 - m0, hi0 = y0 + m0;
+      lo = lo0 < lo ? lo0 : lo;
+      hi = hi0 > hi ? hi0 : hi;
+    }
+    const double mg = 1e-12 * (1.0 + (lo < 0 ? -lo : lo) + (hi < 0 ? -hi : hi));
+    bl[k] = lo - mg;
+    bh[k] = hi + mg;
+    inside = inside && bl[k] > w.blo[k] && bh[k] < w.bhi[k];
+  }
+  const int64_t row = static_cast<int64_t>(j) * t_stride + t;
+  int nl = 0;
+  for (int o0 = 0; o0 < w.n_obs; o0 += 32) {
+    const int o = o0 + lane;
+    bool meet = false;
+    if (o < w.n_obs) {
+      bool sep = false;
+#pragma unroll
+      for (int k = 0; k < DW; ++k) {
+        const double bl_o = w.blo[k] < 0 ? -w.blo[k] : w.blo[k], bh_o = w.bhi[k] < 0 ? -w.bhi[k] : w.bhi[k];
+        const double lo = w.lo[o * DW + k], hi = w.hi[o * DW + k];
+        const double M = 1e-9 * (1.0 + (lo < 0 ? -lo : lo) + (hi < 0 ? -hi : hi) + 2.0 * (bl_o > bh_o ? bl_o : bh_o));
+        sep = sep || (bh[k] < lo - M) || (bl[k] > hi + M);
+      }
+      meet = !sep;
+    }
+    const unsigned bal = __ballot_sync(0xffffffffu, meet);
+    const int at = nl + __popc(bal & ((1u << lane) - 1u));
+    if (meet && at < kStepCap) g_list[row * kStepCap + at] = static_cast<uint16_t>(o);
+    nl += __popc(bal);
+  }
+  if (nl > kStepCap) nl = -1;
+  if (lane == 0) {
+    g_nl[row] = nl;
+    g_skip[row] = (inside && nl == 0) ? 1 : 0;
+  }
+}
+
 template <int DW, int kMcSub>  // kMcSub sub-chunks per block: a block spans kMcSpan steps
 __global__ void __launch_bounds__(kMcBlock) k_mc_tab(WorldD w, const int64_t* __restrict__ traj_off,
                                                      const double* __restrict__ ynom_all, int64_t r0, int64_t r1,
                                                      int64_t tab_r0, int64_t tab_n, const double* __restrict__ dy,
                                                      const unsigned long long* __restrict__ maxdev, double eps_cc,
-                                                     uint8_t* __restrict__ flags, const int32_t* __restrict__ live) {
+                                                     uint8_t* __restrict__ flags, const int32_t* __restrict__ live,
+                                                     int t_stride, const uint16_t* __restrict__ g_list,
+                                                     const int32_t* __restrict__ g_nl,
+                                                     const uint8_t* __restrict__ g_skip) {
   extern __shared__ double smem[];
   constexpr int kMcSpan = kMcChunk * kMcSub;
-  constexpr int kStepCap = 64;  // block-wide candidate obstacles per step (more: test all)
   __shared__ uint16_t s_list[kMcSpan + 1][kStepCap];
   __shared__ int s_nlist[kMcSpan + 1];  // -1: more than kStepCap candidates
   __shared__ int s_skip[kMcSpan + 1];
-  __shared__ int s_all_skip;
   const int j = blockIdx.y;
   if (live && !live[j]) return;  // trajectory not certified (its nominal collides): flags stay 0
   const int64_t p_begin = traj_off[j];
@@ -703,6 +772,19 @@ __global__ void __launch_bounds__(kMcBlock) k_mc_tab(WorldD w, const int64_t* __
   const int t_hi = min(T, t_lo + kMcSpan - 1);
   const int s_lo_t = t_lo > 0 ? t_lo - 1 : 0;  // rows staged: [s_lo_t, t_hi]
   const int rows = t_hi - s_lo_t + 1;
+  // the span's step flags and lists (k_mc_steps); a span where every step
+  // skips exits before staging anything
+  const int64_t row0 = static_cast<int64_t>(j) * t_stride + s_lo_t;
+  bool act = false;
+  if (threadIdx.x <= kMcSpan) {
+    const int r = threadIdx.x, t = s_lo_t + r;
+    const bool in = t >= t_lo && t <= t_hi;
+    const int skip = in ? g_skip[row0 + r] : 1;
+    s_skip[r] = skip;
+    s_nlist[r] = in ? g_nl[row0 + r] : 0;
+    act = !skip;
+  }
+  if (!__syncthreads_or(act)) return;
   double* s_y = smem;
   double* s_lo = s_y + rows * DW;
   double* s_hi = s_lo + w.n_obs * DW;
@@ -719,65 +801,11 @@ __global__ void __launch_bounds__(kMcBlock) k_mc_tab(WorldD w, const int64_t* __
     s_clo[x] = lo;
     s_chi[x] = hi;
   }
-  if (threadIdx.x == 0) s_all_skip = 1;
-  __syncthreads();
-  // Per step, the box every rollout's realized points (and the subdivision
-  // points between them) lie in: ynom -/+ the largest |dy| over the table's
-  // rollouts (fl is monotone, so fl(ynom +- maxdev) bounds fl(ynom + dy)),
-  // widened by the sub-segment rounding margin.  The (inflated) obstacles
-  // meeting that box are the only ones any rollout can touch at this step:
-  // listed per step (a warp per step, ballot compaction); a step with an
-  // empty list and its box inside the workspace holds no failing test for
-  // any rollout and is skipped, loads included.
-  {
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    for (int r = warp; r <= kMcSpan; r += kMcBlock / 32) {
-      const int t = s_lo_t + r;
-      int skip = 1, nl = 0;
-      if (t >= t_lo && t <= t_hi) {
-        double bl[DW], bh[DW];
-        bool inside = true;
-#pragma unroll
-        for (int k = 0; k < DW; ++k) {
-          const double m1 = __longlong_as_double(static_cast<long long>(maxdev[t * DW + k]));
-          double lo = s_y[r * DW + k] - m1, hi = s_y[r * DW + k] + m1;
-          if (t > 0) {
-            const double m0 = __longlong_as_double(static_cast<long long>(maxdev[(t - 1) * DW + k]));
-            const double lo0 = s_y[(r - 1) * DW + k] - m0, hi0 = s_y[(r - 1) * DW + k] + m0;
-            lo = lo0 < lo ? lo0 : lo;
-            hi = hi0 > hi ? hi0 : hi;
-          }
-          const double mg = 1e-12 * (1.0 + (lo < 0 ? -lo : lo) + (hi < 0 ? -hi : hi));
-          bl[k] = lo - mg;
-          bh[k] = hi + mg;
-          inside = inside && bl[k] > w.blo[k] && bh[k] < w.bhi[k];
-        }
-        for (int o0 = 0; o0 < w.n_obs; o0 += 32) {
-          const int o = o0 + lane;
-          bool meet = false;
-          if (o < w.n_obs) {
-            bool sep = false;
-#pragma unroll
-            for (int k = 0; k < DW; ++k) sep = sep || (bh[k] < s_lo[o * DW + k]) || (bl[k] > s_hi[o * DW + k]);
-            meet = !sep;
-          }
-          const unsigned bal = __ballot_sync(0xffffffffu, meet);
-          const int at = nl + __popc(bal & ((1u << lane) - 1u));
-          if (meet && at < kStepCap) s_list[r][at] = static_cast<uint16_t>(o);
-          nl += __popc(bal);
-        }
-        if (nl > kStepCap) nl = -1;
-        skip = (inside && nl == 0) ? 1 : 0;
-      }
-      if (lane == 0) {
-        s_nlist[r] = nl;
-        s_skip[r] = skip;
-        if (!skip) s_all_skip = 0;
-      }
-    }
+  for (int x = threadIdx.x; x < (kMcSpan + 1) * kStepCap; x += blockDim.x) {
+    const int r = x / kStepCap, q = x % kStepCap;
+    if (q < s_nlist[r]) s_list[r][q] = g_list[(row0 + r) * kStepCap + q];
   }
   __syncthreads();
-  if (s_all_skip) return;
   const double e = eps_cc > 1e-12 ? eps_cc : 1e-12;  // std::max(eps_cc, 1e-12)
   const int64_t i = r0 + static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i >= r1) return;
@@ -1066,6 +1094,15 @@ void launch_mc(const HostLoop& HL, const DevWorld& w, int n_traj, const int64_t*
     PUMP_CUDA(cudaMemsetAsync(table->flags.p, 0, static_cast<size_t>(n) * n_traj, st));
     dispatch_dw(HL.dw, [&]<int DW>() {
       static const int sub = std::getenv("PUMP_MC_SUB") ? std::atoi(std::getenv("PUMP_MC_SUB")) : 2;
+      // per-(trajectory, step) candidate lists, once per certification
+      const size_t rows_all = static_cast<size_t>(n_traj) * max_points;
+      table->step_list.ensure(rows_all * kStepCap * 2 + 256);
+      table->step_nl.ensure(rows_all * 4 + 256);
+      table->step_skip.ensure(rows_all + 256);
+      k_mc_steps<DW><<<dim3((max_points + 3) / 4, n_traj), 128, 0, st>>>(
+          wd, d_traj_off, d_ynom, table->maxdev.as<unsigned long long>(), max_points,
+          table->step_list.as<uint16_t>(), table->step_nl.as<int32_t>(), table->step_skip.as<uint8_t>(), d_live);
+      ++*launches;
       auto go = [&]<int SUB>() {
         constexpr int span = kMcChunk * SUB;
         const size_t smem = (static_cast<size_t>(span + 1) * DW + 4 * static_cast<size_t>(w.n_obs) * DW) * sizeof(double);
@@ -1076,7 +1113,9 @@ void launch_mc(const HostLoop& HL, const DevWorld& w, int n_traj, const int64_t*
         k_mc_tab<DW, SUB><<<grid, kMcBlock, smem, st>>>(wd, d_traj_off, d_ynom, r0, r1, table->r0,
                                                         table->r1 - table->r0, table->dy.as<double>(),
                                                         table->maxdev.as<unsigned long long>(), eps_cc,
-                                                        table->flags.as<uint8_t>(), d_live);
+                                                        table->flags.as<uint8_t>(), d_live, max_points,
+                                                        table->step_list.as<uint16_t>(), table->step_nl.as<int32_t>(),
+                                                        table->step_skip.as<uint8_t>());
       };
       KScope ks(st, F_MC);
       if (sub == 2) go.template operator()<2>();
