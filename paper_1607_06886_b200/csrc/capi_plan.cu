@@ -376,6 +376,105 @@ __global__ void k_path_compact(int ns, int max_len, int dw, const int32_t* __res
   }
 }
 
+// path_trajectory (planner.hpp:292-315) of every front plan on the device: a
+// warp per plan walks its edges in order (the time offset is the running sum
+// of the edge durations, as the reference adds them) and the lanes write each
+// edge's waypoints (motion_waypoints, steer.hpp:192-212: i dt for i <= k, the
+// end state at tau; a later edge drops its first waypoint).  A plan's
+// waypoint count is t_end + 1, so the host knows every offset up front.
+template <int DW>
+__global__ void k_traj_build(int ns, int max_len, const int32_t* __restrict__ nodes, const int64_t* __restrict__ edges,
+                             const int32_t* __restrict__ lens, const int64_t* __restrict__ off,
+                             const double* __restrict__ pos, const double* __restrict__ vel,
+                             const double* __restrict__ e_tau, const double* __restrict__ e_acc0,
+                             const double* __restrict__ e_jerk, double dt, double* __restrict__ wt,
+                             double* __restrict__ wp, double* __restrict__ wv, double* __restrict__ wu) {
+  const int s = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (s >= ns) return;
+  const int len = lens[s];
+  const int32_t* nd = nodes + static_cast<int64_t>(s) * max_len;
+  const int64_t* ed = edges + static_cast<int64_t>(s) * max_len;
+  int64_t w = off[s];
+  if (len == 1 && lane == 0) {
+    wt[w] = 0;
+#pragma unroll
+    for (int k = 0; k < DW; ++k) {
+      wp[w * DW + k] = pos[nd[0] * DW + k];
+      wv[w * DW + k] = vel[nd[0] * DW + k];
+      wu[w * DW + k] = 0;
+    }
+  }
+  double offset = 0;
+  for (int j = 0; j + 1 < len; ++j) {
+    const int64_t e = ed[j];
+    MotionD<DW> m;
+    m.tau = e_tau[e];
+    const int v = nd[j], u = nd[j + 1];
+#pragma unroll
+    for (int k = 0; k < DW; ++k) {
+      m.p0[k] = pos[v * DW + k];
+      m.v0[k] = vel[v * DW + k];
+      m.p1[k] = pos[u * DW + k];
+      m.v1[k] = vel[u * DW + k];
+      m.a[k] = e_acc0[e * DW + k];
+      m.j[k] = e_jerk[e * DW + k];
+    }
+    int kk = 0, cnt = 1;
+    bool extra = false;
+    if (m.tau > 0) {
+      kk = static_cast<int>(floor(m.tau / dt + 1e-9));
+      const double rem = m.tau - kk * dt;
+      extra = rem > 1e-9;
+      cnt = kk + 1 + (extra ? 1 : 0);
+    }
+    const int i0 = j == 0 ? 0 : 1;
+    for (int i = i0 + lane; i < cnt; i += 32) {
+      double t = 0, p[DW], vv[DW], uu[DW];
+      if (m.tau <= 0) {
+#pragma unroll
+        for (int k = 0; k < DW; ++k) {
+          p[k] = m.p0[k];
+          vv[k] = m.v0[k];
+          uu[k] = 0;
+        }
+      } else if (extra && i == kk + 1) {
+        t = m.tau;
+#pragma unroll
+        for (int k = 0; k < DW; ++k) {
+          p[k] = m.p1[k];
+          vv[k] = m.v1[k];
+          uu[k] = m.a[k] + m.j[k] * m.tau;
+        }
+      } else {
+        t = i * dt;
+        motion_state<DW>(m, t, p, vv);
+        const double sc = t < 0 ? 0.0 : (m.tau < t ? m.tau : t);  // std::clamp(t, 0, tau)
+#pragma unroll
+        for (int k = 0; k < DW; ++k) uu[k] = m.a[k] + m.j[k] * sc;
+        if (!extra && i == kk) {  // the last waypoint is the end state at tau
+          t = m.tau;
+#pragma unroll
+          for (int k = 0; k < DW; ++k) {
+            p[k] = m.p1[k];
+            vv[k] = m.v1[k];
+          }
+        }
+      }
+      const int64_t x = w + (i - i0);
+      wt[x] = t + offset;
+#pragma unroll
+      for (int k = 0; k < DW; ++k) {
+        wp[x * DW + k] = p[k];
+        wv[x * DW + k] = vv[k];
+        wu[x * DW + k] = uu[k];
+      }
+    }
+    w += cnt - i0;
+    offset += m.tau;
+  }
+}
+
 static PathSet resolve_paths(Ctx& c, const DevGraph& G, const DevExplore& X, const std::vector<int>& sel) {
   PathSet ps;
   const int ns = static_cast<int>(sel.size());
@@ -470,6 +569,37 @@ static std::vector<HWp> path_trajectory(const DevGraph& G, const std::vector<int
 }
 
 // Batched MC over trajectories (rollouts [0, n_mc)); values = hits / n_mc
+// MC values of nt trajectories already on the device (positions d_y, point
+// offsets d_off); this rank's rollouts, hit counts summed over the ranks
+static std::vector<double> mc_values_dev(Ctx& c, const HostLoop& L, const DevWorld& w, int nt, const int64_t* d_off,
+                                         const double* d_y, int max_pts, int n_mc, uint64_t seed, double eps_cc,
+                                         double* mc_ms, int64_t* rollouts) {
+  DBuf& d_h = c.buf("r_mc_hits", (nt + 1) * 8 + 256);
+  PUMP_CUDA(cudaMemsetAsync(d_h.p, 0, (nt + 1) * 8, c.stream));
+  // this rank's rollouts (all of them on one GPU), then the hit counts of all
+  // ranks are summed over NVLink (bit-identical for any world size)
+  int64_t r0 = 0, r1 = n_mc;
+  shard_range(n_mc, c.rank, c.world, &r0, &r1);
+  if (c.mc_join_pending) {
+    PUMP_CUDA(cudaStreamWaitEvent(c.stream, c.join, 0));
+    c.mc_join_pending = false;
+  }
+  c.tic();
+  launch_mc(L, w, nt, d_off, d_y, max_pts, r0, r1, seed, eps_cc, d_h.as<unsigned long long>(), c.stream, &c.launches,
+            d_h.as<unsigned long long>() + nt, &c.mc_table);
+  allreduce_sum_i64(c, d_h.as<int64_t>(), nt);
+  *mc_ms += c.toc();
+  *rollouts += (r1 - r0) * nt;
+  std::vector<int64_t> hits(nt + 1);
+  c.d2h(hits.data(), d_h.p, (nt + 1) * 8);
+  c.sync();
+  kprof_work(F_MC, hits[nt]);
+  c.mc_rollout_steps += hits[nt];
+  std::vector<double> v(nt);
+  for (int j = 0; j < nt; ++j) v[j] = static_cast<double>(hits[j]) / n_mc;
+  return v;
+}
+
 static std::vector<double> mc_values(Ctx& c, const HostLoop& L, const DevWorld& w,
                                      const std::vector<std::vector<HWp>>& trajs, int n_mc, uint64_t seed,
                                      double eps_cc, double* mc_ms, int64_t* rollouts) {
@@ -487,32 +617,10 @@ static std::vector<double> mc_values(Ctx& c, const HostLoop& L, const DevWorld& 
   const int nt = static_cast<int>(trajs.size());
   DBuf& d_off = c.buf("r_mc_off", (nt + 1) * 8 + 256);
   DBuf& d_y = c.buf("r_mc_y", y.size() * 8 + 256);
-  DBuf& d_h = c.buf("r_mc_hits", (nt + 1) * 8 + 256);
   c.h2d(d_off.p, off.data(), (nt + 1) * 8);
   c.h2d(d_y.p, y.data(), y.size() * 8);
-  PUMP_CUDA(cudaMemsetAsync(d_h.p, 0, (nt + 1) * 8, c.stream));
-  // this rank's rollouts (all of them on one GPU), then the hit counts of all
-  // ranks are summed over NVLink (bit-identical for any world size)
-  int64_t r0 = 0, r1 = n_mc;
-  shard_range(n_mc, c.rank, c.world, &r0, &r1);
-  if (c.mc_join_pending) {
-    PUMP_CUDA(cudaStreamWaitEvent(c.stream, c.join, 0));
-    c.mc_join_pending = false;
-  }
-  c.tic();
-  launch_mc(L, w, nt, d_off.as<int64_t>(), d_y.as<double>(), max_pts, r0, r1, seed, eps_cc,
-            d_h.as<unsigned long long>(), c.stream, &c.launches, d_h.as<unsigned long long>() + nt, &c.mc_table);
-  allreduce_sum_i64(c, d_h.as<int64_t>(), nt);
-  *mc_ms += c.toc();
-  *rollouts += (r1 - r0) * nt;
-  std::vector<int64_t> hits(nt + 1);
-  c.d2h(hits.data(), d_h.p, (nt + 1) * 8);
-  c.sync();
-  kprof_work(F_MC, hits[nt]);
-  c.mc_rollout_steps += hits[nt];
-  std::vector<double> v(nt);
-  for (int j = 0; j < nt; ++j) v[j] = static_cast<double>(hits[j]) / n_mc;
-  return v;
+  return mc_values_dev(c, L, w, nt, d_off.as<int64_t>(), d_y.as<double>(), max_pts, n_mc, seed, eps_cc, mc_ms,
+                       rollouts);
 }
 
 }  // namespace pumpg
@@ -953,7 +1061,11 @@ static void run_pump_device(Ctx& c, const pumpb::Scenario& s, const DevGraph* pr
     R.pareto_cp.push_back(gcp[k]);
   }
   std::vector<int> sorted_ids;  // ascending cp_hat
-  for (auto it = front.rbegin(); it != front.rend(); ++it) sorted_ids.push_back(gids[*it]);
+  std::vector<int> sorted_tend;
+  for (auto it = front.rbegin(); it != front.rend(); ++it) {
+    sorted_ids.push_back(gids[*it]);
+    sorted_tend.push_back(gtend[*it]);
+  }
 
   // Alg. 4 bisection (pump.hpp:23-51): every front plan is certified in one
   // batched MC launch (speculatively), then the bisection is replayed from
@@ -974,16 +1086,60 @@ static void run_pump_device(Ctx& c, const pumpb::Scenario& s, const DevGraph* pr
     c.mc_join_pending = true;  // the first certification waits for it (mc_values)
   }
   mark("front");
-  PathSet ps = resolve_paths(c, *graph, X, sorted_ids);
-  mark("resolve_paths");
-  std::vector<std::vector<HWp>> trajs;
-  for (size_t k = 0; k < sorted_ids.size(); ++k)
-    trajs.push_back(path_trajectory(*graph, ps.nodes[k], ps.edges[k], ps.motion[k]));
-  mark("path_trajectory");
-  std::vector<double> memo = trajs.empty() ? std::vector<double>{}
-                                           : mc_values(c, L, dwld, trajs, s.mc_samples, s.seeds.mc, eps_cc,
-                                                       &R.s.mc_ms, &R.s.mc_rollouts);
+  // The front plans' node paths and trajectories on the device (k_paths,
+  // k_traj_build): plan q has t_end + 1 waypoints, so the offsets are known
+  // here; their positions feed the MC batch directly and only the selected
+  // plan is copied back.  PUMP_HOST_PATHS=1: paths and trajectories on the host.
+  static const bool host_paths = std::getenv("PUMP_HOST_PATHS") != nullptr;
   const int nf = static_cast<int>(sorted_ids.size());
+  constexpr int kMaxLen = 4096;
+  PathSet ps;
+  std::vector<std::vector<HWp>> trajs;
+  std::vector<int64_t> woff(nf + 1, 0);
+  std::vector<double> memo;
+  if (host_paths) {
+    ps = resolve_paths(c, *graph, X, sorted_ids);
+    for (size_t k = 0; k < sorted_ids.size(); ++k)
+      trajs.push_back(path_trajectory(*graph, ps.nodes[k], ps.edges[k], ps.motion[k]));
+    if (!trajs.empty())
+      memo = mc_values(c, L, dwld, trajs, s.mc_samples, s.seeds.mc, eps_cc, &R.s.mc_ms, &R.s.mc_rollouts);
+  } else if (nf > 0) {
+    int max_pts = 0;
+    for (int q = 0; q < nf; ++q) {
+      woff[q + 1] = woff[q] + sorted_tend[q] + 1;
+      max_pts = std::max(max_pts, sorted_tend[q] + 1);
+    }
+    const int64_t total = woff[nf];
+    std::vector<int64_t> in(nf + 1 + (nf + 1) / 2 + 1, 0);  // offsets, then the plan ids (int32 pairs)
+    std::memcpy(in.data(), woff.data(), (nf + 1) * 8);
+    std::memcpy(in.data() + nf + 1, sorted_ids.data(), nf * 4);
+    DBuf& d_in = c.buf("p_in", in.size() * 8 + 256);
+    c.h2d(d_in.p, in.data(), in.size() * 8);
+    const int64_t* d_woff = d_in.as<int64_t>();
+    const int32_t* d_sel = reinterpret_cast<const int32_t*>(d_in.as<int64_t>() + nf + 1);
+    DBuf& d_nodes = c.buf("p_nodes", static_cast<size_t>(nf) * kMaxLen * 4 + 256);
+    DBuf& d_edges = c.buf("p_edges", static_cast<size_t>(nf) * kMaxLen * 8 + 256);
+    DBuf& d_lens = c.buf("p_lens", nf * 4 + 256);
+    DBuf& d_wt = c.buf("p_wt", total * 8 + 256);
+    DBuf& d_wp = c.buf("p_wp", total * dw * 8 + 256);
+    DBuf& d_wv = c.buf("p_wv", total * dw * 8 + 256);
+    DBuf& d_wu = c.buf("p_wu", total * dw * 8 + 256);
+    const DevGraph& G = *graph;
+    k_paths<<<(nf + 127) / 128, 128, 0, c.stream>>>(nf, d_sel, X.head.as<int32_t>(), X.parent.as<int32_t>(),
+                                                    G.row_ptr.as<int64_t>(), G.e_to.as<int32_t>(), kMaxLen,
+                                                    d_nodes.as<int32_t>(), d_edges.as<int64_t>(), d_lens.as<int32_t>());
+    dispatch_dw(dw, [&]<int DW>() {
+      k_traj_build<DW><<<(nf * 32 + 127) / 128, 128, 0, c.stream>>>(
+          nf, kMaxLen, d_nodes.as<int32_t>(), d_edges.as<int64_t>(), d_lens.as<int32_t>(), d_woff,
+          G.pos.as<double>(), G.vel.as<double>(), G.e_tau.as<double>(), G.e_acc0.as<double>(), G.e_jerk.as<double>(),
+          G.dt, d_wt.as<double>(), d_wp.as<double>(), d_wv.as<double>(), d_wu.as<double>());
+    });
+    c.launches += 2;
+    PUMP_CUDA(cudaGetLastError());
+    memo = mc_values_dev(c, L, dwld, nf, d_woff, d_wp.as<double>(), max_pts, s.mc_samples, s.seeds.mc, eps_cc,
+                         &R.s.mc_ms, &R.s.mc_rollouts);
+  }
+  mark("paths + trajectories");
   std::vector<char> seen(nf, 0);
   auto eval = [&](int m) {
     if (!seen[m - 1]) {
@@ -1016,7 +1172,36 @@ static void run_pump_device(Ctx& c, const pumpb::Scenario& s, const DevGraph* pr
   }
   mark("front mc");
   const int sel_id = sorted_ids[sel];
-  R.path.assign(ps.nodes[sel].begin(), ps.nodes[sel].end());
+  std::vector<HWp> plan_sel;
+  if (host_paths) {
+    R.path.assign(ps.nodes[sel].begin(), ps.nodes[sel].end());
+    plan_sel = trajs[sel];
+  } else {
+    // the selected plan's node path and waypoints
+    const int64_t n_wp = woff[sel + 1] - woff[sel];
+    int32_t len = 0;
+    c.d2h(&len, c.scratch["p_lens"].as<int32_t>() + sel, 4);
+    std::vector<int32_t> nodes(kMaxLen);
+    c.d2h(nodes.data(), c.scratch["p_nodes"].as<int32_t>() + static_cast<int64_t>(sel) * kMaxLen, kMaxLen * 4);
+    std::vector<double> wt(n_wp), wpv(n_wp * dw), wvv(n_wp * dw), wuv(n_wp * dw);
+    c.d2h(wt.data(), c.scratch["p_wt"].as<double>() + woff[sel], n_wp * 8);
+    c.d2h(wpv.data(), c.scratch["p_wp"].as<double>() + woff[sel] * dw, n_wp * dw * 8);
+    c.d2h(wvv.data(), c.scratch["p_wv"].as<double>() + woff[sel] * dw, n_wp * dw * 8);
+    c.d2h(wuv.data(), c.scratch["p_wu"].as<double>() + woff[sel] * dw, n_wp * dw * 8);
+    c.sync();
+    R.path.assign(nodes.begin(), nodes.begin() + len);
+    plan_sel.resize(n_wp);
+    for (int64_t q = 0; q < n_wp; ++q) {
+      HWp& h = plan_sel[q];
+      h = HWp{};
+      h.t = wt[q];
+      for (int k = 0; k < dw; ++k) {
+        h.p[k] = wpv[q * dw + k];
+        h.v[k] = wvv[q * dw + k];
+        h.u[k] = wuv[q * dw + k];
+      }
+    }
+  }
   {
     double cph, cst;
     c.d2h(&cph, X.cp.as<double>() + sel_id, 8);
@@ -1032,7 +1217,7 @@ static void run_pump_device(Ctx& c, const pumpb::Scenario& s, const DevGraph* pr
   // (candidates whose blended nominal collides get no MC, as in the
   // reference) and the bisection is then replayed from the memo: the accepted
   // s, trajectory and certified CP are exactly the reference's.
-  const std::vector<HWp>& plan = trajs[sel];
+  const std::vector<HWp>& plan = plan_sel;
   std::vector<HWp> best = plan;
   double best_cost = trajectory_cost(plan, dw), best_mc = memo[sel], best_s = 0;
   if (plan.size() >= 2) {
