@@ -1367,7 +1367,7 @@ void run_explore_device(DevExplore& X, Ctx& c, const DevGraph& G, const ExploreA
     }
     const int64_t Th = h.T;
     max_T = std::max<int64_t>(max_T, Th);
-    const bool pipe = coop_ok && kBatch > 1 && !prm.on_round && !force_sync;
+    const bool pipe = coop_ok && kBatch > 1 && (!prm.on_round || prm.on_round_batched) && !force_sync;
     force_sync = false;
     // buffer sizes: this round's T, or a per-round capacity for a batch
     const int64_t T = pipe ? std::max<int64_t>({Th, 2 * max_T, 4096}) : Th;

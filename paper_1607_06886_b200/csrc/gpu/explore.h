@@ -44,6 +44,9 @@ struct ExploreArgs {
   // called after every round's status readback (run_pump extends the MC
   // table on the side stream up to the goal plans' largest t_end)
   std::function<void(const ExploreStatus&)> on_round = nullptr;
+  // the hook only needs the latest status, not every round's: pipelined
+  // batches stay on and it runs once per status read
+  bool on_round_batched = false;
 };
 
 void run_explore_device(DevExplore& X, Ctx& c, const DevGraph& G, const ExploreArgs& a);
