@@ -581,6 +581,14 @@ static std::vector<double> mc_values_dev(Ctx& c, const HostLoop& L, const DevWor
   int64_t r0 = 0, r1 = n_mc;
   shard_range(n_mc, c.rank, c.world, &r0, &r1);
   if (c.mc_join_pending) {
+    static const bool dbg_join = std::getenv("PUMP_DEBUG_TIMING") != nullptr;
+    if (dbg_join) {  // how long the MC table on the side stream keeps the certification waiting
+      c.sync();
+      const auto a = std::chrono::steady_clock::now();
+      PUMP_CUDA(cudaEventSynchronize(c.join));
+      std::fprintf(stderr, "[pump t] mc table wait          %8.3f ms\n",
+                   1e3 * std::chrono::duration<double>(std::chrono::steady_clock::now() - a).count());
+    }
     PUMP_CUDA(cudaStreamWaitEvent(c.stream, c.join, 0));
     c.mc_join_pending = false;
   }

@@ -206,21 +206,72 @@ __device__ __forceinline__ void expand_task(const ExpandArgs& a, int64_t task, i
       j = jn;
     }
   } else {
-    for (int j = 0; j < ns; ++j) {
-      int64_t h0;
-      int cnt;
-      if (j < 32) {
-        h0 = __shfl_sync(0xffffffffu, my_h0, j);
-        cnt = __shfl_sync(0xffffffffu, my_cnt, j);
-      } else {
-        h0 = a.hs_off[w0 + j];
-        cnt = a.hs_cnt[w0 + j];
+    // long edges / many half-spaces: 32 waypoints at a time, each lane its
+    // waypoint's harmless-half-space filter (as above; past 64 half-spaces a
+    // waypoint tests all), then the rows that can lose a particle in order,
+    // the next one prefetched
+    for (int jb = 0; jb < ns; jb += 32) {
+      const int jj = jb + lane;
+      int64_t h0 = 0;
+      int cnt = 0;
+      if (jj < ns) {
+        if (jb == 0) {
+          h0 = my_h0;
+          cnt = my_cnt;
+        } else {
+          h0 = a.hs_off[w0 + jj];
+          cnt = a.hs_cnt[w0 + jj];
+        }
       }
-      tests += cnt;
-      if (cnt == 0) continue;
-      double p[CH][DW];
-      load_row<DW, CH>(a.dy + static_cast<int64_t>(pt + j + 1) * a.N * DW, a.N, lane, p);
-      for (int64_t h = h0; h < h0 + cnt; ++h) hs_test<DW, CH>(hpk[h * 2], hpk[h * 2 + 1], p, kill);
+      uint64_t need = 0;
+      const bool all = cnt > 64;
+      if (cnt > 0 && !all) {
+        const double* box = a.bank_box + static_cast<int64_t>(pt + jj + 1) * 2 * DW;
+        double blo[DW], bhi[DW];
+#pragma unroll
+        for (int k = 0; k < DW; ++k) {
+          blo[k] = box[k];
+          bhi[k] = box[DW + k];
+        }
+        for (int q = 0; q < cnt; ++q) {
+          const double2 q0 = hpk[(h0 + q) * 2], q1 = hpk[(h0 + q) * 2 + 1];
+          const double av[3] = {q0.x, q0.y, q1.x};
+          double bound = 0;
+#pragma unroll
+          for (int k = 0; k < DW; ++k) {
+            const double m1 = av[k] * blo[k], m2 = av[k] * bhi[k];
+            const double mk = m1 > m2 ? m1 : m2;
+            bound = k == 0 ? mk : bound + mk;
+          }
+          if (bound > q1.y) need |= 1ull << q;
+        }
+      }
+      unsigned live = __ballot_sync(0xffffffffu, need != 0 || all);
+      int64_t t_l = all ? cnt : __popcll(need);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) t_l += __shfl_xor_sync(0xffffffffu, t_l, o);
+      tests += t_l;
+      double p[CH][DW], pn[CH][DW];
+      int j = live ? __ffs(live) - 1 : -1;
+      if (j >= 0) load_row<DW, CH>(a.dy + static_cast<int64_t>(pt + jb + j + 1) * a.N * DW, a.N, lane, p);
+      while (j >= 0) {
+        live &= ~(1u << j);
+        const int jn = live ? __ffs(live) - 1 : -1;
+        if (jn >= 0) load_row<DW, CH>(a.dy + static_cast<int64_t>(pt + jb + jn + 1) * a.N * DW, a.N, lane, pn);
+        const int64_t hj = __shfl_sync(0xffffffffu, h0, j);
+        const int cj = __shfl_sync(0xffffffffu, cnt, j);
+        const uint64_t nj = __shfl_sync(0xffffffffu, need, j);
+        const bool aj = cj > 64;
+        for (int h = 0; h < cj; ++h)
+          if (aj || ((nj >> h) & 1ull)) hs_test<DW, CH>(hpk[(hj + h) * 2], hpk[(hj + h) * 2 + 1], p, kill);
+        if (jn >= 0) {
+#pragma unroll
+          for (int c = 0; c < CH; ++c)
+#pragma unroll
+            for (int k = 0; k < DW; ++k) p[c][k] = pn[c][k];
+        }
+        j = jn;
+      }
     }
   }
   if (lane == 0) atomicAdd(reinterpret_cast<unsigned long long*>(&a.st->hs_tests), static_cast<unsigned long long>(tests));
