@@ -296,7 +296,7 @@ __device__ __forceinline__ void expand_task(const ExpandArgs& a, int64_t task, i
 }
 
 template <int DW, int CH>
-__global__ void __launch_bounds__(kExpBlock) k_expand(const ExpandArgs a) {
+__global__ void __launch_bounds__(kExpBlock, (CH <= 2 ? 4 : 2)) k_expand(const ExpandArgs a) {
   __shared__ double2 s_hs[kExpBlock / 32][kExpStage][2];
   const int64_t task = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
