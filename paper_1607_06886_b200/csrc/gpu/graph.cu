@@ -685,7 +685,7 @@ __global__ void k_cand_compact(int n, int64_t n_surv, const uint8_t* __restrict_
 
 
 template <int DW, int LIST>
-__global__ void __launch_bounds__(128) k_collide(GraphArgs g, WorldD w, int64_t n_cand,
+__global__ void __launch_bounds__(128, 6) k_collide(GraphArgs g, WorldD w, int64_t n_cand,
                                                  const int32_t* __restrict__ c_v, const int32_t* __restrict__ c_u,
                                                  const double* __restrict__ c_tau, uint8_t* __restrict__ valid,
                                                  int32_t* __restrict__ nsteps) {
