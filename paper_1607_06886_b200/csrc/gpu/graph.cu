@@ -625,6 +625,23 @@ __global__ void __launch_bounds__(kRowBlock) k_pair_filter_grid(
   if (threadIdx.x == 0) row_cnt[v] = base_run;
 }
 
+// largest per-row survivor count (the slab refit check) without a host copy of the counts
+__global__ void k_max_count(int n, const int32_t* __restrict__ cnt, int* __restrict__ out) {
+  int m = 0;
+  for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) m = max(m, cnt[v]);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0) atomicMax(out, m);
+}
+
+// candidate count, edge count and waypoint count into one fixed place (one copy back)
+__global__ void k_graph_totals(const int64_t* __restrict__ d_ncand, const int64_t* __restrict__ d_E,
+                               const int64_t* __restrict__ wp_off, int64_t* __restrict__ out) {
+  out[0] = *d_ncand;
+  out[1] = *d_E;
+  out[2] = wp_off[*d_E];
+}
+
 __device__ __forceinline__ int find_row(const int64_t* __restrict__ off, int n, int64_t c) {
   int lo = 0, hi = n;  // largest r with off[r] <= c
   while (hi - lo > 1) {
@@ -685,14 +702,14 @@ __global__ void k_cand_compact(int n, int64_t n_surv, const uint8_t* __restrict_
 
 
 template <int DW, int LIST>
-__global__ void __launch_bounds__(128, 6) k_collide(GraphArgs g, WorldD w, int64_t n_cand,
+__global__ void __launch_bounds__(128, 6) k_collide(GraphArgs g, WorldD w, const int64_t* __restrict__ d_ncand,
                                                  const int32_t* __restrict__ c_v, const int32_t* __restrict__ c_u,
                                                  const double* __restrict__ c_tau, uint8_t* __restrict__ valid,
                                                  int32_t* __restrict__ nsteps) {
   extern __shared__ double smem[];
   const WorldD ws = stage_world<DW>(w, smem);
   const int64_t c = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (c >= n_cand) return;
+  if (c >= *d_ncand) return;
   const int v = c_v[c], u = c_u[c];
   MotionD<DW> m;
   m.tau = c_tau[c];
@@ -731,7 +748,8 @@ __global__ void __launch_bounds__(128, 6) k_collide(GraphArgs g, WorldD w, int64
 }
 
 template <int DW>
-__global__ void k_emit_edges(GraphArgs g, int64_t n_cand, const int64_t* __restrict__ cand_off,
+__global__ void k_emit_edges(GraphArgs g, const int64_t* __restrict__ d_ncand, int64_t* __restrict__ d_E,
+                             const int64_t* __restrict__ cand_off,
                              const int32_t* __restrict__ c_v, const int32_t* __restrict__ c_u,
                              const double* __restrict__ c_tau, const double* __restrict__ c_cost,
                              const uint8_t* __restrict__ valid, const int32_t* __restrict__ nsteps,
@@ -740,7 +758,9 @@ __global__ void k_emit_edges(GraphArgs g, int64_t n_cand, const int64_t* __restr
                              double* __restrict__ e_jerk, int32_t* __restrict__ e_nsteps,
                              int64_t* __restrict__ row_ptr) {
   const int64_t c = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t n_cand = *d_ncand;
   if (c < g.n + 1) row_ptr[c] = eoff[cand_off[c]];  // valid candidates before row c
+  if (c == n_cand) *d_E = eoff[c];                  // the edge count
   if (c >= n_cand || !valid[c]) return;
   const int64_t e = eoff[c];
   const int v = c_v[c], u = c_u[c];
@@ -1083,6 +1103,7 @@ void build_graph_device(DevGraph& G, Ctx& c, int n, int dw, const double* h_pos,
     ++c.launches;
     PUMP_CUDA(cudaGetLastError());
   }
+  int64_t n_surv = 0;
   for (;;) {  // pass 1 with an exact per-row refit if a row overflows the slab
     DBuf& suB = c.buf("g_su", al(static_cast<size_t>(n) * cap * 4));
     {
@@ -1109,22 +1130,22 @@ void build_graph_device(DevGraph& G, Ctx& c, int n, int dw, const double* h_pos,
       ++c.launches;
       PUMP_CUDA(cudaGetLastError());
     }
-    std::vector<int32_t> cnt(n);
-    c.d2h(cnt.data(), rcnt.p, n * 4);
-    c.sync();
-    mark("pair_filter");
+    // the slab check and the survivor total in one round trip
+    DBuf& mx = c.buf("g_maxcnt", 256);
+    PUMP_CUDA(cudaMemsetAsync(mx.p, 0, 4, st));
+    k_max_count<<<std::min(148, (n + 255) / 256 + 1), 256, 0, st>>>(n, rcnt.as<int32_t>(), mx.as<int>());
+    exclusive_scan<int32_t>(rcnt.as<int32_t>(), soff.as<int64_t>(), n, stmp.p, st, &c.launches);
+    c.launches += 1;
     int max_cnt = 0;
-    for (int v = 0; v < n; ++v) max_cnt = std::max(max_cnt, cnt[v]);
+    c.d2h(&max_cnt, mx.p, 4);
+    c.d2h(&n_surv, soff.as<int64_t>() + n, 8);
+    c.sync();
+    mark("pair_filter + survivor scan");
     if (max_cnt <= cap) break;
     cap = max_cnt;
   }
   kprof_work(F_CONNECT, static_cast<int64_t>(n) * (n - 1));
   int32_t* su = c.scratch["g_su"].as<int32_t>();
-  exclusive_scan<int32_t>(rcnt.as<int32_t>(), soff.as<int64_t>(), n, stmp.p, st, &c.launches);
-  int64_t n_surv = 0;
-  c.d2h(&n_surv, soff.as<int64_t>() + n, 8);
-  c.sync();
-  mark("survivor scan");
   G.n_connect = n_surv;
   DBuf& skeep = c.buf("g_skeep", al(n_surv + 1));
   DBuf& sv = c.buf("g_sv", al((n_surv + 1) * 4));
@@ -1144,11 +1165,11 @@ void build_graph_device(DevGraph& G, Ctx& c, int n, int dw, const double* h_pos,
   }
   DBuf& stmpc = c.buf("g_scantmpc", scan_temp_bytes(n_surv + 16));
   exclusive_scan<uint8_t>(skeep.as<uint8_t>(), cpos.as<int64_t>(), n_surv, stmpc.p, st, &c.launches);
-  int64_t n_cand = 0;
-  c.d2h(&n_cand, cpos.as<int64_t>() + n_surv, 8);
-  c.sync();
-  mark("connect");
-  G.n_cand = n_cand;
+  // the candidate count stays on the device (cpos[n_surv]); the candidate and
+  // edge arrays are sized by its bound n_surv, so no round trip until the
+  // waypoint count is needed
+  const int64_t n_cand = n_surv;  // bound
+  const int64_t* d_ncand = cpos.as<int64_t>() + n_surv;
   DBuf& cv = c.buf("g_cv", al((n_cand + 1) * 4));
   DBuf& cuu = c.buf("g_cuu", al((n_cand + 1) * 4));
   DBuf& ctau = c.buf("g_ctau2", al((n_cand + 1) * 8));
@@ -1175,18 +1196,16 @@ void build_graph_device(DevGraph& G, Ctx& c, int n, int dw, const double* h_pos,
       auto kern = w.n_obs <= 64 * kCullWords ? k_collide<DW, 0> : k_collide<DW, kCullList>;
       if (wsmem > 48 * 1024)
         PUMP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wsmem));
-      kern<<<grid_for(n_cand, 128), 128, wsmem, st>>>(ga, wd, n_cand, cv.as<int32_t>(), cuu.as<int32_t>(),
+      kern<<<grid_for(n_cand, 128), 128, wsmem, st>>>(ga, wd, d_ncand, cv.as<int32_t>(), cuu.as<int32_t>(),
                                                       ctau.as<double>(), valid.as<uint8_t>(), nst.as<int32_t>());
     });
     ++c.launches;
     PUMP_CUDA(cudaGetLastError());
   }
-  exclusive_scan<uint8_t>(valid.as<uint8_t>(), eoff.as<int64_t>(), n_cand, stmp2.p, st, &c.launches);
-  int64_t E = 0;
-  c.d2h(&E, eoff.as<int64_t>() + n_cand, 8);
-  c.sync();
-  mark("collide");
-  G.E = E;
+  exclusive_scan<uint8_t>(valid.as<uint8_t>(), eoff.as<int64_t>(), n_cand, stmp2.p, st, &c.launches, d_ncand);
+  int64_t E = n_cand;  // bound until the totals come back
+  DBuf& d_tot = c.buf("g_totals", 256);
+  int64_t* d_E = d_tot.as<int64_t>() + 4;
   G.e_from.ensure(al((E + 1) * 4));
   G.e_to.ensure(al((E + 1) * 4));
   G.e_cost.ensure(al((E + 1) * 8));
@@ -1199,9 +1218,9 @@ void build_graph_device(DevGraph& G, Ctx& c, int n, int dw, const double* h_pos,
   {
     KScope ks(st, F_EMIT);
     dispatch_dw(dw, [&]<int DW>() {
-      const int64_t items = std::max<int64_t>(n_cand, n + 1);
+      const int64_t items = std::max<int64_t>(n_cand + 1, n + 1);  // c == n_cand writes the edge count
       k_emit_edges<DW><<<grid_for(items, 256), 256, 0, st>>>(
-          ga, n_cand, coff.as<int64_t>(), cv.as<int32_t>(), cuu.as<int32_t>(), ctau.as<double>(), ccost.as<double>(),
+          ga, d_ncand, d_E, coff.as<int64_t>(), cv.as<int32_t>(), cuu.as<int32_t>(), ctau.as<double>(), ccost.as<double>(),
           valid.as<uint8_t>(), nst.as<int32_t>(), eoff.as<int64_t>(), G.e_from.as<int32_t>(), G.e_to.as<int32_t>(),
           G.e_cost.as<double>(), G.e_tau.as<double>(), G.e_acc0.as<double>(), G.e_jerk.as<double>(),
           G.e_nsteps.as<int32_t>(), G.row_ptr.as<int64_t>());
@@ -1209,7 +1228,15 @@ void build_graph_device(DevGraph& G, Ctx& c, int n, int dw, const double* h_pos,
     ++c.launches;
     PUMP_CUDA(cudaGetLastError());
   }
-  if (gather && c.world > 1) {
+  const bool multi = gather && c.world > 1;
+  if (multi) {  // the gather needs this rank's edge count on the host
+    int64_t nc = 0;
+    c.d2h(&nc, d_ncand, 8);
+    c.d2h(&E, d_E, 8);
+    c.sync();
+    G.n_cand = nc;
+  }
+  if (multi) {
     // ---- concatenate the ranks' row slices (graph sharded by source row)
     DBuf& cnts = c.buf("g_rank_edges", al(static_cast<size_t>(c.world) * 8 + 8));
     PUMP_CUDA(cudaMemsetAsync(cnts.p, 0, static_cast<size_t>(c.world) * 8, st));
@@ -1248,11 +1275,26 @@ void build_graph_device(DevGraph& G, Ctx& c, int n, int dw, const double* h_pos,
     mark("gather");
   }
   DBuf& stmp3 = c.buf("g_scantmp3", scan_temp_bytes(E + 16));
-  exclusive_scan<int32_t>(G.e_nsteps.as<int32_t>(), G.wp_off.as<int64_t>(), E, stmp3.p, st, &c.launches);
   int64_t NW = 0;
-  c.d2h(&NW, G.wp_off.as<int64_t>() + E, 8);
-  c.sync();
-  mark("emit + waypoint scan");
+  if (multi) {
+    exclusive_scan<int32_t>(G.e_nsteps.as<int32_t>(), G.wp_off.as<int64_t>(), E, stmp3.p, st, &c.launches);
+    c.d2h(&NW, G.wp_off.as<int64_t>() + E, 8);
+    c.sync();
+  } else {
+    // waypoint offsets over the device edge count, then candidate / edge /
+    // waypoint totals in one copy
+    exclusive_scan<int32_t>(G.e_nsteps.as<int32_t>(), G.wp_off.as<int64_t>(), E, stmp3.p, st, &c.launches, d_E);
+    k_graph_totals<<<1, 1, 0, st>>>(d_ncand, d_E, G.wp_off.as<int64_t>(), d_tot.as<int64_t>());
+    ++c.launches;
+    int64_t tot[3];
+    c.d2h(tot, d_tot.p, 24);
+    c.sync();
+    G.n_cand = tot[0];
+    E = tot[1];
+    NW = tot[2];
+    G.E = E;
+  }
+  mark("connect .. waypoint scan");
   G.NW = NW;
   DBuf& err = c.buf("g_err", 256);
   G.hs_off.ensure(al((NW + 2) * 8));
