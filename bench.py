@@ -191,6 +191,7 @@ def main():
     L.pump_ctx_io_bytes.argtypes = [C.c_void_p, C.c_void_p]
     L.pump_ctx_flush_l2.argtypes = [C.c_void_p]
     L.pump_peak_fp64.argtypes = [C.c_void_p, C.c_void_p]
+    L.pump_probe_round_latency.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p]
 
     text = load_text(args.config)
     scn = json.loads(text)
@@ -342,6 +343,8 @@ def main():
     # plus the same figures for every family with a work model
     peak = C.c_double()
     L.pump_peak_fp64(ctx.h, C.byref(peak))
+    us_bar, us_l2 = C.c_double(), C.c_double()
+    L.pump_probe_round_latency(ctx.h, C.byref(us_bar), C.byref(us_l2))
     hbm = None
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -350,6 +353,8 @@ def main():
         hbm = None
     d, dw = 2 * len(scn["workspace"]["bounds"]["lo"]), len(scn["workspace"]["bounds"]["lo"])
     n_obs = len(scn["workspace"]["obstacles"])
+
+    ROUND_TAIL_BARRIERS = 10  # grid_sync() calls in k_round_tail (explore.cu)
 
     def roofline_of(fam):
         name = FAMILIES[fam]
@@ -372,6 +377,16 @@ def main():
                       "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy bandwidth)"})
             work = prof_w[fam]
             r["work"] = f"{int(prof_w[fam])} algorithmic bytes (candidate records, arena writes, pool, group)"
+            # the bound that actually binds: the dependent grid-barrier chain
+            # (ROUND_TAIL_BARRIERS grid syncs per launch, each measured live
+            # on the round kernel's own grid shape)
+            avg_us = 1e3 * float(prof_ms[fam] / max(1, prof_n[fam]))
+            floor_us = ROUND_TAIL_BARRIERS * us_bar.value
+            r["latency_floor"] = {"barriers_per_launch": ROUND_TAIL_BARRIERS,
+                                  "us_per_grid_barrier": round(us_bar.value, 3),
+                                  "us_per_dependent_l2_load": round(us_l2.value, 4),
+                                  "floor_us_per_launch": round(floor_us, 2), "avg_launch_us": round(avg_us, 2),
+                                  "frac": round(floor_us / avg_us, 3) if avg_us > 0 else None}
         else:
             r["work"] = None
             r["achieved"] = None

@@ -169,6 +169,9 @@ int pump_ctx_io_bytes(pump_ctx* ctx, int64_t* out);
 int pump_ctx_flush_l2(pump_ctx* ctx);
 /* FP64 DMUL+DADD issue-rate microbenchmark, Gop/s (roofline denominator). */
 int pump_peak_fp64(pump_ctx* ctx, double* gops);
+/* Latency floor of the explore round: microseconds per grid barrier of the
+ * cooperative round kernel's grid, and per dependent L2-resident load. */
+int pump_probe_round_latency(pump_ctx* ctx, double* us_barrier, double* us_l2_load);
 
 /* ------------------------------------------------- host geometry queries */
 /* Single-call queries for the drop-in C++ headers; they run the same

@@ -62,7 +62,7 @@ EXPORTS = [
     "pump_explore_export", "pump_explore_free", "pump_run", "pump_result_summary_get", "pump_result_arrays",
     "pump_result_free", "pump_nccl_unique_id", "pump_ctx_set_comm", "pump_shard_range", "pump_ctx_profile",
     "pump_ctx_profile_read", "pump_ctx_io_bytes", "pump_ctx_flush_l2", "pump_peak_fp64", "pump_ctx_stream",
-    "pump_scenario_nodes", "pump_build_graph_rows", "pump_rrt_run",
+    "pump_scenario_nodes", "pump_build_graph_rows", "pump_rrt_run", "pump_probe_round_latency",
 ]
 
 

@@ -2215,4 +2215,8 @@ int pump_result_free(pump_result* r) {
   return PUMP_OK;
 }
 
+int pump_probe_round_latency(pump_ctx* ctx, double* us_barrier, double* us_l2_load) {
+  return guard([&] { pumpg::probe_round_latency(ctx->c, us_barrier, us_l2_load); });
+}
+
 }  // extern "C"

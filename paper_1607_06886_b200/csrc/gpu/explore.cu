@@ -1735,4 +1735,49 @@ void run_explore_device(DevExplore& X, Ctx& c, const DevGraph& G, const ExploreA
   X.removed = h.removed;
 }
 
+// Latency floor of the cooperative round: microseconds per grid barrier
+// (the kernel's own grid_sync, the round's grid) and per dependent L2 load
+// chain step, measured with the round kernel's launch shape.
+__global__ void __launch_bounds__(kCoopBlock, 2) k_probe_barrier(GridBar* bar, int iters) {
+  for (int k = 0; k < iters; ++k) grid_sync(bar);
+}
+__global__ void k_probe_chain(const int32_t* __restrict__ next, int steps, int32_t* __restrict__ out) {
+  int x = 0;
+  for (int k = 0; k < steps; ++k) x = next[x];
+  out[0] = x;
+}
+void probe_round_latency(Ctx& c, double* us_barrier, double* us_load) {
+  int per_sm = 0, sms = 0;
+  PUMP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, reinterpret_cast<const void*>(&k_probe_barrier),
+                                                          kCoopBlock, 0));
+  PUMP_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c.device));
+  const int blocks = std::min(per_sm, 1) * sms;  // the round kernel's grid (one block per SM)
+  DBuf& bar = c.buf("probe_bar", 256);
+  PUMP_CUDA(cudaMemsetAsync(bar.p, 0, 8, c.stream));
+  GridBar* b = bar.as<GridBar>();
+  int iters = 8;
+  void* args[] = {&b, &iters};
+  PUMP_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(&k_probe_barrier), dim3(blocks),
+                                        dim3(kCoopBlock), args, 0, c.stream));  // warm-up
+  iters = 2000;
+  c.tic();
+  PUMP_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(&k_probe_barrier), dim3(blocks),
+                                        dim3(kCoopBlock), args, 0, c.stream));
+  *us_barrier = c.toc() * 1e3 / iters;
+  // dependent loads over a 64 MiB permutation (L2-missing pointer chase would be
+  // HBM latency; 1 MiB stays L2-resident: the round's working set)
+  const int n = 1 << 18;  // 1 MiB of int32
+  std::vector<int32_t> h(n);
+  for (int k = 0; k < n; ++k) h[k] = static_cast<int32_t>((static_cast<int64_t>(k) * 40503 + 12345) % n);
+  DBuf& nx = c.buf("probe_next", n * 4 + 256);
+  DBuf& o = c.buf("probe_out", 256);
+  c.h2d(nx.p, h.data(), n * 4);
+  k_probe_chain<<<1, 1, 0, c.stream>>>(nx.as<int32_t>(), 1000, o.as<int32_t>());
+  const int steps = 20000;
+  c.tic();
+  k_probe_chain<<<1, 1, 0, c.stream>>>(nx.as<int32_t>(), steps, o.as<int32_t>());
+  *us_load = c.toc() * 1e3 / steps;
+  c.launches += 4;
+}
+
 }  // namespace pumpg

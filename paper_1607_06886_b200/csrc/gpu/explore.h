@@ -50,6 +50,8 @@ struct ExploreArgs {
 };
 
 void run_explore_device(DevExplore& X, Ctx& c, const DevGraph& G, const ExploreArgs& a);
+// microseconds per grid barrier of the round kernel's grid and per dependent L2 load
+void probe_round_latency(Ctx& c, double* us_barrier, double* us_load);
 
 }  // namespace pumpg
 
