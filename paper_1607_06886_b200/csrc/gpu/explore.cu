@@ -994,6 +994,8 @@ __global__ void __launch_bounds__(kCoopBlock, 2) k_round_tail(const CoopArgs A) 
   int64_t* s_run = csm.ms.run;
   __shared__ int64_t red[kCoopBlock / 32];
   __shared__ int64_t s_pre;
+  __shared__ int64_t s_big[kCoopBlock];
+  __shared__ int s_big_n;
   ExploreStatus* S = A.S;
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int64_t gtid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -1065,10 +1067,21 @@ __global__ void __launch_bounds__(kCoopBlock, 2) k_round_tail(const CoopArgs A) 
       if (A.mem_cnt[v] + A.new_cnt[v] <= kDomWarpCap) dom_node_warp(D, wsh[threadIdx.x >> 5], v, P0, lane);
     }
     __syncthreads();  // the block pass reuses the warps' shared memory
-    for (int64_t b = blockIdx.x; b < nt; b += nb) {
-      const int v = A.touched[b];
-      const bool big = A.mem_cnt[v] + A.new_cnt[v] > kDomWarpCap;  // block-uniform
-      if (big) dom_node(D, dsh, b, P0);
+    // this block's touched nodes (b = blockIdx.x + k * nb) are classified by
+    // all its threads at once and the big ones listed in shared memory: a
+    // serial scan paid two dependent L2 round trips per touched node
+    for (int64_t b0 = blockIdx.x; b0 < nt; b0 += static_cast<int64_t>(nb) * blockDim.x) {
+      if (threadIdx.x == 0) s_big_n = 0;
+      __syncthreads();
+      const int64_t b = b0 + static_cast<int64_t>(threadIdx.x) * nb;
+      if (b < nt) {
+        const int v = A.touched[b];
+        if (A.mem_cnt[v] + A.new_cnt[v] > kDomWarpCap) s_big[atomicAdd(&s_big_n, 1)] = b;
+      }
+      __syncthreads();
+      const int nbig = s_big_n;
+      for (int k = 0; k < nbig; ++k) dom_node(D, dsh, s_big[k], P0);  // nodes are independent: any order
+      __syncthreads();
     }
   }
   grid_sync(A.bar);
