@@ -878,6 +878,10 @@ __device__ __forceinline__ int64_t block_excl(int64_t v, int64_t* red, int64_t* 
 // epoch is this scan's), then sums predecessors back to the nearest
 // inclusive prefix.  The caller syncs the grid before reading out[] of
 // other blocks.  Returns the total on the last block only (others: -1).
+#ifndef PUMP_SCAN_DIRECT
+#define PUMP_SCAN_DIRECT 8192
+#endif
+constexpr int64_t kCoopScanDirect = PUMP_SCAN_DIRECT;  // scans up to this many items skip the look-back
 template <class Val, class Post>
 __device__ int64_t coop_scan(int64_t n, Val val, Post post, int64_t* out, unsigned long long* status, unsigned epoch,
                              int64_t* red, int64_t* s_pre) {
@@ -886,11 +890,26 @@ __device__ int64_t coop_scan(int64_t n, Val val, Post post, int64_t* out, unsign
   const int64_t nb = gridDim.x, b = blockIdx.x;
   const int64_t chunk = (n + nb - 1) / nb;
   const int64_t lo = min(n, b * chunk), hi = min(n, lo + chunk);
-  int64_t s = 0;
-  for (int64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) s += val(i, 0);
+  // small scans: every block sums its predecessors' items itself (one batch
+  // of independent loads) instead of waiting on the look-back chain
+  const bool direct = n <= kCoopScanDirect;
+  int64_t s = 0, pre_direct = 0;
+  if (direct) {
+    for (int64_t i = threadIdx.x; i < hi; i += blockDim.x) {
+      const int64_t v = val(i, 0);
+      if (i < lo) pre_direct += v;
+      else s += v;
+    }
+    pre_direct = block_sum(pre_direct, red);
+  } else {
+    for (int64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) s += val(i, 0);
+  }
   s = block_sum(s, red);
   volatile unsigned long long* vs = status;
-  if (threadIdx.x < 32) {
+  // (a direct scan still writes its entry: every scan tags every entry, so a
+  // stale entry can never carry the current epoch)
+  if (direct && threadIdx.x == 0) vs[b] = tag | kInc | static_cast<unsigned long long>(pre_direct + s);
+  if (!direct && threadIdx.x < 32) {
     const int lane = threadIdx.x;
     int64_t pre = 0;
     if (b == 0) {
@@ -916,7 +935,7 @@ __device__ int64_t coop_scan(int64_t n, Val val, Post post, int64_t* out, unsign
     if (lane == 0) *s_pre = pre;
   }
   __syncthreads();
-  int64_t pre = *s_pre;
+  int64_t pre = direct ? pre_direct : *s_pre;
   const int64_t total = pre + s;  // meaningful on the last block
   for (int64_t base = lo; base < hi; base += blockDim.x) {
     const int64_t i = base + threadIdx.x;
