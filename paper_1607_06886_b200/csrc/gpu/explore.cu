@@ -878,6 +878,9 @@ __device__ __forceinline__ int64_t block_excl(int64_t v, int64_t* red, int64_t* 
 // epoch is this scan's), then sums predecessors back to the nearest
 // inclusive prefix.  The caller syncs the grid before reading out[] of
 // other blocks.  Returns the total on the last block only (others: -1).
+#ifndef PUMP_SCAN_ALLAGG
+#define PUMP_SCAN_ALLAGG 1
+#endif
 #ifndef PUMP_SCAN_DIRECT
 #define PUMP_SCAN_DIRECT 8192
 #endif
@@ -909,6 +912,23 @@ __device__ int64_t coop_scan(int64_t n, Val val, Post post, int64_t* out, unsign
   // (a direct scan still writes its entry: every scan tags every entry, so a
   // stale entry can never carry the current epoch)
   if (direct && threadIdx.x == 0) vs[b] = tag | kInc | static_cast<unsigned long long>(pre_direct + s);
+#if PUMP_SCAN_ALLAGG
+  // all predecessors' aggregates at once, a thread per block (the grid is
+  // co-resident and about one block per SM, so one wave of polling loads
+  // replaces the look-back's chain of 32-wide windows)
+  int64_t pre_all = 0;
+  if (!direct) {
+    if (threadIdx.x == 0) vs[b] = tag | kAgg | static_cast<unsigned long long>(s);
+    int64_t acc = 0;
+    for (int64_t j = threadIdx.x; j < b; j += blockDim.x) {
+      unsigned long long w = vs[j];
+      while ((w & (0xffffull << 48)) != tag || (w & (3ull << 46)) == 0) w = vs[j];
+      acc += static_cast<int64_t>(w & kVal);
+    }
+    pre_all = block_sum(acc, red);
+  }
+#else
+  const int64_t pre_all = 0;
   if (!direct && threadIdx.x < 32) {
     const int lane = threadIdx.x;
     int64_t pre = 0;
@@ -934,8 +954,9 @@ __device__ int64_t coop_scan(int64_t n, Val val, Post post, int64_t* out, unsign
     }
     if (lane == 0) *s_pre = pre;
   }
+#endif
   __syncthreads();
-  int64_t pre = direct ? pre_direct : *s_pre;
+  int64_t pre = direct ? pre_direct : PUMP_SCAN_ALLAGG ? pre_all : *s_pre;
   const int64_t total = pre + s;  // meaningful on the last block
   for (int64_t base = lo; base < hi; base += blockDim.x) {
     const int64_t i = base + threadIdx.x;
