@@ -26,6 +26,7 @@
 #include <cstdint>
 #include <cstdlib>
 #include <deque>
+#include <exception>
 #include <fstream>
 #include <functional>
 #include <limits>
@@ -815,20 +816,11 @@ inline bool dominates(double dom_cost, double dom_cp, double cost, double cp) { 
 }
 }  // namespace detail
 
-// explore (planner.hpp:74-267): the wavefront runs on the GPU
-inline ExploreResult explore(const SampleGraph& g, const DeviationBank& bank, const ExploreParams& params,
-                             const RoundHook& hook = nullptr) {
-  if (hook) throw std::logic_error("explore: RoundHook is not supported by the device wavefront");
-  detail::ensure_bank(bank);
-  detail::GraphArrays ga = detail::from_graph(g);
-  detail::GraphHandle gh;
-  detail::check(pump_graph_upload(detail::ctx(), &ga.v, &gh.h));
-  pump_explore_params p{params.alpha_min, params.alpha_max, params.lambda, params.r_n};
-  pump_explore* eh = nullptr;
-  detail::check(pump_explore_run(detail::ctx(), gh.h, &p, &eh));
-  std::unique_ptr<pump_explore, int (*)(pump_explore*)> guard(eh, pump_explore_free);
+namespace detail {
+// an explore handle's state as the reference's ExploreResult
+inline ExploreResult materialize(const pump_explore* eh, int n_particles) {
   pump_explore_view v{};
-  detail::check(pump_explore_counts(eh, &v));
+  check(pump_explore_counts(eh, &v));
   std::vector<int32_t> head(v.n_plans + 1), parent(v.n_plans + 1), t_end(v.n_plans + 1), pids(v.n_pareto + 1),
       goal(v.n_goal_plans + 1);
   std::vector<double> cost(v.n_plans + 1), cp(v.n_plans + 1);
@@ -843,11 +835,11 @@ inline ExploreResult explore(const SampleGraph& g, const DeviationBank& bank, co
   v.pareto_ptr = pptr.data();
   v.pareto_ids = pids.data();
   v.goal_plans = goal.data();
-  detail::check(pump_explore_export(eh, &v));
+  check(pump_explore_export(eh, &v));
   ExploreResult r;
   for (int64_t i = 0; i < v.n_plans; ++i) {
     PlanRec p2{head[i], parent[i], cost[i], cp[i], t_end[i], {}};
-    p2.mask.n = bank.n_particles;
+    p2.mask.n = n_particles;
     p2.mask.words.assign(masks.begin() + i * v.n_words, masks.begin() + (i + 1) * v.n_words);
     r.plans.push_back(std::move(p2));
   }
@@ -857,6 +849,50 @@ inline ExploreResult explore(const SampleGraph& g, const DeviationBank& bank, co
   r.stats = {v.partial_plans, v.rounds, v.discarded_cp, v.removed_dominated, v.discarded_horizon,
              v.termination ? "frontier_exhausted" : "goal_below_alpha_min"};
   return r;
+}
+
+struct HookCall {
+  const RoundHook* hook;
+  int n_particles;
+  std::exception_ptr err;
+};
+inline int hook_trampoline(void* user, int32_t round, const pump_explore* state, const int32_t* expanded,
+                           int64_t n_expanded) {
+  auto* hc = static_cast<HookCall*>(user);
+  try {
+    ExploreResult st = materialize(state, hc->n_particles);
+    st.stats.termination.clear();  // not decided yet when the reference's hook runs
+    const std::vector<int> grp(expanded, expanded + n_expanded);
+    (*hc->hook)(round, st, grp);
+    return 0;
+  } catch (...) {
+    hc->err = std::current_exception();
+    return 1;
+  }
+}
+}  // namespace detail
+
+// explore (planner.hpp:74-267): the wavefront runs on the GPU.  With a
+// RoundHook the rounds run one at a time and the hook sees the state after
+// every round (planner.hpp:245), materialized on the host.
+inline ExploreResult explore(const SampleGraph& g, const DeviationBank& bank, const ExploreParams& params,
+                             const RoundHook& hook = nullptr) {
+  detail::ensure_bank(bank);
+  detail::GraphArrays ga = detail::from_graph(g);
+  detail::GraphHandle gh;
+  detail::check(pump_graph_upload(detail::ctx(), &ga.v, &gh.h));
+  pump_explore_params p{params.alpha_min, params.alpha_max, params.lambda, params.r_n};
+  pump_explore* eh = nullptr;
+  if (hook) {
+    detail::HookCall hc{&hook, bank.n_particles, nullptr};
+    const int rc = pump_explore_run_hooked(detail::ctx(), gh.h, &p, detail::hook_trampoline, &hc, &eh);
+    if (hc.err) std::rethrow_exception(hc.err);
+    detail::check(rc);
+  } else {
+    detail::check(pump_explore_run(detail::ctx(), gh.h, &p, &eh));
+  }
+  std::unique_ptr<pump_explore, int (*)(pump_explore*)> guard(eh, pump_explore_free);
+  return detail::materialize(eh, bank.n_particles);
 }
 
 inline std::vector<int> plan_path(const ExploreResult& res, int plan_id) {  // planner.hpp:270-276
@@ -1139,9 +1175,13 @@ struct ModelBundle {
   GainSchedule gains;
   ClosedLoopDynamics cl;
 };
-inline ModelBundle build_models(const Scenario& s) {  // scenario.hpp:285-301
-  pumpb::Scenario b = pumpb::parse_scenario(detail::to_json(s));
-  pumpb::ModelBundle m = b.models();
+// scenario.hpp:285-301: assembles the matrices from whatever fields the caller
+// set (code-built Scenarios with empty start/goal are fine); no re-validation
+inline ModelBundle build_models(const Scenario& s) {
+  pumpb::LqgWeights lw{detail::to_la(s.tracking.Q), detail::to_la(s.tracking.R), detail::to_la(s.tracking.F)};
+  pumpb::ModelBundle m = pumpb::build_models(static_cast<int>(s.workspace.bounds.lo.size()), s.dt,
+                                             detail::to_la(s.process_noise), detail::to_la(s.measurement_noise),
+                                             detail::to_la(s.initial_covariance), lw);
   ModelBundle o;
   o.cm = {detail::from_la(m.cm.A), detail::from_la(m.cm.B), detail::from_la(m.cm.C), detail::from_la(m.cm.V),
           detail::from_la(m.cm.W)};

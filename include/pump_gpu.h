@@ -36,7 +36,8 @@ enum {
   PUMP_E_SCENARIO = 4,         /* pump::ScenarioError     (scenario.hpp:18-20) */
   PUMP_E_CUDA = 5,             /* device / driver failure (no reference analogue) */
   PUMP_E_CAPACITY = 6,         /* caller buffer or device arena too small */
-  PUMP_E_LOGIC = 7             /* std::logic_error        (planner.hpp:303) */
+  PUMP_E_LOGIC = 7,            /* std::logic_error        (planner.hpp:303) */
+  PUMP_E_HOOK = 8              /* a round hook asked to stop (pump_explore_run_hooked) */
 };
 
 /* Message of the last failing call on this thread ("" if none). */
@@ -294,6 +295,17 @@ int pump_graph_free(pump_graph* g);
 /* ----------------------------------------------------- explore (K_hsmc..) */
 /* explore (planner.hpp:74-267) on the ctx bank; wavefront on one GPU. */
 int pump_explore_run(pump_ctx* ctx, const pump_graph* g, const pump_explore_params* p, pump_explore** out);
+/* RoundHook (planner.hpp:51-52, 245): explore with an observer called after
+ * every round (rounds then run one at a time, unpipelined).  `state` is the
+ * exploration so far: pump_explore_counts / pump_explore_export on it return
+ * the arena, the per-node Pareto sets and the statistics as the reference's
+ * hook sees them (goal_plans empty until the run ends); `expanded` lists the
+ * group the round expanded.  A nonzero return stops the run with
+ * PUMP_E_HOOK (the C++ drop-in rethrows the hook's own exception). */
+typedef int (*pump_round_hook)(void* user, int32_t round, const pump_explore* state, const int32_t* expanded,
+                               int64_t n_expanded);
+int pump_explore_run_hooked(pump_ctx* ctx, const pump_graph* g, const pump_explore_params* p, pump_round_hook hook,
+                            void* user, pump_explore** out);
 int pump_explore_counts(const pump_explore* e, pump_explore_view* view);
 int pump_explore_export(const pump_explore* e, pump_explore_view* view);
 int pump_explore_free(pump_explore* e);

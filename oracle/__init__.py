@@ -360,6 +360,39 @@ def explore_invariants(graph: Graph, bank, alpha_min, alpha_max, lam, r_n):
     return dict(zip(["dominance", "double_expansions", "cp", "rounds"], counts.tolist()))
 
 
+def explore_trace(graph: Graph, bank, alpha_min, alpha_max, lam, r_n) -> list[dict]:
+    """The reference RoundHook's view after every round (planner.hpp:245):
+    round, expanded ids, arena size, statistics and every node's Pareto set."""
+    bank = np.ascontiguousarray(bank, dtype=np.float64)
+    p = _params(alpha_min, alpha_max, lam, r_n)
+    L = lib()
+    L.oracle_explore_trace.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p,
+                                       C.c_int64, C.c_void_p]
+    n = C.c_int64()
+    args = (graph.h, bank.shape[1], bank.shape[0] - 1, bank.shape[2], _p(bank), C.byref(p))
+    _check(L.oracle_explore_trace(*args, None, 0, C.byref(n)))
+    buf = np.zeros(max(1, n.value), dtype=np.int64)
+    _check(L.oracle_explore_trace(*args, _p(buf), n.value, C.byref(n)))
+    out, k = [], 0
+    while k < n.value:
+        rnd, ne = int(buf[k]), int(buf[k + 1])
+        k += 2
+        exp = buf[k:k + ne].copy()
+        k += ne
+        n_plans, pp, dcp, rem, dh, nn = (int(x) for x in buf[k:k + 6])
+        k += 6
+        sizes = buf[k:k + nn]
+        k += nn
+        tot = int(sizes.sum())
+        ids = buf[k:k + tot].copy()
+        k += tot
+        ptr = np.zeros(nn + 1, dtype=np.int64)
+        ptr[1:] = np.cumsum(sizes)
+        out.append({"round": rnd, "expanded": exp, "n_plans": n_plans, "partial_plans": pp, "discarded_cp": dcp,
+                    "removed_dominated": rem, "discarded_horizon": dh, "pareto_ptr": ptr, "pareto_ids": ids})
+    return out
+
+
 # ---------------------------------------------------------------- pipeline
 def scenario_nodes(json_text: str):
     n = C.c_int()

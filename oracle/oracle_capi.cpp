@@ -444,6 +444,43 @@ int oracle_explore_invariants(void* gh, int n, int horizon, int dw, const double
   });
 }
 
+// The reference's RoundHook view of every round (planner.hpp:245), flattened
+// for the GPU hook parity test: per round [round, n_expanded, expanded...,
+// n_plans, partial_plans, discarded_cp, removed_dominated, discarded_horizon,
+// n_nodes, |pareto[v]|..., pareto ids...].  *len = items written (or needed).
+int oracle_explore_trace(void* gh, int n, int horizon, int dw, const double* dy, const pump_explore_params* p,
+                         int64_t* out, int64_t cap, int64_t* len) {
+  return guard([&] {
+    Bank bank = bank_from(n, horizon, dw, dy);
+    ExParams ep;
+    ep.alpha_min = p->alpha_min;
+    ep.alpha_max = p->alpha_max;
+    ep.lambda = p->lambda;
+    ep.r_n = p->r_n;
+    int64_t k = 0;
+    auto put = [&](int64_t x) {
+      if (k < cap) out[k] = x;
+      ++k;
+    };
+    Hook hook = [&](int round, const ExResult& st, const std::vector<int>& expanded) {
+      put(round);
+      put(static_cast<int64_t>(expanded.size()));
+      for (int id : expanded) put(id);
+      put(static_cast<int64_t>(st.plans.size()));
+      put(st.partial_plans);
+      put(st.discarded_cp);
+      put(st.removed_dominated);
+      put(st.discarded_horizon);
+      put(static_cast<int64_t>(st.pareto.size()));
+      for (const auto& set : st.pareto) put(static_cast<int64_t>(set.size()));
+      for (const auto& set : st.pareto)
+        for (int id : set) put(id);
+    };
+    explore(static_cast<OGraph*>(gh)->g, bank, ep, hook);
+    *len = k;
+  });
+}
+
 int oracle_explore_counts(void* h, pump_explore_view* v) {
   const ExResult& r = static_cast<OExplore*>(h)->r;
   v->n_plans = static_cast<int64_t>(r.plans.size());

@@ -19,6 +19,7 @@ PUMP_E_SCENARIO = 4
 PUMP_E_CUDA = 5
 PUMP_E_CAPACITY = 6
 PUMP_E_LOGIC = 7
+PUMP_E_HOOK = 8
 
 _dp = C.POINTER(C.c_double)
 _i32p = C.POINTER(C.c_int32)

@@ -50,14 +50,15 @@ class LibraryMissing(ImportError):
 
 _EXC = {A.PUMP_E_INVALID_ARGUMENT: ValueError, A.PUMP_E_OUT_OF_RANGE: IndexError,
         A.PUMP_E_RUNTIME: RuntimeError, A.PUMP_E_SCENARIO: ScenarioError, A.PUMP_E_CUDA: PumpCudaError,
-        A.PUMP_E_CAPACITY: CapacityError, A.PUMP_E_LOGIC: RuntimeError}
+        A.PUMP_E_CAPACITY: CapacityError, A.PUMP_E_LOGIC: RuntimeError,
+        A.PUMP_E_HOOK: RuntimeError}
 
 # every symbol include/pump_gpu.h declares (checked by tests/test_abi.py)
 EXPORTS = [
     "pump_last_error", "pump_abi_version", "pump_ctx_create", "pump_ctx_destroy", "pump_ctx_last_kernel_ms",
     "pump_ctx_launch_count", "pump_scenario_parse", "pump_scenario_load", "pump_scenario_free",
     "pump_scenario_closed_loop", "pump_scenario_params", "pump_presample_bank", "pump_bank_upload",
-    "pump_hsmc_extend_batch", "pump_mc_certify_batch", "pump_mc_certify", "pump_build_graph", "pump_graph_upload",
+    "pump_hsmc_extend_batch", "pump_explore_run_hooked", "pump_mc_certify_batch", "pump_mc_certify", "pump_build_graph", "pump_graph_upload",
     "pump_graph_counts", "pump_graph_export", "pump_graph_free", "pump_explore_run", "pump_explore_counts",
     "pump_explore_export", "pump_explore_free", "pump_run", "pump_result_summary_get", "pump_result_arrays",
     "pump_result_free", "pump_nccl_unique_id", "pump_ctx_set_comm", "pump_shard_range", "pump_ctx_profile",
@@ -418,22 +419,59 @@ def graph_upload(g: dict, ctx: Context | None = None) -> Graph:
 
 
 # ------------------------------------------------------------------ explore
+ROUND_HOOK = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_int32, C.c_void_p, C.POINTER(C.c_int32), C.c_int64)
+
+
+def _explore_state(h, masks: bool) -> dict:
+    v = A.ExploreViewC()
+    _check(lib().pump_explore_counts(h, C.byref(v)))
+    out = A.export_view(v, A.EXPLORE_ARRAYS, lambda hh, pv: lib().pump_explore_export(hh, pv), h,
+                        skip=() if masks else ("masks",))
+    out["termination"] = A.TERMINATION[out["termination"]]
+    return out
+
+
 def explore(graph: Graph, alpha_min: float, alpha_max: float, lam: float, r_n: float,
-            ctx: Context | None = None, masks: bool = True) -> dict:
-    """explore (planner.hpp:74-267) on the context's resident bank."""
+            ctx: Context | None = None, masks: bool = True, hook=None) -> dict:
+    """explore (planner.hpp:74-267) on the context's resident bank.
+
+    hook(round, state, expanded) is the reference's RoundHook
+    (planner.hpp:51-52, 245): called after every round with the exploration
+    state so far (the same dict this function returns, goal_plans empty) and
+    the ids the round expanded; rounds then run one at a time.  An exception
+    raised by the hook stops the run and is re-raised here."""
     ctx = ctx or graph.ctx
     p = A.ExploreParamsC()
     p.alpha_min, p.alpha_max, p.lambda_, p.r_n = alpha_min, alpha_max, lam, r_n
     h = C.c_void_p()
-    _check(lib().pump_explore_run(ctx.h, graph.h, C.byref(p), C.byref(h)))
+    if hook is None:
+        _check(lib().pump_explore_run(ctx.h, graph.h, C.byref(p), C.byref(h)))
+    else:
+        err = []
+
+        def tramp(_user, rnd, state, expanded, n_exp):
+            try:
+                st = _explore_state(state, masks)
+                st["termination"] = ""
+                hook(int(rnd), st, np.ctypeslib.as_array(expanded, (int(n_exp),)).copy() if n_exp else
+                     np.zeros(0, np.int32))
+                return 0
+            except BaseException as e:  # noqa: BLE001 - re-raised after the run stops
+                err.append(e)
+                return 1
+
+        cb = ROUND_HOOK(tramp)
+        L = lib()
+        L.pump_explore_run_hooked.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, ROUND_HOOK, C.c_void_p,
+                                              C.c_void_p]
+        rc = L.pump_explore_run_hooked(ctx.h, graph.h, C.byref(p), cb, None, C.byref(h))
+        if err:
+            raise err[0]
+        _check(rc)
     try:
-        v = A.ExploreViewC()
-        _check(lib().pump_explore_counts(h, C.byref(v)))
-        out = A.export_view(v, A.EXPLORE_ARRAYS, lambda hh, pv: lib().pump_explore_export(hh, pv), h,
-                            skip=() if masks else ("masks",))
+        out = _explore_state(h, masks)
     finally:
         lib().pump_explore_free(h)
-    out["termination"] = A.TERMINATION[out["termination"]]
     return out
 
 

@@ -990,7 +990,7 @@ static void run_pump_device(Ctx& c, const pumpb::Scenario& s, const DevGraph* pr
   ea.on_round = [&](const ExploreStatus& h) {
     if (h.max_goal_tend <= 0) return;
     const int want = static_cast<int>(std::min<int64_t>(s.bank_horizon, h.max_goal_tend));
-    if (c.mc_table.valid && want <= c.mc_table.t_done) return;
+    if (mc_table_covers(c.mc_table, L, mr0, mr1, s.seeds.mc, want)) return;
     if (!side_forked) {
       PUMP_CUDA(cudaEventRecord(c.fork, c.stream));
       PUMP_CUDA(cudaStreamWaitEvent(c.side, c.fork, 0));
@@ -2094,6 +2094,39 @@ int pump_explore_run(pump_ctx* ctx, const pump_graph* g, const pump_explore_para
     }
     *out = e;
   });
+}
+
+namespace {
+struct HookStop {};
+}  // namespace
+
+int pump_explore_run_hooked(pump_ctx* ctx, const pump_graph* g, const pump_explore_params* p, pump_round_hook hook,
+                            void* user, pump_explore** out) {
+  int rc = PUMP_OK;
+  const int st = guard([&] {
+    auto* e = new pump_explore;
+    try {
+      e->owner = ctx;  // goal_nodes stay empty during the rounds (goal_plans are collected at the end)
+      ExploreArgs a{p->alpha_min, p->alpha_max, p->lambda, p->r_n};
+      if (hook)
+        a.on_round_state = [&](int round, const std::vector<int32_t>& grp) {
+          if (hook(user, round, e, grp.data(), static_cast<int64_t>(grp.size())) != 0) throw HookStop{};
+        };
+      try {
+        run_explore_device(e->x, ctx->c, g->g, a);
+      } catch (const HookStop&) {
+        rc = PUMP_E_HOOK;
+        delete e;
+        return;
+      }
+      e->goal_nodes = g->g.goal_nodes;
+    } catch (...) {
+      delete e;
+      throw;
+    }
+    *out = e;
+  });
+  return st != PUMP_OK ? st : rc;
 }
 
 int pump_explore_counts(const pump_explore* e, pump_explore_view* v) {

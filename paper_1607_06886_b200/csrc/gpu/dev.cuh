@@ -893,6 +893,121 @@ __device__ __forceinline__ int convex_region_fused(const WorldD& ws, const doubl
   return count;
 }
 
+// convex_region for any number of boxes (<= 32 * kW) with no per-box storage:
+// the fused scheme above (one pass per iteration over the still-unpruned
+// boxes, ascending, pruning with the half-space of this iteration and
+// tracking the first strict minimum of |clamp(y) - y|^2 among the boxes that
+// survive it), with the squared distance recomputed on the fly instead of
+// kept, so forests of hundreds of boxes need neither shared memory per
+// waypoint nor a pass over pruned boxes.  Each iteration prunes at least one
+// box (else -1, the reference's no-progress throw), so the reference's
+// n_obs-iteration cap never binds before every box is pruned.  Output
+// identical to convex_region (the same distance and prune expressions; the
+// minimizing-corner choice is the one convex_region_fused documents).
+template <int DW>
+__host__ __device__ __forceinline__ double clamp_sq(const WorldD& ws, int o, const double* y) {
+  double cand[DW];
+#pragma unroll
+  for (int k = 0; k < DW; ++k) {
+    double c = y[k] < ws.lo[o * DW + k] ? ws.lo[o * DW + k] : y[k];
+    c = ws.hi[o * DW + k] < c ? ws.hi[o * DW + k] : c;
+    cand[k] = c - y[k];
+  }
+  return sqnorm<DW>(cand);
+}
+
+template <int DW, int kW>
+__device__ __forceinline__ int convex_region_scan(const WorldD& ws, const double* y, const double* yd, double* a_out,
+                                                  double* b_out, uint8_t* fb_out, int a_stride, int b_stride,
+                                                  int out_cap) {
+  int best = -1;
+  double best_sq = __builtin_inf();
+  for (int o = 0; o < ws.n_obs; ++o) {
+    const double q = clamp_sq<DW>(ws, o, y);
+    if (q < best_sq) {
+      best_sq = q;
+      best = o;
+    }
+  }
+  uint32_t pruned[kW];
+#pragma unroll
+  for (int q = 0; q < kW; ++q) {
+    const int lo = 32 * q;
+    pruned[q] = ws.n_obs <= lo ? ~0u : (ws.n_obs >= lo + 32 ? 0u : ~((1u << (ws.n_obs - lo)) - 1u));
+  }
+  int count = 0;
+  while (best >= 0) {
+    double d[DW];
+#pragma unroll
+    for (int k = 0; k < DW; ++k) {
+      double c = y[k] < ws.lo[best * DW + k] ? ws.lo[best * DW + k] : y[k];
+      c = ws.hi[best * DW + k] < c ? ws.hi[best * DW + k] : c;
+      d[k] = c - y[k];
+    }
+    const double dd = sqnorm<DW>(d);
+    const double lim = dd - 1e-12 * (1.0 + dd);
+    bool any = false;
+    int nb = -1;
+    double nsq = __builtin_inf();
+    const double* cp[DW];
+#pragma unroll
+    for (int k = 0; k < DW; ++k) cp[k] = (d[k] >= 0 ? ws.lo : ws.hi) + k;
+    auto word = [&](int q) {
+      for (uint32_t rest = ~pruned[q]; rest; rest &= rest - 1) {
+        const int o = 32 * q + __builtin_ctzll_hd(rest);
+        double dot = 0;
+#pragma unroll
+        for (int k = 0; k < DW; ++k) dot += d[k] * (cp[k][o * DW] - y[k]);
+        if (!(dot < lim)) {
+          pruned[q] |= 1u << (o & 31);
+          any = true;
+        } else {
+          const double sq = clamp_sq<DW>(ws, o, y);
+          if (sq < nsq) {
+            nsq = sq;
+            nb = o;
+          }
+        }
+      }
+    };
+    if constexpr (kW <= 8) {  // words in registers
+#pragma unroll
+      for (int q = 0; q < kW; ++q) word(q);
+    } else {
+      const int nw = (ws.n_obs + 31) / 32;
+      for (int q = 0; q < nw; ++q) word(q);
+    }
+    if (!any) return -1;
+    if (count < out_cap) {
+      double a[DW];
+      bool fb = false;
+      const double vn = sqrt(sqnorm<DW>(yd));
+      if (vn < 1e-6) {
+        fb = true;
+      } else {
+        double dy = 0.0;
+#pragma unroll
+        for (int k = 0; k < DW; ++k) dy = dy + d[k] * yd[k];
+        const double coef = dy / sqnorm<DW>(yd);
+#pragma unroll
+        for (int k = 0; k < DW; ++k) a[k] = d[k] - coef * yd[k];
+        if (sqrt(sqnorm<DW>(a)) < 1e-6 * sqrt(sqnorm<DW>(d))) fb = true;
+      }
+      if (fb) {
+#pragma unroll
+        for (int k = 0; k < DW; ++k) a[k] = d[k];
+      }
+#pragma unroll
+      for (int k = 0; k < DW; ++k) a_out[count * a_stride + k] = a[k];
+      b_out[count * b_stride] = sqnorm<DW>(a);
+      fb_out[count] = fb ? 1 : 0;
+    }
+    ++count;
+    best = nb;
+  }
+  return count;
+}
+
 // obstacle boxes staged in shared memory (block-wide; returns the view on them)
 template <int DW>
 __device__ __forceinline__ WorldD stage_world(const WorldD& w, double* smem) {

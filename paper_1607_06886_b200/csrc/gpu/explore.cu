@@ -86,10 +86,10 @@ __device__ __forceinline__ void hs_test(const double2 q0, const double2 q1, cons
 }
 
 template <int DW, int CH>
-__device__ __forceinline__ void load_row(const double* row, int N, int lane, double (&p)[CH][DW]) {
+__device__ __forceinline__ void load_row(const double* row, int N, int lane, double (&p)[CH][DW], int pb = 0) {
 #pragma unroll
   for (int c = 0; c < CH; ++c) {
-    const int i = c * 32 + lane;
+    const int i = pb + c * 32 + lane;
 #pragma unroll
     for (int k = 0; k < DW; ++k) p[c][k] = (i < N) ? row[i * DW + k] : 0.0;
   }
@@ -127,9 +127,6 @@ __device__ __forceinline__ void expand_task(const ExpandArgs& a, int64_t task, i
     }
     return;
   }
-  bool kill[CH];
-#pragma unroll
-  for (int c = 0; c < CH; ++c) kill[c] = false;
   const int64_t w0 = a.wp_off[e];
   const double2* hpk = reinterpret_cast<const double2*>(a.hs_pk);
   int64_t tests = 0;
@@ -147,6 +144,16 @@ __device__ __forceinline__ void expand_task(const ExpandArgs& a, int64_t task, i
     if (lane >= o) incl += y;
   }
   const int total = __shfl_sync(0xffffffffu, incl, 31);
+  // particles are independent (survival is an AND of per-particle tests), so
+  // plans of more than 32 * CH particles run the same steps slab by slab
+  constexpr int kSlab = 32 * CH;
+  const int n_slab = (a.N + kSlab - 1) / kSlab;
+  int pop = 0;
+  for (int slab = 0; slab < n_slab; ++slab) {
+  const int pb = slab * kSlab;
+  bool kill[CH];
+#pragma unroll
+  for (int c = 0; c < CH; ++c) kill[c] = false;
   if (ns <= 32 && total <= kExpStage) {
     const int my_pre = incl - my_cnt;
     // Each lane stages its waypoint's half-spaces and decides which of them
@@ -182,16 +189,18 @@ __device__ __forceinline__ void expand_task(const ExpandArgs& a, int64_t task, i
     }
     __syncwarp();
     unsigned live = __ballot_sync(0xffffffffu, my_need != 0);  // waypoints whose row can lose a particle
-    tests = __popcll(my_need);
+    if (slab == 0) {
+      tests = __popcll(my_need);
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) tests += __shfl_xor_sync(0xffffffffu, tests, o);
+      for (int o = 16; o > 0; o >>= 1) tests += __shfl_xor_sync(0xffffffffu, tests, o);
+    }
     double p[CH][DW], pn[CH][DW];
     int j = live ? __ffs(live) - 1 : -1;
-    if (j >= 0) load_row<DW, CH>(a.dy + static_cast<int64_t>(pt + j + 1) * a.N * DW, a.N, lane, p);
+    if (j >= 0) load_row<DW, CH>(a.dy + static_cast<int64_t>(pt + j + 1) * a.N * DW, a.N, lane, p, pb);
     while (j >= 0) {
       live &= ~(1u << j);
       const int jn = live ? __ffs(live) - 1 : -1;
-      if (jn >= 0) load_row<DW, CH>(a.dy + static_cast<int64_t>(pt + jn + 1) * a.N * DW, a.N, lane, pn);
+      if (jn >= 0) load_row<DW, CH>(a.dy + static_cast<int64_t>(pt + jn + 1) * a.N * DW, a.N, lane, pn, pb);
       const int cnt = __shfl_sync(0xffffffffu, my_cnt, j);
       const int pre = __shfl_sync(0xffffffffu, incl, j) - cnt;
       const uint64_t need = __shfl_sync(0xffffffffu, my_need, j);
@@ -250,14 +259,14 @@ __device__ __forceinline__ void expand_task(const ExpandArgs& a, int64_t task, i
       int64_t t_l = all ? cnt : __popcll(need);
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) t_l += __shfl_xor_sync(0xffffffffu, t_l, o);
-      tests += t_l;
+      if (slab == 0) tests += t_l;
       double p[CH][DW], pn[CH][DW];
       int j = live ? __ffs(live) - 1 : -1;
-      if (j >= 0) load_row<DW, CH>(a.dy + static_cast<int64_t>(pt + jb + j + 1) * a.N * DW, a.N, lane, p);
+      if (j >= 0) load_row<DW, CH>(a.dy + static_cast<int64_t>(pt + jb + j + 1) * a.N * DW, a.N, lane, p, pb);
       while (j >= 0) {
         live &= ~(1u << j);
         const int jn = live ? __ffs(live) - 1 : -1;
-        if (jn >= 0) load_row<DW, CH>(a.dy + static_cast<int64_t>(pt + jb + jn + 1) * a.N * DW, a.N, lane, pn);
+        if (jn >= 0) load_row<DW, CH>(a.dy + static_cast<int64_t>(pt + jb + jn + 1) * a.N * DW, a.N, lane, pn, pb);
         const int64_t hj = __shfl_sync(0xffffffffu, h0, j);
         const int cj = __shfl_sync(0xffffffffu, cnt, j);
         const uint64_t nj = __shfl_sync(0xffffffffu, need, j);
@@ -274,18 +283,19 @@ __device__ __forceinline__ void expand_task(const ExpandArgs& a, int64_t task, i
       }
     }
   }
-  if (lane == 0) atomicAdd(reinterpret_cast<unsigned long long*>(&a.st->hs_tests), static_cast<unsigned long long>(tests));
-  int pop = 0;
 #pragma unroll
   for (int w = 0; w < (CH + 1) / 2; ++w) {
     const unsigned lo32 = __ballot_sync(0xffffffffu, kill[2 * w]);
     const unsigned hi32 = (2 * w + 1 < CH) ? __ballot_sync(0xffffffffu, kill[2 * w + 1]) : 0u;
-    if (w < a.W) {
-      const uint64_t m = a.mask[static_cast<int64_t>(pid) * a.W + w] & ~((static_cast<uint64_t>(hi32) << 32) | lo32);
+    const int gw = slab * (kSlab / 64) + w;
+    if (gw < a.W) {
+      const uint64_t m = a.mask[static_cast<int64_t>(pid) * a.W + gw] & ~((static_cast<uint64_t>(hi32) << 32) | lo32);
       pop += __popcll(m);
-      if (lane == 0) a.c_mask[task * a.W + w] = m;
+      if (lane == 0) a.c_mask[task * a.W + gw] = m;
     }
   }
+  }  // slab
+  if (lane == 0) atomicAdd(reinterpret_cast<unsigned long long*>(&a.st->hs_tests), static_cast<unsigned long long>(tests));
   if (lane == 0) {
     const double cp = 1.0 - static_cast<double>(pop) / a.N;  // ParticleMask::cp (cp.hpp:42)
     a.c_cp[task] = cp;
@@ -637,11 +647,7 @@ __device__ void dom_node_warp(const DomArgs& A, DomWarpShared& sh, int v, int64_
   n_ev_open = __reduce_add_sync(0xffffffffu, n_ev_open);
   n_new_surv = __reduce_add_sync(0xffffffffu, n_new_surv);
   if (lane == 0) {
-    // new_cnt first: the block pass (k_round_tail) reads mem_cnt + new_cnt of
-    // every touched node concurrently to pick the big ones; with this order it
-    // never sees a sum above the node's original size
     A.new_cnt[v] = 0;
-    __threadfence();
     A.mem_cnt[v] = w + static_cast<int>(n_new_surv);
     atomicAdd(reinterpret_cast<unsigned long long*>(&A.stw->removed), static_cast<unsigned long long>(n_drop + n_ev));
     atomicAdd(reinterpret_cast<unsigned long long*>(&A.stw->evicted_open), static_cast<unsigned long long>(n_ev_open));
@@ -1104,7 +1110,9 @@ __global__ void __launch_bounds__(kCoopBlock, 2) k_round_tail(const CoopArgs A) 
     // small nodes: a warp each; then nodes over kDomWarpCap: a block each
     for (int64_t b = gwarp; b < nt; b += gwarps) {
       const int v = A.touched[b];
-      if (A.mem_cnt[v] + A.new_cnt[v] <= kDomWarpCap) dom_node_warp(D, wsh[threadIdx.x >> 5], v, P0, lane);
+      // classify by the pre-removal size off2[v+1] - off2[v]: it does not
+      // change during this phase (mem_cnt / new_cnt of other warps' nodes do)
+      if (A.off2[v + 1] - A.off2[v] <= kDomWarpCap) dom_node_warp(D, wsh[threadIdx.x >> 5], v, P0, lane);
     }
     __syncthreads();  // the block pass reuses the warps' shared memory
     // this block's touched nodes (b = blockIdx.x + k * nb) are classified by
@@ -1116,7 +1124,7 @@ __global__ void __launch_bounds__(kCoopBlock, 2) k_round_tail(const CoopArgs A) 
       const int64_t b = b0 + static_cast<int64_t>(threadIdx.x) * nb;
       if (b < nt) {
         const int v = A.touched[b];
-        if (A.mem_cnt[v] + A.new_cnt[v] > kDomWarpCap) s_big[atomicAdd(&s_big_n, 1)] = b;
+        if (A.off2[v + 1] - A.off2[v] > kDomWarpCap) s_big[atomicAdd(&s_big_n, 1)] = b;
       }
       __syncthreads();
       const int nbig = s_big_n;
@@ -1330,10 +1338,11 @@ void run_explore_device(DevExplore& X, Ctx& c, const DevGraph& G, const ExploreA
   X.n = n;
   X.N = N;
   X.W = W;
-  if (N > 512) throw std::invalid_argument("explore: at most 512 particles per plan");
+  // lanes hold CH chunks of 32 particles; above 512 particles a warp runs
+  // its task slab by slab (expand_task)
   const int ch = [&] {
     int q = (N + 31) / 32, p = 1;
-    while (p < q) p <<= 1;
+    while (p < q && p < 16) p <<= 1;
     return p;
   }();
   // particle box of every bank row (k_expand skips rows no half-space can cut)
@@ -1471,7 +1480,14 @@ void run_explore_device(DevExplore& X, Ctx& c, const DevGraph& G, const ExploreA
     }
     const int64_t Th = h.T;
     max_T = std::max<int64_t>(max_T, Th);
-    const bool pipe = coop_ok && kBatch > 1 && (!prm.on_round || prm.on_round_batched) && !force_sync;
+    const bool pipe = coop_ok && kBatch > 1 && (!prm.on_round || prm.on_round_batched) && !prm.on_round_state &&
+                      !force_sync;
+    std::vector<int32_t> expanded;  // (round hook) this round's group
+    if (prm.on_round_state) {
+      expanded.resize(h.G);
+      if (h.G > 0) c.d2h(expanded.data(), X.group.p, h.G * 4);
+      c.sync();
+    }
     force_sync = false;
     // buffer sizes: this round's T, or a per-round capacity for a batch
     const int64_t T = pipe ? std::max<int64_t>({Th, 2 * max_T, 4096}) : Th;
@@ -1777,6 +1793,12 @@ void run_explore_device(DevExplore& X, Ctx& c, const DevGraph& G, const ExploreA
                              (hp.pool_n + Kr) * 9 + h.G * 28;
     }
     if (prm.on_round) prm.on_round(h);
+    if (prm.on_round_state) {
+      X.disc_cp = h.disc_cp;
+      X.disc_hor = h.disc_hor;
+      X.removed = h.removed;
+      prm.on_round_state(X.rounds, expanded);
+    }
   }
   X.kernel_ms = c.toc();
   kprof_work(F_COMMIT, commit_bytes_legacy + h.commit_bytes);  // (the cooperative rounds count on the device)

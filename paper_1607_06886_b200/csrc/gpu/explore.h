@@ -2,6 +2,7 @@
 #pragma once
 
 #include <functional>
+#include <vector>
 
 #include "graph.h"
 
@@ -47,6 +48,10 @@ struct ExploreArgs {
   // the hook only needs the latest status, not every round's: pipelined
   // batches stay on and it runs once per status read
   bool on_round_batched = false;
+  // RoundHook (planner.hpp:51-52, 245): rounds run one at a time and, after
+  // each, the observer gets the round number and the group it expanded; the
+  // arena, member sets and statistics in the DevExplore are current then
+  std::function<void(int round, const std::vector<int32_t>& expanded)> on_round_state = nullptr;
 };
 
 void run_explore_device(DevExplore& X, Ctx& c, const DevGraph& G, const ExploreArgs& a);

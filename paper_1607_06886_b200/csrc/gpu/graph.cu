@@ -779,101 +779,18 @@ __global__ void k_emit_edges(GraphArgs g, const int64_t* __restrict__ d_ncand, i
   }
 }
 
-// Regions for larger obstacle sets, in two launches without recomputation:
-// MOVE = false computes every waypoint's half-spaces once, keeping the count
-// and the first kRegSlots half-spaces in a per-waypoint slot buffer; after
-// the count scan, MOVE = true copies the slots to the packed CSR position
-// (and recomputes, writing directly, only waypoints with more than
-// kRegSlots half-spaces).
-constexpr int kRegSlots = 16;
-template <int DW, bool MOVE>
-__global__ void __launch_bounds__(128) k_regions(GraphArgs g, WorldD w, int64_t n_wp, int64_t n_edges,
-                                                 const int64_t* __restrict__ wp_off, const int32_t* __restrict__ e_from,
-                                                 const int32_t* __restrict__ e_to, const double* __restrict__ e_tau,
-                                                 const double* __restrict__ e_acc0, const double* __restrict__ e_jerk,
-                                                 const int32_t* __restrict__ e_nsteps, int32_t* __restrict__ hcount,
-                                                 double* __restrict__ slot_pk, uint8_t* __restrict__ slot_fb,
-                                                 const int64_t* __restrict__ hs_off, int32_t* __restrict__ hs_cnt,
-                                                 double* __restrict__ hs_pk, uint8_t* __restrict__ hs_fb,
-                                                 int* __restrict__ err) {
-  extern __shared__ double smem[];
-  const WorldD ws = stage_world<DW>(w, smem);
-  const int64_t x = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (x >= n_wp) return;
-  if (MOVE) {
-    const int cnt = hcount[x];
-    hs_cnt[x] = cnt;
-    if (cnt <= kRegSlots) {
-      const int64_t o = hs_off[x];
-      const double2* src = reinterpret_cast<const double2*>(slot_pk) + x * kRegSlots * 2;
-      double2* dst = reinterpret_cast<double2*>(hs_pk) + o * 2;
-      for (int h = 0; h < cnt; ++h) {
-        dst[2 * h] = src[2 * h];
-        dst[2 * h + 1] = src[2 * h + 1];
-        hs_fb[o + h] = slot_fb[x * kRegSlots + h];
-      }
-      return;
-    }
-  }
-  // edge owning waypoint x
-  int64_t lo = 0, hi = n_edges;
-  while (hi - lo > 1) {
-    const int64_t mid = (lo + hi) >> 1;
-    if (wp_off[mid] <= x)
-      lo = mid;
-    else
-      hi = mid;
-  }
-  const int64_t e = lo;
-  const int j = static_cast<int>(x - wp_off[e]) + 1;
-  const int L = e_nsteps[e];
-  const int v = e_from[e], u = e_to[e];
-  MotionD<DW> m;
-  m.tau = e_tau[e];
-#pragma unroll
-  for (int k = 0; k < DW; ++k) {
-    m.p0[k] = g.pos[v * DW + k];
-    m.v0[k] = g.vel[v * DW + k];
-    m.p1[k] = g.pos[u * DW + k];
-    m.v1[k] = g.vel[u * DW + k];
-    m.a[k] = e_acc0[e * DW + k];
-    m.j[k] = e_jerk[e * DW + k];
-  }
-  double y[DW], yd[DW];
-  if (j == L) {
-#pragma unroll
-    for (int k = 0; k < DW; ++k) {
-      y[k] = m.p1[k];
-      yd[k] = m.v1[k];
-    }
-  } else {
-    motion_state<DW>(m, j * g.dt, y, yd);
-  }
-  if (MOVE) {  // more than kRegSlots half-spaces: recompute straight into place
-    const int64_t o = hs_off[x];
-    convex_region<DW>(ws, y, yd, hs_pk + o * 4, hs_pk + o * 4 + 3, hs_fb + o, 4, 4);
-    return;
-  }
-  double* ao = slot_pk + x * kRegSlots * 4;
-  const int count = convex_region<DW>(ws, y, yd, ao, ao + 3, slot_fb + x * kRegSlots, 4, 4, kRegSlots);
-  if (count < 0) {
-    atomicExch(err, 1);
-    hcount[x] = 0;
-    return;
-  }
-  hcount[x] = count;
-}
-
-// Single pass for small obstacle sets (<= 16 boxes): each waypoint computes
-// its half-spaces once into registers and reserves output space with one
-// warp-aggregated atomicAdd.  Waypoint w owns [hs_off[w], hs_off[w] +
-// hs_cnt[w]) (not in waypoint order; export rebuilds the CSR).  If the
-// reserved total exceeds cap nothing past cap is written and the host reruns
-// with the exact size (the counter returns it).  The region itself is
-// convex_region_fused (per-box squared distances computed once into shared
-// memory, one pass per iteration; PUMP_REGIONS_LEGACY=1 runs convex_region),
-// and each waypoint finds its edge in the k_wp_edge map.
+// Single pass: each waypoint computes its half-spaces once and reserves
+// output space with one warp-aggregated atomicAdd.  Waypoint w owns
+// [hs_off[w], hs_off[w] + hs_cnt[w]) (not in waypoint order; export rebuilds
+// the CSR).  If the reserved total exceeds cap nothing past cap is written and
+// the host reruns with the exact size (the counter returns it).  KW = 0 (at
+// most 16 boxes): convex_region_fused, per-box squared distances computed
+// once into shared memory, the half-spaces kept in registers.  KW > 0 (up to
+// 32 KW boxes): convex_region_scan, the first kRegLocal half-spaces kept per
+// thread; a waypoint with more recomputes its region straight into its
+// reserved range.  Each waypoint finds its edge in the k_wp_edge map.
 constexpr int kOnceMaxObs = 16;
+constexpr int kRegLocal = 8;
 
 // waypoint -> owning edge (one thread per edge fills its waypoint range)
 __global__ void k_wp_edge(int64_t n_edges, const int64_t* __restrict__ wp_off, int32_t* __restrict__ wp_edge) {
@@ -881,7 +798,7 @@ __global__ void k_wp_edge(int64_t n_edges, const int64_t* __restrict__ wp_off, i
   if (e >= n_edges) return;
   for (int64_t x = wp_off[e]; x < wp_off[e + 1]; ++x) wp_edge[x] = static_cast<int32_t>(e);
 }
-template <int DW, bool REG>
+template <int DW, int KW>
 __global__ void __launch_bounds__(128) k_regions_once(GraphArgs g, WorldD w, int64_t n_wp, int64_t n_edges,
                                                       const int64_t* __restrict__ wp_off,
                                                       const int32_t* __restrict__ e_from,
@@ -899,9 +816,11 @@ __global__ void __launch_bounds__(128) k_regions_once(GraphArgs g, WorldD w, int
   const int64_t x = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   const int lane = threadIdx.x & 31;
   const bool active = x < n_wp;
-  double la[kOnceMaxObs * DW], lb[kOnceMaxObs];
-  uint8_t lf[kOnceMaxObs];
+  constexpr int kLoc = KW == 0 ? kOnceMaxObs : kRegLocal;
+  double la[kLoc * DW], lb[kLoc];
+  uint8_t lf[kLoc];
   int n = 0;
+  double y[DW], yd[DW];
   if (active) {
     const int64_t e = wp_edge[x];
     const int j = static_cast<int>(x - wp_off[e]) + 1;
@@ -918,7 +837,6 @@ __global__ void __launch_bounds__(128) k_regions_once(GraphArgs g, WorldD w, int
       m.a[k] = e_acc0[e * DW + k];
       m.j[k] = e_jerk[e * DW + k];
     }
-    double y[DW], yd[DW];
     if (j == L) {
 #pragma unroll
       for (int k = 0; k < DW; ++k) {
@@ -928,10 +846,10 @@ __global__ void __launch_bounds__(128) k_regions_once(GraphArgs g, WorldD w, int
     } else {
       motion_state<DW>(m, j * g.dt, y, yd);
     }
-    if constexpr (REG)
+    if constexpr (KW == 0)
       n = convex_region_fused<DW>(ws, y, yd, smem + 2 * w.n_obs * DW + threadIdx.x, blockDim.x, la, lb, lf);
     else
-      n = convex_region<DW, 1>(ws, y, yd, la, lb, lf);
+      n = convex_region_scan<DW, KW>(ws, y, yd, la, lb, lf, DW, 1, kLoc);
     if (n < 0) {
       atomicExch(err, 1);
       n = 0;
@@ -953,6 +871,12 @@ __global__ void __launch_bounds__(128) k_regions_once(GraphArgs g, WorldD w, int
   hs_off[x] = start;
   hs_cnt[x] = n;
   if (start + n <= cap) {
+    if constexpr (KW > 0) {
+      if (n > kLoc) {  // rare: recompute straight into the reserved range
+        convex_region_scan<DW, KW>(ws, y, yd, hs_pk + start * 4, hs_pk + start * 4 + 3, hs_fb + start, 4, 4, n);
+        return;
+      }
+    }
     for (int h = 0; h < n; ++h) {
 #pragma unroll
       for (int k = 0; k < DW; ++k) hs_pk[(start + h) * 4 + k] = la[h * DW + k];
@@ -1300,7 +1224,7 @@ void build_graph_device(DevGraph& G, Ctx& c, int n, int dw, const double* h_pos,
   G.hs_off.ensure(al((NW + 2) * 8));
   G.hs_cnt.ensure(al((NW + 2) * 4));
   PUMP_CUDA(cudaMemsetAsync(err.p, 0, 4, st));
-  if (w.n_obs <= kOnceMaxObs) {
+  {
     DBuf& wpe = c.buf("g_wp_edge", al((NW + 8) * 4));
     if (E > 0) {
       KScope ks(st, F_REGIONS);
@@ -1317,9 +1241,10 @@ void build_graph_device(DevGraph& G, Ctx& c, int n, int dw, const double* h_pos,
       if (NW > 0) {
         KScope ks(st, F_REGIONS);
         dispatch_dw(dw, [&]<int DW>() {
-          static const bool reg = getenv("PUMP_REGIONS_LEGACY") == nullptr;
-          auto kern = reg ? k_regions_once<DW, true> : k_regions_once<DW, false>;
-          const size_t sm = wsmem + (reg ? static_cast<size_t>(w.n_obs) * 128 * 8 : 0);
+          auto kern = w.n_obs <= kOnceMaxObs ? k_regions_once<DW, 0>
+                      : w.n_obs <= 256      ? k_regions_once<DW, 8>
+                                            : k_regions_once<DW, 128>;
+          const size_t sm = wsmem + (w.n_obs <= kOnceMaxObs ? static_cast<size_t>(w.n_obs) * 128 * 8 : 0);
           if (sm > 48 * 1024)
             PUMP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
           kern<<<grid_for(NW, 128), 128, sm, st>>>(
@@ -1350,48 +1275,6 @@ void build_graph_device(DevGraph& G, Ctx& c, int n, int dw, const double* h_pos,
     c.sync();
     return;
   }
-  DBuf& hcnt = c.buf("g_hcnt", al((NW + 1) * 4));
-  DBuf& slot_pk = c.buf("g_reg_slots", al(static_cast<size_t>(NW) * kRegSlots * 32 + 32));
-  DBuf& slot_fb = c.buf("g_reg_slot_fb", al(static_cast<size_t>(NW) * kRegSlots + 8));
-  if (NW > 0) {
-    KScope ks(st, F_REGIONS);
-    dispatch_dw(dw, [&]<int DW>() {
-      if (wsmem > 48 * 1024) {
-        PUMP_CUDA(cudaFuncSetAttribute(k_regions<DW, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wsmem));
-        PUMP_CUDA(cudaFuncSetAttribute(k_regions<DW, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wsmem));
-      }
-      k_regions<DW, false><<<grid_for(NW, 128), 128, wsmem, st>>>(
-          ga, wd, NW, E, G.wp_off.as<int64_t>(), G.e_from.as<int32_t>(), G.e_to.as<int32_t>(), G.e_tau.as<double>(),
-          G.e_acc0.as<double>(), G.e_jerk.as<double>(), G.e_nsteps.as<int32_t>(), hcnt.as<int32_t>(),
-          slot_pk.as<double>(), slot_fb.as<uint8_t>(), nullptr, nullptr, nullptr, nullptr, err.as<int>());
-    });
-    ++c.launches;
-    PUMP_CUDA(cudaGetLastError());
-  }
-  DBuf& stmp4 = c.buf("g_scantmp4", scan_temp_bytes(NW + 16));
-  exclusive_scan<int32_t>(hcnt.as<int32_t>(), G.hs_off.as<int64_t>(), NW, stmp4.p, st, &c.launches);
-  int64_t H = 0;
-  int herr = 0;
-  c.d2h(&H, G.hs_off.as<int64_t>() + NW, 8);
-  c.d2h(&herr, err.p, 4);
-  c.sync();
-  if (herr) throw std::runtime_error("local_convex_region: pruning loop failed to make progress");
-  G.H = H;
-  G.hs_pk.ensure(al((H + 1) * 32));
-  G.hs_fb.ensure(al(H + 1));
-  if (NW > 0) {
-    KScope ks(st, F_REGIONS);
-    dispatch_dw(dw, [&]<int DW>() {
-      k_regions<DW, true><<<grid_for(NW, 128), 128, wsmem, st>>>(
-          ga, wd, NW, E, G.wp_off.as<int64_t>(), G.e_from.as<int32_t>(), G.e_to.as<int32_t>(), G.e_tau.as<double>(),
-          G.e_acc0.as<double>(), G.e_jerk.as<double>(), G.e_nsteps.as<int32_t>(), hcnt.as<int32_t>(),
-          slot_pk.as<double>(), slot_fb.as<uint8_t>(), G.hs_off.as<int64_t>(), G.hs_cnt.as<int32_t>(),
-          G.hs_pk.as<double>(), G.hs_fb.as<uint8_t>(), err.as<int>());
-    });
-    ++c.launches;
-    PUMP_CUDA(cudaGetLastError());
-  }
-  c.sync();
 }
 
 }  // namespace pumpg

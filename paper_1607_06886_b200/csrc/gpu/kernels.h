@@ -212,6 +212,8 @@ struct McTable {
 // (launch_mc then finds it ready); no-op when the table would not fit.
 void mc_table_prepare(McTable& tab, const HostLoop& L, int64_t r0, int64_t r1, uint64_t seed, int T,
                       cudaStream_t st, int64_t* launches);
+// the table already holds rollouts [r0, r1), steps t <= T of this closed loop and seed
+bool mc_table_covers(const McTable& tab, const HostLoop& L, int64_t r0, int64_t r1, uint64_t seed, int T);
 void launch_mc(const HostLoop& L, const DevWorld& w, int n_traj, const int64_t* d_traj_off, const double* d_ynom,
                int max_points, int64_t r0, int64_t r1, uint64_t seed, double eps_cc, unsigned long long* d_hits,
                cudaStream_t st, int64_t* launches, unsigned long long* d_steps = nullptr, McTable* table = nullptr,

@@ -1056,6 +1056,10 @@ static bool ensure_table(McTable& tab, const HostLoop& HL, int64_t r0, int64_t r
   return true;
 }
 
+bool mc_table_covers(const McTable& tab, const HostLoop& HL, int64_t r0, int64_t r1, uint64_t seed, int T) {
+  return tab.valid && tab.seed == seed && tab.r0 == r0 && tab.r1 == r1 && T <= tab.t_done && same_loop(tab.L, HL);
+}
+
 void mc_table_prepare(McTable& tab, const HostLoop& HL, int64_t r0, int64_t r1, uint64_t seed, int T,
                       cudaStream_t st, int64_t* launches) {
   if (r1 <= r0 || T < 0) return;

@@ -1,0 +1,141 @@
+"""GPU parity for the drop-in paths round 1 left open (VERDICT r1 "missing"
+1-2): the RoundHook on explore (planner.hpp:51-52, 245) and particle counts
+above 512 (ParticleMask is dynamic, cp.hpp:20-43; the reference's own
+cp_compare call uses 100000 particles, acceptance.cpp:290).
+
+Bar: every round the hook sees equals the oracle hook's view (expanded ids,
+arena size, statistics, every node's Pareto set, in order); masks word for
+word and arenas bit for bit for N > 512.
+"""
+import json
+import os
+
+import numpy as np
+import pytest
+
+from conftest import scenario_text
+from test_gpu_planner import explore_equal, random_graph_nodes, with_samples, ws_of, goal_of
+
+pytestmark = pytest.mark.gpu
+
+WORKERS = max(1, min(16, os.cpu_count() or 4))
+
+
+def small_world(oracle_lib, gpu_ctx, seed, n_particles, n_nodes=80):
+    from paper_1607_06886_b200 import api
+
+    obstacles = [([-1.0, -4.0], [1.0, 6.0])]
+    pos, vel, ws = random_graph_nodes(seed, n_nodes, obstacles)
+    goal = {"lo": [5.0, 5.0], "hi": [9.0, 9.0], "max_speed": 0.6}
+    scn = {"workspace": {"bounds": {"lo": [-10, -10], "hi": [10, 10]},
+                         "obstacles": [{"lo": o[0], "hi": o[1]} for o in obstacles]},
+           "start": {"position": [-8, -8]}, "goal": {"lo": [5, 5], "hi": [9, 9], "max_speed": 0.6},
+           "noise": {"process": [0, 0, 0.02, 0.02], "measurement": 0.01, "initial": 0.005},
+           "dt": 0.25, "samples": 10, "alpha": 0.05}
+    cl, _ = oracle_lib.scenario_models(json.dumps(scn))
+    og = oracle_lib.build_graph(pos, vel, ws, goal, 9.0, 0.25, 0.05, 200.0, workers=WORKERS)
+    gg = api.build_graph(pos, vel, ws, goal, 9.0, 0.25, 0.05, 200.0, ctx=gpu_ctx)
+    bank = api.presample_bank(cl, 2048, n_particles, 9, ctx=gpu_ctx)
+    return og, gg, bank
+
+
+@pytest.mark.parametrize("seed,n", [(777, 64), (201, 32)])
+def test_round_hook_matches_oracle_every_round(oracle_lib, gpu_ctx, seed, n):
+    from paper_1607_06886_b200 import api
+
+    og, gg, bank = small_world(oracle_lib, gpu_ctx, seed, n)
+    ref = oracle_lib.explore_trace(og, bank, 0.01, 0.2, 0.5, 9.0)
+    seen = []
+
+    def hook(rnd, st, expanded):
+        seen.append((rnd, st, expanded))
+        assert st["n_goal_plans"] == 0 and st["termination"] == ""
+
+    got = api.explore(gg, 0.01, 0.2, 0.5, 9.0, ctx=gpu_ctx, hook=hook)
+    assert len(ref) > 3 and len(seen) == len(ref)
+    for (rnd, st, expanded), r in zip(seen, ref):
+        assert rnd == r["round"]
+        assert np.array_equal(expanded, r["expanded"])
+        for k in ("n_plans", "partial_plans", "discarded_cp", "removed_dominated", "discarded_horizon"):
+            assert st[k] == r[k], (rnd, k, st[k], r[k])
+        assert np.array_equal(st["pareto_ptr"], r["pareto_ptr"]), rnd
+        assert np.array_equal(st["pareto_ids"], r["pareto_ids"]), rnd
+    # the hooked run ends where the pipelined one does
+    plain = api.explore(gg, 0.01, 0.2, 0.5, 9.0, ctx=gpu_ctx)
+    explore_equal(got, plain)
+    explore_equal(got, oracle_lib.explore(og, bank, 0.01, 0.2, 0.5, 9.0, workers=WORKERS))
+
+
+def test_round_hook_exception_stops_the_run(oracle_lib, gpu_ctx):
+    from paper_1607_06886_b200 import api
+
+    _, gg, _ = small_world(oracle_lib, gpu_ctx, 777, 32)
+    calls = []
+
+    def hook(rnd, st, expanded):
+        calls.append(rnd)
+        if rnd == 2:
+            raise KeyError("stop here")
+
+    with pytest.raises(KeyError):
+        api.explore(gg, 0.01, 0.2, 0.5, 9.0, ctx=gpu_ctx, hook=hook)
+    assert calls == [1, 2]
+    api.explore(gg, 0.01, 0.2, 0.5, 9.0, ctx=gpu_ctx)  # the context is still usable
+
+
+@pytest.mark.parametrize("n", [513, 1000, 4096, 100000])
+def test_hsmc_more_than_512_particles(oracle_lib, gpu_ctx, n):
+    from paper_1607_06886_b200 import api
+
+    rng = np.random.default_rng(n)
+    cl, _ = oracle_lib.scenario_models(scenario_text("quad3d_three_obstacle"))
+    T = 120
+    bank = api.presample_bank(cl, T, n, 11, ctx=gpu_ctx)
+    ref_bank = oracle_lib.presample_bank(cl, T, n, 11, workers=WORKERS)
+    assert np.array_equal(bank.view(np.uint64), ref_bank.view(np.uint64))
+    n_tasks = 40 if n < 100000 else 4
+    W = (n + 63) // 64
+    masks = rng.integers(0, 2 ** 63, size=(n_tasks, W), dtype=np.int64).astype(np.uint64)
+    masks &= api.full_mask(n)[None, :]
+    masks[::2] = api.full_mask(n)
+    nst = rng.integers(0, 30, size=n_tasks)
+    step_off = np.concatenate([[0], np.cumsum(nst)]).astype(np.int64)
+    S = int(step_off[-1])
+    step_t = rng.integers(0, T + 1, size=S).astype(np.int32)
+    nh = rng.integers(0, 4, size=S)
+    hs_off = np.concatenate([[0], np.cumsum(nh)]).astype(np.int64)
+    H = int(hs_off[-1])
+    sd = float(np.std(bank))
+    hs_a = rng.normal(size=(H, 3))
+    hs_b = rng.normal(scale=2 * sd, size=H) + 0.5 * sd
+    ref_m, ref_p = oracle_lib.hsmc_extend_batch(bank, masks, step_off, step_t, hs_off, hs_a, hs_b, workers=WORKERS)
+    got_m, got_p = api.hsmc_extend_batch(masks, step_off, step_t, hs_off, hs_a, hs_b, gpu_ctx)
+    assert np.array_equal(got_m, ref_m)
+    assert np.array_equal(got_p, ref_p)
+    assert 0 < ref_p.sum() < n * n_tasks
+    # the range check precedes the null-region skip at any N
+    with pytest.raises(IndexError):
+        api.hsmc_extend_batch(masks[:1], np.array([0, 1]), np.array([T + 1], np.int32), np.array([0, 0]),
+                              np.zeros((0, 3)), np.zeros(0), gpu_ctx)
+
+
+@pytest.mark.parametrize("n", [600, 1024, 1500])
+def test_explore_more_than_512_particles(oracle_lib, gpu_ctx, n):
+    """a warp runs each task slab by slab (512 particles at a time)."""
+    from paper_1607_06886_b200 import api
+
+    og, gg, bank = small_world(oracle_lib, gpu_ctx, 200, n, n_nodes=60)
+    ref = oracle_lib.explore(og, bank, 0.01, 0.2, 0.5, 9.0, workers=WORKERS)
+    got = api.explore(gg, 0.01, 0.2, 0.5, 9.0, ctx=gpu_ctx)
+    assert ref["n_plans"] > 50
+    explore_equal(got, ref)
+
+
+def test_run_pump_more_than_512_particles(oracle_lib, gpu_ctx):
+    from paper_1607_06886_b200 import api
+    from test_gpu_planner import assert_run_equal
+
+    txt = with_samples("three_obstacle", 200, particles=800, mc_samples=2000)
+    got = api.run_pump(api.parse_scenario(txt), ctx=gpu_ctx)
+    ref = oracle_lib.run_pump(txt, workers=WORKERS)
+    assert_run_equal(got, ref)
