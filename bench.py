@@ -1,23 +1,30 @@
 """PUMP solve benchmark (BASELINE.json metric) on B200.
 
-Default workload = BASELINE configs[1]: the indoor/corridor quadrotor scenario
-(scenarios/quad3d_indoor.json: 6-D double integrator, 10 walls, n = 4000
-samples, 64 particles per plan, alpha = 2%, bisection + MC certification with
-20000 rollouts).  One step = one full PUMP solve (pump.hpp:170-263): Halton
-sampling, graph build, particle bank, Pareto exploration, Alg. 4 bisection with
-MC certification and CP-constrained smoothing.
+Default workload = the largest single-GPU BASELINE config, configs[2]: the
+cluttered forest quadrotor scenario (scenarios/quad3d_forest.json: 6-D double
+integrator, 200 synthetic AABBs, n = 16000 samples, 128 particles per plan,
+alpha = 5%, bisection + MC certification with 20000 rollouts, > 1e5 partial
+plans).  One step = one full PUMP solve (pump.hpp:170-263): Halton sampling,
+graph build, particle bank, Pareto exploration, Alg. 4 bisection with MC
+certification and CP-constrained smoothing.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                  [--config quad3d_indoor] [--no-cpu-baseline]
+                  [--config quad3d_forest|quad3d_indoor|quad3d_three_obstacle] [--no-cpu-baseline]
 
 Prints one JSON line on rank 0.  `value` = ms per solve with the scenario
 already parsed (the solve is a synchronous library call whose hot loops all
 run on the GPU; the host only orchestrates); `e2e` = the same solve through
 the C ABI starting from the JSON scenario text on the host and ending with the
 result arrays on the host.  Per-kernel times come from CUDA events recorded
-on the library stream around every launch of the timed region.  Under torchrun (N > 1) every rank runs the solve with
-the MC certification rollouts sharded across ranks (NCCL all-reduce of the
-int64 hit counts); time is the max over ranks.
+on the library stream around every launch of a second timed pass.  Under
+torchrun (N > 1) every rank runs the solve with the MC certification rollouts
+and the graph rows sharded across ranks (NCCL all-reduce of the int64 hit
+counts, grouped broadcasts of the row slices); time is the max over ranks.
+
+--impl reference times the reference's own CPU code (oracle/_ref: the
+reference headers compiled in place, glibc normals) on all host threads, one
+bounded sample of the solve per step (see ref_arm below); the oracle
+restatement stands in only when oracle/_ref was not built.
 """
 from __future__ import annotations
 
@@ -132,49 +139,128 @@ def load_text(config: str) -> str:
         return f.read()
 
 
+def config_of(name: str, scn: dict) -> dict:
+    """The workload description both arms print (identical dicts)."""
+    return {"workload": name, "samples": scn["samples"], "particles": scn["particles"], "alpha": scn["alpha"],
+            "mc_samples": scn["mc_samples"], "obstacles": len(scn["workspace"]["obstacles"]),
+            "l2": "256 MiB buffer overwritten before every timed solve (GPU arm)"}
+
+
+ROW_STRIDE, MC_STRIDE = 8, 8  # reference-arm sample: 1/8 of the graph rows, 1/8 of each certification's rollouts
+
+
+class RefArm:
+    """The reference's own code on the host (oracle/_ref/libpumpref.so: the
+    unmodified reference headers compiled in place by oracle/ref/Makefile).
+
+    A full forest solve takes tens of seconds on the host, so a step is a
+    bounded sample of it (oracle/ref/ref_driver.cpp ref_bench_*): setup builds
+    the graph and runs one complete solve (timed: `full_solve_ms`, and its MC
+    calls recorded); each step re-runs sample_free, the build_graph row loop
+    over every ROW_STRIDE-th source row (x ROW_STRIDE), presample_bank +
+    explore on the full graph, and every recorded mc_certify call over its
+    first n_mc / MC_STRIDE rollouts (x MC_STRIDE)."""
+
+    def __init__(self, text: str, workers: int):
+        import ctypes as C
+
+        import numpy as np
+
+        path = os.path.join(ROOT, "oracle", "_ref", "libpumpref.so")
+        self.L = C.CDLL(path)
+        self.L.ref_last_error.restype = C.c_char_p
+        self.L.ref_bench_setup.argtypes = [C.c_char_p, C.c_int, C.c_void_p, C.c_void_p]
+        self.L.ref_bench_step.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_void_p]
+        self.L.ref_bench_free.argtypes = [C.c_void_p]
+        self.C, self.np = C, np
+        out = np.zeros(9)
+        self.h = C.c_void_p()
+        if self.L.ref_bench_setup(text.encode(), workers, out.ctypes.data_as(C.c_void_p), C.byref(self.h)) != 0:
+            raise RuntimeError(self.L.ref_last_error().decode())
+        self.full_ms = 1e3 * (out[0] + out[1])
+        self.setup = {"build_graph_ms": round(1e3 * out[0], 1), "explore_ms": round(1e3 * out[2], 1),
+                      "selection_ms": round(1e3 * out[3], 1), "partial_plans": int(out[4]),
+                      "mc_calls": int(out[5]), "success": int(out[6]), "cost": float(out[7]), "nodes": int(out[8])}
+
+    def step(self, workers: int, k: int, row_stride: int = ROW_STRIDE, mc_stride: int = MC_STRIDE) -> dict:
+        out = self.np.zeros(9)
+        if self.L.ref_bench_step(self.h, workers, row_stride, k % row_stride, mc_stride,
+                                 out.ctypes.data_as(self.C.c_void_p)) != 0:
+            raise RuntimeError(self.L.ref_last_error().decode())
+        return {"est_ms": 1e3 * out[8], "sample_ms": 1e3 * (out[0] + out[1] + out[2] + out[3]),
+                "rows": int(out[4]), "partial_plans": int(out[6])}
+
+    def close(self):
+        self.L.ref_bench_free(self.h)
+
+
+def have_ref() -> bool:
+    return os.path.exists(os.path.join(ROOT, "oracle", "_ref", "libpumpref.so"))
+
+
 def run_reference(args, world, rank):
-    """The reference's CPU path on the host cores: the oracle restatement (the
-    reference itself cannot be built here: Eigen is absent)."""
+    """The reference's CPU path on the host cores, same config / metric /
+    steps / warm-up as the GPU arm.  Rank 0 only."""
     if rank != 0:
         return
-    import oracle
-
     text = load_text(args.config)
+    scn = json.loads(text)
     cores = os.cpu_count() or 1
-    for _ in range(min(args.warmup, 1)):
-        oracle.run_pump(text, workers=cores)
-    times = []
-    r = None
-    for _ in range(args.steps):
-        t0 = time.perf_counter()
-        r = oracle.run_pump(text, workers=cores)
-        times.append(time.perf_counter() - t0)
-    ms = 1e3 * sum(times) / len(times)
-    line = {"impl": "reference", "metric": "PUMP solve time", "value": round(ms, 3), "unit": "ms",
-            "n_gpus": world, "steps": args.steps, "warmup": min(args.warmup, 1), "ms_per_step": round(ms, 3),
-            "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic (Halton samples of the named scenario, counter-hash particles/rollouts)",
-            "config": {"workload": args.config, "samples": json.loads(text)["samples"],
-                       "particles": json.loads(text)["particles"], "alpha": json.loads(text)["alpha"]},
-            "cpu_baseline": {"value": round(ms, 3), "unit": "ms", "cores": cores, "kind": "port",
-                             "sample": "one full solve per step (oracle restatement, workers = all host threads)"},
-            "e2e": {"value": round(ms, 3), "unit": "ms", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-            "partial_plans": r["partial_plans"], "success": r["success"]}
+    line = {"impl": "reference", "metric": "PUMP solve time", "unit": "ms", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "higher_is_better": False, "scaling": "strong", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic (Halton samples of the named scenario, counter-hash particles/rollouts)",
+            "config": config_of(args.config, scn)}
+    if have_ref():
+        arm = RefArm(text, cores)
+        for k in range(args.warmup):
+            arm.step(cores, k)
+        times, samples = [], []
+        for k in range(args.steps):
+            r = arm.step(cores, args.warmup + k)
+            times.append(r["est_ms"])
+            samples.append(r["sample_ms"])
+        arm.close()
+        ms = sum(times) / len(times)
+        line.update({"value": round(ms, 3), "ms_per_step": round(ms, 3),
+                     "cpu_baseline": {"value": round(ms, 3), "unit": "ms", "cores": cores, "kind": "reference",
+                                      "sample": f"per step: sample_free + build_graph rows v = k (mod {ROW_STRIDE}) "
+                                                f"(x{ROW_STRIDE}) + presample_bank + explore (full) + the solve's "
+                                                f"mc_certify calls on 1/{MC_STRIDE} of their rollouts "
+                                                f"(x{MC_STRIDE}); oracle/_ref, workers = all host threads",
+                                      "sample_ms_per_step": round(sum(samples) / len(samples), 1),
+                                      "full_solve_ms": round(arm.full_ms, 1), "full_solve": arm.setup},
+                     "partial_plans": arm.setup["partial_plans"], "success": arm.setup["success"]})
+    else:  # oracle/_ref not built: the oracle restatement, full solves
+        import oracle
+
+        for _ in range(min(args.warmup, 1)):
+            oracle.run_pump(text, workers=cores)
+        times, r = [], None
+        for _ in range(args.steps):
+            t0 = time.perf_counter()
+            r = oracle.run_pump(text, workers=cores)
+            times.append(time.perf_counter() - t0)
+        ms = 1e3 * sum(times) / len(times)
+        line.update({"value": round(ms, 3), "ms_per_step": round(ms, 3),
+                     "cpu_baseline": {"value": round(ms, 3), "unit": "ms", "cores": cores, "kind": "port",
+                                      "sample": "one full solve per step (oracle restatement, all host threads)"},
+                     "partial_plans": r["partial_plans"], "success": r["success"]})
+    line["e2e"] = {"value": line["value"], "unit": "ms", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}
     print(json.dumps(line), flush=True)
 
 
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=30)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="quad3d_indoor")
+    ap.add_argument("--config", default="quad3d_forest")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-mc-sweep", action="store_true")
     ap.add_argument("--no-rrt", action="store_true")
     args = ap.parse_args()
-    args.warmup = max(args.warmup, 0)
+    args.warmup = max(args.warmup, 3)  # >= 3 warm-up steps (both arms)
     world, rank, local = dist_setup()
     if args.impl == "reference":
         run_reference(args, world, rank)
@@ -207,7 +293,7 @@ def main():
 
     # warm-up (buffers sized, modules loaded)
     res = None
-    for _ in range(max(args.warmup, 3)):
+    for _ in range(args.warmup):
         res = api.run_pump(sc, ctx=ctx)
 
     # ---- timed region: K solves timed with CUDA events on the library's own
@@ -413,11 +499,31 @@ def main():
         t0 = time.perf_counter()
         o = oracle.run_pump(text, workers=cores)
         cpu_s = time.perf_counter() - t0
+        bits = lambda a: np.ascontiguousarray(a).view(np.uint64).tolist()  # noqa: E731
         same = (o["path"].tolist() == res["path"].tolist() and o["certified_cp"] == res["certified_cp"]
-                and o["cost"] == res["cost"] and o["partial_plans"] == res["partial_plans"])
+                and o["cost"] == res["cost"] and o["partial_plans"] == res["partial_plans"]
+                and bits(o["pareto_cost"]) == bits(res["pareto_cost"]) and bits(o["pareto_cp"]) == bits(res["pareto_cp"])
+                and o["mc_eval_ids"].tolist() == res["mc_eval_ids"].tolist()
+                and bits(o["mc_eval_values"]) == bits(res["mc_eval_values"])
+                and bits(o["traj_pos"]) == bits(res["traj_pos"]) and o["smoothing_s"] == res["smoothing_s"])
         cpu = {"value": round(1e3 * cpu_s, 1), "unit": "ms", "cores": cores, "kind": "port",
                "sample": "one full solve of the same scenario (oracle restatement, workers = all host threads)",
-               "identical_result": bool(same)}
+               "identical_result": bool(same),
+               "compared": "path, cost, certified CP, partial plans, Pareto front (cost, cp bits), MC probe ids and "
+                           "values, smoothing fraction, trajectory position bits"}
+        if have_ref():
+            # the reference's own code (oracle/_ref): one full solve on all
+            # threads, and a bounded 1-thread sample (the same RefArm steps
+            # with 1/64 of the rows and of each certification's rollouts)
+            arm = RefArm(text, cores)
+            one = arm.step(1, 0, 64, 64)
+            cpu["reference"] = {"kind": "reference", "cores": cores, "full_solve_ms": round(arm.full_ms, 1),
+                                "phases": arm.setup}
+            cpu["workers_1"] = {"kind": "reference", "cores": 1, "value": round(one["est_ms"], 1), "unit": "ms",
+                                "sample": "sample_free + build_graph rows v = 0 (mod 64) (x64) + bank + explore "
+                                          "(full) + the solve's mc_certify calls on 1/64 of their rollouts (x64)",
+                                "sample_ms": round(one["sample_ms"], 1)}
+            arm.close()
 
     # per-kernel roofline table from the committed ncu --set full captures
     # (tools/ncu_kernels.py; static evidence, not measured in this run)
@@ -432,17 +538,18 @@ def main():
         ncu_tab = None
 
     pp_s = res["partial_plans"] / (res["explore_seconds"]) if res["explore_seconds"] > 0 else None
-    mc_rs = res["mc_rollouts"] / (res["mc_ms"] * 1e-3) if res["mc_ms"] > 0 else None
+    # certification rollouts per second of the solve's MC work: the
+    # certification kernels plus the common-random-number table they read
+    mc_tab_ms = float(prof_ms[FAMILIES.index("mc_table")] / args.steps)
+    mc_rs = res["mc_rollouts"] / ((res["mc_ms"] + mc_tab_ms) * 1e-3) if res["mc_ms"] > 0 else None
     line = {
         "metric": "PUMP solve time", "value": round(ms_per_step, 3), "unit": "ms", "n_gpus": world,
-        "steps": args.steps, "warmup": max(args.warmup, 3), "ms_per_step": round(ms_per_step, 3),
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_per_step, 3),
         "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (Halton samples of the named scenario; counter-hash particle bank and MC rollouts)",
-        "config": {"workload": args.config, "samples": scn["samples"], "particles": scn["particles"],
-                   "alpha": scn["alpha"], "mc_samples": scn["mc_samples"], "obstacles": len(scn["workspace"]["obstacles"]),
-                   "l2": "256 MiB buffer overwritten before every timed solve",
-                   "timing": "CUDA events on the library stream around each solve (profiler off); kernels/roofline "
-                             "from a second K-solve pass with per-launch events"},
+        "config": config_of(args.config, scn),
+        "timing": "CUDA events on the library stream around each solve (profiler off); kernels/roofline "
+                  "from a second K-solve pass with per-launch events",
         "e2e": {"value": round(e2e_ms, 3), "unit": "ms",
                 "h2d_bytes_per_step": int((e_io1[0] - e_io0[0]) // args.steps),
                 "d2h_bytes_per_step": int((e_io1[1] - e_io0[1]) // args.steps)},
@@ -461,6 +568,7 @@ def main():
                   "selection_ms": round(1e3 * res["selection_seconds"], 3)},
         "partial_plans_per_s": round(pp_s, 1) if pp_s else None,
         "mc_rollouts_per_s": round(mc_rs, 1) if mc_rs else None,
+        "mc_rollouts_per_s_note": "solve's certified rollouts / (certification kernels + MC-table build) time",
     }
     if rank == 0:
         print(json.dumps(line), flush=True)

@@ -5,14 +5,41 @@
 // the oracle restatement against the literal reference code paths (glibc
 // normals, reference control flow).  Built by oracle/ref/Makefile into
 // oracle/_ref/libpumpref.so.
+#include <chrono>
 #include <cstring>
 #include <string>
 
+#include "pump/cp.hpp"
+#include "pump/graph.hpp"
+#include "pump/planner.hpp"
+#include "pump/scenario.hpp"
+
+// Every mc_certify call the selection phase makes (pump.hpp:223-255) is
+// recorded when a trace is armed, so the bench's reference arm can replay
+// the same certification work on a rollout sample (ref_bench_step).  The
+// reference headers are not modified: the call sites in pump.hpp / rrt.hpp /
+// compare.hpp, included after this shim, resolve `mc_certify` to it.
+namespace pump {
+struct McCall {
+  std::vector<VectorXd> y;
+  int n_mc;
+  std::uint64_t seed;
+  double eps_cc;
+};
+inline thread_local std::vector<McCall>* g_mc_trace = nullptr;
+inline CpEstimate mc_certify_traced(const std::vector<VectorXd>& y_nom, const ClosedLoopDynamics& cl,
+                                    const Workspace& w, int n_mc, std::uint64_t seed, double eps_cc,
+                                    int workers = 1) {
+  if (g_mc_trace) g_mc_trace->push_back({y_nom, n_mc, seed, eps_cc});
+  return mc_certify(y_nom, cl, w, n_mc, seed, eps_cc, workers);
+}
+}  // namespace pump
+#define mc_certify mc_certify_traced
 #include "pump/pump.hpp"
 #include "pump/compare.hpp"
 #include "pump/report.hpp"
 #include "pump/rrt.hpp"
-#include "pump/scenario.hpp"
+#undef mc_certify
 
 namespace {
 thread_local std::string g_err;
@@ -135,5 +162,144 @@ int ref_cp_compare(const char* text, const char* traj_text, const int* counts, i
     return 1;
   }
 }
+
+// ------------------------------------------------ bench.py reference arm
+// A bounded sample of one reference solve (run_pump, pump.hpp:170-263), for
+// workloads whose full solve takes tens of seconds on the host: setup builds
+// the graph and runs one full solve (timed, and recording its MC calls);
+// each step then re-times, through the reference's own functions,
+//   - sample_free + the build_graph row loop (graph.hpp:63-95, the body
+//     restated over the reference's connect / motion_collides /
+//     motion_waypoints / point_free / local_convex_region) for the rows
+//     v = offset (mod stride), scaled by stride;
+//   - presample_bank + explore on the full graph (unsampled);
+//   - every recorded mc_certify call over its first n_mc / mc_stride
+//     rollouts (rollouts are independent), scaled by mc_stride.
+struct RefBench {
+  pump::Scenario s;
+  pump::ModelBundle mb;
+  pump::SampleGraph g;
+  std::vector<pump::McCall> trace;
+};
+
+int ref_bench_setup(const char* text, int workers, double* out, void** handle) {
+  try {
+    using clk = std::chrono::steady_clock;
+    auto* b = new RefBench;
+    b->s = scn(text);
+    pump::Scenario& s = b->s;
+    b->mb = pump::build_models(s);
+    auto t0 = clk::now();
+    std::vector<pump::State> nodes;
+    nodes.push_back(s.x_init);
+    for (auto& st : pump::sample_free(s.samples, s.workspace, s.max_speed, s.goal)) nodes.push_back(std::move(st));
+    b->g = pump::build_graph(std::move(nodes), s.workspace, s.goal, s.effective_r_n(), s.dt, s.effective_eps_cc(),
+                             s.effective_tau_max(), workers);
+    auto t1 = clk::now();
+    pump::g_mc_trace = &b->trace;
+    pump::PumpResult r = pump::run_pump(s, workers, &b->g);
+    pump::g_mc_trace = nullptr;
+    auto t2 = clk::now();
+    out[0] = std::chrono::duration<double>(t1 - t0).count();
+    out[1] = std::chrono::duration<double>(t2 - t1).count();
+    out[2] = r.explore_seconds;
+    out[3] = r.selection_seconds;
+    out[4] = static_cast<double>(r.partial_plans);
+    out[5] = static_cast<double>(b->trace.size());
+    out[6] = r.success ? 1.0 : 0.0;
+    out[7] = r.cost;
+    out[8] = static_cast<double>(b->g.nodes.size());
+    *handle = b;
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return 1;
+  }
+}
+
+int ref_bench_step(void* handle, int workers, int row_stride, int row_offset, int mc_stride, double* out) {
+  try {
+    using clk = std::chrono::steady_clock;
+    auto secs = [](clk::time_point a, clk::time_point c) { return std::chrono::duration<double>(c - a).count(); };
+    RefBench& b = *static_cast<RefBench*>(handle);
+    const pump::Scenario& s = b.s;
+    const double r_n = s.effective_r_n(), eps_cc = s.effective_eps_cc(), tau_max = s.effective_tau_max();
+    // sampling + graph rows
+    auto t0 = clk::now();
+    std::vector<pump::State> nodes;
+    nodes.push_back(s.x_init);
+    for (auto& st : pump::sample_free(s.samples, s.workspace, s.max_speed, s.goal)) nodes.push_back(std::move(st));
+    const int n = static_cast<int>(nodes.size());
+    auto t_s = clk::now();
+    std::vector<int> rows;
+    for (int v = row_offset; v < n; v += row_stride) rows.push_back(v);
+    std::vector<long> kept(rows.size(), 0);
+    pump::parallel_for(rows.size(), workers, [&](std::size_t lo, std::size_t hi) {
+      for (std::size_t q = lo; q < hi; ++q) {
+        const pump::State& a = nodes[rows[q]];
+        for (int u = 0; u < n; ++u) {
+          if (u == rows[q]) continue;
+          const pump::State& bb = nodes[u];
+          if (2.0 * (bb.velocity - a.velocity).norm() >= r_n) continue;
+          pump::Motion m = pump::connect(a, bb, tau_max);
+          if (!m.ok || m.cost >= r_n || m.tau <= 0) continue;
+          if (pump::motion_collides(s.workspace, m, eps_cc)) continue;
+          auto wps = pump::motion_waypoints(m, s.dt);
+          std::vector<pump::ConvexRegion> regions;
+          regions.reserve(wps.size());
+          bool valid = true;
+          for (std::size_t j = 1; j < wps.size(); ++j) {
+            if (!pump::point_free(s.workspace, wps[j].state.position)) {
+              valid = false;
+              break;
+            }
+            regions.push_back(pump::local_convex_region(s.workspace, wps[j].state.position, wps[j].state.velocity));
+          }
+          if (valid) kept[q]++;
+        }
+      }
+    });
+    auto t1 = clk::now();
+    // bank + explore on the full graph (pump.hpp:194-208)
+    pump::DeviationBank bank = pump::presample_bank(b.mb.dm, b.mb.gains, s.initial_covariance, s.bank_horizon,
+                                                    s.particles, s.seeds.bank, workers);
+    pump::ExploreParams ep;
+    const double eta = s.effective_eta();
+    ep.alpha_min = s.alpha / eta;
+    ep.alpha_max = std::min(1.0, eta * s.alpha);
+    ep.lambda = s.lambda;
+    ep.r_n = r_n;
+    ep.workers = workers;
+    pump::ExploreResult ex = pump::explore(b.g, bank, ep);
+    auto t2 = clk::now();
+    // the selection phase's certifications on a rollout sample
+    long hits = 0;
+    for (const auto& c : b.trace) {
+      const int n_s = std::max(1, c.n_mc / mc_stride);
+      hits += static_cast<long>(pump::mc_certify(c.y, b.mb.cl, s.workspace, n_s, c.seed, c.eps_cc, workers).value *
+                                n_s);
+    }
+    auto t3 = clk::now();
+    long edges = 0;
+    for (long k : kept) edges += k;
+    out[0] = secs(t0, t_s);  // sample_free (full)
+    out[1] = secs(t_s, t1);  // sampled rows
+    out[2] = secs(t1, t2);   // bank + explore (full)
+    out[3] = secs(t2, t3);   // sampled certifications
+    out[4] = static_cast<double>(rows.size());
+    out[5] = static_cast<double>(edges);
+    out[6] = static_cast<double>(ex.stats.partial_plans);
+    out[7] = static_cast<double>(hits);
+    // estimate of the full solve (seconds)
+    out[8] = out[0] + out[1] * (static_cast<double>(n) / std::max<size_t>(1, rows.size())) + out[2] +
+             out[3] * mc_stride;
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return 1;
+  }
+}
+
+void ref_bench_free(void* handle) { delete static_cast<RefBench*>(handle); }
 
 }  // extern "C"
