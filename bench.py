@@ -287,7 +287,7 @@ def main():
         api.set_comm(ctx, rank, world)
 
     def io():
-        b = np.zeros(4, dtype=np.int64)
+        b = np.zeros(5, dtype=np.int64)
         L.pump_ctx_io_bytes(ctx.h, b.ctypes.data_as(C.c_void_p))
         return b
 

@@ -164,7 +164,8 @@ enum {
 int pump_ctx_profile(pump_ctx* ctx, int enable);
 int pump_ctx_profile_read(pump_ctx* ctx, double* ms, int64_t* counts, int64_t* work);
 /* out[0] host->device bytes, out[1] device->host bytes, out[2] MC rollout-steps,
- * out[3] device allocations made so far (process-wide). */
+ * out[3] device allocations made so far (process-wide), out[4] collectives
+ * issued (NCCL or host).  `out` holds 5 values. */
 int pump_ctx_io_bytes(pump_ctx* ctx, int64_t* out);
 /* Overwrite a 256 MiB buffer (> 126 MB L2) on the ctx stream and synchronize. */
 int pump_ctx_flush_l2(pump_ctx* ctx);
@@ -207,6 +208,19 @@ int32_t pump_waypoints(int32_t dw, const double* fp, const double* fv, const dou
  * caller (e.g. torch.distributed). */
 int pump_nccl_unique_id(uint8_t* out128);
 int pump_ctx_set_comm(pump_ctx* ctx, int rank, int world, const uint8_t* id128);
+/* The same sharding over caller-supplied host collectives instead of NCCL
+ * (e.g. a torch.distributed gloo group: several ranks may then share one
+ * GPU, since no kernel waits on another rank).  allreduce: in-place int64 sum
+ * of `count` values over all ranks.  gather: every rank contributes its
+ * len[rank] bytes `send`; on return `recv` holds rank r's bytes at offset
+ * off[r] for every r (off/len have `world` entries).  Both return 0 on
+ * success.  Device data is staged through host memory around each call.
+ * world <= 1 (or NULL functions) removes them. */
+typedef int (*pump_allreduce_i64_fn)(void* user, int64_t* values, int64_t count);
+typedef int (*pump_gather_fn)(void* user, const void* send, void* recv, const int64_t* off, const int64_t* len,
+                              int32_t world);
+int pump_ctx_set_collectives(pump_ctx* ctx, int rank, int world, pump_allreduce_i64_fn allreduce,
+                             pump_gather_fn gather, void* user);
 int pump_shard_range(int64_t n, int rank, int world, int64_t* lo, int64_t* hi);
 
 /* ------------------------------------------------------------- scenario */

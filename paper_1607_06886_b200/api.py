@@ -61,7 +61,7 @@ EXPORTS = [
     "pump_hsmc_extend_batch", "pump_explore_run_hooked", "pump_mc_certify_batch", "pump_mc_certify", "pump_build_graph", "pump_graph_upload",
     "pump_graph_counts", "pump_graph_export", "pump_graph_free", "pump_explore_run", "pump_explore_counts",
     "pump_explore_export", "pump_explore_free", "pump_run", "pump_result_summary_get", "pump_result_arrays",
-    "pump_result_free", "pump_nccl_unique_id", "pump_ctx_set_comm", "pump_shard_range", "pump_ctx_profile",
+    "pump_result_free", "pump_nccl_unique_id", "pump_ctx_set_comm", "pump_ctx_set_collectives", "pump_shard_range", "pump_ctx_profile",
     "pump_ctx_profile_read", "pump_ctx_io_bytes", "pump_ctx_flush_l2", "pump_peak_fp64", "pump_ctx_stream",
     "pump_scenario_nodes", "pump_build_graph_rows", "pump_rrt_run", "pump_probe_round_latency",
 ]
@@ -152,6 +152,14 @@ class Context:
     @property
     def last_kernel_ms(self) -> float:
         return lib().pump_ctx_last_kernel_ms(self.h)
+
+    def io_counters(self) -> dict:
+        """pump_ctx_io_bytes: H2D / D2H bytes, MC rollout-steps, device
+        allocations, collectives issued."""
+        b = np.zeros(5, dtype=np.int64)
+        lib().pump_ctx_io_bytes(self.h, _p(b))
+        return dict(zip(("h2d_bytes", "d2h_bytes", "mc_rollout_steps", "device_allocs", "collectives"),
+                        b.tolist()))
 
     @property
     def launches(self) -> int:
@@ -547,6 +555,55 @@ def set_comm(ctx: Context, rank: int, world: int, group=None):
     dist.broadcast(t, src=0, group=group)
     buf = t.cpu().numpy().astype(np.uint8)
     _check(lib().pump_ctx_set_comm(ctx.h, rank, world, _p(buf)))
+
+
+ALLREDUCE_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.POINTER(C.c_int64), C.c_int64)
+GATHER_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.POINTER(C.c_int64), C.POINTER(C.c_int64),
+                        C.c_int32)
+
+
+def set_collectives(ctx: Context, rank: int, world: int, group=None):
+    """The same sharding as set_comm over the torch.distributed process
+    group's own collectives (any backend, e.g. gloo) instead of NCCL: the
+    library stages the int64 hit counts / graph row slices through host
+    memory and calls back into dist.all_reduce / dist.all_gather.  Several
+    ranks may share one GPU this way (nothing on the device waits for another
+    rank); used by the multi-rank tests on a single B200."""
+    import torch
+    import torch.distributed as dist
+
+    def allreduce(_user, values, count):
+        try:
+            a = np.ctypeslib.as_array(values, (int(count),))
+            t = torch.from_numpy(a.copy())
+            dist.all_reduce(t, group=group)
+            a[:] = t.numpy()
+            return 0
+        except Exception:  # noqa: BLE001 - reported to the library as a failed collective
+            return 1
+
+    def gather(_user, send, recv, off, length, n_ranks):
+        try:
+            offs = np.ctypeslib.as_array(off, (int(n_ranks),)).copy()
+            lens = np.ctypeslib.as_array(length, (int(n_ranks),)).copy()
+            m = int(lens.max()) if n_ranks else 0
+            mine = np.zeros(max(m, 1), np.uint8)
+            if lens[rank]:
+                mine[:lens[rank]] = np.ctypeslib.as_array(C.cast(send, C.POINTER(C.c_uint8)), (int(lens[rank]),))
+            parts = [torch.zeros(max(m, 1), dtype=torch.uint8) for _ in range(int(n_ranks))]
+            dist.all_gather(parts, torch.from_numpy(mine), group=group)
+            total = int((offs + lens).max())
+            out = np.ctypeslib.as_array(C.cast(recv, C.POINTER(C.c_uint8)), (max(total, 1),))
+            for r in range(int(n_ranks)):
+                out[offs[r]:offs[r] + lens[r]] = parts[r].numpy()[:lens[r]]
+            return 0
+        except Exception:  # noqa: BLE001
+            return 1
+
+    ctx._coll = (ALLREDUCE_FN(allreduce), GATHER_FN(gather))  # keep the callbacks alive with the context
+    L = lib()
+    L.pump_ctx_set_collectives.argtypes = [C.c_void_p, C.c_int, C.c_int, ALLREDUCE_FN, GATHER_FN, C.c_void_p]
+    _check(L.pump_ctx_set_collectives(ctx.h, rank, world, ctx._coll[0], ctx._coll[1], None))
 
 
 # ------------------------------------------------------- host-side helpers

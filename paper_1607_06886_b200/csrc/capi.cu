@@ -400,6 +400,7 @@ int pump_ctx_io_bytes(pump_ctx* ctx, int64_t* out) {
   out[1] = ctx->c.d2h_bytes;
   out[2] = ctx->c.mc_rollout_steps;
   out[3] = g_dev_allocs;
+  out[4] = ctx->c.collectives;
   return PUMP_OK;
 }
 

@@ -1897,7 +1897,7 @@ int pump_build_graph(pump_ctx* ctx, int32_t n_nodes, int32_t dw, const double* p
                      double tau_max, pump_graph** out) {
   if (!ctx) return PUMP_E_INVALID_ARGUMENT;
   int64_t lo = 0, hi = n_nodes;
-  const bool shard = ctx->c.world > 1 && ctx->c.nccl;
+  const bool shard = ctx->c.has_comm();
   if (shard) shard_range(n_nodes, ctx->c.rank, ctx->c.world, &lo, &hi);
   return build_graph_rows(ctx, n_nodes, dw, pos, vel, ws, goal, r_n, dt, eps_cc, tau_max, static_cast<int32_t>(lo),
                           static_cast<int32_t>(hi), shard, out);

@@ -6,7 +6,9 @@
 #include <dlfcn.h>
 #include <nccl.h>
 
+#include <algorithm>
 #include <cstring>
+#include <stdexcept>
 #include <vector>
 
 #include "ctx.h"
@@ -59,7 +61,18 @@ void shard_range(int64_t n, int rank, int world, int64_t* lo, int64_t* hi) {
 }
 
 void allreduce_sum_i64(Ctx& c, int64_t* d, size_t count) {
-  if (c.world <= 1 || !c.nccl) return;
+  if (!c.has_comm()) return;
+  if (c.host_ar) {  // caller's host collective: stage through host memory
+    std::vector<int64_t> h(count);
+    c.d2h(h.data(), d, count * 8);
+    c.sync();
+    if (c.host_ar(c.host_user, h.data(), static_cast<int64_t>(count)) != 0)
+      throw std::runtime_error("host allreduce failed");
+    c.h2d(d, h.data(), count * 8);
+    c.sync();
+    ++c.collectives;
+    return;
+  }
   const ncclResult_t r = nccl().AllReduce(d, d, count, ncclInt64, ncclSum, static_cast<ncclComm_t>(c.nccl), c.stream);
   if (r != ncclSuccess) throw CudaError(std::string("ncclAllReduce: ") + nccl().GetErrorString(r));
   ++c.collectives;
@@ -70,7 +83,22 @@ void allreduce_sum_i64(Ctx& c, int64_t* d, size_t count) {
 // root; the root's own copy is the broadcast's send -> recv).
 void gather_segments(Ctx& c, const void* send, void* recv, const std::vector<int64_t>& off,
                      const std::vector<int64_t>& len) {
-  if (c.world <= 1 || !c.nccl) throw CudaError("gather_segments: no communicator");
+  if (!c.has_comm()) throw CudaError("gather_segments: no communicator");
+  if (c.host_ar) {
+    if (!c.host_gather) throw std::runtime_error("gather_segments: no host gather");
+    int64_t total = 0;
+    for (int r = 0; r < c.world; ++r) total = std::max(total, off[r] + len[r]);
+    std::vector<char> hs(static_cast<size_t>(len[c.rank]) + 1), hr(static_cast<size_t>(total) + 1);
+    c.d2h(hs.data(), send, static_cast<size_t>(len[c.rank]));
+    c.sync();
+    if (c.host_gather(c.host_user, hs.data(), hr.data(), off.data(), len.data(), c.world) != 0)
+      throw std::runtime_error("host gather failed");
+    for (int r = 0; r < c.world; ++r)
+      if (len[r]) c.h2d(static_cast<char*>(recv) + off[r], hr.data() + off[r], static_cast<size_t>(len[r]));
+    c.sync();
+    ++c.collectives;
+    return;
+  }
   auto& A = nccl();
   auto chk = [&](ncclResult_t r, const char* what) {
     if (r != ncclSuccess) throw CudaError(std::string(what) + ": " + A.GetErrorString(r));
@@ -89,6 +117,9 @@ void gather_segments(Ctx& c, const void* send, void* recv, const std::vector<int
 void comm_destroy(Ctx& c) {
   if (c.nccl) nccl().CommDestroy(static_cast<ncclComm_t>(c.nccl));
   c.nccl = nullptr;
+  c.host_ar = nullptr;
+  c.host_gather = nullptr;
+  c.host_user = nullptr;
   c.world = 1;
   c.rank = 0;
 }
@@ -122,6 +153,21 @@ int pump_ctx_set_comm(pump_ctx* ctx, int rank, int world, const uint8_t* id128) 
     const ncclResult_t r = nccl().CommInitRank(&comm, world, id, rank);
     if (r != ncclSuccess) throw CudaError(std::string("ncclCommInitRank: ") + nccl().GetErrorString(r));
     c.nccl = comm;
+    c.rank = rank;
+    c.world = world;
+  });
+}
+
+int pump_ctx_set_collectives(pump_ctx* ctx, int rank, int world, pump_allreduce_i64_fn allreduce,
+                             pump_gather_fn gather, void* user) {
+  return guard([&] {
+    Ctx& c = ctx->c;
+    comm_destroy(c);
+    if (world <= 1 || !allreduce) return;
+    if (rank < 0 || rank >= world) throw std::invalid_argument("set_collectives: bad rank");
+    c.host_ar = allreduce;
+    c.host_gather = gather;
+    c.host_user = user;
     c.rank = rank;
     c.world = world;
   });

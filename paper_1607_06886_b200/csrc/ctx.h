@@ -34,6 +34,12 @@ struct Ctx {
   // multi-GPU: NCCL communicator for the sharded MC certification
   void* nccl = nullptr;
   int rank = 0, world = 1;
+  // or host collectives supplied by the caller (pump_ctx_set_collectives):
+  // device data is staged through host memory around each call
+  pump_allreduce_i64_fn host_ar = nullptr;
+  pump_gather_fn host_gather = nullptr;
+  void* host_user = nullptr;
+  bool has_comm() const { return world > 1 && (nccl != nullptr || host_ar != nullptr); }
   KProf prof;
   // resident particle bank
   DBuf bank;

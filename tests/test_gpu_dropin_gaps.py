@@ -139,3 +139,61 @@ def test_run_pump_more_than_512_particles(oracle_lib, gpu_ctx):
     got = api.run_pump(api.parse_scenario(txt), ctx=gpu_ctx)
     ref = oracle_lib.run_pump(txt, workers=WORKERS)
     assert_run_equal(got, ref)
+
+
+def coupled_noise_text(samples=500, mc=3000):
+    """quad3d_three_obstacle with full-matrix (cross-axis correlated) process
+    and measurement noise and a coupled tracking weight: the closed loop is
+    not axis-separable, so the dense bank (k_bank_rec<6,3>) and dense MC-table
+    (k_mctab_dense) kernels run (scenario.hpp:110 accepts full matrices)."""
+    j = json.loads(scenario_text("quad3d_three_obstacle"))
+    q = np.diag([0.0, 0.0, 0.0, 3e-4, 3e-4, 3e-4])
+    q[3, 4] = q[4, 3] = 1e-4
+    q[4, 5] = q[5, 4] = -0.5e-4
+    q[0, 3] = q[3, 0] = 1e-6
+    q[0, 0] = 1e-5
+    w = np.diag([5e-4, 5e-4, 5e-4])
+    w[0, 1] = w[1, 0] = 2e-4
+    Q = np.eye(6)
+    Q[0, 1] = Q[1, 0] = 0.3
+    j["noise"]["process"] = q.tolist()
+    j["noise"]["measurement"] = w.tolist()
+    j["tracking"] = {"Q": Q.tolist()}
+    j["samples"] = samples
+    j["mc_samples"] = mc
+    return json.dumps(j)
+
+
+def test_dense_closed_loop_bank_mc_and_solve(oracle_lib, gpu_ctx):
+    from paper_1607_06886_b200 import api
+    from test_gpu_planner import assert_run_equal
+
+    txt = coupled_noise_text()
+    cl, sc = oracle_lib.scenario_models(txt)
+    axis = np.arange(cl["F"].shape[0]) % 3
+    assert np.any((cl["F"] != 0) & (axis[:, None] != axis[None, :]))  # axes coupled: not separable
+    bank = api.presample_bank(cl, 300, 32, 5, ctx=gpu_ctx)
+    ref = oracle_lib.presample_bank(cl, 300, 32, 5, workers=WORKERS)
+    assert np.array_equal(bank.view(np.uint64), ref.view(np.uint64))
+    j = json.loads(txt)
+    ws = ws_of(j)
+    y = np.linspace([1.0, 5.0, 2.0], [2.4, 6.6, 2.0], 60)
+    got = api.mc_certify_batch(cl, ws, [y, y[:30]], 0, 3000, 2, sc["eps_cc"], gpu_ctx)
+    exp = [oracle_lib.mc_hits(cl, ws, t, 0, 3000, 2, sc["eps_cc"], workers=WORKERS) for t in (y, y[:30])]
+    assert [int(x) for x in got] == [int(x) for x in exp]
+    got_r = api.run_pump(api.parse_scenario(txt), ctx=gpu_ctx)
+    assert_run_equal(got_r, oracle_lib.run_pump(txt, workers=WORKERS))
+
+
+@pytest.mark.parametrize("lam", [0.002, 0.01])
+def test_explore_wide_bucket_range_per_kernel_path(oracle_lib, gpu_ctx, lam):
+    """lambda small -> more than 512 distinct bucket keys in a round: the
+    round takes the per-kernel path (two-pass multisplit) instead of the
+    cooperative kernel; records stay equal."""
+    from paper_1607_06886_b200 import api
+
+    og, gg, bank = small_world(oracle_lib, gpu_ctx, 777, 64)
+    ref = oracle_lib.explore(og, bank, 0.01, 0.2, lam, 9.0, workers=WORKERS)
+    got = api.explore(gg, 0.01, 0.2, lam, 9.0, ctx=gpu_ctx)
+    assert ref["rounds"] > 20
+    explore_equal(got, ref)
