@@ -1001,61 +1001,37 @@ inline bool nominal_free(const Workspace& w, const Trajectory& traj, double eps_
 }
 }  // namespace detail
 
-// smooth (pump.hpp:84-146): host bisection, each probe certified on the GPU
+// smooth (pump.hpp:84-146) on the GPU: the same device chain run_pump uses
+// (blend + nominal check + MC of each bisection probe in depth-2 speculative
+// batches, one synchronisation; pump_smooth)
 inline SmoothResult smooth(const Trajectory& plan_traj, double plan_mc, double alpha, const ClosedLoopDynamics& cl,
                            const Workspace& w, int n_mc, std::uint64_t mc_seed, double eps_cc, int workers = 1) {
-  SmoothResult best;
-  best.traj = plan_traj;
-  best.cost = trajectory_cost(plan_traj);
-  best.mc = plan_mc;
-  if (plan_traj.points.size() < 2) return best;
-  const Motion opt =
-      fixed_time_connect(plan_traj.points.front().state, plan_traj.points.back().state, plan_traj.duration());
-  auto blend = [&](double s) {
-    Trajectory t;
-    for (const auto& wp : plan_traj.points) {
-      Waypoint b;
-      b.t = wp.t;
-      const State o = opt.state_at(wp.t);
-      b.state.position = (1 - s) * wp.state.position + s * o.position;
-      b.state.velocity = (1 - s) * wp.state.velocity + s * o.velocity;
-      b.control = (1 - s) * wp.control + s * opt.control_at(wp.t);
-      t.points.push_back(std::move(b));
-    }
-    return t;
-  };
-  auto certify = [&](const Trajectory& t, double& mc_out) {
-    if (!detail::nominal_free(w, t, eps_cc)) return false;
-    mc_out = mc_certify(t.positions(), cl, w, n_mc, mc_seed, eps_cc, workers).value;
-    return mc_out <= alpha;
-  };
-  auto accept = [&](double s, const Trajectory& t, double mc) {
-    best.traj = t;
-    best.cost = trajectory_cost(t);
-    best.mc = mc;
-    best.s = s;
-  };
-  {
-    Trajectory t = blend(1.0);
-    double mc;
-    if (certify(t, mc)) {
-      accept(1.0, t, mc);
-      return best;
+  (void)workers;
+  const int n = static_cast<int>(plan_traj.points.size()), dw = cl.dw;
+  std::vector<double> t(n + 1), p(static_cast<size_t>(n) * dw + 1), v(p.size()), u(p.size());
+  for (int q = 0; q < n; ++q) {
+    const Waypoint& wp = plan_traj.points[q];
+    t[q] = wp.t;
+    for (int k = 0; k < dw; ++k) {
+      p[q * dw + k] = wp.state.position[k];
+      v[q * dw + k] = wp.state.velocity[k];
+      u[q * dw + k] = wp.control[k];
     }
   }
-  double lo = 0, hi = 1;
-  for (int it = 0; it < 10; ++it) {
-    const double mid = 0.5 * (lo + hi);
-    Trajectory t = blend(mid);
-    double mc;
-    if (certify(t, mc)) {
-      accept(mid, t, mc);
-      lo = mid;
-    } else {
-      hi = mid;
-    }
-  }
-  return best;
+  detail::LoopView lv(cl);
+  detail::WsView wv(w);
+  std::vector<double> op(p.size()), ov(p.size()), ou(p.size());
+  double out3[3] = {0, 0, 0};
+  detail::check(pump_smooth(detail::ctx(), &lv.v, &wv.v, n, t.data(), p.data(), v.data(), u.data(), plan_mc, alpha,
+                            n_mc, mc_seed, eps_cc, op.data(), ov.data(), ou.data(), out3));
+  SmoothResult r;
+  for (int q = 0; q < n; ++q)
+    r.traj.points.push_back({t[q], {detail::vec(op.data() + q * dw, dw), detail::vec(ov.data() + q * dw, dw)},
+                             detail::vec(ou.data() + q * dw, dw)});
+  r.cost = out3[0];
+  r.mc = out3[1];
+  r.s = out3[2];
+  return r;
 }
 
 // ========================================================== scenario.hpp

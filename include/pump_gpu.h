@@ -279,6 +279,18 @@ int pump_mc_certify_batch(pump_ctx* ctx, const pump_closed_loop* cl, const pump_
                           uint64_t seed, double eps_cc, int64_t* hits_out);
 /* Single-trajectory convenience with the reference's signature semantics;
  * value_out = n_hit / n_mc. */
+/* smooth (pump.hpp:84-146): blend the plan trajectory (n_points waypoints:
+ * times t, positions / velocities / controls n_points x dw) toward the
+ * fixed-time optimal motion between its end states; the blend fraction is
+ * bisected (s = 1, then 10 midpoints), each probe a nominal collision check
+ * and an MC certification with (n_mc, seed, eps_cc), in depth-2 speculative
+ * device batches exactly as run_pump does.  plan_mc is the plan's own MC CP
+ * (kept when no blend certifies).  Out: the accepted trajectory (same times),
+ * out3 = {cost, certified CP, s}. */
+int pump_smooth(pump_ctx* ctx, const pump_closed_loop* cl, const pump_workspace* ws, int32_t n_points,
+                const double* t, const double* pos, const double* vel, const double* ctrl, double plan_mc,
+                double alpha, int32_t n_mc, uint64_t seed, double eps_cc, double* out_pos, double* out_vel,
+                double* out_ctrl, double* out3);
 int pump_mc_certify(pump_ctx* ctx, const pump_closed_loop* cl, const pump_workspace* ws, int32_t n_points,
                     const double* y_nom, int32_t n_mc, uint64_t seed, double eps_cc, double* value_out);
 

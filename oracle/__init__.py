@@ -241,6 +241,26 @@ def mc_certify(cl, ws, y_nom, n_mc, seed, eps_cc, workers=1):
 
 
 # ------------------------------------------------------------ steer / geom
+def smooth(t, pos, vel, ctrl, plan_mc, alpha, cl, ws, n_mc, seed, eps_cc, workers=1) -> dict:
+    """pump.hpp:84-146 (the restatement's smooth)."""
+    keep = A.Keep()
+    cls = A.closed_loop_struct(cl, keep)
+    wss = A.workspace_struct(ws, keep)
+    dw = cl["dw"]
+    t = np.ascontiguousarray(t, dtype=np.float64)
+    n = t.shape[0]
+    arrs = [np.ascontiguousarray(a, dtype=np.float64).reshape(n, dw) for a in (pos, vel, ctrl)]
+    outs = [np.zeros((n, dw)) for _ in range(3)]
+    out3 = np.zeros(3)
+    L = lib()
+    L.oracle_smooth.argtypes = [C.c_void_p, C.c_void_p, C.c_int] + [C.c_void_p] * 4 + \
+        [C.c_double, C.c_double, C.c_int, C.c_uint64, C.c_double, C.c_int] + [C.c_void_p] * 4
+    _check(L.oracle_smooth(C.byref(cls), C.byref(wss), n, _p(t), *[_p(a) for a in arrs], plan_mc, alpha, n_mc,
+                           C.c_uint64(seed), eps_cc, workers, *[_p(o) for o in outs], _p(out3)))
+    return {"traj_pos": outs[0], "traj_vel": outs[1], "traj_ctrl": outs[2], "cost": float(out3[0]),
+            "mc": float(out3[1]), "s": float(out3[2])}
+
+
 def connect(ap, av, bp, bv, tau_max):
     dw = len(ap)
     arr = [np.ascontiguousarray(x, dtype=np.float64) for x in (ap, av, bp, bv)]

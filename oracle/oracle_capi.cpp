@@ -187,6 +187,33 @@ int oracle_mc_hits(const pump_closed_loop* cl, const pump_workspace* ws, int n_p
   });
 }
 
+// smooth (pump.hpp:84-146) of a plan trajectory: out3 = {cost, mc, s}
+int oracle_smooth(const pump_closed_loop* cl, const pump_workspace* ws, int n_points, const double* t,
+                  const double* pos, const double* vel, const double* ctrl, double plan_mc, double alpha, int n_mc,
+                  uint64_t seed, double eps_cc, int workers, double* out_pos, double* out_vel, double* out_ctrl,
+                  double* out3) {
+  return guard([&] {
+    const int dw = cl->dw;
+    std::vector<Wp> plan(n_points);
+    for (int q = 0; q < n_points; ++q) {
+      plan[q].t = t[q];
+      plan[q].s.p.assign(pos + q * dw, pos + (q + 1) * dw);
+      plan[q].s.v.assign(vel + q * dw, vel + (q + 1) * dw);
+      plan[q].u.assign(ctrl + q * dw, ctrl + (q + 1) * dw);
+    }
+    Smooth r = smooth(plan, plan_mc, alpha, loop_from(cl), world_from(ws), n_mc, seed, eps_cc, workers);
+    for (int q = 0; q < n_points; ++q)
+      for (int k = 0; k < dw; ++k) {
+        out_pos[q * dw + k] = r.traj[q].s.p[k];
+        out_vel[q * dw + k] = r.traj[q].s.v[k];
+        out_ctrl[q * dw + k] = r.traj[q].u[k];
+      }
+    out3[0] = r.cost;
+    out3[1] = r.mc;
+    out3[2] = r.s;
+  });
+}
+
 int oracle_mc_certify(const pump_closed_loop* cl, const pump_workspace* ws, int n_points, const double* y_nom,
                       int n_mc, uint64_t seed, double eps_cc, int workers, double* value) {
   if (n_mc < 1) {

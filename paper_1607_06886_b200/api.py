@@ -58,7 +58,7 @@ EXPORTS = [
     "pump_last_error", "pump_abi_version", "pump_ctx_create", "pump_ctx_destroy", "pump_ctx_last_kernel_ms",
     "pump_ctx_launch_count", "pump_scenario_parse", "pump_scenario_load", "pump_scenario_free",
     "pump_scenario_closed_loop", "pump_scenario_params", "pump_presample_bank", "pump_bank_upload",
-    "pump_hsmc_extend_batch", "pump_explore_run_hooked", "pump_mc_certify_batch", "pump_mc_certify", "pump_build_graph", "pump_graph_upload",
+    "pump_hsmc_extend_batch", "pump_explore_run_hooked", "pump_smooth", "pump_mc_certify_batch", "pump_mc_certify", "pump_build_graph", "pump_graph_upload",
     "pump_graph_counts", "pump_graph_export", "pump_graph_free", "pump_explore_run", "pump_explore_counts",
     "pump_explore_export", "pump_explore_free", "pump_run", "pump_result_summary_get", "pump_result_arrays",
     "pump_result_free", "pump_nccl_unique_id", "pump_ctx_set_comm", "pump_ctx_set_collectives", "pump_shard_range", "pump_ctx_profile",
@@ -338,6 +338,30 @@ def mc_certify_batch(cl: dict, ws: dict, trajectories, rollout_lo: int, rollout_
     _check(lib().pump_mc_certify_batch(ctx.h, C.byref(cls), C.byref(wss), len(ys), _p(off), _p(y), rollout_lo,
                                        rollout_hi, C.c_uint64(seed), eps_cc, _p(hits)))
     return hits
+
+
+def smooth(t, pos, vel, ctrl, plan_mc: float, alpha: float, cl: dict, ws: dict, n_mc: int, seed: int,
+           eps_cc: float, ctx: Context | None = None) -> dict:
+    """smooth (pump.hpp:84-146) of a plan trajectory on the device (the
+    speculative bisection chain run_pump uses): {traj_pos, traj_vel,
+    traj_ctrl, cost, mc, s}; times are the plan's."""
+    ctx = ctx or default_context()
+    keep = A.Keep()
+    cls = A.closed_loop_struct(cl, keep)
+    wss = A.workspace_struct(ws, keep)
+    dw = cl["dw"]
+    t = np.ascontiguousarray(t, dtype=np.float64)
+    n = t.shape[0]
+    arrs = [np.ascontiguousarray(a, dtype=np.float64).reshape(n, dw) for a in (pos, vel, ctrl)]
+    outs = [np.zeros((n, dw)) for _ in range(3)]
+    out3 = np.zeros(3)
+    L = lib()
+    L.pump_smooth.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32] + [C.c_void_p] * 4 + \
+        [C.c_double, C.c_double, C.c_int32, C.c_uint64, C.c_double] + [C.c_void_p] * 4
+    _check(L.pump_smooth(ctx.h, C.byref(cls), C.byref(wss), n, _p(t), *[_p(a) for a in arrs], plan_mc, alpha, n_mc,
+                         C.c_uint64(seed), eps_cc, *[_p(o) for o in outs], _p(out3)))
+    return {"traj_pos": outs[0], "traj_vel": outs[1], "traj_ctrl": outs[2], "cost": float(out3[0]),
+            "mc": float(out3[1]), "s": float(out3[2])}
 
 
 def mc_certify(y_nom, cl: dict, ws: dict, n_mc: int, seed: int, eps_cc: float, ctx: Context | None = None) -> float:

@@ -909,6 +909,322 @@ static HostLoop loop_of(const pumpb::ClosedLoop& cl) {
 }
 
 // run_pump (pump.hpp:170-263)
+// smooth (pump.hpp:84-146) on the device: the plan trajectory blended toward
+// the fixed-time optimal motion between its end states, the blend fraction
+// bisected (s = 1, then 10 midpoints), each probe a nominal collision check
+// + one MC certification.  Used by run_pump and by pump_smooth.
+struct SmoothOut {
+  std::vector<HWp> traj;
+  double cost = 0, mc = 0, s = 0;
+};
+static SmoothOut smooth_device(Ctx& c, const std::vector<HWp>& plan, double plan_mc, double alpha,
+                               const HostLoop& L, const DevWorld& dwld, const HostWorld& hw, int64_t n_mc,
+                               uint64_t seed, double eps_cc, int dw, double* mc_ms, int64_t* mc_rollouts) {
+  // smoothing (pump.hpp:84-146).  The reference bisects the blend fraction
+  // s sequentially (s = 1, then 10 midpoints), each probe a nominal
+  // collision check + one MC certification.  The probes form a dyadic tree,
+  // so whole subtrees are evaluated speculatively in one batched MC launch
+  // (candidates whose blended nominal collides get no MC, as in the
+  // reference) and the bisection is then replayed from the memo: the accepted
+  // s, trajectory and certified CP are exactly the reference's.
+  std::vector<HWp> best = plan;
+  double best_cost = trajectory_cost(plan, dw), best_mc = plan_mc, best_s = 0;
+  if (plan.size() >= 2) {
+    HMotion opt{};
+    std::memcpy(opt.p0, plan.front().p, sizeof(opt.p0));
+    std::memcpy(opt.v0, plan.front().v, sizeof(opt.v0));
+    std::memcpy(opt.p1, plan.back().p, sizeof(opt.p1));
+    std::memcpy(opt.v1, plan.back().v, sizeof(opt.v1));
+    opt.tau = plan.back().t;
+    fixed_time(opt, dw);
+    auto blend = [&](double sv) {
+      std::vector<HWp> t(plan.size());
+      for (size_t q = 0; q < plan.size(); ++q) {
+        const HWp& wp = plan[q];
+        HWp& b = t[q];
+        b = HWp{};
+        b.t = wp.t;
+        double op[6], ov[6], ou[6];
+        state_at(opt, dw, wp.t, op, ov);
+        control_at(opt, dw, wp.t, ou);
+        for (int k = 0; k < dw; ++k) {
+          b.p[k] = (1 - sv) * wp.p[k] + sv * op[k];
+          b.v[k] = (1 - sv) * wp.v[k] + sv * ov[k];
+          b.u[k] = (1 - sv) * wp.u[k] + sv * ou[k];
+        }
+      }
+      return t;
+    };
+    struct Probe {
+      std::vector<HWp> traj;
+      bool free = false;
+      double mc = 1.0;
+    };
+    std::map<double, Probe> probes;
+    // evaluate the candidates not yet probed: nominal check, then one MC batch
+    auto evaluate = [&](const std::vector<double>& cands) {
+      std::vector<double> todo;
+      std::vector<std::vector<HWp>> batch;
+      for (double sv : cands) {
+        if (probes.count(sv)) continue;
+        Probe p;
+        p.traj = blend(sv);
+        p.free = nominal_free(hw, p.traj, eps_cc);
+        if (p.free) {
+          todo.push_back(sv);
+          batch.push_back(p.traj);
+        }
+        probes.emplace(sv, std::move(p));
+      }
+      if (batch.empty()) return;
+      auto v = mc_values(c, L, dwld, batch, n_mc, seed, eps_cc, mc_ms, mc_rollouts);
+      for (size_t k = 0; k < todo.size(); ++k) probes[todo[k]].mc = v[k];
+    };
+    // the same on the device: blend, nominal check and MC of every new
+    // candidate in one batch (one synchronisation); MC of a candidate whose
+    // nominal collides is computed but never used (the reference skips it)
+    static const bool host_probes = std::getenv("PUMP_SMOOTH_HOST") != nullptr;
+    const int n_wp = static_cast<int>(plan.size());
+    if (!host_probes) {
+      // the plan's times, positions and velocities in one upload
+      std::vector<double> pl(static_cast<size_t>(n_wp) * (1 + 2 * dw));
+      for (int q = 0; q < n_wp; ++q) {
+        pl[q] = plan[q].t;
+        for (int k = 0; k < dw; ++k) {
+          pl[n_wp + q * dw + k] = plan[q].p[k];
+          pl[n_wp * (1 + dw) + q * dw + k] = plan[q].v[k];
+        }
+      }
+      c.h2d(c.buf("sm_plan", pl.size() * 8 + 256).p, pl.data(), pl.size() * 8);
+    }
+    auto evaluate_dev = [&](const std::vector<double>& cands) {
+      std::vector<double> todo;
+      for (double sv : cands)
+        if (!probes.count(sv) && std::find(todo.begin(), todo.end(), sv) == todo.end()) todo.push_back(sv);
+      const int np = static_cast<int>(todo.size());
+      if (np == 0) return;
+      const int64_t items = static_cast<int64_t>(np) * n_wp;
+      DBuf& d_y = c.buf("sm_y", items * dw * 8 + 256);
+      DBuf& d_yv = c.buf("sm_yv", items * dw * 8 + 256);
+      // one upload (s values, MC offsets) and one download (hits, free flags)
+      DBuf& d_in = c.buf("sm_in", (2 * np + 1) * 8 + 256);
+      DBuf& d_out = c.buf("sm_out", (np + 1) * 8 + np * 4 + 256);
+      std::vector<int64_t> in(2 * np + 1);
+      std::memcpy(in.data(), todo.data(), np * 8);
+      for (int k = 0; k <= np; ++k) in[np + k] = static_cast<int64_t>(k) * n_wp;
+      c.h2d(d_in.p, in.data(), (2 * np + 1) * 8);
+      const double* d_s = d_in.as<double>();
+      const int64_t* d_off = d_in.as<int64_t>() + np;
+      unsigned long long* d_h = d_out.as<unsigned long long>();
+      int32_t* d_free = reinterpret_cast<int32_t*>(d_out.as<int64_t>() + np + 1);
+      PUMP_CUDA(cudaMemsetAsync(d_h, 0, (np + 1) * 8, c.stream));
+      PUMP_CUDA(cudaMemsetAsync(d_free, 1, np * 4, c.stream));  // nonzero: free until a check fails
+      WorldD wd;
+      wd.n_obs = dwld.n_obs;
+      wd.lo = dwld.d_lo;
+      wd.hi = dwld.d_hi;
+      for (int k = 0; k < 6; ++k) {
+        wd.blo[k] = dwld.blo[k];
+        wd.bhi[k] = dwld.bhi[k];
+      }
+      c.tic();
+      dispatch_dw(dw, [&]<int DW>() {
+        HMotion o = opt;
+        k_smooth_blend<DW><<<grid_for(items, 128), 128, 0, c.stream>>>(
+            np, n_wp, d_s, c.scratch["sm_plan"].as<double>(), c.scratch["sm_plan"].as<double>() + n_wp,
+            c.scratch["sm_plan"].as<double>() + n_wp * (1 + dw), as_motion<DW>(o), d_y.as<double>(), d_yv.as<double>());
+        k_smooth_check<DW><<<grid_for(items, 128), 128, 0, c.stream>>>(
+            wd, np, n_wp, c.scratch["sm_plan"].as<double>(), d_y.as<double>(), d_yv.as<double>(), eps_cc, d_free);
+      });
+      c.launches += 2;
+      PUMP_CUDA(cudaGetLastError());
+      int64_t r0 = 0, r1 = n_mc;
+      shard_range(n_mc, c.rank, c.world, &r0, &r1);
+      if (c.mc_join_pending) {
+        PUMP_CUDA(cudaStreamWaitEvent(c.stream, c.join, 0));
+        c.mc_join_pending = false;
+      }
+      launch_mc(L, dwld, np, d_off, d_y.as<double>(), n_wp, r0, r1, seed, eps_cc, d_h, c.stream, &c.launches,
+                d_h + np, &c.mc_table, d_free);
+      allreduce_sum_i64(c, reinterpret_cast<int64_t*>(d_h), np);
+      std::vector<int64_t> outv(np + 1 + (np + 1) / 2);
+      c.d2h(outv.data(), d_out.p, (np + 1) * 8 + np * 4);
+      const int64_t* hits = outv.data();
+      const int32_t* fr = reinterpret_cast<const int32_t*>(outv.data() + np + 1);
+      *mc_ms += c.toc();
+      c.sync();
+      kprof_work(F_MC, hits[np]);
+      c.mc_rollout_steps += hits[np];
+      for (int k = 0; k < np; ++k) {
+        Probe p;
+        p.free = fr[k] != 0;
+        if (p.free) {
+          p.mc = static_cast<double>(hits[k]) / n_mc;
+          *mc_rollouts += r1 - r0;
+        }
+        probes.emplace(todo[k], std::move(p));
+      }
+    };
+    auto run_probes = [&](const std::vector<double>& cands) {
+      if (host_probes)
+        evaluate(cands);
+      else
+        evaluate_dev(cands);
+    };
+    auto certified = [&](double sv) {
+      const Probe& p = probes.at(sv);
+      return p.free && p.mc <= alpha;
+    };
+    auto subtree = [&](double lo, double hi, int depth, std::vector<double>& out) {
+      // all midpoints the bisection can visit in its next `depth` steps
+      std::vector<std::pair<double, double>> level{{lo, hi}};
+      for (int d = 0; d < depth; ++d) {
+        std::vector<std::pair<double, double>> next;
+        for (auto [a, b] : level) {
+          const double mid = 0.5 * (a + b);
+          out.push_back(mid);
+          next.push_back({mid, b});
+          next.push_back({a, mid});
+        }
+        level.swap(next);
+      }
+    };
+    auto accept = [&](double sv) {
+      Probe& p = probes.at(sv);
+      if (p.traj.empty()) p.traj = blend(sv);  // device probes keep only the verdicts
+      best = p.traj;
+      best_cost = trajectory_cost(p.traj, dw);
+      best_mc = p.mc;
+      best_s = sv;
+    };
+    // Batch schedule: depths of the speculative subtrees covering the 10
+    // bisection steps.  Host probes (PUMP_SMOOTH_HOST=1): one probe per MC
+    // launch.  Device probes (default): depth-2 subtrees, 3 candidates per
+    // batch (blend + nominal check + MC in one round trip).
+    // PUMP_SMOOTH_SCHEDULE="3,3,4" overrides.
+    std::vector<int> schedule(10, 1);
+    if (!host_probes) schedule = {2, 2, 2, 2, 2};  // PUMP_SMOOTH_SCHEDULE with device probes: speculative subtrees
+    if (const char* e = std::getenv("PUMP_SMOOTH_SCHEDULE")) {
+      schedule.clear();
+      for (const char* q = e; *q;) {
+        schedule.push_back(std::max(1, std::atoi(q)));
+        while (*q && *q != ',') ++q;
+        if (*q == ',') ++q;
+      }
+    }
+    static const bool spec = std::getenv("PUMP_SMOOTH_SCHEDULE") != nullptr;
+    if (!host_probes && !spec) {
+      // five batches enqueued at once, each deciding on the device from the
+      // previous batch's verdicts; one synchronisation for the whole bisection
+      const int64_t items = static_cast<int64_t>(4) * n_wp;
+      DBuf& d_y = c.buf("sm_y", items * dw * 8 + 256);
+      DBuf& d_yv = c.buf("sm_yv", items * dw * 8 + 256);
+      DBuf& d_ch = c.buf("sm_chain", sizeof(SmoothChain) + 256);
+      DBuf& d_off = c.buf("sm_choff", 256);
+      const int64_t offs[5] = {0, n_wp, 2 * static_cast<int64_t>(n_wp), 3 * static_cast<int64_t>(n_wp),
+                               4 * static_cast<int64_t>(n_wp)};
+      c.h2d(d_off.p, offs, sizeof(offs));
+      SmoothChain* ch = d_ch.as<SmoothChain>();
+      WorldD wd;
+      wd.n_obs = dwld.n_obs;
+      wd.lo = dwld.d_lo;
+      wd.hi = dwld.d_hi;
+      for (int k = 0; k < 6; ++k) {
+        wd.blo[k] = dwld.blo[k];
+        wd.bhi[k] = dwld.bhi[k];
+      }
+      int64_t r0 = 0, r1 = n_mc;
+      shard_range(n_mc, c.rank, c.world, &r0, &r1);
+      if (c.mc_join_pending) {
+        PUMP_CUDA(cudaStreamWaitEvent(c.stream, c.join, 0));
+        c.mc_join_pending = false;
+      }
+      c.tic();
+      for (int b = 0; b < 5; ++b) {
+        const int q0 = b == 0 ? 0 : 4 + 3 * (b - 1), np = b == 0 ? 4 : 3;
+        const int64_t it = static_cast<int64_t>(np) * n_wp;
+        k_smooth_decide<<<1, 1, 0, c.stream>>>(ch, b, n_mc, alpha);
+        dispatch_dw(dw, [&]<int DW>() {
+          HMotion o = opt;
+          k_smooth_blend<DW><<<grid_for(it, 128), 128, 0, c.stream>>>(
+              np, n_wp, &ch->s[q0], c.scratch["sm_plan"].as<double>(), c.scratch["sm_plan"].as<double>() + n_wp,
+              c.scratch["sm_plan"].as<double>() + n_wp * (1 + dw), as_motion<DW>(o), d_y.as<double>(),
+              d_yv.as<double>());
+          k_smooth_check<DW><<<grid_for(it, 128), 128, 0, c.stream>>>(
+              wd, np, n_wp, c.scratch["sm_plan"].as<double>(), d_y.as<double>(), d_yv.as<double>(), eps_cc,
+              &ch->live[q0]);
+        });
+        c.launches += 3;
+        launch_mc(L, dwld, np, d_off.as<int64_t>(), d_y.as<double>(), n_wp, r0, r1, seed, eps_cc,
+                  &ch->hits[q0], c.stream, &c.launches, &ch->steps, &c.mc_table, &ch->live[q0]);
+        allreduce_sum_i64(c, reinterpret_cast<int64_t*>(&ch->hits[q0]), np);
+        PUMP_CUDA(cudaGetLastError());
+      }
+      SmoothChain hc{};
+      c.d2h(&hc, ch, sizeof(SmoothChain));
+      *mc_ms += c.toc();
+      c.sync();
+      kprof_work(F_MC, static_cast<int64_t>(hc.steps));
+      c.mc_rollout_steps += static_cast<int64_t>(hc.steps);
+      for (int q = 0; q < kSmoothSlots; ++q) {  // every probe the batches evaluated
+        if (probes.count(hc.s[q]) || (q > 0 && hc.done)) continue;
+        Probe p;
+        p.free = hc.live[q] != 0;
+        if (p.free) {
+          p.mc = static_cast<double>(hc.hits[q]) / n_mc;
+          *mc_rollouts += r1 - r0;
+        }
+        probes.emplace(hc.s[q], std::move(p));
+      }
+      // replay (pump.hpp:118-141) from the history (probes.at throws if a
+      // probe the bisection visits was not evaluated on the device)
+      if (certified(1.0)) {
+        accept(1.0);
+      } else {
+        double lo = 0, hi = 1;
+        for (int k = 1; k <= 10; ++k) {
+          const double mid = 0.5 * (lo + hi);
+          if (!probes.count(mid)) throw std::runtime_error("smoothing: device bisection diverged from the host replay");
+          if (certified(mid)) {
+            accept(mid);
+            lo = mid;
+          } else {
+            hi = mid;
+          }
+        }
+      }
+    } else {
+    run_probes({1.0});
+    if (certified(1.0)) {
+      accept(1.0);
+    } else {
+      double lo = 0, hi = 1;
+      int it = 0;
+      for (size_t b = 0; b < schedule.size() && it < 10; ++b) {
+        std::vector<double> more;
+        subtree(lo, hi, std::min(schedule[b], 10 - it), more);
+        run_probes(more);
+        for (int d = 0; d < schedule[b] && it < 10; ++d, ++it) {
+          const double mid = 0.5 * (lo + hi);
+          if (certified(mid)) {
+            accept(mid);
+            lo = mid;
+          } else {
+            hi = mid;
+          }
+        }
+      }
+    }
+    }
+  }
+  SmoothOut o;
+  o.traj = std::move(best);
+  o.cost = best_cost;
+  o.mc = best_mc;
+  o.s = best_s;
+  return o;
+}
+
 static void run_pump_device(Ctx& c, const pumpb::Scenario& s, const DevGraph* prebuilt, pump_result& R) {
   c.mc_table.invalidate();  // the MC table is built inside every solve (no state across solves)
   using clk = std::chrono::steady_clock;
@@ -1222,309 +1538,15 @@ static void run_pump_device(Ctx& c, const pumpb::Scenario& s, const DevGraph* pr
     R.s.cp_hat = cph;
     R.s.pre_smoothing_cost = cst;
   }
-  // smoothing (pump.hpp:84-146).  The reference bisects the blend fraction
-  // s sequentially (s = 1, then 10 midpoints), each probe a nominal
-  // collision check + one MC certification.  The probes form a dyadic tree,
-  // so whole subtrees are evaluated speculatively in one batched MC launch
-  // (candidates whose blended nominal collides get no MC, as in the
-  // reference) and the bisection is then replayed from the memo: the accepted
-  // s, trajectory and certified CP are exactly the reference's.
-  const std::vector<HWp>& plan = plan_sel;
-  std::vector<HWp> best = plan;
-  double best_cost = trajectory_cost(plan, dw), best_mc = memo[sel], best_s = 0;
-  if (plan.size() >= 2) {
-    HMotion opt{};
-    std::memcpy(opt.p0, plan.front().p, sizeof(opt.p0));
-    std::memcpy(opt.v0, plan.front().v, sizeof(opt.v0));
-    std::memcpy(opt.p1, plan.back().p, sizeof(opt.p1));
-    std::memcpy(opt.v1, plan.back().v, sizeof(opt.v1));
-    opt.tau = plan.back().t;
-    fixed_time(opt, dw);
-    auto blend = [&](double sv) {
-      std::vector<HWp> t(plan.size());
-      for (size_t q = 0; q < plan.size(); ++q) {
-        const HWp& wp = plan[q];
-        HWp& b = t[q];
-        b = HWp{};
-        b.t = wp.t;
-        double op[6], ov[6], ou[6];
-        state_at(opt, dw, wp.t, op, ov);
-        control_at(opt, dw, wp.t, ou);
-        for (int k = 0; k < dw; ++k) {
-          b.p[k] = (1 - sv) * wp.p[k] + sv * op[k];
-          b.v[k] = (1 - sv) * wp.v[k] + sv * ov[k];
-          b.u[k] = (1 - sv) * wp.u[k] + sv * ou[k];
-        }
-      }
-      return t;
-    };
-    struct Probe {
-      std::vector<HWp> traj;
-      bool free = false;
-      double mc = 1.0;
-    };
-    std::map<double, Probe> probes;
-    // evaluate the candidates not yet probed: nominal check, then one MC batch
-    auto evaluate = [&](const std::vector<double>& cands) {
-      std::vector<double> todo;
-      std::vector<std::vector<HWp>> batch;
-      for (double sv : cands) {
-        if (probes.count(sv)) continue;
-        Probe p;
-        p.traj = blend(sv);
-        p.free = nominal_free(hw, p.traj, eps_cc);
-        if (p.free) {
-          todo.push_back(sv);
-          batch.push_back(p.traj);
-        }
-        probes.emplace(sv, std::move(p));
-      }
-      if (batch.empty()) return;
-      auto v = mc_values(c, L, dwld, batch, s.mc_samples, s.seeds.mc, eps_cc, &R.s.mc_ms, &R.s.mc_rollouts);
-      for (size_t k = 0; k < todo.size(); ++k) probes[todo[k]].mc = v[k];
-    };
-    // the same on the device: blend, nominal check and MC of every new
-    // candidate in one batch (one synchronisation); MC of a candidate whose
-    // nominal collides is computed but never used (the reference skips it)
-    static const bool host_probes = std::getenv("PUMP_SMOOTH_HOST") != nullptr;
-    const int n_wp = static_cast<int>(plan.size());
-    if (!host_probes) {
-      // the plan's times, positions and velocities in one upload
-      std::vector<double> pl(static_cast<size_t>(n_wp) * (1 + 2 * dw));
-      for (int q = 0; q < n_wp; ++q) {
-        pl[q] = plan[q].t;
-        for (int k = 0; k < dw; ++k) {
-          pl[n_wp + q * dw + k] = plan[q].p[k];
-          pl[n_wp * (1 + dw) + q * dw + k] = plan[q].v[k];
-        }
-      }
-      c.h2d(c.buf("sm_plan", pl.size() * 8 + 256).p, pl.data(), pl.size() * 8);
-    }
-    auto evaluate_dev = [&](const std::vector<double>& cands) {
-      std::vector<double> todo;
-      for (double sv : cands)
-        if (!probes.count(sv) && std::find(todo.begin(), todo.end(), sv) == todo.end()) todo.push_back(sv);
-      const int np = static_cast<int>(todo.size());
-      if (np == 0) return;
-      const int64_t items = static_cast<int64_t>(np) * n_wp;
-      DBuf& d_y = c.buf("sm_y", items * dw * 8 + 256);
-      DBuf& d_yv = c.buf("sm_yv", items * dw * 8 + 256);
-      // one upload (s values, MC offsets) and one download (hits, free flags)
-      DBuf& d_in = c.buf("sm_in", (2 * np + 1) * 8 + 256);
-      DBuf& d_out = c.buf("sm_out", (np + 1) * 8 + np * 4 + 256);
-      std::vector<int64_t> in(2 * np + 1);
-      std::memcpy(in.data(), todo.data(), np * 8);
-      for (int k = 0; k <= np; ++k) in[np + k] = static_cast<int64_t>(k) * n_wp;
-      c.h2d(d_in.p, in.data(), (2 * np + 1) * 8);
-      const double* d_s = d_in.as<double>();
-      const int64_t* d_off = d_in.as<int64_t>() + np;
-      unsigned long long* d_h = d_out.as<unsigned long long>();
-      int32_t* d_free = reinterpret_cast<int32_t*>(d_out.as<int64_t>() + np + 1);
-      PUMP_CUDA(cudaMemsetAsync(d_h, 0, (np + 1) * 8, c.stream));
-      PUMP_CUDA(cudaMemsetAsync(d_free, 1, np * 4, c.stream));  // nonzero: free until a check fails
-      WorldD wd;
-      wd.n_obs = dwld.n_obs;
-      wd.lo = dwld.d_lo;
-      wd.hi = dwld.d_hi;
-      for (int k = 0; k < 6; ++k) {
-        wd.blo[k] = dwld.blo[k];
-        wd.bhi[k] = dwld.bhi[k];
-      }
-      c.tic();
-      dispatch_dw(dw, [&]<int DW>() {
-        HMotion o = opt;
-        k_smooth_blend<DW><<<grid_for(items, 128), 128, 0, c.stream>>>(
-            np, n_wp, d_s, c.scratch["sm_plan"].as<double>(), c.scratch["sm_plan"].as<double>() + n_wp,
-            c.scratch["sm_plan"].as<double>() + n_wp * (1 + dw), as_motion<DW>(o), d_y.as<double>(), d_yv.as<double>());
-        k_smooth_check<DW><<<grid_for(items, 128), 128, 0, c.stream>>>(
-            wd, np, n_wp, c.scratch["sm_plan"].as<double>(), d_y.as<double>(), d_yv.as<double>(), eps_cc, d_free);
-      });
-      c.launches += 2;
-      PUMP_CUDA(cudaGetLastError());
-      int64_t r0 = 0, r1 = s.mc_samples;
-      shard_range(s.mc_samples, c.rank, c.world, &r0, &r1);
-      if (c.mc_join_pending) {
-        PUMP_CUDA(cudaStreamWaitEvent(c.stream, c.join, 0));
-        c.mc_join_pending = false;
-      }
-      launch_mc(L, dwld, np, d_off, d_y.as<double>(), n_wp, r0, r1, s.seeds.mc, eps_cc, d_h, c.stream, &c.launches,
-                d_h + np, &c.mc_table, d_free);
-      allreduce_sum_i64(c, reinterpret_cast<int64_t*>(d_h), np);
-      std::vector<int64_t> outv(np + 1 + (np + 1) / 2);
-      c.d2h(outv.data(), d_out.p, (np + 1) * 8 + np * 4);
-      const int64_t* hits = outv.data();
-      const int32_t* fr = reinterpret_cast<const int32_t*>(outv.data() + np + 1);
-      R.s.mc_ms += c.toc();
-      c.sync();
-      kprof_work(F_MC, hits[np]);
-      c.mc_rollout_steps += hits[np];
-      for (int k = 0; k < np; ++k) {
-        Probe p;
-        p.free = fr[k] != 0;
-        if (p.free) {
-          p.mc = static_cast<double>(hits[k]) / s.mc_samples;
-          R.s.mc_rollouts += r1 - r0;
-        }
-        probes.emplace(todo[k], std::move(p));
-      }
-    };
-    auto run_probes = [&](const std::vector<double>& cands) {
-      if (host_probes)
-        evaluate(cands);
-      else
-        evaluate_dev(cands);
-    };
-    auto certified = [&](double sv) {
-      const Probe& p = probes.at(sv);
-      return p.free && p.mc <= s.alpha;
-    };
-    auto subtree = [&](double lo, double hi, int depth, std::vector<double>& out) {
-      // all midpoints the bisection can visit in its next `depth` steps
-      std::vector<std::pair<double, double>> level{{lo, hi}};
-      for (int d = 0; d < depth; ++d) {
-        std::vector<std::pair<double, double>> next;
-        for (auto [a, b] : level) {
-          const double mid = 0.5 * (a + b);
-          out.push_back(mid);
-          next.push_back({mid, b});
-          next.push_back({a, mid});
-        }
-        level.swap(next);
-      }
-    };
-    auto accept = [&](double sv) {
-      Probe& p = probes.at(sv);
-      if (p.traj.empty()) p.traj = blend(sv);  // device probes keep only the verdicts
-      best = p.traj;
-      best_cost = trajectory_cost(p.traj, dw);
-      best_mc = p.mc;
-      best_s = sv;
-    };
-    // Batch schedule: depths of the speculative subtrees covering the 10
-    // bisection steps.  Host probes (PUMP_SMOOTH_HOST=1): one probe per MC
-    // launch.  Device probes (default): depth-2 subtrees, 3 candidates per
-    // batch (blend + nominal check + MC in one round trip).
-    // PUMP_SMOOTH_SCHEDULE="3,3,4" overrides.
-    std::vector<int> schedule(10, 1);
-    if (!host_probes) schedule = {2, 2, 2, 2, 2};  // PUMP_SMOOTH_SCHEDULE with device probes: speculative subtrees
-    if (const char* e = std::getenv("PUMP_SMOOTH_SCHEDULE")) {
-      schedule.clear();
-      for (const char* q = e; *q;) {
-        schedule.push_back(std::max(1, std::atoi(q)));
-        while (*q && *q != ',') ++q;
-        if (*q == ',') ++q;
-      }
-    }
-    static const bool spec = std::getenv("PUMP_SMOOTH_SCHEDULE") != nullptr;
-    if (!host_probes && !spec) {
-      // five batches enqueued at once, each deciding on the device from the
-      // previous batch's verdicts; one synchronisation for the whole bisection
-      const int64_t items = static_cast<int64_t>(4) * n_wp;
-      DBuf& d_y = c.buf("sm_y", items * dw * 8 + 256);
-      DBuf& d_yv = c.buf("sm_yv", items * dw * 8 + 256);
-      DBuf& d_ch = c.buf("sm_chain", sizeof(SmoothChain) + 256);
-      DBuf& d_off = c.buf("sm_choff", 256);
-      const int64_t offs[5] = {0, n_wp, 2 * static_cast<int64_t>(n_wp), 3 * static_cast<int64_t>(n_wp),
-                               4 * static_cast<int64_t>(n_wp)};
-      c.h2d(d_off.p, offs, sizeof(offs));
-      SmoothChain* ch = d_ch.as<SmoothChain>();
-      WorldD wd;
-      wd.n_obs = dwld.n_obs;
-      wd.lo = dwld.d_lo;
-      wd.hi = dwld.d_hi;
-      for (int k = 0; k < 6; ++k) {
-        wd.blo[k] = dwld.blo[k];
-        wd.bhi[k] = dwld.bhi[k];
-      }
-      int64_t r0 = 0, r1 = s.mc_samples;
-      shard_range(s.mc_samples, c.rank, c.world, &r0, &r1);
-      if (c.mc_join_pending) {
-        PUMP_CUDA(cudaStreamWaitEvent(c.stream, c.join, 0));
-        c.mc_join_pending = false;
-      }
-      c.tic();
-      for (int b = 0; b < 5; ++b) {
-        const int q0 = b == 0 ? 0 : 4 + 3 * (b - 1), np = b == 0 ? 4 : 3;
-        const int64_t it = static_cast<int64_t>(np) * n_wp;
-        k_smooth_decide<<<1, 1, 0, c.stream>>>(ch, b, s.mc_samples, s.alpha);
-        dispatch_dw(dw, [&]<int DW>() {
-          HMotion o = opt;
-          k_smooth_blend<DW><<<grid_for(it, 128), 128, 0, c.stream>>>(
-              np, n_wp, &ch->s[q0], c.scratch["sm_plan"].as<double>(), c.scratch["sm_plan"].as<double>() + n_wp,
-              c.scratch["sm_plan"].as<double>() + n_wp * (1 + dw), as_motion<DW>(o), d_y.as<double>(),
-              d_yv.as<double>());
-          k_smooth_check<DW><<<grid_for(it, 128), 128, 0, c.stream>>>(
-              wd, np, n_wp, c.scratch["sm_plan"].as<double>(), d_y.as<double>(), d_yv.as<double>(), eps_cc,
-              &ch->live[q0]);
-        });
-        c.launches += 3;
-        launch_mc(L, dwld, np, d_off.as<int64_t>(), d_y.as<double>(), n_wp, r0, r1, s.seeds.mc, eps_cc,
-                  &ch->hits[q0], c.stream, &c.launches, &ch->steps, &c.mc_table, &ch->live[q0]);
-        allreduce_sum_i64(c, reinterpret_cast<int64_t*>(&ch->hits[q0]), np);
-        PUMP_CUDA(cudaGetLastError());
-      }
-      SmoothChain hc{};
-      c.d2h(&hc, ch, sizeof(SmoothChain));
-      R.s.mc_ms += c.toc();
-      c.sync();
-      kprof_work(F_MC, static_cast<int64_t>(hc.steps));
-      c.mc_rollout_steps += static_cast<int64_t>(hc.steps);
-      for (int q = 0; q < kSmoothSlots; ++q) {  // every probe the batches evaluated
-        if (probes.count(hc.s[q]) || (q > 0 && hc.done)) continue;
-        Probe p;
-        p.free = hc.live[q] != 0;
-        if (p.free) {
-          p.mc = static_cast<double>(hc.hits[q]) / s.mc_samples;
-          R.s.mc_rollouts += r1 - r0;
-        }
-        probes.emplace(hc.s[q], std::move(p));
-      }
-      // replay (pump.hpp:118-141) from the history (probes.at throws if a
-      // probe the bisection visits was not evaluated on the device)
-      if (certified(1.0)) {
-        accept(1.0);
-      } else {
-        double lo = 0, hi = 1;
-        for (int k = 1; k <= 10; ++k) {
-          const double mid = 0.5 * (lo + hi);
-          if (!probes.count(mid)) throw std::runtime_error("smoothing: device bisection diverged from the host replay");
-          if (certified(mid)) {
-            accept(mid);
-            lo = mid;
-          } else {
-            hi = mid;
-          }
-        }
-      }
-    } else {
-    run_probes({1.0});
-    if (certified(1.0)) {
-      accept(1.0);
-    } else {
-      double lo = 0, hi = 1;
-      int it = 0;
-      for (size_t b = 0; b < schedule.size() && it < 10; ++b) {
-        std::vector<double> more;
-        subtree(lo, hi, std::min(schedule[b], 10 - it), more);
-        run_probes(more);
-        for (int d = 0; d < schedule[b] && it < 10; ++d, ++it) {
-          const double mid = 0.5 * (lo + hi);
-          if (certified(mid)) {
-            accept(mid);
-            lo = mid;
-          } else {
-            hi = mid;
-          }
-        }
-      }
-    }
-    }
+  {
+    SmoothOut sm = smooth_device(c, plan_sel, memo[sel], s.alpha, L, dwld, hw, s.mc_samples, s.seeds.mc, eps_cc, dw,
+                                 &R.s.mc_ms, &R.s.mc_rollouts);
+    R.traj = std::move(sm.traj);
+    R.s.cost = sm.cost;
+    R.s.certified_cp = sm.mc;
+    R.s.smoothing_s = sm.s;
   }
   mark("smoothing");
-  R.traj = best;
-  R.s.cost = best_cost;
-  R.s.certified_cp = best_mc;
-  R.s.smoothing_s = best_s;
   R.s.success = 1;
   R.s.selection_seconds = secs(t2, clk::now());
 }
@@ -1933,6 +1955,54 @@ int pump_rrt_run(pump_ctx* ctx, const pump_scenario* scn, int32_t trials, double
       throw;
     }
     *out = r;
+  });
+}
+
+int pump_smooth(pump_ctx* ctx, const pump_closed_loop* cl, const pump_workspace* ws, int32_t n_points,
+                const double* t, const double* pos, const double* vel, const double* ctrl, double plan_mc,
+                double alpha, int32_t n_mc, uint64_t seed, double eps_cc, double* out_pos, double* out_vel,
+                double* out_ctrl, double* out3) {
+  return guard([&] {
+    Ctx& c = ctx->c;
+    if (n_mc < 1) throw std::invalid_argument("mc_certify: need at least one rollout");
+    if (n_points < 1) throw std::invalid_argument("smooth: empty trajectory");
+    const HostLoop L = host_loop(cl);
+    const int dw = L.dw;
+    if (ws->dw != dw) throw std::invalid_argument("smooth: workspace / closed-loop dimension mismatch");
+    HostWorld hw;
+    hw.dw = dw;
+    for (int k = 0; k < dw; ++k) {
+      hw.blo[k] = ws->bounds_lo[k];
+      hw.bhi[k] = ws->bounds_hi[k];
+    }
+    hw.lo.assign(ws->obs_lo, ws->obs_lo + static_cast<size_t>(ws->n_obs) * dw);
+    hw.hi.assign(ws->obs_hi, ws->obs_hi + static_cast<size_t>(ws->n_obs) * dw);
+    const DevWorld dwld = upload_world(c, ws, "sm_ws_");
+    std::vector<HWp> plan(n_points);
+    for (int q = 0; q < n_points; ++q) {
+      HWp& h = plan[q];
+      h = HWp{};
+      h.t = t[q];
+      for (int k = 0; k < dw; ++k) {
+        h.p[k] = pos[q * dw + k];
+        h.v[k] = vel[q * dw + k];
+        h.u[k] = ctrl[q * dw + k];
+      }
+    }
+    // the certifications read a common-random-number table built for this call
+    c.mc_table.invalidate();
+    double mc_ms = 0;
+    int64_t rollouts = 0;
+    SmoothOut o = smooth_device(c, plan, plan_mc, alpha, L, dwld, hw, n_mc, seed, eps_cc, dw, &mc_ms, &rollouts);
+    for (int q = 0; q < n_points; ++q)
+      for (int k = 0; k < dw; ++k) {
+        out_pos[q * dw + k] = o.traj[q].p[k];
+        out_vel[q * dw + k] = o.traj[q].v[k];
+        out_ctrl[q * dw + k] = o.traj[q].u[k];
+      }
+    out3[0] = o.cost;
+    out3[1] = o.mc;
+    out3[2] = o.s;
   });
 }
 

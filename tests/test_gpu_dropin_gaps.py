@@ -197,3 +197,30 @@ def test_explore_wide_bucket_range_per_kernel_path(oracle_lib, gpu_ctx, lam):
     got = api.explore(gg, 0.01, 0.2, lam, 9.0, ctx=gpu_ctx)
     assert ref["rounds"] > 20
     explore_equal(got, ref)
+
+
+@pytest.mark.parametrize("name,samples", [("three_obstacle", 200), ("quad3d_three_obstacle", 500),
+                                          ("quad3d_forest", 600)])
+def test_smooth_entry_point_matches_oracle(oracle_lib, gpu_ctx, name, samples):
+    """pump_smooth (the drop-in smooth(), pump.hpp:84-146) runs the device
+    speculative chain; the accepted trajectory, cost, CP and s equal the
+    oracle's.  Plans: a solved trajectory, and the same one slowed down
+    (a different bisection path)."""
+    from paper_1607_06886_b200 import api
+
+    txt = with_samples(name, samples, mc_samples=3000)
+    cl, sc = oracle_lib.scenario_models(txt)
+    j = json.loads(txt)
+    ws = ws_of(j)
+    r = oracle_lib.run_pump(txt, workers=WORKERS)
+    assert r["success"]
+    plans = [(r["traj_t"], r["traj_pos"], r["traj_vel"], r["traj_ctrl"]),
+             (2.0 * r["traj_t"], r["traj_pos"], 0.5 * r["traj_vel"], 0.25 * r["traj_ctrl"])]
+    for alpha in (j["alpha"], 0.5 * j["alpha"]):
+        for t, p, v, u in plans:
+            got = api.smooth(t, p, v, u, 0.01, alpha, cl, ws, 3000, 2, sc["eps_cc"], ctx=gpu_ctx)
+            ref = oracle_lib.smooth(t, p, v, u, 0.01, alpha, cl, ws, 3000, 2, sc["eps_cc"], workers=WORKERS)
+            for k in ("cost", "mc", "s"):
+                assert got[k] == ref[k], (k, got[k], ref[k])
+            for k in ("traj_pos", "traj_vel", "traj_ctrl"):
+                assert np.array_equal(got[k].view(np.uint64), ref[k].view(np.uint64)), k
