@@ -1008,134 +1008,6 @@ __device__ __forceinline__ int convex_region_scan(const WorldD& ws, const double
   return count;
 }
 
-// The same region with the boxes visited nearest-first.  Equivalence with the
-// reference loop: its nearest boxes m_1 < m_2 < ... are increasing in
-// (|clamp(y) - y|^2, index) (each m_k is pruned by its own half-space, else
-// -1), and a box's pruned status before it could be selected is the OR of the
-// prune tests against every earlier half-space -- the order in which those
-// tests run does not matter.  So: take boxes in increasing (sq, index) and
-// keep the first that no half-space so far prunes as the next one.
-// The order comes from a block-wide list sorted by lb_o <= |clamp(y) - y| for
-// every waypoint y of the block (distance to the box from the block's
-// waypoint-box centre minus its half-diagonal, less a rounding margin: the
-// distance to a convex set is 1-Lipschitz).  A pool holds the boxes whose lb
-// is within reach of the current best; boxes beyond it are only ever
-// prune-tested (one min-corner dot per half-space until one prunes them).
-// Returns the count, -1 (no progress, as the reference throws) or -2 (pool /
-// half-space capacity exceeded: the caller falls back to convex_region_scan).
-constexpr int kPoolCap = 64, kPoolMaxH = 64;
-template <int DW>
-__device__ __forceinline__ void project_out(const double* d, const double* yd, double* a_out, double* b_out,
-                                            uint8_t* fb_out) {
-  double a[DW];
-  bool fb = false;
-  const double vn = sqrt(sqnorm<DW>(yd));
-  if (vn < 1e-6) {
-    fb = true;
-  } else {
-    double dy = 0.0;
-#pragma unroll
-    for (int k = 0; k < DW; ++k) dy = dy + d[k] * yd[k];
-    const double coef = dy / sqnorm<DW>(yd);
-#pragma unroll
-    for (int k = 0; k < DW; ++k) a[k] = d[k] - coef * yd[k];
-    if (sqrt(sqnorm<DW>(a)) < 1e-6 * sqrt(sqnorm<DW>(d))) fb = true;
-  }
-  if (fb) {
-#pragma unroll
-    for (int k = 0; k < DW; ++k) a[k] = d[k];
-  }
-#pragma unroll
-  for (int k = 0; k < DW; ++k) a_out[k] = a[k];
-  *b_out = sqnorm<DW>(a);
-  *fb_out = fb ? 1 : 0;
-}
-
-template <int DW>
-__device__ __forceinline__ bool prunes(const WorldD& ws, int o, const double* y, const double* d, double lim) {
-  double dot = 0;
-#pragma unroll
-  for (int k = 0; k < DW; ++k) dot += d[k] * ((d[k] >= 0 ? ws.lo : ws.hi)[o * DW + k] - y[k]);
-  return !(dot < lim);
-}
-
-template <int DW>
-__device__ __forceinline__ int convex_region_pool(const WorldD& ws, const double* y, const double* yd,
-                                                  const int16_t* order, const double* lb, double* a_out,
-                                                  double* b_out, uint8_t* fb_out, int a_stride, int b_stride,
-                                                  int out_cap) {
-  double hd[kPoolMaxH][DW], hl[kPoolMaxH];
-  int pidx[kPoolCap];
-  double psq[kPoolCap];
-  int np = 0, count = 0, p = 0, last = 0;
-  const int n = ws.n_obs;
-  for (;;) {
-    // best pool member (sq, index)
-    int bs = -1;
-    double bq = __builtin_inf();
-    for (int q = 0; q < np; ++q)
-      if (bs < 0 || psq[q] < bq || (psq[q] == bq && pidx[q] < pidx[bs])) {
-        bq = psq[q];
-        bs = q;
-      }
-    // extend the pool while a listed box may still be nearer
-    while (p < n) {
-      const double l = lb[p];
-      if (bs >= 0 && l > 0 && l * l > bq * (1.0 + 1e-9)) break;
-      const int o = order[p++];
-      bool pr = false;
-      for (int t = 0; t < count && !pr; ++t) {
-        const int j = (last + t) % count;
-        if (prunes<DW>(ws, o, y, hd[j], hl[j])) {
-          pr = true;
-          last = j;
-        }
-      }
-      if (pr) continue;
-      if (np == kPoolCap) return -2;
-      const double q = clamp_sq<DW>(ws, o, y);
-      pidx[np] = o;
-      psq[np] = q;
-      if (q < bq || (q == bq && (bs < 0 || o < pidx[bs]))) {
-        bq = q;
-        bs = np;
-      }
-      ++np;
-    }
-    if (bs < 0) break;  // every box pruned
-    const int m = pidx[bs];
-    pidx[bs] = pidx[np - 1];
-    psq[bs] = psq[np - 1];
-    --np;
-    double d[DW];
-#pragma unroll
-    for (int k = 0; k < DW; ++k) {
-      double c = y[k] < ws.lo[m * DW + k] ? ws.lo[m * DW + k] : y[k];
-      c = ws.hi[m * DW + k] < c ? ws.hi[m * DW + k] : c;
-      d[k] = c - y[k];
-    }
-    const double dd = sqnorm<DW>(d);
-    const double lim = dd - 1e-12 * (1.0 + dd);
-    if (!prunes<DW>(ws, m, y, d, lim)) return -1;
-    if (count == kPoolMaxH) return -2;
-#pragma unroll
-    for (int k = 0; k < DW; ++k) hd[count][k] = d[k];
-    hl[count] = lim;
-    if (count < out_cap) project_out<DW>(d, yd, a_out + count * a_stride, b_out + count * b_stride, fb_out + count);
-    ++count;
-    // the new half-space prunes pool members
-    int w = 0;
-    for (int q = 0; q < np; ++q)
-      if (!prunes<DW>(ws, pidx[q], y, d, lim)) {
-        pidx[w] = pidx[q];
-        psq[w] = psq[q];
-        ++w;
-      }
-    np = w;
-  }
-  return count;
-}
-
 // obstacle boxes staged in shared memory (block-wide; returns the view on them)
 template <int DW>
 __device__ __forceinline__ WorldD stage_world(const WorldD& w, double* smem) {

@@ -791,7 +791,6 @@ __global__ void k_emit_edges(GraphArgs g, const int64_t* __restrict__ d_ncand, i
 // reserved range.  Each waypoint finds its edge in the k_wp_edge map.
 constexpr int kOnceMaxObs = 16;
 constexpr int kRegLocal = 8;
-constexpr int kPoolMaxKW = 32;  // nearest-first pool path up to 1024 boxes (block-sorted box list in shared memory)
 
 // waypoint -> owning edge (one thread per edge fills its waypoint range)
 __global__ void k_wp_edge(int64_t n_edges, const int64_t* __restrict__ wp_off, int32_t* __restrict__ wp_edge) {
@@ -799,59 +798,6 @@ __global__ void k_wp_edge(int64_t n_edges, const int64_t* __restrict__ wp_off, i
   if (e >= n_edges) return;
   for (int64_t x = wp_off[e]; x < wp_off[e + 1]; ++x) wp_edge[x] = static_cast<int32_t>(e);
 }
-// Per-warp nearest-first box order for convex_region_pool: the warp's
-// waypoint box (centre c, half-diagonal R), per box lb = |clamp(c) - c| - R
-// less a rounding margin, sorted ascending (bitonic within the warp, ns =
-// pow2 >= n_obs entries in the warp's slice of shared memory).  A warp's 32
-// waypoints lie on one or two edges, so R stays small.
-template <int DW>
-__device__ __forceinline__ void warp_box_order(const WorldD& ws, bool active, const double* y, int ns, double* s_lb,
-                                               int16_t* s_order) {
-  const int lane = threadIdx.x & 31;
-  double c[DW], r2 = 0;
-#pragma unroll
-  for (int k = 0; k < DW; ++k) {
-    double lo = active ? y[k] : __builtin_inf(), hi = active ? y[k] : -__builtin_inf();
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      lo = fmin(lo, __shfl_xor_sync(0xffffffffu, lo, o));
-      hi = fmax(hi, __shfl_xor_sync(0xffffffffu, hi, o));
-    }
-    if (!(lo <= hi)) lo = hi = 0.0;  // no active waypoint in the warp
-    c[k] = 0.5 * (lo + hi);
-    r2 += (hi - lo) * (hi - lo);
-  }
-  const double R = 0.5 * sqrt(r2);
-  for (int o = lane; o < ns; o += 32) {
-    double l = __builtin_inf();
-    if (o < ws.n_obs) {
-      const double D = sqrt(clamp_sq<DW>(ws, o, c));
-      l = D - R - 1e-9 * (1.0 + D + R);
-    }
-    s_lb[o] = l;
-    s_order[o] = static_cast<int16_t>(o);
-  }
-  __syncwarp();
-  for (int k2 = 2; k2 <= ns; k2 <<= 1)
-    for (int j = k2 >> 1; j > 0; j >>= 1) {
-      for (int i = lane; i < ns; i += 32) {
-        const int ixj = i ^ j;
-        if (ixj > i) {
-          const bool up = (i & k2) == 0;
-          const double a = s_lb[i], b = s_lb[ixj];
-          if ((a > b) == up) {
-            s_lb[i] = b;
-            s_lb[ixj] = a;
-            const int16_t t = s_order[i];
-            s_order[i] = s_order[ixj];
-            s_order[ixj] = t;
-          }
-        }
-      }
-      __syncwarp();
-    }
-}
-
 template <int DW, int KW>
 __global__ void __launch_bounds__(128) k_regions_once(GraphArgs g, WorldD w, int64_t n_wp, int64_t n_edges,
                                                       const int64_t* __restrict__ wp_off,
@@ -871,11 +817,6 @@ __global__ void __launch_bounds__(128) k_regions_once(GraphArgs g, WorldD w, int
   const int lane = threadIdx.x & 31;
   const bool active = x < n_wp;
   constexpr int kLoc = KW == 0 ? kOnceMaxObs : kRegLocal;
-#ifndef PUMP_NO_REGION_POOL
-  constexpr bool kPool = KW > 0 && KW <= kPoolMaxKW;
-#else
-  constexpr bool kPool = false;
-#endif
   double la[kLoc * DW], lb[kLoc];
   uint8_t lf[kLoc];
   int n = 0;
@@ -906,25 +847,11 @@ __global__ void __launch_bounds__(128) k_regions_once(GraphArgs g, WorldD w, int
       motion_state<DW>(m, j * g.dt, y, yd);
     }
   }
-  double* s_lb = nullptr;
-  int16_t* s_order = nullptr;
-  if constexpr (kPool) {
-    int ns = 1;
-    while (ns < w.n_obs) ns <<= 1;
-    const int wid = threadIdx.x >> 5;
-    s_lb = smem + 2 * w.n_obs * DW + static_cast<size_t>(wid) * ns;
-    s_order = reinterpret_cast<int16_t*>(smem + 2 * w.n_obs * DW + static_cast<size_t>(blockDim.x >> 5) * ns) +
-              static_cast<size_t>(wid) * ns;
-    warp_box_order<DW>(ws, active, y, ns, s_lb, s_order);
-  }
   auto region = [&](double* ao, double* bo, uint8_t* fo, int as, int bst, int ocap) {
     if constexpr (KW == 0) {
       return convex_region_fused<DW>(ws, y, yd, smem + 2 * w.n_obs * DW + threadIdx.x, blockDim.x, ao, bo, fo);
     } else {
-      int c = -2;
-      if constexpr (kPool) c = convex_region_pool<DW>(ws, y, yd, s_order, s_lb, ao, bo, fo, as, bst, ocap);
-      if (c == -2) c = convex_region_scan<DW, KW>(ws, y, yd, ao, bo, fo, as, bst, ocap);
-      return c;
+      return convex_region_scan<DW, KW>(ws, y, yd, ao, bo, fo, as, bst, ocap);
     }
   };
   if (active) {
@@ -1322,13 +1249,8 @@ void build_graph_device(DevGraph& G, Ctx& c, int n, int dw, const double* h_pos,
         dispatch_dw(dw, [&]<int DW>() {
           auto kern = w.n_obs <= kOnceMaxObs ? k_regions_once<DW, 0>
                       : w.n_obs <= 256      ? k_regions_once<DW, 8>
-                      : w.n_obs <= 1024     ? k_regions_once<DW, 32>
                                             : k_regions_once<DW, 128>;
-          size_t ns = 1;
-          while (ns < static_cast<size_t>(w.n_obs)) ns <<= 1;
-          const size_t sm = wsmem + (w.n_obs <= kOnceMaxObs ? static_cast<size_t>(w.n_obs) * 128 * 8
-                                     : w.n_obs <= 1024      ? ns * 10 * 4 + 16
-                                                            : 0);
+          const size_t sm = wsmem + (w.n_obs <= kOnceMaxObs ? static_cast<size_t>(w.n_obs) * 128 * 8 : 0);
           if (sm > 48 * 1024)
             PUMP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
           kern<<<grid_for(NW, 128), 128, sm, st>>>(

@@ -200,7 +200,7 @@ def test_explore_wide_bucket_range_per_kernel_path(oracle_lib, gpu_ctx, lam):
 
 
 @pytest.mark.parametrize("name,samples", [("three_obstacle", 200), ("quad3d_three_obstacle", 500),
-                                          ("quad3d_forest", 600)])
+                                          ("quad3d_indoor", 1200), ("quad3d_forest", 3000)])
 def test_smooth_entry_point_matches_oracle(oracle_lib, gpu_ctx, name, samples):
     """pump_smooth (the drop-in smooth(), pump.hpp:84-146) runs the device
     speculative chain; the accepted trajectory, cost, CP and s equal the
