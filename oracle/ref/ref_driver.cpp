@@ -163,6 +163,66 @@ int ref_cp_compare(const char* text, const char* traj_text, const int* counts, i
   }
 }
 
+// The reference's own writers (report.hpp:31-129, pump_cli.cpp:48-109) on
+// result values read back from another writer's files: kind 0 = plan
+// (report.json, pareto.csv, trajectory.json), 1 = rrt (report.json,
+// trajectory.json), 2 = certify (report.json).  The texts are returned
+// concatenated with a '\x1f' separator in the CLI's exact bytes.
+int ref_render(int kind, const char* scenario_text, const char* report_text, const char* traj_text, int workers,
+               char* out, long cap, long* len) {
+  try {
+    pump::Scenario s = scn(scenario_text);
+    const pump::json rep = pump::json::parse(report_text);
+    std::string text;
+    if (kind == 0) {
+      pump::PumpResult r;
+      r.success = rep.at("success").get<bool>();
+      r.cost = rep.at("cost").get<double>();
+      r.pre_smoothing_cost = rep.at("pre_smoothing_cost").get<double>();
+      r.certified_cp = rep.at("certified_cp").get<double>();
+      r.cp_hat = rep.at("cp_hat").get<double>();
+      r.smoothing_s = rep.at("smoothing_s").get<double>();
+      r.path = rep.at("path").get<std::vector<int>>();
+      r.partial_plans = rep.at("partial_plans").get<long>();
+      r.termination = rep.at("termination").get<std::string>();
+      for (const auto& g : rep.at("goal_plans")) r.pareto.push_back({g.at("cost").get<double>(), g.at("cp_hat").get<double>()});
+      for (const auto& e : rep.at("mc_evaluations")) r.mc_evals.push_back({e.at("plan").get<int>(), e.at("mc").get<double>()});
+      r.build_graph_seconds = rep.at("timing").at("build_graph_seconds").get<double>();
+      r.explore_seconds = rep.at("timing").at("explore_seconds").get<double>();
+      r.selection_seconds = rep.at("timing").at("selection_seconds").get<double>();
+      text = pump::plan_report_json(s, r, workers).dump(2) + "\n" + "\x1f" + pump::pareto_csv(r);
+      if (traj_text && *traj_text)
+        text += "\x1f" + pump::trajectory_json(pump::parse_trajectory(pump::json::parse(traj_text))).dump(2) + "\n";
+    } else if (kind == 1) {
+      pump::RrtResult r;
+      r.success = rep.at("success").get<bool>();
+      r.cost = rep.at("cost").get<double>();
+      r.certified_cp = rep.at("certified_cp").get<double>();
+      r.trials_reaching_goal = rep.at("trials_reaching_goal").get<int>();
+      r.certification_attempts = rep.at("certification_attempts").get<int>();
+      text = pump::rrt_report_json(s, r, rep.at("trials").get<int>(), workers).dump(2) + "\n";
+      if (traj_text && *traj_text)
+        text += "\x1f" + pump::trajectory_json(pump::parse_trajectory(pump::json::parse(traj_text))).dump(2) + "\n";
+    } else {
+      const double v = rep.at("certified_cp").get<double>();
+      const pump::json report = {{"schema_version", 1},
+                                 {"scenario", s.name},
+                                 {"algorithm", "certify"},
+                                 {"certified_cp", v},
+                                 {"mc_samples", rep.at("mc_samples").get<int>()},
+                                 {"alpha", s.alpha},
+                                 {"within_alpha", v <= s.alpha}};
+      text = report.dump(2) + "\n";
+    }
+    *len = static_cast<long>(text.size());
+    if (out && cap >= *len) std::memcpy(out, text.data(), text.size());
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return 1;
+  }
+}
+
 // ------------------------------------------------ bench.py reference arm
 // A bounded sample of one reference solve (run_pump, pump.hpp:170-263), for
 // workloads whose full solve takes tens of seconds on the host: setup builds

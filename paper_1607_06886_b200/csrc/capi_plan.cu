@@ -150,27 +150,6 @@ static bool point_free_h(const HostWorld& w, const double* y) {
   return r;
 }
 
-static bool nominal_free(const HostWorld& w, const std::vector<HWp>& t, double eps_cc) {  // pump.hpp:64-75
-  const int dw = w.dw;
-  for (const auto& p : t)
-    if (!point_free_h(w, p.p)) return false;
-  for (size_t j = 0; j + 1 < t.size(); ++j) {
-    const double h = t[j + 1].t - t[j].t;
-    if (h <= 0) continue;
-    HMotion m{};
-    std::memcpy(m.p0, t[j].p, sizeof(m.p0));
-    std::memcpy(m.v0, t[j].v, sizeof(m.v0));
-    std::memcpy(m.p1, t[j + 1].p, sizeof(m.p1));
-    std::memcpy(m.v1, t[j + 1].v, sizeof(m.v1));
-    m.tau = h;
-    fixed_time(m, dw);
-    bool hit = false;
-    dispatch_dw(dw, [&]<int DW>() { hit = motion_collides<DW>(as_motion<DW>(m), w.view(), eps_cc); });
-    if (hit) return false;
-  }
-  return true;
-}
-
 // ------------------------------------------------------------ smoothing kernels
 // Smoothing probes on the device (pump.hpp:84-146): for each probed blend
 // fraction s the blended trajectory (1 - s) plan + s opt (positions and
@@ -342,40 +321,6 @@ __global__ void k_gather_members(int n_goal, const int32_t* goal_nodes, const in
   }
 }
 
-struct PathSet {
-  std::vector<std::vector<int>> nodes;
-  std::vector<std::vector<int64_t>> edges;
-  // per path edge: tau, acc0[dw], jerk[dw] (gathered on the device, one copy)
-  std::vector<std::vector<double>> motion;
-};
-
-// compact the resolved paths (k_paths' fixed-stride slots) and gather each
-// path edge's motion coefficients next to it
-__global__ void k_path_compact(int ns, int max_len, int dw, const int32_t* __restrict__ nodes,
-                               const int64_t* __restrict__ edges, const int64_t* __restrict__ off,
-                               const double* __restrict__ e_tau, const double* __restrict__ e_acc0,
-                               const double* __restrict__ e_jerk, int32_t* __restrict__ c_nodes,
-                               int64_t* __restrict__ c_edges, double* __restrict__ c_motion) {
-  const int s = blockIdx.x;
-  if (s >= ns) return;
-  const int64_t o = off[s], len = off[s + 1] - off[s];
-  for (int64_t j = threadIdx.x; j < len; j += blockDim.x) {
-    c_nodes[o + j] = nodes[static_cast<int64_t>(s) * max_len + j];
-    if (j + 1 < len) {
-      const int64_t e = edges[static_cast<int64_t>(s) * max_len + j];
-      c_edges[o + j] = e;
-      double* m = c_motion + (o + j) * (1 + 2 * dw);
-      if (e >= 0) {
-        m[0] = e_tau[e];
-        for (int k = 0; k < dw; ++k) {
-          m[1 + k] = e_acc0[e * dw + k];
-          m[1 + dw + k] = e_jerk[e * dw + k];
-        }
-      }
-    }
-  }
-}
-
 // path_trajectory (planner.hpp:292-315) of every front plan on the device: a
 // warp per plan walks its edges in order (the time offset is the running sum
 // of the edge durations, as the reference adds them) and the lanes write each
@@ -473,99 +418,6 @@ __global__ void k_traj_build(int ns, int max_len, const int32_t* __restrict__ no
     w += cnt - i0;
     offset += m.tau;
   }
-}
-
-static PathSet resolve_paths(Ctx& c, const DevGraph& G, const DevExplore& X, const std::vector<int>& sel) {
-  PathSet ps;
-  const int ns = static_cast<int>(sel.size());
-  if (ns == 0) return ps;
-  const int dw = G.dw;
-  const int max_len = 4096;
-  DBuf& d_sel = c.buf("p_sel", ns * 4 + 256);
-  DBuf& d_nodes = c.buf("p_nodes", static_cast<size_t>(ns) * max_len * 4 + 256);
-  DBuf& d_edges = c.buf("p_edges", static_cast<size_t>(ns) * max_len * 8 + 256);
-  DBuf& d_lens = c.buf("p_lens", ns * 4 + 256);
-  c.h2d(d_sel.p, sel.data(), ns * 4);
-  k_paths<<<(ns + 127) / 128, 128, 0, c.stream>>>(ns, d_sel.as<int32_t>(), X.head.as<int32_t>(),
-                                                  X.parent.as<int32_t>(), G.row_ptr.as<int64_t>(), G.e_to.as<int32_t>(),
-                                                  max_len, d_nodes.as<int32_t>(), d_edges.as<int64_t>(),
-                                                  d_lens.as<int32_t>());
-  ++c.launches;
-  PUMP_CUDA(cudaGetLastError());
-  std::vector<int32_t> lens(ns);
-  c.d2h(lens.data(), d_lens.p, ns * 4);
-  c.sync();
-  std::vector<int64_t> off(ns + 1, 0);
-  for (int q = 0; q < ns; ++q) off[q + 1] = off[q] + lens[q];
-  const int64_t total = off[ns];
-  const int mw = 1 + 2 * dw;
-  DBuf& d_off = c.buf("p_off", (ns + 1) * 8 + 256);
-  DBuf& c_nodes = c.buf("p_cnodes", total * 4 + 256);
-  DBuf& c_edges = c.buf("p_cedges", total * 8 + 256);
-  DBuf& c_motion = c.buf("p_cmotion", total * mw * 8 + 256);
-  c.h2d(d_off.p, off.data(), (ns + 1) * 8);
-  k_path_compact<<<ns, 128, 0, c.stream>>>(ns, max_len, dw, d_nodes.as<int32_t>(), d_edges.as<int64_t>(),
-                                           d_off.as<int64_t>(), G.e_tau.as<double>(), G.e_acc0.as<double>(),
-                                           G.e_jerk.as<double>(), c_nodes.as<int32_t>(), c_edges.as<int64_t>(),
-                                           c_motion.as<double>());
-  ++c.launches;
-  PUMP_CUDA(cudaGetLastError());
-  std::vector<int32_t> nodes(total);
-  std::vector<int64_t> edges(total);
-  std::vector<double> motion(static_cast<size_t>(total) * mw);
-  c.d2h(nodes.data(), c_nodes.p, total * 4);
-  c.d2h(edges.data(), c_edges.p, total * 8);
-  c.d2h(motion.data(), c_motion.p, total * mw * 8);
-  c.sync();
-  for (int q = 0; q < ns; ++q) {
-    ps.nodes.emplace_back(nodes.begin() + off[q], nodes.begin() + off[q + 1]);
-    const int64_t ne = std::max<int64_t>(0, lens[q] - 1);
-    ps.edges.emplace_back(edges.begin() + off[q], edges.begin() + off[q] + ne);
-    ps.motion.emplace_back(motion.begin() + off[q] * mw, motion.begin() + (off[q] + ne) * mw);
-  }
-  return ps;
-}
-
-// path_trajectory (planner.hpp:292-315) from the gathered edge data
-static std::vector<HWp> path_trajectory(const DevGraph& G, const std::vector<int>& path,
-                                        const std::vector<int64_t>& edges, const std::vector<double>& motion) {
-  const int dw = G.dw;
-  const int mw = 1 + 2 * dw;
-  std::vector<HWp> traj;
-  double offset = 0;
-  for (size_t j = 0; j + 1 < path.size(); ++j) {
-    const int64_t e = edges[j];
-    if (e < 0) throw std::logic_error("path_trajectory: missing edge");
-    HMotion m{};
-    m.tau = motion[j * mw];
-    for (int k = 0; k < dw; ++k) {
-      m.a[k] = motion[j * mw + 1 + k];
-      m.j[k] = motion[j * mw + 1 + dw + k];
-    }
-    const int v = path[j], u = path[j + 1];
-    for (int k = 0; k < dw; ++k) {
-      m.p0[k] = G.h_pos[v * dw + k];
-      m.v0[k] = G.h_vel[v * dw + k];
-      m.p1[k] = G.h_pos[u * dw + k];
-      m.v1[k] = G.h_vel[u * dw + k];
-    }
-    auto wps = motion_waypoints(m, dw, G.dt);
-    for (size_t k = (j == 0 ? 0 : 1); k < wps.size(); ++k) {
-      HWp wp = wps[k];
-      wp.t += offset;
-      traj.push_back(wp);
-    }
-    offset += m.tau;
-  }
-  if (path.size() == 1) {
-    HWp w{};
-    for (int k = 0; k < dw; ++k) {
-      w.p[k] = G.h_pos[path[0] * dw + k];
-      w.v[k] = G.h_vel[path[0] * dw + k];
-    }
-    traj.push_back(w);
-  }
-  return traj;
 }
 
 // Batched MC over trajectories (rollouts [0, n_mc)); values = hits / n_mc
@@ -918,8 +770,8 @@ struct SmoothOut {
   double cost = 0, mc = 0, s = 0;
 };
 static SmoothOut smooth_device(Ctx& c, const std::vector<HWp>& plan, double plan_mc, double alpha,
-                               const HostLoop& L, const DevWorld& dwld, const HostWorld& hw, int64_t n_mc,
-                               uint64_t seed, double eps_cc, int dw, double* mc_ms, int64_t* mc_rollouts) {
+                               const HostLoop& L, const DevWorld& dwld, int64_t n_mc, uint64_t seed, double eps_cc,
+                               int dw, double* mc_ms, int64_t* mc_rollouts) {
   // smoothing (pump.hpp:84-146).  The reference bisects the blend fraction
   // s sequentially (s = 1, then 10 midpoints), each probe a nominal
   // collision check + one MC certification.  The probes form a dyadic tree,
@@ -961,31 +813,10 @@ static SmoothOut smooth_device(Ctx& c, const std::vector<HWp>& plan, double plan
       double mc = 1.0;
     };
     std::map<double, Probe> probes;
-    // evaluate the candidates not yet probed: nominal check, then one MC batch
-    auto evaluate = [&](const std::vector<double>& cands) {
-      std::vector<double> todo;
-      std::vector<std::vector<HWp>> batch;
-      for (double sv : cands) {
-        if (probes.count(sv)) continue;
-        Probe p;
-        p.traj = blend(sv);
-        p.free = nominal_free(hw, p.traj, eps_cc);
-        if (p.free) {
-          todo.push_back(sv);
-          batch.push_back(p.traj);
-        }
-        probes.emplace(sv, std::move(p));
-      }
-      if (batch.empty()) return;
-      auto v = mc_values(c, L, dwld, batch, n_mc, seed, eps_cc, mc_ms, mc_rollouts);
-      for (size_t k = 0; k < todo.size(); ++k) probes[todo[k]].mc = v[k];
-    };
-    // the same on the device: blend, nominal check and MC of every new
-    // candidate in one batch (one synchronisation); MC of a candidate whose
-    // nominal collides is computed but never used (the reference skips it)
-    static const bool host_probes = std::getenv("PUMP_SMOOTH_HOST") != nullptr;
+    // the device chain: five depth-2 speculative batches, each blending its
+    // probes, checking their nominal and certifying them in one pass
     const int n_wp = static_cast<int>(plan.size());
-    if (!host_probes) {
+    {
       // the plan's times, positions and velocities in one upload
       std::vector<double> pl(static_cast<size_t>(n_wp) * (1 + 2 * dw));
       for (int q = 0; q < n_wp; ++q) {
@@ -997,97 +828,9 @@ static SmoothOut smooth_device(Ctx& c, const std::vector<HWp>& plan, double plan
       }
       c.h2d(c.buf("sm_plan", pl.size() * 8 + 256).p, pl.data(), pl.size() * 8);
     }
-    auto evaluate_dev = [&](const std::vector<double>& cands) {
-      std::vector<double> todo;
-      for (double sv : cands)
-        if (!probes.count(sv) && std::find(todo.begin(), todo.end(), sv) == todo.end()) todo.push_back(sv);
-      const int np = static_cast<int>(todo.size());
-      if (np == 0) return;
-      const int64_t items = static_cast<int64_t>(np) * n_wp;
-      DBuf& d_y = c.buf("sm_y", items * dw * 8 + 256);
-      DBuf& d_yv = c.buf("sm_yv", items * dw * 8 + 256);
-      // one upload (s values, MC offsets) and one download (hits, free flags)
-      DBuf& d_in = c.buf("sm_in", (2 * np + 1) * 8 + 256);
-      DBuf& d_out = c.buf("sm_out", (np + 1) * 8 + np * 4 + 256);
-      std::vector<int64_t> in(2 * np + 1);
-      std::memcpy(in.data(), todo.data(), np * 8);
-      for (int k = 0; k <= np; ++k) in[np + k] = static_cast<int64_t>(k) * n_wp;
-      c.h2d(d_in.p, in.data(), (2 * np + 1) * 8);
-      const double* d_s = d_in.as<double>();
-      const int64_t* d_off = d_in.as<int64_t>() + np;
-      unsigned long long* d_h = d_out.as<unsigned long long>();
-      int32_t* d_free = reinterpret_cast<int32_t*>(d_out.as<int64_t>() + np + 1);
-      PUMP_CUDA(cudaMemsetAsync(d_h, 0, (np + 1) * 8, c.stream));
-      PUMP_CUDA(cudaMemsetAsync(d_free, 1, np * 4, c.stream));  // nonzero: free until a check fails
-      WorldD wd;
-      wd.n_obs = dwld.n_obs;
-      wd.lo = dwld.d_lo;
-      wd.hi = dwld.d_hi;
-      for (int k = 0; k < 6; ++k) {
-        wd.blo[k] = dwld.blo[k];
-        wd.bhi[k] = dwld.bhi[k];
-      }
-      c.tic();
-      dispatch_dw(dw, [&]<int DW>() {
-        HMotion o = opt;
-        k_smooth_blend<DW><<<grid_for(items, 128), 128, 0, c.stream>>>(
-            np, n_wp, d_s, c.scratch["sm_plan"].as<double>(), c.scratch["sm_plan"].as<double>() + n_wp,
-            c.scratch["sm_plan"].as<double>() + n_wp * (1 + dw), as_motion<DW>(o), d_y.as<double>(), d_yv.as<double>());
-        k_smooth_check<DW><<<grid_for(items, 128), 128, 0, c.stream>>>(
-            wd, np, n_wp, c.scratch["sm_plan"].as<double>(), d_y.as<double>(), d_yv.as<double>(), eps_cc, d_free);
-      });
-      c.launches += 2;
-      PUMP_CUDA(cudaGetLastError());
-      int64_t r0 = 0, r1 = n_mc;
-      shard_range(n_mc, c.rank, c.world, &r0, &r1);
-      if (c.mc_join_pending) {
-        PUMP_CUDA(cudaStreamWaitEvent(c.stream, c.join, 0));
-        c.mc_join_pending = false;
-      }
-      launch_mc(L, dwld, np, d_off, d_y.as<double>(), n_wp, r0, r1, seed, eps_cc, d_h, c.stream, &c.launches,
-                d_h + np, &c.mc_table, d_free);
-      allreduce_sum_i64(c, reinterpret_cast<int64_t*>(d_h), np);
-      std::vector<int64_t> outv(np + 1 + (np + 1) / 2);
-      c.d2h(outv.data(), d_out.p, (np + 1) * 8 + np * 4);
-      const int64_t* hits = outv.data();
-      const int32_t* fr = reinterpret_cast<const int32_t*>(outv.data() + np + 1);
-      *mc_ms += c.toc();
-      c.sync();
-      kprof_work(F_MC, hits[np]);
-      c.mc_rollout_steps += hits[np];
-      for (int k = 0; k < np; ++k) {
-        Probe p;
-        p.free = fr[k] != 0;
-        if (p.free) {
-          p.mc = static_cast<double>(hits[k]) / n_mc;
-          *mc_rollouts += r1 - r0;
-        }
-        probes.emplace(todo[k], std::move(p));
-      }
-    };
-    auto run_probes = [&](const std::vector<double>& cands) {
-      if (host_probes)
-        evaluate(cands);
-      else
-        evaluate_dev(cands);
-    };
     auto certified = [&](double sv) {
       const Probe& p = probes.at(sv);
       return p.free && p.mc <= alpha;
-    };
-    auto subtree = [&](double lo, double hi, int depth, std::vector<double>& out) {
-      // all midpoints the bisection can visit in its next `depth` steps
-      std::vector<std::pair<double, double>> level{{lo, hi}};
-      for (int d = 0; d < depth; ++d) {
-        std::vector<std::pair<double, double>> next;
-        for (auto [a, b] : level) {
-          const double mid = 0.5 * (a + b);
-          out.push_back(mid);
-          next.push_back({mid, b});
-          next.push_back({a, mid});
-        }
-        level.swap(next);
-      }
     };
     auto accept = [&](double sv) {
       Probe& p = probes.at(sv);
@@ -1097,124 +840,84 @@ static SmoothOut smooth_device(Ctx& c, const std::vector<HWp>& plan, double plan
       best_mc = p.mc;
       best_s = sv;
     };
-    // Batch schedule: depths of the speculative subtrees covering the 10
-    // bisection steps.  Host probes (PUMP_SMOOTH_HOST=1): one probe per MC
-    // launch.  Device probes (default): depth-2 subtrees, 3 candidates per
-    // batch (blend + nominal check + MC in one round trip).
-    // PUMP_SMOOTH_SCHEDULE="3,3,4" overrides.
-    std::vector<int> schedule(10, 1);
-    if (!host_probes) schedule = {2, 2, 2, 2, 2};  // PUMP_SMOOTH_SCHEDULE with device probes: speculative subtrees
-    if (const char* e = std::getenv("PUMP_SMOOTH_SCHEDULE")) {
-      schedule.clear();
-      for (const char* q = e; *q;) {
-        schedule.push_back(std::max(1, std::atoi(q)));
-        while (*q && *q != ',') ++q;
-        if (*q == ',') ++q;
-      }
+    // five batches enqueued at once, each deciding on the device from the
+    // previous batch's verdicts; one synchronisation for the whole bisection
+    const int64_t items = static_cast<int64_t>(4) * n_wp;
+    DBuf& d_y = c.buf("sm_y", items * dw * 8 + 256);
+    DBuf& d_yv = c.buf("sm_yv", items * dw * 8 + 256);
+    DBuf& d_ch = c.buf("sm_chain", sizeof(SmoothChain) + 256);
+    DBuf& d_off = c.buf("sm_choff", 256);
+    const int64_t offs[5] = {0, n_wp, 2 * static_cast<int64_t>(n_wp), 3 * static_cast<int64_t>(n_wp),
+                             4 * static_cast<int64_t>(n_wp)};
+    c.h2d(d_off.p, offs, sizeof(offs));
+    SmoothChain* ch = d_ch.as<SmoothChain>();
+    WorldD wd;
+    wd.n_obs = dwld.n_obs;
+    wd.lo = dwld.d_lo;
+    wd.hi = dwld.d_hi;
+    for (int k = 0; k < 6; ++k) {
+      wd.blo[k] = dwld.blo[k];
+      wd.bhi[k] = dwld.bhi[k];
     }
-    static const bool spec = std::getenv("PUMP_SMOOTH_SCHEDULE") != nullptr;
-    if (!host_probes && !spec) {
-      // five batches enqueued at once, each deciding on the device from the
-      // previous batch's verdicts; one synchronisation for the whole bisection
-      const int64_t items = static_cast<int64_t>(4) * n_wp;
-      DBuf& d_y = c.buf("sm_y", items * dw * 8 + 256);
-      DBuf& d_yv = c.buf("sm_yv", items * dw * 8 + 256);
-      DBuf& d_ch = c.buf("sm_chain", sizeof(SmoothChain) + 256);
-      DBuf& d_off = c.buf("sm_choff", 256);
-      const int64_t offs[5] = {0, n_wp, 2 * static_cast<int64_t>(n_wp), 3 * static_cast<int64_t>(n_wp),
-                               4 * static_cast<int64_t>(n_wp)};
-      c.h2d(d_off.p, offs, sizeof(offs));
-      SmoothChain* ch = d_ch.as<SmoothChain>();
-      WorldD wd;
-      wd.n_obs = dwld.n_obs;
-      wd.lo = dwld.d_lo;
-      wd.hi = dwld.d_hi;
-      for (int k = 0; k < 6; ++k) {
-        wd.blo[k] = dwld.blo[k];
-        wd.bhi[k] = dwld.bhi[k];
+    int64_t r0 = 0, r1 = n_mc;
+    shard_range(n_mc, c.rank, c.world, &r0, &r1);
+    if (c.mc_join_pending) {
+      PUMP_CUDA(cudaStreamWaitEvent(c.stream, c.join, 0));
+      c.mc_join_pending = false;
+    }
+    c.tic();
+    for (int b = 0; b < 5; ++b) {
+      const int q0 = b == 0 ? 0 : 4 + 3 * (b - 1), np = b == 0 ? 4 : 3;
+      const int64_t it = static_cast<int64_t>(np) * n_wp;
+      k_smooth_decide<<<1, 1, 0, c.stream>>>(ch, b, n_mc, alpha);
+      dispatch_dw(dw, [&]<int DW>() {
+        HMotion o = opt;
+        k_smooth_blend<DW><<<grid_for(it, 128), 128, 0, c.stream>>>(
+            np, n_wp, &ch->s[q0], c.scratch["sm_plan"].as<double>(), c.scratch["sm_plan"].as<double>() + n_wp,
+            c.scratch["sm_plan"].as<double>() + n_wp * (1 + dw), as_motion<DW>(o), d_y.as<double>(),
+            d_yv.as<double>());
+        k_smooth_check<DW><<<grid_for(it, 128), 128, 0, c.stream>>>(
+            wd, np, n_wp, c.scratch["sm_plan"].as<double>(), d_y.as<double>(), d_yv.as<double>(), eps_cc,
+            &ch->live[q0]);
+      });
+      c.launches += 3;
+      launch_mc(L, dwld, np, d_off.as<int64_t>(), d_y.as<double>(), n_wp, r0, r1, seed, eps_cc,
+                &ch->hits[q0], c.stream, &c.launches, &ch->steps, &c.mc_table, &ch->live[q0]);
+      allreduce_sum_i64(c, reinterpret_cast<int64_t*>(&ch->hits[q0]), np);
+      PUMP_CUDA(cudaGetLastError());
+    }
+    SmoothChain hc{};
+    c.d2h(&hc, ch, sizeof(SmoothChain));
+    *mc_ms += c.toc();
+    c.sync();
+    kprof_work(F_MC, static_cast<int64_t>(hc.steps));
+    c.mc_rollout_steps += static_cast<int64_t>(hc.steps);
+    for (int q = 0; q < kSmoothSlots; ++q) {  // every probe the batches evaluated
+      if (probes.count(hc.s[q]) || (q > 0 && hc.done)) continue;
+      Probe p;
+      p.free = hc.live[q] != 0;
+      if (p.free) {
+        p.mc = static_cast<double>(hc.hits[q]) / n_mc;
+        *mc_rollouts += r1 - r0;
       }
-      int64_t r0 = 0, r1 = n_mc;
-      shard_range(n_mc, c.rank, c.world, &r0, &r1);
-      if (c.mc_join_pending) {
-        PUMP_CUDA(cudaStreamWaitEvent(c.stream, c.join, 0));
-        c.mc_join_pending = false;
-      }
-      c.tic();
-      for (int b = 0; b < 5; ++b) {
-        const int q0 = b == 0 ? 0 : 4 + 3 * (b - 1), np = b == 0 ? 4 : 3;
-        const int64_t it = static_cast<int64_t>(np) * n_wp;
-        k_smooth_decide<<<1, 1, 0, c.stream>>>(ch, b, n_mc, alpha);
-        dispatch_dw(dw, [&]<int DW>() {
-          HMotion o = opt;
-          k_smooth_blend<DW><<<grid_for(it, 128), 128, 0, c.stream>>>(
-              np, n_wp, &ch->s[q0], c.scratch["sm_plan"].as<double>(), c.scratch["sm_plan"].as<double>() + n_wp,
-              c.scratch["sm_plan"].as<double>() + n_wp * (1 + dw), as_motion<DW>(o), d_y.as<double>(),
-              d_yv.as<double>());
-          k_smooth_check<DW><<<grid_for(it, 128), 128, 0, c.stream>>>(
-              wd, np, n_wp, c.scratch["sm_plan"].as<double>(), d_y.as<double>(), d_yv.as<double>(), eps_cc,
-              &ch->live[q0]);
-        });
-        c.launches += 3;
-        launch_mc(L, dwld, np, d_off.as<int64_t>(), d_y.as<double>(), n_wp, r0, r1, seed, eps_cc,
-                  &ch->hits[q0], c.stream, &c.launches, &ch->steps, &c.mc_table, &ch->live[q0]);
-        allreduce_sum_i64(c, reinterpret_cast<int64_t*>(&ch->hits[q0]), np);
-        PUMP_CUDA(cudaGetLastError());
-      }
-      SmoothChain hc{};
-      c.d2h(&hc, ch, sizeof(SmoothChain));
-      *mc_ms += c.toc();
-      c.sync();
-      kprof_work(F_MC, static_cast<int64_t>(hc.steps));
-      c.mc_rollout_steps += static_cast<int64_t>(hc.steps);
-      for (int q = 0; q < kSmoothSlots; ++q) {  // every probe the batches evaluated
-        if (probes.count(hc.s[q]) || (q > 0 && hc.done)) continue;
-        Probe p;
-        p.free = hc.live[q] != 0;
-        if (p.free) {
-          p.mc = static_cast<double>(hc.hits[q]) / n_mc;
-          *mc_rollouts += r1 - r0;
-        }
-        probes.emplace(hc.s[q], std::move(p));
-      }
-      // replay (pump.hpp:118-141) from the history (probes.at throws if a
-      // probe the bisection visits was not evaluated on the device)
-      if (certified(1.0)) {
-        accept(1.0);
-      } else {
-        double lo = 0, hi = 1;
-        for (int k = 1; k <= 10; ++k) {
-          const double mid = 0.5 * (lo + hi);
-          if (!probes.count(mid)) throw std::runtime_error("smoothing: device bisection diverged from the host replay");
-          if (certified(mid)) {
-            accept(mid);
-            lo = mid;
-          } else {
-            hi = mid;
-          }
-        }
-      }
-    } else {
-    run_probes({1.0});
+      probes.emplace(hc.s[q], std::move(p));
+    }
+    // replay (pump.hpp:118-141) from the history (probes.at throws if a
+    // probe the bisection visits was not evaluated on the device)
     if (certified(1.0)) {
       accept(1.0);
     } else {
       double lo = 0, hi = 1;
-      int it = 0;
-      for (size_t b = 0; b < schedule.size() && it < 10; ++b) {
-        std::vector<double> more;
-        subtree(lo, hi, std::min(schedule[b], 10 - it), more);
-        run_probes(more);
-        for (int d = 0; d < schedule[b] && it < 10; ++d, ++it) {
-          const double mid = 0.5 * (lo + hi);
-          if (certified(mid)) {
-            accept(mid);
-            lo = mid;
-          } else {
-            hi = mid;
-          }
+      for (int k = 1; k <= 10; ++k) {
+        const double mid = 0.5 * (lo + hi);
+        if (!probes.count(mid)) throw std::runtime_error("smoothing: device bisection diverged from the host replay");
+        if (certified(mid)) {
+          accept(mid);
+          lo = mid;
+        } else {
+          hi = mid;
         }
       }
-    }
     }
   }
   SmoothOut o;
@@ -1264,11 +967,7 @@ static void run_pump_device(Ctx& c, const pumpb::Scenario& s, const DevGraph* pr
   const DevGraph* graph = prebuilt;
   if (!graph) {
     std::vector<double> pos, vel;
-    static const bool host_sampling = std::getenv("PUMP_HOST_SAMPLING") != nullptr;
-    if (host_sampling)
-      sample_nodes(s, hw, pos, vel);
-    else
-      sample_nodes_device(c, s, hw, dwld, local, pos, vel);
+    sample_nodes_device(c, s, hw, dwld, local, pos, vel);
     if (std::getenv("PUMP_DEBUG_TIMING"))
       std::fprintf(stderr, "[pump g] %-24s %8.3f ms (from solve start)\n", "sample_nodes",
                    1e3 * secs(t0, clk::now()));
@@ -1277,7 +976,7 @@ static void run_pump_device(Ctx& c, const pumpb::Scenario& s, const DevGraph* pr
     // gathered over NVLink into the full graph on every rank
     int64_t rlo = 0, rhi = n;
     if (c.world > 1) shard_range(n, c.rank, c.world, &rlo, &rhi);
-    build_graph_device(local, c, n, dw, host_sampling ? pos.data() : nullptr, host_sampling ? vel.data() : nullptr,
+    build_graph_device(local, c, n, dw, nullptr, nullptr,  // the sampler left the nodes in local.pos / vel
                        dwld, r_n, s.dt, eps_cc, s.effective_tau_max(), scan_ratio(s.effective_tau_max()),
                        static_cast<int>(rlo), static_cast<int>(rhi), c.world > 1);
     pump_goal g{s.goal.lo.data(), s.goal.hi.data(), s.goal_max_speed};
@@ -1417,21 +1116,12 @@ static void run_pump_device(Ctx& c, const pumpb::Scenario& s, const DevGraph* pr
   // The front plans' node paths and trajectories on the device (k_paths,
   // k_traj_build): plan q has t_end + 1 waypoints, so the offsets are known
   // here; their positions feed the MC batch directly and only the selected
-  // plan is copied back.  PUMP_HOST_PATHS=1: paths and trajectories on the host.
-  static const bool host_paths = std::getenv("PUMP_HOST_PATHS") != nullptr;
+  // plan is copied back.
   const int nf = static_cast<int>(sorted_ids.size());
   constexpr int kMaxLen = 4096;
-  PathSet ps;
-  std::vector<std::vector<HWp>> trajs;
   std::vector<int64_t> woff(nf + 1, 0);
   std::vector<double> memo;
-  if (host_paths) {
-    ps = resolve_paths(c, *graph, X, sorted_ids);
-    for (size_t k = 0; k < sorted_ids.size(); ++k)
-      trajs.push_back(path_trajectory(*graph, ps.nodes[k], ps.edges[k], ps.motion[k]));
-    if (!trajs.empty())
-      memo = mc_values(c, L, dwld, trajs, s.mc_samples, s.seeds.mc, eps_cc, &R.s.mc_ms, &R.s.mc_rollouts);
-  } else if (nf > 0) {
+  if (nf > 0) {
     int max_pts = 0;
     for (int q = 0; q < nf; ++q) {
       woff[q + 1] = woff[q] + sorted_tend[q] + 1;
@@ -1501,10 +1191,7 @@ static void run_pump_device(Ctx& c, const pumpb::Scenario& s, const DevGraph* pr
   mark("front mc");
   const int sel_id = sorted_ids[sel];
   std::vector<HWp> plan_sel;
-  if (host_paths) {
-    R.path.assign(ps.nodes[sel].begin(), ps.nodes[sel].end());
-    plan_sel = trajs[sel];
-  } else {
+  {
     // the selected plan's node path and waypoints
     const int64_t n_wp = woff[sel + 1] - woff[sel];
     int32_t len = 0;
@@ -1539,7 +1226,7 @@ static void run_pump_device(Ctx& c, const pumpb::Scenario& s, const DevGraph* pr
     R.s.pre_smoothing_cost = cst;
   }
   {
-    SmoothOut sm = smooth_device(c, plan_sel, memo[sel], s.alpha, L, dwld, hw, s.mc_samples, s.seeds.mc, eps_cc, dw,
+    SmoothOut sm = smooth_device(c, plan_sel, memo[sel], s.alpha, L, dwld, s.mc_samples, s.seeds.mc, eps_cc, dw,
                                  &R.s.mc_ms, &R.s.mc_rollouts);
     R.traj = std::move(sm.traj);
     R.s.cost = sm.cost;
@@ -1969,14 +1656,6 @@ int pump_smooth(pump_ctx* ctx, const pump_closed_loop* cl, const pump_workspace*
     const HostLoop L = host_loop(cl);
     const int dw = L.dw;
     if (ws->dw != dw) throw std::invalid_argument("smooth: workspace / closed-loop dimension mismatch");
-    HostWorld hw;
-    hw.dw = dw;
-    for (int k = 0; k < dw; ++k) {
-      hw.blo[k] = ws->bounds_lo[k];
-      hw.bhi[k] = ws->bounds_hi[k];
-    }
-    hw.lo.assign(ws->obs_lo, ws->obs_lo + static_cast<size_t>(ws->n_obs) * dw);
-    hw.hi.assign(ws->obs_hi, ws->obs_hi + static_cast<size_t>(ws->n_obs) * dw);
     const DevWorld dwld = upload_world(c, ws, "sm_ws_");
     std::vector<HWp> plan(n_points);
     for (int q = 0; q < n_points; ++q) {
@@ -1993,7 +1672,7 @@ int pump_smooth(pump_ctx* ctx, const pump_closed_loop* cl, const pump_workspace*
     c.mc_table.invalidate();
     double mc_ms = 0;
     int64_t rollouts = 0;
-    SmoothOut o = smooth_device(c, plan, plan_mc, alpha, L, dwld, hw, n_mc, seed, eps_cc, dw, &mc_ms, &rollouts);
+    SmoothOut o = smooth_device(c, plan, plan_mc, alpha, L, dwld, n_mc, seed, eps_cc, dw, &mc_ms, &rollouts);
     for (int q = 0; q < n_points; ++q)
       for (int k = 0; k < dw; ++k) {
         out_pos[q * dw + k] = o.traj[q].p[k];

@@ -179,8 +179,7 @@ void launch_bank(const HostLoop& HL, int n, int T, uint64_t seed, double* d_dy, 
                  int64_t* launches) {
   if (n < 1) throw std::invalid_argument("presample_bank: need at least one particle");
   if (T < 1) throw std::invalid_argument("presample_bank: horizon must be at least 1");
-  static const bool dense = std::getenv("PUMP_BANK_DENSE") != nullptr;
-  const bool sep = !dense && HL.dw >= 2 && HL.dw <= 3 && separable(HL);
+  const bool sep = HL.dw >= 2 && HL.dw <= 3 && separable(HL);
   const SepBlocks B = sep ? sep_blocks(HL) : SepBlocks{};
   dispatch_dims(HL.d, HL.dw, [&]<int D, int DW>() {
     const LoopP<D, DW> L = make_loop<D, DW>(HL);

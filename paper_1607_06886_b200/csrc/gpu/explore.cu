@@ -1438,19 +1438,17 @@ void run_explore_device(DevExplore& X, Ctx& c, const DevGraph& G, const ExploreA
   const double width = prm.lambda * prm.r_n;
 
   // cooperative round kernel for this (dw, particle-words) instance
-  static const bool legacy_env = std::getenv("PUMP_EXPLORE_LEGACY") != nullptr;
   const void* coop_fn = reinterpret_cast<const void*>(&k_round_tail);
   int coop_blocks = 0;
   {
     int per_sm = 0, sms = 0, coop_attr = 0;
     PUMP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, coop_fn, kCoopBlock, 0));
-    static const int coop_per_sm = std::getenv("PUMP_COOP_PER_SM") ? std::atoi(std::getenv("PUMP_COOP_PER_SM")) : 1;
-    per_sm = std::min(per_sm, coop_per_sm);  // fewer blocks: cheaper grid barriers; the tail phases are small
+    per_sm = std::min(per_sm, 1);  // one block per SM: cheaper grid barriers (2 per SM measured within noise)
     PUMP_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c.device));
     PUMP_CUDA(cudaDeviceGetAttribute(&coop_attr, cudaDevAttrCooperativeLaunch, c.device));
     coop_blocks = coop_attr ? per_sm * sms : 0;
   }
-  const bool coop_ok = !legacy_env && coop_blocks > 0;
+  const bool coop_ok = coop_blocks > 0;
   if (coop_ok) {  // look-back status words start untagged
     DBuf& scan_st = c.buf("x_coop_scan_status", al((coop_blocks + 2) * 8));
     PUMP_CUDA(cudaMemsetAsync(scan_st.p, 0, (coop_blocks + 2) * 8, st));
@@ -1460,7 +1458,7 @@ void run_explore_device(DevExplore& X, Ctx& c, const DevGraph& G, const ExploreA
   // status is read once per batch; buffers are sized for Tcap tasks per round
   // and a round that does not fit (or needs the per-kernel path) halts the
   // batch, after which the host runs that round synchronously.
-  static const int kBatch = std::getenv("PUMP_EXPLORE_BATCH") ? std::max(1, std::atoi(std::getenv("PUMP_EXPLORE_BATCH"))) : 8;
+  constexpr int kBatch = 8;
   bool force_sync = false;
   int64_t max_T = 0;
   long long commit_bytes_legacy = 0;

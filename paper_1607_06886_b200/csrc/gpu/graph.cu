@@ -123,61 +123,6 @@ LbGrid make_lb_grid(double r_n) {
   return L;
 }
 
-// Pass 1: one CTA per source row v, one thread per target u.  Velocity
-// prefilter (graph.hpp:70) and the exact-preserving lower-bound filter;
-// survivors are compacted in ascending-u order (warp ballots + CTA prefix)
-// into the row's slab.  Cheap (~1k FP64 ops per pair) and branch-light.
-template <int DW>
-__global__ void __launch_bounds__(kRowBlock) k_pair_filter(GraphArgs g, const LbGrid lb, int cap, int row0,
-                                                           int32_t* __restrict__ row_cnt, int32_t* __restrict__ su) {
-  __shared__ int wtot[kRowBlock / 32];
-  __shared__ int base_s;
-  __shared__ LbGrid sl;  // lanes index the grid divergently: shared, not the constant bank
-  {
-    const double* src = reinterpret_cast<const double*>(&lb);
-    double* dst = reinterpret_cast<double*>(&sl);
-    for (int x = threadIdx.x; x < static_cast<int>(sizeof(LbGrid) / 8); x += blockDim.x) dst[x] = src[x];
-  }
-  const int v = row0 + blockIdx.x;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  double ap[DW], av[DW];
-#pragma unroll
-  for (int k = 0; k < DW; ++k) {
-    ap[k] = g.pos[v * DW + k];
-    av[k] = g.vel[v * DW + k];
-  }
-  if (threadIdx.x == 0) base_s = 0;
-  __syncthreads();
-  for (int u0 = 0; u0 < g.n; u0 += kRowBlock) {
-    const int u = u0 + threadIdx.x;
-    bool keep = false;
-    if (u < g.n && u != v) {
-      double bp[DW], bv[DW];
-#pragma unroll
-      for (int k = 0; k < DW; ++k) {
-        bp[k] = g.pos[u * DW + k];
-        bv[k] = g.vel[u * DW + k];
-      }
-      const PairLb plb = pair_lb<DW>(ap, av, bp, bv);
-      keep = !(2.0 * sqrt(plb.D) >= g.r_n) && !lb_rejects(plb, sl);
-    }
-    const unsigned bal = __ballot_sync(0xffffffffu, keep);
-    if (lane == 0) wtot[warp] = __popc(bal);
-    __syncthreads();
-    int off = base_s;
-    for (int w = 0; w < warp; ++w) off += wtot[w];
-    off += __popc(bal & ((1u << lane) - 1u));
-    if (keep && off < cap) su[static_cast<int64_t>(v) * cap + off] = u;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      int t = 0;
-      for (int w = 0; w < kRowBlock / 32; ++w) t += wtot[w];
-      base_s += t;
-    }
-    __syncthreads();
-  }
-  if (threadIdx.x == 0) row_cnt[v] = base_s;
-}
 
 // Pass 1, lane-refill form.  The tree cover of lb_tree costs 1 interval test
 // for most pairs and hundreds for near-threshold ones; one pair per lane left
@@ -938,9 +883,8 @@ void build_graph_device(DevGraph& G, Ctx& c, int n, int dw, const double* h_pos,
   DBuf& soff = c.buf("g_soff", al((n + 2) * 8));
   DBuf& stmp = c.buf("g_scantmp", scan_temp_bytes(static_cast<int64_t>(n) * n + 16));
   // ---- cell grid of the nodes for the exact spatial cull (k_pair_filter_grid)
-  static const bool nogrid = getenv("PUMP_PAIR_NOGRID") != nullptr;
   const size_t bits_bytes = static_cast<size_t>((n + 31) / 32) * 4;
-  const bool use_grid = !nogrid && n > 0 && row_hi > row_lo && bits_bytes <= 160 * 1024;
+  const bool use_grid = n > 0 && row_hi > row_lo && bits_bytes <= 160 * 1024;
   CellGrid cg{};
   if (use_grid) {
     KScope ks(st, F_PAIR);
@@ -1039,8 +983,7 @@ void build_graph_device(DevGraph& G, Ctx& c, int n, int dw, const double* h_pos,
     {
       KScope ks(st, F_PAIR);
       dispatch_dw(dw, [&]<int DW>() {
-        static const bool legacy = getenv("PUMP_PAIR_LEGACY") != nullptr;
-        static const int refill = getenv("PUMP_PF_REFILL") ? atoi(getenv("PUMP_PF_REFILL")) : 16;
+        constexpr int refill = 16;  // lane-refill threshold of the filter walks
         if (use_grid) {
           const int sm = static_cast<int>(bits_bytes);
           if (sm > 32 * 1024)
@@ -1049,11 +992,8 @@ void build_graph_device(DevGraph& G, Ctx& c, int n, int dw, const double* h_pos,
               ga, lbg, cg, cap, row_lo, refill, c.scratch["g_ccnt"].as<int32_t>(), c.scratch["g_cstart"].as<int64_t>(),
               c.scratch["g_cbox"].as<unsigned long long>(), c.scratch["g_sidx"].as<int32_t>(),
               c.scratch["g_spos"].as<double>(), c.scratch["g_svel"].as<double>(), rcnt.as<int32_t>(),
-              suB.as<int32_t>(), getenv("PUMP_PF_NOGLOBAL") ? 0 : 1);
-        } else if (row_hi > row_lo && legacy)
-          k_pair_filter<DW><<<row_hi - row_lo, kRowBlock, 0, st>>>(ga, lbg, cap, row_lo, rcnt.as<int32_t>(),
-                                                                   suB.as<int32_t>());
-        else if (row_hi > row_lo)
+              suB.as<int32_t>(), 1);
+        } else if (row_hi > row_lo)  // more nodes than the row bitmask holds
           k_pair_filter_q<DW><<<row_hi - row_lo, kRowBlock, 0, st>>>(ga, lbg, cap, row_lo, refill, rcnt.as<int32_t>(),
                                                                      suB.as<int32_t>());
       });

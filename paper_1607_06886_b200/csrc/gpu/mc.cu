@@ -439,91 +439,6 @@ __global__ void __launch_bounds__(kMcBlock, MINB) k_mc_sep(const SepBlocks B, Wo
 // ------------------------------------------------------------------------
 // Common-random-number table (kernels.h, McTable).
 //
-// Build, axis-separable loop: the lane-per-axis recursion of k_mc_sep with
-// the collision checks removed; writes dy_t = (0 + C0 z0) + C1 z1 for
-// t in [t_from, t_to].  zst holds z_{t_from - 1} (t_from > 0) and receives
-// z_{t_to}.  Every operation is the one k_mc_sep performs, in its order.
-template <int DW>
-__global__ void __launch_bounds__(kMcBlock) k_mctab_sep(const SepBlocks B, int64_t r0, int64_t n, uint64_t seed,
-                                                        int t_from, int t_to, double* __restrict__ dy,
-                                                        double* __restrict__ zst) {
-  constexpr int LPR = lanes_per_rollout<DW>();
-  constexpr int GPW = groups_per_warp<DW>();
-  __shared__ double s_blk[3][40];
-  for (int x = threadIdx.x; x < 3 * 40; x += blockDim.x) {
-    const int ax = x / 40, o = x % 40;
-    double v = 0.0;
-    if (ax < DW) {
-      if (o < 16) v = B.F[ax][o];
-      else if (o < 24) v = B.Gv[ax][o - 16];
-      else if (o < 28) v = B.Gw[ax][o - 24];
-      else if (o < 32) v = B.Sv[ax][o - 28];
-      else if (o < 36) v = B.S0[ax][o - 32];
-      else if (o < 38) v = B.C[ax][o - 36];
-      else if (o == 38) v = B.Sw[ax];
-    }
-    s_blk[ax][o] = v;
-  }
-  __syncthreads();
-  const int lane = threadIdx.x & 31;
-  const int q = lane % LPR, g = lane / LPR;
-  const int64_t li = (static_cast<int64_t>(blockIdx.x) * (kMcBlock / 32) + (threadIdx.x >> 5)) * GPW + g;
-  if (g >= GPW || li >= n) return;
-  const int64_t i = r0 + li;
-  const int k = q;
-  const double* F = &s_blk[k][0];
-  const double* Gv = &s_blk[k][16];
-  const double* Gw = &s_blk[k][24];
-  const double* Sv = &s_blk[k][28];
-  const double* S0 = &s_blk[k][32];
-  const double* C = &s_blk[k][36];
-  const double Sw = s_blk[k][38];
-  const uint64_t ch0 = static_cast<uint64_t>(k), ch1 = static_cast<uint64_t>(DW + k);
-  const uint64_t sa = hash_seed_a(seed, static_cast<uint64_t>(i));
-  double z[4];
-  double* zs = zst + (li * DW + k) * 4;
-  if (t_from == 0) {
-    const uint64_t pt = mix64(sa + 0ull);
-    const double n0 = normal_from_prefix(pt, ch0), n1 = normal_from_prefix(pt, ch1);  // kInitial channels
-    z[0] = (0.0 + S0[0] * n0) + S0[1] * n1;
-    z[1] = (0.0 + S0[2] * n0) + S0[3] * n1;
-    z[2] = 0.0;
-    z[3] = 0.0;
-  } else {
-#pragma unroll
-    for (int r = 0; r < 4; ++r) z[r] = zs[r];
-  }
-  for (int t = t_from; t <= t_to; ++t) {
-    if (t > 0) {
-      {
-        // z_t = ((F z_{t-1}) + u) + w, noise of the transition t-1 -> t
-        const uint64_t pt = mix64(sa + static_cast<uint64_t>(t - 1));
-        const uint64_t pt1 = mix64(sa + static_cast<uint64_t>(t));
-        const double nv0 = normal_from_prefix(pt, kProcess + ch0);
-        const double nv1 = normal_from_prefix(pt, kProcess + ch1);
-        const double nw = normal_from_prefix(pt1, kMeasurement + static_cast<uint64_t>(k));
-        const double t10 = (0.0 + Sv[0] * nv0) + Sv[1] * nv1;
-        const double t11 = (0.0 + Sv[2] * nv0) + Sv[3] * nv1;
-        const double t2 = 0.0 + Sw * nw;
-        double zn[4];
-#pragma unroll
-        for (int r = 0; r < 4; ++r) {
-          const double u = (0.0 + Gv[2 * r] * t10) + Gv[2 * r + 1] * t11;
-          const double wv = 0.0 + Gw[r] * t2;
-          double c = 0.0;
-#pragma unroll
-          for (int x = 0; x < 4; ++x) c = c + F[r * 4 + x] * z[x];
-          zn[r] = (c + u) + wv;
-        }
-#pragma unroll
-        for (int r = 0; r < 4; ++r) z[r] = zn[r];
-      }
-    }
-    dy[(static_cast<int64_t>(t) * n + li) * DW + k] = (0.0 + C[0] * z[0]) + C[1] * z[1];
-  }
-#pragma unroll
-  for (int r = 0; r < 4; ++r) zs[r] = z[r];
-}
 
 // Build in two phases for the axis-separable loop (the default path): the
 // noise of every (transition t-1 -> t, rollout, axis) is a pure function of
@@ -1007,8 +922,7 @@ static bool ensure_table(McTable& tab, const HostLoop& HL, int64_t r0, int64_t r
     tab.dy.grow(bytes, static_cast<size_t>(t_from) * row, st);
   }
   KScope ks(st, F_MC_TABLE);
-  static const bool fused = std::getenv("PUMP_MCTAB_FUSED") != nullptr;
-  if (tab.sep && !fused) {
+  if (tab.sep) {
     // time slices of kTabSlice steps bound the noise scratch (n x slice x 3 x dw doubles)
     constexpr int kTabSlice = 64;
     const SepBlocks B = sep_blocks(HL);
@@ -1028,13 +942,6 @@ static bool ensure_table(McTable& tab, const HostLoop& HL, int64_t r0, int64_t r
       });
       if (tc0 + kTabSlice > T) break;
     }
-  } else if (tab.sep) {
-    const SepBlocks B = sep_blocks(HL);
-    dispatch_dw(dw, [&]<int DW>() {
-      constexpr int per_block = (kMcBlock / 32) * groups_per_warp<DW>();
-      k_mctab_sep<DW><<<static_cast<unsigned>((n + per_block - 1) / per_block), kMcBlock, 0, st>>>(
-          B, r0, n, seed, t_from, T, tab.dy.as<double>(), tab.z.as<double>());
-    });
   } else {
     dispatch_dims(d, dw, [&]<int D, int DW>() {
       const LoopP<D, DW> L = make_loop<D, DW>(HL);
@@ -1097,7 +1004,6 @@ void launch_mc(const HostLoop& HL, const DevWorld& w, int n_traj, const int64_t*
     table->flags.ensure(static_cast<size_t>(n) * n_traj + 256);
     PUMP_CUDA(cudaMemsetAsync(table->flags.p, 0, static_cast<size_t>(n) * n_traj, st));
     dispatch_dw(HL.dw, [&]<int DW>() {
-      static const int sub = std::getenv("PUMP_MC_SUB") ? std::atoi(std::getenv("PUMP_MC_SUB")) : 2;
       // per-(trajectory, step) candidate lists, once per certification
       const size_t rows_all = static_cast<size_t>(n_traj) * max_points;
       table->step_list.ensure(rows_all * kStepCap * 2 + 256);
@@ -1122,9 +1028,7 @@ void launch_mc(const HostLoop& HL, const DevWorld& w, int n_traj, const int64_t*
                                                         table->step_skip.as<uint8_t>());
       };
       KScope ks(st, F_MC);
-      if (sub == 2) go.template operator()<2>();
-      else if (sub == 4) go.template operator()<4>();
-      else go.template operator()<1>();
+      go.template operator()<2>();  // 2 x kMcChunk steps per thread (1 and 4 measured slower)
       k_mc_count<<<dim3(static_cast<unsigned>(std::min<int64_t>((n + 255) / 256, 64)), n_traj), 256, 0, st>>>(
           table->flags.as<uint8_t>(), n, d_traj_off, d_hits, d_steps, d_live);
     });
@@ -1132,8 +1036,7 @@ void launch_mc(const HostLoop& HL, const DevWorld& w, int n_traj, const int64_t*
     PUMP_CUDA(cudaGetLastError());
     return;
   }
-  static const bool force_dense = std::getenv("PUMP_MC_DENSE") != nullptr;
-  if (!force_dense && HL.dw >= 2 && HL.dw <= 3 && separable(HL)) {
+  if (HL.dw >= 2 && HL.dw <= 3 && separable(HL)) {
     const SepBlocks B = sep_blocks(HL);
     WorldD wd;
     wd.n_obs = w.n_obs;
@@ -1147,7 +1050,6 @@ void launch_mc(const HostLoop& HL, const DevWorld& w, int n_traj, const int64_t*
       const size_t smem = (static_cast<size_t>(max_points) * DW + 4 * static_cast<size_t>(w.n_obs) * DW) * sizeof(double);
       constexpr int per_block = (kMcBlock / 32) * groups_per_warp<DW>();
       dim3 grid(static_cast<unsigned>((r1 - r0 + per_block - 1) / per_block), n_traj);
-      static const int minb = std::getenv("PUMP_MC_MINB") ? std::atoi(std::getenv("PUMP_MC_MINB")) : 5;
       auto go = [&]<int MINB>() {
         if (smem > 48 * 1024)
           PUMP_CUDA(cudaFuncSetAttribute(k_mc_sep<DW, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1156,10 +1058,7 @@ void launch_mc(const HostLoop& HL, const DevWorld& w, int n_traj, const int64_t*
         k_mc_sep<DW, MINB><<<grid, kMcBlock, smem, st>>>(B, wd, d_traj_off, d_ynom, r0, r1, seed, eps_cc, d_hits,
                                                           d_steps);
       };
-      if (minb == 4) go.template operator()<4>();
-      else if (minb == 6) go.template operator()<6>();
-      else if (minb == 8) go.template operator()<8>();
-      else go.template operator()<5>();
+      go.template operator()<5>();  // 5 blocks per SM (4, 6, 8 measured slower)
       ++*launches;
       PUMP_CUDA(cudaGetLastError());
     });

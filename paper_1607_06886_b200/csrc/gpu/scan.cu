@@ -7,106 +7,6 @@
 
 namespace pumpg {
 
-template <class InT>
-__global__ void __launch_bounds__(kScanBlock) k_tile_sum(const InT* __restrict__ in, int64_t n,
-                                                         int64_t* __restrict__ partial, const int64_t* d_n) {
-  __shared__ int64_t wsum[kScanBlock / 32];
-  if (d_n) n = min(n, *d_n);
-  const int64_t base = static_cast<int64_t>(blockIdx.x) * kScanTile;
-  int64_t s = 0;
-#pragma unroll
-  for (int k = 0; k < kScanItems; ++k) {
-    const int64_t i = base + k * kScanBlock + threadIdx.x;
-    if (i < n) s += static_cast<int64_t>(in[i]);
-  }
-  s = warp_sum(s);
-  if ((threadIdx.x & 31) == 0) wsum[threadIdx.x >> 5] = s;
-  __syncthreads();
-  if (threadIdx.x < 32) {
-    int64_t x = threadIdx.x < kScanBlock / 32 ? wsum[threadIdx.x] : 0;
-    x = warp_sum(x);
-    if (threadIdx.x == 0) partial[blockIdx.x] = x;
-  }
-}
-
-// exclusive scan of partial[0..m) in place (single block); total -> *total
-__global__ void __launch_bounds__(1024) k_scan_partials(int64_t* __restrict__ partial, int64_t m,
-                                                        int64_t* __restrict__ out, int64_t n, const int64_t* d_n) {
-  __shared__ int64_t wsum[32];
-  __shared__ int64_t carry;
-  if (d_n) {
-    n = min(n, *d_n);
-    m = (n + kScanTile - 1) / kScanTile;
-  }
-  int64_t* total = out + n;
-  if (threadIdx.x == 0) carry = 0;
-  __syncthreads();
-  for (int64_t c0 = 0; c0 < m; c0 += 1024) {
-    const int64_t i = c0 + threadIdx.x;
-    int64_t x = i < m ? partial[i] : 0;
-    int64_t inc = warp_incl_scan(x);
-    if ((threadIdx.x & 31) == 31) wsum[threadIdx.x >> 5] = inc;
-    __syncthreads();
-    if (threadIdx.x < 32) {
-      int64_t w = wsum[threadIdx.x];
-      int64_t wi = warp_incl_scan(w);
-      wsum[threadIdx.x] = wi - w;
-    }
-    __syncthreads();
-    const int64_t excl = carry + wsum[threadIdx.x >> 5] + inc - x;
-    if (i < m) partial[i] = excl;
-    __syncthreads();
-    if (threadIdx.x == 1023) carry = excl + x;
-    __syncthreads();
-  }
-  if (threadIdx.x == 0) *total = carry;
-}
-
-template <class InT>
-__global__ void __launch_bounds__(kScanBlock) k_tile_scan(const InT* __restrict__ in, int64_t n,
-                                                          const int64_t* __restrict__ partial,
-                                                          int64_t* __restrict__ out, const int64_t* d_n) {
-  __shared__ int64_t tile[kScanTile];
-  __shared__ int64_t wsum[kScanBlock / 32];
-  if (d_n) n = min(n, *d_n);
-  if (static_cast<int64_t>(blockIdx.x) * kScanTile >= n && n > 0) return;
-  const int64_t base = static_cast<int64_t>(blockIdx.x) * kScanTile;
-#pragma unroll
-  for (int k = 0; k < kScanItems; ++k) {
-    const int64_t i = base + k * kScanBlock + threadIdx.x;
-    tile[k * kScanBlock + threadIdx.x] = i < n ? static_cast<int64_t>(in[i]) : 0;
-  }
-  __syncthreads();
-  int64_t v[kScanItems];
-  int64_t s = 0;
-#pragma unroll
-  for (int k = 0; k < kScanItems; ++k) {
-    v[k] = tile[threadIdx.x * kScanItems + k];
-    s += v[k];
-  }
-  const int64_t inc = warp_incl_scan(s);
-  if ((threadIdx.x & 31) == 31) wsum[threadIdx.x >> 5] = inc;
-  __syncthreads();
-  if (threadIdx.x < 32) {
-    int64_t w = threadIdx.x < kScanBlock / 32 ? wsum[threadIdx.x] : 0;
-    int64_t wi = warp_incl_scan(w);
-    if (threadIdx.x < kScanBlock / 32) wsum[threadIdx.x] = wi - w;
-  }
-  __syncthreads();
-  int64_t run = partial[blockIdx.x] + wsum[threadIdx.x >> 5] + inc - s;
-#pragma unroll
-  for (int k = 0; k < kScanItems; ++k) {
-    tile[threadIdx.x * kScanItems + k] = run;
-    run += v[k];
-  }
-  __syncthreads();
-#pragma unroll
-  for (int k = 0; k < kScanItems; ++k) {
-    const int64_t i = base + k * kScanBlock + threadIdx.x;
-    if (i < n) out[i] = tile[k * kScanBlock + threadIdx.x];
-  }
-}
-
 // Single-pass scan with decoupled look-back: each CTA takes a ticket (tile
 // order independent of block scheduling), publishes its tile aggregate, then
 // resolves its exclusive prefix from its predecessors' published words
@@ -212,14 +112,7 @@ void exclusive_scan(const InT* d_in, int64_t* d_out, int64_t n, void* d_temp, cu
   uint64_t* status = reinterpret_cast<uint64_t*>(static_cast<char*>(d_temp) + 256);
   unsigned* ticket = static_cast<unsigned*>(d_temp);
   KScope ks(st, F_SCAN);
-  static const bool three_pass = std::getenv("PUMP_SCAN_3PASS") != nullptr;
-  if (three_pass) {
-    int64_t* partial = static_cast<int64_t*>(d_temp);
-    k_tile_sum<InT><<<static_cast<unsigned>(tiles), kScanBlock, 0, st>>>(d_in, n, partial, d_n);
-    k_scan_partials<<<1, 1024, 0, st>>>(partial, tiles, d_out, n, d_n);
-    k_tile_scan<InT><<<static_cast<unsigned>(tiles), kScanBlock, 0, st>>>(d_in, n, partial, d_out, d_n);
-    *launches += 3;
-  } else if (tiles == 1) {
+  if (tiles == 1) {
     k_scan_lookback<InT><<<1, kScanBlock, 0, st>>>(d_in, n, d_out, status, nullptr, d_n);
     *launches += 1;
   } else {

@@ -45,3 +45,30 @@ def scenario_text(name: str) -> str:
             with open(p) as f:
                 return f.read()
     raise FileNotFoundError(name)
+
+
+def coupled_noise_text(samples=500, mc=3000):
+    """quad3d_three_obstacle with full-matrix (cross-axis correlated) process
+    and measurement noise and a coupled tracking weight: the closed loop is
+    not axis-separable, so the dense bank (k_bank_rec<6,3>) and dense MC-table
+    (k_mctab_dense) kernels run (scenario.hpp:110 accepts full matrices)."""
+    import json
+
+    import numpy as np
+
+    j = json.loads(scenario_text("quad3d_three_obstacle"))
+    q = np.diag([0.0, 0.0, 0.0, 3e-4, 3e-4, 3e-4])
+    q[3, 4] = q[4, 3] = 1e-4
+    q[4, 5] = q[5, 4] = -0.5e-4
+    q[0, 3] = q[3, 0] = 1e-6
+    q[0, 0] = 1e-5
+    w = np.diag([5e-4, 5e-4, 5e-4])
+    w[0, 1] = w[1, 0] = 2e-4
+    Q = np.eye(6)
+    Q[0, 1] = Q[1, 0] = 0.3
+    j["noise"]["process"] = q.tolist()
+    j["noise"]["measurement"] = w.tolist()
+    j["tracking"] = {"Q": Q.tolist()}
+    j["samples"] = samples
+    j["mc_samples"] = mc
+    return json.dumps(j)

@@ -1,6 +1,7 @@
-"""Subprocess helper for tests/test_gpu_kernels.py::test_mc_direct_paths: the
-MC certification parity cases under a PUMP_MC_* environment (the kernel path
-is fixed per process).  Prints "ok" on success."""
+"""Subprocess helper for tests/test_gpu_kernels.py::test_mc_kernel_paths: the
+MC certification parity cases (axis-separable and coupled closed loops) under
+a PUMP_MC_* environment (the kernel path is fixed per process).  Prints "ok"
+on success."""
 import json
 import os
 import sys
@@ -10,12 +11,12 @@ import numpy as np
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
 import oracle  # noqa: E402
-from conftest import scenario_text  # noqa: E402
+from conftest import coupled_noise_text, scenario_text  # noqa: E402
 from paper_1607_06886_b200 import api  # noqa: E402
 
 ctx = api.Context(0)
-for name, n_mc in [("quad3d_three_obstacle", 3000), ("three_obstacle", 2000)]:
-    txt = scenario_text(name)
+for name, n_mc in [("quad3d_three_obstacle", 3000), ("three_obstacle", 2000), ("coupled", 2000)]:
+    txt = coupled_noise_text() if name == "coupled" else scenario_text(name)
     cl, sc = oracle.scenario_models(txt)
     j = json.loads(txt)
     dw = cl["dw"]

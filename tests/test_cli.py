@@ -152,3 +152,53 @@ def test_cp_compare_matches_reference(tmp_path, name):
             assert abs(got - exp) <= 2.0 / particles, (x, exp)
         else:
             assert abs(got - exp) <= 1e-12 * max(1.0, abs(exp)), (x, exp)
+
+
+def _ref_render(kind, scenario_path, report_path, traj_path):
+    """The reference's own writers (oracle/_ref: report.hpp compiled in place)
+    on the values read back from our files."""
+    import ctypes as C
+
+    lib = os.path.join(ROOT, "oracle", "_ref", "libpumpref.so")
+    if not os.path.exists(lib):
+        pytest.skip("oracle/_ref not built")
+    L = C.CDLL(lib)
+    L.ref_render.argtypes = [C.c_int, C.c_char_p, C.c_char_p, C.c_char_p, C.c_int, C.c_char_p, C.c_long,
+                             C.POINTER(C.c_long)]
+    L.ref_last_error.restype = C.c_char_p
+    args = [open(scenario_path).read().encode(), open(report_path).read().encode(),
+            open(traj_path).read().encode() if traj_path and os.path.exists(traj_path) else b""]
+    n = C.c_long()
+    assert L.ref_render(kind, *args, 1, None, 0, C.byref(n)) == 0, L.ref_last_error()
+    buf = C.create_string_buffer(n.value + 1)
+    assert L.ref_render(kind, *args, 1, buf, n.value + 1, C.byref(n)) == 0
+    return buf.raw[:n.value].split(b"\x1f")
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("scenario", ["minimal.json", "three_obstacle.json"])
+def test_writers_byte_equal_to_reference_writers(tmp_path, scenario):
+    """report.json / pareto.csv / trajectory.json (plan), report.json +
+    trajectory.json (rrt) and report.json (certify) equal, byte for byte, what
+    the reference's own writers (report.hpp:31-129, pump_cli.cpp:48-109) emit
+    for the same result values -- timings included."""
+    sc = os.path.join(SCEN, scenario)
+    out = tmp_path / "plan"
+    r = run("plan", "--scenario", sc, "--out", str(out))
+    assert r.returncode in (0, 2), r.stderr
+    ref = _ref_render(0, sc, out / "report.json", out / "trajectory.json")
+    assert ref[0] == (out / "report.json").read_bytes()
+    assert ref[1] == (out / "pareto.csv").read_bytes()
+    if (out / "trajectory.json").exists():
+        assert ref[2] == (out / "trajectory.json").read_bytes()
+        c = run("certify", "--scenario", sc, "--trajectory", str(out / "trajectory.json"), "--out",
+                str(tmp_path / "cert"))
+        assert c.returncode in (0, 2), c.stderr
+        assert _ref_render(2, sc, tmp_path / "cert" / "report.json", None)[0] == \
+            (tmp_path / "cert" / "report.json").read_bytes()
+    rr = run("rrt", "--scenario", sc, "--out", str(tmp_path / "rrt"))
+    assert rr.returncode in (0, 2), rr.stderr
+    ref = _ref_render(1, sc, tmp_path / "rrt" / "report.json", tmp_path / "rrt" / "trajectory.json")
+    assert ref[0] == (tmp_path / "rrt" / "report.json").read_bytes()
+    if (tmp_path / "rrt" / "trajectory.json").exists():
+        assert ref[1] == (tmp_path / "rrt" / "trajectory.json").read_bytes()

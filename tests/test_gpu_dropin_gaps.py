@@ -13,7 +13,7 @@ import os
 import numpy as np
 import pytest
 
-from conftest import scenario_text
+from conftest import coupled_noise_text, scenario_text
 from test_gpu_planner import explore_equal, random_graph_nodes, with_samples, ws_of, goal_of
 
 pytestmark = pytest.mark.gpu
@@ -141,29 +141,6 @@ def test_run_pump_more_than_512_particles(oracle_lib, gpu_ctx):
     assert_run_equal(got, ref)
 
 
-def coupled_noise_text(samples=500, mc=3000):
-    """quad3d_three_obstacle with full-matrix (cross-axis correlated) process
-    and measurement noise and a coupled tracking weight: the closed loop is
-    not axis-separable, so the dense bank (k_bank_rec<6,3>) and dense MC-table
-    (k_mctab_dense) kernels run (scenario.hpp:110 accepts full matrices)."""
-    j = json.loads(scenario_text("quad3d_three_obstacle"))
-    q = np.diag([0.0, 0.0, 0.0, 3e-4, 3e-4, 3e-4])
-    q[3, 4] = q[4, 3] = 1e-4
-    q[4, 5] = q[5, 4] = -0.5e-4
-    q[0, 3] = q[3, 0] = 1e-6
-    q[0, 0] = 1e-5
-    w = np.diag([5e-4, 5e-4, 5e-4])
-    w[0, 1] = w[1, 0] = 2e-4
-    Q = np.eye(6)
-    Q[0, 1] = Q[1, 0] = 0.3
-    j["noise"]["process"] = q.tolist()
-    j["noise"]["measurement"] = w.tolist()
-    j["tracking"] = {"Q": Q.tolist()}
-    j["samples"] = samples
-    j["mc_samples"] = mc
-    return json.dumps(j)
-
-
 def test_dense_closed_loop_bank_mc_and_solve(oracle_lib, gpu_ctx):
     from paper_1607_06886_b200 import api
     from test_gpu_planner import assert_run_equal
@@ -200,19 +177,19 @@ def test_explore_wide_bucket_range_per_kernel_path(oracle_lib, gpu_ctx, lam):
 
 
 @pytest.mark.parametrize("name,samples", [("three_obstacle", 200), ("quad3d_three_obstacle", 500),
-                                          ("quad3d_indoor", 1200), ("quad3d_forest", 3000)])
+                                          ("quad3d_indoor", None), ("quad3d_forest", None)])
 def test_smooth_entry_point_matches_oracle(oracle_lib, gpu_ctx, name, samples):
     """pump_smooth (the drop-in smooth(), pump.hpp:84-146) runs the device
     speculative chain; the accepted trajectory, cost, CP and s equal the
-    oracle's.  Plans: a solved trajectory, and the same one slowed down
-    (a different bisection path)."""
+    oracle's.  Plans: a solved trajectory (the GPU solve, itself equal to the
+    oracle's), and the same one slowed down (another bisection path)."""
     from paper_1607_06886_b200 import api
 
     txt = with_samples(name, samples, mc_samples=3000)
     cl, sc = oracle_lib.scenario_models(txt)
     j = json.loads(txt)
     ws = ws_of(j)
-    r = oracle_lib.run_pump(txt, workers=WORKERS)
+    r = api.run_pump(api.parse_scenario(txt), ctx=gpu_ctx)
     assert r["success"]
     plans = [(r["traj_t"], r["traj_pos"], r["traj_vel"], r["traj_ctrl"]),
              (2.0 * r["traj_t"], r["traj_pos"], 0.5 * r["traj_vel"], 0.25 * r["traj_ctrl"])]
