@@ -458,6 +458,21 @@ def main():
         elif name == "expand":
             work = prof_w[fam] * 2 * dw
             r["work"] = f"{int(prof_w[fam])} particle-halfspace tests performed x {2 * dw} FP64 ops"
+            # SURVEY §8d K_hsmc HBM-byte model: per task the parent mask in and
+            # the candidate mask out (8 W bytes each), the 32-byte record, and
+            # every half-space of the edge's waypoints ((dw + 1) x 8 bytes)
+            Wm = (scn["particles"] + 63) // 64
+            hbm_bytes = res["partial_plans"] * (2 * 8 * Wm + 32) + res["explore_hs_read"] * (dw + 1) * 8
+            t_solve = prof_ms[fam] / args.steps * 1e-3
+            r["hbm_model"] = {"bytes_per_solve": int(hbm_bytes),
+                              "achieved_gbs": round(hbm_bytes / t_solve / 1e9, 1) if t_solve > 0 else None,
+                              "peak_gbs": hbm, "frac": round(hbm_bytes / t_solve / 1e9 / hbm, 5)
+                              if (t_solve > 0 and hbm) else None,
+                              "model": "tasks x (2 x 8 W mask + 32 record) + half-spaces read x (dw + 1) x 8"}
+        elif name == "regions":
+            work = prof_w[fam]
+            r["work"] = (f"{int(prof_w[fam])} FP64-pipe ops of the region loop (14 per box distance, 10 per prune "
+                         "test, counted in the kernel)")
         elif name == "round_tail":
             r.update({"bound": "hbm", "unit": "GB/s", "peak": hbm,
                       "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy bandwidth)"})
@@ -483,8 +498,31 @@ def main():
         r["frac"] = round(achieved / r["peak"], 5) if r.get("peak") else None
         return r
 
-    roof = roofline_of(int(np.argmax(prof_ms)))
-    rooflines = [roofline_of(FAMILIES.index(f)) for f in ("expand", "round_tail", "mc_table")
+    # ncu DRAM traffic per launch of the family's kernel (committed --set full
+    # captures, tools/ncu_kernels.py; cold-cache, one launch each)
+    ncu_rows = []
+    for f in ("r2_ncu_kernels.json", "r1_ncu_kernels.json"):
+        try:
+            with open(os.path.join(ROOT, "profiles", f)) as fh:
+                ncu_rows = [dict(d, source=f) for d in json.load(fh)["kernels"]]
+            break
+        except Exception:
+            continue
+    FAM_KERNEL = {"regions": "k_regions_once", "round_tail": "k_round_tail", "expand": "k_expand",
+                  "pair_filter": "k_pair_filter_grid", "bank_rec": "k_bank_rec_sep", "mc_table": "k_mcnoise_sep",
+                  "connect": "k_connect", "collide": "k_collide", "mc": "k_mc_tab"}
+
+    def with_traffic(r):
+        pre = FAM_KERNEL.get(r["kernel"])
+        for d in ncu_rows:
+            if pre and d["kernel"].startswith(pre):
+                r["traffic"] = int(d.get("dram_read", 0) + d.get("dram_write", 0))
+                r["traffic_source"] = f"profiles/{d['source']} ({d['kernel']}, ncu dram__bytes_read + write, one launch)"
+                break
+        return r
+
+    roof = with_traffic(roofline_of(int(np.argmax(prof_ms))))
+    rooflines = [with_traffic(roofline_of(FAMILIES.index(f))) for f in ("regions", "expand", "round_tail", "mc_table")
                  if prof_n[FAMILIES.index(f)] > 0]
     kernels = {FAMILIES[i]: {"ms_per_step": round(float(prof_ms[i] / args.steps), 3),
                              "launches_per_step": round(float(prof_n[i] / args.steps), 1)}

@@ -135,6 +135,8 @@ typedef struct pump_result_summary {
   int64_t n_edges, n_plans, mc_rollouts;
   /* repeated_rrt results (pump_rrt_run; 0 for pump_run) */
   int32_t rrt_trials_reaching_goal, rrt_certification_attempts;
+  /* explore: half-spaces of every expanded edge (the HBM-byte model's region reads) */
+  int64_t explore_hs_read;
 } pump_result_summary;
 
 typedef struct pump_ctx pump_ctx;

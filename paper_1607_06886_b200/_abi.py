@@ -78,7 +78,8 @@ class ResultSummaryC(C.Structure):
                 ("selection_seconds", C.c_double),
                 ("bank_ms", C.c_double), ("explore_kernel_ms", C.c_double), ("mc_ms", C.c_double),
                 ("n_edges", C.c_int64), ("n_plans", C.c_int64), ("mc_rollouts", C.c_int64),
-                ("rrt_trials_reaching_goal", C.c_int32), ("rrt_certification_attempts", C.c_int32)]
+                ("rrt_trials_reaching_goal", C.c_int32), ("rrt_certification_attempts", C.c_int32),
+                ("explore_hs_read", C.c_int64)]
 
 
 TERMINATION = {0: "goal_below_alpha_min", 1: "frontier_exhausted"}

@@ -1030,6 +1030,7 @@ static void run_pump_device(Ctx& c, const pumpb::Scenario& s, const DevGraph* pr
   R.s.partial_plans = X.partial_plans;
   R.s.termination = X.termination;
   R.s.n_plans = X.n_plans;
+  R.s.explore_hs_read = X.hs_read;
 
   // goal plans = concat over goal nodes (ascending) of pareto[v] (planner.hpp:264-265)
   std::vector<int32_t> gids, gtend;

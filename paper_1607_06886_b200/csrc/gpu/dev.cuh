@@ -811,7 +811,9 @@ __host__ __device__ inline int convex_region(const WorldD& ws, const double* y, 
 //    same number.
 template <int DW>
 __device__ __forceinline__ int convex_region_fused(const WorldD& ws, const double* y, const double* yd, double* sq,
-                                                   int sq_stride, double* a_out, double* b_out, uint8_t* fb_out) {
+                                                   int sq_stride, double* a_out, double* b_out, uint8_t* fb_out,
+                                                   unsigned& n_clamp, unsigned& n_prune) {
+  n_clamp += ws.n_obs;
   int best = -1;
   double best_sq = __builtin_inf();
   for (int o = 0; o < ws.n_obs; ++o) {
@@ -850,6 +852,7 @@ __device__ __forceinline__ int convex_region_fused(const WorldD& ws, const doubl
     const uint32_t all = ws.n_obs >= 32 ? ~0u : ((1u << ws.n_obs) - 1u);
     for (uint32_t rest = all & ~pruned; rest; rest &= rest - 1) {  // unpruned boxes, ascending
       const int o = __builtin_ctzll_hd(rest);
+      ++n_prune;
       double dot = 0;
 #pragma unroll
       for (int k = 0; k < DW; ++k) dot += d[k] * (cp[k][o * DW] - y[k]);
@@ -919,7 +922,8 @@ __host__ __device__ __forceinline__ double clamp_sq(const WorldD& ws, int o, con
 template <int DW, int kW>
 __device__ __forceinline__ int convex_region_scan(const WorldD& ws, const double* y, const double* yd, double* a_out,
                                                   double* b_out, uint8_t* fb_out, int a_stride, int b_stride,
-                                                  int out_cap) {
+                                                  int out_cap, unsigned& n_clamp, unsigned& n_prune) {
+  n_clamp += ws.n_obs;
   int best = -1;
   double best_sq = __builtin_inf();
   for (int o = 0; o < ws.n_obs; ++o) {
@@ -955,6 +959,7 @@ __device__ __forceinline__ int convex_region_scan(const WorldD& ws, const double
     auto word = [&](int q) {
       for (uint32_t rest = ~pruned[q]; rest; rest &= rest - 1) {
         const int o = 32 * q + __builtin_ctzll_hd(rest);
+        ++n_prune;
         double dot = 0;
 #pragma unroll
         for (int k = 0; k < DW; ++k) dot += d[k] * (cp[k][o * DW] - y[k]);
@@ -963,6 +968,7 @@ __device__ __forceinline__ int convex_region_scan(const WorldD& ws, const double
           any = true;
         } else {
           const double sq = clamp_sq<DW>(ws, o, y);
+          ++n_clamp;
           if (sq < nsq) {
             nsq = sq;
             nb = o;

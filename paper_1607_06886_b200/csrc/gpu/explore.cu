@@ -56,6 +56,7 @@ struct ExpandArgs {
   const uint64_t* mask;
   const double* dy;
   const double* bank_box;  // per bank row: particle box lo[DW], hi[DW]
+  const uint32_t* e_live;  // per edge: waypoints 1..32 with a half-space that can cut the bank's union box
   int N, horizon, W;
   double alpha_max;
   uint8_t* keep;
@@ -144,6 +145,7 @@ __device__ __forceinline__ void expand_task(const ExpandArgs& a, int64_t task, i
     if (lane >= o) incl += y;
   }
   const int total = __shfl_sync(0xffffffffu, incl, 31);
+  int64_t hs_sum = total;  // the edge's half-spaces (first 32 waypoints; the rest below)
   // particles are independent (survival is an AND of per-particle tests), so
   // plans of more than 32 * CH particles run the same steps slab by slab
   constexpr int kSlab = 32 * CH;
@@ -154,7 +156,11 @@ __device__ __forceinline__ void expand_task(const ExpandArgs& a, int64_t task, i
   bool kill[CH];
 #pragma unroll
   for (int c = 0; c < CH; ++c) kill[c] = false;
-  if (ns <= 32 && total <= kExpStage) {
+  const uint32_t live_e = a.e_live[e];
+  if (live_e == 0 && ns <= 32) {
+    // no half-space of the edge can cut the union particle box of all bank
+    // rows: no particle of any plan dies on it (mask copied below)
+  } else if (ns <= 32 && total <= kExpStage) {
     const int my_pre = incl - my_cnt;
     // Each lane stages its waypoint's half-spaces and decides which of them
     // can kill any particle of the bank row the waypoint reads: with the
@@ -164,16 +170,17 @@ __device__ __forceinline__ void expand_task(const ExpandArgs& a, int64_t task, i
     // every particle of the row, bit-exactly.  Waypoints without such a
     // half-space skip the row load and the tests.
     uint64_t my_need = 0;
-    const double* box = my_cnt > 0 ? a.bank_box + static_cast<int64_t>(pt + lane + 1) * 2 * DW : nullptr;
+    const bool my_live = (live_e >> lane) & 1u;
+    const double* box = my_live ? a.bank_box + static_cast<int64_t>(pt + lane + 1) * 2 * DW : nullptr;
     double blo[DW], bhi[DW];
-    if (my_cnt > 0) {
+    if (my_live) {
 #pragma unroll
       for (int k = 0; k < DW; ++k) {
         blo[k] = box[k];
         bhi[k] = box[DW + k];
       }
     }
-    for (int q = 0; q < my_cnt; ++q) {
+    for (int q = 0; q < (my_live ? my_cnt : 0); ++q) {
       const double2 q0 = hpk[(my_h0 + q) * 2], q1 = hpk[(my_h0 + q) * 2 + 1];
       s_hs[wib][my_pre + q][0] = q0;
       s_hs[wib][my_pre + q][1] = q1;
@@ -259,7 +266,15 @@ __device__ __forceinline__ void expand_task(const ExpandArgs& a, int64_t task, i
       int64_t t_l = all ? cnt : __popcll(need);
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) t_l += __shfl_xor_sync(0xffffffffu, t_l, o);
-      if (slab == 0) tests += t_l;
+      if (slab == 0) {
+        tests += t_l;
+        if (jb > 0) {
+          int c_l = cnt;
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) c_l += __shfl_xor_sync(0xffffffffu, c_l, o);
+          hs_sum += c_l;
+        }
+      }
       double p[CH][DW], pn[CH][DW];
       int j = live ? __ffs(live) - 1 : -1;
       if (j >= 0) load_row<DW, CH>(a.dy + static_cast<int64_t>(pt + jb + j + 1) * a.N * DW, a.N, lane, p, pb);
@@ -295,7 +310,10 @@ __device__ __forceinline__ void expand_task(const ExpandArgs& a, int64_t task, i
     }
   }
   }  // slab
-  if (lane == 0) atomicAdd(reinterpret_cast<unsigned long long*>(&a.st->hs_tests), static_cast<unsigned long long>(tests));
+  if (lane == 0) {
+    atomicAdd(reinterpret_cast<unsigned long long*>(&a.st->hs_tests), static_cast<unsigned long long>(tests));
+    atomicAdd(reinterpret_cast<unsigned long long*>(&a.st->hs_read), static_cast<unsigned long long>(hs_sum));
+  }
   if (lane == 0) {
     const double cp = 1.0 - static_cast<double>(pop) / a.N;  // ParticleMask::cp (cp.hpp:42)
     a.c_cp[task] = cp;
@@ -1296,6 +1314,79 @@ __global__ void __launch_bounds__(128) k_bank_box(const double* __restrict__ dy,
   }
 }
 
+// union of the per-row particle boxes over every bank row (one block)
+__global__ void __launch_bounds__(256) k_box_union(const double* __restrict__ box, int rows, int dw,
+                                                   double* __restrict__ out) {
+  __shared__ double s[2][256];
+  for (int k = 0; k < dw; ++k) {
+    double lo = __builtin_inf(), hi = -__builtin_inf();
+    for (int t = threadIdx.x; t < rows; t += blockDim.x) {
+      const double a = box[static_cast<int64_t>(t) * 2 * dw + k], b = box[static_cast<int64_t>(t) * 2 * dw + dw + k];
+      lo = a < lo ? a : lo;
+      hi = b > hi ? b : hi;
+    }
+    s[0][threadIdx.x] = lo;
+    s[1][threadIdx.x] = hi;
+    __syncthreads();
+    for (int o = blockDim.x / 2; o > 0; o >>= 1) {
+      if (threadIdx.x < o) {
+        s[0][threadIdx.x] = s[0][threadIdx.x + o] < s[0][threadIdx.x] ? s[0][threadIdx.x + o] : s[0][threadIdx.x];
+        s[1][threadIdx.x] = s[1][threadIdx.x + o] > s[1][threadIdx.x] ? s[1][threadIdx.x + o] : s[1][threadIdx.x];
+      }
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+      out[k] = s[0][0];
+      out[dw + k] = s[1][0];
+    }
+    __syncthreads();
+  }
+}
+
+// Per edge, the waypoints 1..32 that own a half-space able to cut the union
+// particle box of all bank rows (lane j: waypoint j + 1; the bound is
+// expand_task's, computed on the union box, which contains every row's box,
+// so a clear bit proves the waypoint harmless for every plan: bit-exact).
+// Edges of more than 32 waypoints get every bit (expand's long path tests
+// them anyway).
+template <int DW>
+__global__ void __launch_bounds__(256) k_edge_live(int64_t E, const int64_t* __restrict__ wp_off,
+                                                   const int64_t* __restrict__ hs_off,
+                                                   const int32_t* __restrict__ hs_cnt, const double* __restrict__ hs_pk,
+                                                   const double* __restrict__ ubox, uint32_t* __restrict__ e_live) {
+  const int64_t e = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (e >= E) return;
+  const int64_t w0 = wp_off[e];
+  const int ns = static_cast<int>(wp_off[e + 1] - w0);
+  bool live = ns > 32;
+  if (!live && lane < ns) {
+    double blo[DW], bhi[DW];
+#pragma unroll
+    for (int k = 0; k < DW; ++k) {
+      blo[k] = ubox[k];
+      bhi[k] = ubox[DW + k];
+    }
+    const int64_t h0 = hs_off[w0 + lane];
+    const int cnt = hs_cnt[w0 + lane];
+    const double2* hpk = reinterpret_cast<const double2*>(hs_pk);
+    for (int q = 0; q < cnt && !live; ++q) {
+      const double2 q0 = hpk[(h0 + q) * 2], q1 = hpk[(h0 + q) * 2 + 1];
+      const double av[3] = {q0.x, q0.y, q1.x};
+      double bound = 0;
+#pragma unroll
+      for (int k = 0; k < DW; ++k) {
+        const double m1 = av[k] * blo[k], m2 = av[k] * bhi[k];
+        const double mk = m1 > m2 ? m1 : m2;
+        bound = k == 0 ? mk : bound + mk;
+      }
+      live = bound > q1.y;
+    }
+  }
+  const unsigned m = __ballot_sync(0xffffffffu, live);
+  if (lane == 0) e_live[e] = m;
+}
+
 static void swap_buf(DBuf& a, DBuf& b) {
   std::swap(a.p, b.p);
   std::swap(a.cap, b.cap);
@@ -1348,7 +1439,18 @@ void run_explore_device(DevExplore& X, Ctx& c, const DevGraph& G, const ExploreA
   // particle box of every bank row (k_expand skips rows no half-space can cut)
   DBuf& box = c.buf("x_bank_box", al(static_cast<size_t>(c.bank_horizon + 2) * 2 * G.dw * 8));
   k_bank_box<<<c.bank_horizon + 1, 128, 0, st>>>(c.bank.as<double>(), N, G.dw, box.as<double>());
-  ++c.launches;
+  DBuf& ubox = c.buf("x_bank_ubox", 256);
+  k_box_union<<<1, 256, 0, st>>>(box.as<double>(), c.bank_horizon + 1, G.dw, ubox.as<double>());
+  DBuf& e_live = c.buf("x_e_live", al((G.E + 1) * 4));
+  if (G.E > 0) {
+    KScope ks(st, F_EXPAND);
+    dispatch_dw(G.dw, [&]<int DW>() {
+      k_edge_live<DW><<<grid_for(G.E * 32, 256), 256, 0, st>>>(G.E, G.wp_off.as<int64_t>(), G.hs_off.as<int64_t>(),
+                                                               G.hs_cnt.as<int32_t>(), G.hs_pk.as<double>(),
+                                                               ubox.as<double>(), e_live.as<uint32_t>());
+    });
+  }
+  c.launches += 3;
   X.n_plans = 0;  // buffers (and their capacity) persist across solves
   ensure_arena(X, 1 << 16, st);
   if (!X.status_h) PUMP_CUDA(cudaMallocHost(&X.status_h, sizeof(ExploreStatus)));
@@ -1545,7 +1647,8 @@ void run_explore_device(DevExplore& X, Ctx& c, const DevGraph& G, const ExploreA
                         G.row_ptr.as<int64_t>(), G.e_to.as<int32_t>(), G.e_cost.as<double>(),
                         G.e_nsteps.as<int32_t>(), G.wp_off.as<int64_t>(), G.hs_off.as<int64_t>(),
                         G.hs_cnt.as<int32_t>(), G.hs_pk.as<double>(), X.head.as<int32_t>(), X.cost.as<double>(),
-                        X.t_end.as<int32_t>(), X.mask.as<uint64_t>(), c.bank.as<double>(), box.as<double>(), N,
+                        X.t_end.as<int32_t>(), X.mask.as<uint64_t>(), c.bank.as<double>(), box.as<double>(),
+                        e_live.as<uint32_t>(), N,
                         c.bank_horizon, W,
                         prm.alpha_max, X.cand_keep.as<uint8_t>(), X.cand_head.as<int32_t>(),
                         X.cand_src.as<int32_t>(), X.cand_tend.as<int32_t>(), X.cand_cost.as<double>(),
@@ -1647,7 +1750,7 @@ void run_explore_device(DevExplore& X, Ctx& c, const DevGraph& G, const ExploreA
                       G.hs_off.as<int64_t>(), G.hs_cnt.as<int32_t>(), G.hs_pk.as<double>(),
                       X.head.as<int32_t>(),
                       X.cost.as<double>(), X.t_end.as<int32_t>(), X.mask.as<uint64_t>(), c.bank.as<double>(),
-                    box.as<double>(), N,
+                    box.as<double>(), e_live.as<uint32_t>(), N,
                       c.bank_horizon, W, prm.alpha_max, X.cand_keep.as<uint8_t>(), X.cand_head.as<int32_t>(),
                       X.cand_src.as<int32_t>(), X.cand_tend.as<int32_t>(), X.cand_cost.as<double>(),
                       X.cand_cp.as<double>(), X.cand_mask.as<uint64_t>(), S};
@@ -1802,6 +1905,7 @@ void run_explore_device(DevExplore& X, Ctx& c, const DevGraph& G, const ExploreA
   kprof_work(F_COMMIT, commit_bytes_legacy + h.commit_bytes);  // (the cooperative rounds count on the device)
   kprof_work(F_EXPAND, h.hs_tests * N);
   X.hs_tests = h.hs_tests;
+  X.hs_read = h.hs_read;
   X.n_plans = h.n_plans;
   X.disc_cp = h.disc_cp;
   X.disc_hor = h.disc_hor;

@@ -13,6 +13,7 @@ struct ExploreStatus {  // read back once per round (pinned)
   long long best_goal_bits, min_group_bits;
   long long disc_cp, disc_hor, removed, n_surv, evicted_open, err, touched, hs_tests;
   long long max_goal_tend;  // largest t_end of any plan committed at a goal node
+  long long hs_read;        // half-spaces of every expanded edge (SURVEY §8d HBM-byte model)
   // pipelined rounds (k_round_gate): halt 0 run, 1 the loop-top termination
   // holds, 2 a buffer is too small / the round needs the per-kernel path
   long long halt, n_keys, rounds, partial_plans, commit_bytes;
@@ -32,7 +33,7 @@ struct DevExplore {
   DBuf status_d;
   ExploreStatus* status_h = nullptr;  // pinned
   // results
-  int64_t n_plans = 0, partial_plans = 0, disc_cp = 0, disc_hor = 0, removed = 0, hs_tests = 0;
+  int64_t n_plans = 0, partial_plans = 0, disc_cp = 0, disc_hor = 0, removed = 0, hs_tests = 0, hs_read = 0;
   int rounds = 0;
   unsigned coop_epoch = 0;  // tags the cooperative round's scan status words
   int termination = 0;  // 0 goal_below_alpha_min, 1 frontier_exhausted

@@ -792,11 +792,13 @@ __global__ void __launch_bounds__(128) k_regions_once(GraphArgs g, WorldD w, int
       motion_state<DW>(m, j * g.dt, y, yd);
     }
   }
+  unsigned n_clamp = 0, n_prune = 0;
   auto region = [&](double* ao, double* bo, uint8_t* fo, int as, int bst, int ocap) {
     if constexpr (KW == 0) {
-      return convex_region_fused<DW>(ws, y, yd, smem + 2 * w.n_obs * DW + threadIdx.x, blockDim.x, ao, bo, fo);
+      return convex_region_fused<DW>(ws, y, yd, smem + 2 * w.n_obs * DW + threadIdx.x, blockDim.x, ao, bo, fo,
+                                     n_clamp, n_prune);
     } else {
-      return convex_region_scan<DW, KW>(ws, y, yd, ao, bo, fo, as, bst, ocap);
+      return convex_region_scan<DW, KW>(ws, y, yd, ao, bo, fo, as, bst, ocap, n_clamp, n_prune);
     }
   };
   if (active) {
@@ -805,6 +807,17 @@ __global__ void __launch_bounds__(128) k_regions_once(GraphArgs g, WorldD w, int
       atomicExch(err, 1);
       n = 0;
     }
+  }
+  // algorithmic work of the region loop (distance evaluations, prune tests)
+  unsigned long long wc = n_clamp, wp = n_prune;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    wc += __shfl_xor_sync(0xffffffffu, wc, o);
+    wp += __shfl_xor_sync(0xffffffffu, wp, o);
+  }
+  if (lane == 0) {
+    atomicAdd(counter + 1, wc);
+    atomicAdd(counter + 2, wp);
   }
   // warp-aggregated reservation
   int incl = n;
@@ -1183,7 +1196,7 @@ void build_graph_device(DevGraph& G, Ctx& c, int n, int dw, const double* h_pos,
       G.hs_pk.ensure(al((cap + 1) * 32));
       G.hs_fb.ensure(al(cap + 1));
       G.hs_cap = cap;
-      PUMP_CUDA(cudaMemsetAsync(ctr.p, 0, 8, st));
+      PUMP_CUDA(cudaMemsetAsync(ctr.p, 0, 24, st));
       if (NW > 0) {
         KScope ks(st, F_REGIONS);
         dispatch_dw(dw, [&]<int DW>() {
@@ -1203,11 +1216,16 @@ void build_graph_device(DevGraph& G, Ctx& c, int n, int dw, const double* h_pos,
         ++c.launches;
         PUMP_CUDA(cudaGetLastError());
       }
-      int64_t H = 0;
+      int64_t Hw[3] = {0, 0, 0};
       int herr = 0;
-      c.d2h(&H, ctr.p, 8);
+      c.d2h(Hw, ctr.p, 24);
       c.d2h(&herr, err.p, 4);
       c.sync();
+      const int64_t H = Hw[0];
+      // FP64-pipe ops of the region loop: a box distance |clamp(y) - y|^2 is
+      // 6 compares + 3 sub + 3 mul + 2 add, a prune test 3 sub + 3 mul + 3 add
+      // + 1 compare (the fraction in bench.py's roofline)
+      kprof_work(F_REGIONS, 14 * Hw[1] + 10 * Hw[2]);
       mark("regions");
       if (herr) throw std::runtime_error("local_convex_region: pruning loop failed to make progress");
       G.H = H;

@@ -1,7 +1,8 @@
 """Scenario and scaling sweep on one GPU (BASELINE configs[0], [2] and [4]).
 
     python tools/sweep.py named 3 oracle > gpurun_out/sweep_named.jsonl  # the named scenarios, + oracle check
-    python tools/sweep.py scaling > gpurun_out/sweep_scaling.jsonl # samples x particles x obstacles, one axis at a time
+    python tools/sweep.py scaling 3 oracle > gpurun_out/sweep_scaling.jsonl  # samples x particles x obstacles,
+        one axis at a time, oracle parity on the ORACLE_POINTS (the host oracle finishes them in seconds)
 
 One JSON line per workload: ms per solve (CUDA events on the library stream,
 L2 flushed before each solve, median of K), the reference's phase split
@@ -38,19 +39,24 @@ def variants(kind):
         for n in ("quad3d_three_obstacle", "quad3d_indoor", "quad3d_forest"):
             yield n, named(n)
         return
-    # scaling (configs[4]): one axis at a time around the forest world with 30 boxes
-    base = make_scenarios.forest(n_boxes=30)
-    base.update({"samples": 4000, "particles": 64, "bank_horizon": 1024})
+    # scaling (configs[4]): one axis at a time, on worlds that explore
+    # (> 1e5 partial plans): samples and particles around quad3d_indoor,
+    # obstacles in the quad3d_forest world (40 x 40 x 8 m, n = 16000, N = 128)
+    base = named("quad3d_indoor")
     for n in (2000, 4000, 8000, 16000, 32000, 64000):
-        s = dict(base, samples=n)
-        yield f"forest30_n{n}_N64", s
+        yield f"indoor_n{n}_N64", dict(base, samples=n)
     for p in (16, 32, 128, 256):
-        s = dict(base, particles=p)
-        yield f"forest30_n4000_N{p}", s
-    for k in (3, 10, 100, 300, 1000):
+        yield f"indoor_n4000_N{p}", dict(base, particles=p)
+    fb = named("quad3d_forest")
+    for k in (3, 10, 30, 100, 300, 1000):
         s = make_scenarios.forest(n_boxes=k)
-        s.update({"samples": 4000, "particles": 64, "bank_horizon": 1024})
-        yield f"forest{k}_n4000_N64", s
+        s.update({key: fb[key] for key in ("samples", "particles", "alpha", "bank_horizon", "mc_samples",
+                                           "connection_radius") if key in fb})
+        yield f"forest{k}_n16000_N128", s
+
+
+ORACLE_POINTS = {"quad3d_three_obstacle", "quad3d_indoor", "quad3d_forest", "indoor_n2000_N64", "indoor_n4000_N64",
+                 "indoor_n4000_N16", "indoor_n4000_N32", "indoor_n8000_N64"}
 
 
 def main():
@@ -89,8 +95,26 @@ def main():
             L.pump_ctx_profile_read(ctx.h, pm.ctypes.data_as(C.c_void_p), pn.ctypes.data_as(C.c_void_p),
                                     pw.ctypes.data_as(C.c_void_p))
             L.pump_ctx_profile(ctx.h, 0)
+            # per-family roofline fractions (bench.py's work models)
+            peak = C.c_double()
+            L.pump_peak_fp64.argtypes = [C.c_void_p, C.c_void_p]
+            L.pump_peak_fp64(ctx.h, C.byref(peak))
+            dw = len(scn["workspace"]["bounds"]["lo"])
+            d = 2 * dw
+            F = bench.FAMILIES
+            roof = {}
+            for f, ops in (("regions", 1.0), ("expand", 2.0 * dw), ("mc_table", bench.mc_table_ops_per_step(d, dw))):
+                i = F.index(f)
+                if pn[i] > 0 and pm[i] > 0:
+                    roof[f] = {"fp64_frac": round(pw[i] * ops / (pm[i] * 1e-3) / 1e9 / peak.value, 4),
+                               "ms": round(float(pm[i]), 3)}
+            i = F.index("expand")
+            if pm[i] > 0:
+                Wm = (scn["particles"] + 63) // 64
+                hb = r["partial_plans"] * (2 * 8 * Wm + 32) + r["explore_hs_read"] * (dw + 1) * 8
+                roof["expand"]["hbm_frac"] = round(hb / (pm[i] * 1e-3) / 1e9 / 6553.3, 4)
             line.update({
-                "ms_per_solve": round(statistics.median(ms), 3), "reps": reps,
+                "ms_per_solve": round(statistics.median(ms), 3), "reps": reps, "roofline": roof,
                 "build_graph_ms": round(1e3 * r["build_graph_seconds"], 3),
                 "explore_ms": round(1e3 * r["explore_seconds"], 3),
                 "selection_ms": round(1e3 * r["selection_seconds"], 3),
@@ -99,18 +123,23 @@ def main():
                 "partial_plans_per_s": round(r["partial_plans"] / r["explore_seconds"], 1)
                 if r["explore_seconds"] > 0 else None,
                 "kernels_ms": {bench.FAMILIES[i]: round(float(pm[i]), 3) for i in range(fam) if pn[i] > 0}})
-            if check:
+            if check and (kind == "named" or name in ORACLE_POINTS):
                 import time
 
                 import oracle
 
                 t0 = time.perf_counter()
                 o = oracle.run_pump(json.dumps(scn), workers=os.cpu_count() or 1)
+                bits = lambda a: np.ascontiguousarray(a).view(np.uint64).tolist()  # noqa: E731
                 line["oracle"] = {"ms": round(1e3 * (time.perf_counter() - t0), 1), "cores": os.cpu_count(),
                                   "identical_result": bool(o["path"].tolist() == r["path"].tolist()
                                                            and o["cost"] == r["cost"]
                                                            and o["certified_cp"] == r["certified_cp"]
-                                                           and o["partial_plans"] == r["partial_plans"])}
+                                                           and o["partial_plans"] == r["partial_plans"]
+                                                           and bits(o["pareto_cp"]) == bits(r["pareto_cp"])
+                                                           and bits(o["pareto_cost"]) == bits(r["pareto_cost"])
+                                                           and o["mc_eval_ids"].tolist() == r["mc_eval_ids"].tolist()
+                                                           and bits(o["traj_pos"]) == bits(r["traj_pos"]))}
             del sc
         except Exception as e:  # report and continue with the next workload
             line["error"] = f"{type(e).__name__}: {e}"
