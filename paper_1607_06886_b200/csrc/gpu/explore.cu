@@ -56,7 +56,6 @@ struct ExpandArgs {
   const uint64_t* mask;
   const double* dy;
   const double* bank_box;  // per bank row: particle box lo[DW], hi[DW]
-  const uint32_t* e_live;  // per edge: waypoints 1..32 with a half-space that can cut the bank's union box
   int N, horizon, W;
   double alpha_max;
   uint8_t* keep;
@@ -156,11 +155,7 @@ __device__ __forceinline__ void expand_task(const ExpandArgs& a, int64_t task, i
   bool kill[CH];
 #pragma unroll
   for (int c = 0; c < CH; ++c) kill[c] = false;
-  const uint32_t live_e = a.e_live[e];
-  if (live_e == 0 && ns <= 32) {
-    // no half-space of the edge can cut the union particle box of all bank
-    // rows: no particle of any plan dies on it (mask copied below)
-  } else if (ns <= 32 && total <= kExpStage) {
+  if (ns <= 32 && total <= kExpStage) {
     const int my_pre = incl - my_cnt;
     // Each lane stages its waypoint's half-spaces and decides which of them
     // can kill any particle of the bank row the waypoint reads: with the
@@ -170,17 +165,16 @@ __device__ __forceinline__ void expand_task(const ExpandArgs& a, int64_t task, i
     // every particle of the row, bit-exactly.  Waypoints without such a
     // half-space skip the row load and the tests.
     uint64_t my_need = 0;
-    const bool my_live = (live_e >> lane) & 1u;
-    const double* box = my_live ? a.bank_box + static_cast<int64_t>(pt + lane + 1) * 2 * DW : nullptr;
+    const double* box = my_cnt > 0 ? a.bank_box + static_cast<int64_t>(pt + lane + 1) * 2 * DW : nullptr;
     double blo[DW], bhi[DW];
-    if (my_live) {
+    if (my_cnt > 0) {
 #pragma unroll
       for (int k = 0; k < DW; ++k) {
         blo[k] = box[k];
         bhi[k] = box[DW + k];
       }
     }
-    for (int q = 0; q < (my_live ? my_cnt : 0); ++q) {
+    for (int q = 0; q < my_cnt; ++q) {
       const double2 q0 = hpk[(my_h0 + q) * 2], q1 = hpk[(my_h0 + q) * 2 + 1];
       s_hs[wib][my_pre + q][0] = q0;
       s_hs[wib][my_pre + q][1] = q1;
@@ -1032,6 +1026,8 @@ struct CoopArgs {
   int32_t* group;
   int64_t* task_off;
   int32_t* task_grp;
+  int64_t* task_e;
+  int64_t task_cap;  // task buffer capacity: the next round's map is written only if it fits
   const int64_t* row_ptr;
   unsigned long long* stamps;  // optional phase timestamps (PUMP_DEBUG_COOP)
 };
@@ -1282,6 +1278,23 @@ __global__ void __launch_bounds__(kCoopBlock, 2) k_round_tail(const CoopArgs A) 
     S->commit_bytes += T * (37 + 8 * Wd) + K * (33 + 8 * Wd) + static_cast<long long>(n) * 16 + (pool_old + K) * 9 +
                        Gn * 28;
   }
+  grid_sync(A.bar);
+  STAMP();
+  // the next round's task -> (plan, edge) map (k_task_map's body), so that
+  // round needs no launch for it; skipped when the tasks do not fit (the next
+  // round's gate then halts it and the host runs it with k_task_map)
+  const int64_t Tn = A.task_off[Gn];
+  if (Tn <= A.task_cap) {
+    for (int64_t g = gwarp; g < Gn; g += gwarps) {
+      const int64_t t0 = A.task_off[g], t1 = A.task_off[g + 1];
+      const int pid = A.group[g];
+      const int64_t e0 = A.row_ptr[A.ex.head[pid]];
+      for (int64_t t = t0 + lane; t < t1; t += 32) {
+        A.task_grp[t] = pid;
+        A.task_e[t] = e0 + (t - t0);
+      }
+    }
+  }
   STAMP();
 }
 
@@ -1312,79 +1325,6 @@ __global__ void __launch_bounds__(128) k_bank_box(const double* __restrict__ dy,
     box[static_cast<int64_t>(t) * 2 * dw + k] = a;
     box[static_cast<int64_t>(t) * 2 * dw + dw + k] = b;
   }
-}
-
-// union of the per-row particle boxes over every bank row (one block)
-__global__ void __launch_bounds__(256) k_box_union(const double* __restrict__ box, int rows, int dw,
-                                                   double* __restrict__ out) {
-  __shared__ double s[2][256];
-  for (int k = 0; k < dw; ++k) {
-    double lo = __builtin_inf(), hi = -__builtin_inf();
-    for (int t = threadIdx.x; t < rows; t += blockDim.x) {
-      const double a = box[static_cast<int64_t>(t) * 2 * dw + k], b = box[static_cast<int64_t>(t) * 2 * dw + dw + k];
-      lo = a < lo ? a : lo;
-      hi = b > hi ? b : hi;
-    }
-    s[0][threadIdx.x] = lo;
-    s[1][threadIdx.x] = hi;
-    __syncthreads();
-    for (int o = blockDim.x / 2; o > 0; o >>= 1) {
-      if (threadIdx.x < o) {
-        s[0][threadIdx.x] = s[0][threadIdx.x + o] < s[0][threadIdx.x] ? s[0][threadIdx.x + o] : s[0][threadIdx.x];
-        s[1][threadIdx.x] = s[1][threadIdx.x + o] > s[1][threadIdx.x] ? s[1][threadIdx.x + o] : s[1][threadIdx.x];
-      }
-      __syncthreads();
-    }
-    if (threadIdx.x == 0) {
-      out[k] = s[0][0];
-      out[dw + k] = s[1][0];
-    }
-    __syncthreads();
-  }
-}
-
-// Per edge, the waypoints 1..32 that own a half-space able to cut the union
-// particle box of all bank rows (lane j: waypoint j + 1; the bound is
-// expand_task's, computed on the union box, which contains every row's box,
-// so a clear bit proves the waypoint harmless for every plan: bit-exact).
-// Edges of more than 32 waypoints get every bit (expand's long path tests
-// them anyway).
-template <int DW>
-__global__ void __launch_bounds__(256) k_edge_live(int64_t E, const int64_t* __restrict__ wp_off,
-                                                   const int64_t* __restrict__ hs_off,
-                                                   const int32_t* __restrict__ hs_cnt, const double* __restrict__ hs_pk,
-                                                   const double* __restrict__ ubox, uint32_t* __restrict__ e_live) {
-  const int64_t e = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
-  if (e >= E) return;
-  const int64_t w0 = wp_off[e];
-  const int ns = static_cast<int>(wp_off[e + 1] - w0);
-  bool live = ns > 32;
-  if (!live && lane < ns) {
-    double blo[DW], bhi[DW];
-#pragma unroll
-    for (int k = 0; k < DW; ++k) {
-      blo[k] = ubox[k];
-      bhi[k] = ubox[DW + k];
-    }
-    const int64_t h0 = hs_off[w0 + lane];
-    const int cnt = hs_cnt[w0 + lane];
-    const double2* hpk = reinterpret_cast<const double2*>(hs_pk);
-    for (int q = 0; q < cnt && !live; ++q) {
-      const double2 q0 = hpk[(h0 + q) * 2], q1 = hpk[(h0 + q) * 2 + 1];
-      const double av[3] = {q0.x, q0.y, q1.x};
-      double bound = 0;
-#pragma unroll
-      for (int k = 0; k < DW; ++k) {
-        const double m1 = av[k] * blo[k], m2 = av[k] * bhi[k];
-        const double mk = m1 > m2 ? m1 : m2;
-        bound = k == 0 ? mk : bound + mk;
-      }
-      live = bound > q1.y;
-    }
-  }
-  const unsigned m = __ballot_sync(0xffffffffu, live);
-  if (lane == 0) e_live[e] = m;
 }
 
 static void swap_buf(DBuf& a, DBuf& b) {
@@ -1439,18 +1379,7 @@ void run_explore_device(DevExplore& X, Ctx& c, const DevGraph& G, const ExploreA
   // particle box of every bank row (k_expand skips rows no half-space can cut)
   DBuf& box = c.buf("x_bank_box", al(static_cast<size_t>(c.bank_horizon + 2) * 2 * G.dw * 8));
   k_bank_box<<<c.bank_horizon + 1, 128, 0, st>>>(c.bank.as<double>(), N, G.dw, box.as<double>());
-  DBuf& ubox = c.buf("x_bank_ubox", 256);
-  k_box_union<<<1, 256, 0, st>>>(box.as<double>(), c.bank_horizon + 1, G.dw, ubox.as<double>());
-  DBuf& e_live = c.buf("x_e_live", al((G.E + 1) * 4));
-  if (G.E > 0) {
-    KScope ks(st, F_EXPAND);
-    dispatch_dw(G.dw, [&]<int DW>() {
-      k_edge_live<DW><<<grid_for(G.E * 32, 256), 256, 0, st>>>(G.E, G.wp_off.as<int64_t>(), G.hs_off.as<int64_t>(),
-                                                               G.hs_cnt.as<int32_t>(), G.hs_pk.as<double>(),
-                                                               ubox.as<double>(), e_live.as<uint32_t>());
-    });
-  }
-  c.launches += 3;
+  ++c.launches;
   X.n_plans = 0;  // buffers (and their capacity) persist across solves
   ensure_arena(X, 1 << 16, st);
   if (!X.status_h) PUMP_CUDA(cudaMallocHost(&X.status_h, sizeof(ExploreStatus)));
@@ -1562,6 +1491,7 @@ void run_explore_device(DevExplore& X, Ctx& c, const DevGraph& G, const ExploreA
   // batch, after which the host runs that round synchronously.
   constexpr int kBatch = 8;
   bool force_sync = false;
+  bool map_ready = false;  // the task map of the next round is already on the device
   int64_t max_T = 0;
   long long commit_bytes_legacy = 0;
   c.tic();
@@ -1620,6 +1550,7 @@ void run_explore_device(DevExplore& X, Ctx& c, const DevGraph& G, const ExploreA
      ran_coop = true;
      const long long rounds0 = h.rounds;  // (pipelined: the status counts the rounds that ran)
      const int64_t pool_ub = h.pool_n + (pipe ? kBatch * T : T) + 1;
+     map_ready = false;  // one k_task_map per batch: the batch's tails chain the rest
      for (int64_t rr = 0; rr < nrounds; ++rr) {
       // ---- one cooperative launch for the whole round
       if (pipe) {
@@ -1647,8 +1578,7 @@ void run_explore_device(DevExplore& X, Ctx& c, const DevGraph& G, const ExploreA
                         G.row_ptr.as<int64_t>(), G.e_to.as<int32_t>(), G.e_cost.as<double>(),
                         G.e_nsteps.as<int32_t>(), G.wp_off.as<int64_t>(), G.hs_off.as<int64_t>(),
                         G.hs_cnt.as<int32_t>(), G.hs_pk.as<double>(), X.head.as<int32_t>(), X.cost.as<double>(),
-                        X.t_end.as<int32_t>(), X.mask.as<uint64_t>(), c.bank.as<double>(), box.as<double>(),
-                        e_live.as<uint32_t>(), N,
+                        X.t_end.as<int32_t>(), X.mask.as<uint64_t>(), c.bank.as<double>(), box.as<double>(), N,
                         c.bank_horizon, W,
                         prm.alpha_max, X.cand_keep.as<uint8_t>(), X.cand_head.as<int32_t>(),
                         X.cand_src.as<int32_t>(), X.cand_tend.as<int32_t>(), X.cand_cost.as<double>(),
@@ -1692,16 +1622,21 @@ void run_explore_device(DevExplore& X, Ctx& c, const DevGraph& G, const ExploreA
       A.group = X.group.as<int32_t>();
       A.task_off = X.task_off.as<int64_t>();
       A.task_grp = X.task_grp.as<int32_t>();
+      A.task_e = X.task_e.as<int64_t>();
+      A.task_cap = T;  // task_grp / task_e hold T + 1 entries
       A.row_ptr = G.row_ptr.as<int64_t>();
       static const bool dbg_coop = std::getenv("PUMP_DEBUG_COOP") != nullptr;
       DBuf& stamps = c.buf("x_coop_stamps", 64 * 8);
       A.stamps = dbg_coop ? stamps.as<unsigned long long>() : nullptr;
       const int64_t grid_cap = static_cast<int64_t>(coop_blocks) * 8;
-      k_task_map<<<pipe ? static_cast<unsigned>(std::min<int64_t>(grid_for(pool_ub * 32, 256), grid_cap))
-                        : grid_for(h.G * 32, 256),
-                   256, 0, st>>>(d_G, X.task_off.as<int64_t>(), X.group.as<int32_t>(), X.head.as<int32_t>(),
-                                 G.row_ptr.as<int64_t>(), X.task_grp.as<int32_t>(), X.task_e.as<int64_t>(), S);
-      ++c.launches;
+      if (!map_ready) {  // else the previous round's tail wrote this round's map
+        k_task_map<<<pipe ? static_cast<unsigned>(std::min<int64_t>(grid_for(pool_ub * 32, 256), grid_cap))
+                          : grid_for(h.G * 32, 256),
+                     256, 0, st>>>(d_G, X.task_off.as<int64_t>(), X.group.as<int32_t>(), X.head.as<int32_t>(),
+                                   G.row_ptr.as<int64_t>(), X.task_grp.as<int32_t>(), X.task_e.as<int64_t>(), S);
+        ++c.launches;
+      }
+      map_ready = pipe;  // within a batch the tails chain the maps (a round that did not fit halts)
       {
         const unsigned grid = grid_for(T * 32, 256);  // pipelined: T is the per-round task capacity
         KScope ks(st, F_EXPAND);
@@ -1750,7 +1685,7 @@ void run_explore_device(DevExplore& X, Ctx& c, const DevGraph& G, const ExploreA
                       G.hs_off.as<int64_t>(), G.hs_cnt.as<int32_t>(), G.hs_pk.as<double>(),
                       X.head.as<int32_t>(),
                       X.cost.as<double>(), X.t_end.as<int32_t>(), X.mask.as<uint64_t>(), c.bank.as<double>(),
-                    box.as<double>(), e_live.as<uint32_t>(), N,
+                    box.as<double>(), N,
                       c.bank_horizon, W, prm.alpha_max, X.cand_keep.as<uint8_t>(), X.cand_head.as<int32_t>(),
                       X.cand_src.as<int32_t>(), X.cand_tend.as<int32_t>(), X.cand_cost.as<double>(),
                       X.cand_cp.as<double>(), X.cand_mask.as<uint64_t>(), S};
