@@ -440,7 +440,7 @@ def main():
     d, dw = 2 * len(scn["workspace"]["bounds"]["lo"]), len(scn["workspace"]["bounds"]["lo"])
     n_obs = len(scn["workspace"]["obstacles"])
 
-    ROUND_TAIL_BARRIERS = 11  # grid_sync() calls in k_round_tail (explore.cu)
+    ROUND_TAIL_BARRIERS = 10  # grid_sync() calls in k_round_tail (explore.cu)
 
     def roofline_of(fam):
         name = FAMILIES[fam]

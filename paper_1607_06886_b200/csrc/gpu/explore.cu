@@ -106,7 +106,7 @@ constexpr int kExpStage = 64;  // half-spaces staged per warp (2 KB of shared me
 // current one, so the loop does not wait on a chain of global round trips.
 template <int DW, int CH>
 __device__ __forceinline__ void expand_task(const ExpandArgs& a, int64_t task, int lane, int wib,
-                                            double2 (*s_hs)[kExpStage][2]) {
+                                            double2 (*s_hs)[kExpStage][2], unsigned long long* cnt) {
   const int pid = a.task_pid[task];  // the task's plan and edge (k_task_map)
   const int64_t e = a.task_e[task];
   const double cc = a.cost[pid] + a.e_cost[e];
@@ -304,15 +304,16 @@ __device__ __forceinline__ void expand_task(const ExpandArgs& a, int64_t task, i
     }
   }
   }  // slab
-  if (lane == 0) {
-    atomicAdd(reinterpret_cast<unsigned long long*>(&a.st->hs_tests), static_cast<unsigned long long>(tests));
-    atomicAdd(reinterpret_cast<unsigned long long*>(&a.st->hs_read), static_cast<unsigned long long>(hs_sum));
+  if (lane == 0) {  // block-aggregated by k_expand (one pair of global atomics per block)
+    atomicAdd(&cnt[0], static_cast<unsigned long long>(tests));
+    atomicAdd(&cnt[1], static_cast<unsigned long long>(hs_sum));
   }
   if (lane == 0) {
     const double cp = 1.0 - static_cast<double>(pop) / a.N;  // ParticleMask::cp (cp.hpp:42)
     a.c_cp[task] = cp;
     const bool keep = cp < a.alpha_max;
     a.keep[task] = keep ? 1 : 0;
+    if (keep) atomicMax(&cnt[2], static_cast<unsigned long long>(te));
     if (!keep) atomicAdd(reinterpret_cast<unsigned long long*>(&a.st->disc_cp), 1ull);
   }
 }
@@ -320,11 +321,19 @@ __device__ __forceinline__ void expand_task(const ExpandArgs& a, int64_t task, i
 template <int DW, int CH>
 __global__ void __launch_bounds__(kExpBlock, (CH <= 2 ? 4 : 2)) k_expand(const ExpandArgs a) {
   __shared__ double2 s_hs[kExpBlock / 32][kExpStage][2];
+  __shared__ unsigned long long s_cnt[3];  // half-space tests performed, half-spaces of the edges, max kept t_end
   const int64_t task = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   // (a pipelined round's grid covers its task capacity; a halted round has none)
-  if (task >= *a.d_T || a.st->halt) return;
-  expand_task<DW, CH>(a, task, lane, wib, s_hs);
+  if (a.st->halt || static_cast<int64_t>(blockIdx.x) * (kExpBlock / 32) >= *a.d_T) return;  // block-uniform
+  if (threadIdx.x < 3) s_cnt[threadIdx.x] = 0;
+  __syncthreads();
+  if (task < *a.d_T) expand_task<DW, CH>(a, task, lane, wib, s_hs, s_cnt);
+  __syncthreads();
+  if (threadIdx.x < 2) atomicAdd(threadIdx.x == 0 ? reinterpret_cast<unsigned long long*>(&a.st->hs_tests)
+                                                  : reinterpret_cast<unsigned long long*>(&a.st->hs_read),
+                                 s_cnt[threadIdx.x]);
+  if (threadIdx.x == 2 && s_cnt[2] > 0) atomicMax(&a.st->max_tend, static_cast<long long>(s_cnt[2]));
 }
 
 struct CommitArgs {
@@ -1026,8 +1035,6 @@ struct CoopArgs {
   int32_t* group;
   int64_t* task_off;
   int32_t* task_grp;
-  int64_t* task_e;
-  int64_t task_cap;  // task buffer capacity: the next round's map is written only if it fits
   const int64_t* row_ptr;
   unsigned long long* stamps;  // optional phase timestamps (PUMP_DEBUG_COOP)
 };
@@ -1278,23 +1285,6 @@ __global__ void __launch_bounds__(kCoopBlock, 2) k_round_tail(const CoopArgs A) 
     S->commit_bytes += T * (37 + 8 * Wd) + K * (33 + 8 * Wd) + static_cast<long long>(n) * 16 + (pool_old + K) * 9 +
                        Gn * 28;
   }
-  grid_sync(A.bar);
-  STAMP();
-  // the next round's task -> (plan, edge) map (k_task_map's body), so that
-  // round needs no launch for it; skipped when the tasks do not fit (the next
-  // round's gate then halts it and the host runs it with k_task_map)
-  const int64_t Tn = A.task_off[Gn];
-  if (Tn <= A.task_cap) {
-    for (int64_t g = gwarp; g < Gn; g += gwarps) {
-      const int64_t t0 = A.task_off[g], t1 = A.task_off[g + 1];
-      const int pid = A.group[g];
-      const int64_t e0 = A.row_ptr[A.ex.head[pid]];
-      for (int64_t t = t0 + lane; t < t1; t += 32) {
-        A.task_grp[t] = pid;
-        A.task_e[t] = e0 + (t - t0);
-      }
-    }
-  }
   STAMP();
 }
 
@@ -1491,7 +1481,6 @@ void run_explore_device(DevExplore& X, Ctx& c, const DevGraph& G, const ExploreA
   // batch, after which the host runs that round synchronously.
   constexpr int kBatch = 8;
   bool force_sync = false;
-  bool map_ready = false;  // the task map of the next round is already on the device
   int64_t max_T = 0;
   long long commit_bytes_legacy = 0;
   c.tic();
@@ -1550,7 +1539,6 @@ void run_explore_device(DevExplore& X, Ctx& c, const DevGraph& G, const ExploreA
      ran_coop = true;
      const long long rounds0 = h.rounds;  // (pipelined: the status counts the rounds that ran)
      const int64_t pool_ub = h.pool_n + (pipe ? kBatch * T : T) + 1;
-     map_ready = false;  // one k_task_map per batch: the batch's tails chain the rest
      for (int64_t rr = 0; rr < nrounds; ++rr) {
       // ---- one cooperative launch for the whole round
       if (pipe) {
@@ -1622,21 +1610,16 @@ void run_explore_device(DevExplore& X, Ctx& c, const DevGraph& G, const ExploreA
       A.group = X.group.as<int32_t>();
       A.task_off = X.task_off.as<int64_t>();
       A.task_grp = X.task_grp.as<int32_t>();
-      A.task_e = X.task_e.as<int64_t>();
-      A.task_cap = T;  // task_grp / task_e hold T + 1 entries
       A.row_ptr = G.row_ptr.as<int64_t>();
       static const bool dbg_coop = std::getenv("PUMP_DEBUG_COOP") != nullptr;
       DBuf& stamps = c.buf("x_coop_stamps", 64 * 8);
       A.stamps = dbg_coop ? stamps.as<unsigned long long>() : nullptr;
       const int64_t grid_cap = static_cast<int64_t>(coop_blocks) * 8;
-      if (!map_ready) {  // else the previous round's tail wrote this round's map
-        k_task_map<<<pipe ? static_cast<unsigned>(std::min<int64_t>(grid_for(pool_ub * 32, 256), grid_cap))
-                          : grid_for(h.G * 32, 256),
-                     256, 0, st>>>(d_G, X.task_off.as<int64_t>(), X.group.as<int32_t>(), X.head.as<int32_t>(),
-                                   G.row_ptr.as<int64_t>(), X.task_grp.as<int32_t>(), X.task_e.as<int64_t>(), S);
-        ++c.launches;
-      }
-      map_ready = pipe;  // within a batch the tails chain the maps (a round that did not fit halts)
+      k_task_map<<<pipe ? static_cast<unsigned>(std::min<int64_t>(grid_for(pool_ub * 32, 256), grid_cap))
+                        : grid_for(h.G * 32, 256),
+                   256, 0, st>>>(d_G, X.task_off.as<int64_t>(), X.group.as<int32_t>(), X.head.as<int32_t>(),
+                                 G.row_ptr.as<int64_t>(), X.task_grp.as<int32_t>(), X.task_e.as<int64_t>(), S);
+      ++c.launches;
       {
         const unsigned grid = grid_for(T * 32, 256);  // pipelined: T is the per-round task capacity
         KScope ks(st, F_EXPAND);
