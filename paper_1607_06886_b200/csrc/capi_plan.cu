@@ -1003,13 +1003,8 @@ static void run_pump_device(Ctx& c, const pumpb::Scenario& s, const DevGraph* pr
   shard_range(s.mc_samples, c.rank, c.world, &mr0, &mr1);
   bool side_forked = false;
   ea.on_round = [&](const ExploreStatus& h) {
-    // every certified trajectory is a goal plan's path, whose t_end is at
-    // most the largest t_end of any kept candidate: grow the table to that
-    // from the first rounds on (it leads the goal plans' t_end by about one
-    // edge), so it is ready when explore ends
-    const int64_t lead = std::max<int64_t>(h.max_goal_tend, h.max_tend);
-    if (lead <= 0) return;
-    const int want = static_cast<int>(std::min<int64_t>(s.bank_horizon, lead));
+    if (h.max_goal_tend <= 0) return;
+    const int want = static_cast<int>(std::min<int64_t>(s.bank_horizon, h.max_goal_tend));
     if (mc_table_covers(c.mc_table, L, mr0, mr1, s.seeds.mc, want)) return;
     if (!side_forked) {
       PUMP_CUDA(cudaEventRecord(c.fork, c.stream));
@@ -1020,14 +1015,12 @@ static void run_pump_device(Ctx& c, const pumpb::Scenario& s, const DevGraph* pr
     PUMP_CUDA(cudaEventRecord(c.join, c.side));
     c.mc_join_pending = true;
   };
-#ifdef PUMP_MC_TABLE_BATCHED
-  ea.on_round_batched = true;  // pipelined rounds; the table grows once per batch
-#else
   // per-round hook (not batched): the table must start growing as soon as the
   // first goal plans appear, so the certification does not wait for it later
-  // (batched, the front MC waited ~0.35 ms longer on quad3d_indoor)
+  // (batched, the front MC waited ~0.35 ms longer on quad3d_indoor).  Growing
+  // it eagerly from the kept candidates' largest t_end instead measured slower
+  // (the over-built table's kernels crowd the explore rounds' SMs).
   ea.on_round_batched = false;
-#endif
   run_explore_device(X, c, *graph, ea);
   auto t2 = clk::now();
   static const bool dbg_t = std::getenv("PUMP_DEBUG_TIMING") != nullptr;

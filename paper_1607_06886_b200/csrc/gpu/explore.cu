@@ -313,7 +313,6 @@ __device__ __forceinline__ void expand_task(const ExpandArgs& a, int64_t task, i
     a.c_cp[task] = cp;
     const bool keep = cp < a.alpha_max;
     a.keep[task] = keep ? 1 : 0;
-    if (keep) atomicMax(&cnt[2], static_cast<unsigned long long>(te));
     if (!keep) atomicAdd(reinterpret_cast<unsigned long long*>(&a.st->disc_cp), 1ull);
   }
 }
@@ -321,19 +320,18 @@ __device__ __forceinline__ void expand_task(const ExpandArgs& a, int64_t task, i
 template <int DW, int CH>
 __global__ void __launch_bounds__(kExpBlock, (CH <= 2 ? 4 : 2)) k_expand(const ExpandArgs a) {
   __shared__ double2 s_hs[kExpBlock / 32][kExpStage][2];
-  __shared__ unsigned long long s_cnt[3];  // half-space tests performed, half-spaces of the edges, max kept t_end
+  __shared__ unsigned long long s_cnt[2];  // half-space tests performed, half-spaces of the expanded edges
   const int64_t task = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   // (a pipelined round's grid covers its task capacity; a halted round has none)
   if (a.st->halt || static_cast<int64_t>(blockIdx.x) * (kExpBlock / 32) >= *a.d_T) return;  // block-uniform
-  if (threadIdx.x < 3) s_cnt[threadIdx.x] = 0;
+  if (threadIdx.x < 2) s_cnt[threadIdx.x] = 0;
   __syncthreads();
   if (task < *a.d_T) expand_task<DW, CH>(a, task, lane, wib, s_hs, s_cnt);
   __syncthreads();
   if (threadIdx.x < 2) atomicAdd(threadIdx.x == 0 ? reinterpret_cast<unsigned long long*>(&a.st->hs_tests)
                                                   : reinterpret_cast<unsigned long long*>(&a.st->hs_read),
                                  s_cnt[threadIdx.x]);
-  if (threadIdx.x == 2 && s_cnt[2] > 0) atomicMax(&a.st->max_tend, static_cast<long long>(s_cnt[2]));
 }
 
 struct CommitArgs {

@@ -14,7 +14,6 @@ struct ExploreStatus {  // read back once per round (pinned)
   long long disc_cp, disc_hor, removed, n_surv, evicted_open, err, touched, hs_tests;
   long long max_goal_tend;  // largest t_end of any plan committed at a goal node
   long long hs_read;        // half-spaces of every expanded edge (SURVEY §8d HBM-byte model)
-  long long max_tend;       // largest t_end of any kept candidate (bounds every goal plan's t_end)
   // pipelined rounds (k_round_gate): halt 0 run, 1 the loop-top termination
   // holds, 2 a buffer is too small / the round needs the per-kernel path
   long long halt, n_keys, rounds, partial_plans, commit_bytes;
