@@ -920,28 +920,17 @@ __host__ __device__ __forceinline__ double clamp_sq(const WorldD& ws, int o, con
 }
 
 //
-// lbw (optional): per box a lower bound of |clamp(y) - y| valid for this y
-// (the warp's waypoint box, see k_regions_once), already less a rounding
-// margin.  A box with lbw^2 > best (1 + 1e-9) has a computed squared distance
-// strictly above the current best, so it can be neither the nearest box nor
-// tie with it: its distance is not evaluated.  The counters report the work
-// of the reference's loop (geom.hpp:189-225): a distance per unpruned box per
-// nearest search, a prune test per unpruned box per iteration.
+// The counters report the work of the reference's loop (geom.hpp:189-225): a
+// distance per unpruned box per nearest search, a prune test per unpruned box
+// per iteration.
 template <int DW, int kW>
 __device__ __forceinline__ int convex_region_scan(const WorldD& ws, const double* y, const double* yd, double* a_out,
                                                   double* b_out, uint8_t* fb_out, int a_stride, int b_stride,
-                                                  int out_cap, unsigned& n_clamp, unsigned& n_prune,
-                                                  const double* lbw = nullptr) {
+                                                  int out_cap, unsigned& n_clamp, unsigned& n_prune) {
   n_clamp += ws.n_obs;
-  auto far = [&](int o, double best) {
-    if (!lbw) return false;
-    const double l = lbw[o];
-    return l > 0 && l * l > best * (1.0 + 1e-9);
-  };
   int best = -1;
   double best_sq = __builtin_inf();
   for (int o = 0; o < ws.n_obs; ++o) {
-    if (far(o, best_sq)) continue;
     const double q = clamp_sq<DW>(ws, o, y);
     if (q < best_sq) {
       best_sq = q;
@@ -983,7 +972,6 @@ __device__ __forceinline__ int convex_region_scan(const WorldD& ws, const double
           any = true;
         } else {
           ++n_clamp;
-          if (far(o, nsq)) continue;
           const double sq = clamp_sq<DW>(ws, o, y);
           if (sq < nsq) {
             nsq = sq;

@@ -792,41 +792,13 @@ __global__ void __launch_bounds__(128) k_regions_once(GraphArgs g, WorldD w, int
       motion_state<DW>(m, j * g.dt, y, yd);
     }
   }
-  // per-warp lower bounds of every box's distance for the warp's waypoints:
-  // with c, R the centre and half-diagonal of their bounding box, |clamp(y) -
-  // y| >= |clamp(c) - c| - R (the distance to a convex set is 1-Lipschitz),
-  // less a rounding margin (convex_region_scan skips the distances they rule out)
-  const double* s_lbw = nullptr;
-  if constexpr (KW > 0 && KW <= 8) {  // up to 256 boxes (8 KB per warp)
-    double* lbw = smem + 2 * w.n_obs * DW + static_cast<size_t>(threadIdx.x >> 5) * w.n_obs;
-    double c[DW], r2 = 0;
-#pragma unroll
-    for (int k = 0; k < DW; ++k) {
-      double lo = active ? y[k] : __builtin_inf(), hi = active ? y[k] : -__builtin_inf();
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        lo = fmin(lo, __shfl_xor_sync(0xffffffffu, lo, o));
-        hi = fmax(hi, __shfl_xor_sync(0xffffffffu, hi, o));
-      }
-      if (!(lo <= hi)) lo = hi = 0.0;
-      c[k] = 0.5 * (lo + hi);
-      r2 += (hi - lo) * (hi - lo);
-    }
-    const double R = 0.5 * sqrt(r2);
-    for (int o = lane; o < w.n_obs; o += 32) {
-      const double D = sqrt(clamp_sq<DW>(ws, o, c));
-      lbw[o] = D - R - 1e-9 * (1.0 + D + R);
-    }
-    __syncwarp();
-    s_lbw = lbw;
-  }
   unsigned n_clamp = 0, n_prune = 0;
   auto region = [&](double* ao, double* bo, uint8_t* fo, int as, int bst, int ocap) {
     if constexpr (KW == 0) {
       return convex_region_fused<DW>(ws, y, yd, smem + 2 * w.n_obs * DW + threadIdx.x, blockDim.x, ao, bo, fo,
                                      n_clamp, n_prune);
     } else {
-      return convex_region_scan<DW, KW>(ws, y, yd, ao, bo, fo, as, bst, ocap, n_clamp, n_prune, s_lbw);
+      return convex_region_scan<DW, KW>(ws, y, yd, ao, bo, fo, as, bst, ocap, n_clamp, n_prune);
     }
   };
   if (active) {
@@ -1237,10 +1209,7 @@ void build_graph_device(DevGraph& G, Ctx& c, int n, int dw, const double* h_pos,
           auto kern = w.n_obs <= kOnceMaxObs ? k_regions_once<DW, 0>
                       : w.n_obs <= 256      ? k_regions_once<DW, 8>
                                             : k_regions_once<DW, 128>;
-          // fused: per-thread box distances; scan: per-warp distance lower bounds
-          const size_t sm = wsmem + (w.n_obs <= kOnceMaxObs ? static_cast<size_t>(w.n_obs) * 128 * 8
-                                     : w.n_obs <= 256      ? static_cast<size_t>(w.n_obs) * 4 * 8
-                                                            : 0);
+          const size_t sm = wsmem + (w.n_obs <= kOnceMaxObs ? static_cast<size_t>(w.n_obs) * 128 * 8 : 0);
           if (sm > 48 * 1024)
             PUMP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
           kern<<<grid_for(NW, 128), 128, sm, st>>>(
