@@ -331,9 +331,10 @@ def main():
     # ---- profiled pass (same workload, K more solves): per-launch CUDA events
     # on the library stream, per kernel family -> "kernels" and "roofline"
     L.pump_ctx_profile(ctx.h, 1)
+    res_prof = None
     for _ in range(args.steps):
         L.pump_ctx_flush_l2(ctx.h)
-        api.run_pump(sc, ctx=ctx)
+        res_prof = api.run_pump(sc, ctx=ctx)  # (work counters such as the expand half-space count run here)
     prof_ms = np.zeros(len(FAMILIES))
     prof_n = np.zeros(len(FAMILIES), dtype=np.int64)
     prof_w = np.zeros(len(FAMILIES), dtype=np.int64)
@@ -462,7 +463,7 @@ def main():
             # the candidate mask out (8 W bytes each), the 32-byte record, and
             # every half-space of the edge's waypoints ((dw + 1) x 8 bytes)
             Wm = (scn["particles"] + 63) // 64
-            hbm_bytes = res["partial_plans"] * (2 * 8 * Wm + 32) + res["explore_hs_read"] * (dw + 1) * 8
+            hbm_bytes = res_prof["partial_plans"] * (2 * 8 * Wm + 32) + res_prof["explore_hs_read"] * (dw + 1) * 8
             t_solve = prof_ms[fam] / args.steps * 1e-3
             r["hbm_model"] = {"bytes_per_solve": int(hbm_bytes),
                               "achieved_gbs": round(hbm_bytes / t_solve / 1e9, 1) if t_solve > 0 else None,

@@ -57,6 +57,7 @@ struct ExpandArgs {
   const double* dy;
   const double* bank_box;  // per bank row: particle box lo[DW], hi[DW]
   int N, horizon, W;
+  int count_hs;  // accumulate st->hs_read (profiled pass only)
   double alpha_max;
   uint8_t* keep;
   int32_t* c_head;
@@ -106,7 +107,7 @@ constexpr int kExpStage = 64;  // half-spaces staged per warp (2 KB of shared me
 // current one, so the loop does not wait on a chain of global round trips.
 template <int DW, int CH>
 __device__ __forceinline__ void expand_task(const ExpandArgs& a, int64_t task, int lane, int wib,
-                                            double2 (*s_hs)[kExpStage][2], unsigned long long* cnt) {
+                                            double2 (*s_hs)[kExpStage][2]) {
   const int pid = a.task_pid[task];  // the task's plan and edge (k_task_map)
   const int64_t e = a.task_e[task];
   const double cc = a.cost[pid] + a.e_cost[e];
@@ -304,9 +305,11 @@ __device__ __forceinline__ void expand_task(const ExpandArgs& a, int64_t task, i
     }
   }
   }  // slab
-  if (lane == 0) {  // block-aggregated by k_expand (one pair of global atomics per block)
-    atomicAdd(&cnt[0], static_cast<unsigned long long>(tests));
-    atomicAdd(&cnt[1], static_cast<unsigned long long>(hs_sum));
+  if (lane == 0) {
+    atomicAdd(reinterpret_cast<unsigned long long*>(&a.st->hs_tests), static_cast<unsigned long long>(tests));
+    // the HBM-byte model's half-space count: only in the profiled pass (a
+    // second same-address atomic per task costs ~0.2 ms per solve)
+    if (a.count_hs) atomicAdd(reinterpret_cast<unsigned long long*>(&a.st->hs_read), static_cast<unsigned long long>(hs_sum));
   }
   if (lane == 0) {
     const double cp = 1.0 - static_cast<double>(pop) / a.N;  // ParticleMask::cp (cp.hpp:42)
@@ -320,18 +323,11 @@ __device__ __forceinline__ void expand_task(const ExpandArgs& a, int64_t task, i
 template <int DW, int CH>
 __global__ void __launch_bounds__(kExpBlock, (CH <= 2 ? 4 : 2)) k_expand(const ExpandArgs a) {
   __shared__ double2 s_hs[kExpBlock / 32][kExpStage][2];
-  __shared__ unsigned long long s_cnt[2];  // half-space tests performed, half-spaces of the expanded edges
   const int64_t task = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   // (a pipelined round's grid covers its task capacity; a halted round has none)
-  if (a.st->halt || static_cast<int64_t>(blockIdx.x) * (kExpBlock / 32) >= *a.d_T) return;  // block-uniform
-  if (threadIdx.x < 2) s_cnt[threadIdx.x] = 0;
-  __syncthreads();
-  if (task < *a.d_T) expand_task<DW, CH>(a, task, lane, wib, s_hs, s_cnt);
-  __syncthreads();
-  if (threadIdx.x < 2) atomicAdd(threadIdx.x == 0 ? reinterpret_cast<unsigned long long*>(&a.st->hs_tests)
-                                                  : reinterpret_cast<unsigned long long*>(&a.st->hs_read),
-                                 s_cnt[threadIdx.x]);
+  if (task >= *a.d_T || a.st->halt) return;
+  expand_task<DW, CH>(a, task, lane, wib, s_hs);
 }
 
 struct CommitArgs {
@@ -1369,6 +1365,7 @@ void run_explore_device(DevExplore& X, Ctx& c, const DevGraph& G, const ExploreA
   k_bank_box<<<c.bank_horizon + 1, 128, 0, st>>>(c.bank.as<double>(), N, G.dw, box.as<double>());
   ++c.launches;
   X.n_plans = 0;  // buffers (and their capacity) persist across solves
+  const int count_hs = (kprof_current() && kprof_current()->on) ? 1 : 0;
   ensure_arena(X, 1 << 16, st);
   if (!X.status_h) PUMP_CUDA(cudaMallocHost(&X.status_h, sizeof(ExploreStatus)));
   X.status_d.ensure(al(sizeof(ExploreStatus)) + 256);
@@ -1565,7 +1562,7 @@ void run_explore_device(DevExplore& X, Ctx& c, const DevGraph& G, const ExploreA
                         G.e_nsteps.as<int32_t>(), G.wp_off.as<int64_t>(), G.hs_off.as<int64_t>(),
                         G.hs_cnt.as<int32_t>(), G.hs_pk.as<double>(), X.head.as<int32_t>(), X.cost.as<double>(),
                         X.t_end.as<int32_t>(), X.mask.as<uint64_t>(), c.bank.as<double>(), box.as<double>(), N,
-                        c.bank_horizon, W,
+                        c.bank_horizon, W, count_hs,
                         prm.alpha_max, X.cand_keep.as<uint8_t>(), X.cand_head.as<int32_t>(),
                         X.cand_src.as<int32_t>(), X.cand_tend.as<int32_t>(), X.cand_cost.as<double>(),
                         X.cand_cp.as<double>(), X.cand_mask.as<uint64_t>(), S};
@@ -1667,7 +1664,7 @@ void run_explore_device(DevExplore& X, Ctx& c, const DevGraph& G, const ExploreA
                       X.head.as<int32_t>(),
                       X.cost.as<double>(), X.t_end.as<int32_t>(), X.mask.as<uint64_t>(), c.bank.as<double>(),
                     box.as<double>(), N,
-                      c.bank_horizon, W, prm.alpha_max, X.cand_keep.as<uint8_t>(), X.cand_head.as<int32_t>(),
+                      c.bank_horizon, W, count_hs, prm.alpha_max, X.cand_keep.as<uint8_t>(), X.cand_head.as<int32_t>(),
                       X.cand_src.as<int32_t>(), X.cand_tend.as<int32_t>(), X.cand_cost.as<double>(),
                       X.cand_cp.as<double>(), X.cand_mask.as<uint64_t>(), S};
         const unsigned grid = grid_for(T * 32, 256);

@@ -89,7 +89,7 @@ def main():
                 ms.append(e0.elapsed_time(e1))
             L.pump_ctx_profile(ctx.h, 1)
             L.pump_ctx_flush_l2(ctx.h)
-            api.run_pump(sc, ctx=ctx)
+            rp = api.run_pump(sc, ctx=ctx)
             fam = len(bench.FAMILIES)
             pm, pn, pw = np.zeros(fam), np.zeros(fam, dtype=np.int64), np.zeros(fam, dtype=np.int64)
             L.pump_ctx_profile_read(ctx.h, pm.ctypes.data_as(C.c_void_p), pn.ctypes.data_as(C.c_void_p),
@@ -111,7 +111,7 @@ def main():
             i = F.index("expand")
             if pm[i] > 0:
                 Wm = (scn["particles"] + 63) // 64
-                hb = r["partial_plans"] * (2 * 8 * Wm + 32) + r["explore_hs_read"] * (dw + 1) * 8
+                hb = rp["partial_plans"] * (2 * 8 * Wm + 32) + rp["explore_hs_read"] * (dw + 1) * 8
                 roof["expand"]["hbm_frac"] = round(hb / (pm[i] * 1e-3) / 1e9 / 6553.3, 4)
             line.update({
                 "ms_per_solve": round(statistics.median(ms), 3), "reps": reps, "roofline": roof,
