@@ -149,7 +149,7 @@ __device__ __forceinline__ void expand_task(const ExpandArgs& a, int64_t task, i
   // particles are independent (survival is an AND of per-particle tests), so
   // plans of more than 32 * CH particles run the same steps slab by slab
   constexpr int kSlab = 32 * CH;
-  const int n_slab = (a.N + kSlab - 1) / kSlab;
+  const int n_slab = CH == 16 ? (a.N + kSlab - 1) / kSlab : 1;  // (N <= 32 CH below 16 chunks)
   int pop = 0;
   for (int slab = 0; slab < n_slab; ++slab) {
   const int pb = slab * kSlab;
