@@ -20,7 +20,12 @@ struct CudaError : std::runtime_error {
 };
 
 inline void cuda_check(cudaError_t e, const char* what) {
-  if (e != cudaSuccess) throw CudaError(std::string(what) + ": " + cudaGetErrorString(e));
+  if (e != cudaSuccess) {
+    // clear a non-sticky error (e.g. an allocation that did not fit) so the
+    // next call of the context does not report it again
+    (void)cudaGetLastError();
+    throw CudaError(std::string(what) + ": " + cudaGetErrorString(e));
+  }
 }
 #define PUMP_CUDA(x) ::pumpg::cuda_check((x), #x)
 

@@ -201,3 +201,15 @@ def test_smooth_entry_point_matches_oracle(oracle_lib, gpu_ctx, name, samples):
                 assert got[k] == ref[k], (k, got[k], ref[k])
             for k in ("traj_pos", "traj_vel", "traj_ctrl"):
                 assert np.array_equal(got[k].view(np.uint64), ref[k].view(np.uint64)), k
+
+
+def test_out_of_memory_does_not_poison_the_context(gpu_ctx):
+    """A solve that does not fit in HBM fails with PumpCudaError, and the next
+    solve on the same context runs (the allocation error is not reported again)."""
+    from paper_1607_06886_b200 import api
+
+    big = with_samples("quad3d_indoor", 64000)
+    with pytest.raises(api.PumpCudaError):
+        api.run_pump(api.parse_scenario(big), ctx=gpu_ctx)
+    r = api.run_pump(api.parse_scenario(with_samples("three_obstacle", None)), ctx=gpu_ctx)
+    assert r["success"]
