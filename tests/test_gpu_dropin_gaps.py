@@ -203,13 +203,18 @@ def test_smooth_entry_point_matches_oracle(oracle_lib, gpu_ctx, name, samples):
                 assert np.array_equal(got[k].view(np.uint64), ref[k].view(np.uint64)), k
 
 
-def test_out_of_memory_does_not_poison_the_context(gpu_ctx):
+def test_out_of_memory_does_not_poison_the_context():
     """A solve that does not fit in HBM fails with PumpCudaError, and the next
-    solve on the same context runs (the allocation error is not reported again)."""
+    solve on the same context runs (the allocation error is not reported again).
+    Its own context: the buffers the failed solve did get are freed after."""
     from paper_1607_06886_b200 import api
 
-    big = with_samples("quad3d_indoor", 64000)
-    with pytest.raises(api.PumpCudaError):
-        api.run_pump(api.parse_scenario(big), ctx=gpu_ctx)
-    r = api.run_pump(api.parse_scenario(with_samples("three_obstacle", None)), ctx=gpu_ctx)
-    assert r["success"]
+    ctx = api.Context(0)
+    try:
+        big = with_samples("quad3d_indoor", 64000)
+        with pytest.raises(api.PumpCudaError):
+            api.run_pump(api.parse_scenario(big), ctx=ctx)
+        r = api.run_pump(api.parse_scenario(with_samples("three_obstacle", None)), ctx=ctx)
+        assert r["success"]
+    finally:
+        ctx.close()
