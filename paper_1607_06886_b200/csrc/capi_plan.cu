@@ -202,6 +202,75 @@ __global__ void k_smooth_check(WorldD w, int n_probe, int n_wp, const double* __
   if (!ok) free_flag[pr] = 0;
 }
 
+// The same check with a warp per (probe, waypoint): the waypoint's point_free
+// and the segment's obstacle cull (motion_cull: the boxes not separated from
+// the motion's widened bounding box) run with the lanes over the boxes, then
+// every lane runs motion_collides on the warp's bitmask (identical data, no
+// divergence).  Same tests, same verdicts; a warp instead of a thread because
+// a batch holds only ~4 x 260 items.  Worlds of at most 64 kCullWords boxes.
+template <int DW>
+__global__ void __launch_bounds__(128) k_smooth_check_warp(WorldD w, int n_probe, int n_wp,
+                                                           const double* __restrict__ pt,
+                                                           const double* __restrict__ y,
+                                                           const double* __restrict__ yv, double eps_cc,
+                                                           int32_t* __restrict__ free_flag) {
+  extern __shared__ double smem[];
+  const WorldD ws = stage_world<DW>(w, smem);
+  const int64_t x = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (x >= static_cast<int64_t>(n_probe) * n_wp) return;
+  const int64_t pr = x / n_wp;
+  const int j = static_cast<int>(x % n_wp);
+  if (free_flag[pr] == 0) return;
+  const double* yp = y + x * DW;
+  // point_free (geom.hpp:56-61): bounds, then every box, lanes over the boxes
+  bool hit = false;
+  for (int o = lane; o < ws.n_obs && !hit; o += 32) hit = box_contains<DW>(ws.lo + o * DW, ws.hi + o * DW, yp);
+  bool ok = box_contains<DW>(ws.blo, ws.bhi, yp) && !__any_sync(0xffffffffu, hit);
+  if (ok && j + 1 < n_wp) {
+    const double h = pt[j + 1] - pt[j];
+    if (h > 0) {
+      MotionD<DW> m;
+#pragma unroll
+      for (int k = 0; k < DW; ++k) {
+        m.p0[k] = yp[k];
+        m.v0[k] = yv[x * DW + k];
+        m.p1[k] = y[(x + 1) * DW + k];
+        m.v1[k] = yv[(x + 1) * DW + k];
+      }
+      m.tau = h;
+      coeffs_dev<DW>(m.p0, m.v0, m.p1, m.v1, m.tau, m.a, m.j);
+      // motion_cull with the lanes over the boxes (the same separation test)
+      MotionCull c;
+      double bl[DW], bh[DW];
+      motion_bbox<DW>(m, bl, bh);
+      c.inside = true;
+#pragma unroll
+      for (int k = 0; k < DW; ++k) c.inside = c.inside && bl[k] > ws.blo[k] && bh[k] < ws.bhi[k];
+      c.nlist = -1;
+      c.masked = true;
+      for (int q = 0; q < kCullWords; ++q) {
+        uint64_t word = 0;
+        for (int half = 0; half < 2; ++half) {
+          const int o = q * 64 + half * 32 + lane;
+          bool cand = false;
+          if (o < ws.n_obs) {
+            bool sep = false;
+#pragma unroll
+            for (int k = 0; k < DW; ++k) sep = sep || (bh[k] < ws.lo[o * DW + k]) || (bl[k] > ws.hi[o * DW + k]);
+            cand = !sep;
+          }
+          word |= static_cast<uint64_t>(__ballot_sync(0xffffffffu, cand)) << (32 * half);
+        }
+        c.cand[q] = word;
+      }
+      c.any = (c.cand[0] | c.cand[1] | c.cand[2] | c.cand[3]) != 0;
+      ok = !motion_collides<DW>(m, ws, eps_cc, &c);
+    }
+  }
+  if (!ok && lane == 0) free_flag[pr] = 0;
+}
+
 // The reference's smoothing bisection (pump.hpp:118-141) chained on the
 // stream in depth-2 speculative batches: batch 0 probes s = 1 and the first
 // two bisection levels {0.5, 0.75, 0.25}; batch b >= 1 first replays the two
@@ -876,9 +945,19 @@ static SmoothOut smooth_device(Ctx& c, const std::vector<HWp>& plan, double plan
             np, n_wp, &ch->s[q0], c.scratch["sm_plan"].as<double>(), c.scratch["sm_plan"].as<double>() + n_wp,
             c.scratch["sm_plan"].as<double>() + n_wp * (1 + dw), as_motion<DW>(o), d_y.as<double>(),
             d_yv.as<double>());
-        k_smooth_check<DW><<<grid_for(it, 128), 128, 0, c.stream>>>(
-            wd, np, n_wp, c.scratch["sm_plan"].as<double>(), d_y.as<double>(), d_yv.as<double>(), eps_cc,
-            &ch->live[q0]);
+        if (wd.n_obs <= 64 * kCullWords) {
+          const size_t sm = static_cast<size_t>(2 * wd.n_obs * DW) * 8 + 16;
+          if (sm > 48 * 1024)
+            PUMP_CUDA(cudaFuncSetAttribute(k_smooth_check_warp<DW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           static_cast<int>(sm)));
+          k_smooth_check_warp<DW><<<grid_for(it * 32, 128), 128, sm, c.stream>>>(
+              wd, np, n_wp, c.scratch["sm_plan"].as<double>(), d_y.as<double>(), d_yv.as<double>(), eps_cc,
+              &ch->live[q0]);
+        } else {
+          k_smooth_check<DW><<<grid_for(it, 128), 128, 0, c.stream>>>(
+              wd, np, n_wp, c.scratch["sm_plan"].as<double>(), d_y.as<double>(), d_yv.as<double>(), eps_cc,
+              &ch->live[q0]);
+        }
       });
       c.launches += 3;
       launch_mc(L, dwld, np, d_off.as<int64_t>(), d_y.as<double>(), n_wp, r0, r1, seed, eps_cc,
