@@ -69,7 +69,8 @@ def main():
         d["source"] = os.path.basename(p)
         out.append(d)
     print(json.dumps({"peak_hbm_gbs": hbm, "note": "ncu --set full --clock-control none, one launch per kernel "
-                      "(quad3d_indoor warm solve); frac = the utilization of the bound that applies",
+                      f"({os.environ.get('NCU_WORKLOAD', 'quad3d_forest')} warm solve); frac = the utilization of "
+                      "the bound that applies",
                       "kernels": out}, indent=1))
 
 
