@@ -568,9 +568,10 @@ def main():
     # (tools/ncu_kernels.py; static evidence, not measured in this run)
     ncu_tab = None
     try:
-        with open(os.path.join(ROOT, "profiles", "r1_ncu_kernels.json")) as f:
+        with open(os.path.join(ROOT, "profiles", "r2_ncu_kernels.json")) as f:
             nk = json.load(f)
-        ncu_tab = {"source": "profiles/r1_ncu_kernels.json (ncu --set full, one launch each; not this run)",
+        ncu_tab = {"source": "profiles/r2_ncu_kernels.json (ncu --set full on quad3d_forest, one launch each; "
+                             "not this run)",
                    "kernels": [{k: d.get(k) for k in ("kernel", "dur_us", "bound", "frac", "fp64_pipe_pct",
                                                        "issue_pct", "dram_gbs")} for d in nk["kernels"]]}
     except Exception:
