@@ -1099,7 +1099,7 @@ static void run_pump_device(Ctx& c, const pumpb::Scenario& s, const DevGraph* pr
   // (batched, the front MC waited ~0.35 ms longer on quad3d_indoor).  Growing
   // it eagerly from the kept candidates' largest t_end instead measured slower
   // (the over-built table's kernels crowd the explore rounds' SMs).
-  ea.on_round_batched = false;
+  ea.on_round_batched = false;  // (pipelined batches re-measured in round 2: forest equal, indoor +0.4 ms)
   run_explore_device(X, c, *graph, ea);
   auto t2 = clk::now();
   static const bool dbg_t = std::getenv("PUMP_DEBUG_TIMING") != nullptr;

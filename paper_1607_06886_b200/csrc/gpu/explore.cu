@@ -1105,10 +1105,27 @@ __global__ void __launch_bounds__(kCoopBlock, 2) k_round_tail(const CoopArgs A) 
       A.off2, A.scan_status, ep++, red, &s_pre);
   grid_sync(A.bar);
   STAMP();
-  for (int64_t v = gwarp; v < n; v += gwarps) {
-    const int m = A.mem_cnt[v];
-    const int64_t a0 = A.mem_off[v], b0 = A.off2[v];
-    for (int k = lane; k < m; k += 32) A.new_ids[b0 + k] = A.old_ids[a0 + k];
+  // a warp takes 32 consecutive nodes: each lane loads its node's segment
+  // (one round trip for all 32) and copies a short segment itself; segments of
+  // more than 8 members are then copied by the whole warp, one after another
+  for (int64_t v0 = gwarp * 32; v0 < n; v0 += gwarps * 32) {
+    const int64_t v = v0 + lane;
+    int m = 0;
+    int64_t a0 = 0, b0 = 0;
+    if (v < n) {
+      m = A.mem_cnt[v];
+      a0 = A.mem_off[v];
+      b0 = A.off2[v];
+    }
+    const bool small = m <= 8;
+    if (small)
+      for (int k = 0; k < m; ++k) A.new_ids[b0 + k] = A.old_ids[a0 + k];
+    for (unsigned big = __ballot_sync(0xffffffffu, !small); big; big &= big - 1) {
+      const int src = __ffs(big) - 1;
+      const int mb = __shfl_sync(0xffffffffu, m, src);
+      const int64_t ab = __shfl_sync(0xffffffffu, a0, src), bb = __shfl_sync(0xffffffffu, b0, src);
+      for (int k = lane; k < mb; k += 32) A.new_ids[bb + k] = A.old_ids[ab + k];
+    }
   }
   for (int64_t r = gtid; r < K; r += gthreads) {
     const int64_t id = P0 + r;
