@@ -960,32 +960,41 @@ __device__ __forceinline__ int convex_region_scan(const WorldD& ws, const double
     const double* cp[DW];
 #pragma unroll
     for (int k = 0; k < DW; ++k) cp[k] = (d[k] >= 0 ? ws.lo : ws.hi) + k;
-    auto word = [&](int q) {
+    // prune pass, then the nearest search over the survivors: two loops
+    // with no data-dependent branch inside (a warp's lanes prune different
+    // boxes; one fused loop ran both paths on every trip)
+    auto prune_word = [&](int q) {
+      uint32_t kill = 0u;
       for (uint32_t rest = ~pruned[q]; rest; rest &= rest - 1) {
-        const int o = 32 * q + __builtin_ctzll_hd(rest);
+        const int b = __builtin_ctzll_hd(rest);
+        const int o = 32 * q + b;
         ++n_prune;
         double dot = 0;
 #pragma unroll
         for (int k = 0; k < DW; ++k) dot += d[k] * (cp[k][o * DW] - y[k]);
-        if (!(dot < lim)) {
-          pruned[q] |= 1u << (o & 31);
-          any = true;
-        } else {
-          ++n_clamp;
-          const double sq = clamp_sq<DW>(ws, o, y);
-          if (sq < nsq) {
-            nsq = sq;
-            nb = o;
-          }
-        }
+        kill |= (dot < lim ? 0u : 1u) << b;
+      }
+      pruned[q] |= kill;
+      any = any || kill != 0u;
+    };
+    auto near_word = [&](int q) {
+      for (uint32_t rest = ~pruned[q]; rest; rest &= rest - 1) {
+        const int o = 32 * q + __builtin_ctzll_hd(rest);
+        ++n_clamp;
+        const double sq = clamp_sq<DW>(ws, o, y);
+        nb = sq < nsq ? o : nb;
+        nsq = sq < nsq ? sq : nsq;
       }
     };
     if constexpr (kW <= 8) {  // words in registers
 #pragma unroll
-      for (int q = 0; q < kW; ++q) word(q);
+      for (int q = 0; q < kW; ++q) prune_word(q);
+#pragma unroll
+      for (int q = 0; q < kW; ++q) near_word(q);
     } else {
       const int nw = (ws.n_obs + 31) / 32;
-      for (int q = 0; q < nw; ++q) word(q);
+      for (int q = 0; q < nw; ++q) prune_word(q);
+      for (int q = 0; q < nw; ++q) near_word(q);
     }
     if (!any) return -1;
     if (count < out_cap) {

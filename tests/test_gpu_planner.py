@@ -69,9 +69,10 @@ def test_build_graph_bit_exact(oracle_lib, gpu_ctx, name, samples):
     assert_graph_equal(gg, og)
 
 
-@pytest.mark.parametrize("n_boxes,samples", [(300, 500), (1000, 400)])
+@pytest.mark.parametrize("n_boxes,samples", [(17, 400), (40, 500), (129, 400), (256, 400), (300, 500), (1000, 400)])
 def test_build_graph_many_obstacles(oracle_lib, gpu_ctx, n_boxes, samples):
-    """> 256 boxes: the motion cull keeps a candidate index list instead of the bitmask."""
+    """17-256 boxes: grouped region scan (k-d groups of <= 8 boxes); > 256 boxes: the motion cull keeps a
+    candidate index list instead of the bitmask and regions take the plain scan."""
     import sys
 
     from paper_1607_06886_b200 import api
@@ -88,6 +89,35 @@ def test_build_graph_many_obstacles(oracle_lib, gpu_ctx, n_boxes, samples):
     og = oracle_lib.build_graph(pos, vel, *args, workers=WORKERS).export()
     gg = api.build_graph(pos, vel, *args, ctx=gpu_ctx).export()
     assert og["n_edges"] > 0
+    assert_graph_equal(gg, og)
+
+
+def test_build_graph_duplicate_boxes(oracle_lib, gpu_ctx):
+    """Grouped regions with distance ties: every box listed twice (equal squared distances, the lower
+    workspace index must win as in nearest_obstacle_vector's strict first minimum, geom.hpp:128-141) and
+    boxes sharing faces."""
+    import sys
+
+    from paper_1607_06886_b200 import api
+
+    sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "scenarios"))
+    import make_scenarios
+
+    j = make_scenarios.forest(n_boxes=60)
+    obs = j["workspace"]["obstacles"]
+    # a second copy of each box, interleaved so duplicates land in different k-d groups or the same one
+    twins = [dict(o) for o in obs[::-1]]
+    faces = [{"lo": [o["hi"][0], o["lo"][1], o["lo"][2]], "hi": [o["hi"][0] + 0.5, o["hi"][1], o["hi"][2]]}
+             for o in obs[:20]]
+    j["workspace"]["obstacles"] = obs + twins + faces
+    j["samples"] = 400
+    txt = json.dumps(j)
+    _, sc = oracle_lib.scenario_models(txt)
+    pos, vel = oracle_lib.scenario_nodes(txt)
+    args = (ws_of(j), goal_of(j), sc["r_n"], sc["dt"], sc["eps_cc"], sc["tau_max"])
+    og = oracle_lib.build_graph(pos, vel, *args, workers=WORKERS).export()
+    gg = api.build_graph(pos, vel, *args, ctx=gpu_ctx).export()
+    assert og["n_edges"] > 0 and og["n_halfspaces"] > 0
     assert_graph_equal(gg, og)
 
 

@@ -6,7 +6,8 @@ WANT = ['gpu__time_duration.sum', 'dram__bytes_read.sum', 'dram__bytes_write.sum
         'sm__warps_active.avg.pct_of_peak_sustained_active', 'smsp__issue_active.avg.pct_of_peak_sustained_active',
         'sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active', 'sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active',
         'sm__inst_executed_pipe_fma.avg.pct_of_peak_sustained_active', 'smsp__inst_executed.sum', 'launch__registers_per_thread',
-        'launch__grid_size', 'launch__block_size', 'sm__maximum_warps_per_active_cycle_pct', 'launch__occupancy_limit_registers']
+        'launch__grid_size', 'launch__block_size', 'sm__maximum_warps_per_active_cycle_pct', 'launch__occupancy_limit_registers',
+        'smsp__thread_inst_executed_per_inst_executed.ratio', 'smsp__thread_inst_executed.sum']
 
 
 def summarize(path):
