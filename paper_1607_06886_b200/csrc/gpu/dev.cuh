@@ -923,14 +923,24 @@ __host__ __device__ __forceinline__ double clamp_sq(const WorldD& ws, int o, con
 // The counters report the work of the reference's loop (geom.hpp:189-225): a
 // distance per unpruned box per nearest search, a prune test per unpruned box
 // per iteration.
+//
+// lbs (optional, per warp): lbs[o] <= a lower bound of box o's squared
+// distance to every waypoint of the warp, shrunk by 2e-9 relative, and ub >=
+// the squared distance from any of them to its nearest box.  A box with
+// lbs[o] > ub (first search) or lbs[o] > the best squared distance found so
+// far (later searches) has a computed |clamp(y) - y|^2 strictly larger than
+// the current best (the margin covers every rounding on both sides), so it
+// can neither win nor tie and its distance is not evaluated.
 template <int DW, int kW>
 __device__ __forceinline__ int convex_region_scan(const WorldD& ws, const double* y, const double* yd, double* a_out,
                                                   double* b_out, uint8_t* fb_out, int a_stride, int b_stride,
-                                                  int out_cap, unsigned& n_clamp, unsigned& n_prune) {
+                                                  int out_cap, unsigned& n_clamp, unsigned& n_prune,
+                                                  const double* lbs = nullptr, double ub = 0.0) {
   n_clamp += ws.n_obs;
   int best = -1;
   double best_sq = __builtin_inf();
   for (int o = 0; o < ws.n_obs; ++o) {
+    if (lbs && lbs[o] > ub) continue;  // warp-uniform
     const double q = clamp_sq<DW>(ws, o, y);
     if (q < best_sq) {
       best_sq = q;
@@ -981,6 +991,7 @@ __device__ __forceinline__ int convex_region_scan(const WorldD& ws, const double
       for (uint32_t rest = ~pruned[q]; rest; rest &= rest - 1) {
         const int o = 32 * q + __builtin_ctzll_hd(rest);
         ++n_clamp;
+        if (lbs && lbs[o] > nsq) continue;
         const double sq = clamp_sq<DW>(ws, o, y);
         nb = sq < nsq ? o : nb;
         nsq = sq < nsq ? sq : nsq;
