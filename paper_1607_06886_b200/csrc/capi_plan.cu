@@ -1081,8 +1081,9 @@ static void run_pump_device(Ctx& c, const pumpb::Scenario& s, const DevGraph* pr
   int64_t mr0 = 0, mr1 = s.mc_samples;
   shard_range(s.mc_samples, c.rank, c.world, &mr0, &mr1);
   bool side_forked = false;
+  static const bool dbg_r = std::getenv("PUMP_DEBUG_TIMING") != nullptr;
   ea.on_round = [&](const ExploreStatus& h) {
-    if (std::getenv("PUMP_DEBUG_TIMING"))
+    if (dbg_r)
       std::fprintf(stderr, "[pump r] %8.3f ms plans %lld open %lld max_goal_tend %lld\n", 1e3 * secs(t1, clk::now()),
                    h.n_plans, h.open_count, h.max_goal_tend);
     // before any goal plan: track the wavefront.  A plan's cost is at least
@@ -1092,7 +1093,9 @@ static void run_pump_device(Ctx& c, const pumpb::Scenario& s, const DevGraph* pr
     int64_t w64 = h.max_goal_tend;
     if (w64 <= 0) {
       w64 = static_cast<int64_t>(std::floor(static_cast<double>(h.i) * s.lambda * r_n / s.dt)) - 16;
-      if (w64 <= (c.mc_table.valid ? c.mc_table.t_done : -1) + 16) return;  // grow in slices of >= 16 steps
+      if (w64 < 16) return;
+      const int have = static_cast<int>(std::min<int64_t>(s.bank_horizon, w64 - 16));
+      if (mc_table_covers(c.mc_table, L, mr0, mr1, s.seeds.mc, have)) return;  // grow in slices of >= 16 steps
     }
     const int want = static_cast<int>(std::min<int64_t>(s.bank_horizon, w64));
     if (want < 0) return;

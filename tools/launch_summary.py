@@ -36,7 +36,8 @@ def main():
         a[0] += 1
         a[1] += us
     total = sum(v[1] for v in agg.values())
-    print(f"# ncu --metrics gpu__time_duration.sum --clock-control none python tools/prof_solve.py quad3d_indoor {reps}")
+    cmd = sys.argv[3] if len(sys.argv) > 3 else f"tools/one_solve.py quad3d_forest {reps}"
+    print(f"# ncu --metrics gpu__time_duration.sum --clock-control none python {cmd}")
     print("# last (warm) solve of the process; ncu serializes launches (bank / MC-table side-stream kernels included)")
     print(f"# {len(last)} launches, kernel time sum {total:.1f} us")
     print(f"{'kernel':<54}{'n':>3}{'avg_us':>10}{'total_us':>10}{'share':>8}")
