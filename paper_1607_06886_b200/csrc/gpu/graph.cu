@@ -263,7 +263,23 @@ __global__ void __launch_bounds__(kRowBlock) k_pair_filter_q(GraphArgs g, const 
 // R^2 (1 + 1e-9), far above the distance's rounding).  Survivors land in a
 // bitmask over all n and are compacted in ascending u, so the per-row slab
 // holds exactly the pairs k_pair_filter_q keeps among the cells visited.
-constexpr int kCellMaxList = 512;  // (2 kr + 1)^DW with kr <= 3
+constexpr int kCellMaxList = 2048;  // cells a row may examine (the host sizes the grid for it)
+// Velocity-aware reach of a row (the cell cull of k_pair_filter_grid): a pair
+// of cost <= thr has some tau <= thr with 12 |dp - vbar tau|^2 / tau^3 <=
+// thr - tau, vbar = (av + bv) / 2, so for tau in an interval [tl, th]
+//   |dp - av tau / 2| <= V th / 2 + sqrt((thr - tl) th^3 / 12) = rho
+// (|bv| <= V): dp lies within rho of the box swept by av tau / 2.  A cell
+// whose exact node box is farther than rho from every interval's swept box
+// holds no pair of cost <= thr.  kSaus intervals: (0, thr/64], [thr/64,
+// thr/32], then steps of thr/32 (the outer reach is set by the last ones).
+constexpr int kSaus = 33;
+constexpr int kSausGroups = 8;  // groups of 4 intervals (the first also holds the head)
+__host__ __device__ constexpr int saus_g0(int q) { return q == 0 ? 0 : 1 + 4 * q; }
+struct SausTab {
+  double tl[kSaus], th[kSaus], rho2[kSaus];  // rho2 = (rho (1 + 1e-9) + 1e-12)^2
+  double grho2[kSausGroups];                 // largest rho2 of a group's intervals
+  double ext;                                // largest reach of any interval (rho + V th / 2)
+};
 struct CellGrid {
   double lo[3];
   double inv_h;
@@ -377,7 +393,7 @@ __global__ void k_cell_scatter(int n, const double* __restrict__ pos, const doub
 // the lane-refill walk are k_pair_filter_q's.
 template <int DW>
 __global__ void __launch_bounds__(kRowBlock) k_pair_filter_grid(
-    GraphArgs g, const LbGrid lb, const CellGrid G, int cap, int row0, int refill,
+    GraphArgs g, const LbGrid lb, const CellGrid G, const SausTab SZ, int cap, int row0, int refill,
     const int32_t* __restrict__ ccnt, const int64_t* __restrict__ cstart,
     const unsigned long long* __restrict__ cbox, const int32_t* __restrict__ sidx, const double* __restrict__ spos,
     const double* __restrict__ svel, int32_t* __restrict__ row_cnt, int32_t* __restrict__ su, int use_global) {
@@ -408,39 +424,80 @@ __global__ void __launch_bounds__(kRowBlock) k_pair_filter_grid(
     s_next = 0;
   }
   __syncthreads();
-  // candidate cells: the (2 kr + 1)^DW neighbourhood, kept when non-empty and
-  // its exact box lies within R of the node
+  // candidate cells: the boxes swept by av tau / 2 over the reach intervals
+  // (SausTab), their union's extent bounding the cell range; a non-empty cell
+  // is kept when its exact node box is within rho of some interval's box
+  __shared__ double s_sw[kSaus][2 * DW];
+  __shared__ double s_gw[kSausGroups][2 * DW];  // per group of intervals: the union of their boxes
+  __shared__ int s_c0[DW], s_c1[DW];
+  for (int i = threadIdx.x; i < kSaus; i += blockDim.x) {
+#pragma unroll
+    for (int k = 0; k < DW; ++k) {
+      const double a0 = av[k] * SZ.tl[i] * 0.5, a1 = av[k] * SZ.th[i] * 0.5;
+      s_sw[i][k] = a0 < a1 ? a0 : a1;
+      s_sw[i][DW + k] = a0 < a1 ? a1 : a0;
+    }
+  }
+  if (threadIdx.x < kSausGroups) {  // group q: intervals [saus_g0(q), saus_g0(q + 1)) (av tau / 2 is monotone in tau)
+    const int q = threadIdx.x;
+#pragma unroll
+    for (int k = 0; k < DW; ++k) {
+      const double a0 = av[k] * SZ.tl[saus_g0(q)] * 0.5, a1 = av[k] * SZ.th[saus_g0(q + 1) - 1] * 0.5;
+      s_gw[q][k] = a0 < a1 ? a0 : a1;
+      s_gw[q][DW + k] = a0 < a1 ? a1 : a0;
+    }
+  }
+  if (threadIdx.x < DW) {  // the cell range: every interval's box widened by its rho (ext bounds both)
+    const int k = threadIdx.x;
+    const double c = av[k] * SZ.th[kSaus - 1] * 0.5;
+    double e0 = ap[k] + (c < 0 ? c : 0.0) - SZ.ext, e1 = ap[k] + (c > 0 ? c : 0.0) + SZ.ext;
+    const double x0 = floor((e0 - G.lo[k]) * G.inv_h), x1 = floor((e1 - G.lo[k]) * G.inv_h);
+    s_c0[k] = x0 < 0 ? 0 : (x0 >= G.dims[k] ? G.dims[k] - 1 : static_cast<int>(x0));
+    s_c1[k] = x1 < 0 ? 0 : (x1 >= G.dims[k] ? G.dims[k] - 1 : static_cast<int>(x1));
+  }
+  __syncthreads();
   {
-    int cc[DW];
+    int ext[DW], tot = 1;
 #pragma unroll
-    for (int k = 0; k < DW; ++k) cc[k] = cell_coord<DW>(G, ap, k);
-    const int side = 2 * G.kr + 1;
-    int tot = 1;
-#pragma unroll
-    for (int k = 0; k < DW; ++k) tot *= side;
+    for (int k = 0; k < DW; ++k) {
+      ext[k] = s_c1[k] - s_c0[k] + 1;
+      tot *= ext[k];
+    }
     for (int o = threadIdx.x; o < tot; o += blockDim.x) {
       int r = o, id = 0, mul = 1;
-      bool in = true;
 #pragma unroll
       for (int k = 0; k < DW; ++k) {
-        const int c = cc[k] + (r % side) - G.kr;
-        r /= side;
-        in = in && c >= 0 && c < G.dims[k];
-        id += c * mul;
+        const int cxy = s_c0[k] + r % ext[k];
+        r /= ext[k];
+        id += cxy * mul;
         mul *= G.dims[k];
       }
-      if (!in) continue;
       const int cnt = ccnt[id];
       if (cnt == 0) continue;
-      double d2 = 0.0;
+      double bl[DW], bh[DW];
 #pragma unroll
       for (int k = 0; k < DW; ++k) {
-        const double blo = dbl_of(cbox[static_cast<int64_t>(id) * 6 + k]);
-        const double bhi = dbl_of(cbox[static_cast<int64_t>(id) * 6 + 3 + k]);
-        const double e = ap[k] < blo ? blo - ap[k] : (ap[k] > bhi ? ap[k] - bhi : 0.0);
-        d2 += e * e;
+        bl[k] = dbl_of(cbox[static_cast<int64_t>(id) * 6 + k]) - ap[k];
+        bh[k] = dbl_of(cbox[static_cast<int64_t>(id) * 6 + 3 + k]) - ap[k];
       }
-      if (d2 > G.R2) continue;
+      auto near = [&](const double* sw, double rho2) {
+        double d2 = 0.0;
+#pragma unroll
+        for (int k = 0; k < DW; ++k) {
+          const double g1 = bl[k] - sw[DW + k], g2 = sw[k] - bh[k];
+          const double gap = g1 > 0 ? g1 : (g2 > 0 ? g2 : 0.0);
+          d2 += gap * gap;
+        }
+        return d2 <= rho2;
+      };
+      // the groups with the widest reach first; a group's intervals only when
+      // the cell is within the group's largest rho of the union of their boxes
+      bool keep = false;
+      for (int q = kSausGroups - 1; q >= 0 && !keep; --q) {
+        if (!near(s_gw[q], SZ.grho2[q])) continue;
+        for (int i = saus_g0(q + 1) - 1; i >= saus_g0(q) && !keep; --i) keep = near(s_sw[i], SZ.rho2[i]);
+      }
+      if (!keep) continue;
       const int slot = atomicAdd(&s_ncl, 1);
       cl_start[slot] = static_cast<int>(cstart[id]);
       cl_pref[slot + 1] = cnt;
@@ -1011,6 +1068,7 @@ void build_graph_device(DevGraph& G, Ctx& c, int n, int dw, const double* h_pos,
   const size_t bits_bytes = static_cast<size_t>((n + 31) / 32) * 4;
   const bool use_grid = n > 0 && row_hi > row_lo && bits_bytes <= 160 * 1024;
   CellGrid cg{};
+  SausTab sz{};
   if (use_grid) {
     KScope ks(st, F_PAIR);
     DBuf& stats = c.buf("g_nstats", 256);
@@ -1049,20 +1107,33 @@ void build_graph_device(DevGraph& G, Ctx& c, int n, int dw, const double* h_pos,
       R = std::max(R, V * th + std::sqrt(thr * th * th * th / 12.0));
       R *= 1.0 + 1e-9;
     }
-    double h = 0.5 * R;
-    bool finite = std::isfinite(R) && R > 0;
+    // velocity-aware reach intervals (SausTab, k_pair_filter_grid)
+    for (int i = 0; i < kSaus; ++i) {
+      sz.tl[i] = i == 0 ? 0.0 : i == 1 ? thr / 64 : thr * (i - 1) / 32;
+      sz.th[i] = i == 0 ? thr / 64 : thr * i / 32;
+      const double rho = V * sz.th[i] * 0.5 + std::sqrt((thr - sz.tl[i]) * sz.th[i] * sz.th[i] * sz.th[i] / 12.0);
+      const double r = rho * (1.0 + 1e-9) + 1e-12;
+      sz.rho2[i] = r * r;
+      sz.ext = std::max(sz.ext, r + V * sz.th[i] * 0.5 * (1.0 + 1e-9));
+    }
+    for (int q = 0; q < kSausGroups; ++q)
+      for (int i = saus_g0(q); i < saus_g0(q + 1); ++i) sz.grho2[q] = std::max(sz.grho2[q], sz.rho2[i]);
+    // cells of ~ext / 3.5 (measured on the forest: 430 candidates per row vs
+    // 2249 with the position-only reach), grown until a row's cell range fits
+    // kCellMaxList and the grid 2^22 cells
+    double h = sz.ext / 3.5;
+    bool finite = std::isfinite(R) && R > 0 && std::isfinite(sz.ext);
     for (int k = 0; k < dw; ++k) finite = finite && std::isfinite(lo[k]) && std::isfinite(hi[k]);
     if (finite) {
       for (;;) {
-        int64_t cells = 1;
+        int64_t cells = 1, range = 1;
         for (int k = 0; k < dw; ++k) {
           cg.dims[k] = static_cast<int>(std::min(1024.0, std::floor((hi[k] - lo[k]) / h) + 1.0));
           cells *= cg.dims[k];
+          range *= std::min<int64_t>(cg.dims[k], static_cast<int64_t>(std::floor(2.0 * sz.ext / h)) + 2);
         }
-        cg.kr = static_cast<int>(std::ceil(R / h)) + 1;
-        int side = 1;
-        for (int k = 0; k < dw; ++k) side *= 2 * cg.kr + 1;
-        if (cells <= (int64_t(1) << 22) && side <= kCellMaxList) break;
+        cg.kr = 0;
+        if (cells <= (int64_t(1) << 22) && range <= kCellMaxList) break;
         h *= 1.03;
       }
       for (int k = 0; k < dw; ++k) cg.lo[k] = lo[k];
@@ -1073,6 +1144,9 @@ void build_graph_device(DevGraph& G, Ctx& c, int n, int dw, const double* h_pos,
       cg.inv_h = 0.0;
       cg.kr = 0;
       cg.R2 = INFINITY;
+      for (int i = 0; i < kSaus; ++i) sz.rho2[i] = INFINITY;
+      for (int q = 0; q < kSausGroups; ++q) sz.grho2[q] = INFINITY;
+      sz.ext = INFINITY;
     }
     int n_cells = 1;
     for (int k = 0; k < dw; ++k) n_cells *= cg.dims[k];
@@ -1114,7 +1188,7 @@ void build_graph_device(DevGraph& G, Ctx& c, int n, int dw, const double* h_pos,
           if (sm > 32 * 1024)
             PUMP_CUDA(cudaFuncSetAttribute(k_pair_filter_grid<DW>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
           k_pair_filter_grid<DW><<<row_hi - row_lo, kRowBlock, sm, st>>>(
-              ga, lbg, cg, cap, row_lo, refill, c.scratch["g_ccnt"].as<int32_t>(), c.scratch["g_cstart"].as<int64_t>(),
+              ga, lbg, cg, sz, cap, row_lo, refill, c.scratch["g_ccnt"].as<int32_t>(), c.scratch["g_cstart"].as<int64_t>(),
               c.scratch["g_cbox"].as<unsigned long long>(), c.scratch["g_sidx"].as<int32_t>(),
               c.scratch["g_spos"].as<double>(), c.scratch["g_svel"].as<double>(), rcnt.as<int32_t>(),
               suB.as<int32_t>(), 1);
