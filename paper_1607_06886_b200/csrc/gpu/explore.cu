@@ -1496,6 +1496,8 @@ void run_explore_device(DevExplore& X, Ctx& c, const DevGraph& G, const ExploreA
   int64_t max_T = 0;
   long long commit_bytes_legacy = 0;
   c.tic();
+  ExploreStatus h_hook{};
+  bool hook_pending = false;
   for (;;) {
     // loop-top termination (planner.hpp:126-138); h is the status after the
     // previous collection
@@ -1792,6 +1794,12 @@ void run_explore_device(DevExplore& X, Ctx& c, const DevGraph& G, const ExploreA
       X.pool_flip = !X.pool_flip;
       PUMP_CUDA(cudaGetLastError());
     }
+    // the previous round's hook (side-stream launches) runs here, while the
+    // device works on this round, instead of between the rounds
+    if (hook_pending) {
+      prm.on_round(h_hook);
+      hook_pending = false;
+    }
     c.d2h(X.status_h, S, sizeof(ExploreStatus));
     c.sync();
     const ExploreStatus hp = h;
@@ -1823,7 +1831,10 @@ void run_explore_device(DevExplore& X, Ctx& c, const DevGraph& G, const ExploreA
       commit_bytes_legacy += Tr * (37 + 8 * W) + Kr * (33 + 8 * W) + static_cast<int64_t>(n) * 16 +
                              (hp.pool_n + Kr) * 9 + h.G * 28;
     }
-    if (prm.on_round) prm.on_round(h);
+    if (prm.on_round) {
+      h_hook = h;
+      hook_pending = true;
+    }
     if (prm.on_round_state) {
       X.disc_cp = h.disc_cp;
       X.disc_hor = h.disc_hor;
@@ -1831,6 +1842,7 @@ void run_explore_device(DevExplore& X, Ctx& c, const DevGraph& G, const ExploreA
       prm.on_round_state(X.rounds, expanded);
     }
   }
+  if (hook_pending) prm.on_round(h_hook);  // the last round's
   X.kernel_ms = c.toc();
   kprof_work(F_COMMIT, commit_bytes_legacy + h.commit_bytes);  // (the cooperative rounds count on the device)
   kprof_work(F_EXPAND, h.hs_tests * N);
