@@ -1421,6 +1421,15 @@ void build_graph_device(DevGraph& G, Ctx& c, int n, int dw, const double* h_pos,
     }
     DBuf& ctr = c.buf("g_hs_counter", 256);
     int64_t cap = std::max<int64_t>(G.hs_cap, NW * 4 + 16);
+    // the first pass counts even what does not fit (the exact rerun below), so
+    // its buffer never needs more than the free memory
+    auto room = [&]() {
+      size_t free_b = 0, total_b = 0;
+      PUMP_CUDA(cudaMemGetInfo(&free_b, &total_b));
+      const size_t mine = G.hs_pk.cap + G.hs_fb.cap, keep = size_t(1) << 30;
+      return static_cast<int64_t>((free_b + mine > keep ? free_b + mine - keep : 0) / 33);
+    };
+    cap = std::max<int64_t>(16, std::min(cap, room()));
     for (int attempt = 0; attempt < 2; ++attempt) {
       G.hs_pk.ensure(al((cap + 1) * 32));
       G.hs_fb.ensure(al(cap + 1));
@@ -1477,6 +1486,11 @@ void build_graph_device(DevGraph& G, Ctx& c, int n, int dw, const double* h_pos,
                      (long long)G.E, (long long)NW, (long long)H);
       if (H <= cap) break;
       cap = H + H / 8;  // rerun with room to spare (per-waypoint content is deterministic)
+      if (H > room())
+        throw CudaError("build_graph: the convex regions of " + std::to_string(NW) + " edge waypoints hold " +
+                        std::to_string(H) + " half-spaces (" + std::to_string(static_cast<long long>(H * 33 / 1e9)) +
+                        " GB), more than the free device memory");
+      cap = std::min(cap, room());
     }
     c.sync();
     return;

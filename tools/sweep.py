@@ -56,7 +56,9 @@ def variants(kind):
 
 
 ORACLE_POINTS = {"quad3d_three_obstacle", "quad3d_indoor", "quad3d_forest", "indoor_n2000_N64", "indoor_n4000_N64",
-                 "indoor_n4000_N16", "indoor_n4000_N32", "indoor_n8000_N64"}
+                 "indoor_n4000_N16", "indoor_n4000_N32", "indoor_n8000_N64", "indoor_n4000_N128",
+                 "indoor_n4000_N256", "forest3_n16000_N128", "forest10_n16000_N128", "forest30_n16000_N128",
+                 "forest100_n16000_N128", "forest300_n16000_N128"}
 
 
 def main():
