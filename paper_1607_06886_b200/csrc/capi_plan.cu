@@ -715,6 +715,27 @@ __global__ void k_halton_take(int dw, int64_t M, int64_t need, int64_t row0, con
   if (ing[x]) atomicOr(goal_flag, 1);
 }
 
+// the goal fallback of sample_free (sample.hpp:63-88): the first goal Halton
+// index in [1, kGoalTries] whose state is within the goal speed and free
+constexpr int kGoalTries = 100000;
+template <int DW>
+__global__ void k_goal_halton(SampleBox B, WorldD w, int* __restrict__ first) {
+  const int gi = 1 + blockIdx.x * blockDim.x + threadIdx.x;
+  if (gi > kGoalTries) return;
+  constexpr int kPrimes[12] = {2, 3, 5, 7, 11, 13, 17, 19, 23, 29, 31, 37};
+  double p[DW], v[DW];
+#pragma unroll
+  for (int k = 0; k < DW; ++k) {
+    const double u = halton_dev(static_cast<uint64_t>(gi), kPrimes[k]);
+    p[k] = B.glo[k] + u * (B.ghi[k] - B.glo[k]);
+    const double q = halton_dev(static_cast<uint64_t>(gi), kPrimes[DW + k]);
+    v[k] = -B.gms + q * 2 * B.gms;
+  }
+  if (sqrt(sqnorm<DW>(v)) > B.gms) return;
+  if (!point_free<DW>(w, p)) return;
+  atomicMin(first, gi);
+}
+
 static void sample_nodes_device(Ctx& c, const pumpb::Scenario& s, const HostWorld& hw, const DevWorld& dwld,
                                 DevGraph& G, std::vector<double>& pos, std::vector<double>& vel) {
   const int dw = s.workspace_dim();
@@ -787,11 +808,21 @@ static void sample_nodes_device(Ctx& c, const pumpb::Scenario& s, const HostWorl
       v[k] = 0.0;
     }
     bool placed = point_free_h(hw, p);
-    for (uint64_t gi = 1; gi <= 100000 && !placed; ++gi) {
-      halton_state(gi, s.goal.lo.data(), s.goal.hi.data(), dw, s.goal_max_speed, p, v);
-      if (std::sqrt(seq_sqn(v, dw)) > s.goal_max_speed) continue;
-      if (!point_free_h(hw, p)) continue;
-      placed = true;
+    if (!placed) {  // the goal Halton sequence, searched on the device
+      DBuf& fb = c.buf("s_goal_first", 256);
+      const int none = kGoalTries + 1;
+      c.h2d(fb.p, &none, 4);
+      dispatch_dw(dw, [&]<int DW>() {
+        k_goal_halton<DW><<<grid_for(kGoalTries, 256), 256, 0, c.stream>>>(B, wd, fb.as<int>());
+      });
+      ++c.launches;
+      int first = none;
+      c.d2h(&first, fb.p, 4);
+      c.sync();
+      if (first <= kGoalTries) {
+        halton_state(static_cast<uint64_t>(first), s.goal.lo.data(), s.goal.hi.data(), dw, s.goal_max_speed, p, v);
+        placed = true;
+      }
     }
     if (!placed) throw std::runtime_error("sample_free: goal region appears entirely in collision");
     pos.insert(pos.end(), p, p + dw);

@@ -257,6 +257,32 @@ def test_run_pump_matches_oracle(oracle_lib, gpu_ctx, name, samples, mc):
     assert_run_equal(got, ref)
 
 
+def test_run_pump_goal_fallback_sample(oracle_lib, gpu_ctx):
+    """sample_free's goal fallback (sample.hpp:63-88): no Halton sample lands in the goal and its centre is blocked
+    (the 10-box forest), so the first free goal Halton state is appended; searched on the device."""
+    import sys
+
+    from paper_1607_06886_b200 import api
+
+    sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "scenarios"))
+    import make_scenarios
+
+    j = make_scenarios.forest(n_boxes=10)
+    j.update({"samples": 1500, "mc_samples": 3000})
+    j["goal"]["lo"] = [20.0, 20.0, 3.5]  # a 0.3 m goal box is missed by 1500 Halton samples: its free centre is
+    j["goal"]["hi"] = [20.3, 20.3, 3.8]  # appended
+    txt = json.dumps(j)
+    got = api.run_pump(api.parse_scenario(txt), ctx=gpu_ctx)
+    ref = oracle_lib.run_pump(txt, workers=WORKERS)
+    assert_run_equal(got, ref)
+    box = {"lo": [20.1, 20.1, 3.6], "hi": [20.2, 20.2, 3.7]}  # and with the goal centre inside an obstacle
+    j["workspace"]["obstacles"] = j["workspace"]["obstacles"] + [box]
+    txt = json.dumps(j)
+    got = api.run_pump(api.parse_scenario(txt), ctx=gpu_ctx)
+    ref = oracle_lib.run_pump(txt, workers=WORKERS)
+    assert_run_equal(got, ref)
+
+
 @pytest.mark.parametrize("name,samples", [("three_obstacle", None), ("quad3d_three_obstacle", 600)])
 def test_run_pump_prebuilt_graph(oracle_lib, gpu_ctx, name, samples):
     """run_pump(s, workers, prebuilt) (pump.hpp:170-171): a graph built from
