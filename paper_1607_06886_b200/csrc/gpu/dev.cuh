@@ -925,7 +925,8 @@ __host__ __device__ __forceinline__ double clamp_sq(const WorldD& ws, int o, con
 // per iteration.
 //
 // lbs (optional, per warp): lbs[o] <= a lower bound of box o's squared
-// distance to every waypoint of the warp, shrunk by 2e-9 relative, and ub >=
+// distance to every waypoint of the warp, shrunk by 2e-9 relative and rounded
+// down to binary32 (a float compared as a double: exact), and ub >=
 // the squared distance from any of them to its nearest box.  A box with
 // lbs[o] > ub (first search) or lbs[o] > the best squared distance found so
 // far (later searches) has a computed |clamp(y) - y|^2 strictly larger than
@@ -935,7 +936,7 @@ template <int DW, int kW>
 __device__ __forceinline__ int convex_region_scan(const WorldD& ws, const double* y, const double* yd, double* a_out,
                                                   double* b_out, uint8_t* fb_out, int a_stride, int b_stride,
                                                   int out_cap, unsigned& n_clamp, unsigned& n_prune,
-                                                  const double* lbs = nullptr, double ub = 0.0) {
+                                                  const float* lbs = nullptr, double ub = 0.0) {
   n_clamp += ws.n_obs;
   int best = -1;
   double best_sq = __builtin_inf();

@@ -918,10 +918,10 @@ __global__ void __launch_bounds__(128) k_regions_once(GraphArgs g, WorldD w, int
   // squared distance to W (lbs, shrunk by 2e-9) and the warp minimum over the
   // boxes of the largest squared distance from W (ub): convex_region_scan
   // skips the distances these bounds prove cannot be the nearest
-  double* lbs = nullptr;
+  float* lbs = nullptr;
   double ub = __builtin_inf();
   if (KW > 0 && w.n_obs <= kLbsMaxObs) {
-    lbs = smem + 2 * w.n_obs * DW + (threadIdx.x >> 5) * w.n_obs;
+    lbs = reinterpret_cast<float*>(smem + 2 * w.n_obs * DW) + (threadIdx.x >> 5) * w.n_obs;
     double wlo[DW], whi[DW];
 #pragma unroll
     for (int k = 0; k < DW; ++k) {
@@ -949,7 +949,7 @@ __global__ void __launch_bounds__(128) k_regions_once(GraphArgs g, WorldD w, int
           const double e = e1 > e2 ? e1 : e2;
           far = far + e * e;
         }
-        lbs[o] = lb * (1.0 - 2e-9);
+        lbs[o] = __double2float_rd(lb * (1.0 - 2e-9));  // rounded down: still a lower bound
         ub = far < ub ? far : ub;
       }
 #pragma unroll
@@ -1447,7 +1447,7 @@ void build_graph_device(DevGraph& G, Ctx& c, int n, int dw, const double* h_pos,
                       : w.n_obs <= 256      ? k_regions_once<DW, 8>
                                             : k_regions_once<DW, 128>;
           const size_t sm = wsmem + (w.n_obs <= kOnceMaxObs ? static_cast<size_t>(w.n_obs) * 128 * 8
-                                     : w.n_obs <= kLbsMaxObs ? static_cast<size_t>(w.n_obs) * 4 * 8  // lbs, 4 warps
+                                     : w.n_obs <= kLbsMaxObs ? static_cast<size_t>(w.n_obs) * 4 * 4  // lbs, 4 warps
                                                              : 0);
           if (sm > 48 * 1024)
             PUMP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
