@@ -130,40 +130,53 @@ __global__ void __launch_bounds__(32) k_bank_rec_sep(const SepBlocks B, int n, i
 #pragma unroll
     for (int r = 0; r < 4; ++r) z[r] = zstate[static_cast<int64_t>(x) * 4 + r];
   }
-  double un[8];
-  if (tc > 0) {
+  // only n dw / 32 warps run, so the step loop is bound by the latency of
+  // its noise loads: a ring of kRecPf steps in registers, each step's load
+  // issued kRecPf steps before it is consumed (the loop unrolled by the ring
+  // length so the ring stays in registers)
+  constexpr int kRecPf = 4;
+  double ring[kRecPf][8];
+  auto fetch = [&](int tl, double* dst) {
+    const double* u = uw + static_cast<int64_t>(tl) * (4 * D) * n + i;
 #pragma unroll
     for (int r = 0; r < 4; ++r) {
-      un[r] = uw[static_cast<int64_t>(g[r]) * n + i];
-      un[4 + r] = uw[static_cast<int64_t>(D * 2 + g[r]) * n + i];
+      dst[r] = u[static_cast<int64_t>(g[r]) * n];
+      dst[4 + r] = u[static_cast<int64_t>(2 * D + g[r]) * n];
     }
-  }
-  for (int tl = 0; tl <= tc; ++tl) {
-    const int t = t0 + tl;
-    if (tl == tc && t != T) break;  // next chunk stores y_t
-    dy[(static_cast<int64_t>(t) * n + i) * DW + k] = (0.0 + B.C[k][0] * z[0]) + B.C[k][1] * z[1];
-    if (t == T) break;
-    double uc[8];
+  };
 #pragma unroll
-    for (int r = 0; r < 8; ++r) uc[r] = un[r];
-    if (tl + 1 < tc) {
-      const double* u = uw + static_cast<int64_t>(tl + 1) * (4 * D) * n + i;
+  for (int q = 0; q < kRecPf; ++q)
+    if (q < tc) fetch(q, ring[q]);
+  bool done = false;
+  for (int tb = 0; tb <= tc && !done; tb += kRecPf) {
+#pragma unroll
+    for (int q = 0; q < kRecPf; ++q) {
+      const int tl = tb + q;
+      const int t = t0 + tl;
+      if (tl > tc || (tl == tc && t != T)) {  // next chunk stores y_t
+        done = true;
+        break;
+      }
+      dy[(static_cast<int64_t>(t) * n + i) * DW + k] = (0.0 + B.C[k][0] * z[0]) + B.C[k][1] * z[1];
+      if (t == T) {
+        done = true;
+        break;
+      }
+      double uc[8];
+#pragma unroll
+      for (int r = 0; r < 8; ++r) uc[r] = ring[q][r];
+      if (tl + kRecPf < tc) fetch(tl + kRecPf, ring[q]);
+      double zn[4];
 #pragma unroll
       for (int r = 0; r < 4; ++r) {
-        un[r] = u[static_cast<int64_t>(g[r]) * n];
-        un[4 + r] = u[static_cast<int64_t>(2 * D + g[r]) * n];
+        double c = 0.0;
+#pragma unroll
+        for (int w = 0; w < 4; ++w) c = c + F[r * 4 + w] * z[w];
+        zn[r] = (c + uc[r]) + uc[4 + r];
       }
+#pragma unroll
+      for (int r = 0; r < 4; ++r) z[r] = zn[r];
     }
-    double zn[4];
-#pragma unroll
-    for (int r = 0; r < 4; ++r) {
-      double c = 0.0;
-#pragma unroll
-      for (int q = 0; q < 4; ++q) c = c + F[r * 4 + q] * z[q];
-      zn[r] = (c + uc[r]) + uc[4 + r];
-    }
-#pragma unroll
-    for (int r = 0; r < 4; ++r) z[r] = zn[r];
   }
 #pragma unroll
   for (int r = 0; r < 4; ++r) zstate[static_cast<int64_t>(x) * 4 + r] = z[r];

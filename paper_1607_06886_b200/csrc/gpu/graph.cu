@@ -1429,7 +1429,8 @@ void build_graph_device(DevGraph& G, Ctx& c, int n, int dw, const double* h_pos,
       const size_t mine = G.hs_pk.cap + G.hs_fb.cap, keep = size_t(1) << 30;
       return static_cast<int64_t>((free_b + mine > keep ? free_b + mine - keep : 0) / 33);
     };
-    cap = std::max<int64_t>(16, std::min(cap, room()));
+    // (only when the buffer must grow: cudaMemGetInfo is not free)
+    if (static_cast<size_t>(cap + 1) * 32 > G.hs_pk.cap) cap = std::max<int64_t>(16, std::min(cap, room()));
     for (int attempt = 0; attempt < 2; ++attempt) {
       G.hs_pk.ensure(al((cap + 1) * 32));
       G.hs_fb.ensure(al(cap + 1));
