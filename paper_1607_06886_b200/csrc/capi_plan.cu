@@ -736,8 +736,33 @@ __global__ void k_goal_halton(SampleBox B, WorldD w, int* __restrict__ first) {
   atomicMin(first, gi);
 }
 
-static void sample_nodes_device(Ctx& c, const pumpb::Scenario& s, const HostWorld& hw, const DevWorld& dwld,
-                                DevGraph& G, std::vector<double>& pos, std::vector<double>& vel) {
+// goal nodes (graph_goal_nodes) on the device: flag, scan, ascending scatter
+__global__ void k_goal_flags(int n, int dw, const double* __restrict__ pos, const double* __restrict__ vel, SampleBox B,
+                             uint8_t* __restrict__ flag) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  bool in = true;
+  double sq = 0.0;
+  for (int k = 0; k < dw; ++k) {
+    const double p = pos[i * dw + k], v = vel[i * dw + k];
+    in = in && !(p < B.glo[k] || p > B.ghi[k]);
+    sq = sq + v * v;  // seq_sqn
+  }
+  flag[i] = (in && sqrt(sq) <= B.gms) ? 1 : 0;
+}
+__global__ void k_goal_scatter(int n, const uint8_t* __restrict__ flag, const int64_t* __restrict__ off,
+                               int32_t* __restrict__ out) {  // out[0] = count, out[1 + j] = goal node j
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i == n) out[0] = static_cast<int32_t>(off[n]);
+  if (i >= n || !flag[i]) return;
+  out[1 + off[i]] = i;
+}
+
+// sample_free on the device; `overlap` (host work) runs while the first
+// batch's kernels do.  Returns the node count (the nodes stay in G.pos / G.vel).
+template <class Overlap>
+static int sample_nodes_device(Ctx& c, const pumpb::Scenario& s, const HostWorld& hw, const DevWorld& dwld,
+                               DevGraph& G, Overlap&& overlap) {
   const int dw = s.workspace_dim();
   const int64_t need_total = s.samples;
   const int64_t rows_cap = 1 + need_total + 1;
@@ -763,6 +788,7 @@ static void sample_nodes_device(Ctx& c, const pumpb::Scenario& s, const HostWorl
     wd.bhi[k] = dwld.bhi[k];
   }
   int64_t got = 0;
+  int have_goal = 0;
   uint64_t idx0 = 1;
   int64_t M = need_total + need_total / 2 + 256;
   DBuf& gflag = c.buf("s_goal_flag", 256);
@@ -786,21 +812,17 @@ static void sample_nodes_device(Ctx& c, const pumpb::Scenario& s, const HostWorl
                                                           gflag.as<int>());
     ++c.launches;
     PUMP_CUDA(cudaGetLastError());
+    if (idx0 == 1) overlap();
     int64_t acc = 0;
     c.d2h(&acc, rank.as<int64_t>() + M, 8);
+    c.d2h(&have_goal, gflag.p, 4);
     c.sync();
     got += std::min(acc, need_total - got);
     idx0 += static_cast<uint64_t>(M);
     M = 2 * (need_total - got) + 256;
   }
-  int have_goal = 0;
+  if (idx0 == 1) overlap();  // (no sample needed)
   const int64_t n = 1 + need_total;
-  pos.resize(n * dw);
-  vel.resize(n * dw);
-  c.d2h(&have_goal, gflag.p, 4);
-  c.d2h(pos.data(), G.pos.p, n * dw * 8);
-  c.d2h(vel.data(), G.vel.p, n * dw * 8);
-  c.sync();
   if (!have_goal) {  // goal centre, else a goal Halton sample (sample.hpp:63-88), on the host
     double p[6], v[6];
     for (int k = 0; k < dw; ++k) {
@@ -825,11 +847,11 @@ static void sample_nodes_device(Ctx& c, const pumpb::Scenario& s, const HostWorl
       }
     }
     if (!placed) throw std::runtime_error("sample_free: goal region appears entirely in collision");
-    pos.insert(pos.end(), p, p + dw);
-    vel.insert(vel.end(), v, v + dw);
     c.h2d(G.pos.as<double>() + n * dw, p, dw * 8);
     c.h2d(G.vel.as<double>() + n * dw, v, dw * 8);
+    return static_cast<int>(n + 1);
   }
+  return static_cast<int>(n);
 }
 
 static HostWorld host_world(const pumpb::World& sw) {
@@ -1044,8 +1066,6 @@ static void run_pump_device(Ctx& c, const pumpb::Scenario& s, const DevGraph* pr
   auto secs = [](clk::time_point a, clk::time_point b) { return std::chrono::duration<double>(b - a).count(); };
   const int dw = s.workspace_dim();
   R.dw = dw;
-  pumpb::ModelBundle mb = s.models();
-  HostLoop L = loop_of(mb.cl);
   const double eps_cc = s.effective_eps_cc();
   const double r_n = s.effective_r_n();
   HostWorld hw = host_world(s.workspace);
@@ -1055,11 +1075,19 @@ static void run_pump_device(Ctx& c, const pumpb::Scenario& s, const DevGraph* pr
   DevWorld dwld = upload_world(c, &pw, "run_ws_");
 
   auto t0 = clk::now();
-  // The particle bank (presample_bank, lti.hpp:257-292) depends only on the
-  // model and seed: it runs on the side stream while the graph is built (a
-  // few latency-bound warps next to the FP64-bound graph kernels); explore
-  // waits for it through the join event.
-  {
+  // The models (host: discretisation, Riccati, closed loop) and the particle
+  // bank (presample_bank, lti.hpp:257-292) depend only on the model and seed:
+  // the models are synthesised while the sampler's first batch runs, and the
+  // bank runs on the side stream while the graph is built (a few
+  // latency-bound warps next to the FP64-bound graph kernels); explore waits
+  // for it through the join event.
+  HostLoop L;
+  auto models_and_bank = [&]() {
+    const auto tm0 = clk::now();
+    pumpb::ModelBundle mb = s.models();
+    L = loop_of(mb.cl);
+    if (std::getenv("PUMP_DEBUG_TIMING"))
+      std::fprintf(stderr, "[pump g] %-24s %8.3f ms\n", "models", 1e3 * secs(tm0, clk::now()));
     const size_t bytes = static_cast<size_t>(s.bank_horizon + 1) * s.particles * dw * sizeof(double);
     c.bank.ensure(bytes);
     DBuf& scr = c.buf("bank_scratch", bank_scratch_bytes(L, s.particles, s.bank_horizon));
@@ -1070,18 +1098,36 @@ static void run_pump_device(Ctx& c, const pumpb::Scenario& s, const DevGraph* pr
     c.bank_n = s.particles;
     c.bank_horizon = s.bank_horizon;
     c.bank_dw = dw;
-  }
+  };
   if (!c.run_graph) c.run_graph = std::make_shared<DevGraph>();
   if (!c.run_explore) c.run_explore = std::make_shared<DevExplore>();
   DevGraph& local = *c.run_graph;
   const DevGraph* graph = prebuilt;
   if (!graph) {
-    std::vector<double> pos, vel;
-    sample_nodes_device(c, s, hw, dwld, local, pos, vel);
+    const int n = sample_nodes_device(c, s, hw, dwld, local, models_and_bank);
     if (std::getenv("PUMP_DEBUG_TIMING"))
       std::fprintf(stderr, "[pump g] %-24s %8.3f ms (from solve start)\n", "sample_nodes",
                    1e3 * secs(t0, clk::now()));
-    const int n = static_cast<int>(pos.size()) / dw;
+    // goal nodes (graph_goal_nodes) on the device, read back after the graph
+    // build's own synchronisations: no host copy of the sampled nodes
+    DBuf& gfl = c.buf("r_goal_flag", al(n + 8));
+    DBuf& gof = c.buf("r_goal_off", al((n + 2) * 8));
+    DBuf& gls = c.buf("r_goal_list", al((n + 2) * 4));
+    DBuf& gtmp = c.buf("r_goal_tmp", scan_temp_bytes(n + 16));
+    {
+      SampleBox GB{};
+      for (int k = 0; k < dw; ++k) {
+        GB.glo[k] = s.goal.lo[k];
+        GB.ghi[k] = s.goal.hi[k];
+      }
+      GB.gms = s.goal_max_speed;
+      k_goal_flags<<<grid_for(n, 256), 256, 0, c.stream>>>(n, dw, local.pos.as<double>(), local.vel.as<double>(), GB,
+                                                          gfl.as<uint8_t>());
+      exclusive_scan<uint8_t>(gfl.as<uint8_t>(), gof.as<int64_t>(), n, gtmp.p, c.stream, &c.launches);
+      k_goal_scatter<<<grid_for(n + 1, 256), 256, 0, c.stream>>>(n, gfl.as<uint8_t>(), gof.as<int64_t>(),
+                                                                gls.as<int32_t>());
+      c.launches += 2;
+    }
     // multi-GPU: each rank builds the rows of its slice; the slices are
     // gathered over NVLink into the full graph on every rank
     int64_t rlo = 0, rhi = n;
@@ -1089,11 +1135,19 @@ static void run_pump_device(Ctx& c, const pumpb::Scenario& s, const DevGraph* pr
     build_graph_device(local, c, n, dw, nullptr, nullptr,  // the sampler left the nodes in local.pos / vel
                        dwld, r_n, s.dt, eps_cc, s.effective_tau_max(), scan_ratio(s.effective_tau_max()),
                        static_cast<int>(rlo), static_cast<int>(rhi), c.world > 1);
-    pump_goal g{s.goal.lo.data(), s.goal.hi.data(), s.goal_max_speed};
-    local.h_pos = pos;
-    local.h_vel = vel;
-    graph_goal_nodes(local, pos.data(), vel.data(), &g);
+    int32_t ng = 0;
+    c.d2h(&ng, gls.p, 4);
+    c.sync();
+    local.goal_nodes.resize(ng);
+    if (ng > 0) {
+      c.d2h(local.goal_nodes.data(), gls.as<int32_t>() + 1, static_cast<size_t>(ng) * 4);
+      c.sync();
+    }
+    local.h_pos.clear();  // (run_pump keeps its nodes on the device)
+    local.h_vel.clear();
     graph = &local;
+  } else {
+    models_and_bank();
   }
   auto t1 = clk::now();
   R.s.build_graph_seconds = secs(t0, t1);
