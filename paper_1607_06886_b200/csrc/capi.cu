@@ -5,6 +5,7 @@
 #include <string>
 
 #include "ctx.h"
+#include "host/scenario_fast.hpp"
 #include "guard.h"
 
 static_assert(static_cast<int>(pumpg::F_COUNT) == PUMP_FAM_COUNT && static_cast<int>(pumpg::F_PAIR) == PUMP_FAM_PAIR,
@@ -117,7 +118,9 @@ int pump_scenario_parse(const char* json_text, pump_scenario** out) {
   return guard([&] {
     auto* s = new pump_scenario;
     try {
-      s->s = pumpb::parse_scenario_text(json_text ? json_text : "");
+      const char* t = json_text ? json_text : "";
+      auto fast = pumpb::parse_scenario_fast(t);  // the strict fast reader, else the nlohmann path (same errors)
+      s->s = fast ? std::move(*fast) : pumpb::parse_scenario_text(t);
     } catch (...) {
       delete s;
       throw;
