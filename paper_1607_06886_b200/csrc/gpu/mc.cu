@@ -934,7 +934,17 @@ static bool ensure_table(McTable& tab, const HostLoop& HL, int64_t r0, int64_t r
       dispatch_dw(dw, [&]<int DW>() {
         if (steps > 0) {
           const int64_t items = static_cast<int64_t>(steps) * n * DW;
-          k_mcnoise_sep<DW><<<grid_for(items, 256), 256, 0, st>>>(B, r0, n, seed, tn0, steps, tab.nz.as<double>());
+          // 60 KB of (unused) dynamic shared memory caps the kernel at 3 blocks
+          // per SM, so the cooperative round kernel (24k registers, 24 KB) or an
+          // expand block always fits next to it during explore
+          constexpr int kNoiseSmem = 60 * 1024;
+          static bool attr = false;
+          if (!attr) {
+            PUMP_CUDA(cudaFuncSetAttribute(k_mcnoise_sep<DW>, cudaFuncAttributeMaxDynamicSharedMemorySize, kNoiseSmem));
+            attr = true;
+          }
+          k_mcnoise_sep<DW><<<grid_for(items, 256), 256, kNoiseSmem, st>>>(B, r0, n, seed, tn0, steps,
+                                                                           tab.nz.as<double>());
           ++*launches;
         }
         k_mcrec_sep<DW><<<grid_for(n * DW, 128), 128, 0, st>>>(B, r0, n, seed, tc0, tc1, tn0, tab.nz.as<double>(),
