@@ -67,6 +67,12 @@ struct ExpandArgs {
   double* c_cp;
   uint64_t* c_mask;
   ExploreStatus* st;
+  // a kept candidate's slot among its node's newcomers, the per-node newcomer
+  // counts and the touched-node list (before: assigned in commit_one; here the
+  // round tail's commit scan and node-size scan need not wait for each other)
+  int32_t* new_cnt;
+  int32_t* new_slot;  // per task
+  int32_t* touched;
 };
 
 // The particle test of one half-space (cp.hpp:197-201): s = 0 + a0 p0 + ...
@@ -305,18 +311,25 @@ __device__ __forceinline__ void expand_task(const ExpandArgs& a, int64_t task, i
     }
   }
   }  // slab
-  if (lane == 0) {
+  if (lane == 0 && a.count_hs) {
+    // the roofline's work counts: only in the profiled pass (a same-address
+    // atomic per task costs ~0.2 ms per solve)
     atomicAdd(reinterpret_cast<unsigned long long*>(&a.st->hs_tests), static_cast<unsigned long long>(tests));
-    // the HBM-byte model's half-space count: only in the profiled pass (a
-    // second same-address atomic per task costs ~0.2 ms per solve)
-    if (a.count_hs) atomicAdd(reinterpret_cast<unsigned long long*>(&a.st->hs_read), static_cast<unsigned long long>(hs_sum));
+    atomicAdd(reinterpret_cast<unsigned long long*>(&a.st->hs_read), static_cast<unsigned long long>(hs_sum));
   }
   if (lane == 0) {
     const double cp = 1.0 - static_cast<double>(pop) / a.N;  // ParticleMask::cp (cp.hpp:42)
     a.c_cp[task] = cp;
     const bool keep = cp < a.alpha_max;
     a.keep[task] = keep ? 1 : 0;
-    if (!keep) atomicAdd(reinterpret_cast<unsigned long long*>(&a.st->disc_cp), 1ull);
+    if (!keep) {
+      atomicAdd(reinterpret_cast<unsigned long long*>(&a.st->disc_cp), 1ull);
+    } else {
+      const int hv = a.e_to[e];
+      const int slot = atomicAdd(&a.new_cnt[hv], 1);
+      a.new_slot[task] = slot;
+      if (slot == 0) a.touched[atomicAdd(reinterpret_cast<unsigned long long*>(&a.st->touched), 1ull)] = hv;
+    }
   }
 }
 
@@ -378,9 +391,6 @@ __device__ __forceinline__ void commit_one(const CommitArgs& a, int64_t t, int64
       atomicMin(&a.st->best_goal_bits, __double_as_longlong(c));
     atomicMax(&a.st->max_goal_tend, static_cast<long long>(a.c_tend[t]));
   }
-  const int slot = atomicAdd(&a.new_cnt[hv], 1);
-  a.new_slot[r] = slot;
-  if (slot == 0) a.touched[atomicAdd(reinterpret_cast<unsigned long long*>(&a.st->touched), 1ull)] = hv;
 }
 
 __global__ void k_commit(const CommitArgs a) {
@@ -414,13 +424,14 @@ __global__ void k_relayout(int n, const int64_t* old_off, const int32_t* mem_cnt
   for (int k = lane; k < m; k += 32) new_ids[b + k] = old_ids[a + k];
 }
 
-__global__ void k_place_new(const int64_t* d_K, const ExploreStatus* st, const int32_t* head, const int64_t* new_off,
-                            const int32_t* mem_cnt, const int32_t* new_slot, int32_t* new_ids) {
-  const int64_t r = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (r >= *d_K) return;
-  const int64_t id = st->n_plans + r;
-  const int hv = head[id];
-  new_ids[new_off[hv] + mem_cnt[hv] + new_slot[r]] = static_cast<int32_t>(id);
+__global__ void k_place_new(const int64_t* d_T, const ExploreStatus* st, const uint8_t* keep, const int64_t* rank,
+                            const int32_t* c_head, const int64_t* new_off, const int32_t* mem_cnt,
+                            const int32_t* new_slot, int32_t* new_ids) {
+  const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (t >= *d_T || !keep[t]) return;
+  const int64_t id = st->n_plans + rank[t];
+  const int hv = c_head[t];
+  new_ids[new_off[hv] + mem_cnt[hv] + new_slot[t]] = static_cast<int32_t>(id);
 }
 
 // RemoveDominated, both directions, for one touched node per CTA.
@@ -1084,12 +1095,20 @@ __global__ void __launch_bounds__(kCoopBlock, 2) k_round_tail(const CoopArgs A) 
   const uint8_t* keep = A.cm.keep;
   unsigned ep = A.epoch * 8u;
   int64_t* rank = const_cast<int64_t*>(A.cm.rank);
+  // and, in the same phase (expand already counted each node's newcomers),
+  // the member relayout's new offsets: the second scan keeps its look-back
+  // words in the upper half of scan_status (a block's entry for one scan may
+  // still be polled while it posts the other)
   coop_scan(
       T, [&](int64_t i, int) -> int64_t { return keep[i]; },
       [&](int64_t i, int64_t ex, int64_t v) {
         if (v) commit_one(A.cm, i, ex);
       },
       rank, A.scan_status, ep++, red, &s_pre);
+  const int n = A.n;
+  coop_scan(
+      n, [&](int64_t v, int) -> int64_t { return A.mem_cnt[v] + A.new_cnt[v]; }, [](int64_t, int64_t, int64_t) {},
+      A.off2, A.scan_status + nb + 2, ep++, red, &s_pre);
   grid_sync(A.bar);
   const int64_t K = rank[T];
   if (gtid == 0) {
@@ -1098,12 +1117,6 @@ __global__ void __launch_bounds__(kCoopBlock, 2) k_round_tail(const CoopArgs A) 
     S->min_bucket = LLONG_MAX;
   }
   STAMP();
-  // member relayout: new offsets, old members, newcomers at their slots
-  const int n = A.n;
-  coop_scan(
-      n, [&](int64_t v, int) -> int64_t { return A.mem_cnt[v] + A.new_cnt[v]; }, [](int64_t, int64_t, int64_t) {},
-      A.off2, A.scan_status, ep++, red, &s_pre);
-  grid_sync(A.bar);
   STAMP();
   // a warp takes 32 consecutive nodes: each lane loads its node's segment
   // (one round trip for all 32) and copies a short segment itself; segments of
@@ -1127,10 +1140,10 @@ __global__ void __launch_bounds__(kCoopBlock, 2) k_round_tail(const CoopArgs A) 
       for (int k = lane; k < mb; k += 32) A.new_ids[bb + k] = A.old_ids[ab + k];
     }
   }
-  for (int64_t r = gtid; r < K; r += gthreads) {
-    const int64_t id = P0 + r;
-    const int hv = A.ex.head[id];
-    A.new_ids[A.off2[hv] + A.mem_cnt[hv] + A.new_slot[r]] = static_cast<int32_t>(id);
+  for (int64_t t = gtid; t < T; t += gthreads) {
+    if (!keep[t]) continue;
+    const int hv = A.cm.c_head[t];
+    A.new_ids[A.off2[hv] + A.mem_cnt[hv] + A.new_slot[t]] = static_cast<int32_t>(P0 + rank[t]);
   }
   grid_sync(A.bar);
   STAMP();
@@ -1483,8 +1496,8 @@ void run_explore_device(DevExplore& X, Ctx& c, const DevGraph& G, const ExploreA
   }
   const bool coop_ok = coop_blocks > 0;
   if (coop_ok) {  // look-back status words start untagged
-    DBuf& scan_st = c.buf("x_coop_scan_status", al((coop_blocks + 2) * 8));
-    PUMP_CUDA(cudaMemsetAsync(scan_st.p, 0, (coop_blocks + 2) * 8, st));
+    DBuf& scan_st = c.buf("x_coop_scan_status", al((2 * coop_blocks + 4) * 8));
+    PUMP_CUDA(cudaMemsetAsync(scan_st.p, 0, (2 * coop_blocks + 4) * 8, st));
   }
   // Pipelined rounds: with the cooperative path and no round hook, batches of
   // kBatch rounds are enqueued behind device-side gates (k_round_gate) and the
@@ -1568,7 +1581,7 @@ void run_explore_device(DevExplore& X, Ctx& c, const DevGraph& G, const ExploreA
       DBuf& stay_pos = c.buf("x_stay_pos", al((pool_ub + 2) * 8));
       DBuf& msc = c.buf("x_coop_counts", al(static_cast<size_t>(kCoopKeys) * coop_blocks * 4));
       DBuf& mso = c.buf("x_coop_offs", al((static_cast<size_t>(kCoopKeys) * coop_blocks + 2) * 8));
-      DBuf& scan_st = c.buf("x_coop_scan_status", al((coop_blocks + 2) * 8));
+      DBuf& scan_st = c.buf("x_coop_scan_status", al((2 * coop_blocks + 4) * 8));
       DBuf& bar = c.buf("x_coop_bar", 256);
       DBuf& old_ids = X.mem_flip ? X.mem_b : X.mem_a;
       DBuf& new_ids = X.mem_flip ? X.mem_a : X.mem_b;
@@ -1584,7 +1597,8 @@ void run_explore_device(DevExplore& X, Ctx& c, const DevGraph& G, const ExploreA
                         c.bank_horizon, W, count_hs,
                         prm.alpha_max, X.cand_keep.as<uint8_t>(), X.cand_head.as<int32_t>(),
                         X.cand_src.as<int32_t>(), X.cand_tend.as<int32_t>(), X.cand_cost.as<double>(),
-                        X.cand_cp.as<double>(), X.cand_mask.as<uint64_t>(), S};
+                        X.cand_cp.as<double>(), X.cand_mask.as<uint64_t>(), S,
+                        X.new_cnt.as<int32_t>(), X.new_slot.as<int32_t>(), X.touched.as<int32_t>()};
       A.cm = CommitArgs{d_T, X.cand_keep.as<uint8_t>(), X.cand_rank.as<int64_t>(), X.cand_head.as<int32_t>(),
                         X.cand_src.as<int32_t>(), X.cand_tend.as<int32_t>(), X.cand_cost.as<double>(),
                         X.cand_cp.as<double>(), X.cand_mask.as<uint64_t>(), W, width, prm.alpha_min,
@@ -1685,7 +1699,8 @@ void run_explore_device(DevExplore& X, Ctx& c, const DevGraph& G, const ExploreA
                     box.as<double>(), N,
                       c.bank_horizon, W, count_hs, prm.alpha_max, X.cand_keep.as<uint8_t>(), X.cand_head.as<int32_t>(),
                       X.cand_src.as<int32_t>(), X.cand_tend.as<int32_t>(), X.cand_cost.as<double>(),
-                      X.cand_cp.as<double>(), X.cand_mask.as<uint64_t>(), S};
+                      X.cand_cp.as<double>(), X.cand_mask.as<uint64_t>(), S,
+                        X.new_cnt.as<int32_t>(), X.new_slot.as<int32_t>(), X.touched.as<int32_t>()};
         const unsigned grid = grid_for(T * 32, 256);
         KScope ks(st, F_EXPAND);
         dispatch_dw(G.dw, [&]<int DW>() {
@@ -1726,7 +1741,8 @@ void run_explore_device(DevExplore& X, Ctx& c, const DevGraph& G, const ExploreA
           new_ids.as<int32_t>());
       c.launches += 2;
       if (T > 0) {
-        k_place_new<<<grid_for(T, 256), 256, 0, st>>>(d_K, S, X.head.as<int32_t>(), off2.as<int64_t>(),
+        k_place_new<<<grid_for(T, 256), 256, 0, st>>>(d_T, S, X.cand_keep.as<uint8_t>(), X.cand_rank.as<int64_t>(),
+                                                        X.cand_head.as<int32_t>(), off2.as<int64_t>(),
                                                         X.mem_cnt.as<int32_t>(), X.new_slot.as<int32_t>(),
                                                         new_ids.as<int32_t>());
         const unsigned gd = static_cast<unsigned>(std::min<int64_t>(std::max<int64_t>(T, 1), 148 * 16));
