@@ -938,10 +938,12 @@ static bool ensure_table(McTable& tab, const HostLoop& HL, int64_t r0, int64_t r
           // per SM, so the cooperative round kernel (24k registers, 24 KB) or an
           // expand block always fits next to it during explore
           constexpr int kNoiseSmem = 60 * 1024;
-          static bool attr = false;
-          if (!attr) {
+          static bool attr[64] = {};  // per device (the attribute is set in each device's context)
+          int dev = 0;
+          PUMP_CUDA(cudaGetDevice(&dev));
+          if (dev < 0 || dev >= 64 || !attr[dev]) {
             PUMP_CUDA(cudaFuncSetAttribute(k_mcnoise_sep<DW>, cudaFuncAttributeMaxDynamicSharedMemorySize, kNoiseSmem));
-            attr = true;
+            if (dev >= 0 && dev < 64) attr[dev] = true;
           }
           k_mcnoise_sep<DW><<<grid_for(items, 256), 256, kNoiseSmem, st>>>(B, r0, n, seed, tn0, steps,
                                                                            tab.nz.as<double>());
