@@ -283,9 +283,7 @@ struct SausTab {
 struct CellGrid {
   double lo[3];
   double inv_h;
-  double R2;
   int dims[3];
-  int kr;
 };
 
 __device__ __forceinline__ unsigned long long ord_of(double x) {
@@ -1090,23 +1088,6 @@ void build_graph_device(DevGraph& G, Ctx& c, int n, int dw, const double* h_pos,
     }
     const double V = std::sqrt(dbl_of(hs[6])) * (1.0 + 1e-12);
     const double thr = r_n * (1.0 + 1e-6);
-    // R: on each interval [tl, th] of a geometric cover of (0, thr],
-    // c >= tl + 12 (d - V th)^2 / th^3, which exceeds thr once
-    // d >= V th + sqrt((thr - tl) th^3 / 12); the head (0, tk] needs
-    // d >= V tk + sqrt(thr tk^3 / 12).  R is the largest requirement.
-    double R = 0.0;
-    {
-      constexpr int kK = 4096;
-      const double rho = std::pow(1e6, 1.0 / kK);
-      double th = thr;
-      for (int i = 0; i < kK; ++i) {
-        const double tl = th / rho;
-        R = std::max(R, V * th + std::sqrt((thr - tl) * th * th * th / 12.0));
-        th = tl;
-      }
-      R = std::max(R, V * th + std::sqrt(thr * th * th * th / 12.0));
-      R *= 1.0 + 1e-9;
-    }
     // velocity-aware reach intervals (SausTab, k_pair_filter_grid)
     for (int i = 0; i < kSaus; ++i) {
       sz.tl[i] = i == 0 ? 0.0 : i == 1 ? thr / 64 : thr * (i - 1) / 32;
@@ -1122,7 +1103,7 @@ void build_graph_device(DevGraph& G, Ctx& c, int n, int dw, const double* h_pos,
     // 2249 with the position-only reach), grown until a row's cell range fits
     // kCellMaxList and the grid 2^22 cells
     double h = sz.ext / 3.5;
-    bool finite = std::isfinite(R) && R > 0 && std::isfinite(sz.ext);
+    bool finite = std::isfinite(sz.ext) && sz.ext > 0;
     for (int k = 0; k < dw; ++k) finite = finite && std::isfinite(lo[k]) && std::isfinite(hi[k]);
     if (finite) {
       for (;;) {
@@ -1132,18 +1113,14 @@ void build_graph_device(DevGraph& G, Ctx& c, int n, int dw, const double* h_pos,
           cells *= cg.dims[k];
           range *= std::min<int64_t>(cg.dims[k], static_cast<int64_t>(std::floor(2.0 * sz.ext / h)) + 2);
         }
-        cg.kr = 0;
         if (cells <= (int64_t(1) << 22) && range <= kCellMaxList) break;
         h *= 1.03;
       }
       for (int k = 0; k < dw; ++k) cg.lo[k] = lo[k];
       cg.inv_h = 1.0 / h;
-      cg.R2 = R * R * (1.0 + 1e-9);
     } else {
       cg.dims[0] = cg.dims[1] = cg.dims[2] = 1;  // one cell: every node is visited
       cg.inv_h = 0.0;
-      cg.kr = 0;
-      cg.R2 = INFINITY;
       for (int i = 0; i < kSaus; ++i) sz.rho2[i] = INFINITY;
       for (int q = 0; q < kSausGroups; ++q) sz.grho2[q] = INFINITY;
       sz.ext = INFINITY;

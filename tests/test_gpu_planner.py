@@ -92,6 +92,38 @@ def test_build_graph_many_obstacles(oracle_lib, gpu_ctx, n_boxes, samples):
     assert_graph_equal(gg, og)
 
 
+@pytest.mark.parametrize("n_boxes,samples", [(40, 600), (300, 500)])
+def test_build_graph_2d_many_boxes(oracle_lib, gpu_ctx, n_boxes, samples):
+    """2-D worlds above 16 boxes: the spatially ordered region pass and its per-warp distance bounds for dw = 2
+    (k_wp_prep / k_regions_once<2, 8> and, above 256 boxes, <2, 128>), small boxes scattered over the 2-D indoor
+    world."""
+    from paper_1607_06886_b200 import api
+
+    j = json.loads(scenario_text("indoor"))
+    rng = np.random.default_rng(7)
+    obs = list(j["workspace"]["obstacles"])
+    start, glo, ghi = np.array(j["start"]["position"]), np.array(j["goal"]["lo"]), np.array(j["goal"]["hi"])
+    while len(obs) < n_boxes:
+        c = rng.uniform([0.5, 0.5], [19.5, 11.5])
+        e = rng.uniform(0.1, 0.4, size=2)
+        lo, hi = c - e / 2, c + e / 2
+        if np.all(lo - 0.8 <= start) and np.all(start <= hi + 0.8):
+            continue
+        if np.all(lo - 0.8 <= ghi) and np.all(glo <= hi + 0.8):
+            continue
+        obs.append({"lo": [round(float(x), 6) for x in lo], "hi": [round(float(x), 6) for x in hi]})
+    j["workspace"]["obstacles"] = obs
+    j["samples"] = samples
+    txt = json.dumps(j)
+    _, sc = oracle_lib.scenario_models(txt)
+    pos, vel = oracle_lib.scenario_nodes(txt)
+    args = (ws_of(j), goal_of(j), sc["r_n"], sc["dt"], sc["eps_cc"], sc["tau_max"])
+    og = oracle_lib.build_graph(pos, vel, *args, workers=WORKERS).export()
+    gg = api.build_graph(pos, vel, *args, ctx=gpu_ctx).export()
+    assert og["n_edges"] > 0 and og["n_halfspaces"] > 0
+    assert_graph_equal(gg, og)
+
+
 def test_build_graph_duplicate_boxes(oracle_lib, gpu_ctx):
     """Grouped regions with distance ties: every box listed twice (equal squared distances, the lower
     workspace index must win as in nearest_obstacle_vector's strict first minimum, geom.hpp:128-141) and
