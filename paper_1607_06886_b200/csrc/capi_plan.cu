@@ -173,42 +173,17 @@ __global__ void k_smooth_blend(int n_probe, int n_wp, const double* __restrict__
   }
 }
 
-template <int DW>
-__global__ void k_smooth_check(WorldD w, int n_probe, int n_wp, const double* __restrict__ pt,
-                               const double* __restrict__ y, const double* __restrict__ yv, double eps_cc,
-                               int32_t* __restrict__ free_flag) {
-  const int64_t x = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (x >= static_cast<int64_t>(n_probe) * n_wp) return;
-  const int64_t pr = x / n_wp;
-  const int j = static_cast<int>(x % n_wp);
-  if (free_flag[pr] == 0) return;  // already colliding (or a chained step that does not run)
-  bool ok = point_free<DW>(w, y + x * DW);
-  if (ok && j + 1 < n_wp) {
-    const double h = pt[j + 1] - pt[j];
-    if (h > 0) {
-      MotionD<DW> m;
-#pragma unroll
-      for (int k = 0; k < DW; ++k) {
-        m.p0[k] = y[x * DW + k];
-        m.v0[k] = yv[x * DW + k];
-        m.p1[k] = y[(x + 1) * DW + k];
-        m.v1[k] = yv[(x + 1) * DW + k];
-      }
-      m.tau = h;
-      coeffs_dev<DW>(m.p0, m.v0, m.p1, m.v1, m.tau, m.a, m.j);
-      ok = !motion_collides<DW>(m, w, eps_cc);
-    }
-  }
-  if (!ok) free_flag[pr] = 0;
-}
-
-// The same check with a warp per (probe, waypoint): the waypoint's point_free
+// The nominal check of the blended probes (point_free of every waypoint,
+// motion_collides of every segment), a warp per (probe, waypoint): the waypoint's point_free
 // and the segment's obstacle cull (motion_cull: the boxes not separated from
 // the motion's widened bounding box) run with the lanes over the boxes, then
 // every lane runs motion_collides on the warp's bitmask (identical data, no
 // divergence).  Same tests, same verdicts; a warp instead of a thread because
-// a batch holds only ~4 x 260 items.  Worlds of at most 64 kCullWords boxes.
-template <int DW>
+// a batch holds only ~4 x 260 items.  LIST = 0: worlds of at most 64
+// kCullWords boxes (bitmask); LIST = kCullList: larger worlds, the candidates
+// listed in ascending order by ballot, all boxes tested past LIST of them
+// (motion_cull's list mode).
+template <int DW, int LIST>
 __global__ void __launch_bounds__(128) k_smooth_check_warp(WorldD w, int n_probe, int n_wp,
                                                            const double* __restrict__ pt,
                                                            const double* __restrict__ y,
@@ -241,14 +216,39 @@ __global__ void __launch_bounds__(128) k_smooth_check_warp(WorldD w, int n_probe
       m.tau = h;
       coeffs_dev<DW>(m.p0, m.v0, m.p1, m.v1, m.tau, m.a, m.j);
       // motion_cull with the lanes over the boxes (the same separation test)
-      MotionCull c;
+      MotionCullT<LIST> c;
       double bl[DW], bh[DW];
       motion_bbox<DW>(m, bl, bh);
       c.inside = true;
 #pragma unroll
       for (int k = 0; k < DW; ++k) c.inside = c.inside && bl[k] > ws.blo[k] && bh[k] < ws.bhi[k];
-      c.nlist = -1;
       c.masked = true;
+      if constexpr (LIST > 0) {
+        for (int q = 0; q < kCullWords; ++q) c.cand[q] = 0;
+        c.nlist = 0;
+        c.any = false;
+        for (int o0 = 0; o0 < ws.n_obs && c.masked; o0 += 32) {
+          const int o = o0 + lane;
+          bool cand = false;
+          if (o < ws.n_obs) {
+            bool sep = false;
+#pragma unroll
+            for (int k = 0; k < DW; ++k) sep = sep || (bh[k] < ws.lo[o * DW + k]) || (bl[k] > ws.hi[o * DW + k]);
+            cand = !sep;
+          }
+          unsigned bal = __ballot_sync(0xffffffffu, cand);
+          if (bal) c.any = true;
+          for (; bal; bal &= bal - 1) {
+            if (c.nlist == LIST) {
+              c.masked = false;  // too many candidates: every box is tested
+              break;
+            }
+            c.list[c.nlist++] = static_cast<uint16_t>(o0 + __ffs(bal) - 1);
+          }
+        }
+        ok = !motion_collides<DW, LIST>(m, ws, eps_cc, &c);
+      } else {
+      c.nlist = -1;
       for (int q = 0; q < kCullWords; ++q) {
         uint64_t word = 0;
         for (int half = 0; half < 2; ++half) {
@@ -266,6 +266,7 @@ __global__ void __launch_bounds__(128) k_smooth_check_warp(WorldD w, int n_probe
       }
       c.any = (c.cand[0] | c.cand[1] | c.cand[2] | c.cand[3]) != 0;
       ok = !motion_collides<DW>(m, ws, eps_cc, &c);
+      }
     }
   }
   if (!ok && lane == 0) free_flag[pr] = 0;
@@ -998,19 +999,13 @@ static SmoothOut smooth_device(Ctx& c, const std::vector<HWp>& plan, double plan
             np, n_wp, &ch->s[q0], c.scratch["sm_plan"].as<double>(), c.scratch["sm_plan"].as<double>() + n_wp,
             c.scratch["sm_plan"].as<double>() + n_wp * (1 + dw), as_motion<DW>(o), d_y.as<double>(),
             d_yv.as<double>());
-        if (wd.n_obs <= 64 * kCullWords) {
-          const size_t sm = static_cast<size_t>(2 * wd.n_obs * DW) * 8 + 16;
-          if (sm > 48 * 1024)
-            PUMP_CUDA(cudaFuncSetAttribute(k_smooth_check_warp<DW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           static_cast<int>(sm)));
-          k_smooth_check_warp<DW><<<grid_for(it * 32, 128), 128, sm, c.stream>>>(
-              wd, np, n_wp, c.scratch["sm_plan"].as<double>(), d_y.as<double>(), d_yv.as<double>(), eps_cc,
-              &ch->live[q0]);
-        } else {
-          k_smooth_check<DW><<<grid_for(it, 128), 128, 0, c.stream>>>(
-              wd, np, n_wp, c.scratch["sm_plan"].as<double>(), d_y.as<double>(), d_yv.as<double>(), eps_cc,
-              &ch->live[q0]);
-        }
+        auto kern = wd.n_obs <= 64 * kCullWords ? k_smooth_check_warp<DW, 0> : k_smooth_check_warp<DW, kCullList>;
+        const size_t sm = static_cast<size_t>(2 * wd.n_obs * DW) * 8 + 16;
+        if (sm > 48 * 1024)
+          PUMP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm)));
+        kern<<<grid_for(it * 32, 128), 128, sm, c.stream>>>(wd, np, n_wp, c.scratch["sm_plan"].as<double>(),
+                                                            d_y.as<double>(), d_yv.as<double>(), eps_cc,
+                                                            &ch->live[q0]);
       });
       c.launches += 3;
       launch_mc(L, dwld, np, d_off.as<int64_t>(), d_y.as<double>(), n_wp, r0, r1, seed, eps_cc,

@@ -949,10 +949,9 @@ __device__ __forceinline__ int convex_region_scan(const WorldD& ws, const double
     }
   }
   uint32_t pruned[kW];
-#pragma unroll
-  for (int q = 0; q < kW; ++q) {
+  for (int q = 0; q < (ws.n_obs + 31) / 32; ++q) {  // (only the words in use)
     const int lo = 32 * q;
-    pruned[q] = ws.n_obs <= lo ? ~0u : (ws.n_obs >= lo + 32 ? 0u : ~((1u << (ws.n_obs - lo)) - 1u));
+    pruned[q] = ws.n_obs >= lo + 32 ? 0u : ~((1u << (ws.n_obs - lo)) - 1u);
   }
   int count = 0;
   while (best >= 0) {

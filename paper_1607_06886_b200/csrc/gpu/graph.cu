@@ -874,8 +874,11 @@ __global__ void k_wp_scatter(int64_t n_wp, const int32_t* __restrict__ key, cons
   perm[cell_off[c] + atomicAdd(cursor + c, 1)] = static_cast<int32_t>(x);
 }
 
+// blocks of 128 threads, 512 above 256 boxes (the staged boxes are shared by
+// more warps: forest1000 regions at 12 -> 32 resident warps per SM)
+__host__ __device__ constexpr int regions_block(int kw) { return kw >= 32 ? 512 : 128; }
 template <int DW, int KW>
-__global__ void __launch_bounds__(128) k_regions_once(GraphArgs g, WorldD w, int64_t n_wp, int64_t n_edges,
+__global__ void __launch_bounds__(regions_block(KW)) k_regions_once(GraphArgs g, WorldD w, int64_t n_wp, int64_t n_edges,
                                                       const int64_t* __restrict__ wp_off,
                                                       const int32_t* __restrict__ e_from,
                                                       const int32_t* __restrict__ e_to, const double* __restrict__ e_tau,
@@ -1423,13 +1426,15 @@ void build_graph_device(DevGraph& G, Ctx& c, int n, int dw, const double* h_pos,
         dispatch_dw(dw, [&]<int DW>() {
           auto kern = w.n_obs <= kOnceMaxObs ? k_regions_once<DW, 0>
                       : w.n_obs <= 256      ? k_regions_once<DW, 8>
+                      : w.n_obs <= 1024     ? k_regions_once<DW, 32>
                                             : k_regions_once<DW, 128>;
+          const int blk = w.n_obs <= 256 ? 128 : regions_block(w.n_obs <= 1024 ? 32 : 128);
           const size_t sm = wsmem + (w.n_obs <= kOnceMaxObs ? static_cast<size_t>(w.n_obs) * 128 * 8
-                                     : w.n_obs <= kLbsMaxObs ? static_cast<size_t>(w.n_obs) * 4 * 4  // lbs, 4 warps
+                                     : w.n_obs <= kLbsMaxObs ? static_cast<size_t>(w.n_obs) * (blk / 32) * 4  // lbs
                                                              : 0);
           if (sm > 48 * 1024)
             PUMP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-          kern<<<grid_for(NW, 128), 128, sm, st>>>(
+          kern<<<grid_for(NW, blk), blk, sm, st>>>(
               ga, wd, NW, E, G.wp_off.as<int64_t>(), G.e_from.as<int32_t>(), G.e_to.as<int32_t>(),
               G.e_tau.as<double>(), G.e_acc0.as<double>(), G.e_jerk.as<double>(), G.e_nsteps.as<int32_t>(),
               c.scratch["g_wp_edge"].as<int32_t>(), cap,

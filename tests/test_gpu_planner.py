@@ -289,6 +289,24 @@ def test_run_pump_matches_oracle(oracle_lib, gpu_ctx, name, samples, mc):
     assert_run_equal(got, ref)
 
 
+def test_run_pump_many_boxes(oracle_lib, gpu_ctx):
+    """More than 256 boxes: the list-mode motion cull in collide, the region scan above 256 boxes, and the
+    smoothing probes' nominal check with the list-mode warp cull (k_smooth_check_warp<DW, kCullList>)."""
+    import sys
+
+    from paper_1607_06886_b200 import api
+
+    sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "scenarios"))
+    import make_scenarios
+
+    j = make_scenarios.forest(n_boxes=300)
+    j.update({"samples": 5000, "mc_samples": 3000})  # (reaches the goal and smooths: s = 0.072)
+    txt = json.dumps(j)
+    got = api.run_pump(api.parse_scenario(txt), ctx=gpu_ctx)
+    ref = oracle_lib.run_pump(txt, workers=WORKERS)
+    assert_run_equal(got, ref)
+
+
 def test_run_pump_goal_fallback_sample(oracle_lib, gpu_ctx):
     """sample_free's goal fallback (sample.hpp:63-88): no Halton sample lands in the goal and its centre is blocked
     (the 10-box forest), so the first free goal Halton state is appended; searched on the device."""
