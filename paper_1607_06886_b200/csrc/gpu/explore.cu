@@ -1559,8 +1559,12 @@ void run_explore_device(DevExplore& X, Ctx& c, const DevGraph& G, const ExploreA
     DBuf& spos = c.buf("x_spos", al((T + 2) * 8));
     DBuf& stmp = c.buf("x_scan_tmp", scan_temp_bytes(std::max<int64_t>({T, n, X.cap}) + 16));
 
-    int64_t n_keys_r = 1 << 18;  // see k_select: distinct bucket keys this round
-    if (h.min_bucket != LLONG_MAX && h.i + 2 - h.min_bucket <= 512) n_keys_r = std::max<int64_t>(1, h.i + 2 - h.min_bucket);
+    // distinct bucket keys of the next selection (see k_select): <= i + 2 -
+    // min_bucket; with no open plan yet (the first round) the newcomers'
+    // minimum is unknown but >= 0 (buckets are clamped at 0), so i + 2 bounds it
+    int64_t n_keys_r = 1 << 18;
+    const long long mb = h.min_bucket == LLONG_MAX ? 0 : h.min_bucket;
+    if (h.i + 2 - mb <= 512) n_keys_r = std::max<int64_t>(1, h.i + 2 - mb);
     bool ran_coop = false;
     if (pipe || (coop_ok && T > 0 && n_keys_r <= kCoopKeys)) {
      ran_coop = true;
