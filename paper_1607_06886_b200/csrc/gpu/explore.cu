@@ -1375,6 +1375,51 @@ static T* ptr(DBuf& b) {
   return b.as<T>();
 }
 
+__global__ void k_explore_init(int n, int W, int N, int ng, const int32_t* __restrict__ goal_sorted,
+                               int64_t* __restrict__ mem_off, int32_t* __restrict__ mem_cnt, int32_t* __restrict__ new_cnt,
+                               uint8_t* __restrict__ is_goal, int32_t* head, int32_t* parent, double* cost, double* cp,
+                               int32_t* t_end, int32_t* bucket, uint64_t* mask, uint8_t* flags, int32_t* mem_a,
+                               int32_t* group, const int64_t* __restrict__ row_ptr, ExploreStatus h0,
+                               ExploreStatus* S, int64_t* d_scal, int64_t* task_off) {
+  const int v = blockIdx.x * blockDim.x + threadIdx.x;
+  if (v <= n) mem_off[v] = v == 0 ? 0 : 1;  // pareto[0] = {0}: node 0's segment holds one entry
+  if (v < n) {
+    mem_cnt[v] = v == 0 ? 1 : 0;
+    new_cnt[v] = 0;
+    int lo = 0, hi = ng;  // v in the ascending goal list?
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if (goal_sorted[mid] < v)
+        lo = mid + 1;
+      else
+        hi = mid;
+    }
+    is_goal[v] = (lo < ng && goal_sorted[lo] == v) ? 1 : 0;
+  }
+  if (v == 0) {
+    head[0] = 0;
+    parent[0] = -1;
+    cost[0] = 0.0;
+    cp[0] = 0.0;
+    t_end[0] = 0;
+    bucket[0] = 0;
+    for (int w = 0; w < W; ++w)
+      mask[w] = (w == W - 1 && N % 64) ? (1ull << (N % 64)) - 1 : ~0ull;
+    flags[0] = 0;
+    mem_a[0] = 0;
+    group[0] = 0;
+    const int64_t T0 = row_ptr[1] - row_ptr[0];
+    h0.T = T0;
+    *S = h0;
+    task_off[0] = 0;
+    task_off[1] = T0;
+    d_scal[0] = 0;
+    d_scal[1] = 0;
+    d_scal[2] = 1;
+    d_scal[3] = T0;
+  }
+}
+
 void run_explore_device(DevExplore& X, Ctx& c, const DevGraph& G, const ExploreArgs& prm) {
   if (!c.bank.p) throw std::invalid_argument("explore: no particle bank in this context");
   if (c.bank_dw != G.dw) throw std::invalid_argument("explore: bank / graph dimension mismatch");
@@ -1416,41 +1461,9 @@ void run_explore_device(DevExplore& X, Ctx& c, const DevGraph& G, const ExploreA
   X.touched.ensure(al(n * 4));
   DBuf& node_sz = c.buf("x_node_sz", al(n * 4));
   DBuf& off2 = c.buf("x_off2", al((n + 1) * 8));
-  PUMP_CUDA(cudaMemsetAsync(X.mem_cnt.p, 0, n * 4, st));
-  PUMP_CUDA(cudaMemsetAsync(X.new_cnt.p, 0, n * 4, st));
-  PUMP_CUDA(cudaMemsetAsync(X.mem_off.p, 0, (n + 1) * 8, st));
-  std::vector<uint8_t> goal(n, 0);
-  for (int v : G.goal_nodes) goal[v] = 1;
-  c.h2d(X.is_goal.p, goal.data(), n);
-
-  // root plan (planner.hpp:100-103)
-  {
-    const int32_t zero = 0, minus1 = -1;
-    const double dz = 0.0;
-    c.h2d(X.head.p, &zero, 4);
-    c.h2d(X.parent.p, &minus1, 4);
-    c.h2d(X.cost.p, &dz, 8);
-    c.h2d(X.cp.p, &dz, 8);
-    c.h2d(X.t_end.p, &zero, 4);
-    c.h2d(X.bucket.p, &zero, 4);
-    std::vector<uint64_t> full(W, ~0ull);
-    if (N % 64) full[W - 1] = (1ull << (N % 64)) - 1;
-    c.h2d(X.mask.p, full.data(), W * 8);
-    const uint8_t f0 = 0;
-    c.h2d(X.flags.p, &f0, 1);
-    // pareto[0] = {0}: member segment of node 0 starts at 0 with one entry
-    const int32_t one = 1;
-    c.h2d(X.mem_cnt.p, &one, 4);
-    std::vector<int64_t> off(n + 1, 1);
-    off[0] = 0;
-    c.h2d(X.mem_off.p, off.data(), (n + 1) * 8);
-    c.h2d(X.mem_a.p, &zero, 4);
-    X.mem_flip = false;
-    // group = [0]
-    X.group.ensure(al(64 * 4));
-    c.h2d(X.group.p, &zero, 4);
-  }
-  const bool root_goal = n > 0 && goal[0];
+  std::vector<int32_t> goal_sorted(G.goal_nodes);  // (an uploaded graph's list may come in any order)
+  std::sort(goal_sorted.begin(), goal_sorted.end());
+  const bool root_goal = n > 0 && !goal_sorted.empty() && goal_sorted[0] == 0;
   ExploreStatus h{};
   h.G = 1;
   h.n_plans = 1;
@@ -1461,23 +1474,27 @@ void run_explore_device(DevExplore& X, Ctx& c, const DevGraph& G, const ExploreA
   h.pool_n = 0;
   h.best_goal_bits = root_goal && 0.0 < prm.alpha_min ? 0ll : 0x7ff0000000000000ll;
   h.min_group_bits = 0;  // root cost 0
-  // task count of the first group
-  int64_t T0 = 0;
+  // the initial state in one kernel (root plan, planner.hpp:100-103; node 0's
+  // member segment {0}; is_goal; group [0]; the first round's task count)
+  X.group.ensure(al(64 * 4));
+  X.task_off.ensure(al(64 * 8));
+  X.mem_flip = false;
   {
-    std::vector<int64_t> rp(2);
-    c.d2h(rp.data(), G.row_ptr.p, 16);
-    c.sync();
-    T0 = rp[1] - rp[0];
+    const int ng = static_cast<int>(goal_sorted.size());
+    DBuf& gl = c.buf("x_goal_list", al((ng + 1) * 4));
+    if (ng) c.h2d(gl.p, goal_sorted.data(), ng * 4);
+    k_explore_init<<<grid_for(n + 1, 256), 256, 0, st>>>(
+        n, W, N, ng, gl.as<int32_t>(), X.mem_off.as<int64_t>(), X.mem_cnt.as<int32_t>(), X.new_cnt.as<int32_t>(),
+        X.is_goal.as<uint8_t>(), X.head.as<int32_t>(), X.parent.as<int32_t>(), X.cost.as<double>(),
+        X.cp.as<double>(), X.t_end.as<int32_t>(), X.bucket.as<int32_t>(), X.mask.as<uint64_t>(),
+        X.flags.as<uint8_t>(), X.mem_a.as<int32_t>(), X.group.as<int32_t>(), G.row_ptr.as<int64_t>(), h, S, d_scal,
+        X.task_off.as<int64_t>());
+    ++c.launches;
   }
+  int64_t T0 = 0;  // the host sizes the first round by it
+  c.d2h(&T0, d_scal + 3, 8);
+  c.sync();
   h.T = T0;
-  c.h2d(S, &h, sizeof(h));
-  {
-    const int64_t toff[2] = {0, T0};
-    X.task_off.ensure(al(64 * 8));
-    c.h2d(X.task_off.p, toff, 16);
-    const int64_t sc[4] = {0, 0, 1, T0};
-    c.h2d(d_scal, sc, 32);
-  }
   X.partial_plans = 0;
   X.rounds = 0;
   X.pool_flip = false;
