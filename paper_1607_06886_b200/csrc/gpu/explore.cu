@@ -17,6 +17,7 @@
 //                 min(i, nb-1), stably ordered by (bucket, id) (:248-261)
 //   k_group_post + scan      task offsets (degree prefix sum) of the group
 // The arena, member segments, pool and group stay resident in HBM.
+#include <algorithm>
 #include <climits>
 #include <cstdio>
 #include <cstdlib>
