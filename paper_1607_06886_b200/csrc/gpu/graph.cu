@@ -26,6 +26,7 @@
 namespace pumpg {
 
 constexpr int kRowBlock = 256;
+constexpr int kGridBlock = 128;  // k_pair_filter_grid: a block per row
 
 struct GraphArgs {
   int n;
@@ -390,7 +391,7 @@ __global__ void k_cell_scatter(int n, const double* __restrict__ pos, const doub
 // Pass 1 over the cells within R of the row's node; the per-pair decision and
 // the lane-refill walk are k_pair_filter_q's.
 template <int DW>
-__global__ void __launch_bounds__(kRowBlock) k_pair_filter_grid(
+__global__ void __launch_bounds__(kGridBlock) k_pair_filter_grid(
     GraphArgs g, const LbGrid lb, const CellGrid G, const SausTab SZ, int cap, int row0, int refill,
     const int32_t* __restrict__ ccnt, const int64_t* __restrict__ cstart,
     const unsigned long long* __restrict__ cbox, const int32_t* __restrict__ sidx, const double* __restrict__ spos,
@@ -398,7 +399,7 @@ __global__ void __launch_bounds__(kRowBlock) k_pair_filter_grid(
   __shared__ LbGrid sl;
   __shared__ int cl_start[kCellMaxList];
   __shared__ int cl_pref[kCellMaxList + 1];
-  __shared__ int wtot[kRowBlock / 32];
+  __shared__ int wtot[kGridBlock / 32];
   __shared__ int s_next, s_ncl;
   extern __shared__ uint32_t bits[];  // ceil(n / 32) words
   {
@@ -595,9 +596,9 @@ __global__ void __launch_bounds__(kRowBlock) k_pair_filter_grid(
     }
   }
   __syncthreads();
-  // ascending-u compaction of the bitmask, kRowBlock words per pass
+  // ascending-u compaction of the bitmask, kGridBlock words per pass
   int base_run = 0;
-  for (int w0 = 0; w0 < nw; w0 += kRowBlock) {
+  for (int w0 = 0; w0 < nw; w0 += kGridBlock) {
     const int x = w0 + threadIdx.x;
     const uint32_t wb = x < nw ? bits[x] : 0u;
     const int cnt = __popc(wb);
@@ -610,7 +611,7 @@ __global__ void __launch_bounds__(kRowBlock) k_pair_filter_grid(
     if (lane == 31) wtot[warp] = inc;
     __syncthreads();
     int off = base_run + inc - cnt, blk = 0;
-    for (int w = 0; w < kRowBlock / 32; ++w) {
+    for (int w = 0; w < kGridBlock / 32; ++w) {
       if (w < warp) off += wtot[w];
       blk += wtot[w];
     }
@@ -1167,7 +1168,7 @@ void build_graph_device(DevGraph& G, Ctx& c, int n, int dw, const double* h_pos,
           const int sm = static_cast<int>(bits_bytes);
           if (sm > 32 * 1024)
             PUMP_CUDA(cudaFuncSetAttribute(k_pair_filter_grid<DW>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
-          k_pair_filter_grid<DW><<<row_hi - row_lo, kRowBlock, sm, st>>>(
+          k_pair_filter_grid<DW><<<row_hi - row_lo, kGridBlock, sm, st>>>(
               ga, lbg, cg, sz, cap, row_lo, refill, c.scratch["g_ccnt"].as<int32_t>(), c.scratch["g_cstart"].as<int64_t>(),
               c.scratch["g_cbox"].as<unsigned long long>(), c.scratch["g_sidx"].as<int32_t>(),
               c.scratch["g_spos"].as<double>(), c.scratch["g_svel"].as<double>(), rcnt.as<int32_t>(),
