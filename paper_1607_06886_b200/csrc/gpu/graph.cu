@@ -1103,10 +1103,10 @@ void build_graph_device(DevGraph& G, Ctx& c, int n, int dw, const double* h_pos,
     }
     for (int q = 0; q < kSausGroups; ++q)
       for (int i = saus_g0(q); i < saus_g0(q + 1); ++i) sz.grho2[q] = std::max(sz.grho2[q], sz.rho2[i]);
-    // cells of ~ext / 3.5 (measured on the forest: 430 candidates per row vs
+    // cells of ~ext / 2.8 (A/B on the forest: 3.5 and 2.2 slower; ~500 candidates per row vs
     // 2249 with the position-only reach), grown until a row's cell range fits
     // kCellMaxList and the grid 2^22 cells
-    double h = sz.ext / 3.5;
+    double h = sz.ext / 2.8;
     bool finite = std::isfinite(sz.ext) && sz.ext > 0;
     for (int k = 0; k < dw; ++k) finite = finite && std::isfinite(lo[k]) && std::isfinite(hi[k]);
     if (finite) {
