@@ -23,6 +23,7 @@
 namespace pumpg {
 
 constexpr int kMcBlock = 128;
+constexpr int kMcTabBlock = 256;  // k_mc_tab: the staged span (nominal rows, boxes, step lists) shared by 8 warps
 
 template <int D, int DW>
 __global__ void __launch_bounds__(kMcBlock) k_mc(const LoopP<D, DW> L, WorldD w, const int64_t* __restrict__ traj_off,
@@ -664,7 +665,7 @@ __global__ void __launch_bounds__(128) k_mc_steps(WorldD w, const int64_t* __res
 }
 
 template <int DW, int kMcSub>  // kMcSub sub-chunks per block: a block spans kMcSpan steps
-__global__ void __launch_bounds__(kMcBlock) k_mc_tab(WorldD w, const int64_t* __restrict__ traj_off,
+__global__ void __launch_bounds__(kMcTabBlock) k_mc_tab(WorldD w, const int64_t* __restrict__ traj_off,
                                                      const double* __restrict__ ynom_all, int64_t r0, int64_t r1,
                                                      int64_t tab_r0, int64_t tab_n, const double* __restrict__ dy,
                                                      const unsigned long long* __restrict__ maxdev, double eps_cc,
@@ -1031,8 +1032,8 @@ void launch_mc(const HostLoop& HL, const DevWorld& w, int n_traj, const int64_t*
         if (smem > 48 * 1024)
           PUMP_CUDA(cudaFuncSetAttribute(k_mc_tab<DW, SUB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(smem)));
-        dim3 grid(grid_for(n, kMcBlock), n_traj, (max_points + span - 1) / span);
-        k_mc_tab<DW, SUB><<<grid, kMcBlock, smem, st>>>(wd, d_traj_off, d_ynom, r0, r1, table->r0,
+        dim3 grid(grid_for(n, kMcTabBlock), n_traj, (max_points + span - 1) / span);
+        k_mc_tab<DW, SUB><<<grid, kMcTabBlock, smem, st>>>(wd, d_traj_off, d_ynom, r0, r1, table->r0,
                                                         table->r1 - table->r0, table->dy.as<double>(),
                                                         table->maxdev.as<unsigned long long>(), eps_cc,
                                                         table->flags.as<uint8_t>(), d_live, max_points,
