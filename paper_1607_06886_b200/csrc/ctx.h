@@ -52,6 +52,7 @@ struct Ctx {
   McTable mc_table;
   // named scratch buffers
   std::map<std::string, DBuf> scratch;
+  double lbgrid_rn = -1.0;  // r_n of the interval table in scratch "g_lbgrid" (graph.cu)
   DBuf& buf(const std::string& name, size_t bytes) {
     DBuf& b = scratch[name];
     if (bytes > b.cap && std::getenv("PUMP_DEBUG_ALLOC")) std::fprintf(stderr, "[pump alloc] scratch %s\n", name.c_str());

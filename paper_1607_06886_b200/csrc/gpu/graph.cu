@@ -392,21 +392,19 @@ __global__ void k_cell_scatter(int n, const double* __restrict__ pos, const doub
 // the lane-refill walk are k_pair_filter_q's.
 template <int DW>
 __global__ void __launch_bounds__(kGridBlock) k_pair_filter_grid(
-    GraphArgs g, const LbGrid lb, const CellGrid G, const SausTab SZ, int cap, int row0, int refill,
+    GraphArgs g, const LbGrid* __restrict__ lbp, const CellGrid G, const SausTab SZ, int cap, int row0, int refill,
     const int32_t* __restrict__ ccnt, const int64_t* __restrict__ cstart,
     const unsigned long long* __restrict__ cbox, const int32_t* __restrict__ sidx, const double* __restrict__ spos,
     const double* __restrict__ svel, int32_t* __restrict__ row_cnt, int32_t* __restrict__ su, int use_global) {
-  __shared__ LbGrid sl;
+  // the interval table from global memory (L1-resident; staging its 6 KB
+  // into shared memory per row cost more than the walks' reads of it)
+  const LbGrid& sl = *lbp;
   __shared__ int cl_start[kCellMaxList];
   __shared__ int cl_pref[kCellMaxList + 1];
   __shared__ int wtot[kGridBlock / 32];
-  __shared__ int s_next, s_ncl;
+  __shared__ int s_next, s_ncl, s_nsurv;
+  __shared__ int s_surv[32];  // the first 32 survivors (a row has ~8): sorted by one warp
   extern __shared__ uint32_t bits[];  // ceil(n / 32) words
-  {
-    const double* src = reinterpret_cast<const double*>(&lb);
-    double* dst = reinterpret_cast<double*>(&sl);
-    for (int x = threadIdx.x; x < static_cast<int>(sizeof(LbGrid) / 8); x += blockDim.x) dst[x] = src[x];
-  }
   const int v = row0 + blockIdx.x;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const unsigned lt = (1u << lane) - 1u;
@@ -421,6 +419,7 @@ __global__ void __launch_bounds__(kGridBlock) k_pair_filter_grid(
   if (threadIdx.x == 0) {
     s_ncl = 0;
     s_next = 0;
+    s_nsurv = 0;
   }
   __syncthreads();
   // candidate cells: the boxes swept by av tau / 2 over the reach intervals
@@ -529,6 +528,11 @@ __global__ void __launch_bounds__(kGridBlock) k_pair_filter_grid(
   }
   __syncthreads();
   const int total = cl_pref[ncl];
+  auto keep_surv = [&](int uu) {
+    atomicOr(&bits[uu >> 5], 1u << (uu & 31));
+    const int k = atomicAdd(&s_nsurv, 1);
+    if (k < 32) s_surv[k] = uu;
+  };
   bool active = false, exhausted = false;
   PairLb p{};
   int i = 0, s = 0, u = 0;
@@ -566,7 +570,7 @@ __global__ void __launch_bounds__(kGridBlock) k_pair_filter_grid(
             p = pair_lb<DW>(ap, av, bp, bv);
             if (!(2.0 * sqrt(p.D) >= g.r_n)) {
               if (!lb_head_clears(p, sl)) {
-                atomicOr(&bits[u >> 5], 1u << (u & 31));
+                keep_surv(u);
               } else {
                 active = true;
                 i = 0;
@@ -586,7 +590,7 @@ __global__ void __launch_bounds__(kGridBlock) k_pair_filter_grid(
         s = z < 4 ? (z > s ? z : s) : 4;
         if (i == kLbK) active = false;
       } else if (s == 0) {
-        atomicOr(&bits[u >> 5], 1u << (u & 31));
+        keep_surv(u);
         active = false;
       } else if (s == 4 && use_global && lb_global_clears(p, sl.thr)) {
         active = false;  // the root did not clear, the global bound does: rejected
@@ -596,6 +600,17 @@ __global__ void __launch_bounds__(kGridBlock) k_pair_filter_grid(
     }
   }
   __syncthreads();
+  const int nsurv = s_nsurv;
+  if (nsurv <= 32) {  // the short list in ascending order: a lane's rank among the listed nodes
+    if (warp == 0) {
+      const int x = lane < nsurv ? s_surv[lane] : 0x7fffffff;
+      int rank = 0;
+      for (int q = 0; q < nsurv; ++q) rank += __shfl_sync(0xffffffffu, x, q) < x ? 1 : 0;
+      if (lane < nsurv && rank < cap) su[static_cast<int64_t>(v) * cap + rank] = x;
+      if (lane == 0) row_cnt[v] = nsurv;
+    }
+    return;
+  }
   // ascending-u compaction of the bitmask, kGridBlock words per pass
   int base_run = 0;
   for (int w0 = 0; w0 < nw; w0 += kGridBlock) {
@@ -1052,6 +1067,13 @@ void build_graph_device(DevGraph& G, Ctx& c, int n, int dw, const double* h_pos,
   }
   GraphArgs ga{n, G.pos.as<double>(), G.vel.as<double>(), r_n, dt, eps_cc, tau_max, ratio};
   const LbGrid lbg = make_lb_grid(r_n);
+  {  // k_pair_filter_grid reads the table from device memory (uploaded when r_n changes)
+    DBuf& lbb = c.buf("g_lbgrid", sizeof(LbGrid));
+    if (c.lbgrid_rn != r_n) {
+      c.h2d(lbb.p, &lbg, sizeof(LbGrid));
+      c.lbgrid_rn = r_n;
+    }
+  }
   WorldD wd;
   wd.n_obs = w.n_obs;
   wd.lo = w.d_lo;
@@ -1169,7 +1191,7 @@ void build_graph_device(DevGraph& G, Ctx& c, int n, int dw, const double* h_pos,
           if (sm > 32 * 1024)
             PUMP_CUDA(cudaFuncSetAttribute(k_pair_filter_grid<DW>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
           k_pair_filter_grid<DW><<<row_hi - row_lo, kGridBlock, sm, st>>>(
-              ga, lbg, cg, sz, cap, row_lo, refill, c.scratch["g_ccnt"].as<int32_t>(), c.scratch["g_cstart"].as<int64_t>(),
+              ga, c.scratch["g_lbgrid"].as<LbGrid>(), cg, sz, cap, row_lo, refill, c.scratch["g_ccnt"].as<int32_t>(), c.scratch["g_cstart"].as<int64_t>(),
               c.scratch["g_cbox"].as<unsigned long long>(), c.scratch["g_sidx"].as<int32_t>(),
               c.scratch["g_spos"].as<double>(), c.scratch["g_svel"].as<double>(), rcnt.as<int32_t>(),
               suB.as<int32_t>(), 1);
