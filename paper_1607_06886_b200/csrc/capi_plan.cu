@@ -1895,6 +1895,7 @@ int pump_graph_upload(pump_ctx* ctx, const pump_graph_view* v, pump_graph** out)
       G.E = E;
       G.NW = NW;
       G.H = H;
+      G.H_pk = H;
       auto up = [&](DBuf& b, const void* src, size_t bytes) {
         b.ensure(bytes + 256);
         c.h2d(b.p, src, bytes);
@@ -1972,7 +1973,7 @@ int pump_graph_export(const pump_graph* g, pump_graph_view* v) {
     // half-spaces: waypoint w owns [hs_off[w], hs_off[w] + hs_cnt[w]) on the
     // device; the exported view is the reference's waypoint-ordered CSR
     if (v->wp_hs_off || v->hs_a || v->hs_b || v->hs_fallback) {
-      const int64_t NW = G.NW, H = G.H;
+      const int64_t NW = G.NW, H = G.H_pk;  // (stored records; waypoints may share them)
       std::vector<int64_t> start(NW + 1);
       std::vector<int32_t> cnt(NW + 1);
       std::vector<double> pk(static_cast<size_t>(H) * 4 + 4);

@@ -854,6 +854,10 @@ __device__ __forceinline__ void wp_state(const GraphArgs& g, int64_t x, const in
 // Spatial order of the waypoints for the region pass: state into ys
 // ([x][y, yd]), a row-major cell id of a grid over the workspace bounds, and
 // the cell histogram.  k_wp_scatter then lists the waypoints cell by cell.
+// An edge's end waypoint is its end node's state (wp_state), so its region is
+// the node's: the pass takes the n nodes as items n_wp + u instead of the E end
+// waypoints (key -1: not listed), and k_wp_end_link points each end waypoint at
+// its node's records.
 struct WpCells {
   double lo[3], inv[3];
   int dim[3];
@@ -866,9 +870,22 @@ __global__ void k_wp_prep(GraphArgs g, int64_t n_wp, const int64_t* __restrict__
                           const int32_t* __restrict__ wp_edge, WpCells cg, double* __restrict__ ys,
                           int32_t* __restrict__ key, int32_t* __restrict__ hist) {
   const int64_t x = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (x >= n_wp) return;
+  if (x >= n_wp + g.n) return;
   double y[DW], yd[DW];
-  wp_state<DW>(g, x, wp_off, e_from, e_to, e_tau, e_acc0, e_jerk, e_nsteps, wp_edge, y, yd);
+  if (x >= n_wp) {  // node u = x - n_wp
+#pragma unroll
+    for (int k = 0; k < DW; ++k) {
+      y[k] = g.pos[(x - n_wp) * DW + k];
+      yd[k] = g.vel[(x - n_wp) * DW + k];
+    }
+  } else {
+    const int e = wp_edge[x];
+    if (x == wp_off[e + 1] - 1) {  // the end waypoint: its node's region
+      key[x] = -1;
+      return;
+    }
+    wp_state<DW>(g, x, wp_off, e_from, e_to, e_tau, e_acc0, e_jerk, e_nsteps, wp_edge, y, yd);
+  }
   int id = 0;
 #pragma unroll
   for (int k = DW - 1; k >= 0; --k) {
@@ -887,7 +904,27 @@ __global__ void k_wp_scatter(int64_t n_wp, const int32_t* __restrict__ key, cons
   const int64_t x = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (x >= n_wp) return;
   const int c = key[x];
+  if (c < 0) return;
   perm[cell_off[c] + atomicAdd(cursor + c, 1)] = static_cast<int32_t>(x);
+}
+// an edge's end waypoint -> its end node's records (items n_wp + u of the
+// region pass); *delta += (shared records - the nodes' own records), so the
+// waypoint total H = stored + delta
+__global__ void k_wp_end_link(int64_t n_edges, int n_nodes, int64_t n_wp, const int64_t* __restrict__ wp_off,
+                              const int32_t* __restrict__ e_to, int64_t* __restrict__ hs_off,
+                              int32_t* __restrict__ hs_cnt, unsigned long long* __restrict__ delta) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  long long d = 0;
+  if (i < n_edges && wp_off[i + 1] > wp_off[i]) {
+    const int64_t x = wp_off[i + 1] - 1, src = n_wp + e_to[i];
+    hs_off[x] = hs_off[src];
+    hs_cnt[x] = hs_cnt[src];
+    d += hs_cnt[src];
+  }
+  if (i < n_nodes) d -= hs_cnt[n_wp + i];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) d += __shfl_xor_sync(0xffffffffu, d, o);
+  if ((threadIdx.x & 31) == 0 && d != 0) atomicAdd(delta, static_cast<unsigned long long>(d));
 }
 
 // blocks of 128 threads, 512 above 256 boxes (the staged boxes are shared by
@@ -906,12 +943,16 @@ __global__ void __launch_bounds__(regions_block(KW)) k_regions_once(GraphArgs g,
                                                       int64_t* __restrict__ hs_off, int32_t* __restrict__ hs_cnt,
                                                       double* __restrict__ hs_pk, uint8_t* __restrict__ hs_fb,
                                                       int* __restrict__ err, unsigned long long* __restrict__ work,
-                                                      const int32_t* __restrict__ perm, const double* __restrict__ ys) {
+                                                      const int32_t* __restrict__ perm, const double* __restrict__ ys,
+                                                      const int64_t* __restrict__ n_list) {
   extern __shared__ double smem[];
+  // sorted pass: n_list = the listed items (perm entries), on the device
+  const int64_t n_act = n_list ? *n_list : n_wp;
+  if (static_cast<int64_t>(blockIdx.x) * blockDim.x >= n_act) return;  // (block-uniform)
   const WorldD ws = stage_world<DW>(w, smem);
   const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   const int lane = threadIdx.x & 31;
-  const bool active = t < n_wp;
+  const bool active = t < n_act;
   // spatially ordered pass (perm given): thread t takes waypoint perm[t] with
   // its state precomputed by k_wp_prep, so a warp holds nearby waypoints
   const int64_t x = !active ? t : perm ? perm[t] : t;
@@ -1369,8 +1410,8 @@ void build_graph_device(DevGraph& G, Ctx& c, int n, int dw, const double* h_pos,
   mark("connect .. waypoint scan");
   G.NW = NW;
   DBuf& err = c.buf("g_err", 256);
-  G.hs_off.ensure(al((NW + 2) * 8));
-  G.hs_cnt.ensure(al((NW + 2) * 4));
+  G.hs_off.ensure(al((NW + n + 2) * 8));  // (+ n: the nodes' regions, sorted pass)
+  G.hs_cnt.ensure(al((NW + n + 2) * 4));
   PUMP_CUDA(cudaMemsetAsync(err.p, 0, 4, st));
   {
     DBuf& wpe = c.buf("g_wp_edge", al((NW + 8) * 4));
@@ -1386,6 +1427,8 @@ void build_graph_device(DevGraph& G, Ctx& c, int n, int dw, const double* h_pos,
     const bool sorted = w.n_obs > kOnceMaxObs && NW > 0;
     const int32_t* d_perm = nullptr;
     const double* d_ys = nullptr;
+    const int64_t* d_nlist = nullptr;
+    int64_t n_items = NW;
     if (sorted) {
       WpCells cg{};
       double vol = 1.0;
@@ -1400,27 +1443,31 @@ void build_graph_device(DevGraph& G, Ctx& c, int n, int dw, const double* h_pos,
         cg.inv[k] = cg.dim[k] / ext;
         ncell *= cg.dim[k];
       }
-      DBuf& ysb = c.buf("g_wp_ys", al(NW * 2 * dw * 8 + 64));
-      DBuf& keyb = c.buf("g_wp_key", al(NW * 4 + 64));
-      DBuf& permb = c.buf("g_wp_perm", al(NW * 4 + 64));
+      // items: the waypoints but the edges' end waypoints, then the n nodes
+      const int64_t NI = NW + n;
+      DBuf& ysb = c.buf("g_wp_ys", al(NI * 2 * dw * 8 + 64));
+      DBuf& keyb = c.buf("g_wp_key", al(NI * 4 + 64));
+      DBuf& permb = c.buf("g_wp_perm", al(NI * 4 + 64));
       DBuf& hist = c.buf("g_wp_hist", al((ncell + 2) * 4));
       DBuf& hoff = c.buf("g_wp_hoff", al((ncell + 2) * 8));
       DBuf& htmp = c.buf("g_wp_htmp", scan_temp_bytes(ncell + 2));
       PUMP_CUDA(cudaMemsetAsync(hist.p, 0, (ncell + 1) * 4, st));
       KScope ks(st, F_REGIONS);
       dispatch_dw(dw, [&]<int DW>() {
-        k_wp_prep<DW><<<grid_for(NW, 256), 256, 0, st>>>(
+        k_wp_prep<DW><<<grid_for(NI, 256), 256, 0, st>>>(
             ga, NW, G.wp_off.as<int64_t>(), G.e_from.as<int32_t>(), G.e_to.as<int32_t>(), G.e_tau.as<double>(),
             G.e_acc0.as<double>(), G.e_jerk.as<double>(), G.e_nsteps.as<int32_t>(), wpe.as<int32_t>(), cg,
             ysb.as<double>(), keyb.as<int32_t>(), hist.as<int32_t>());
       });
       exclusive_scan<int32_t>(hist.as<int32_t>(), hoff.as<int64_t>(), ncell, htmp.p, st, &c.launches);
       PUMP_CUDA(cudaMemsetAsync(hist.p, 0, (ncell + 1) * 4, st));
-      k_wp_scatter<<<grid_for(NW, 256), 256, 0, st>>>(NW, keyb.as<int32_t>(), hoff.as<int64_t>(), hist.as<int32_t>(),
+      k_wp_scatter<<<grid_for(NI, 256), 256, 0, st>>>(NI, keyb.as<int32_t>(), hoff.as<int64_t>(), hist.as<int32_t>(),
                                                      permb.as<int32_t>());
       c.launches += 2;
       d_perm = permb.as<int32_t>();
       d_ys = ysb.as<double>();
+      d_nlist = hoff.as<int64_t>() + ncell;  // the listed items (the scan total)
+      n_items = NI;
     }
     DBuf& ctr = c.buf("g_hs_counter", 256);
     int64_t cap = std::max<int64_t>(G.hs_cap, NW * 4 + 16);
@@ -1438,7 +1485,7 @@ void build_graph_device(DevGraph& G, Ctx& c, int n, int dw, const double* h_pos,
       G.hs_pk.ensure(al((cap + 1) * 32));
       G.hs_fb.ensure(al(cap + 1));
       G.hs_cap = cap;
-      PUMP_CUDA(cudaMemsetAsync(ctr.p, 0, 8, st));
+      PUMP_CUDA(cudaMemsetAsync(ctr.p, 0, 16, st));  // stored records, end-waypoint delta
       // work counters only while the per-kernel profiler is on (bench.py's second pass)
       KProf* kp = kprof_current();
       const bool count = kp && kp->on;
@@ -1457,23 +1504,31 @@ void build_graph_device(DevGraph& G, Ctx& c, int n, int dw, const double* h_pos,
                                                              : 0);
           if (sm > 48 * 1024)
             PUMP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-          kern<<<grid_for(NW, blk), blk, sm, st>>>(
+          kern<<<grid_for(n_items, blk), blk, sm, st>>>(
               ga, wd, NW, E, G.wp_off.as<int64_t>(), G.e_from.as<int32_t>(), G.e_to.as<int32_t>(),
               G.e_tau.as<double>(), G.e_acc0.as<double>(), G.e_jerk.as<double>(), G.e_nsteps.as<int32_t>(),
               c.scratch["g_wp_edge"].as<int32_t>(), cap,
               ctr.as<unsigned long long>(), G.hs_off.as<int64_t>(), G.hs_cnt.as<int32_t>(), G.hs_pk.as<double>(),
-              G.hs_fb.as<uint8_t>(), err.as<int>(), count ? wk.as<unsigned long long>() : nullptr, d_perm, d_ys);
+              G.hs_fb.as<uint8_t>(), err.as<int>(), count ? wk.as<unsigned long long>() : nullptr, d_perm, d_ys,
+              d_nlist);
         });
         ++c.launches;
         PUMP_CUDA(cudaGetLastError());
+        if (sorted) {
+          k_wp_end_link<<<grid_for(std::max<int64_t>(E, n), 256), 256, 0, st>>>(
+              E, n, NW, G.wp_off.as<int64_t>(), G.e_to.as<int32_t>(), G.hs_off.as<int64_t>(), G.hs_cnt.as<int32_t>(),
+              ctr.as<unsigned long long>() + 1);
+          ++c.launches;
+        }
       }
-      int64_t H = 0;
+      int64_t Hd[2] = {0, 0};
       int herr = 0;
       std::vector<int64_t> wv(count ? 256 : 0);
-      c.d2h(&H, ctr.p, 8);
+      c.d2h(Hd, ctr.p, 16);
       if (count) c.d2h(wv.data(), wk.p, 256 * 8);
       c.d2h(&herr, err.p, 4);
       c.sync();
+      const int64_t H = Hd[0];  // stored records (the capacity check)
       int64_t Hw[3] = {H, 0, 0};
       for (int q = 0; q < 128 && count; ++q) {
         Hw[1] += wv[2 * q];
@@ -1485,11 +1540,12 @@ void build_graph_device(DevGraph& G, Ctx& c, int n, int dw, const double* h_pos,
       kprof_work(F_REGIONS, 14 * Hw[1] + 10 * Hw[2]);
       mark("regions");
       if (herr) throw std::runtime_error("local_convex_region: pruning loop failed to make progress");
-      G.H = H;
+      G.H_pk = H;
+      G.H = H + Hd[1];  // every waypoint's half-spaces
       if (H <= cap && std::getenv("PUMP_DEBUG_GRAPH"))
         std::fprintf(stderr, "[pump graph] n=%d pairs=%lld survivors=%lld candidates=%lld edges=%lld waypoints=%lld "
-                     "halfspaces=%lld\n", n, (long long)n * (n - 1), (long long)G.n_connect, (long long)G.n_cand,
-                     (long long)G.E, (long long)NW, (long long)H);
+                     "halfspaces=%lld stored=%lld\n", n, (long long)n * (n - 1), (long long)G.n_connect,
+                     (long long)G.n_cand, (long long)G.E, (long long)NW, (long long)G.H, (long long)H);
       if (H <= cap) break;
       cap = H + H / 8;  // rerun with room to spare (per-waypoint content is deterministic)
       if (H > room())

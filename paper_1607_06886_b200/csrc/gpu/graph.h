@@ -8,12 +8,14 @@ namespace pumpg {
 struct DevGraph {
   int n = 0, dw = 0;
   double r_n = 0, dt = 0;
-  int64_t E = 0, NW = 0, H = 0, n_cand = 0, n_connect = 0;
+  // H: half-spaces over all waypoints (the reference's count); H_pk: records
+  // stored in hs_pk (the edges' end waypoints share their end node's records)
+  int64_t E = 0, NW = 0, H = 0, H_pk = 0, n_cand = 0, n_connect = 0;
   DBuf pos, vel;                                          // n x dw
   DBuf row_ptr;                                           // n + 1 (int64)
   DBuf e_from, e_to, e_cost, e_tau, e_acc0, e_jerk, e_nsteps;
   DBuf wp_off;                                            // E + 1 (int64)
-  DBuf hs_off;                                            // NW (+1): first half-space of each waypoint
+  DBuf hs_off;                                            // NW (+ n): first half-space of each waypoint (then node)
   int64_t hs_cap = 0;                                     // half-space slots in hs_pk/hs_fb
   DBuf hs_cnt;                                            // NW: half-spaces of each waypoint
   // half-spaces packed 32 B each {a_0 .. a_{dw-1}, (pad), b at [3]}: one
