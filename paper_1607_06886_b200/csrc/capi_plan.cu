@@ -156,48 +156,165 @@ static bool point_free_h(const HostWorld& w, const double* y) {
 // velocities, the host blend's expressions), then nominal_free of it
 // (pump.hpp:64-75: every waypoint point_free, every positive-length segment's
 // cubic Hermite motion_collides).  The positions feed the MC batch directly.
-template <int DW>
-__global__ void k_smooth_blend(int n_probe, int n_wp, const double* __restrict__ sv, const double* __restrict__ pt,
-                               const double* __restrict__ pp, const double* __restrict__ pv, MotionD<DW> opt,
-                               double* __restrict__ y, double* __restrict__ yv) {
-  const int64_t x = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (x >= static_cast<int64_t>(n_probe) * n_wp) return;
-  const int q = static_cast<int>(x % n_wp);
-  const double s = sv[x / n_wp];
-  double op[DW], ov[DW];
-  motion_state<DW>(opt, pt[q], op, ov);
-#pragma unroll
-  for (int k = 0; k < DW; ++k) {
-    y[x * DW + k] = (1 - s) * pp[q * DW + k] + s * op[k];
-    yv[x * DW + k] = (1 - s) * pv[q * DW + k] + s * ov[k];
+//
+// The reference's bisection (pump.hpp:118-141) is chained on the stream in
+// depth-2 speculative batches: batch 0 probes s = 1 and the first two
+// bisection levels {0.5, 0.75, 0.25}; batch b >= 1 first replays the two steps
+// of the previous batch (certified = free and hits / n_mc <= alpha, the host's
+// expressions) and then probes m = 0.5 (lo + hi) with both of its children
+// 0.5 (m + hi) and 0.5 (lo + m).  Five batches cover the 10 steps.  Once s = 1
+// certifies every later probe is marked done (no check, no MC).  The host
+// reads the history once and replays the bisection from it.
+constexpr int kSmoothSlots = 16;  // 4 + 4 batches x 3
+constexpr int kSmoothBatches = 5;
+struct SmoothChain {
+  // bisection state entering batch b (b = 0: the initial [0, 1]): batch b
+  // reads entry b and writes entry b + 1, so the blocks of one launch never
+  // read what its first block writes
+  double lo[kSmoothBatches + 1], hi[kSmoothBatches + 1];
+  int32_t done_b[kSmoothBatches + 1];
+  int32_t done, pad;
+  double s[kSmoothSlots];
+  unsigned long long hits[kSmoothSlots];
+  int32_t live[kSmoothSlots];  // 1 until the nominal check fails (0: no MC; also when done)
+  unsigned long long steps;
+};
+__global__ void k_smooth_init(SmoothChain* c) {
+  const int q = threadIdx.x;
+  if (q < kSmoothSlots) {
+    c->live[q] = 1;
+    c->hits[q] = 0;
+  }
+  if (q == 0) {
+    c->lo[0] = 0;
+    c->hi[0] = 1;
+    c->done_b[0] = 0;
+    c->done = 0;
+    c->steps = 0;
   }
 }
+__device__ __forceinline__ bool smooth_cert(const SmoothChain* c, int q, int64_t n_mc, double alpha) {
+  return c->live[q] != 0 && static_cast<double>(c->hits[q]) / n_mc <= alpha;
+}
+// one bisection step on probe slots (m, m_hi child, m_lo child)
+__device__ __forceinline__ void smooth_two_steps(const SmoothChain* c, int q, int64_t n_mc, double alpha, double& lo,
+                                                 double& hi) {
+  const bool cm = smooth_cert(c, q, n_mc, alpha);
+  if (cm)
+    lo = c->s[q];
+  else
+    hi = c->s[q];
+  const int qc = cm ? q + 1 : q + 2;  // the child the bisection visits next
+  if (smooth_cert(c, qc, n_mc, alpha))
+    lo = c->s[qc];
+  else
+    hi = c->s[qc];
+}
+// batch b's decision (the previous batches' verdicts are final): its probes
+// s[0..np) and whether the bisection is done
+__device__ __forceinline__ void smooth_decide(const SmoothChain* c, int batch, int64_t n_mc, double alpha,
+                                              double* sv, double& lo, double& hi, int& done) {
+  lo = c->lo[batch];
+  hi = c->hi[batch];
+  done = c->done_b[batch];
+  if (batch == 0) {
+    sv[0] = 1.0;
+    const double m = 0.5 * (lo + hi);
+    sv[1] = m;
+    sv[2] = 0.5 * (m + hi);
+    sv[3] = 0.5 * (lo + m);
+    return;
+  }
+  const int q0 = 4 + 3 * (batch - 1);
+  if (!done) {
+    if (batch == 1) {
+      if (smooth_cert(c, 0, n_mc, alpha))
+        done = 1;  // s = 1 certifies: no bisection
+      else
+        smooth_two_steps(c, 1, n_mc, alpha, lo, hi);
+    } else {
+      smooth_two_steps(c, q0 - 3, n_mc, alpha, lo, hi);
+    }
+  }
+  const double m = 0.5 * (lo + hi);
+  sv[0] = m;
+  sv[1] = 0.5 * (m + hi);
+  sv[2] = 0.5 * (lo + m);
+}
 
-// The nominal check of the blended probes (point_free of every waypoint,
-// motion_collides of every segment), a warp per (probe, waypoint): the waypoint's point_free
-// and the segment's obstacle cull (motion_cull: the boxes not separated from
-// the motion's widened bounding box) run with the lanes over the boxes, then
-// every lane runs motion_collides on the warp's bitmask (identical data, no
-// divergence).  Same tests, same verdicts; a warp instead of a thread because
-// a batch holds only ~4 x 260 items.  LIST = 0: worlds of at most 64
-// kCullWords boxes (bitmask); LIST = kCullList: larger worlds, the candidates
-// listed in ascending order by ballot, all boxes tested past LIST of them
-// (motion_cull's list mode).
+// One batch in one launch: every block takes the batch's decision itself
+// (block 0 records it), then a warp per (probe, waypoint) blends the
+// waypoint and its successor, stores the waypoint for the MC batch, and runs
+// the nominal check: point_free with the lanes over the boxes, the segment's
+// obstacle cull (motion_cull: the boxes not separated from the motion's
+// widened bounding box) likewise, then every lane runs motion_collides on the
+// warp's candidates (identical data, no divergence).  Same tests, same
+// verdicts.  LIST = 0: worlds of at most 64 kCullWords boxes (bitmask);
+// LIST = kCullList: larger worlds, the candidates listed in ascending order by
+// ballot, all boxes tested past LIST of them (motion_cull's list mode).
 template <int DW, int LIST>
-__global__ void __launch_bounds__(128) k_smooth_check_warp(WorldD w, int n_probe, int n_wp,
-                                                           const double* __restrict__ pt,
-                                                           const double* __restrict__ y,
-                                                           const double* __restrict__ yv, double eps_cc,
-                                                           int32_t* __restrict__ free_flag) {
+__global__ void __launch_bounds__(128) k_smooth_probe(SmoothChain* chn, int batch, int64_t n_mc, double alpha, WorldD w,
+                                                      int n_wp, const double* __restrict__ pt,
+                                                      const double* __restrict__ pp, const double* __restrict__ pv,
+                                                      MotionD<DW> opt, double eps_cc, double* __restrict__ y,
+                                                      double* __restrict__ yv) {
   extern __shared__ double smem[];
-  const WorldD ws = stage_world<DW>(w, smem);
+  __shared__ double s_sv[4];
+  __shared__ int s_done;
+  const int q0 = batch == 0 ? 0 : 4 + 3 * (batch - 1), n_probe = batch == 0 ? 4 : 3;
+  if (threadIdx.x == 0) {
+    double sv[4], lo, hi;
+    int done;
+    smooth_decide(chn, batch, n_mc, alpha, sv, lo, hi, done);
+    for (int k = 0; k < n_probe; ++k) s_sv[k] = sv[k];
+    s_done = done;
+    if (blockIdx.x == 0) {
+      chn->lo[batch + 1] = lo;
+      chn->hi[batch + 1] = hi;
+      chn->done_b[batch + 1] = done;
+      chn->done = done;
+      for (int k = 0; k < n_probe; ++k) {
+        chn->s[q0 + k] = sv[k];
+        if (done) chn->live[q0 + k] = 0;
+      }
+    }
+  }
+  const WorldD ws = stage_world<DW>(w, smem);  // (its __syncthreads publishes s_sv / s_done)
+  if (s_done) return;
   const int64_t x = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (x >= static_cast<int64_t>(n_probe) * n_wp) return;
   const int64_t pr = x / n_wp;
   const int j = static_cast<int>(x % n_wp);
-  if (free_flag[pr] == 0) return;
-  const double* yp = y + x * DW;
+  const double sp = s_sv[pr];
+  // the blend of waypoints j and j + 1 (k_smooth_blend's expressions)
+  double y_j[DW], yv_j[DW], y_n[DW], yv_n[DW];
+  {
+    double op[DW], ov[DW];
+    motion_state<DW>(opt, pt[j], op, ov);
+#pragma unroll
+    for (int k = 0; k < DW; ++k) {
+      y_j[k] = (1 - sp) * pp[j * DW + k] + sp * op[k];
+      yv_j[k] = (1 - sp) * pv[j * DW + k] + sp * ov[k];
+    }
+    if (lane == 0) {
+#pragma unroll
+      for (int k = 0; k < DW; ++k) {
+        y[x * DW + k] = y_j[k];
+        yv[x * DW + k] = yv_j[k];
+      }
+    }
+    if (j + 1 < n_wp) {
+      motion_state<DW>(opt, pt[j + 1], op, ov);
+#pragma unroll
+      for (int k = 0; k < DW; ++k) {
+        y_n[k] = (1 - sp) * pp[(j + 1) * DW + k] + sp * op[k];
+        yv_n[k] = (1 - sp) * pv[(j + 1) * DW + k] + sp * ov[k];
+      }
+    }
+  }
+  if (chn->live[q0 + pr] == 0) return;  // another waypoint of this probe already failed
+  const double* yp = y_j;
   // point_free (geom.hpp:56-61): bounds, then every box, lanes over the boxes
   bool hit = false;
   for (int o = lane; o < ws.n_obs && !hit; o += 32) hit = box_contains<DW>(ws.lo + o * DW, ws.hi + o * DW, yp);
@@ -209,9 +326,9 @@ __global__ void __launch_bounds__(128) k_smooth_check_warp(WorldD w, int n_probe
 #pragma unroll
       for (int k = 0; k < DW; ++k) {
         m.p0[k] = yp[k];
-        m.v0[k] = yv[x * DW + k];
-        m.p1[k] = y[(x + 1) * DW + k];
-        m.v1[k] = yv[(x + 1) * DW + k];
+        m.v0[k] = yv_j[k];
+        m.p1[k] = y_n[k];
+        m.v1[k] = yv_n[k];
       }
       m.tau = h;
       coeffs_dev<DW>(m.p0, m.v0, m.p1, m.v1, m.tau, m.a, m.j);
@@ -269,79 +386,9 @@ __global__ void __launch_bounds__(128) k_smooth_check_warp(WorldD w, int n_probe
       }
     }
   }
-  if (!ok && lane == 0) free_flag[pr] = 0;
+  if (!ok && lane == 0) chn->live[q0 + pr] = 0;
 }
 
-// The reference's smoothing bisection (pump.hpp:118-141) chained on the
-// stream in depth-2 speculative batches: batch 0 probes s = 1 and the first
-// two bisection levels {0.5, 0.75, 0.25}; batch b >= 1 first replays the two
-// steps of the previous batch (certified = free and hits / n_mc <= alpha, the
-// host's expressions) and then probes m = 0.5 (lo + hi) with both of its
-// children 0.5 (m + hi) and 0.5 (lo + m).  Five batches cover the 10 steps.
-// Once s = 1 certifies every later probe is marked done (no check, no MC).
-// The host reads the history once and replays the bisection from it.
-constexpr int kSmoothSlots = 16;  // 4 + 4 batches x 3
-struct SmoothChain {
-  double lo, hi;
-  int32_t done, pad;
-  double s[kSmoothSlots];
-  unsigned long long hits[kSmoothSlots];
-  int32_t live[kSmoothSlots];  // 1 until the nominal check fails (0: no MC; also when done)
-  unsigned long long steps;
-};
-__device__ __forceinline__ bool smooth_cert(const SmoothChain* c, int q, int64_t n_mc, double alpha) {
-  return c->live[q] != 0 && static_cast<double>(c->hits[q]) / n_mc <= alpha;
-}
-// one bisection step on probe slots (m, m_hi child, m_lo child)
-__device__ __forceinline__ void smooth_two_steps(SmoothChain* c, int q, int64_t n_mc, double alpha) {
-  const bool cm = smooth_cert(c, q, n_mc, alpha);
-  if (cm)
-    c->lo = c->s[q];
-  else
-    c->hi = c->s[q];
-  const int qc = cm ? q + 1 : q + 2;  // the child the bisection visits next
-  if (smooth_cert(c, qc, n_mc, alpha))
-    c->lo = c->s[qc];
-  else
-    c->hi = c->s[qc];
-}
-__global__ void k_smooth_decide(SmoothChain* c, int batch, int64_t n_mc, double alpha) {
-  int q0, np;
-  if (batch == 0) {
-    c->done = 0;
-    c->steps = 0;
-    c->lo = 0;
-    c->hi = 1;
-    q0 = 0;
-    np = 4;
-    c->s[0] = 1.0;
-    const double m = 0.5 * (c->lo + c->hi);
-    c->s[1] = m;
-    c->s[2] = 0.5 * (m + c->hi);
-    c->s[3] = 0.5 * (c->lo + m);
-  } else {
-    q0 = 4 + 3 * (batch - 1);
-    np = 3;
-    if (!c->done) {
-      if (batch == 1) {
-        if (smooth_cert(c, 0, n_mc, alpha))
-          c->done = 1;  // s = 1 certifies: no bisection
-        else
-          smooth_two_steps(c, 1, n_mc, alpha);
-      } else {
-        smooth_two_steps(c, q0 - 3, n_mc, alpha);
-      }
-      const double m = 0.5 * (c->lo + c->hi);
-      c->s[q0] = m;
-      c->s[q0 + 1] = 0.5 * (m + c->hi);
-      c->s[q0 + 2] = 0.5 * (c->lo + m);
-    }
-  }
-  for (int k = 0; k < np; ++k) {
-    c->live[q0 + k] = c->done ? 0 : 1;
-    c->hits[q0 + k] = 0;
-  }
-}
 
 // ------------------------------------------------------------ path kernels
 // Walk parent pointers of selected plans and resolve each hop to its edge
@@ -989,25 +1036,23 @@ static SmoothOut smooth_device(Ctx& c, const std::vector<HWp>& plan, double plan
       c.mc_join_pending = false;
     }
     c.tic();
-    for (int b = 0; b < 5; ++b) {
+    k_smooth_init<<<1, 32, 0, c.stream>>>(ch);
+    ++c.launches;
+    for (int b = 0; b < kSmoothBatches; ++b) {
       const int q0 = b == 0 ? 0 : 4 + 3 * (b - 1), np = b == 0 ? 4 : 3;
       const int64_t it = static_cast<int64_t>(np) * n_wp;
-      k_smooth_decide<<<1, 1, 0, c.stream>>>(ch, b, n_mc, alpha);
       dispatch_dw(dw, [&]<int DW>() {
         HMotion o = opt;
-        k_smooth_blend<DW><<<grid_for(it, 128), 128, 0, c.stream>>>(
-            np, n_wp, &ch->s[q0], c.scratch["sm_plan"].as<double>(), c.scratch["sm_plan"].as<double>() + n_wp,
-            c.scratch["sm_plan"].as<double>() + n_wp * (1 + dw), as_motion<DW>(o), d_y.as<double>(),
-            d_yv.as<double>());
-        auto kern = wd.n_obs <= 64 * kCullWords ? k_smooth_check_warp<DW, 0> : k_smooth_check_warp<DW, kCullList>;
+        auto kern = wd.n_obs <= 64 * kCullWords ? k_smooth_probe<DW, 0> : k_smooth_probe<DW, kCullList>;
         const size_t sm = static_cast<size_t>(2 * wd.n_obs * DW) * 8 + 16;
         if (sm > 48 * 1024)
           PUMP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm)));
-        kern<<<grid_for(it * 32, 128), 128, sm, c.stream>>>(wd, np, n_wp, c.scratch["sm_plan"].as<double>(),
-                                                            d_y.as<double>(), d_yv.as<double>(), eps_cc,
-                                                            &ch->live[q0]);
+        const double* plan_d = c.scratch["sm_plan"].as<double>();
+        kern<<<grid_for(it * 32, 128), 128, sm, c.stream>>>(ch, b, n_mc, alpha, wd, n_wp, plan_d, plan_d + n_wp,
+                                                            plan_d + n_wp * (1 + dw), as_motion<DW>(o), eps_cc,
+                                                            d_y.as<double>(), d_yv.as<double>());
       });
-      c.launches += 3;
+      c.launches += 1;
       launch_mc(L, dwld, np, d_off.as<int64_t>(), d_y.as<double>(), n_wp, r0, r1, seed, eps_cc,
                 &ch->hits[q0], c.stream, &c.launches, &ch->steps, &c.mc_table, &ch->live[q0]);
       allreduce_sum_i64(c, reinterpret_cast<int64_t*>(&ch->hits[q0]), np);

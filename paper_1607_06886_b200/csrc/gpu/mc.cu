@@ -15,6 +15,7 @@
 // obstacles are staged in shared memory; hits are reduced with a warp
 // ballot + popc, one atomicAdd per warp; rollout-steps are counted the same
 // way for the roofline.
+#include <cooperative_groups.h>
 #include <cmath>
 #include <cstdlib>
 
@@ -594,7 +595,8 @@ __global__ void __launch_bounds__(kMcBlock) k_mctab_dense(const LoopP<D, DW> L, 
 // spread over the grid: thread = (trajectory, rollout, span of kMcSpan
 // steps), y_t = ynom_t + dy_t (the addition k_mc performs), the collision
 // tests of k_mc_sep (bounds, bbox-culled obstacles, eps_cc-subdivided
-// segment).  A hit sets flag[j][i]; k_mc_count sums the flags.
+// segment).  A hit claims flag[j][i] (the rollout's first hit over the
+// span blocks counts it into hits[j]).
 constexpr int kMcChunk = 8;   // steps whose table rows a thread loads up front
 // Per (trajectory, step) the candidate obstacles every rollout of the table
 // can meet (see k_mc_tab), listed once per certification instead of once per
@@ -669,10 +671,12 @@ __global__ void __launch_bounds__(kMcTabBlock) k_mc_tab(WorldD w, const int64_t*
                                                      const double* __restrict__ ynom_all, int64_t r0, int64_t r1,
                                                      int64_t tab_r0, int64_t tab_n, const double* __restrict__ dy,
                                                      const unsigned long long* __restrict__ maxdev, double eps_cc,
-                                                     uint8_t* __restrict__ flags, const int32_t* __restrict__ live,
+                                                     uint32_t* __restrict__ flags, const int32_t* __restrict__ live,
                                                      int t_stride, const uint16_t* __restrict__ g_list,
                                                      const int32_t* __restrict__ g_nl,
-                                                     const uint8_t* __restrict__ g_skip) {
+                                                     const uint8_t* __restrict__ g_skip,
+                                                     unsigned long long* __restrict__ hits,
+                                                     unsigned long long* __restrict__ steps_out) {
   extern __shared__ double smem[];
   constexpr int kMcSpan = kMcChunk * kMcSub;
   __shared__ uint16_t s_list[kMcSpan + 1][kStepCap];
@@ -680,6 +684,9 @@ __global__ void __launch_bounds__(kMcTabBlock) k_mc_tab(WorldD w, const int64_t*
   __shared__ int s_skip[kMcSpan + 1];
   const int j = blockIdx.y;
   if (live && !live[j]) return;  // trajectory not certified (its nominal collides): flags stay 0
+  if (steps_out && blockIdx.x == 0 && blockIdx.z == 0 && threadIdx.x == 0)  // rollouts x (T_j + 1)
+    atomicAdd(steps_out, static_cast<unsigned long long>(r1 - r0) *
+                             static_cast<unsigned long long>(traj_off[j + 1] - traj_off[j]));
   const int64_t p_begin = traj_off[j];
   const int n_pts = static_cast<int>(traj_off[j + 1] - p_begin);
   const int T = n_pts - 1;
@@ -837,26 +844,11 @@ __global__ void __launch_bounds__(kMcTabBlock) k_mc_tab(WorldD w, const int64_t*
     }
   }
   }
-  if (hit) flags[static_cast<int64_t>(j) * (r1 - r0) + (i - r0)] = 1;
-}
-
-// hits[j] += rollouts flagged for trajectory j; steps += rollouts x (T_j + 1)
-__global__ void __launch_bounds__(256) k_mc_count(const uint8_t* __restrict__ flags, int64_t n,
-                                                  const int64_t* __restrict__ traj_off,
-                                                  unsigned long long* __restrict__ hits,
-                                                  unsigned long long* __restrict__ steps_out,
-                                                  const int32_t* __restrict__ live) {
-  const int j = blockIdx.y;
-  if (live && !live[j]) return;
-  const uint8_t* f = flags + static_cast<int64_t>(j) * n;
-  unsigned c = 0;
-  for (int64_t x = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; x < n;
-       x += static_cast<int64_t>(gridDim.x) * blockDim.x)
-    c += f[x];
-  c = __reduce_add_sync(0xffffffffu, c);
-  if ((threadIdx.x & 31) == 0 && c) atomicAdd(hits + j, static_cast<unsigned long long>(c));
-  if (steps_out && blockIdx.x == 0 && threadIdx.x == 0)
-    atomicAdd(steps_out, static_cast<unsigned long long>(n) * static_cast<unsigned long long>(traj_off[j + 1] - traj_off[j]));
+  // a rollout can hit in several spans: the first claim counts it
+  const bool first = hit && atomicExch(flags + static_cast<int64_t>(j) * (r1 - r0) + (i - r0), 1u) == 0u;
+  const cooperative_groups::coalesced_group cg = cooperative_groups::coalesced_threads();
+  const unsigned b = cg.ballot(first);
+  if (b && cg.thread_rank() == 0) atomicAdd(hits + j, static_cast<unsigned long long>(__popc(b)));
 }
 
 // maxdev[t][k] = max_i |dy[t][i][k]| over the table's rollouts, as the bit
@@ -1014,8 +1006,8 @@ void launch_mc(const HostLoop& HL, const DevWorld& w, int n_traj, const int64_t*
       wd.bhi[k] = w.bhi[k];
     }
     const int64_t n = r1 - r0;
-    table->flags.ensure(static_cast<size_t>(n) * n_traj + 256);
-    PUMP_CUDA(cudaMemsetAsync(table->flags.p, 0, static_cast<size_t>(n) * n_traj, st));
+    table->flags.ensure(static_cast<size_t>(n) * n_traj * 4 + 256);
+    PUMP_CUDA(cudaMemsetAsync(table->flags.p, 0, static_cast<size_t>(n) * n_traj * 4, st));
     dispatch_dw(HL.dw, [&]<int DW>() {
       // per-(trajectory, step) candidate lists, once per certification
       const size_t rows_all = static_cast<size_t>(n_traj) * max_points;
@@ -1036,16 +1028,14 @@ void launch_mc(const HostLoop& HL, const DevWorld& w, int n_traj, const int64_t*
         k_mc_tab<DW, SUB><<<grid, kMcTabBlock, smem, st>>>(wd, d_traj_off, d_ynom, r0, r1, table->r0,
                                                         table->r1 - table->r0, table->dy.as<double>(),
                                                         table->maxdev.as<unsigned long long>(), eps_cc,
-                                                        table->flags.as<uint8_t>(), d_live, max_points,
+                                                        table->flags.as<uint32_t>(), d_live, max_points,
                                                         table->step_list.as<uint16_t>(), table->step_nl.as<int32_t>(),
-                                                        table->step_skip.as<uint8_t>());
+                                                        table->step_skip.as<uint8_t>(), d_hits, d_steps);
       };
       KScope ks(st, F_MC);
       go.template operator()<2>();  // 2 x kMcChunk steps per thread (1 and 4 measured slower)
-      k_mc_count<<<dim3(static_cast<unsigned>(std::min<int64_t>((n + 255) / 256, 64)), n_traj), 256, 0, st>>>(
-          table->flags.as<uint8_t>(), n, d_traj_off, d_hits, d_steps, d_live);
     });
-    *launches += 2;
+    *launches += 1;
     PUMP_CUDA(cudaGetLastError());
     return;
   }

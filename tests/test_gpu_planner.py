@@ -291,7 +291,7 @@ def test_run_pump_matches_oracle(oracle_lib, gpu_ctx, name, samples, mc):
 
 def test_run_pump_many_boxes(oracle_lib, gpu_ctx):
     """More than 256 boxes: the list-mode motion cull in collide, the region scan above 256 boxes, and the
-    smoothing probes' nominal check with the list-mode warp cull (k_smooth_check_warp<DW, kCullList>)."""
+    smoothing probes' nominal check with the list-mode warp cull (k_smooth_probe<DW, kCullList>)."""
     import sys
 
     from paper_1607_06886_b200 import api

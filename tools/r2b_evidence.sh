@@ -7,7 +7,7 @@ TAG=${1:-r2b}
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv,noheader
 rm -f gpurun_out/ncu_k_*.ncu-rep
 bash tools/ncu_full.sh quad3d_forest k_regions_once k_round_tail:15 k_expand:15 k_pair_filter_grid k_bank_rec_sep \
-  k_mcnoise_sep k_connect k_collide k_mc_tab k_smooth_check_warp k_wp_prep k_task_map:15
+  k_mcnoise_sep k_connect k_collide k_mc_tab k_smooth_probe k_wp_prep k_task_map:15
 python tools/ncu_kernels.py gpurun_out/ncu_k_*.ncu-rep > gpurun_out/${TAG}_ncu_kernels.json
 python tools/ncu_summary.py gpurun_out/ncu_k_*.ncu-rep > gpurun_out/${TAG}_ncu_full.txt
 cp gpurun_out/${TAG}_ncu_kernels.json profiles/r2_ncu_kernels.json
