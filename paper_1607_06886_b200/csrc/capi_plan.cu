@@ -257,7 +257,10 @@ __global__ void __launch_bounds__(128) k_smooth_probe(SmoothChain* chn, int batc
                                                       int n_wp, const double* __restrict__ pt,
                                                       const double* __restrict__ pp, const double* __restrict__ pv,
                                                       MotionD<DW> opt, double eps_cc, double* __restrict__ y,
-                                                      double* __restrict__ yv) {
+                                                      double* __restrict__ yv,
+                                                      const unsigned long long* __restrict__ maxdev,
+                                                      uint16_t* __restrict__ g_list, int32_t* __restrict__ g_nl,
+                                                      uint8_t* __restrict__ g_skip) {
   extern __shared__ double smem[];
   __shared__ double s_sv[4];
   __shared__ int s_done;
@@ -314,6 +317,13 @@ __global__ void __launch_bounds__(128) k_smooth_probe(SmoothChain* chn, int batc
     }
   }
   if (chn->live[q0 + pr] == 0) return;  // another waypoint of this probe already failed
+  // the MC batch's candidate lists (k_mc_steps' rows): step 0 and step j + 1
+  // (the segment j -> j + 1) of this probe
+  if (maxdev) {
+    if (j == 0) mc_step_row<DW, kStepCap>(ws, y_j, nullptr, maxdev, 0, pr * n_wp, lane, g_list, g_nl, g_skip);
+    if (j + 1 < n_wp)
+      mc_step_row<DW, kStepCap>(ws, y_n, y_j, maxdev, j + 1, pr * n_wp + j + 1, lane, g_list, g_nl, g_skip);
+  }
   const double* yp = y_j;
   // point_free (geom.hpp:56-61): bounds, then every box, lanes over the boxes
   bool hit = false;
@@ -1035,6 +1045,11 @@ static SmoothOut smooth_device(Ctx& c, const std::vector<HWp>& plan, double plan
       PUMP_CUDA(cudaStreamWaitEvent(c.stream, c.join, 0));
       c.mc_join_pending = false;
     }
+    // the probes' MC step lists are written by the probe kernel when the
+    // table holds every probe step (else launch_mc lists them itself)
+    mc_table_prepare(c.mc_table, L, r0, r1, seed, n_wp - 1, c.stream, &c.launches);
+    const bool lists = mc_table_covers(c.mc_table, L, r0, r1, seed, n_wp - 1) && r1 - r0 <= kTabRollouts;
+    if (lists) mc_step_buffers(c.mc_table, 4, n_wp);
     c.tic();
     k_smooth_init<<<1, 32, 0, c.stream>>>(ch);
     ++c.launches;
@@ -1050,11 +1065,15 @@ static SmoothOut smooth_device(Ctx& c, const std::vector<HWp>& plan, double plan
         const double* plan_d = c.scratch["sm_plan"].as<double>();
         kern<<<grid_for(it * 32, 128), 128, sm, c.stream>>>(ch, b, n_mc, alpha, wd, n_wp, plan_d, plan_d + n_wp,
                                                             plan_d + n_wp * (1 + dw), as_motion<DW>(o), eps_cc,
-                                                            d_y.as<double>(), d_yv.as<double>());
+                                                            d_y.as<double>(), d_yv.as<double>(),
+                                                            lists ? c.mc_table.maxdev.as<unsigned long long>() : nullptr,
+                                                            c.mc_table.step_list.as<uint16_t>(),
+                                                            c.mc_table.step_nl.as<int32_t>(),
+                                                            c.mc_table.step_skip.as<uint8_t>());
       });
       c.launches += 1;
       launch_mc(L, dwld, np, d_off.as<int64_t>(), d_y.as<double>(), n_wp, r0, r1, seed, eps_cc,
-                &ch->hits[q0], c.stream, &c.launches, &ch->steps, &c.mc_table, &ch->live[q0]);
+                &ch->hits[q0], c.stream, &c.launches, &ch->steps, &c.mc_table, &ch->live[q0], lists);
       allreduce_sum_i64(c, reinterpret_cast<int64_t*>(&ch->hits[q0]), np);
       PUMP_CUDA(cudaGetLastError());
     }

@@ -1034,6 +1034,61 @@ __device__ __forceinline__ int convex_region_scan(const WorldD& ws, const double
   return count;
 }
 
+// One (trajectory, step) row of the MC table path's candidate lists (a warp):
+// the box of the step's nominal points y1 (and y0, the previous step's) widened
+// by the table's largest deviations maxdev[t] (maxdev[t - 1]), the obstacles
+// (widened by their margin) it meets listed in ascending order, up to kStepCap
+// (more: nl = -1), and skip = the box lies strictly inside the bounds and meets
+// no obstacle (no rollout of the table can hit in this step).  CAP = kStepCap.
+template <int DW, int CAP>
+__device__ __forceinline__ void mc_step_row(const WorldD& w, const double* y1, const double* y0,
+                                            const unsigned long long* __restrict__ maxdev, int t, int64_t row,
+                                            int lane, uint16_t* __restrict__ g_list, int32_t* __restrict__ g_nl,
+                                            uint8_t* __restrict__ g_skip) {
+  double bl[DW], bh[DW];
+  bool inside = true;
+#pragma unroll
+  for (int k = 0; k < DW; ++k) {
+    const double m1 = __longlong_as_double(static_cast<long long>(maxdev[t * DW + k]));
+    double lo = y1[k] - m1, hi = y1[k] + m1;
+    if (y0) {
+      const double m0 = __longlong_as_double(static_cast<long long>(maxdev[(t - 1) * DW + k]));
+      const double lo0 = y0[k] - m0, hi0 = y0[k] + m0;
+      lo = lo0 < lo ? lo0 : lo;
+      hi = hi0 > hi ? hi0 : hi;
+    }
+    const double mg = 1e-12 * (1.0 + (lo < 0 ? -lo : lo) + (hi < 0 ? -hi : hi));
+    bl[k] = lo - mg;
+    bh[k] = hi + mg;
+    inside = inside && bl[k] > w.blo[k] && bh[k] < w.bhi[k];
+  }
+  int nl = 0;
+  for (int o0 = 0; o0 < w.n_obs; o0 += 32) {
+    const int o = o0 + lane;
+    bool meet = false;
+    if (o < w.n_obs) {
+      bool sep = false;
+#pragma unroll
+      for (int k = 0; k < DW; ++k) {
+        const double bl_o = w.blo[k] < 0 ? -w.blo[k] : w.blo[k], bh_o = w.bhi[k] < 0 ? -w.bhi[k] : w.bhi[k];
+        const double lo = w.lo[o * DW + k], hi = w.hi[o * DW + k];
+        const double M = 1e-9 * (1.0 + (lo < 0 ? -lo : lo) + (hi < 0 ? -hi : hi) + 2.0 * (bl_o > bh_o ? bl_o : bh_o));
+        sep = sep || (bh[k] < lo - M) || (bl[k] > hi + M);
+      }
+      meet = !sep;
+    }
+    const unsigned bal = __ballot_sync(0xffffffffu, meet);
+    const int at = nl + __popc(bal & ((1u << lane) - 1u));
+    if (meet && at < CAP) g_list[row * CAP + at] = static_cast<uint16_t>(o);
+    nl += __popc(bal);
+  }
+  if (nl > CAP) nl = -1;
+  if (lane == 0) {
+    g_nl[row] = nl;
+    g_skip[row] = (inside && nl == 0) ? 1 : 0;
+  }
+}
+
 // obstacle boxes staged in shared memory (block-wide; returns the view on them)
 template <int DW>
 __device__ __forceinline__ WorldD stage_world(const WorldD& w, double* smem) {

@@ -219,9 +219,16 @@ void mc_table_prepare(McTable& tab, const HostLoop& L, int64_t r0, int64_t r1, u
                       cudaStream_t st, int64_t* launches);
 // the table already holds rollouts [r0, r1), steps t <= T of this closed loop and seed
 bool mc_table_covers(const McTable& tab, const HostLoop& L, int64_t r0, int64_t r1, uint64_t seed, int T);
+// candidate obstacles listed per (trajectory, step) for the table path (more: nl = -1, test all)
+constexpr int kStepCap = 64;
+// rollouts per table certification (larger ones go in chunks)
+constexpr int64_t kTabRollouts = int64_t(1) << 19;
+// the table's per-(trajectory, step) list buffers for n_traj x max_points rows
+void mc_step_buffers(McTable& tab, int n_traj, int max_points);
 void launch_mc(const HostLoop& L, const DevWorld& w, int n_traj, const int64_t* d_traj_off, const double* d_ynom,
                int max_points, int64_t r0, int64_t r1, uint64_t seed, double eps_cc, unsigned long long* d_hits,
                cudaStream_t st, int64_t* launches, unsigned long long* d_steps = nullptr, McTable* table = nullptr,
-               const int32_t* d_live = nullptr);  // d_live[j] == 0: skip trajectory j (table path; hits stay 0)
+               const int32_t* d_live = nullptr,  // d_live[j] == 0: skip trajectory j (table path; hits stay 0)
+               bool lists_ready = false);  // the caller wrote the table's step lists (mc_step_row)
 
 }  // namespace pumpg

@@ -605,7 +605,6 @@ constexpr int kMcChunk = 8;   // steps whose table rows a thread loads up front
 // by the sub-segment rounding margin; the inflated obstacles meeting it, a
 // warp per step (ballot compaction).  A step with an empty list whose box is
 // inside the workspace holds no failing test for any rollout: skip = 1.
-constexpr int kStepCap = 64;  // candidate obstacles per step (more: nl = -1, test all)
 template <int DW>
 __global__ void __launch_bounds__(128) k_mc_steps(WorldD w, const int64_t* __restrict__ traj_off,
                                                   const double* __restrict__ ynom_all,
@@ -619,51 +618,9 @@ __global__ void __launch_bounds__(128) k_mc_steps(WorldD w, const int64_t* __res
   const int64_t p_begin = traj_off[j];
   const int T = static_cast<int>(traj_off[j + 1] - p_begin) - 1;
   if (t > T) return;
-  double bl[DW], bh[DW];
-  bool inside = true;
-#pragma unroll
-  for (int k = 0; k < DW; ++k) {
-    const double m1 = __longlong_as_double(static_cast<long long>(maxdev[t * DW + k]));
-    const double y1 = ynom_all[(p_begin + t) * DW + k];
-    double lo = y1 - m1, hi = y1 + m1;
-    if (t > 0) {
-      const double m0 = __longlong_as_double(static_cast<long long>(maxdev[(t - 1) * DW + k]));
-      const double y0 = ynom_all[(p_begin + t - 1) * DW + k];
-      const double lo0 = y0 - m0, hi0 = y0 + m0;
-      lo = lo0 < lo ? lo0 : lo;
-      hi = hi0 > hi ? hi0 : hi;
-    }
-    const double mg = 1e-12 * (1.0 + (lo < 0 ? -lo : lo) + (hi < 0 ? -hi : hi));
-    bl[k] = lo - mg;
-    bh[k] = hi + mg;
-    inside = inside && bl[k] > w.blo[k] && bh[k] < w.bhi[k];
-  }
-  const int64_t row = static_cast<int64_t>(j) * t_stride + t;
-  int nl = 0;
-  for (int o0 = 0; o0 < w.n_obs; o0 += 32) {
-    const int o = o0 + lane;
-    bool meet = false;
-    if (o < w.n_obs) {
-      bool sep = false;
-#pragma unroll
-      for (int k = 0; k < DW; ++k) {
-        const double bl_o = w.blo[k] < 0 ? -w.blo[k] : w.blo[k], bh_o = w.bhi[k] < 0 ? -w.bhi[k] : w.bhi[k];
-        const double lo = w.lo[o * DW + k], hi = w.hi[o * DW + k];
-        const double M = 1e-9 * (1.0 + (lo < 0 ? -lo : lo) + (hi < 0 ? -hi : hi) + 2.0 * (bl_o > bh_o ? bl_o : bh_o));
-        sep = sep || (bh[k] < lo - M) || (bl[k] > hi + M);
-      }
-      meet = !sep;
-    }
-    const unsigned bal = __ballot_sync(0xffffffffu, meet);
-    const int at = nl + __popc(bal & ((1u << lane) - 1u));
-    if (meet && at < kStepCap) g_list[row * kStepCap + at] = static_cast<uint16_t>(o);
-    nl += __popc(bal);
-  }
-  if (nl > kStepCap) nl = -1;
-  if (lane == 0) {
-    g_nl[row] = nl;
-    g_skip[row] = (inside && nl == 0) ? 1 : 0;
-  }
+  const double* y1 = ynom_all + (p_begin + t) * DW;
+  mc_step_row<DW, kStepCap>(w, y1, t > 0 ? y1 - DW : nullptr, maxdev, t, static_cast<int64_t>(j) * t_stride + t, lane, g_list,
+                  g_nl, g_skip);
 }
 
 template <int DW, int kMcSub>  // kMcSub sub-chunks per block: a block spans kMcSpan steps
@@ -968,6 +925,13 @@ static bool ensure_table(McTable& tab, const HostLoop& HL, int64_t r0, int64_t r
   return true;
 }
 
+void mc_step_buffers(McTable& tab, int n_traj, int max_points) {
+  const size_t rows_all = static_cast<size_t>(n_traj) * max_points;
+  tab.step_list.ensure(rows_all * kStepCap * 2 + 256);
+  tab.step_nl.ensure(rows_all * 4 + 256);
+  tab.step_skip.ensure(rows_all + 256);
+}
+
 bool mc_table_covers(const McTable& tab, const HostLoop& HL, int64_t r0, int64_t r1, uint64_t seed, int T) {
   return tab.valid && tab.seed == seed && tab.r0 == r0 && tab.r1 == r1 && T <= tab.t_done && same_loop(tab.L, HL);
 }
@@ -983,17 +947,16 @@ void mc_table_prepare(McTable& tab, const HostLoop& HL, int64_t r0, int64_t r1, 
 void launch_mc(const HostLoop& HL, const DevWorld& w, int n_traj, const int64_t* d_traj_off, const double* d_ynom,
                int max_points, int64_t r0, int64_t r1, uint64_t seed, double eps_cc, unsigned long long* d_hits,
                cudaStream_t st, int64_t* launches, unsigned long long* d_steps, McTable* table,
-               const int32_t* d_live) {
+               const int32_t* d_live, bool lists_ready) {
   if (r1 <= r0 || n_traj <= 0) return;
   if (HL.dw != w.dw) throw std::invalid_argument("mc_certify: workspace / model dimension mismatch");
   static const bool direct = std::getenv("PUMP_MC_DIRECT") != nullptr;
   // Large certifications (SURVEY config 4: up to 1e7 rollouts) go through the
   // table in rollout chunks; each chunk's hits accumulate into d_hits.
-  constexpr int64_t kTabRollouts = int64_t(1) << 19;
   if (table && !direct && r1 - r0 > kTabRollouts) {
     for (int64_t c0 = r0; c0 < r1; c0 += kTabRollouts)
       launch_mc(HL, w, n_traj, d_traj_off, d_ynom, max_points, c0, std::min(r1, c0 + kTabRollouts), seed, eps_cc,
-                d_hits, st, launches, d_steps, table, d_live);
+                d_hits, st, launches, d_steps, table, d_live);  // (lists per chunk: each chunk's table)
     return;
   }
   if (table && !direct && ensure_table(*table, HL, r0, r1, seed, max_points - 1, st, launches)) {
@@ -1010,14 +973,13 @@ void launch_mc(const HostLoop& HL, const DevWorld& w, int n_traj, const int64_t*
     PUMP_CUDA(cudaMemsetAsync(table->flags.p, 0, static_cast<size_t>(n) * n_traj * 4, st));
     dispatch_dw(HL.dw, [&]<int DW>() {
       // per-(trajectory, step) candidate lists, once per certification
-      const size_t rows_all = static_cast<size_t>(n_traj) * max_points;
-      table->step_list.ensure(rows_all * kStepCap * 2 + 256);
-      table->step_nl.ensure(rows_all * 4 + 256);
-      table->step_skip.ensure(rows_all + 256);
-      k_mc_steps<DW><<<dim3((max_points + 3) / 4, n_traj), 128, 0, st>>>(
-          wd, d_traj_off, d_ynom, table->maxdev.as<unsigned long long>(), max_points,
-          table->step_list.as<uint16_t>(), table->step_nl.as<int32_t>(), table->step_skip.as<uint8_t>(), d_live);
-      ++*launches;
+      mc_step_buffers(*table, n_traj, max_points);
+      if (!lists_ready) {
+        k_mc_steps<DW><<<dim3((max_points + 3) / 4, n_traj), 128, 0, st>>>(
+            wd, d_traj_off, d_ynom, table->maxdev.as<unsigned long long>(), max_points,
+            table->step_list.as<uint16_t>(), table->step_nl.as<int32_t>(), table->step_skip.as<uint8_t>(), d_live);
+        ++*launches;
+      }
       auto go = [&]<int SUB>() {
         constexpr int span = kMcChunk * SUB;
         const size_t smem = (static_cast<size_t>(span + 1) * DW + 4 * static_cast<size_t>(w.n_obs) * DW) * sizeof(double);
