@@ -1202,31 +1202,24 @@ __global__ void __launch_bounds__(kCoopBlock, 2) k_round_tail(const CoopArgs A) 
   }
   grid_sync(A.bar);
   STAMP();
-  // end-of-round bookkeeping and the next threshold (k_round_i)
+  // end-of-round bookkeeping and the next threshold (k_round_i): every
+  // thread derives the values the selection needs from the status (final
+  // after the barrier above); thread 0 records them after the next barrier,
+  // when no block reads the old ones any more
   const int64_t NS = A.spos[K];
-  if (gtid == 0) {
-    S->n_surv = NS;
-    S->pool_n += NS;
-    S->open_count += NS - S->evicted_open - S->G;
-    S->n_plans += K;
-    long long i = S->i + 1;
-    if (S->min_bucket != LLONG_MAX && S->min_bucket > i) i = S->min_bucket;
-    S->i = i;
-    const long long limit = i < S->max_bucket ? i : S->max_bucket;
-    A.limits[0] = limit;
-    A.limits[1] = S->min_bucket == LLONG_MAX ? 0 : S->min_bucket;
-    *A.d_pool_n = S->pool_n;
-    S->G = 0;
-    S->T = 0;
-    S->min_group_bits = 0x7ff0000000000000ll;
-    S->touched = 0;
-    S->evicted_open = 0;
-  }
-  grid_sync(A.bar);
+  const long long pool_n_new = S->pool_n + NS;
+  const long long min_b = S->min_bucket, max_b = S->max_bucket;
+  long long i_new = S->i + 1;
+  if (min_b != LLONG_MAX && min_b > i_new) i_new = min_b;
+  const long long lim0 = i_new < max_b ? i_new : max_b, lim1 = min_b == LLONG_MAX ? 0 : min_b;
+  const long long open_new = S->open_count + NS - S->evicted_open - S->G, n_plans_new = S->n_plans + K;
   STAMP();
-  // bucket selection (k_select) fused into the stay scan; stayers compacted
-  const int64_t m = *A.d_pool_n;
-  const int64_t lim0 = A.limits[0], lim1 = A.limits[1];
+  // bucket selection (k_select) fused into the stay scan; stayers compacted;
+  // the multisplit's per-block key histogram over the scan's own chunk
+  const int64_t m = pool_n_new;
+  const int nk = static_cast<int>(n_keys);
+  for (int k = threadIdx.x; k < nk; k += blockDim.x) s_hist[k] = 0;
+  __syncthreads();
   coop_scan(
       m,
       [&](int64_t x, int pass) -> int64_t {
@@ -1238,6 +1231,7 @@ __global__ void __launch_bounds__(kCoopBlock, 2) k_round_tail(const CoopArgs A) 
           const int64_t key = b - lim1;
           if (sel && key >= n_keys) atomicExch(reinterpret_cast<unsigned long long*>(&S->err), 3ull);
           A.keys[x] = sel ? static_cast<int32_t>(key) : -1;
+          if (sel && key < n_keys) atomicAdd(&s_hist[key], 1);
         }
         return (open && !sel) ? 1 : 0;
       },
@@ -1245,23 +1239,31 @@ __global__ void __launch_bounds__(kCoopBlock, 2) k_round_tail(const CoopArgs A) 
         if (v) A.pool_nxt[ex] = A.pool_cur[x];
       },
       A.stay_pos, A.scan_status, ep++, red, &s_pre);
-  grid_sync(A.bar);
-  const int64_t stay_n = A.stay_pos[m];
-  STAMP();
-  // stable multisplit by key (one radix pass, keys < n_keys <= 512):
-  // per-block histograms over contiguous chunks, key-major scan, ordered scatter
-  const int64_t chunk = (m + nb - 1) / nb;
-  const int64_t lo = min(m, static_cast<int64_t>(blockIdx.x) * chunk), hi = min(m, lo + chunk);
-  const int nk = static_cast<int>(n_keys);
-  for (int k = threadIdx.x; k < nk; k += blockDim.x) s_hist[k] = 0;
-  __syncthreads();
-  for (int64_t x = lo + threadIdx.x; x < hi; x += blockDim.x) {
-    const int key = A.keys[x];
-    if (key >= 0) atomicAdd(&s_hist[key], 1);
-  }
   __syncthreads();
   for (int k = threadIdx.x; k < nk; k += blockDim.x) A.ms_counts[static_cast<int64_t>(k) * nb + blockIdx.x] = s_hist[k];
   grid_sync(A.bar);
+  const int64_t stay_n = A.stay_pos[m];
+  if (gtid == 0) {
+    S->n_surv = NS;
+    S->pool_n = pool_n_new;
+    S->open_count = open_new;
+    S->n_plans = n_plans_new;
+    S->i = i_new;
+    A.limits[0] = lim0;
+    A.limits[1] = lim1;
+    *A.d_pool_n = pool_n_new;
+    S->G = 0;
+    S->T = 0;
+    S->min_group_bits = 0x7ff0000000000000ll;
+    S->touched = 0;
+    S->evicted_open = 0;
+  }
+  STAMP();
+  // stable multisplit by key (one radix pass, keys < n_keys <= 512): the
+  // per-block histograms (above, over the scan's contiguous chunks), key-major
+  // scan, ordered scatter
+  const int64_t chunk = (m + nb - 1) / nb;
+  const int64_t lo = min(m, static_cast<int64_t>(blockIdx.x) * chunk), hi = min(m, lo + chunk);
   STAMP();
   coop_scan(
       static_cast<int64_t>(nk) * nb, [&](int64_t i, int) -> int64_t { return A.ms_counts[i]; },
