@@ -1265,14 +1265,45 @@ __global__ void __launch_bounds__(kCoopBlock, 2) k_round_tail(const CoopArgs A) 
   const int64_t chunk = (m + nb - 1) / nb;
   const int64_t lo = min(m, static_cast<int64_t>(blockIdx.x) * chunk), hi = min(m, lo + chunk);
   STAMP();
-  coop_scan(
-      static_cast<int64_t>(nk) * nb, [&](int64_t i, int) -> int64_t { return A.ms_counts[i]; },
-      [](int64_t, int64_t, int64_t) {}, A.ms_offs, A.scan_status, ep++, red, &s_pre);
-  grid_sync(A.bar);
-  const int64_t Gn = A.ms_offs[static_cast<int64_t>(nk) * nb];
+  int64_t Gn = 0;
+  if (nk <= 32) {
+    // few keys: each block derives its own run starts (key k's total over the
+    // blocks and the part before this block, then the keys' exclusive scan)
+    // from the counts directly, with no grid-wide scan and barrier
+    __shared__ int64_t s_ktot[32], s_kpre[32], s_gn;
+    for (int k = wib; k < nk; k += kCoopBlock / 32) {
+      int64_t tot = 0, pre = 0;
+      for (int b2 = lane; b2 < nb; b2 += 32) {
+        const int cnt = A.ms_counts[static_cast<int64_t>(k) * nb + b2];
+        tot += cnt;
+        pre += b2 < static_cast<int>(blockIdx.x) ? cnt : 0;
+      }
+      tot = warp_sum(tot);
+      pre = warp_sum(pre);
+      if (lane == 0) {
+        s_ktot[k] = tot;
+        s_kpre[k] = pre;
+      }
+    }
+    __syncthreads();
+    if (wib == 0) {
+      const int64_t t = lane < nk ? s_ktot[lane] : 0;
+      const int64_t inc = warp_incl_scan(t);
+      if (lane < nk) s_run[lane] = inc - t + s_kpre[lane];
+      if (lane == 31) s_gn = inc;
+    }
+    __syncthreads();
+    Gn = s_gn;
+  } else {
+    coop_scan(
+        static_cast<int64_t>(nk) * nb, [&](int64_t i, int) -> int64_t { return A.ms_counts[i]; },
+        [](int64_t, int64_t, int64_t) {}, A.ms_offs, A.scan_status, ep++, red, &s_pre);
+    grid_sync(A.bar);
+    Gn = A.ms_offs[static_cast<int64_t>(nk) * nb];
+    for (int k = threadIdx.x; k < nk; k += blockDim.x) s_run[k] = A.ms_offs[static_cast<int64_t>(k) * nb + blockIdx.x];
+    __syncthreads();
+  }
   STAMP();
-  for (int k = threadIdx.x; k < nk; k += blockDim.x) s_run[k] = A.ms_offs[static_cast<int64_t>(k) * nb + blockIdx.x];
-  __syncthreads();
   if (wib == 0) {
     const unsigned lt = (1u << lane) - 1u;
     for (int64_t base = lo; base < hi; base += 32) {
