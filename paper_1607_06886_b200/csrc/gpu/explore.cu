@@ -1184,6 +1184,9 @@ __global__ void __launch_bounds__(kCoopBlock, 2) k_round_tail(const CoopArgs A) 
   const int64_t pool_old = S->pool_n;
   const int32_t* bucket = A.cm.bucket;
   uint8_t* flags = A.cm.flags;
+  // (bucket extremes reduced per thread, then per warp: one atomic per warp
+  // instead of one per plan on a single address)
+  int b_min = INT_MAX, b_max = INT_MIN;
   coop_scan(
       K, [&](int64_t r, int) -> int64_t { return A.surv[r]; },
       [&](int64_t r, int64_t ex, int64_t v) {
@@ -1191,14 +1194,20 @@ __global__ void __launch_bounds__(kCoopBlock, 2) k_round_tail(const CoopArgs A) 
           const int64_t id = P0 + r;
           A.pool_cur[pool_old + ex] = static_cast<int32_t>(id);
           flags[id] |= kOpen;
-          atomicMax(&S->max_bucket, static_cast<long long>(bucket[id]));
-          atomicMin(&S->min_bucket, static_cast<long long>(bucket[id]));
+          b_max = max(b_max, bucket[id]);
+          b_min = min(b_min, bucket[id]);
         }
       },
       A.spos, A.scan_status, ep++, red, &s_pre);
   for (int64_t x = gtid; x < pool_old; x += gthreads) {
     const int id = A.pool_cur[x];
-    if (flags[id] & kOpen) atomicMin(&S->min_bucket, static_cast<long long>(bucket[id]));
+    if (flags[id] & kOpen) b_min = min(b_min, bucket[id]);
+  }
+  b_min = __reduce_min_sync(0xffffffffu, b_min);
+  b_max = __reduce_max_sync(0xffffffffu, b_max);
+  if (lane == 0) {
+    if (b_min != INT_MAX) atomicMin(&S->min_bucket, static_cast<long long>(b_min));
+    if (b_max != INT_MIN) atomicMax(&S->max_bucket, static_cast<long long>(b_max));
   }
   grid_sync(A.bar);
   STAMP();
@@ -1321,6 +1330,7 @@ __global__ void __launch_bounds__(kCoopBlock, 2) k_round_tail(const CoopArgs A) 
   grid_sync(A.bar);
   STAMP();
   // the new group: close it, its degrees -> task offsets, cheapest cost
+  long long g_min = LLONG_MAX;  // (the costs are non-negative: their bits order like the values)
   const int64_t Tn_last = coop_scan(
       Gn,
       [&](int64_t g, int pass) -> int64_t {
@@ -1328,11 +1338,18 @@ __global__ void __launch_bounds__(kCoopBlock, 2) k_round_tail(const CoopArgs A) 
         const int hv = A.ex.head[id];
         if (pass) {
           flags[id] &= static_cast<uint8_t>(~kOpen);
-          atomicMin(&S->min_group_bits, __double_as_longlong(A.cm.cost[id]));
+          const long long cb = __double_as_longlong(A.cm.cost[id]);
+          g_min = cb < g_min ? cb : g_min;
         }
         return A.row_ptr[hv + 1] - A.row_ptr[hv];
       },
       [](int64_t, int64_t, int64_t) {}, A.task_off, A.scan_status, ep++, red, &s_pre);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const long long t = __shfl_xor_sync(0xffffffffu, g_min, o);
+    g_min = t < g_min ? t : g_min;
+  }
+  if (lane == 0 && g_min != LLONG_MAX) atomicMin(&S->min_group_bits, g_min);
   if (blockIdx.x == gridDim.x - 1 && threadIdx.x == 0) {  // the scan's last block holds the total
     S->G = Gn;
     S->T = Tn_last;
