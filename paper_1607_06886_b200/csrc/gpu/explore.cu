@@ -21,6 +21,7 @@
 #include <climits>
 #include <cstdio>
 #include <cstdlib>
+#include <utility>
 
 #include "dispatch.cuh"
 #include <cooperative_groups.h>
@@ -104,6 +105,13 @@ __device__ __forceinline__ void load_row(const double* row, int N, int lane, dou
 }
 
 constexpr int kExpBlock = 256;
+
+// Programmatic dependent launch: the per-round chain (gate, task map, expand,
+// cooperative tail) is enqueued with programmatic stream serialization, so a
+// kernel's launch and block ramp overlap its predecessor's last blocks; each
+// of them waits here for its predecessor's completion (and memory) before it
+// reads anything.  A no-op for a kernel launched without the attribute.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 constexpr int kExpStage = 64;  // half-spaces staged per warp (2 KB of shared memory)
 
 // One warp per task (planner.hpp:140-176): the parent plan's particle mask is
@@ -339,6 +347,7 @@ __global__ void __launch_bounds__(kExpBlock, (CH <= 2 ? 4 : 2)) k_expand(const E
   __shared__ double2 s_hs[kExpBlock / 32][kExpStage][2];
   const int64_t task = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  pdl_wait();
   // (a pipelined round's grid covers its task capacity; a halted round has none)
   if (task >= *a.d_T || a.st->halt) return;
   expand_task<DW, CH>(a, task, lane, wib, s_hs);
@@ -782,6 +791,7 @@ __global__ void k_group_post(const int64_t* d_G, const int32_t* group, const int
 __global__ void k_task_map(const int64_t* d_G, const int64_t* task_off, const int32_t* group, const int32_t* head,
                            const int64_t* row_ptr, int32_t* task_pid, int64_t* task_e, const ExploreStatus* st) {
   const int lane = threadIdx.x & 31;
+  pdl_wait();
   if (st->halt) return;
   const int64_t Gn = *d_G;
   const int64_t stride = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
@@ -805,6 +815,7 @@ struct GateCaps {
   long long T, arena, pool;
 };
 __global__ void k_round_gate(ExploreStatus* S, GateCaps cap) {
+  pdl_wait();
   if (S->halt) return;
   const double best_goal = __longlong_as_double(S->best_goal_bits);
   const double min_group = __longlong_as_double(S->min_group_bits);
@@ -1084,6 +1095,7 @@ __global__ void __launch_bounds__(kCoopBlock, 2) k_round_tail(const CoopArgs A) 
     }
     ++stamp_i;
   };
+  pdl_wait();
   STAMP();
   if (S->halt) return;  // pipelined round that does not run (uniform: the gate ran before this launch)
   const int64_t n_keys = A.n_keys > 0 ? A.n_keys : S->n_keys;
@@ -1471,6 +1483,32 @@ __global__ void k_explore_init(int n, int W, int N, int ng, const int32_t* __res
   }
 }
 
+// a round's kernels after the first: programmatic stream serialization (see
+// pdl_wait), plus the cooperative attribute for the round tail
+template <class... KArgs, class... Args>
+static void launch_round(void (*k)(KArgs...), dim3 grid, dim3 block, cudaStream_t st, bool coop, Args&&... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = st;
+  cudaLaunchAttribute at[2];
+  int na = 0;
+#ifndef PUMP_NO_PDL
+  at[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[na].val.programmaticStreamSerializationAllowed = 1;
+  ++na;
+#endif
+  if (coop) {
+    at[na].id = cudaLaunchAttributeCooperative;
+    at[na].val.cooperative = 1;
+    ++na;
+  }
+  cfg.attrs = at;
+  cfg.numAttrs = na;
+  PUMP_CUDA(cudaLaunchKernelEx(&cfg, k, std::forward<Args>(args)...));
+}
+
 void run_explore_device(DevExplore& X, Ctx& c, const DevGraph& G, const ExploreArgs& prm) {
   if (!c.bank.p) throw std::invalid_argument("explore: no particle bank in this context");
   if (c.bank_dw != G.dw) throw std::invalid_argument("explore: bank / graph dimension mismatch");
@@ -1642,7 +1680,7 @@ void run_explore_device(DevExplore& X, Ctx& c, const DevGraph& G, const ExploreA
       // ---- one cooperative launch for the whole round
       if (pipe) {
         const GateCaps caps{T, X.cap, pool_ub};
-        k_round_gate<<<1, 1, 0, st>>>(S, caps);
+        launch_round(k_round_gate, dim3(1), dim3(1), st, false, S, caps);
         ++c.launches;
       }
       X.task_grp.ensure(al((T + 1) * 4));
@@ -1659,7 +1697,9 @@ void run_explore_device(DevExplore& X, Ctx& c, const DevGraph& G, const ExploreA
       DBuf& new_ids = X.mem_flip ? X.mem_a : X.mem_b;
       DBuf& pool_cur = X.pool_flip ? X.pool_b : X.pool_a;
       DBuf& pool_nxt = X.pool_flip ? X.pool_a : X.pool_b;
-      PUMP_CUDA(cudaMemsetAsync(bar.p, 0, 8, st));
+#ifdef PUMP_OWN_GRID_BAR
+      PUMP_CUDA(cudaMemsetAsync(bar.p, 0, 8, st));  // (the cooperative-groups barrier needs no state)
+#endif
       CoopArgs A{};
       A.ex = ExpandArgs{X.group.as<int32_t>(), X.task_off.as<int64_t>(), X.task_grp.as<int32_t>(), X.task_e.as<int64_t>(), d_G, d_T,
                         G.row_ptr.as<int64_t>(), G.e_to.as<int32_t>(), G.e_cost.as<double>(),
@@ -1715,29 +1755,30 @@ void run_explore_device(DevExplore& X, Ctx& c, const DevGraph& G, const ExploreA
       DBuf& stamps = c.buf("x_coop_stamps", 64 * 8);
       A.stamps = dbg_coop ? stamps.as<unsigned long long>() : nullptr;
       const int64_t grid_cap = static_cast<int64_t>(coop_blocks) * 8;
-      k_task_map<<<pipe ? static_cast<unsigned>(std::min<int64_t>(grid_for(pool_ub * 32, 256), grid_cap))
-                        : grid_for(h.G * 32, 256),
-                   256, 0, st>>>(d_G, X.task_off.as<int64_t>(), X.group.as<int32_t>(), X.head.as<int32_t>(),
-                                 G.row_ptr.as<int64_t>(), X.task_grp.as<int32_t>(), X.task_e.as<int64_t>(), S);
+      launch_round(k_task_map,
+                   dim3(pipe ? static_cast<unsigned>(std::min<int64_t>(grid_for(pool_ub * 32, 256), grid_cap))
+                             : grid_for(h.G * 32, 256)),
+                   dim3(256), st, false, static_cast<const int64_t*>(d_G), X.task_off.as<int64_t>(),
+                   X.group.as<int32_t>(), X.head.as<int32_t>(), G.row_ptr.as<int64_t>(), X.task_grp.as<int32_t>(),
+                   X.task_e.as<int64_t>(), static_cast<const ExploreStatus*>(S));
       ++c.launches;
       {
         const unsigned grid = grid_for(T * 32, 256);  // pipelined: T is the per-round task capacity
         KScope ks(st, F_EXPAND);
         dispatch_dw(G.dw, [&]<int DW>() {
           switch (ch) {
-            case 1: k_expand<DW, 1><<<grid, 256, 0, st>>>(A.ex); break;
-            case 2: k_expand<DW, 2><<<grid, 256, 0, st>>>(A.ex); break;
-            case 4: k_expand<DW, 4><<<grid, 256, 0, st>>>(A.ex); break;
-            case 8: k_expand<DW, 8><<<grid, 256, 0, st>>>(A.ex); break;
-            default: k_expand<DW, 16><<<grid, 256, 0, st>>>(A.ex); break;
+            case 1: launch_round(k_expand<DW, 1>, dim3(grid), dim3(256), st, false, A.ex); break;
+            case 2: launch_round(k_expand<DW, 2>, dim3(grid), dim3(256), st, false, A.ex); break;
+            case 4: launch_round(k_expand<DW, 4>, dim3(grid), dim3(256), st, false, A.ex); break;
+            case 8: launch_round(k_expand<DW, 8>, dim3(grid), dim3(256), st, false, A.ex); break;
+            default: launch_round(k_expand<DW, 16>, dim3(grid), dim3(256), st, false, A.ex); break;
           }
         });
         ++c.launches;
       }
       {
         KScope ks(st, F_COMMIT);
-        void* args[] = {&A};
-        PUMP_CUDA(cudaLaunchCooperativeKernel(coop_fn, dim3(coop_blocks), dim3(kCoopBlock), args, 0, st));
+        launch_round(k_round_tail, dim3(coop_blocks), dim3(kCoopBlock), st, true, A);
       }
       ++c.launches;
       PUMP_CUDA(cudaGetLastError());
