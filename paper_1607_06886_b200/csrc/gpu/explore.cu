@@ -35,6 +35,8 @@ constexpr int kOpen = 1;
 
 DevExplore::~DevExplore() {
   if (status_h) cudaFreeHost(status_h);
+  for (cudaEvent_t e : status_ev)
+    if (e) cudaEventDestroy(e);
 }
 
 struct ExpandArgs {
@@ -1412,11 +1414,12 @@ static void swap_buf(DBuf& a, DBuf& b) {
 // ------------------------------------------------------------------ host
 static inline size_t al(size_t x) { return (x + 255) & ~size_t(255); }
 
-static void ensure_arena(DevExplore& X, int64_t need, cudaStream_t st) {
+// keep_all: a round in flight may commit plans past X.n_plans, keep them all
+static void ensure_arena(DevExplore& X, int64_t need, cudaStream_t st, bool keep_all = false) {
   if (need <= X.cap) return;
   int64_t cap = X.cap ? X.cap : 1 << 16;
   while (cap < need) cap += cap / 2 + 1024;
-  const int64_t old = X.n_plans;
+  const int64_t old = keep_all ? X.cap : X.n_plans;
   X.head.grow(al(cap * 4), old * 4, st);
   X.parent.grow(al(cap * 4), old * 4, st);
   X.cost.grow(al(cap * 8), old * 8, st);
@@ -1531,7 +1534,9 @@ void run_explore_device(DevExplore& X, Ctx& c, const DevGraph& G, const ExploreA
   X.n_plans = 0;  // buffers (and their capacity) persist across solves
   const int count_hs = (kprof_current() && kprof_current()->on) ? 1 : 0;
   ensure_arena(X, 1 << 16, st);
-  if (!X.status_h) PUMP_CUDA(cudaMallocHost(&X.status_h, sizeof(ExploreStatus)));
+  if (!X.status_h) PUMP_CUDA(cudaMallocHost(&X.status_h, 3 * sizeof(ExploreStatus)));
+  for (cudaEvent_t& e : X.status_ev)
+    if (!e) PUMP_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   X.status_d.ensure(al(sizeof(ExploreStatus)) + 256);
   ExploreStatus* S = X.status_d.as<ExploreStatus>();
   int64_t* d_scal = reinterpret_cast<int64_t*>(reinterpret_cast<char*>(X.status_d.p) + al(sizeof(ExploreStatus)));
@@ -1617,23 +1622,72 @@ void run_explore_device(DevExplore& X, Ctx& c, const DevGraph& G, const ExploreA
   c.tic();
   ExploreStatus h_hook{};
   bool hook_pending = false;
+  // Window (per-round hook, run_pump): gated rounds as in a batch, but the
+  // host keeps one round in flight and consumes the status of the round
+  // before it (copied into a pinned slot behind that round), so the device
+  // never idles while the host reads a status, runs the hook and enqueues the
+  // next round.  A halt (termination or capacity) stops the window: the round
+  // in flight halts too and is drained before the host goes on.
+  const bool window = coop_ok && kBatch > 1 && prm.on_round && !prm.on_round_batched && !prm.on_round_state;
+  bool inflight = false;
+  int in_slot = 0, next_slot = 0;
+  // a gated round's status: rounds that ran, undo the flips of one that did
+  // not, clear a halt; true when the round (or an earlier one) halted
+  auto win_consume = [&](const ExploreStatus& hs) {
+    const ExploreStatus hp = h;
+    h = hs;
+    X.n_plans = h.n_plans;
+    if (h.err) throw std::runtime_error("explore: device error " + std::to_string(h.err));
+    const long long ran = h.rounds - hp.rounds;
+    if (ran == 0) {
+      swap_buf(X.mem_off, off2);
+      X.mem_flip = !X.mem_flip;
+      X.pool_flip = !X.pool_flip;
+    }
+    X.rounds += static_cast<int>(ran);
+    X.partial_plans += h.partial_plans - hp.partial_plans;
+    bool halted = false;
+    if (h.halt) {
+      if (h.halt == 2) force_sync = true;
+      h.halt = 0;
+      const long long zero = 0;
+      c.h2d(&S->halt, &zero, 8);
+      halted = true;
+    }
+    prm.on_round(h);
+    return halted;
+  };
+  auto win_drain = [&]() {
+    PUMP_CUDA(cudaEventSynchronize(X.status_ev[in_slot]));
+    win_consume(X.status_h[1 + in_slot]);
+    inflight = false;
+  };
   for (;;) {
     // loop-top termination (planner.hpp:126-138); h is the status after the
     // previous collection
     const double best_goal = __builtin_bit_cast(double, h.best_goal_bits);
     const double min_group = __builtin_bit_cast(double, h.min_group_bits);
     if (h.G > 0 && best_goal != __builtin_inf() && best_goal <= min_group) {
+      if (inflight) {  // (its gate halts it: drain, then decide on its status)
+        win_drain();
+        continue;
+      }
       X.termination = 0;
       break;
     }
     if (h.G == 0 && h.open_count == 0) {
+      if (inflight) {
+        win_drain();
+        continue;
+      }
       X.termination = best_goal == __builtin_inf() ? 1 : 0;
       break;
     }
     const int64_t Th = h.T;
     max_T = std::max<int64_t>(max_T, Th);
-    const bool pipe = coop_ok && kBatch > 1 && (!prm.on_round || prm.on_round_batched) && !prm.on_round_state &&
-                      !force_sync;
+    const bool pipe = coop_ok && kBatch > 1 && (!prm.on_round || prm.on_round_batched || window) &&
+                      !prm.on_round_state && !force_sync;
+    const bool win = window && pipe;
     std::vector<int32_t> expanded;  // (round hook) this round's group
     if (prm.on_round_state) {
       expanded.resize(h.G);
@@ -1643,12 +1697,13 @@ void run_explore_device(DevExplore& X, Ctx& c, const DevGraph& G, const ExploreA
     force_sync = false;
     // buffer sizes: this round's T, or a per-round capacity for a batch
     const int64_t T = pipe ? std::max<int64_t>({Th, 2 * max_T, 4096}) : Th;
-    const int64_t nrounds = pipe ? kBatch : 1;
+    const int64_t nrounds = win ? 1 : pipe ? kBatch : 1;
+    const int64_t ahead = win ? 2 : nrounds;  // rounds past the status h the buffers must hold
     if (!pipe) {
       X.rounds++;
       X.partial_plans += Th;
     }
-    ensure_arena(X, X.n_plans + (pipe ? kBatch * T / 2 : T) + 1, st);
+    ensure_arena(X, X.n_plans + (win ? 2 * T : pipe ? kBatch * T / 2 : T) + 1, st, inflight);
     // candidate buffers
     X.cand_keep.ensure(al(T + 1));
     X.cand_head.ensure(al((T + 1) * 4));
@@ -1675,7 +1730,7 @@ void run_explore_device(DevExplore& X, Ctx& c, const DevGraph& G, const ExploreA
     if (pipe || (coop_ok && T > 0 && n_keys_r <= kCoopKeys)) {
      ran_coop = true;
      const long long rounds0 = h.rounds;  // (pipelined: the status counts the rounds that ran)
-     const int64_t pool_ub = h.pool_n + (pipe ? kBatch * T : T) + 1;
+     const int64_t pool_ub = h.pool_n + (pipe ? ahead * T : T) + 1;
      for (int64_t rr = 0; rr < nrounds; ++rr) {
       // ---- one cooperative launch for the whole round
       if (pipe) {
@@ -1685,8 +1740,9 @@ void run_explore_device(DevExplore& X, Ctx& c, const DevGraph& G, const ExploreA
       }
       X.task_grp.ensure(al((T + 1) * 4));
       X.task_e.ensure(al((T + 1) * 8));
-      X.group.grow(al((pool_ub + 1) * 4), static_cast<size_t>(h.G) * 4, st);
-      X.task_off.grow(al((pool_ub + 2) * 8), static_cast<size_t>(h.G + 1) * 8, st);
+      // (a round in flight may be writing the next group: keep everything)
+      X.group.grow(al((pool_ub + 1) * 4), inflight ? X.group.cap : static_cast<size_t>(h.G) * 4, st);
+      X.task_off.grow(al((pool_ub + 2) * 8), inflight ? X.task_off.cap : static_cast<size_t>(h.G + 1) * 8, st);
       DBuf& keys = c.buf("x_sel_keys", al((pool_ub + 1) * 4));
       DBuf& stay_pos = c.buf("x_stay_pos", al((pool_ub + 2) * 8));
       DBuf& msc = c.buf("x_coop_counts", al(static_cast<size_t>(kCoopKeys) * coop_blocks * 4));
@@ -1928,6 +1984,22 @@ void run_explore_device(DevExplore& X, Ctx& c, const DevGraph& G, const ExploreA
     if (hook_pending) {
       prm.on_round(h_hook);
       hook_pending = false;
+    }
+    if (win) {
+      const int sl = next_slot;
+      next_slot ^= 1;
+      c.d2h(X.status_h + 1 + sl, S, sizeof(ExploreStatus));
+      PUMP_CUDA(cudaEventRecord(X.status_ev[sl], st));
+      if (inflight) {
+        const int prev = in_slot;
+        in_slot = sl;
+        PUMP_CUDA(cudaEventSynchronize(X.status_ev[prev]));
+        if (win_consume(X.status_h[1 + prev])) win_drain();  // the round just enqueued halts too
+      } else {
+        in_slot = sl;
+        inflight = true;
+      }
+      continue;
     }
     c.d2h(X.status_h, S, sizeof(ExploreStatus));
     c.sync();

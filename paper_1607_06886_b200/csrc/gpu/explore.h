@@ -31,7 +31,8 @@ struct DevExplore {
   DBuf is_goal, new_cnt, touched, drop, surv, fpos;
   DBuf cand_keep, cand_head, cand_src, cand_tend, cand_cost, cand_cp, cand_mask, cand_rank, new_slot;
   DBuf status_d;
-  ExploreStatus* status_h = nullptr;  // pinned
+  ExploreStatus* status_h = nullptr;  // pinned: [0] read back synchronously, [1..2] the window's in-flight rounds
+  cudaEvent_t status_ev[2] = {nullptr, nullptr};
   // results
   int64_t n_plans = 0, partial_plans = 0, disc_cp = 0, disc_hor = 0, removed = 0, hs_tests = 0, hs_read = 0;
   int rounds = 0;
