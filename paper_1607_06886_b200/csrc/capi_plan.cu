@@ -1432,8 +1432,9 @@ static void run_pump_device(Ctx& c, const pumpb::Scenario& s, const DevGraph* pr
   mark("front mc");
   const int sel_id = sorted_ids[sel];
   std::vector<HWp> plan_sel;
+  double cph = 0.0, cst = 0.0;
   {
-    // the selected plan's node path and waypoints
+    // the selected plan's node path and waypoints, its cp_hat and cost (one readback)
     const int64_t n_wp = woff[sel + 1] - woff[sel];
     int32_t len = 0;
     c.d2h(&len, c.scratch["p_lens"].as<int32_t>() + sel, 4);
@@ -1444,6 +1445,8 @@ static void run_pump_device(Ctx& c, const pumpb::Scenario& s, const DevGraph* pr
     c.d2h(wpv.data(), c.scratch["p_wp"].as<double>() + woff[sel] * dw, n_wp * dw * 8);
     c.d2h(wvv.data(), c.scratch["p_wv"].as<double>() + woff[sel] * dw, n_wp * dw * 8);
     c.d2h(wuv.data(), c.scratch["p_wu"].as<double>() + woff[sel] * dw, n_wp * dw * 8);
+    c.d2h(&cph, X.cp.as<double>() + sel_id, 8);
+    c.d2h(&cst, X.cost.as<double>() + sel_id, 8);
     c.sync();
     R.path.assign(nodes.begin(), nodes.begin() + len);
     plan_sel.resize(n_wp);
@@ -1458,14 +1461,8 @@ static void run_pump_device(Ctx& c, const pumpb::Scenario& s, const DevGraph* pr
       }
     }
   }
-  {
-    double cph, cst;
-    c.d2h(&cph, X.cp.as<double>() + sel_id, 8);
-    c.d2h(&cst, X.cost.as<double>() + sel_id, 8);
-    c.sync();
-    R.s.cp_hat = cph;
-    R.s.pre_smoothing_cost = cst;
-  }
+  R.s.cp_hat = cph;
+  R.s.pre_smoothing_cost = cst;
   {
     SmoothOut sm = smooth_device(c, plan_sel, memo[sel], s.alpha, L, dwld, s.mc_samples, s.seeds.mc, eps_cc, dw,
                                  &R.s.mc_ms, &R.s.mc_rollouts);

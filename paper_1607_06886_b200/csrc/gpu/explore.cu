@@ -826,8 +826,11 @@ __global__ void k_round_gate(ExploreStatus* S, GateCaps cap) {
     return;
   }
   const long long T = S->T;
+  // (as the host's n_keys_r: with no open plan yet the newcomers' minimum
+  // bucket is unknown but >= 0, so i + 2 bounds the key range)
   long long nk = 1 << 18;
-  if (S->min_bucket != LLONG_MAX && S->i + 2 - S->min_bucket <= 512) nk = S->i + 2 - S->min_bucket > 1 ? S->i + 2 - S->min_bucket : 1;
+  const long long mb = S->min_bucket == LLONG_MAX ? 0 : S->min_bucket;
+  if (S->i + 2 - mb <= 512) nk = S->i + 2 - mb > 1 ? S->i + 2 - mb : 1;
   if (T <= 0 || nk > 512 || T + 1 > cap.T || S->n_plans + T + 1 > cap.arena || S->pool_n + T + 1 > cap.pool) {
     S->halt = 2;
     return;
@@ -1648,6 +1651,8 @@ void run_explore_device(DevExplore& X, Ctx& c, const DevGraph& G, const ExploreA
     X.partial_plans += h.partial_plans - hp.partial_plans;
     bool halted = false;
     if (h.halt) {
+      static const bool dbg_w = std::getenv("PUMP_DEBUG_TIMING") != nullptr;
+      if (dbg_w) std::fprintf(stderr, "[pump w] window halt %lld after round %lld\n", h.halt, h.rounds);
       if (h.halt == 2) force_sync = true;
       h.halt = 0;
       const long long zero = 0;

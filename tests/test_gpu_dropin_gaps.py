@@ -218,3 +218,20 @@ def test_out_of_memory_does_not_poison_the_context():
         assert r["success"]
     finally:
         ctx.close()
+
+
+@pytest.mark.parametrize("lam", [0.01, 0.05])
+def test_run_pump_wide_bucket_range_window_halts(oracle_lib, gpu_ctx, lam):
+    """run_pump keeps one gated explore round in flight (the per-round hook's
+    window); with a small lambda many rounds exceed the cooperative kernel's
+    512 bucket keys, so gates halt the window, the round in flight is drained
+    and the host runs those rounds synchronously before the window resumes.
+    The whole solve stays equal to the oracle's."""
+    from paper_1607_06886_b200 import api
+    from test_gpu_planner import assert_run_equal
+
+    txt = with_samples("quad3d_three_obstacle", 500, mc_samples=3000, **{"lambda": lam})
+    got = api.run_pump(api.parse_scenario(txt), ctx=gpu_ctx)
+    ref = oracle_lib.run_pump(txt, workers=WORKERS)
+    assert got["partial_plans"] > 1000
+    assert_run_equal(got, ref)
