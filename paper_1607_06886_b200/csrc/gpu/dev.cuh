@@ -932,20 +932,56 @@ __host__ __device__ __forceinline__ double clamp_sq(const WorldD& ws, int o, con
 // far (later searches) has a computed |clamp(y) - y|^2 strictly larger than
 // the current best (the margin covers every rounding on both sides), so it
 // can neither win nor tie and its distance is not evaluated.
+//
+// BoxOrder (optional, per warp, with lbs): the boxes in 32 buckets of
+// ascending lbs (a monotone bucket map, so every bound of a later bucket is
+// >= every bound of an earlier one), each bucket's smallest bound.  The
+// nearest searches then visit the boxes bucket by bucket and stop at the
+// first bucket whose smallest bound exceeds the best distance so far; ties
+// are broken by the lower box index explicitly, so the winner is the
+// reference's first strict minimum in index order.
+#ifndef PUMP_BUCKET_NEAR
+#define PUMP_BUCKET_NEAR 0
+#endif
+constexpr bool kBucketNear = PUMP_BUCKET_NEAR;  // bucketed later searches: measured slower (they visit pruned boxes)
+struct BoxOrder {
+  const uint16_t* order;  // n_obs box indices, bucket-major
+  const int* start;       // 33 bucket offsets into order
+  const float* bmin;      // 32 smallest bounds (+inf: empty)
+};
+
 template <int DW, int kW>
 __device__ __forceinline__ int convex_region_scan(const WorldD& ws, const double* y, const double* yd, double* a_out,
                                                   double* b_out, uint8_t* fb_out, int a_stride, int b_stride,
                                                   int out_cap, unsigned& n_clamp, unsigned& n_prune,
-                                                  const float* lbs = nullptr, double ub = 0.0) {
+                                                  const float* lbs = nullptr, double ub = 0.0,
+                                                  const BoxOrder* bo = nullptr) {
   n_clamp += ws.n_obs;
   int best = -1;
   double best_sq = __builtin_inf();
-  for (int o = 0; o < ws.n_obs; ++o) {
-    if (lbs && lbs[o] > ub) continue;  // warp-uniform
-    const double q = clamp_sq<DW>(ws, o, y);
-    if (q < best_sq) {
-      best_sq = q;
-      best = o;
+  if (bo) {
+    for (int bk = 0; bk < 32; ++bk) {
+      const int s0 = bo->start[bk], s1 = bo->start[bk + 1];
+      if (s0 == s1) continue;
+      if (bo->bmin[bk] > (best_sq < ub ? best_sq : ub)) break;
+      for (int x = s0; x < s1; ++x) {
+        const int o = bo->order[x];
+        if (lbs[o] > (best_sq < ub ? best_sq : ub)) continue;
+        const double q = clamp_sq<DW>(ws, o, y);
+        if (q < best_sq || (q == best_sq && o < best)) {
+          best_sq = q;
+          best = o;
+        }
+      }
+    }
+  } else {
+    for (int o = 0; o < ws.n_obs; ++o) {
+      if (lbs && lbs[o] > ub) continue;  // warp-uniform
+      const double q = clamp_sq<DW>(ws, o, y);
+      if (q < best_sq) {
+        best_sq = q;
+        best = o;
+      }
     }
   }
   uint32_t pruned[kW];
@@ -1002,7 +1038,26 @@ __device__ __forceinline__ int convex_region_scan(const WorldD& ws, const double
     // instruction-cache pressure)
     const int nw = (ws.n_obs + 31) / 32;
     for (int q = 0; q < nw; ++q) prune_word(q);
-    for (int q = 0; q < nw; ++q) near_word(q);
+    if (kBucketNear && bo) {
+      for (int q = 0; q < nw; ++q) n_clamp += __popc(~pruned[q]);
+      for (int bk = 0; bk < 32; ++bk) {
+        const int s0 = bo->start[bk], s1 = bo->start[bk + 1];
+        if (s0 == s1) continue;
+        if (bo->bmin[bk] > nsq) break;
+        for (int x = s0; x < s1; ++x) {
+          const int o = bo->order[x];
+          if ((pruned[o >> 5] >> (o & 31)) & 1u) continue;
+          if (lbs[o] > nsq) continue;
+          const double sq = clamp_sq<DW>(ws, o, y);
+          if (sq < nsq || (sq == nsq && o < nb)) {
+            nb = o;
+            nsq = sq;
+          }
+        }
+      }
+    } else {
+      for (int q = 0; q < nw; ++q) near_word(q);
+    }
     if (!any) return -1;
     if (count < out_cap) {
       double a[DW];

@@ -810,6 +810,7 @@ __global__ void k_emit_edges(GraphArgs g, const int64_t* __restrict__ d_ncand, i
 constexpr int kOnceMaxObs = 16;
 constexpr int kRegLocal = 8;
 constexpr int kLbsMaxObs = 1024;  // per-warp distance bounds in shared memory up to this many boxes
+constexpr int kOrdMeta = (33 + 32 + 32) * 4 + 12;  // per-warp bucket offsets, cursors, minima (+ pad to 16 B)
 
 // waypoint -> owning edge (one thread per edge fills its waypoint range)
 __global__ void k_wp_edge(int64_t n_edges, const int64_t* __restrict__ wp_off, int32_t* __restrict__ wp_edge) {
@@ -978,6 +979,8 @@ __global__ void __launch_bounds__(regions_block(KW)) k_regions_once(GraphArgs g,
   // skips the distances these bounds prove cannot be the nearest
   float* lbs = nullptr;
   double ub = __builtin_inf();
+  BoxOrder box_order{};
+  const BoxOrder* bord = nullptr;
   if (KW > 0 && w.n_obs <= kLbsMaxObs) {
     lbs = reinterpret_cast<float*>(smem + 2 * w.n_obs * DW) + (threadIdx.x >> 5) * w.n_obs;
     double wlo[DW], whi[DW];
@@ -1015,6 +1018,48 @@ __global__ void __launch_bounds__(regions_block(KW)) k_regions_once(GraphArgs g,
         const double t = __shfl_xor_sync(0xffffffffu, ub, o);
         ub = t < ub ? t : ub;
       }
+      __syncwarp();
+      // the boxes in 32 buckets of ascending bound (counting sort by the
+      // monotone map lbs -> floor(lbs * 31 / ub), bounds above ub last)
+      char* wbase = reinterpret_cast<char*>(smem + 2 * w.n_obs * DW) +
+                    static_cast<size_t>(blockDim.x / 32) * w.n_obs * 4 +
+                    static_cast<size_t>(threadIdx.x >> 5) * (kOrdMeta + ((2 * w.n_obs + 15) & ~15));
+      int* bstart = reinterpret_cast<int*>(wbase);               // 33 counts -> offsets
+      int* bcur = bstart + 33;                                    // 32 cursors
+      unsigned* bminu = reinterpret_cast<unsigned*>(bcur + 32);  // 32 smallest bounds (float bits)
+      uint16_t* order = reinterpret_cast<uint16_t*>(wbase + kOrdMeta);
+      const float scale = ub > 0.0 ? static_cast<float>(31.0 / ub) : 0.0f;
+      auto bucket_of = [&](float l) -> int {
+        if (static_cast<double>(l) > ub) return 31;
+        const int b = static_cast<int>(l * scale);
+        return b < 30 ? b : 30;
+      };
+      bstart[lane] = 0;
+      if (lane == 0) bstart[32] = 0;
+      bminu[lane] = 0x7f800000u;
+      __syncwarp();
+      for (int o = lane; o < w.n_obs; o += 32) {
+        const int b = bucket_of(lbs[o]);
+        atomicAdd(&bstart[b], 1);
+        atomicMin(&bminu[b], __float_as_uint(lbs[o]));
+      }
+      __syncwarp();
+      const int cnt = bstart[lane];
+      int inc = cnt;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int t = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += t;
+      }
+      __syncwarp();
+      bstart[lane] = inc - cnt;
+      bcur[lane] = inc - cnt;
+      if (lane == 31) bstart[32] = inc;
+      __syncwarp();
+      for (int o = lane; o < w.n_obs; o += 32) order[atomicAdd(&bcur[bucket_of(lbs[o])], 1)] = static_cast<uint16_t>(o);
+      __syncwarp();
+      box_order = BoxOrder{order, bstart, reinterpret_cast<const float*>(bminu)};
+      bord = &box_order;
     }
     __syncwarp();
   }
@@ -1024,7 +1069,7 @@ __global__ void __launch_bounds__(regions_block(KW)) k_regions_once(GraphArgs g,
       return convex_region_fused<DW>(ws, y, yd, smem + 2 * w.n_obs * DW + threadIdx.x, blockDim.x, ao, bo, fo,
                                      n_clamp, n_prune);
     } else {
-      return convex_region_scan<DW, KW>(ws, y, yd, ao, bo, fo, as, bst, ocap, n_clamp, n_prune, lbs, ub);
+      return convex_region_scan<DW, KW>(ws, y, yd, ao, bo, fo, as, bst, ocap, n_clamp, n_prune, lbs, ub, bord);
     }
   };
   if (active) {
@@ -1500,8 +1545,10 @@ void build_graph_device(DevGraph& G, Ctx& c, int n, int dw, const double* h_pos,
                                             : k_regions_once<DW, 128>;
           const int blk = w.n_obs <= 256 ? 128 : regions_block(w.n_obs <= 1024 ? 32 : 128);
           const size_t sm = wsmem + (w.n_obs <= kOnceMaxObs ? static_cast<size_t>(w.n_obs) * 128 * 8
-                                     : w.n_obs <= kLbsMaxObs ? static_cast<size_t>(w.n_obs) * (blk / 32) * 4  // lbs
-                                                             : 0);
+                                     : w.n_obs <= kLbsMaxObs
+                                         ? static_cast<size_t>(w.n_obs) * (blk / 32) * 4  // lbs
+                                               + static_cast<size_t>(blk / 32) * (kOrdMeta + ((2 * w.n_obs + 15) & ~15))
+                                         : 0);
           if (sm > 48 * 1024)
             PUMP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
           kern<<<grid_for(n_items, blk), blk, sm, st>>>(
