@@ -1057,6 +1057,11 @@ struct CoopArgs {
   int32_t* group;
   int64_t* task_off;
   int32_t* task_grp;
+  int64_t* task_e;
+  // > 0: the next round's task map (k_task_map's records) is written here for
+  // every group entry whose tasks end below map_cap (the host skips
+  // k_task_map when the next round runs gated with this capacity)
+  int64_t map_cap;
   const int64_t* row_ptr;
   unsigned long long* stamps;  // optional phase timestamps (PUMP_DEBUG_COOP)
 };
@@ -1360,7 +1365,18 @@ __global__ void __launch_bounds__(kCoopBlock, 2) k_round_tail(const CoopArgs A) 
         }
         return A.row_ptr[hv + 1] - A.row_ptr[hv];
       },
-      [](int64_t, int64_t, int64_t) {}, A.task_off, A.scan_status, ep++, red, &s_pre);
+      [&](int64_t g, int64_t t0, int64_t deg) {
+        // the next round's task map (as k_task_map): task t of entry g is
+        // (its plan, the edge row_ptr[head] + t - t0)
+        if (t0 + deg + 1 > A.map_cap) return;
+        const int id = A.group[g];
+        const int64_t e0 = A.row_ptr[A.ex.head[id]];
+        for (int64_t k = 0; k < deg; ++k) {
+          A.task_grp[t0 + k] = id;
+          A.task_e[t0 + k] = e0 + k;
+        }
+      },
+      A.task_off, A.scan_status, ep++, red, &s_pre);
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
     const long long t = __shfl_xor_sync(0xffffffffu, g_min, o);
@@ -1662,6 +1678,12 @@ void run_explore_device(DevExplore& X, Ctx& c, const DevGraph& G, const ExploreA
     prm.on_round(h);
     return halted;
   };
+  struct MapPrev {
+    int64_t cap;
+    const void* grp;
+    const void* e;
+  };
+  MapPrev map_prev{0, nullptr, nullptr};  // the last cooperative launch's task-map capacity and buffers
   auto win_drain = [&]() {
     PUMP_CUDA(cudaEventSynchronize(X.status_ev[in_slot]));
     win_consume(X.status_h[1 + in_slot]);
@@ -1811,18 +1833,25 @@ void run_explore_device(DevExplore& X, Ctx& c, const DevGraph& G, const ExploreA
       A.group = X.group.as<int32_t>();
       A.task_off = X.task_off.as<int64_t>();
       A.task_grp = X.task_grp.as<int32_t>();
+      A.task_e = X.task_e.as<int64_t>();
+      A.map_cap = T;
       A.row_ptr = G.row_ptr.as<int64_t>();
       static const bool dbg_coop = std::getenv("PUMP_DEBUG_COOP") != nullptr;
       DBuf& stamps = c.buf("x_coop_stamps", 64 * 8);
       A.stamps = dbg_coop ? stamps.as<unsigned long long>() : nullptr;
       const int64_t grid_cap = static_cast<int64_t>(coop_blocks) * 8;
-      launch_round(k_task_map,
+      // the previous cooperative round wrote this round's task map when it
+      // fit its capacity; a gated round with that same capacity (and the same
+      // buffers) either fits it or halts at its gate
+      const bool map_ready = pipe && map_prev.cap == T && map_prev.grp == X.task_grp.p && map_prev.e == X.task_e.p;
+      map_prev = MapPrev{T, X.task_grp.p, X.task_e.p};
+      if (!map_ready) launch_round(k_task_map,
                    dim3(pipe ? static_cast<unsigned>(std::min<int64_t>(grid_for(pool_ub * 32, 256), grid_cap))
                              : grid_for(h.G * 32, 256)),
                    dim3(256), st, false, static_cast<const int64_t*>(d_G), X.task_off.as<int64_t>(),
                    X.group.as<int32_t>(), X.head.as<int32_t>(), G.row_ptr.as<int64_t>(), X.task_grp.as<int32_t>(),
                    X.task_e.as<int64_t>(), static_cast<const ExploreStatus*>(S));
-      ++c.launches;
+      if (!map_ready) ++c.launches;
       {
         const unsigned grid = grid_for(T * 32, 256);  // pipelined: T is the per-round task capacity
         KScope ks(st, F_EXPAND);
@@ -1857,6 +1886,7 @@ void run_explore_device(DevExplore& X, Ctx& c, const DevGraph& G, const ExploreA
      }
      (void)rounds0;
     } else {
+      map_prev = MapPrev{0, nullptr, nullptr};  // (no task map written for the next round)
       if (T > 0) {
         X.task_grp.ensure(al((T + 1) * 4));
         X.task_e.ensure(al((T + 1) * 8));
