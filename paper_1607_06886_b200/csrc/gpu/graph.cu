@@ -811,6 +811,7 @@ constexpr int kOnceMaxObs = 16;
 constexpr int kRegLocal = 8;
 constexpr int kLbsMaxObs = 1024;  // per-warp distance bounds in shared memory up to this many boxes
 constexpr int kOrdMeta = (33 + 32 + 32) * 4 + 12;  // per-warp bucket offsets, cursors, minima (+ pad to 16 B)
+constexpr int kBucketMaxObs = 512;  // bucket order for the first search up to this many boxes (1000: measured slower)
 
 // waypoint -> owning edge (one thread per edge fills its waypoint range)
 __global__ void k_wp_edge(int64_t n_edges, const int64_t* __restrict__ wp_off, int32_t* __restrict__ wp_edge) {
@@ -1019,6 +1020,8 @@ __global__ void __launch_bounds__(regions_block(KW)) k_regions_once(GraphArgs g,
         ub = t < ub ? t : ub;
       }
       __syncwarp();
+    }
+    if (wlo[0] <= whi[0] && w.n_obs <= kBucketMaxObs) {
       // the boxes in 32 buckets of ascending bound (counting sort by the
       // monotone map lbs -> floor(lbs * 31 / ub), bounds above ub last)
       char* wbase = reinterpret_cast<char*>(smem + 2 * w.n_obs * DW) +
@@ -1547,7 +1550,9 @@ void build_graph_device(DevGraph& G, Ctx& c, int n, int dw, const double* h_pos,
           const size_t sm = wsmem + (w.n_obs <= kOnceMaxObs ? static_cast<size_t>(w.n_obs) * 128 * 8
                                      : w.n_obs <= kLbsMaxObs
                                          ? static_cast<size_t>(w.n_obs) * (blk / 32) * 4  // lbs
-                                               + static_cast<size_t>(blk / 32) * (kOrdMeta + ((2 * w.n_obs + 15) & ~15))
+                                               + (w.n_obs <= kBucketMaxObs
+                                                      ? static_cast<size_t>(blk / 32) * (kOrdMeta + ((2 * w.n_obs + 15) & ~15))
+                                                      : 0)
                                          : 0);
           if (sm > 48 * 1024)
             PUMP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
